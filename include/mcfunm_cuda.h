@@ -1,0 +1,170 @@
+/*
+ * mcfunm_cuda.h -- C ABI of the B200 walk-sampling estimator (libmcfunm_cuda.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `mcfunm`
+ * (arXiv 2308.01037).  The reference has no native code and no FFI: its hot
+ * path is the per-column Python loop of the (SPEC-only) estimators around
+ * walker.run_walks_batch (/root/reference/pkg/src/mcfunm/walker.py:245-290) with
+ * a per-step Python callback `on_step(k, states, weights, ids)` that cannot
+ * cross a device boundary.  Each entry point below replaces one piece of that
+ * path; the replaced reference interface is cited per function.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Array arguments marked [dev] are CUDA
+ *    device pointers owned by the caller (e.g. torch.Tensor.data_ptr());
+ *    [host] pointers are ordinary host memory.
+ *  - `stream` is a cudaStream_t passed as void*; 0 = legacy default stream.
+ *    Every call is stream-ordered; calls that must return a host-visible
+ *    value synchronise that stream and say so.
+ *  - Return value: MCF_OK or an error code that maps 1:1 onto the reference
+ *    exception hierarchy (errors.py:8-47); mcf_last_error() gives the message
+ *    (thread-local).
+ *  - Node ids fit int32 (n < 2^31); nnz < 2^31 (int32 entry indices in replay
+ *    streams).  All arithmetic is fp64.
+ */
+#ifndef MCFUNM_CUDA_H
+#define MCFUNM_CUDA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MCF_API __attribute__((visibility("default")))
+#else
+#define MCF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes (errors.py:8-47; CLI exit codes SPEC.md:623). */
+#define MCF_OK 0
+#define MCF_ERR_ARGUMENT 1    /* errors.ArgumentError: bad parameters (walker.py:60-67) */
+#define MCF_ERR_DEGENERATE 2  /* errors.DegenerateInputError: nnz == 0 (walker.py:100-103) */
+#define MCF_ERR_CONVERGENCE 3 /* errors.ConvergenceError */
+#define MCF_ERR_RESOURCE 4    /* errors.ResourceError: device out of memory */
+#define MCF_ERR_CUDA 5        /* any other CUDA failure (kernel fault, no device) */
+
+/* mcf_walk_params.flags */
+#define MCF_FLAG_NONE 0
+
+typedef struct mcf_graph mcf_graph;
+
+/* Square sparse matrix in both CSR and CSC form, already scaled by gamma
+ * (sparsemat.py:29-100, scale() sparsemat.py:338-352).  Column ids inside each
+ * row (row ids inside each column) must be sorted.  For a symmetric matrix the
+ * csc_* pointers may alias the csr ones. */
+typedef struct {
+    int64_t n;
+    int64_t nnz;
+    const int64_t *row_ptr;  /* [dev] n+1 */
+    const int32_t *col_ids;  /* [dev] nnz */
+    const double *vals;      /* [dev] nnz */
+    const int64_t *csc_ptr;  /* [dev] n+1 */
+    const int32_t *csc_rows; /* [dev] nnz */
+    const double *csc_vals;  /* [dev] nnz */
+} mcf_csr;
+
+/* Host-visible facts about a built graph. */
+typedef struct {
+    int64_t n;
+    int64_t nnz;
+    int64_t n_uniform_rows;   /* rows whose |a_ij| are all equal (index sampling) */
+    int64_t n_empty_rows;     /* absorbing rows (walker.py:274-278) */
+    int64_t n_negative;       /* stored entries with a < 0 */
+    int64_t max_degree;
+    double max_row_abs_sum;   /* sqrt(alpha_diagnostic) (walker.py:293-302) */
+    double col_norm_total;    /* sum_j ||C_j||_2 (walker.py:128) */
+} mcf_graph_info;
+
+/* Walk termination and RNG (WalkConfig, walker.py:44-67) plus the series. */
+typedef struct {
+    int64_t max_steps;       /* hard cap m_max >= 1 */
+    double weight_cutoff;    /* W_c in (0,1): walk stops once |W| <= W_c * W0 */
+    uint64_t seed;           /* Philox key; stream per (seed, column, walk, step) */
+    const double *zeta;      /* [host] max_steps + 2 coefficients zeta_0.. (series.py:69-80) */
+    int32_t flags;
+} mcf_walk_params;
+
+/* Device-side counters, int64[4], accumulated (never reset) by walk calls:
+ * [0] walks run, [1] emissions (= reference WalkOutcome.steps), [2] walks
+ * truncated by max_steps, [3] walks absorbed in an empty row. */
+#define MCF_STATS_LEN 4
+
+MCF_API const char *mcf_version(void);
+MCF_API const char *mcf_last_error(void);
+
+/* Build the device transition tables for `csr` (replaces
+ * walker.build_transition_model, walker.py:97-145): per-row |a| sums in CSR
+ * order, uniform-row flags, within-row CDFs for weighted rows, column norms
+ * ||C_j||_2 and the start distribution p_j (walker.py:127-129, reproduced
+ * bit-for-bit).  Keeps the caller's arrays by pointer: they must outlive the
+ * handle.  Synchronises `stream`.  nnz == 0 -> MCF_ERR_DEGENERATE. */
+MCF_API int mcf_graph_create(const mcf_csr *csr, void *stream, mcf_graph **out);
+MCF_API int mcf_graph_destroy(mcf_graph *g);
+MCF_API int mcf_graph_get_info(const mcf_graph *g, mcf_graph_info *info);
+
+/* Copy derived tables out ([dev] n each; any pointer may be NULL):
+ * row |a| sums (sparsemat.row_abs_sums), column norms, start probabilities. */
+MCF_API int mcf_graph_tables(const mcf_graph *g, double *row_abs_sum, double *col_norms,
+                     double *init_prob, void *stream);
+
+/* Per-column walk budgets N_i = floor(p_i N_s) + largest-remainder correction,
+ * ties by ascending index, p_i = 0 -> 0 (replaces walker.allocate_walks /
+ * largest_remainder, walker.py:148-170; identical output).  Writes ni[n] and
+ * walk_pre[n+1] = exclusive prefix sum of ni ([dev] int64). */
+MCF_API int mcf_allocate_walks(mcf_graph *g, int64_t n_walks, int64_t *ni, int64_t *walk_pre, void *stream);
+
+/* y = alpha * v + beta * r + A x over rows [row_begin, row_end) ([dev] n; v, r
+ * may be NULL).  With alpha = beta = 0 this is r = A v; with
+ * (zeta_0, zeta_1, q) it is the Alg. 3 combine y = z0 v + z1 r + A q
+ * (PAPER.md:362). */
+MCF_API int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
+             const double *x, double *y, int64_t row_begin, int64_t row_end, void *stream);
+
+/* Action walks (Alg. 3 inner loops): for
+ * every column c in [col_begin, col_end) run N_c = walk_pre[c+1]-walk_pre[c]
+ * walks with W0 = 1/N_c and write
+ *     q[c] = sum_walks sum_k zeta_{k+2} W_k r[l_k]
+ * and, if q_var != NULL, the estimated variance of q[c] from the per-walk
+ * contributions.  Replaces the estimator's per-column loop around
+ * run_walks_batch (walker.py:245-290) with its on_step accumulation.
+ * Counter-based Philox-4x32-10 keyed by (seed, column, walk, step). */
+MCF_API int mcf_walk_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre,
+                    int64_t col_begin, int64_t col_end, const double *r, double *q,
+                    double *q_var, int64_t *stats, void *stream);
+
+/* Same, but every draw is taken from a recorded entry stream instead of the
+ * RNG: walk g = walk_pre[c] + w consumes entries[walk_off[g] .. walk_off[g+1])
+ * (global CSR entry indices, step order), exactly the entries the reference
+ * batch driver picked (walker.py:280-283).  The device re-derives weights and
+ * termination and checks the stream is consumed exactly; synchronises
+ * `stream`; a mismatch -> MCF_ERR_ARGUMENT. */
+MCF_API int mcf_replay_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre,
+                      int64_t col_begin, int64_t col_end, const int64_t *walk_off,
+                      const int32_t *entries, const double *r, double *q, int64_t *stats,
+                      void *stream);
+
+/* Diagonal walks + Eq. 20 partials (Alg. 2):
+ * for every column c in [col_begin, col_end) builds Q_c (sum of zeta_{k+2} W_k
+ * per visited state, W0 = 1/N_c) and writes, for every stored entry (i, c) of
+ * column c, pcol[csc_ptr[c] + t] = a_ic <Q_c, C_i>.  Entries of columns outside
+ * the range or with N_c = 0 are left untouched (caller zeroes pcol).
+ * Deterministic: Q_c is accumulated in a fixed order. */
+MCF_API int mcf_walk_diag(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre,
+                  int64_t col_begin, int64_t col_end, double *pcol, int64_t *stats, void *stream);
+
+/* Replay variant of mcf_walk_diag (see mcf_replay_action). Synchronises. */
+MCF_API int mcf_replay_diag(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre,
+                    int64_t col_begin, int64_t col_end, const int64_t *walk_off,
+                    const int32_t *entries, double *pcol, int64_t *stats, void *stream);
+
+/* d_i = zeta_0 + zeta_1 a_ii + sum_{c} pcol[(i,c)] for rows [row_begin, row_end)
+ * (Eq. 20 final sum), fixed summation order. */
+MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d,
+                     int64_t row_begin, int64_t row_end, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCFUNM_CUDA_H */

@@ -1,0 +1,436 @@
+// Diagonal estimator (Alg. 2 + Eq. 20, :267-305).
+//
+//   1. k_walk_emit   one lane per walk (same walk engine as the action path)
+//                    writes its emissions (state, zeta_{k+2} W_k) into fixed
+//                    slots of an emission buffer, column-contiguous.
+//   2. k_diag_q      one CTA per walked column c (persistent, work counter):
+//                    builds Q_c in a shared-memory hash table (global-memory
+//                    table for very wide columns) and, for every stored entry
+//                    (i, c), writes pcol[(i,c)] = a_ic <Q_c, C_i> -- the
+//                    column's whole contribution to Eq. 20.  Q_c is summed in
+//                    a fixed order (emission order within a warp, warps in
+//                    index order), so results are deterministic.
+//   3. k_diag_final  d_i = zeta_0 + zeta_1 a_ii + sum_c pcol[(i,c)], rows in
+//                    fixed order (mcf_diag_combine).
+// Partials per CSC entry make the result independent of how columns are
+// split across batches, CTAs or GPUs.
+#include <cstdlib>
+#include <string>
+
+#include "mcf_internal.cuh"
+
+namespace mcf {
+
+// implemented in mcf_walk.cu (shares the walk engine with the action path)
+int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce);
+int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                     int mode, const long long *walk_off, const int *entries, long long slot_len, long long off_base,
+                     long long *eaux, int *est, double *ewt, long long *stats, int *err, cudaStream_t s);
+enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
+
+}  // namespace mcf
+
+namespace mcf {
+
+constexpr int Q_THREADS = 512;
+constexpr int Q_WARPS = Q_THREADS / 32;
+constexpr int SCAP = 16384;  // shared table slots: 16384 * (4 + 8) B = 192 KB
+constexpr int EMPTY_KEY = -1;
+
+struct QArgs {
+    const long long *__restrict__ walk_pre;
+    long long wb;        // first walk of the batch
+    long long slot_len;  // fixed slots per walk (0 -> eoff or replay layout)
+    const long long *__restrict__ eoff;      // explicit layout (relative to wb), or null
+    const long long *__restrict__ walk_off;
+    long long off_base;
+    const int *__restrict__ est;
+    const double *__restrict__ ewt;
+    const long long *__restrict__ csc_ptr;
+    const int *__restrict__ csc_rows;
+    const double *__restrict__ csc_vals;
+    long long n;
+    long long col_begin, col_end;
+    double *__restrict__ pcol;
+    int *gkeys;
+    double *gvals;
+    long long gcap;
+    unsigned long long *counter;
+};
+
+__device__ __forceinline__ long long slot_of(const QArgs &a, long long g) {
+    if (a.slot_len > 0) return (g - a.wb) * a.slot_len;
+    if (a.eoff) return a.eoff[g - a.wb];
+    return a.walk_off[g] - a.off_base + (g - a.wb);
+}
+
+__device__ __forceinline__ uint32_t hash_slot(int key, uint32_t mask) {
+    return ((uint32_t)key * 0x9E3779B1u) & mask;
+}
+
+__device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        int k = keys[s];
+        if (k == key) return (int)s;
+        if (k == EMPTY_KEY) {
+            int old = atomicCAS(&keys[s], EMPTY_KEY, key);
+            if (old == EMPTY_KEY || old == key) return (int)s;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+__device__ __forceinline__ double lookup(const int *keys, const double *vals, uint32_t mask, int key) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        int k = keys[s];
+        if (k == key) return vals[s];
+        if (k == EMPTY_KEY) return 0.0;
+        s = (s + 1) & mask;
+    }
+}
+
+__global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *svals = reinterpret_cast<double *>(smem_raw);
+    int *skeys = reinterpret_cast<int *>(svals + SCAP);
+    __shared__ long long s_col;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
+    double *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
+
+    while (true) {
+        __syncthreads();
+        if (tid == 0) s_col = a.col_begin + (long long)atomicAdd(a.counter, 1ull);
+        __syncthreads();
+        const long long c = s_col;
+        if (c >= a.col_end) break;
+        const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
+        if (g0 == g1) continue;
+        const long long s0 = slot_of(a, g0), m = slot_of(a, g1) - s0;
+        long long need = m < a.n ? m : a.n;
+        uint32_t cap = 32;
+        while ((long long)cap * 3 < need * 4 + 4) cap <<= 1;  // load factor <= 3/4
+        int *keys;
+        double *vals;
+        if (cap <= (uint32_t)SCAP) {
+            keys = skeys;
+            vals = svals;
+        } else {
+            keys = gkeys;
+            vals = gvals;
+        }
+        const uint32_t mask = cap - 1;
+        for (uint32_t t = tid; t < cap; t += Q_THREADS) {
+            keys[t] = EMPTY_KEY;
+            vals[t] = 0.0;
+        }
+        __syncthreads();
+
+        // Q_c[j] += zeta_{k+2} W over visits (Alg. 2 line "q_{i l_k} += ...")
+        for (long long base = 0; base < m; base += Q_THREADS) {
+            long long i = base + tid;
+            int s = (i < m) ? a.est[s0 + i] : EMPTY_KEY;
+            double w = (s >= 0) ? a.ewt[s0 + i] : 0.0;
+            unsigned grp = __match_any_sync(MCF_FULL, s);
+            int leader = __ffs(grp) - 1;
+            double sum = w;
+            if (!__all_sync(MCF_FULL, __popc(grp) == 1)) {  // equal states in this warp: sum in lane order
+                sum = 0.0;
+                for (int src = 0; src < 32; ++src) {
+                    double o = __shfl_sync(MCF_FULL, w, src);
+                    if ((grp >> src) & 1u) sum += o;
+                }
+            }
+            int slot = -1;
+            if (s >= 0 && lane == leader) slot = find_or_insert(keys, mask, s);
+            for (int ph = 0; ph < Q_WARPS; ++ph) {  // warps add in index order -> fixed summation order
+                if (warp == ph && slot >= 0) vals[slot] += sum;
+                __syncthreads();
+            }
+        }
+
+        // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
+        const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        for (long long t = warp; t < cn; t += Q_WARPS) {
+            int i = a.csc_rows[cs + t];
+            double aic = a.csc_vals[cs + t];
+            long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+            double acc = 0.0;
+            for (long long e = ilo + lane; e < ihi; e += 32) {
+                double qv = lookup(keys, vals, mask, __ldg(a.csc_rows + e));
+                acc = fma(__ldg(a.csc_vals + e), qv, acc);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) a.pcol[cs + t] = aic * acc;
+        }
+    }
+}
+
+// d_i = zeta_0 + zeta_1 a_ii + sum over row i of pcol[csr2csc[e]] (4 lanes per row)
+__global__ void k_diag_final(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                             const double *__restrict__ vals, const long long *__restrict__ csr2csc,
+                             const double *__restrict__ pcol, double z0, double z1, double *__restrict__ d,
+                             long long rb, long long re) {
+    long long i = rb + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 2);
+    int sub = threadIdx.x & 3;
+    bool in = i < re;
+    double s = 0.0, aii = 0.0;
+    if (in) {
+        for (long long e = row_ptr[i] + sub; e < row_ptr[i + 1]; e += 4) {
+            s += pcol[csr2csc[e]];
+            if (col_ids[e] == i) aii = vals[e];
+        }
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(MCF_FULL, s, o, 4);
+        aii += __shfl_xor_sync(MCF_FULL, aii, o, 4);
+    }
+    if (in && sub == 0) d[i] = (z0 + z1 * aii) + s;
+}
+
+__global__ void k_batch_bounds(const long long *__restrict__ walk_pre, long long cb, long long ce, long long wb,
+                               long long cap_walks, long long nb, long long *__restrict__ bounds) {
+    long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    if (b == 0) { bounds[0] = cb; return; }
+    if (b == nb) { bounds[nb] = ce; return; }
+    long long target = wb + b * cap_walks;  // largest c in [cb, ce] with walk_pre[c] <= target
+    long long lo = cb, hi = ce;
+    while (lo < hi) {
+        long long mid = (lo + hi + 1) >> 1;
+        if (walk_pre[mid] <= target) lo = mid;
+        else hi = mid - 1;
+    }
+    bounds[b] = lo;
+}
+
+__global__ void k_max_walks(const long long *__restrict__ walk_pre, long long cb, long long ce,
+                            unsigned long long *out) {
+    long long c = cb + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = (c < ce) ? (unsigned long long)(walk_pre[c + 1] - walk_pre[c]) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_xor_sync(MCF_FULL, v, o);
+        v = x > v ? x : v;
+    }
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
+// default emission-buffer budget (slots of 12 B): 2^28 -> 3 GiB
+static long long emission_budget() {
+    static long long v = 0;
+    if (!v) {
+        const char *e = getenv("MCF_EMISSION_SLOTS");
+        v = e ? atoll(e) : (1ll << 28);
+        if (v < (1ll << 16)) v = 1ll << 16;
+    }
+    return v;
+}
+
+static int run_q(mcf_graph *g, const long long *walk_pre, long long cb, long long ce, long long wb, long long slot_len,
+                 const long long *eoff, const long long *walk_off, long long off_base, const int *est, const double *ewt, double *pcol,
+                 long long max_slots_per_col, cudaStream_t s) {
+    QArgs q;
+    q.walk_pre = walk_pre;
+    q.wb = wb;
+    q.slot_len = slot_len;
+    q.eoff = eoff;
+    q.walk_off = walk_off;
+    q.off_base = off_base;
+    q.est = est;
+    q.ewt = ewt;
+    q.csc_ptr = (const long long *)g->csc_ptr;
+    q.csc_rows = g->csc_rows;
+    q.csc_vals = g->csc_vals;
+    q.n = g->n;
+    q.col_begin = cb;
+    q.col_end = ce;
+    q.pcol = pcol;
+    q.gkeys = nullptr;
+    q.gvals = nullptr;
+    q.gcap = 0;
+    int grid = sm_count();
+    long long need = max_slots_per_col < g->n ? max_slots_per_col : g->n;
+    long long cap = 32;
+    while (cap * 3 < need * 4 + 4) cap <<= 1;
+    unsigned char *gbuf = nullptr;
+    if (cap > SCAP) {
+        q.gcap = cap;
+        MCF_CUDA(cudaMallocAsync(&gbuf, (size_t)grid * cap * (sizeof(int) + sizeof(double)), s));
+        q.gvals = reinterpret_cast<double *>(gbuf);
+        q.gkeys = reinterpret_cast<int *>(q.gvals + (size_t)grid * cap);
+    }
+    unsigned long long *counter = nullptr;
+    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
+    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    q.counter = counter;
+    size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(double));
+    MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
+    MCF_LAUNCHED("k_diag_q");
+    cudaFreeAsync(counter, s);
+    if (gbuf) cudaFreeAsync(gbuf, s);
+    return MCF_OK;
+}
+
+static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                const long long *walk_off, const int *entries, double *pcol, long long *stats, cudaStream_t s,
+                bool replay) {
+    int rc = check_params(g, p, walk_pre, cb, ce);
+    if (rc) return rc;
+    MCF_ARG(pcol && stats, "diag walk: null pcol/stats");
+    if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
+    long long wb = 0, we = 0;
+    rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
+    if (rc) return rc;
+    if (we == wb) return MCF_OK;
+    int *err = nullptr;
+    unsigned long long *maxw = nullptr;
+    MCF_CUDA(cudaMallocAsync(&err, sizeof(int) + sizeof(unsigned long long) + 4, s));
+    maxw = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(err) + 8);
+    MCF_CUDA(cudaMemsetAsync(err, 0, 16, s));
+    long long ncol = ce - cb;
+    k_max_walks<<<(unsigned)((ncol + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, maxw);
+    MCF_LAUNCHED("k_max_walks");
+    unsigned long long hmax = 0;
+    MCF_CUDA(cudaMemcpyAsync(&hmax, maxw, sizeof(hmax), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+
+    if (replay) {
+        long long hoff[2];
+        MCF_CUDA(cudaMemcpyAsync(&hoff[0], walk_off + wb, 8, cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaMemcpyAsync(&hoff[1], walk_off + we, 8, cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        long long slots = hoff[1] - hoff[0] + (we - wb);
+        int *est = nullptr;
+        double *ewt = nullptr;
+        MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * slots, s));
+        MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * slots, s));
+        rc = launch_walk_emit(g, p, walk_pre, cb, ce, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est, ewt,
+                              stats, err, s);
+        if (rc) return rc;
+        // table size is bounded by min(slots, n) per column
+        rc = run_q(g, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
+        if (rc) return rc;
+        int herr = 0;
+        MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        cudaFreeAsync(est, s);
+        cudaFreeAsync(ewt, s);
+        cudaFreeAsync(err, s);
+        if (herr) {
+            set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) + ")");
+            return MCF_ERR_ARGUMENT;
+        }
+        return MCF_OK;
+    }
+
+    // walks of at most FIXED_MAX steps get fixed slots; longer caps (cutoff-
+    // terminated walks, e.g. max_steps = 10^4) use a count pass instead
+    const bool fixed = p->max_steps <= 64;
+    const long long L = fixed ? p->max_steps : 64;
+    long long cap_walks = emission_budget() / L;
+    if (cap_walks < (long long)hmax) cap_walks = (long long)hmax;
+    long long nb = (we - wb + cap_walks - 1) / cap_walks;
+    long long *dbounds = nullptr;
+    MCF_CUDA(cudaMallocAsync(&dbounds, sizeof(long long) * (nb + 1), s));
+    k_batch_bounds<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, wb, cap_walks, nb, dbounds);
+    MCF_LAUNCHED("k_batch_bounds");
+    long long *hb = new long long[nb + 1];
+    MCF_CUDA(cudaMemcpyAsync(hb, dbounds, sizeof(long long) * (nb + 1), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    long long buf_slots = (cap_walks + (long long)hmax) * L;
+    int *est = nullptr;
+    double *ewt = nullptr;
+    MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * buf_slots, s));
+    MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s));
+    for (long long b = 0; b < nb; ++b) {
+        long long c0 = hb[b], c1 = hb[b + 1];
+        if (c1 <= c0) continue;
+        long long bw0 = 0, bw1 = 0;
+        rc = read_walk_range(walk_pre, c0, c1, &bw0, &bw1, s);
+        if (rc) break;
+        if (bw1 == bw0) continue;
+        if (fixed) {
+            rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, stats,
+                                  err, s);
+            if (rc) break;
+            rc = run_q(g, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
+            if (rc) break;
+            continue;
+        }
+        // variable-length walks: count pass, scan, emit at exact offsets
+        long long nwb = bw1 - bw0;
+        long long *elen = nullptr;
+        MCF_CUDA(cudaMallocAsync(&elen, sizeof(long long) * (2 * nwb + 1), s));
+        long long *eoff = elen + nwb;
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
+                              stats, err, s);
+        if (rc) break;
+        rc = exclusive_scan_i64(elen, eoff, nwb, s);
+        if (rc) break;
+        long long total = 0;
+        MCF_CUDA(cudaMemcpyAsync(&total, eoff + nwb, sizeof(long long), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        if (total > buf_slots) {
+            cudaFreeAsync(est, s);
+            cudaFreeAsync(ewt, s);
+            buf_slots = total;
+            MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * buf_slots, s));
+            MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s));
+        }
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, stats,
+                              err, s);
+        if (rc) break;
+        rc = run_q(g, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
+        cudaFreeAsync(elen, s);
+        if (rc) break;
+    }
+    delete[] hb;
+    cudaFreeAsync(est, s);
+    cudaFreeAsync(ewt, s);
+    cudaFreeAsync(dbounds, s);
+    cudaFreeAsync(err, s);
+    return rc;
+}
+
+static int diag_combine(mcf_graph *g, double z0, double z1, const double *pcol, double *d, long long rb, long long re,
+                        cudaStream_t s) {
+    MCF_ARG(g && pcol && d, "mcf_diag_combine: null argument");
+    MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_diag_combine: bad row range");
+    int rc = ensure_csr2csc(g, s);
+    if (rc) return rc;
+    long long rows = re - rb;
+    if (rows == 0) return MCF_OK;
+    k_diag_final<<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->vals,
+                                                                   (const long long *)g->csr2csc, pcol, z0, z1, d, rb, re);
+    MCF_LAUNCHED("k_diag_final");
+    return MCF_OK;
+}
+
+}  // namespace mcf
+
+extern "C" {
+
+int mcf_walk_diag(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin, int64_t col_end,
+                  double *pcol, int64_t *stats, void *stream) {
+    return mcf::diag(g, p, (const long long *)walk_pre, col_begin, col_end, nullptr, nullptr, pcol, (long long *)stats,
+                     (cudaStream_t)stream, false);
+}
+
+int mcf_replay_diag(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin,
+                    int64_t col_end, const int64_t *walk_off, const int32_t *entries, double *pcol, int64_t *stats,
+                    void *stream) {
+    return mcf::diag(g, p, (const long long *)walk_pre, col_begin, col_end, (const long long *)walk_off, entries, pcol,
+                     (long long *)stats, (cudaStream_t)stream, true);
+}
+
+int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d, int64_t row_begin,
+                     int64_t row_end, void *stream) {
+    return mcf::diag_combine(g, zeta0, zeta1, pcol, d, row_begin, row_end, (cudaStream_t)stream);
+}
+
+}  // extern "C"

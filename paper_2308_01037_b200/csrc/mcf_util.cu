@@ -1,0 +1,206 @@
+// Shared host/device utilities: error state, prefix scans, walk -> column
+// index, coefficient upload, CSR -> CSC entry map.
+#include <cstdio>
+#include <string>
+
+#include "mcf_internal.cuh"
+
+namespace mcf {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+const char *last_error() { return g_last_error.c_str(); }
+
+int cuda_status(cudaError_t e, const char *what) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // clear the sticky-free allocation error
+        return MCF_ERR_RESOURCE;
+    }
+    return MCF_ERR_CUDA;
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+        if (cached <= 0) cached = 148;
+    }
+    return cached;
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan of int64: out[0..n] (out[n] = total); reduce-then-scan
+// ---------------------------------------------------------------------------
+constexpr int SCAN_T = 512;
+constexpr int SCAN_I = 8;
+constexpr int SCAN_TILE = SCAN_T * SCAN_I;
+
+__device__ __forceinline__ long long block_excl_scan(long long v, long long *total) {
+    __shared__ long long warp_tot[SCAN_T / 32];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(MCF_FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        long long t = (lane < SCAN_T / 32) ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(MCF_FULL, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < SCAN_T / 32) warp_tot[lane] = t;  // inclusive
+    }
+    __syncthreads();
+    long long before = (wid > 0 ? warp_tot[wid - 1] : 0) + x - v;
+    *total = warp_tot[SCAN_T / 32 - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void k_tile_sums(const long long *__restrict__ in, long long n, long long *__restrict__ bsum) {
+    long long base = (long long)blockIdx.x * SCAN_TILE;
+    long long s = 0;
+    for (int i = threadIdx.x; i < SCAN_TILE; i += SCAN_T) {
+        long long j = base + i;
+        if (j < n) s += in[j];
+    }
+    long long tot;
+    block_excl_scan(s, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void k_tile_scan(const long long *__restrict__ in, long long n, const long long *__restrict__ boff,
+                            long long *__restrict__ out) {
+    long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_I;
+    long long v[SCAN_I];
+    long long s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_I; ++i) {
+        long long j = base + i;
+        v[i] = (j < n) ? in[j] : 0;
+        s += v[i];
+    }
+    long long tot;
+    long long run = block_excl_scan(s, &tot) + (boff ? boff[blockIdx.x] : 0);
+#pragma unroll
+    for (int i = 0; i < SCAN_I; ++i) {
+        long long j = base + i;
+        if (j < n) out[j] = run;
+        run += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == SCAN_T - 1) out[n] = run;
+}
+
+int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s) {
+    if (n <= 0) {
+        MCF_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), s));
+        return MCF_OK;
+    }
+    long long nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb == 1) {
+        k_tile_scan<<<1, SCAN_T, 0, s>>>(in, n, nullptr, out);
+        MCF_LAUNCHED("k_tile_scan");
+        return MCF_OK;
+    }
+    long long *bsum = nullptr, *boff = nullptr;
+    MCF_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (2 * nb + 1), s));
+    boff = bsum + nb;
+    k_tile_sums<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum);
+    MCF_LAUNCHED("k_tile_sums");
+    int rc = exclusive_scan_i64(bsum, boff, nb, s);
+    if (rc) return rc;
+    k_tile_scan<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, boff, out);
+    MCF_LAUNCHED("k_tile_scan");
+    MCF_CUDA(cudaFreeAsync(bsum, s));
+    return MCF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// walk-block -> column index for a column range
+// ---------------------------------------------------------------------------
+__global__ void k_blk_col(const long long *__restrict__ walk_pre, long long col_begin, long long col_end,
+                          long long walk_begin, int *__restrict__ blk_col) {
+    long long c = col_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= col_end) return;
+    long long a = walk_pre[c] - walk_begin, b = walk_pre[c + 1] - walk_begin;
+    if (b <= a) return;
+    const long long B = 1ll << WALK_BLK_SHIFT;
+    for (long long blk = (a + B - 1) >> WALK_BLK_SHIFT; blk * B < b; ++blk) blk_col[blk] = (int)c;
+}
+
+int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end, long long walk_begin,
+                  long long walk_end, int **blk_col, long long *nblk, cudaStream_t s) {
+    long long w = walk_end - walk_begin;
+    long long nb = (w + (1ll << WALK_BLK_SHIFT) - 1) >> WALK_BLK_SHIFT;
+    if (nb < 1) nb = 1;
+    MCF_CUDA(cudaMallocAsync(blk_col, sizeof(int) * nb, s));
+    long long nc = col_end - col_begin;
+    if (nc > 0 && w > 0) {
+        k_blk_col<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(walk_pre, col_begin, col_end, walk_begin, *blk_col);
+        MCF_LAUNCHED("k_blk_col");
+    }
+    *nblk = nb;
+    return MCF_OK;
+}
+
+int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end, long long *wb,
+                    long long *we, cudaStream_t s) {
+    long long h[2];
+    MCF_CUDA(cudaMemcpyAsync(&h[0], walk_pre + col_begin, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaMemcpyAsync(&h[1], walk_pre + col_end, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    *wb = h[0];
+    *we = h[1];
+    return MCF_OK;
+}
+
+int upload_zeta(const double *host_zeta, long long count, double **dev, cudaStream_t s) {
+    MCF_CUDA(cudaMallocAsync(dev, sizeof(double) * count, s));
+    MCF_CUDA(cudaMemcpyAsync(*dev, host_zeta, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+    // host buffer may be freed by the caller right after return
+    MCF_CUDA(cudaStreamSynchronize(s));
+    return MCF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CSR entry e = (i, c) -> position of (i, c) inside CSC column c
+// ---------------------------------------------------------------------------
+__global__ void k_csr2csc(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                          const long long *__restrict__ csc_ptr, const int *__restrict__ csc_rows,
+                          long long n, long long *__restrict__ out) {
+    long long i = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    int lane = threadIdx.x & 31;
+    for (long long e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) {
+        int c = col_ids[e];
+        long long lo = csc_ptr[c], hi = csc_ptr[c + 1];  // search row id i in column c
+        while (lo < hi) {
+            long long mid = (lo + hi) >> 1;
+            if (csc_rows[mid] < i) lo = mid + 1;
+            else hi = mid;
+        }
+        out[e] = lo;
+    }
+}
+
+int ensure_csr2csc(mcf_graph *g, cudaStream_t s) {
+    if (g->csr2csc) return MCF_OK;
+    MCF_CUDA(cudaMalloc(&g->csr2csc, sizeof(long long) * (g->nnz > 0 ? g->nnz : 1)));
+    long long blocks = (g->n + 7) / 8;
+    k_csr2csc<<<(unsigned)blocks, 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids,
+                                               (const long long *)g->csc_ptr, g->csc_rows, g->n,
+                                               (long long *)g->csr2csc);
+    MCF_LAUNCHED("k_csr2csc");
+    return MCF_OK;
+}
+
+}  // namespace mcf

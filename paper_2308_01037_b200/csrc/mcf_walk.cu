@@ -1,0 +1,502 @@
+// Action walks (Alg. 3, :337-367) and the SpMV combine.
+//
+// Replaces the reference hot loop: the estimator's per-column Python loop
+// around walker.run_walks_batch (walker.py:245-290) whose on_step callback
+// accumulates q_c += zeta_{k+2} W r[l_k].
+//
+// Work decomposition: every walk is one lane.  A warp refills idle lanes from
+// a global walk counter with one aggregated atomic, so walks of different
+// columns and different lengths share a warp without waiting for each other
+// (Katz walks end at the weight cutoff after 1..60 steps).  Per step a lane
+// touches two random 32-byte sectors: the node header of its state and the
+// sampled CSR entry -- the 64 B/step algorithmic traffic of DESIGN.md.
+//
+// Per-walk contributions are written to a buffer and summed per column in a
+// fixed order, so q does not depend on scheduling, on the number of GPUs or on
+// how the column range is split.
+#include "mcf_internal.cuh"
+
+namespace mcf {
+
+constexpr uint32_t PHILOX_SALT = 0x6d636621u;  // "mcf!"
+
+struct WalkCommon {
+    const NodeHdr *__restrict__ hdr;
+    const int *__restrict__ ecol;
+    const double *__restrict__ cdf;
+    const double *__restrict__ zeta;
+    const long long *__restrict__ walk_pre;
+    const int *__restrict__ blk_col;
+    long long nblk;
+    long long walk_begin, walk_end;
+    int col_last;
+    long long max_steps;
+    double cutoff;
+    uint32_t key0, key1;
+    const long long *__restrict__ walk_off;  // replay only
+    const int *__restrict__ entries;          // replay only
+    unsigned long long *counter;
+    long long *stats;
+    int *err;
+};
+
+// Inverse-CDF draw inside one non-uniform row: first t with cdf[t] > u.
+__device__ __forceinline__ int cdf_pick(const double *__restrict__ cdf, int deg, double u) {
+    int lo = 0, hi = deg - 1;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (__ldg(cdf + mid) > u) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// Draw the next CSR entry of row h for step k of walk (c, wl).
+__device__ __forceinline__ long long draw_entry(const WalkCommon &a, const NodeHdr &h, long long k, long long wl,
+                                                int c) {
+    U4 r = philox4x32_10(U4{(uint32_t)k, (uint32_t)wl, (uint32_t)c, PHILOX_SALT}, a.key0, a.key1);
+    if (h.flags & HDR_UNIFORM) {
+        uint64_t x = ((uint64_t)r.x << 32) | r.y;
+        return h.start + (long long)__umul64hi(x, (uint64_t)h.deg);
+    }
+    return h.start + cdf_pick(a.cdf + h.start, h.deg, u53(r.z, r.w));
+}
+
+__device__ __forceinline__ void flush_stats(long long *stats, long long walks, long long em, long long tr,
+                                            long long ab) {
+    walks = warp_sum_ll(walks);
+    em = warp_sum_ll(em);
+    tr = warp_sum_ll(tr);
+    ab = warp_sum_ll(ab);
+    if ((threadIdx.x & 31) == 0) {
+        if (walks) atomicAdd((unsigned long long *)&stats[0], (unsigned long long)walks);
+        if (em) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)em);
+        if (tr) atomicAdd((unsigned long long *)&stats[2], (unsigned long long)tr);
+        if (ab) atomicAdd((unsigned long long *)&stats[3], (unsigned long long)ab);
+    }
+}
+
+// Walk state of one lane.
+struct Lane {
+    long long g;  // global walk index; -1 wants a walk, -2 no walks left
+    long long wl, k;
+    int c, state;
+    double w, thr;
+    long long epos, eend;  // replay cursor
+};
+
+// Warp-aggregated refill of lanes that finished their walk.
+template <bool REPLAY>
+__device__ __forceinline__ bool refill(const WalkCommon &a, Lane &L, long long &n_walks) {
+    unsigned need = __ballot_sync(MCF_FULL, L.g == -1);
+    if (need) {
+        int lane = threadIdx.x & 31;
+        int leader = __ffs(need) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(a.counter, (unsigned long long)__popc(need));
+        base = __shfl_sync(MCF_FULL, base, leader);
+        if (L.g == -1) {
+            long long rel = (long long)base + __popc(need & lanemask_lt());
+            long long g = a.walk_begin + rel;
+            if (g < a.walk_end) {
+                int c = column_of_walk(g, rel, a.walk_pre, a.blk_col, a.nblk, a.col_last);
+                long long pre = __ldg(a.walk_pre + c);
+                long long nc = __ldg(a.walk_pre + c + 1) - pre;
+                L.g = g;
+                L.c = c;
+                L.wl = g - pre;
+                L.k = 0;
+                L.state = c;
+                L.w = 1.0 / (double)nc;       // W0 = 1/N_c (walker.py:263)
+                L.thr = a.cutoff * L.w;       // strict cutoff W_c * W0 (walker.py:264)
+                if (REPLAY) {
+                    L.epos = __ldg(a.walk_off + g);
+                    L.eend = __ldg(a.walk_off + g + 1);
+                }
+                ++n_walks;
+            } else {
+                L.g = -2;
+            }
+        }
+    }
+    return !__all_sync(MCF_FULL, L.g == -2);
+}
+
+// One step of walker.py:270-288 for one lane: the emission at step k has
+// already been consumed by the caller; this draws, updates W and the state
+// and applies the termination rules.  Returns true when the walk ended.
+template <bool REPLAY>
+__device__ __forceinline__ bool advance(const WalkCommon &a, Lane &L, const NodeHdr &h, long long &tr, long long &ab) {
+    if (h.deg == 0) {  // absorbing row (walker.py:274-278)
+        ++ab;
+        return true;
+    }
+    long long e;
+    if (REPLAY) {
+        if (L.epos >= L.eend) {
+            atomicOr(a.err, 1);
+            return true;
+        }
+        e = __ldg(a.entries + L.epos);
+        ++L.epos;
+        if (e < h.start || e >= h.start + h.deg) atomicOr(a.err, 2);
+    } else {
+        e = draw_entry(a, h, L.k, L.wl, L.c);
+    }
+    int pc = __ldg(a.ecol + e);
+    L.w *= (pc < 0) ? -h.rsum : h.rsum;  // a/t = copysign(rowsum, a) (walker.py:124-125, :282)
+    L.state = pc & 0x7fffffff;
+    ++L.k;
+    if (!(fabs(L.w) > L.thr)) return true;  // walker.py:286-288
+    if (L.k >= a.max_steps) {               // step cap: truncated (walker.py:270, :289)
+        ++tr;
+        return true;
+    }
+    return false;
+}
+
+template <bool REPLAY>
+__global__ void __launch_bounds__(256) k_walk_action(WalkCommon a, double *__restrict__ xw) {
+    Lane L;
+    L.g = -1;
+    double x = 0.0;
+    long long n_walks = 0, em = 0, tr = 0, ab = 0;
+    while (refill<REPLAY>(a, L, n_walks)) {
+        if (L.g < 0) continue;
+        if (L.k == 0) x = 0.0;
+        NodeHdr h = load_hdr(a.hdr + L.state);
+        x = fma(__ldg(a.zeta + L.k + 2) * L.w, h.aux, x);  // q_c += zeta_{k+2} W r[l]
+        ++em;
+        if (advance<REPLAY>(a, L, h, tr, ab)) {
+            if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
+            xw[L.g - a.walk_begin] = x;
+            L.g = -1;
+        }
+    }
+    flush_stats(a.stats, n_walks, em, tr, ab);
+}
+
+// Diagonal-mode walks.  Slot layout of the emission buffer per MODE:
+//   EMIT_FIXED     walk rel owns slots [rel*L, rel*L + L)
+//   EMIT_REPLAY    walk g owns walk_off[g]-off_base+rel .. + draws+1
+//   EMIT_COUNT     no emission written; elen[rel] = number of emissions
+//   EMIT_EXPLICIT  walk rel owns [eoff[rel], eoff[rel+1]) (exclusive scan of a
+//                  previous EMIT_COUNT pass over the same Philox stream)
+// Each emission (state, zeta_{k+2} W_k) goes to slot sb + k; unused slots of a
+// walk are marked -1.
+enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_len, long long off_base,
+                                                   long long *__restrict__ eaux, int *__restrict__ est,
+                                                   double *__restrict__ ewt) {
+    constexpr bool REPLAY = MODE == EMIT_REPLAY;
+    Lane L;
+    L.g = -1;
+    long long n_walks = 0, em = 0, tr = 0, ab = 0;
+    long long sb = 0, scap = 0;
+    while (refill<REPLAY>(a, L, n_walks)) {
+        if (L.g < 0) continue;
+        const long long rel = L.g - a.walk_begin;
+        if (L.k == 0) {
+            if (MODE == EMIT_REPLAY) {
+                sb = L.epos - off_base + rel;
+                scap = L.eend - L.epos + 1;
+            } else if (MODE == EMIT_FIXED) {
+                sb = rel * slot_len;
+                scap = slot_len;
+            } else if (MODE == EMIT_EXPLICIT) {
+                sb = eaux[rel];
+                scap = eaux[rel + 1] - sb;
+            }
+        }
+        NodeHdr h = load_hdr(a.hdr + L.state);
+        if (MODE != EMIT_COUNT) {
+            est[sb + L.k] = L.state;
+            ewt[sb + L.k] = __ldg(a.zeta + L.k + 2) * L.w;
+        }
+        ++em;
+        long long emitted = L.k + 1;
+        if (advance<REPLAY>(a, L, h, tr, ab)) {
+            if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
+            if (MODE == EMIT_COUNT) eaux[rel] = emitted;
+            else
+                for (long long t = emitted; t < scap; ++t) est[sb + t] = -1;
+            L.g = -1;
+        }
+    }
+    if (MODE != EMIT_COUNT) flush_stats(a.stats, n_walks, em, tr, ab);
+}
+
+// hdr[i].aux = r[i]
+__global__ void k_set_aux(NodeHdr *__restrict__ hdr, const double *__restrict__ r, long long n) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) hdr[i].aux = r[i];
+}
+
+// q[c] = sum of the per-walk contributions of column c, fixed order; optional
+// variance of that mean from the per-walk spread (SE for the z-tests).
+// One warp per 32 consecutive columns: a lane sums a small column serially,
+// the warp cooperates on large ones.
+constexpr int SMALL_COL = 32;
+
+__global__ void k_col_reduce(const long long *__restrict__ walk_pre, long long col_begin, long long col_end,
+                             long long walk_begin, const double *__restrict__ xw, double *__restrict__ q,
+                             double *__restrict__ qvar) {
+    long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    long long c = col_begin + wid * 32 + lane;
+    bool in = c < col_end;
+    long long lo = 0, hi = 0;
+    if (in) {
+        lo = walk_pre[c] - walk_begin;
+        hi = walk_pre[c + 1] - walk_begin;
+    }
+    long long nc = hi - lo;
+    if (in && nc <= SMALL_COL) {
+        double s = 0.0;
+        for (long long i = lo; i < hi; ++i) s += xw[i];
+        q[c] = s;
+        if (qvar) {
+            double m2 = 0.0;
+            for (long long i = lo; i < hi; ++i) {
+                double d = (double)nc * xw[i] - s;
+                m2 += d * d;
+            }
+            qvar[c] = nc > 1 ? m2 / ((double)(nc - 1) * (double)nc) : 0.0;
+        }
+    }
+    unsigned big = __ballot_sync(MCF_FULL, in && nc > SMALL_COL);
+    while (big) {
+        int src = __ffs(big) - 1;
+        big &= big - 1;
+        long long blo = __shfl_sync(MCF_FULL, lo, src), bhi = __shfl_sync(MCF_FULL, hi, src);
+        long long bc = __shfl_sync(MCF_FULL, c, src);
+        double s = 0.0;
+        for (long long i = blo + lane; i < bhi; i += 32) s += xw[i];
+        s = warp_sum(s);
+        if (lane == 0) q[bc] = s;
+        if (qvar) {
+            double bn = (double)(bhi - blo), m2 = 0.0;
+            for (long long i = blo + lane; i < bhi; i += 32) {
+                double d = bn * xw[i] - s;
+                m2 += d * d;
+            }
+            m2 = warp_sum(m2);
+            if (lane == 0) qvar[bc] = m2 / ((bn - 1.0) * bn);
+        }
+    }
+}
+
+// y = alpha v + beta r + A x; G lanes per row, fixed reduction order.
+template <int G>
+__global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                       const double *__restrict__ vals, double alpha, const double *__restrict__ v, double beta,
+                       const double *__restrict__ r, const double *__restrict__ x, double *__restrict__ y,
+                       long long row_begin, long long row_end) {
+    long long i = row_begin + (((long long)blockIdx.x * blockDim.x + threadIdx.x) / G);
+    int sub = threadIdx.x % G;
+    bool in = i < row_end;
+    double s = 0.0;
+    if (in) {
+        long long e1 = row_ptr[i + 1];
+        for (long long e = row_ptr[i] + sub; e < e1; e += G) s = fma(__ldg(vals + e), __ldg(x + __ldg(col_ids + e)), s);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, G);
+    if (in && sub == 0) {
+        double h = 0.0;
+        if (v) h = alpha * v[i];
+        if (r) h += beta * r[i];
+        y[i] = h + s;
+    }
+}
+
+int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,
+         long long rb, long long re, cudaStream_t s) {
+    MCF_ARG(g && x && y, "mcf_spmv: null argument");
+    MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv: bad row range");
+    if (re == rb) return MCF_OK;
+    long long avg = g->nnz / g->n;
+    long long rows = re - rb;
+    const long long *rp = (const long long *)g->row_ptr;
+    if (avg <= 8) {
+        k_spmv<4><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+    } else if (avg <= 32) {
+        k_spmv<8><<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+    } else {
+        k_spmv<32><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+    }
+    MCF_LAUNCHED("k_spmv");
+    return MCF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host drivers
+// ---------------------------------------------------------------------------
+int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb,
+                 long long ce) {
+    MCF_ARG(g && p && walk_pre, "walk call: null argument");
+    MCF_ARG(p->max_steps >= 1, "max_steps must be at least 1");                          // walker.py:66-67
+    MCF_ARG(p->weight_cutoff > 0.0 && p->weight_cutoff < 1.0,
+            "weight_cutoff must lie strictly between 0 and 1");                         // walker.py:64-65
+    MCF_ARG(p->max_steps < (1ll << 31), "max_steps must be below 2^31");
+    MCF_ARG(p->zeta, "zeta coefficients missing");
+    MCF_ARG(0 <= cb && cb <= ce && ce <= g->n, "bad column range");
+    return MCF_OK;
+}
+
+int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                 WalkCommon &a, double **zeta_dev, int **blk, cudaStream_t s) {
+    long long wb = 0, we = 0;
+    int rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
+    if (rc) return rc;
+    rc = upload_zeta(p->zeta, p->max_steps + 2, zeta_dev, s);
+    if (rc) return rc;
+    long long nblk = 0;
+    rc = build_blk_col(walk_pre, cb, ce, wb, we, blk, &nblk, s);
+    if (rc) return rc;
+    a.hdr = g->hdr;
+    a.ecol = g->ecol;
+    a.cdf = g->cdf;
+    a.zeta = *zeta_dev;
+    a.walk_pre = walk_pre;
+    a.blk_col = *blk;
+    a.nblk = nblk;
+    a.walk_begin = wb;
+    a.walk_end = we;
+    a.col_last = (int)(ce > cb ? ce - 1 : cb);
+    a.max_steps = p->max_steps;
+    a.cutoff = p->weight_cutoff;
+    a.key0 = (uint32_t)(p->seed & 0xffffffffu);
+    a.key1 = (uint32_t)(p->seed >> 32);
+    a.walk_off = nullptr;
+    a.entries = nullptr;
+    return MCF_OK;
+}
+
+template <typename K>
+int walk_grid(K kernel, int threads, size_t smem) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    return per_sm * sm_count();
+}
+
+int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                     int mode, const long long *walk_off, const int *entries, long long slot_len, long long off_base,
+                     long long *eaux, int *est, double *ewt, long long *stats, int *err, cudaStream_t s) {
+    WalkCommon a;
+    double *zeta = nullptr;
+    int *blk = nullptr;
+    int rc = setup_common(g, p, walk_pre, cb, ce, a, &zeta, &blk, s);
+    if (rc) return rc;
+    unsigned long long *counter = nullptr;
+    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
+    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    a.counter = counter;
+    a.err = err;
+    a.stats = stats;
+    a.walk_off = walk_off;
+    a.entries = entries;
+    switch (mode) {
+        case EMIT_FIXED:
+            k_walk_emit<EMIT_FIXED><<<walk_grid(k_walk_emit<EMIT_FIXED>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt);
+            break;
+        case EMIT_REPLAY:
+            k_walk_emit<EMIT_REPLAY><<<walk_grid(k_walk_emit<EMIT_REPLAY>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt);
+            break;
+        case EMIT_COUNT:
+            k_walk_emit<EMIT_COUNT><<<walk_grid(k_walk_emit<EMIT_COUNT>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+            break;
+        default:
+            k_walk_emit<EMIT_EXPLICIT><<<walk_grid(k_walk_emit<EMIT_EXPLICIT>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+    }
+    MCF_LAUNCHED("k_walk_emit");
+    cudaFreeAsync(counter, s);
+    cudaFreeAsync(zeta, s);
+    cudaFreeAsync(blk, s);
+    return MCF_OK;
+}
+
+static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                  const long long *walk_off, const int *entries, const double *r, double *q, double *qvar,
+                  long long *stats, cudaStream_t s, bool replay) {
+    int rc = check_params(g, p, walk_pre, cb, ce);
+    if (rc) return rc;
+    MCF_ARG(r && q && stats, "action walk: null r/q/stats");
+    if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
+    WalkCommon a;
+    double *zeta = nullptr;
+    int *blk = nullptr;
+    rc = setup_common(g, p, walk_pre, cb, ce, a, &zeta, &blk, s);
+    if (rc) return rc;
+    long long nw = a.walk_end - a.walk_begin;
+    double *xw = nullptr;
+    unsigned long long *counter = nullptr;
+    int *err = nullptr;
+    MCF_CUDA(cudaMallocAsync(&xw, sizeof(double) * (nw > 0 ? nw : 1), s));
+    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) + sizeof(int) * 2, s));
+    err = (int *)(counter + 1);
+    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
+    a.counter = counter;
+    a.err = err;
+    a.stats = stats;
+    a.walk_off = walk_off;
+    a.entries = entries;
+    k_set_aux<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, r, g->n);
+    MCF_LAUNCHED("k_set_aux");
+    if (nw > 0) {
+        if (replay) {
+            k_walk_action<true><<<walk_grid(k_walk_action<true>, 256, 0), 256, 0, s>>>(a, xw);
+        } else {
+            k_walk_action<false><<<walk_grid(k_walk_action<false>, 256, 0), 256, 0, s>>>(a, xw);
+        }
+        MCF_LAUNCHED("k_walk_action");
+    }
+    long long ncol = ce - cb;
+    if (ncol > 0) {
+        long long warps = (ncol + 31) / 32;
+        k_col_reduce<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, a.walk_begin, xw, q, qvar);
+        MCF_LAUNCHED("k_col_reduce");
+    }
+    int herr = 0;
+    if (replay) {
+        MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+    }
+    cudaFreeAsync(xw, s);
+    cudaFreeAsync(counter, s);
+    cudaFreeAsync(zeta, s);
+    cudaFreeAsync(blk, s);
+    if (herr) {
+        set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) +
+                  "): entries missing, surplus, or outside the current row");
+        return MCF_ERR_ARGUMENT;
+    }
+    return MCF_OK;
+}
+
+}  // namespace mcf
+
+extern "C" {
+
+int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,
+             int64_t row_begin, int64_t row_end, void *stream) {
+    return mcf::spmv(g, alpha, v, beta, r, x, y, row_begin, row_end, (cudaStream_t)stream);
+}
+
+int mcf_walk_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin,
+                    int64_t col_end, const double *r, double *q, double *q_var, int64_t *stats, void *stream) {
+    return mcf::action(g, p, (const long long *)walk_pre, col_begin, col_end, nullptr, nullptr, r, q, q_var,
+                       (long long *)stats, (cudaStream_t)stream, false);
+}
+
+int mcf_replay_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin,
+                      int64_t col_end, const int64_t *walk_off, const int32_t *entries, const double *r, double *q,
+                      int64_t *stats, void *stream) {
+    return mcf::action(g, p, (const long long *)walk_pre, col_begin, col_end, (const long long *)walk_off, entries,
+                       r, q, nullptr, (long long *)stats, (cudaStream_t)stream, true);
+}
+
+}  // extern "C"

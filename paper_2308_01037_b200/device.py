@@ -1,0 +1,226 @@
+"""Device-resident graph: CSR/CSC arrays in HBM plus the C-ABI handle that owns
+the derived transition tables (node headers, packed column ids, row CDFs,
+column norms, start distribution).
+
+PyTorch only provides device memory and the stream; every computation is a
+kernel of libmcfunm_cuda.so called through ``_native``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ArgumentError, DegenerateInputError, DeviceError
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the estimator runs only on the GPU (no CPU fallback)")
+    N.lib()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ArgumentError(f"device must be a CUDA device, got {dev}")
+    return dev
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class WalkParams:
+    """mcf_walk_params for one call; keeps the zeta table alive."""
+
+    def __init__(self, config, zeta: np.ndarray):
+        self.zeta = np.ascontiguousarray(zeta, dtype=np.float64)
+        if self.zeta.size < config.max_steps + 2:
+            raise ArgumentError("zeta table shorter than max_steps + 2")
+        self.c = N.McfWalkParams(int(config.max_steps), float(config.weight_cutoff),
+                                 int(config.seed) & 0xFFFFFFFFFFFFFFFF,
+                                 self.zeta.ctypes.data_as(C.c_void_p), 0)
+
+
+class DeviceGraph:
+    """Square sparse matrix on one GPU, scaled by ``gamma`` on the device.
+
+    ``a`` is any object with scipy ``.csr``/``.csc`` arrays (this package's or
+    the reference's SparseMatrix).  A matrix with ``symmetric_hint`` whose CSC
+    arrays equal its CSR arrays is uploaded once and the CSC view aliases it.
+    """
+
+    def __init__(self, a, gamma: float = 1.0, device=None):
+        self.device = require_cuda(device)
+        csr, csc = a.csr, a.csc
+        self.n = int(csr.shape[0])
+        self.nnz = int(csr.nnz)
+        if self.nnz == 0:
+            raise DegenerateInputError("all columns are zero: the initial distribution is undefined")
+        if not gamma > 0:
+            raise ArgumentError(f"gamma must be positive, got {gamma}")
+        self.gamma = float(gamma)
+        self.symmetric_hint = bool(getattr(a, "symmetric_hint", False))
+        if not csr.has_sorted_indices:
+            csr = csr.sorted_indices()
+        dev = self.device
+        self.row_ptr = torch.from_numpy(np.ascontiguousarray(csr.indptr, dtype=np.int64)).to(dev)
+        self.col_ids = torch.from_numpy(np.ascontiguousarray(csr.indices, dtype=np.int32)).to(dev)
+        self.vals = torch.from_numpy(np.ascontiguousarray(csr.data, dtype=np.float64)).to(dev)
+        same = (self.symmetric_hint and csc.indptr.shape == csr.indptr.shape
+                and (csc is csr or (np.array_equal(csc.indptr, csr.indptr) and np.array_equal(csc.indices, csr.indices)
+                                    and np.array_equal(csc.data, csr.data))))
+        if same:
+            self.csc_ptr, self.csc_rows, self.csc_vals = self.row_ptr, self.col_ids, self.vals
+        else:
+            if not csc.has_sorted_indices:
+                csc = csc.sorted_indices()
+            self.csc_ptr = torch.from_numpy(np.ascontiguousarray(csc.indptr, dtype=np.int64)).to(dev)
+            self.csc_rows = torch.from_numpy(np.ascontiguousarray(csc.indices, dtype=np.int32)).to(dev)
+            self.csc_vals = torch.from_numpy(np.ascontiguousarray(csc.data, dtype=np.float64)).to(dev)
+        if self.gamma != 1.0:  # scale() on the device: every stored value times gamma
+            self.vals = self.vals * self.gamma
+            self.csc_vals = self.vals if same else self.csc_vals * self.gamma
+        self.aliased = same
+        self._build()
+
+    @classmethod
+    def from_device_arrays(cls, n, row_ptr, col_ids, vals, csc_ptr=None, csc_rows=None, csc_vals=None,
+                           symmetric=True):
+        """Adopt arrays that already live on the GPU (graph generators, benches)."""
+        self = cls.__new__(cls)
+        self.device = require_cuda(row_ptr.device)
+        self.n = int(n)
+        self.nnz = int(col_ids.numel())
+        if self.nnz == 0:
+            raise DegenerateInputError("all columns are zero: the initial distribution is undefined")
+        self.gamma = 1.0
+        self.symmetric_hint = bool(symmetric)
+        self.row_ptr = row_ptr.to(torch.int64).contiguous()
+        self.col_ids = col_ids.to(torch.int32).contiguous()
+        self.vals = vals.to(torch.float64).contiguous()
+        if csc_ptr is None:
+            if not symmetric:
+                raise ArgumentError("non-symmetric input needs CSC arrays")
+            self.csc_ptr, self.csc_rows, self.csc_vals = self.row_ptr, self.col_ids, self.vals
+            self.aliased = True
+        else:
+            self.csc_ptr = csc_ptr.to(torch.int64).contiguous()
+            self.csc_rows = csc_rows.to(torch.int32).contiguous()
+            self.csc_vals = csc_vals.to(torch.float64).contiguous()
+            self.aliased = False
+        self._build()
+        return self
+
+    def scaled(self, gamma: float) -> "DeviceGraph":
+        """New handle over gamma * A (device multiply, structure shared)."""
+        if not gamma > 0:
+            raise ArgumentError(f"gamma must be positive, got {gamma}")
+        vals = self.vals * gamma
+        if self.aliased:
+            out = DeviceGraph.from_device_arrays(self.n, self.row_ptr, self.col_ids, vals, symmetric=True)
+        else:
+            out = DeviceGraph.from_device_arrays(self.n, self.row_ptr, self.col_ids, vals, self.csc_ptr,
+                                                 self.csc_rows, self.csc_vals * gamma, self.symmetric_hint)
+        out.gamma = self.gamma * gamma
+        return out
+
+    # ------------------------------------------------------------------
+    def _build(self):
+        self._csr = N.McfCsr(self.n, self.nnz, _ptr(self.row_ptr), _ptr(self.col_ids), _ptr(self.vals),
+                             _ptr(self.csc_ptr), _ptr(self.csc_rows), _ptr(self.csc_vals))
+        h = C.c_void_p()
+        N.check(N.lib().mcf_graph_create(C.byref(self._csr), self.stream, C.byref(h)), "mcf_graph_create")
+        self.handle = h
+        info = N.McfGraphInfo()
+        N.check(N.lib().mcf_graph_get_info(h, C.byref(info)), "mcf_graph_get_info")
+        self.info = {f: getattr(info, f) for f, _ in info._fields_}
+
+    @property
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def close(self):
+        h = getattr(self, "handle", None)
+        if h:
+            N.lib().mcf_graph_destroy(h)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _f64(self, n=None):
+        return torch.empty(self.n if n is None else n, dtype=torch.float64, device=self.device)
+
+    def new_stats(self):
+        return torch.zeros(N.MCF_STATS_LEN, dtype=torch.int64, device=self.device)
+
+    # ------------------------------------------------------------------ tables
+    def tables(self) -> dict:
+        rs, cn, ip = self._f64(), self._f64(), self._f64()
+        N.check(N.lib().mcf_graph_tables(self.handle, _ptr(rs), _ptr(cn), _ptr(ip), self.stream), "tables")
+        return {"row_abs_sum": rs, "col_norms": cn, "init_prob": ip}
+
+    def diagonal(self) -> torch.Tensor:
+        rows = torch.repeat_interleave(torch.arange(self.n, device=self.device), self.row_ptr.diff())
+        d = torch.zeros(self.n, dtype=torch.float64, device=self.device)
+        on = rows == self.col_ids.to(torch.int64)
+        d[rows[on]] = self.vals[on]
+        return d
+
+    # ------------------------------------------------------------------ budgets
+    def allocate(self, n_walks: int):
+        ni = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        pre = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
+        N.check(N.lib().mcf_allocate_walks(self.handle, int(n_walks), _ptr(ni), _ptr(pre), self.stream),
+                "mcf_allocate_walks")
+        return ni, pre
+
+    def budgets(self, ni):
+        ni = torch.as_tensor(np.asarray(ni, dtype=np.int64)).to(self.device)
+        if ni.numel() != self.n or bool((ni < 0).any()):
+            raise ArgumentError("walk budgets must be n non-negative integers")
+        pre = torch.zeros(self.n + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(ni, 0, out=pre[1:])
+        return ni, pre
+
+    # ------------------------------------------------------------------ kernels
+    def spmv(self, x, alpha=0.0, v=None, beta=0.0, r=None, out=None, rows=None):
+        out = self._f64() if out is None else out
+        rb, re = (0, self.n) if rows is None else rows
+        N.check(N.lib().mcf_spmv(self.handle, float(alpha), _ptr(v), float(beta), _ptr(r), _ptr(x), _ptr(out),
+                                 int(rb), int(re), self.stream), "mcf_spmv")
+        return out
+
+    def walk_action(self, params: WalkParams, walk_pre, r, q, qvar=None, cols=None, stats=None):
+        cb, ce = (0, self.n) if cols is None else cols
+        N.check(N.lib().mcf_walk_action(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce), _ptr(r),
+                                        _ptr(q), _ptr(qvar), _ptr(stats), self.stream), "mcf_walk_action")
+
+    def replay_action(self, params: WalkParams, walk_pre, walk_off, entries, r, q, cols=None, stats=None):
+        cb, ce = (0, self.n) if cols is None else cols
+        N.check(N.lib().mcf_replay_action(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce),
+                                          _ptr(walk_off), _ptr(entries), _ptr(r), _ptr(q), _ptr(stats),
+                                          self.stream), "mcf_replay_action")
+
+    def walk_diag(self, params: WalkParams, walk_pre, pcol, cols=None, stats=None):
+        cb, ce = (0, self.n) if cols is None else cols
+        N.check(N.lib().mcf_walk_diag(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce), _ptr(pcol),
+                                      _ptr(stats), self.stream), "mcf_walk_diag")
+
+    def replay_diag(self, params: WalkParams, walk_pre, walk_off, entries, pcol, cols=None, stats=None):
+        cb, ce = (0, self.n) if cols is None else cols
+        N.check(N.lib().mcf_replay_diag(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce),
+                                        _ptr(walk_off), _ptr(entries), _ptr(pcol), _ptr(stats), self.stream),
+                "mcf_replay_diag")
+
+    def diag_combine(self, z0, z1, pcol, d=None, rows=None):
+        d = self._f64() if d is None else d
+        rb, re = (0, self.n) if rows is None else rows
+        N.check(N.lib().mcf_diag_combine(self.handle, float(z0), float(z1), _ptr(pcol), _ptr(d), int(rb), int(re),
+                                         self.stream), "mcf_diag_combine")
+        return d

@@ -1,0 +1,246 @@
+"""Device parity against the reference (golden fixtures) and the CPU oracle.
+
+Bar (BASELINE.json north_star): replaying the reference's own sampled entry
+stream reproduces its estimates to 1e-10 relative (fp64); integer work (walk
+budgets, emission / truncation counts) is bit-exact; the device transition
+tables equal the reference's bit for bit."""
+import numpy as np
+import pytest
+from scipy import sparse
+
+from oracle import port
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10  # replay tolerance stated by the north star
+
+
+@pytest.fixture(scope="module")
+def mc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2308_01037_b200 as m
+    return m
+
+
+def as_matrix(a: port.Csr, symmetric=False):
+    class M:
+        pass
+    m = M()
+    m.csr = sparse.csr_array((a.vals, a.col_ids.astype(np.int32), a.row_ptr), shape=(a.n, a.n))
+    m.csc = sparse.csc_array((a.csc_vals, a.csc_rows.astype(np.int32), a.csc_ptr), shape=(a.n, a.n))
+    m.symmetric_hint = symmetric
+    return m
+
+
+def rel_err(x, ref):
+    x, ref = np.asarray(x), np.asarray(ref)
+    scale = np.maximum(np.abs(ref), 1e-300)
+    return float(np.max(np.abs(x - ref) / scale))
+
+
+@pytest.mark.parametrize("name", golden_io.CASES)
+def test_device_tables_bitwise(mc, name):
+    c = golden_io.load(name)
+    g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
+    t = {k: v.cpu().numpy() for k, v in g.tables().items()}
+    assert np.array_equal(t["row_abs_sum"], c["m_row_abs_sum"])
+    assert np.array_equal(t["col_norms"], c["m_col_norms"])
+    assert np.array_equal(t["init_prob"], c["m_init_prob"])
+    assert g.info["max_row_abs_sum"] ** 2 == float(c["alpha"])
+
+
+@pytest.mark.parametrize("name", golden_io.CASES)
+def test_device_allocation_bitwise(mc, name):
+    c = golden_io.load(name)
+    g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
+    for ns in (1, 7, 1000, 12345, 10 * c.n + 3):
+        ni, pre = g.allocate(ns)
+        assert np.array_equal(ni.cpu().numpy(), c[f"ni_{ns}"]), ns
+        assert int(pre[-1]) == ns
+
+
+@pytest.mark.parametrize("name", golden_io.CASES)
+def test_replay_matches_reference(mc, name):
+    c = golden_io.load(name)
+    g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
+    for j, r in enumerate(c.runs):
+        p = f"r{j}_"
+        cfg = mc.WalkConfig(r["n_walks"], r["cutoff"], r["max_steps"], r["seed"])
+        if r["mode"] == "action":
+            out = mc.rand_funm_action(g, r["tag"], c[p + "v"], cfg, replay=c.record(j))
+            assert rel_err(out.values, c[p + "y"]) < REL
+            assert rel_err(out.aux["q"].cpu().numpy(), c[p + "q"]) < REL or np.allclose(
+                out.aux["q"].cpu().numpy(), c[p + "q"], rtol=REL, atol=1e-300)
+        else:
+            out = mc.rand_funm_diag(g, r["tag"], cfg, replay=c.record(j))
+            assert rel_err(out.values, c[p + "d"]) < REL
+        assert out.emissions == int(c[p + "emissions"])
+        assert out.truncated == int(c[p + "truncated"])
+        assert out.walks == r["n_walks"]
+
+
+def test_replay_rejects_corrupt_stream(mc):
+    c = golden_io.load("signed6")
+    g = mc.DeviceGraph(as_matrix(c.sa))
+    r = c.runs[0]
+    rec = c.record(0)
+    bad = port.Record(rec.walk_pre, rec.walk_off.copy(), rec.entries.copy())
+    bad.walk_off[1:] += 1  # walk 0 claims an extra entry it never consumes
+    bad.entries = np.concatenate([bad.entries[:1], bad.entries])
+    cfg = mc.WalkConfig(r["n_walks"], r["cutoff"], r["max_steps"], r["seed"])
+    with pytest.raises(mc.ArgumentError):
+        mc.rand_funm_action(g, r["tag"], c["r0_v"], cfg, replay=bad)
+
+
+def test_replay_oracle_stream_er2000(mc):
+    """Larger case recorded at test time by the oracle (config-1 shape, ER LCC)."""
+    rng = np.random.default_rng(4)
+    n = 2000
+    u, v = rng.integers(0, n, 8000), rng.integers(0, n, 8000)
+    keep = u != v
+    m = sparse.coo_array((np.ones(keep.sum() * 2), (np.r_[u[keep], v[keep]], np.r_[v[keep], u[keep]])), shape=(n, n))
+    m = sparse.csr_array(m)
+    m.data[:] = 1.0
+    m.sum_duplicates()
+    m.data[:] = 1.0
+    a = port.Csr.from_any(m)
+    lam = float(np.max(np.linalg.eigvalsh(m.toarray())))
+    a = a.scaled(1.0 / lam)
+    g = mc.DeviceGraph(as_matrix(a, True))
+    for mode in ("action", "diag"):
+        if mode == "action":
+            run = port.funm_action(a, "exponential", np.ones(n), 20 * n, 1e-300, 28, 0, record=True)
+            out = mc.rand_funm_action(g, "exponential", np.ones(n), mc.WalkConfig(20 * n, 1e-300, 28, 0),
+                                      replay=run.record)
+        else:
+            run = port.funm_diag(a, "exponential", 20 * n, 1e-300, 28, 0, record=True)
+            out = mc.rand_funm_diag(g, "exponential", mc.WalkConfig(20 * n, 1e-300, 28, 0), replay=run.record)
+        assert rel_err(out.values, run.payload) < REL
+        assert out.emissions == run.emissions
+
+
+@pytest.mark.parametrize("m_steps", [1, 5, 28])
+def test_truncation_mapping_kat_device(mc, m_steps):
+    """gamma*[[0,1],[1,0]]: deterministic walks -> exactly dense_funm(terms=M+1)."""
+    for gam in (0.5, 0.9):
+        a = mc.SparseMatrix.from_dense([[0, gam], [gam, 0]], True)
+        ref = port.dense_funm(port.Csr.from_dense([[0, gam], [gam, 0]]), "exponential", m_steps + 1)
+        cfg = mc.WalkConfig(64, 1e-300, m_steps, 3)
+        d = mc.rand_funm_diag(a, mc.EXPONENTIAL, cfg)
+        y = mc.rand_funm_action(a, mc.EXPONENTIAL, np.ones(2), cfg)
+        np.testing.assert_allclose(d.values, np.diag(ref), rtol=4e-15)
+        np.testing.assert_allclose(y.values, ref.sum(1), rtol=4e-15)
+        assert d.truncated == 64 and y.emissions == 64 * m_steps
+
+
+def test_spec_closed_forms_device(mc):
+    """zero-variance involutory graph."""
+    a = mc.SparseMatrix.from_dense([[0, 1], [1, 0]], True)
+    cfg = mc.WalkConfig(10**6, 1e-10, 10_000, 0)
+    rep = mc.total_communicability(a, 0.1, cfg)
+    np.testing.assert_allclose(rep.scores, np.exp(0.1), rtol=5e-3)
+    rep = mc.subgraph_centrality(a, 0.1, cfg)
+    np.testing.assert_allclose(rep.scores, np.cosh(0.1), rtol=5e-3)
+    k = mc.katz_centrality(a, 0.5, mc.WalkConfig(10**5, 1e-10, 10_000, 0), gamma=0.5)
+    np.testing.assert_allclose(k.scores, [2.0, 2.0], rtol=5e-3)
+    kc = mc.katz_centrality(a, 0.5, None, method="cg", gamma=0.5)
+    np.testing.assert_allclose(kc.scores, [2.0, 2.0], rtol=1e-9)
+
+
+def test_self_loop_and_absorbing_kats(mc):
+    # self loop 0.5, W_c = 0.1 -> 4 emissions
+    a = mc.SparseMatrix.from_dense([[0.5]])
+    y = mc.rand_funm_action(a, mc.EXPONENTIAL, np.ones(1), mc.WalkConfig(1, 0.1, 100, 0))
+    assert y.emissions == 4 and y.truncated == 0
+    # absorbing start column: single emission then terminal
+    b = mc.SparseMatrix.from_dense([[0, 0], [1, 0]])
+    y = mc.rand_funm_action(b, mc.EXPONENTIAL, np.ones(2), mc.WalkConfig(5, 1e-6, 100, 0))
+    assert y.emissions == 5 and y.absorbed == 5
+
+
+def test_degenerate_and_argument_errors(mc):
+    with pytest.raises(mc.DegenerateInputError):
+        mc.DeviceGraph(mc.SparseMatrix(sparse.csr_array((3, 3)), sparse.csc_array((3, 3))))
+    a = mc.SparseMatrix.from_dense([[0, 1], [1, 0]], True)
+    with pytest.raises(mc.ArgumentError):
+        mc.rand_funm_action(a, mc.EXPONENTIAL, np.ones(3), mc.WalkConfig(10))
+    with pytest.raises(mc.ArgumentError):
+        mc.subgraph_centrality(mc.SparseMatrix.from_dense([[0, 1], [0, 0]]), 0.1, mc.WalkConfig(10))
+
+
+def test_determinism_and_partition_invariance(mc):
+    import torch
+    c = golden_io.load("kron8")
+    g = mc.DeviceGraph(as_matrix(c.sa, True))
+    cfg = mc.WalkConfig(50_000, 1e-300, 23, 9)
+    from paper_2308_01037_b200.device import WalkParams
+    z = mc.EXPONENTIAL.prefix(cfg.max_steps + 2)
+    p = WalkParams(cfg, z)
+    ni, pre = g.allocate(cfg.n_walks)
+    r = g.spmv(torch.ones(g.n, dtype=torch.float64, device=g.device))
+    outs = []
+    for cuts in ([0, g.n], [0, 57, g.n], [0, 3, 100, 101, g.n]):
+        q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
+        pc = torch.zeros(g.nnz, dtype=torch.float64, device=g.device)
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            g.walk_action(p, pre, r, q, cols=(lo, hi), stats=g.new_stats())
+            g.walk_diag(p, pre, pc, cols=(lo, hi), stats=g.new_stats())
+        outs.append((q.cpu().numpy(), g.diag_combine(z[0], z[1], pc).cpu().numpy()))
+    for q, d in outs[1:]:
+        assert np.array_equal(q, outs[0][0])
+        assert np.array_equal(d, outs[0][1])
+
+
+def _z_check(z, n):
+    from scipy.stats import norm
+    bound = norm.isf(0.01 / (2 * n))  # Bonferroni
+    assert np.mean(np.abs(z) <= 3) >= 0.99, np.sort(np.abs(z))[-10:]
+    assert np.max(np.abs(z)) <= bound + 0.5, (np.max(np.abs(z)), bound)
+    assert abs(np.mean(z)) < 0.15 and 0.8 < np.std(z) < 1.2, (np.mean(z), np.std(z))
+
+
+def test_device_rng_action_statistics(mc):
+    """Device RNG vs exact 30-term Taylor action (SURVEY.md §4 z-test recipe)."""
+    c = golden_io.load("ba400")
+    g = mc.DeviceGraph(as_matrix(c.sa, True))
+    cfg = mc.WalkConfig(400 * 5000, 1e-300, 28, 123)
+    y = mc.rand_funm_action(g, mc.EXPONENTIAL, np.ones(c.n), cfg, stderr=True)
+    exact = port.taylor_action(c.sa, "exponential", np.ones(c.n), 29)
+    _z_check((y.values - exact) / y.stderr, c.n)
+
+
+def test_device_rng_diag_statistics(mc):
+    """Device RNG diag vs exact truncated series, SE from independent replicas."""
+    c = golden_io.load("er300")
+    g = mc.DeviceGraph(as_matrix(c.sa, True))
+    exact = np.diag(port.dense_funm(c.sa, "exponential", 29))
+    reps = np.array([mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(300 * 400, 1e-300, 28, s)).values
+                     for s in range(32)])
+    z = (reps.mean(0) - exact) / (reps.std(0, ddof=1) / np.sqrt(reps.shape[0]))
+    assert np.mean(np.abs(z) <= 3.5) >= 0.98
+    assert abs(np.mean(z)) < 0.3
+
+
+def test_device_rng_weighted_signed_rows(mc):
+    """Non-uniform rows (inverse-CDF path) and negative values (packed signs)."""
+    c = golden_io.load("signed6")
+    g = mc.DeviceGraph(as_matrix(c.sa))
+    exact = port.taylor_action(c.sa, "exponential", np.ones(c.n), 41)
+    reps = np.array([mc.rand_funm_action(g, mc.EXPONENTIAL, np.ones(c.n), mc.WalkConfig(200_000, 1e-300, 40, s))
+                     .values for s in range(16)])
+    z = (reps.mean(0) - exact) / (reps.std(0, ddof=1) / 4.0)
+    assert np.all(np.abs(z) < 5), z
+
+
+def test_katz_resolvent_statistics(mc):
+    c = golden_io.load("sw64_katz")
+    a = as_matrix(c.a, True)
+    gam = c.gamma
+    exact = port.cg_solve(c.a, gam, np.ones(c.n), tol=1e-13)
+    rep = mc.katz_centrality(a, 0.85, mc.WalkConfig(10**6, 1e-8, 10_000, 1), stderr=True)
+    assert rep.gamma == pytest.approx(gam, rel=1e-15)
+    z = (rep.scores - exact) / rep.result.stderr
+    assert np.max(np.abs(z)) < 5
