@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the walk-sampling estimator (BASELINE.json metric: walk-steps/s
+and nodes/s; achieved HBM GB/s vs peak).
+
+Default workload = BASELINE configs[1] ("config 2"): total communicability
+exp(beta A) 1 on a Barabasi-Albert graph, n = 1e6, m = 4, beta = 1/lambda_max,
+30 Taylor terms (max_steps = 28), 10,000 batches x 64 = 640,000 walks.
+A "step" is one full estimator pass: walk budgets, r = A v, the walks, the
+per-column reduction and y = z0 v + z1 r + A q.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|1] [--impl mcfunm|reference]
+
+Under torchrun (N > 1) the start columns are sharded over the ranks and the
+per-column results assembled with NCCL (paper_2308_01037_b200/parallel.py).
+Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "walk-steps/s and nodes/s at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+BYTES_PER_STEP = 64  # two dependent random 32-B sectors per emitted step
+
+CONFIGS = {
+    2: dict(workload="config2: total communicability exp(beta A) 1, Barabasi-Albert n=1e6 m=4, "
+                     "beta=1/lambda_max, 30 Taylor terms, 10,000 batches x 64 walks",
+            kind="action", graph="ba", n=1_000_000, m=4, n_walks=640_000, max_steps=28, cutoff=1e-300, seed=0),
+    1: dict(workload="config1: subgraph centrality diag(exp(beta A)), Erdos-Renyi n=1e4 mean degree 8 (LCC), "
+                     "beta=1/lambda_max, 30 Taylor terms, 1000 walks per node",
+            kind="diag", graph="er", n=10_000, deg=8, walks_per_node=1000, max_steps=28, cutoff=1e-300, seed=0),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_graph(cfg, pinned=False):
+    from paper_2308_01037_b200 import graphs
+    if cfg["graph"] == "ba":
+        a = graphs.barabasi_albert(cfg["n"], cfg["m"], seed=cfg["seed"], pinned=pinned)
+    else:
+        a = graphs.erdos_renyi_lcc(cfg["n"], cfg["deg"], seed=cfg["seed"])
+    beta = 1.0 / graphs.lambda_max(a)
+    n_walks = cfg.get("n_walks") or cfg["walks_per_node"] * a.n
+    return a, beta, n_walks
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------
+# clocks during the timed region
+# --------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# CPU legs (oracle port of the reference, sampled)
+# --------------------------------------------------------------------------
+_CPU = {}
+
+
+def _cpu_worker(cols):
+    from oracle import port
+    g = _CPU
+    t0 = time.perf_counter()
+    if g["kind"] == "action":
+        _, em = port.action_columns(g["t"], g["r"], g["z"], g["ni"], cols, g["max_steps"], g["cutoff"], g["seed"])
+    else:
+        _, em = port.diag_columns(g["A"], g["t"], g["z"], g["ni"], cols, g["max_steps"], g["cutoff"], g["seed"])
+    return em, time.perf_counter() - t0
+
+
+class CpuBaseline:
+    """The reference's CPU algorithm (oracle/port.py restatement, same
+    PCG64DXSM streams and searchsorted walker) over a bounded, evenly spaced
+    sample of the walked columns, on all host cores (fork pool)."""
+
+    def __init__(self, a, beta, n_walks, cfg, cores=None):
+        import multiprocessing as mp
+        from oracle import port
+        t0 = time.perf_counter()
+        A = port.Csr.from_any(a).scaled(beta)
+        t = port.transition_tables(A)
+        ni = port.allocate(t, n_walks)
+        z = port.zeta_prefix("exponential", cfg["max_steps"] + 2)
+        _CPU.update(kind=cfg["kind"], t=t, A=A, ni=ni, z=z, r=A.scipy_csr() @ np.ones(A.n),
+                    max_steps=cfg["max_steps"], cutoff=cfg["cutoff"], seed=cfg["seed"])
+        self.setup_s = time.perf_counter() - t0
+        self.walked = np.flatnonzero(ni)
+        self.ni = ni
+        self.n = A.n
+        self.total_emissions_est = None
+        self.cores = cores or os.cpu_count() or 1
+        self.pool = mp.get_context("fork").Pool(self.cores)
+        # calibrate: per-column cost on a small evenly spaced probe
+        probe = self.walked[:: max(1, self.walked.size // 256)][:256]
+        em, dt = _cpu_worker(probe)
+        self.sec_per_col = dt / max(1, probe.size)
+        self.em_per_col = em / max(1, probe.size)
+
+    def run(self, budget_s):
+        k = int(min(self.walked.size, max(self.cores, self.cores * budget_s / max(self.sec_per_col, 1e-9))))
+        cols = self.walked[np.linspace(0, self.walked.size - 1, k).astype(np.int64)]
+        chunks = np.array_split(cols, self.cores * 4)
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_worker, chunks)
+        wall = time.perf_counter() - t0
+        em = sum(r[0] for r in res)
+        return em, wall, k
+
+    def describe(self, k):
+        return (f"{k} of {self.walked.size} walked start columns (evenly spaced by index), full walks of each "
+                f"column, reference PCG64DXSM streams; {self.cores} processes")
+
+    def close(self):
+        self.pool.terminate()
+
+
+# --------------------------------------------------------------------------
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    a, beta, n_walks = make_graph(cfg)
+    cpu = CpuBaseline(a, beta, n_walks, cfg)
+    per_step = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu.run(per_step / 4)
+    em_tot, wall_tot, k = 0, 0.0, 0
+    for _ in range(args.steps):
+        em, wall, k = cpu.run(per_step)
+        em_tot += em
+        wall_tot += wall
+    cpu.close()
+    value = em_tot / wall_tot
+    total_em = cpu.em_per_col * cpu.walked.size
+    line = {
+        "impl": "reference", "metric": "walk-steps/s", "baseline_metric": BASELINE_METRIC, "value": value,
+        "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall_tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "nodes_per_s": cpu.n / (total_em / value),
+        "config": {"workload": cfg["workload"], "n": int(a.n), "nnz": int(a.nnz), "n_walks": int(n_walks),
+                   "beta": beta, "max_steps": cfg["max_steps"], "weight_cutoff": cfg["cutoff"]},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cpu.cores, "kind": "port",
+                         "sample": cpu.describe(k)},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_device(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2308_01037_b200 as mc
+    from paper_2308_01037_b200 import _native, parallel
+    from paper_2308_01037_b200.device import DeviceGraph, WalkParams
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _native.lib()
+
+    t0 = time.perf_counter()
+    a, beta, n_walks = make_graph(cfg, pinned=True)
+    log(f"[bench] graph n={a.n} nnz={a.nnz} beta={beta:.6e} walks={n_walks} ({time.perf_counter() - t0:.1f}s)")
+    wcfg = mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"], cfg["seed"])
+    z = mc.EXPONENTIAL.prefix(cfg["max_steps"] + 2)
+    params = WalkParams(wcfg, z)
+    g = DeviceGraph(a, gamma=beta)
+    v = torch.ones(g.n, dtype=torch.float64, device=g.device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=g.device)  # > 126 MB L2
+
+    def step():
+        if cfg["kind"] == "action":
+            return parallel.sharded_action(g, mc.EXPONENTIAL, v, wcfg, params=params)
+        return parallel.sharded_diag(g, mc.EXPONENTIAL, wcfg, params=params)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    _native.check(lib.mcf_graph_kernel_times(g.handle, None, None, None))
+
+    # ---- device-resident timed region -------------------------------------------------
+    params.c.flags = _native.MCF_FLAG_TIME_KERNELS
+    clocks = Clocks(local) if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stats = []
+    launches0 = lib.mcf_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record()
+        _, st = step()
+        ev[i][1].record()
+        stats.append(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.mcf_kernel_launches() - launches0
+    clk = clocks.stop() if clocks else None
+    ms = sum(s.elapsed_time(e) for s, e in ev)
+    walk_ms, q_ms, walk_n = _native.C.c_double(), _native.C.c_double(), _native.C.c_int64()
+    _native.check(lib.mcf_graph_kernel_times(g.handle, _native.C.byref(walk_ms), _native.C.byref(q_ms),
+                                             _native.C.byref(walk_n)))
+    params.c.flags = 0
+    # emissions of the whole job (all ranks) over the timed steps
+    em_t = torch.stack([s_[1] for s_ in stats]).sum().to(torch.float64).reshape(1)
+    if world > 1:
+        dist.all_reduce(em_t)
+        t_ms = torch.tensor([ms], dtype=torch.float64, device=g.device)
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        ms = float(t_ms.item())
+    em_per_step = float(em_t.item()) / args.steps
+    value = em_per_step * args.steps / (ms / 1e3)
+    nodes_per_s = g.n * args.steps / (ms / 1e3)
+
+    # ---- dominant kernel roofline -------------------------------------------------------
+    peak, peak_src = measured_peak()
+    walk_avg_ms = walk_ms.value / max(1, walk_n.value)
+    em_per_walk_launch = em_per_step / world  # this rank's launches process its share
+    achieved = BYTES_PER_STEP * em_per_walk_launch / (walk_avg_ms / 1e3) / 1e9 if walk_avg_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": "k_walk_action" if cfg["kind"] == "action" else "k_walk_emit",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src, "bytes_per_step": BYTES_PER_STEP,
+                "kernel_ms_avg": walk_avg_ms, "kernel_share_of_step": (walk_ms.value / ms) if ms else None,
+                "note": "algorithmic bytes = 64 B x emissions per launch; config-2 tables (~70 MB touched) fit in "
+                        "the 126 MB L2 after the flush, so frac can exceed the HBM roofline"}
+    if cfg["kind"] == "diag":
+        roofline["q_kernel_ms"] = q_ms.value / max(1, args.steps)
+
+    # ---- end to end through the public API (host matrix -> host result) --------------
+    e2e = None
+    if not args.no_e2e:
+        h2d = int(a.csr.indptr.nbytes + a.csr.indices.nbytes + a.csr.data.nbytes)
+        d2h = 8 * a.n
+        e2e_ms = []
+        for i in range(max(1, args.steps) + 1):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ge = DeviceGraph(a, gamma=beta)
+            ve = torch.ones(ge.n, dtype=torch.float64, device=ge.device)
+            if cfg["kind"] == "action":
+                y, _ = parallel.sharded_action(ge, mc.EXPONENTIAL, ve, wcfg)
+            else:
+                y, _ = parallel.sharded_diag(ge, mc.EXPONENTIAL, wcfg)
+            host = y.cpu().numpy()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t1
+            ge.close()
+            if i > 0:  # first call warms the allocator
+                e2e_ms.append(dt * 1e3)
+            assert np.isfinite(host).all()
+        e_ms = sum(e2e_ms)
+        if world > 1:
+            t_ms = torch.tensor([e_ms], dtype=torch.float64, device=g.device)
+            dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+            e_ms = float(t_ms.item())
+        e2e = {"value": em_per_step * len(e2e_ms) / (e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / len(e2e_ms),
+               "nodes_per_s": g.n * len(e2e_ms) / (e_ms / 1e3),
+               "path": "DeviceGraph(host SparseMatrix, gamma) + estimator + y.cpu(): pinned H2D of CSR, D2H of y"}
+
+    # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cb = CpuBaseline(a, beta, n_walks, cfg)
+        em, wall, k = cb.run(args.cpu_seconds)
+        cpu = {"value": em / wall, "unit": "steps/s", "cores": cb.cores, "kind": "port", "sample": cb.describe(k)}
+        cb.close()
+
+    if rank == 0:
+        line = {
+            "metric": "walk-steps/s", "baseline_metric": BASELINE_METRIC, "value": value, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "nodes_per_s": nodes_per_s,
+            "config": {"workload": cfg["workload"], "n": g.n, "nnz": g.nnz, "n_walks": int(n_walks),
+                       "emissions_per_step": em_per_step, "beta": beta, "max_steps": cfg["max_steps"],
+                       "weight_cutoff": cfg["cutoff"], "seed": cfg["seed"], "sampling": "philox (device RNG)",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "parallelism": f"start-column shards x{world}, graph replicated"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="mcfunm", choices=["mcfunm", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_device(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

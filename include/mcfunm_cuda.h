@@ -47,6 +47,8 @@ extern "C" {
 
 /* mcf_walk_params.flags */
 #define MCF_FLAG_NONE 0
+#define MCF_FLAG_TIME_KERNELS 1 /* bracket the walk / Q-build kernels with CUDA events
+                                   (read with mcf_graph_kernel_times) */
 
 typedef struct mcf_graph mcf_graph;
 
@@ -93,6 +95,10 @@ typedef struct {
 
 MCF_API const char *mcf_version(void);
 MCF_API const char *mcf_last_error(void);
+
+/* Cumulative number of kernels this library has launched in the process
+ * (benchmark accounting; no reference counterpart). */
+MCF_API int64_t mcf_kernel_launches(void);
 
 /* Build the device transition tables for `csr` (replaces
  * walker.build_transition_model, walker.py:97-145): per-row |a| sums in CSR
@@ -163,6 +169,12 @@ MCF_API int mcf_replay_diag(mcf_graph *g, const mcf_walk_params *p, const int64_
  * (Eq. 20 final sum), fixed summation order. */
 MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d,
                      int64_t row_begin, int64_t row_end, void *stream);
+
+/* Device time of the kernels launched with MCF_FLAG_TIME_KERNELS since the
+ * last call: the walk kernels (action walks or diag emission walks) and the
+ * diag Q-build/combine kernel, in ms, plus the number of timed walk launches.
+ * Synchronises on the recorded events; clears them. */
+MCF_API int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches);
 
 #ifdef __cplusplus
 }

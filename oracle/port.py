@@ -531,3 +531,42 @@ def cg_solve(a: Csr, gamma: float, b: np.ndarray, tol: float = 1e-10, max_iter: 
 def gershgorin_gamma(a: Csr, fraction: float) -> float:
     """oracle.py:128-136."""
     return fraction / float(np.max(row_abs_sums(a)))
+
+
+# --------------------------------------------------------------------------
+# column-sample drivers for the CPU baseline (bench.py cpu_baseline and
+# --impl reference legs): the same per-column loop as funm_action /
+# funm_diag, restricted to a set of start columns.
+# --------------------------------------------------------------------------
+def action_columns(t: Tables, r: np.ndarray, z: np.ndarray, ni: np.ndarray, cols, max_steps: int,
+                   cutoff: float, seed: int):
+    """q_c for the given columns (dict) and the emissions they made."""
+    out, em = {}, 0
+    for c in cols:
+        acc = [0.0]
+
+        def on_step(k, s, w, ids, acc=acc):
+            acc[0] += z[k + 2] * (w * r[s]).sum()
+        e, _ = batch_walks(t, int(c), int(ni[c]), max_steps, cutoff, column_stream(seed, int(c)), on_step)
+        out[int(c)] = acc[0]
+        em += e
+    return out, em
+
+
+def diag_columns(a: Csr, t: Tables, z: np.ndarray, ni: np.ndarray, cols, max_steps: int, cutoff: float,
+                 seed: int):
+    """Eq. 20 contributions {i: sum} of the given columns and their emissions."""
+    contrib, em = {}, 0
+    qrow = np.zeros(a.n)
+    for c in cols:
+        qrow[:] = 0.0
+
+        def on_step(k, s, w, ids):
+            np.add.at(qrow, s, z[k + 2] * w)
+        e, _ = batch_walks(t, int(c), int(ni[c]), max_steps, cutoff, column_stream(seed, int(c)), on_step)
+        em += e
+        lo, hi = a.csc_ptr[c], a.csc_ptr[c + 1]
+        for i, aic in zip(a.csc_rows[lo:hi], a.csc_vals[lo:hi]):
+            ilo, ihi = a.csc_ptr[i], a.csc_ptr[i + 1]
+            contrib[int(i)] = contrib.get(int(i), 0.0) + aic * (qrow[a.csc_rows[ilo:ihi]] @ a.csc_vals[ilo:ihi])
+    return contrib, em

@@ -15,6 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MCFUNM_CUDA_LIB", os.path.join(_HERE, "lib", "libmcfunm_cuda.so"))
 
 MCF_STATS_LEN = 4
+MCF_FLAG_TIME_KERNELS = 1
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -40,6 +41,8 @@ class McfWalkParams(C.Structure):
 SIGNATURES = {
     "mcf_version": (C.c_char_p, []),
     "mcf_last_error": (C.c_char_p, []),
+    "mcf_kernel_launches": (I64, []),
+    "mcf_graph_kernel_times": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(I64)]),
     "mcf_graph_create": (C.c_int, [C.POINTER(McfCsr), P, C.POINTER(P)]),
     "mcf_graph_destroy": (C.c_int, [P]),
     "mcf_graph_get_info": (C.c_int, [P, C.POINTER(McfGraphInfo)]),

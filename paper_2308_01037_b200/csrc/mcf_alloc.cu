@@ -100,18 +100,24 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(SelectState), s));
     unsigned nb = (unsigned)((n + 255) / 256);
     k_floor<<<nb, 256, 0, s>>>(g->init_prob, n, (double)n_walks, ni, key, st);
+    mcf::note_launch();
     k_select_init<<<1, 1, 0, s>>>(st, n_walks);
+    mcf::note_launch();
     int hb = sm_count() * 4;
     for (int pass = 0; pass < 8; ++pass) {
         int shift = 56 - 8 * pass;
         k_hist<<<hb, 256, 0, s>>>(key, n, shift, st);
+        mcf::note_launch();
         k_pick<<<1, 1, 0, s>>>(shift, st);
+        mcf::note_launch();
     }
     k_tie_flags<<<nb, 256, 0, s>>>(key, n, st, tmp);
+    mcf::note_launch();
     MCF_LAUNCHED("allocate");
     int rc = exclusive_scan_i64(tmp, tmp + n, n, s);
     if (rc) return rc;
     k_final<<<nb, 256, 0, s>>>(key, n, st, tmp + n, ni);
+    mcf::note_launch();
     MCF_LAUNCHED("k_final");
     rc = exclusive_scan_i64(ni, walk_pre, n, s);
     if (rc) return rc;

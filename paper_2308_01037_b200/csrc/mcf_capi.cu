@@ -3,6 +3,7 @@
 
 namespace mcf {
 const char *last_error();
+long long launches();
 }
 
 extern "C" {
@@ -10,5 +11,34 @@ extern "C" {
 const char *mcf_version(void) { return "mcfunm_cuda 0.1.0 (sm_100a)"; }
 
 const char *mcf_last_error(void) { return mcf::last_error(); }
+
+int64_t mcf_kernel_launches(void) { return (int64_t)mcf::launches(); }
+
+static double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, int64_t *count) {
+    double ms = 0.0;
+    for (auto &p : v) {
+        cudaEventSynchronize(p.second);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, p.first, p.second);
+        ms += t;
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    if (count) *count = (int64_t)v.size();
+    v.clear();
+    return ms;
+}
+
+int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches) {
+    if (!g) {
+        mcf::set_error("mcf_graph_kernel_times: null graph");
+        return MCF_ERR_ARGUMENT;
+    }
+    double w = drain(g->ev_walk, walk_launches);
+    double q = drain(g->ev_q, nullptr);
+    if (walk_ms) *walk_ms = w;
+    if (q_ms) *q_ms = q;
+    return MCF_OK;
+}
 
 }  // extern "C"

@@ -230,7 +230,7 @@ static long long emission_budget() {
     return v;
 }
 
-static int run_q(mcf_graph *g, const long long *walk_pre, long long cb, long long ce, long long wb, long long slot_len,
+static int run_q(bool timed, mcf_graph *g, const long long *walk_pre, long long cb, long long ce, long long wb, long long slot_len,
                  const long long *eoff, const long long *walk_off, long long off_base, const int *est, const double *ewt, double *pcol,
                  long long max_slots_per_col, cudaStream_t s) {
     QArgs q;
@@ -269,8 +269,13 @@ static int run_q(mcf_graph *g, const long long *walk_pre, long long cb, long lon
     q.counter = counter;
     size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(double));
     MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int rc = timed_begin(g, timed, g->ev_q, s);
+    if (rc) return rc;
     k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
+    mcf::note_launch();
     MCF_LAUNCHED("k_diag_q");
+    rc = timed_end(timed, g->ev_q, s);
+    if (rc) return rc;
     cudaFreeAsync(counter, s);
     if (gbuf) cudaFreeAsync(gbuf, s);
     return MCF_OK;
@@ -294,6 +299,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     MCF_CUDA(cudaMemsetAsync(err, 0, 16, s));
     long long ncol = ce - cb;
     k_max_walks<<<(unsigned)((ncol + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, maxw);
+    mcf::note_launch();
     MCF_LAUNCHED("k_max_walks");
     unsigned long long hmax = 0;
     MCF_CUDA(cudaMemcpyAsync(&hmax, maxw, sizeof(hmax), cudaMemcpyDeviceToHost, s));
@@ -313,7 +319,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
                               stats, err, s);
         if (rc) return rc;
         // table size is bounded by min(slots, n) per column
-        rc = run_q(g, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
+        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
         if (rc) return rc;
         int herr = 0;
         MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -338,6 +344,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     long long *dbounds = nullptr;
     MCF_CUDA(cudaMallocAsync(&dbounds, sizeof(long long) * (nb + 1), s));
     k_batch_bounds<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, wb, cap_walks, nb, dbounds);
+    mcf::note_launch();
     MCF_LAUNCHED("k_batch_bounds");
     long long *hb = new long long[nb + 1];
     MCF_CUDA(cudaMemcpyAsync(hb, dbounds, sizeof(long long) * (nb + 1), cudaMemcpyDeviceToHost, s));
@@ -358,7 +365,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
             rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, stats,
                                   err, s);
             if (rc) break;
-            rc = run_q(g, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
+            rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
             if (rc) break;
             continue;
         }
@@ -385,7 +392,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, stats,
                               err, s);
         if (rc) break;
-        rc = run_q(g, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
+        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
         cudaFreeAsync(elen, s);
         if (rc) break;
     }
@@ -407,6 +414,7 @@ static int diag_combine(mcf_graph *g, double z0, double z1, const double *pcol, 
     if (rows == 0) return MCF_OK;
     k_diag_final<<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->vals,
                                                                    (const long long *)g->csr2csc, pcol, z0, z1, d, rb, re);
+    mcf::note_launch();
     MCF_LAUNCHED("k_diag_final");
     return MCF_OK;
 }

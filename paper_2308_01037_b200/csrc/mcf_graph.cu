@@ -130,12 +130,49 @@ __device__ double pw_block(const double *a, long long n) {
     return res;
 }
 
+// The recursion of pairwise_sum evaluated with an explicit stack (device
+// recursion is avoided): frame state 0 = descend left, 1 = left done -> descend
+// right, 2 = both done -> combine and pop.  `ret` carries the value of the
+// child that just finished.
 template <bool SQUARE>
-__device__ __noinline__ double pw_sum(const double *a, long long n) {
+__device__ double pw_sum(const double *a, long long n) {
     if (n <= 128) return pw_block<SQUARE>(a, n);
-    long long n2 = n / 2;
-    n2 -= n2 % 8;
-    return __dadd_rn(pw_sum<SQUARE>(a, n2), pw_sum<SQUARE>(a + n2, n - n2));
+    long long off[48], len[48];
+    double left[48];
+    unsigned char st[48];
+    int sp = 0;
+    off[0] = 0;
+    len[0] = n;
+    st[0] = 0;
+    double ret = 0.0;
+    while (sp >= 0) {
+        const long long L = len[sp];
+        if (L <= 128) {
+            ret = pw_block<SQUARE>(a + off[sp], L);
+            --sp;
+            continue;
+        }
+        long long n2 = L / 2;
+        n2 -= n2 % 8;
+        if (st[sp] == 0) {
+            st[sp] = 1;
+            off[sp + 1] = off[sp];
+            len[sp + 1] = n2;
+            st[sp + 1] = 0;
+            ++sp;
+        } else if (st[sp] == 1) {
+            left[sp] = ret;
+            st[sp] = 2;
+            off[sp + 1] = off[sp] + n2;
+            len[sp + 1] = L - n2;
+            st[sp + 1] = 0;
+            ++sp;
+        } else {
+            ret = __dadd_rn(left[sp], ret);
+            --sp;
+        }
+    }
+    return ret;
 }
 
 // ||C_j||_2 exactly as scipy computes csc.multiply(csc).sum(axis=0) then sqrt
@@ -201,6 +238,7 @@ static int numpy_sum(const double *dev, long long n, cudaStream_t s, double *out
     MCF_CUDA(cudaMemcpyAsync(d_lo, lo.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, s));
     MCF_CUDA(cudaMemcpyAsync(d_ln, ln.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s));
     k_leaf_sums<<<(nl + 255) / 256, 256, 0, s>>>(dev, d_lo, d_ln, nl, d_sum);
+    mcf::note_launch();
     MCF_LAUNCHED("k_leaf_sums");
     std::vector<double> h(nl);
     MCF_CUDA(cudaMemcpyAsync(h.data(), d_sum, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
@@ -258,7 +296,9 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     cudaMemsetAsync(cnt, 0, sizeof(BuildCounters), s);
     unsigned nb = (unsigned)((g->n + 255) / 256);
     k_rows<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->vals, g->n, g->hdr, cnt);
+    mcf::note_launch();
     k_colnorm<<<nb, 256, 0, s>>>((const long long *)g->csc_ptr, g->csc_vals, g->n, g->col_norm);
+    mcf::note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "k_rows/k_colnorm"));
     BuildCounters hc;
     cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s);
@@ -275,12 +315,14 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
         if ((e = cudaMalloc(&g->ecol, sizeof(int) * g->nnz)) != cudaSuccess) return fail(cuda_status(e, "ecol"));
         g->ecol_owned = true;
         k_ecol<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>(g->col_ids, g->vals, g->nnz, g->ecol);
+        mcf::note_launch();
     } else {
         g->ecol = const_cast<int32_t *>(g->col_ids);
     }
     if (hc.n_uniform + hc.n_empty < (unsigned long long)g->n) {
         if ((e = cudaMalloc(&g->cdf, sizeof(double) * g->nnz)) != cudaSuccess) return fail(cuda_status(e, "cdf"));
         k_cdf<<<nb, 256, 0, s>>>(g->hdr, g->vals, g->n, g->cdf);
+        mcf::note_launch();
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "k_ecol/k_cdf"));
     double total = 0.0;
@@ -288,6 +330,7 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     if (rc) return fail(rc);
     g->info.col_norm_total = total;
     k_divide<<<nb, 256, 0, s>>>(g->col_norm, total, g->n, g->init_prob);
+    mcf::note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "k_divide"));
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_status(e, "graph build"));
     *out = g;

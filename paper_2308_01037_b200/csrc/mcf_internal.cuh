@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/mcfunm_cuda.h"
 
@@ -17,6 +19,7 @@ namespace mcf {
 
 void set_error(const std::string &msg);
 int cuda_status(cudaError_t e, const char *what);
+void note_launch();  // counts kernel launches (mcf_kernel_launches)
 
 }  // namespace mcf
 
@@ -82,6 +85,8 @@ struct mcf_graph {
     int64_t *csr2csc = nullptr;      // nnz, lazily built for diag
     mcf_graph_info info{};
     int device = 0;
+    // optional per-launch timing of the dominant kernels (MCF_FLAG_TIME_KERNELS)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_walk, ev_q;
 };
 
 namespace mcf {
@@ -178,5 +183,8 @@ int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
 int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end,
                     long long *wb, long long *we, cudaStream_t s);
 int sm_count();
+// event pair around one launch of a timed kernel (no-op unless flag set)
+int timed_begin(mcf_graph *g, bool on, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, cudaStream_t s);
+int timed_end(bool on, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, cudaStream_t s);
 
 }  // namespace mcf

@@ -1,5 +1,6 @@
 // Shared host/device utilities: error state, prefix scans, walk -> column
 // index, coefficient upload, CSR -> CSC entry map.
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -8,6 +9,26 @@
 namespace mcf {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launches() { return g_launches.load(); }
+
+int timed_begin(mcf_graph *, bool on, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, cudaStream_t s) {
+    if (!on) return MCF_OK;
+    cudaEvent_t a, b;
+    MCF_CUDA(cudaEventCreate(&a));
+    MCF_CUDA(cudaEventCreate(&b));
+    MCF_CUDA(cudaEventRecord(a, s));
+    v.emplace_back(a, b);
+    return MCF_OK;
+}
+
+int timed_end(bool on, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, cudaStream_t s) {
+    if (!on || v.empty()) return MCF_OK;
+    MCF_CUDA(cudaEventRecord(v.back().second, s));
+    return MCF_OK;
+}
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 const char *last_error() { return g_last_error.c_str(); }
@@ -108,6 +129,7 @@ int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStr
     long long nb = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (nb == 1) {
         k_tile_scan<<<1, SCAN_T, 0, s>>>(in, n, nullptr, out);
+        mcf::note_launch();
         MCF_LAUNCHED("k_tile_scan");
         return MCF_OK;
     }
@@ -115,10 +137,12 @@ int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStr
     MCF_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (2 * nb + 1), s));
     boff = bsum + nb;
     k_tile_sums<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum);
+    mcf::note_launch();
     MCF_LAUNCHED("k_tile_sums");
     int rc = exclusive_scan_i64(bsum, boff, nb, s);
     if (rc) return rc;
     k_tile_scan<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, boff, out);
+    mcf::note_launch();
     MCF_LAUNCHED("k_tile_scan");
     MCF_CUDA(cudaFreeAsync(bsum, s));
     return MCF_OK;
@@ -146,6 +170,7 @@ int build_blk_col(const long long *walk_pre, long long col_begin, long long col_
     long long nc = col_end - col_begin;
     if (nc > 0 && w > 0) {
         k_blk_col<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(walk_pre, col_begin, col_end, walk_begin, *blk_col);
+        mcf::note_launch();
         MCF_LAUNCHED("k_blk_col");
     }
     *nblk = nb;
@@ -199,6 +224,7 @@ int ensure_csr2csc(mcf_graph *g, cudaStream_t s) {
     k_csr2csc<<<(unsigned)blocks, 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids,
                                                (const long long *)g->csc_ptr, g->csc_rows, g->n,
                                                (long long *)g->csr2csc);
+    mcf::note_launch();
     MCF_LAUNCHED("k_csr2csc");
     return MCF_OK;
 }

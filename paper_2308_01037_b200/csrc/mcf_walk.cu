@@ -322,10 +322,13 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
     const long long *rp = (const long long *)g->row_ptr;
     if (avg <= 8) {
         k_spmv<4><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+        mcf::note_launch();
     } else if (avg <= 32) {
         k_spmv<8><<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+        mcf::note_launch();
     } else {
         k_spmv<32><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+        mcf::note_launch();
     }
     MCF_LAUNCHED("k_spmv");
     return MCF_OK;
@@ -399,20 +402,29 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     a.stats = stats;
     a.walk_off = walk_off;
     a.entries = entries;
+    const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0 && mode != EMIT_COUNT;
+    rc = timed_begin(g, timed, g->ev_walk, s);
+    if (rc) return rc;
     switch (mode) {
         case EMIT_FIXED:
             k_walk_emit<EMIT_FIXED><<<walk_grid(k_walk_emit<EMIT_FIXED>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt);
+            mcf::note_launch();
             break;
         case EMIT_REPLAY:
             k_walk_emit<EMIT_REPLAY><<<walk_grid(k_walk_emit<EMIT_REPLAY>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt);
+            mcf::note_launch();
             break;
         case EMIT_COUNT:
             k_walk_emit<EMIT_COUNT><<<walk_grid(k_walk_emit<EMIT_COUNT>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+            mcf::note_launch();
             break;
         default:
             k_walk_emit<EMIT_EXPLICIT><<<walk_grid(k_walk_emit<EMIT_EXPLICIT>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+            mcf::note_launch();
     }
     MCF_LAUNCHED("k_walk_emit");
+    rc = timed_end(timed, g->ev_walk, s);
+    if (rc) return rc;
     cudaFreeAsync(counter, s);
     cudaFreeAsync(zeta, s);
     cudaFreeAsync(blk, s);
@@ -445,19 +457,28 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     a.walk_off = walk_off;
     a.entries = entries;
     k_set_aux<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, r, g->n);
+    mcf::note_launch();
     MCF_LAUNCHED("k_set_aux");
+    const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0;
     if (nw > 0) {
+        rc = timed_begin(g, timed, g->ev_walk, s);
+        if (rc) return rc;
         if (replay) {
             k_walk_action<true><<<walk_grid(k_walk_action<true>, 256, 0), 256, 0, s>>>(a, xw);
+            mcf::note_launch();
         } else {
             k_walk_action<false><<<walk_grid(k_walk_action<false>, 256, 0), 256, 0, s>>>(a, xw);
+            mcf::note_launch();
         }
         MCF_LAUNCHED("k_walk_action");
+        rc = timed_end(timed, g->ev_walk, s);
+        if (rc) return rc;
     }
     long long ncol = ce - cb;
     if (ncol > 0) {
         long long warps = (ncol + 31) / 32;
         k_col_reduce<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, a.walk_begin, xw, q, qvar);
+        mcf::note_launch();
         MCF_LAUNCHED("k_col_reduce");
     }
     int herr = 0;

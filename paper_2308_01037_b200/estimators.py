@@ -128,8 +128,12 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
     res.aux = {"q": q, "r": r, "ni": ni, "walk_pre": pre}
     if stderr:
         # Var(y_a) = sum_i a_ai^2 Var(q_i): SpMV with squared values
-        a2 = torch.sparse_csr_tensor(g.row_ptr, g.col_ids.to(torch.int64), g.vals * g.vals, (g.n, g.n))
-        res.stderr = torch.sqrt(a2 @ qvar).cpu().numpy()
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            a2 = torch.sparse_csr_tensor(g.row_ptr, g.col_ids.to(torch.int64), g.vals * g.vals, (g.n, g.n),
+                                         check_invariants=False)
+            res.stderr = torch.sqrt(a2 @ qvar).cpu().numpy()
     return res
 
 

@@ -1,0 +1,83 @@
+"""Synthetic benchmark graphs for the BASELINE.json configs (workload
+generation, not the hot path).  All return this package's SparseMatrix with
+symmetric 0/1 values; callers scale by beta = 1 / lambda_max."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+from scipy import sparse
+
+from .errors import ArgumentError
+from .sparsemat import SparseMatrix
+
+_GEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmcfunm_gen.so")
+
+
+def _gen_lib():
+    lib = C.CDLL(_GEN)
+    lib.mcfgen_ba_nnz.restype = C.c_int64
+    lib.mcfgen_ba_nnz.argtypes = [C.c_int64, C.c_int64]
+    lib.mcfgen_barabasi_albert.restype = C.c_int64
+    lib.mcfgen_barabasi_albert.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p]
+    return lib
+
+
+def _alloc(shape, dtype, pinned):
+    if pinned:
+        import torch
+        t = torch.empty(shape, dtype={np.int64: torch.int64, np.int32: torch.int32,
+                                      np.float64: torch.float64}[dtype], pin_memory=True)
+        return t.numpy()
+    return np.empty(shape, dtype=dtype)
+
+
+def barabasi_albert(n: int, m: int, seed: int = 0, pinned: bool = False) -> SparseMatrix:
+    """BASELINE config 2 graph (n = 1e6, m = 4 -> nnz 7,999,968)."""
+    lib = _gen_lib()
+    nnz = lib.mcfgen_ba_nnz(n, m)
+    if nnz < 0:
+        raise ArgumentError("need m >= 1 and n > m + 1")
+    rp = _alloc(n + 1, np.int64, pinned)
+    ci = _alloc(nnz, np.int32, pinned)
+    got = lib.mcfgen_barabasi_albert(n, m, seed, rp.ctypes.data, ci.ctypes.data)
+    assert got == nnz
+    vals = _alloc(nnz, np.float64, pinned)
+    vals[:] = 1.0
+    meta = {"generator": "barabasi-albert", "n": n, "m": m, "seed": seed, "nnz": int(nnz)}
+    return SparseMatrix.from_csr_arrays(n, rp, ci, vals, symmetric_hint=True, meta=meta)
+
+
+def erdos_renyi_lcc(n: int, mean_degree: float, seed: int = 0) -> SparseMatrix:
+    """BASELINE config 1 graph: G(n, m = n d / 2 random pairs), simple,
+    undirected, largest connected component only (ids compacted)."""
+    from scipy.sparse.csgraph import connected_components
+    rng = np.random.default_rng(seed)
+    m = int(n * mean_degree / 2)
+    u, v = rng.integers(0, n, m), rng.integers(0, n, m)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    a = sparse.coo_array((np.ones(2 * u.size), (np.r_[u, v], np.r_[v, u])), shape=(n, n)).tocsr()
+    a.sum_duplicates()
+    a.data[:] = 1.0
+    _, lab = connected_components(a, directed=False)
+    big = np.flatnonzero(lab == np.argmax(np.bincount(lab)))
+    sub = sparse.csr_array(a[big][:, big])
+    sub.sort_indices()
+    out = SparseMatrix.from_csr_arrays(big.size, sub.indptr.astype(np.int64), sub.indices.astype(np.int32),
+                                       sub.data, symmetric_hint=True,
+                                       meta={"generator": "erdos-renyi-lcc", "n0": n, "seed": seed})
+    out.original_ids = big
+    return out
+
+
+def lambda_max(a) -> float:
+    """Largest eigenvalue of a symmetric matrix (ARPACK, deterministic start
+    vector, so every process computes the same fp64 beta)."""
+    from scipy.sparse.linalg import eigsh
+    m = sparse.csr_array(a.csr, dtype=np.float64)
+    if m.shape[0] <= 512:
+        return float(np.linalg.eigvalsh(m.toarray())[-1])
+    return float(eigsh(m, k=1, which="LA", v0=np.ones(m.shape[0]), tol=1e-12)[0][0])
