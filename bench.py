@@ -71,44 +71,65 @@ def measured_peak():
 # clocks during the timed region
 # --------------------------------------------------------------------------
 class Clocks:
+    """nvidia-smi sampler (recipe clocks line); keeps timestamped samples so
+    the ones inside the timed region can be selected."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=50):
+        import threading
+        self.samples = []
         self.proc = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(index)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", str(period_ms), "-i", str(index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except Exception:
-            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 10:  # wait for the sampler to run
+            time.sleep(0.02)
 
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out = ""
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in out.splitlines():
+    def _read(self):
+        for ln in self.proc.stdout:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
+                self.samples.append((time.time(), float(f[0]), float(f[1]), f[3:7]))
             except ValueError:
-                continue
-            for nm, val in zip(names, f[3:7]):
+                pass
+
+    def summary(self, t0, t1):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        inside = [x for x in self.samples if t0 <= x[0] <= t1]
+        note = "samples inside the timed region"
+        if not inside:  # region shorter than the sampling period: nearest samples around it
+            inside = sorted(self.samples, key=lambda x: min(abs(x[0] - t0), abs(x[0] - t1)))[:2]
+            note = "timed region shorter than the sampling period; nearest samples"
+        reasons = set()
+        for x in inside:
+            for nm, val in zip(self.NAMES, x[3]):
                 if val.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(x[1] for x in inside) if inside else None,
+                "sm_max_mhz": max(x[2] for x in inside) if inside else None, "reasons": sorted(reasons),
+                "samples": len(inside), "note": note}
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
 
 
 # --------------------------------------------------------------------------
@@ -239,35 +260,76 @@ def run_device(args, cfg):
             return parallel.sharded_action(g, mc.EXPONENTIAL, v, wcfg, params=params)
         return parallel.sharded_diag(g, mc.EXPONENTIAL, wcfg, params=params)
 
+    clocks = Clocks(local) if rank == 0 else None
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    _native.check(lib.mcf_graph_kernel_times(g.handle, None, None, None))
+    g.kernel_times(reset=True)
+
+    # One estimator pass has no host synchronisation on the action path, so on
+    # one GPU it is captured once as a CUDA graph and replayed per step.
+    params.c.flags = _native.MCF_FLAG_TIME_KERNELS
+    graph = None
+    launches_per_step = None
+    if cfg["kind"] == "action" and world == 1 and not args.no_graph:
+        try:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            g.kernel_times(reset=True)
+            l0 = lib.mcf_kernel_launches()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                static_out = step()
+            launches_per_step = lib.mcf_kernel_launches() - l0
+            graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:  # fall back to eager steps
+            log(f"[bench] CUDA graph capture failed ({exc}); timing eager steps")
+            graph = None
+            torch.cuda.synchronize()
+            g.kernel_times(reset=True)
 
     # ---- device-resident timed region -------------------------------------------------
-    params.c.flags = _native.MCF_FLAG_TIME_KERNELS
-    clocks = Clocks(local) if rank == 0 else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stats = []
+    walk_ms_tot, q_ms_tot, walk_launches = 0.0, 0.0, 0
     launches0 = lib.mcf_kernel_launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    t_wall0 = time.time()
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record()
-        _, st = step()
+        if graph is not None:
+            graph.replay()
+            st = static_out[1].clone()
+        else:
+            _, st = step()
         ev[i][1].record()
         stats.append(st)
+        if graph is not None:  # read this replay's walk-kernel events
+            w_, q_, n_ = g.kernel_times(reset=False)
+            walk_ms_tot += w_
+            q_ms_tot += q_
+            walk_launches += n_
     torch.cuda.synchronize()
+    t_wall1 = time.time()
     if world > 1:
         dist.barrier()
-    launches = lib.mcf_kernel_launches() - launches0
-    clk = clocks.stop() if clocks else None
-    ms = sum(s.elapsed_time(e) for s, e in ev)
-    walk_ms, q_ms, walk_n = _native.C.c_double(), _native.C.c_double(), _native.C.c_int64()
-    _native.check(lib.mcf_graph_kernel_times(g.handle, _native.C.byref(walk_ms), _native.C.byref(q_ms),
-                                             _native.C.byref(walk_n)))
+    launches = (launches_per_step * args.steps if graph is not None
+                else lib.mcf_kernel_launches() - launches0)
+    clk = clocks.summary(t_wall0, t_wall1) if clocks else None
+    if clocks:
+        clocks.stop()
+    ms = sum(s_.elapsed_time(e_) for s_, e_ in ev)
+    w_, q_, n_ = g.kernel_times(reset=True)
+    if graph is None:
+        walk_ms_tot, q_ms_tot, walk_launches = w_, q_, n_
     params.c.flags = 0
     # emissions of the whole job (all ranks) over the timed steps
     em_t = torch.stack([s_[1] for s_ in stats]).sum().to(torch.float64).reshape(1)
@@ -282,7 +344,7 @@ def run_device(args, cfg):
 
     # ---- dominant kernel roofline -------------------------------------------------------
     peak, peak_src = measured_peak()
-    walk_avg_ms = walk_ms.value / max(1, walk_n.value)
+    walk_avg_ms = walk_ms_tot / max(1, walk_launches)
     em_per_walk_launch = em_per_step / world  # this rank's launches process its share
     achieved = BYTES_PER_STEP * em_per_walk_launch / (walk_avg_ms / 1e3) / 1e9 if walk_avg_ms > 0 else None
     traffic = None
@@ -294,11 +356,11 @@ def run_device(args, cfg):
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "bytes_per_step": BYTES_PER_STEP,
-                "kernel_ms_avg": walk_avg_ms, "kernel_share_of_step": (walk_ms.value / ms) if ms else None,
+                "kernel_ms_avg": walk_avg_ms, "kernel_share_of_step": (walk_ms_tot / ms) if ms else None,
                 "note": "algorithmic bytes = 64 B x emissions per launch; config-2 tables (~70 MB touched) fit in "
                         "the 126 MB L2 after the flush, so frac can exceed the HBM roofline"}
     if cfg["kind"] == "diag":
-        roofline["q_kernel_ms"] = q_ms.value / max(1, args.steps)
+        roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
 
     # ---- end to end through the public API (host matrix -> host result) --------------
     e2e = None
@@ -355,6 +417,7 @@ def run_device(args, cfg):
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
                        "parallelism": f"start-column shards x{world}, graph replicated"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "timing": "CUDA-graph replay of one full estimator pass" if graph is not None else "eager steps",
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -373,6 +436,7 @@ def main():
     ap.add_argument("--impl", default="mcfunm", choices=["mcfunm", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

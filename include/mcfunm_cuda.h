@@ -84,7 +84,9 @@ typedef struct {
     int64_t max_steps;       /* hard cap m_max >= 1 */
     double weight_cutoff;    /* W_c in (0,1): walk stops once |W| <= W_c * W0 */
     uint64_t seed;           /* Philox key; stream per (seed, column, walk, step) */
-    const double *zeta;      /* [host] max_steps + 2 coefficients zeta_0.. (series.py:69-80) */
+    const double *zeta;      /* [dev] max_steps + 2 coefficients zeta_0.. (series.py:69-80) */
+    int64_t walk_capacity;   /* upper bound on the walks of the column range (e.g. N_s);
+                                0 = read the exact count (synchronises the stream) */
     int32_t flags;
 } mcf_walk_params;
 
@@ -171,10 +173,13 @@ MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const dou
                      int64_t row_begin, int64_t row_end, void *stream);
 
 /* Device time of the kernels launched with MCF_FLAG_TIME_KERNELS since the
- * last call: the walk kernels (action walks or diag emission walks) and the
+ * last reset: the walk kernels (action walks or diag emission walks) and the
  * diag Q-build/combine kernel, in ms, plus the number of timed walk launches.
- * Synchronises on the recorded events; clears them. */
-MCF_API int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches);
+ * Synchronises on the recorded events.  reset != 0 destroys them; reset == 0
+ * keeps them, so events captured into a CUDA graph can be re-read after every
+ * replay. */
+MCF_API int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches,
+                                   int reset);
 
 #ifdef __cplusplus
 }

@@ -34,7 +34,7 @@ class McfGraphInfo(C.Structure):
 
 class McfWalkParams(C.Structure):
     _fields_ = [("max_steps", I64), ("weight_cutoff", C.c_double), ("seed", C.c_uint64),
-                ("zeta", P), ("flags", C.c_int32)]
+                ("zeta", P), ("walk_capacity", I64), ("flags", C.c_int32)]
 
 
 # name -> (restype, argtypes); exactly the symbols include/mcfunm_cuda.h declares
@@ -42,7 +42,7 @@ SIGNATURES = {
     "mcf_version": (C.c_char_p, []),
     "mcf_last_error": (C.c_char_p, []),
     "mcf_kernel_launches": (I64, []),
-    "mcf_graph_kernel_times": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(I64)]),
+    "mcf_graph_kernel_times": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(I64), C.c_int]),
     "mcf_graph_create": (C.c_int, [C.POINTER(McfCsr), P, C.POINTER(P)]),
     "mcf_graph_destroy": (C.c_int, [P]),
     "mcf_graph_get_info": (C.c_int, [P, C.POINTER(McfGraphInfo)]),

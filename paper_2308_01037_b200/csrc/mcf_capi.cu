@@ -14,28 +14,30 @@ const char *mcf_last_error(void) { return mcf::last_error(); }
 
 int64_t mcf_kernel_launches(void) { return (int64_t)mcf::launches(); }
 
-static double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, int64_t *count) {
+static double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, int64_t *count, bool reset) {
     double ms = 0.0;
     for (auto &p : v) {
         cudaEventSynchronize(p.second);
         float t = 0.f;
         cudaEventElapsedTime(&t, p.first, p.second);
         ms += t;
-        cudaEventDestroy(p.first);
-        cudaEventDestroy(p.second);
+        if (reset) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
     }
     if (count) *count = (int64_t)v.size();
-    v.clear();
+    if (reset) v.clear();
     return ms;
 }
 
-int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches) {
+int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches, int reset) {
     if (!g) {
         mcf::set_error("mcf_graph_kernel_times: null graph");
         return MCF_ERR_ARGUMENT;
     }
-    double w = drain(g->ev_walk, walk_launches);
-    double q = drain(g->ev_q, nullptr);
+    double w = drain(g->ev_walk, walk_launches, reset != 0);
+    double q = drain(g->ev_q, nullptr, reset != 0);
     if (walk_ms) *walk_ms = w;
     if (q_ms) *q_ms = q;
     return MCF_OK;

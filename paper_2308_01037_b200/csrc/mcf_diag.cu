@@ -24,8 +24,9 @@ namespace mcf {
 // implemented in mcf_walk.cu (shares the walk engine with the action path)
 int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce);
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
-                     int mode, const long long *walk_off, const int *entries, long long slot_len, long long off_base,
-                     long long *eaux, int *est, double *ewt, long long *stats, int *err, cudaStream_t s);
+                     long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
+                     long long off_base, long long *eaux, int *est, double *ewt, long long *stats, int *err,
+                     cudaStream_t s);
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
 }  // namespace mcf
@@ -315,7 +316,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         double *ewt = nullptr;
         MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * slots, s));
         MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * slots, s));
-        rc = launch_walk_emit(g, p, walk_pre, cb, ce, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est, ewt,
+        rc = launch_walk_emit(g, p, walk_pre, cb, ce, we - wb, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est, ewt,
                               stats, err, s);
         if (rc) return rc;
         // table size is bounded by min(slots, n) per column
@@ -362,7 +363,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         if (rc) break;
         if (bw1 == bw0) continue;
         if (fixed) {
-            rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, stats,
+            rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, stats,
                                   err, s);
             if (rc) break;
             rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
@@ -374,7 +375,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         long long *elen = nullptr;
         MCF_CUDA(cudaMallocAsync(&elen, sizeof(long long) * (2 * nwb + 1), s));
         long long *eoff = elen + nwb;
-        rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
                               stats, err, s);
         if (rc) break;
         rc = exclusive_scan_i64(elen, eoff, nwb, s);
@@ -389,7 +390,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
             MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * buf_slots, s));
             MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s));
         }
-        rc = launch_walk_emit(g, p, walk_pre, c0, c1, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, stats,
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, stats,
                               err, s);
         if (rc) break;
         rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);

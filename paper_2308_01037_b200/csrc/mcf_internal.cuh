@@ -154,14 +154,14 @@ __device__ __forceinline__ NodeHdr load_hdr(const NodeHdr *h) {
 // column of global walk g: blk_col[g >> WALK_BLK_SHIFT] brackets the search
 constexpr int WALK_BLK_SHIFT = 6;
 
-// g is the global walk index, g_rel = g - walk_begin of the call.
-__device__ __forceinline__ int column_of_walk(long long g, long long g_rel,
+// g is the global walk index, g_rel = g - walk_begin of the call, nw the
+// number of walks in the call's range.
+__device__ __forceinline__ int column_of_walk(long long g, long long g_rel, long long nw,
                                               const long long *__restrict__ walk_pre,
-                                              const int *__restrict__ blk_col, long long nblk,
-                                              int col_last) {
+                                              const int *__restrict__ blk_col, int col_last) {
     long long b = g_rel >> WALK_BLK_SHIFT;
     int lo = __ldg(blk_col + b);
-    int hi = (b + 1 < nblk) ? __ldg(blk_col + b + 1) : col_last;
+    int hi = ((b + 1) << WALK_BLK_SHIFT) < nw ? __ldg(blk_col + b + 1) : col_last;
     // find largest c in [lo, hi] with walk_pre[c] <= g
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
@@ -175,10 +175,8 @@ __device__ __forceinline__ int column_of_walk(long long g, long long g_rel,
 // host helpers implemented in mcf_util.cu
 // ---------------------------------------------------------------------------
 int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s);
-int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end,
-                  long long walk_begin, long long walk_end, int **blk_col, long long *nblk,
-                  cudaStream_t s);
-int upload_zeta(const double *host_zeta, long long count, double **dev, cudaStream_t s);
+int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end, long long capacity,
+                  int **blk_col, cudaStream_t s);
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
 int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end,
                     long long *wb, long long *we, cudaStream_t s);

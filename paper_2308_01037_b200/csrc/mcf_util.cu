@@ -152,28 +152,27 @@ int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStr
 // walk-block -> column index for a column range
 // ---------------------------------------------------------------------------
 __global__ void k_blk_col(const long long *__restrict__ walk_pre, long long col_begin, long long col_end,
-                          long long walk_begin, int *__restrict__ blk_col) {
+                          int *__restrict__ blk_col) {
     long long c = col_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= col_end) return;
+    const long long walk_begin = __ldg(walk_pre + col_begin);
     long long a = walk_pre[c] - walk_begin, b = walk_pre[c + 1] - walk_begin;
     if (b <= a) return;
     const long long B = 1ll << WALK_BLK_SHIFT;
     for (long long blk = (a + B - 1) >> WALK_BLK_SHIFT; blk * B < b; ++blk) blk_col[blk] = (int)c;
 }
 
-int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end, long long walk_begin,
-                  long long walk_end, int **blk_col, long long *nblk, cudaStream_t s) {
-    long long w = walk_end - walk_begin;
-    long long nb = (w + (1ll << WALK_BLK_SHIFT) - 1) >> WALK_BLK_SHIFT;
+int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end, long long capacity,
+                  int **blk_col, cudaStream_t s) {
+    long long nb = (capacity + (1ll << WALK_BLK_SHIFT) - 1) >> WALK_BLK_SHIFT;
     if (nb < 1) nb = 1;
     MCF_CUDA(cudaMallocAsync(blk_col, sizeof(int) * nb, s));
     long long nc = col_end - col_begin;
-    if (nc > 0 && w > 0) {
-        k_blk_col<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(walk_pre, col_begin, col_end, walk_begin, *blk_col);
+    if (nc > 0 && capacity > 0) {
+        k_blk_col<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(walk_pre, col_begin, col_end, *blk_col);
         mcf::note_launch();
         MCF_LAUNCHED("k_blk_col");
     }
-    *nblk = nb;
     return MCF_OK;
 }
 
@@ -185,14 +184,6 @@ int read_walk_range(const long long *walk_pre, long long col_begin, long long co
     MCF_CUDA(cudaStreamSynchronize(s));
     *wb = h[0];
     *we = h[1];
-    return MCF_OK;
-}
-
-int upload_zeta(const double *host_zeta, long long count, double **dev, cudaStream_t s) {
-    MCF_CUDA(cudaMallocAsync(dev, sizeof(double) * count, s));
-    MCF_CUDA(cudaMemcpyAsync(*dev, host_zeta, sizeof(double) * count, cudaMemcpyHostToDevice, s));
-    // host buffer may be freed by the caller right after return
-    MCF_CUDA(cudaStreamSynchronize(s));
     return MCF_OK;
 }
 

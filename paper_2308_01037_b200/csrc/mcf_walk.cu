@@ -27,8 +27,7 @@ struct WalkCommon {
     const double *__restrict__ zeta;
     const long long *__restrict__ walk_pre;
     const int *__restrict__ blk_col;
-    long long nblk;
-    long long walk_begin, walk_end;
+    long long col_begin, col_end;  // walk range = [walk_pre[col_begin], walk_pre[col_end]), read on the device
     int col_last;
     long long max_steps;
     double cutoff;
@@ -87,7 +86,7 @@ struct Lane {
 
 // Warp-aggregated refill of lanes that finished their walk.
 template <bool REPLAY>
-__device__ __forceinline__ bool refill(const WalkCommon &a, Lane &L, long long &n_walks) {
+__device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long long we, Lane &L, long long &n_walks) {
     unsigned need = __ballot_sync(MCF_FULL, L.g == -1);
     if (need) {
         int lane = threadIdx.x & 31;
@@ -97,9 +96,9 @@ __device__ __forceinline__ bool refill(const WalkCommon &a, Lane &L, long long &
         base = __shfl_sync(MCF_FULL, base, leader);
         if (L.g == -1) {
             long long rel = (long long)base + __popc(need & lanemask_lt());
-            long long g = a.walk_begin + rel;
-            if (g < a.walk_end) {
-                int c = column_of_walk(g, rel, a.walk_pre, a.blk_col, a.nblk, a.col_last);
+            long long g = wb + rel;
+            if (g < we) {
+                int c = column_of_walk(g, rel, we - wb, a.walk_pre, a.blk_col, a.col_last);
                 long long pre = __ldg(a.walk_pre + c);
                 long long nc = __ldg(a.walk_pre + c + 1) - pre;
                 L.g = g;
@@ -157,11 +156,12 @@ __device__ __forceinline__ bool advance(const WalkCommon &a, Lane &L, const Node
 
 template <bool REPLAY>
 __global__ void __launch_bounds__(256) k_walk_action(WalkCommon a, double *__restrict__ xw) {
+    const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
     Lane L;
     L.g = -1;
     double x = 0.0;
     long long n_walks = 0, em = 0, tr = 0, ab = 0;
-    while (refill<REPLAY>(a, L, n_walks)) {
+    while (refill<REPLAY>(a, wb, we, L, n_walks)) {
         if (L.g < 0) continue;
         if (L.k == 0) x = 0.0;
         NodeHdr h = load_hdr(a.hdr + L.state);
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) k_walk_action(WalkCommon a, double *__res
         ++em;
         if (advance<REPLAY>(a, L, h, tr, ab)) {
             if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
-            xw[L.g - a.walk_begin] = x;
+            xw[L.g - wb] = x;
             L.g = -1;
         }
     }
@@ -191,13 +191,14 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
                                                    long long *__restrict__ eaux, int *__restrict__ est,
                                                    double *__restrict__ ewt) {
     constexpr bool REPLAY = MODE == EMIT_REPLAY;
+    const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
     Lane L;
     L.g = -1;
     long long n_walks = 0, em = 0, tr = 0, ab = 0;
     long long sb = 0, scap = 0;
-    while (refill<REPLAY>(a, L, n_walks)) {
+    while (refill<REPLAY>(a, wb, we, L, n_walks)) {
         if (L.g < 0) continue;
-        const long long rel = L.g - a.walk_begin;
+        const long long rel = L.g - wb;
         if (L.k == 0) {
             if (MODE == EMIT_REPLAY) {
                 sb = L.epos - off_base + rel;
@@ -241,8 +242,8 @@ __global__ void k_set_aux(NodeHdr *__restrict__ hdr, const double *__restrict__ 
 constexpr int SMALL_COL = 32;
 
 __global__ void k_col_reduce(const long long *__restrict__ walk_pre, long long col_begin, long long col_end,
-                             long long walk_begin, const double *__restrict__ xw, double *__restrict__ q,
-                             double *__restrict__ qvar) {
+                             const double *__restrict__ xw, double *__restrict__ q, double *__restrict__ qvar) {
+    const long long walk_begin = __ldg(walk_pre + col_begin);
     long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     long long c = col_begin + wid * 32 + lane;
@@ -349,25 +350,22 @@ int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *
     return MCF_OK;
 }
 
+// Kernel arguments for a column range.  No host synchronisation: the walk
+// range is read by the kernels from walk_pre, buffers are sized by the
+// caller's upper bound `capacity` (so the whole call can be captured in a
+// CUDA graph).
 int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
-                 WalkCommon &a, double **zeta_dev, int **blk, cudaStream_t s) {
-    long long wb = 0, we = 0;
-    int rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
-    if (rc) return rc;
-    rc = upload_zeta(p->zeta, p->max_steps + 2, zeta_dev, s);
-    if (rc) return rc;
-    long long nblk = 0;
-    rc = build_blk_col(walk_pre, cb, ce, wb, we, blk, &nblk, s);
+                 long long capacity, WalkCommon &a, int **blk, cudaStream_t s) {
+    int rc = build_blk_col(walk_pre, cb, ce, capacity, blk, s);
     if (rc) return rc;
     a.hdr = g->hdr;
     a.ecol = g->ecol;
     a.cdf = g->cdf;
-    a.zeta = *zeta_dev;
+    a.zeta = p->zeta;
     a.walk_pre = walk_pre;
     a.blk_col = *blk;
-    a.nblk = nblk;
-    a.walk_begin = wb;
-    a.walk_end = we;
+    a.col_begin = cb;
+    a.col_end = ce;
     a.col_last = (int)(ce > cb ? ce - 1 : cb);
     a.max_steps = p->max_steps;
     a.cutoff = p->weight_cutoff;
@@ -376,6 +374,19 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.walk_off = nullptr;
     a.entries = nullptr;
     return MCF_OK;
+}
+
+// Upper bound on the walks of [cb, ce): the caller's hint, else read (sync).
+int walk_capacity(const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce, long long *cap,
+                  cudaStream_t s) {
+    if (p->walk_capacity > 0) {
+        *cap = p->walk_capacity;
+        return MCF_OK;
+    }
+    long long wb = 0, we = 0;
+    int rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
+    *cap = we - wb;
+    return rc;
 }
 
 template <typename K>
@@ -387,12 +398,12 @@ int walk_grid(K kernel, int threads, size_t smem) {
 }
 
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
-                     int mode, const long long *walk_off, const int *entries, long long slot_len, long long off_base,
-                     long long *eaux, int *est, double *ewt, long long *stats, int *err, cudaStream_t s) {
+                     long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
+                     long long off_base, long long *eaux, int *est, double *ewt, long long *stats, int *err,
+                     cudaStream_t s) {
     WalkCommon a;
-    double *zeta = nullptr;
     int *blk = nullptr;
-    int rc = setup_common(g, p, walk_pre, cb, ce, a, &zeta, &blk, s);
+    int rc = setup_common(g, p, walk_pre, cb, ce, nwalks, a, &blk, s);
     if (rc) return rc;
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
@@ -426,7 +437,6 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     rc = timed_end(timed, g->ev_walk, s);
     if (rc) return rc;
     cudaFreeAsync(counter, s);
-    cudaFreeAsync(zeta, s);
     cudaFreeAsync(blk, s);
     return MCF_OK;
 }
@@ -439,11 +449,12 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     MCF_ARG(r && q && stats, "action walk: null r/q/stats");
     if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
     WalkCommon a;
-    double *zeta = nullptr;
     int *blk = nullptr;
-    rc = setup_common(g, p, walk_pre, cb, ce, a, &zeta, &blk, s);
+    long long nw = 0;
+    rc = walk_capacity(p, walk_pre, cb, ce, &nw, s);
     if (rc) return rc;
-    long long nw = a.walk_end - a.walk_begin;
+    rc = setup_common(g, p, walk_pre, cb, ce, nw, a, &blk, s);
+    if (rc) return rc;
     double *xw = nullptr;
     unsigned long long *counter = nullptr;
     int *err = nullptr;
@@ -477,7 +488,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     long long ncol = ce - cb;
     if (ncol > 0) {
         long long warps = (ncol + 31) / 32;
-        k_col_reduce<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, a.walk_begin, xw, q, qvar);
+        k_col_reduce<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, xw, q, qvar);
         mcf::note_launch();
         MCF_LAUNCHED("k_col_reduce");
     }
@@ -488,7 +499,6 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     }
     cudaFreeAsync(xw, s);
     cudaFreeAsync(counter, s);
-    cudaFreeAsync(zeta, s);
     cudaFreeAsync(blk, s);
     if (herr) {
         set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) +

@@ -27,20 +27,35 @@ def require_cuda(device=None) -> torch.device:
     return dev
 
 
+def _same_storage(csr, csc) -> bool:
+    """CSC arrays of a symmetric matrix that are (or equal) the CSR arrays."""
+    if csc.indptr is csr.indptr and csc.indices is csr.indices and csc.data is csr.data:
+        return True
+    return (csc.indptr.shape == csr.indptr.shape and csc.indices.shape == csr.indices.shape
+            and np.array_equal(csc.indptr, csr.indptr) and np.array_equal(csc.indices, csr.indices)
+            and np.array_equal(csc.data, csr.data))
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
 class WalkParams:
-    """mcf_walk_params for one call; keeps the zeta table alive."""
+    """mcf_walk_params for one configuration; owns the device zeta table.
 
-    def __init__(self, config, zeta: np.ndarray):
-        self.zeta = np.ascontiguousarray(zeta, dtype=np.float64)
-        if self.zeta.size < config.max_steps + 2:
+    walk_capacity = N_s bounds the walks of any column range, which lets the
+    library size its buffers without reading the budgets back (no host sync:
+    a whole estimator pass can be captured in a CUDA graph)."""
+
+    def __init__(self, config, zeta: np.ndarray, device=None):
+        z = np.ascontiguousarray(zeta, dtype=np.float64)
+        if z.size < config.max_steps + 2:
             raise ArgumentError("zeta table shorter than max_steps + 2")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.zeta = torch.from_numpy(z).to(dev)
         self.c = N.McfWalkParams(int(config.max_steps), float(config.weight_cutoff),
-                                 int(config.seed) & 0xFFFFFFFFFFFFFFFF,
-                                 self.zeta.ctypes.data_as(C.c_void_p), 0)
+                                 int(config.seed) & 0xFFFFFFFFFFFFFFFF, self.zeta.data_ptr(),
+                                 int(config.n_walks), 0)
 
 
 class DeviceGraph:
@@ -68,9 +83,7 @@ class DeviceGraph:
         self.row_ptr = torch.from_numpy(np.ascontiguousarray(csr.indptr, dtype=np.int64)).to(dev)
         self.col_ids = torch.from_numpy(np.ascontiguousarray(csr.indices, dtype=np.int32)).to(dev)
         self.vals = torch.from_numpy(np.ascontiguousarray(csr.data, dtype=np.float64)).to(dev)
-        same = (self.symmetric_hint and csc.indptr.shape == csr.indptr.shape
-                and (csc is csr or (np.array_equal(csc.indptr, csr.indptr) and np.array_equal(csc.indices, csr.indices)
-                                    and np.array_equal(csc.data, csr.data))))
+        same = self.symmetric_hint and _same_storage(csr, csc)
         if same:
             self.csc_ptr, self.csc_rows, self.csc_vals = self.row_ptr, self.col_ids, self.vals
         else:
@@ -155,6 +168,14 @@ class DeviceGraph:
 
     def _f64(self, n=None):
         return torch.empty(self.n if n is None else n, dtype=torch.float64, device=self.device)
+
+    def kernel_times(self, reset: bool = True):
+        """(walk-kernel ms, Q-kernel ms, timed walk launches) recorded with
+        MCF_FLAG_TIME_KERNELS; reset=False keeps the events (CUDA-graph replays)."""
+        w, q, k = C.c_double(), C.c_double(), C.c_int64()
+        N.check(N.lib().mcf_graph_kernel_times(self.handle, C.byref(w), C.byref(q), C.byref(k), int(reset)),
+                "mcf_graph_kernel_times")
+        return w.value, q.value, k.value
 
     def new_stats(self):
         return torch.zeros(N.MCF_STATS_LEN, dtype=torch.int64, device=self.device)

@@ -111,7 +111,7 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
         return FunmResult(vals, "action", config=_cfg_echo(cfg, coeffs, mode))
     g = _graph(a, device)
     vd = v.to(g.device, torch.float64) if isinstance(v, torch.Tensor) else torch.from_numpy(v_np).to(g.device)
-    params = WalkParams(cfg, z)
+    params = WalkParams(cfg, z, g.device)
     ni, pre = _budgets(g, cfg, replay, budgets)
     r = g.spmv(vd)                       # r = A v
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
@@ -150,7 +150,7 @@ def rand_funm_diag(a, coeffs, config, *, replay=None, budgets=None, device=None,
     if nnz == 0:  # A = 0 -> d = zeta_0 exactly
         return FunmResult(np.full(n, z[0]), "diag", config=_cfg_echo(cfg, coeffs, mode))
     g = _graph(a, device)
-    params = WalkParams(cfg, z)
+    params = WalkParams(cfg, z, g.device)
     ni, pre = _budgets(g, cfg, replay, budgets)
     pcol = torch.zeros(g.nnz, dtype=torch.float64, device=g.device)
     st = g.new_stats()

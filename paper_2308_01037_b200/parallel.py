@@ -65,7 +65,7 @@ def sharded_action(g: DeviceGraph, coeffs, v: torch.Tensor, config, *, params=No
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
     z = coeffs.prefix(cfg.max_steps + 2)
-    params = params or WalkParams(cfg, z)
+    params = params or WalkParams(cfg, z, g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     cols = column_shards(pre, size)[rank] if size > 1 else (0, g.n)
     rows = row_shards(g.n, size)[rank] if size > 1 else (0, g.n)
@@ -86,7 +86,7 @@ def sharded_diag(g: DeviceGraph, coeffs, config, *, params=None, budgets=None, g
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
     z = coeffs.prefix(cfg.max_steps + 2)
-    params = params or WalkParams(cfg, z)
+    params = params or WalkParams(cfg, z, g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     cols = column_shards(pre, size)[rank] if size > 1 else (0, g.n)
     rows = row_shards(g.n, size)[rank] if size > 1 else (0, g.n)

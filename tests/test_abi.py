@@ -43,4 +43,5 @@ def test_struct_layouts():
     # offsets must match the C structs in include/mcfunm_cuda.h
     assert ctypes.sizeof(_native.McfCsr) == 8 * 8
     assert ctypes.sizeof(_native.McfGraphInfo) == 8 * 8
-    assert _native.McfWalkParams.zeta.offset == 24 and ctypes.sizeof(_native.McfWalkParams) == 40
+    assert _native.McfWalkParams.zeta.offset == 24 and _native.McfWalkParams.flags.offset == 40
+    assert ctypes.sizeof(_native.McfWalkParams) == 48

@@ -178,7 +178,7 @@ def test_determinism_and_partition_invariance(mc):
     cfg = mc.WalkConfig(50_000, 1e-300, 23, 9)
     from paper_2308_01037_b200.device import WalkParams
     z = mc.EXPONENTIAL.prefix(cfg.max_steps + 2)
-    p = WalkParams(cfg, z)
+    p = WalkParams(cfg, z, g.device)
     ni, pre = g.allocate(cfg.n_walks)
     r = g.spmv(torch.ones(g.n, dtype=torch.float64, device=g.device))
     outs = []
