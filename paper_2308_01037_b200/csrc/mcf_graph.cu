@@ -137,9 +137,9 @@ __device__ double pw_block(const double *a, long long n) {
 template <bool SQUARE>
 __device__ double pw_sum(const double *a, long long n) {
     if (n <= 128) return pw_block<SQUARE>(a, n);
-    long long off[48], len[48];
-    double left[48];
-    unsigned char st[48];
+    long long off[28], len[28];  // depth <= 25 for n < 2^31
+    double left[28];
+    unsigned char st[28];
     int sp = 0;
     off[0] = 0;
     len[0] = n;
