@@ -14,12 +14,16 @@ const char *mcf_last_error(void) { return mcf::last_error(); }
 
 int64_t mcf_kernel_launches(void) { return (int64_t)mcf::launches(); }
 
-static double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, int64_t *count, bool reset) {
+static double drain(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, int64_t *count, bool reset, int *rc) {
     double ms = 0.0;
     for (auto &p : v) {
-        cudaEventSynchronize(p.second);
         float t = 0.f;
-        cudaEventElapsedTime(&t, p.first, p.second);
+        cudaError_t e = cudaEventSynchronize(p.second);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, p.first, p.second);
+        if (e != cudaSuccess) {
+            *rc = mcf::cuda_status(e, "kernel timing events");
+            cudaGetLastError();  // do not leave the error for later calls
+        }
         ms += t;
         if (reset) {
             cudaEventDestroy(p.first);
@@ -36,11 +40,12 @@ int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t 
         mcf::set_error("mcf_graph_kernel_times: null graph");
         return MCF_ERR_ARGUMENT;
     }
-    double w = drain(g->ev_walk, walk_launches, reset != 0);
-    double q = drain(g->ev_q, nullptr, reset != 0);
+    int rc = MCF_OK;
+    double w = drain(g->ev_walk, walk_launches, reset != 0, &rc);
+    double q = drain(g->ev_q, nullptr, reset != 0, &rc);
     if (walk_ms) *walk_ms = w;
     if (q_ms) *q_ms = q;
-    return MCF_OK;
+    return rc;
 }
 
 }  // extern "C"

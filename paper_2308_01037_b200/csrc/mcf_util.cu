@@ -14,19 +14,29 @@ static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 long long launches() { return g_launches.load(); }
 
+// Inside stream capture a plain cudaEventRecord only expresses a dependency;
+// an external record makes the event a node that fires on every graph replay.
+static cudaError_t record_event(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t err = cudaStreamIsCapturing(s, &cs);
+    if (err != cudaSuccess) return err;
+    if (cs == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    return cudaEventRecord(e, s);
+}
+
 int timed_begin(mcf_graph *, bool on, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, cudaStream_t s) {
     if (!on) return MCF_OK;
     cudaEvent_t a, b;
     MCF_CUDA(cudaEventCreate(&a));
     MCF_CUDA(cudaEventCreate(&b));
-    MCF_CUDA(cudaEventRecord(a, s));
+    MCF_CUDA(record_event(a, s));
     v.emplace_back(a, b);
     return MCF_OK;
 }
 
 int timed_end(bool on, std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, cudaStream_t s) {
     if (!on || v.empty()) return MCF_OK;
-    MCF_CUDA(cudaEventRecord(v.back().second, s));
+    MCF_CUDA(record_event(v.back().second, s));
     return MCF_OK;
 }
 
