@@ -14,11 +14,15 @@ struct SelectState {
     unsigned long long prefix, mask;
     long long k;     // still to select inside the current prefix bucket
     long long left;  // residue R
-    unsigned long long hist[256];
+    unsigned int done;
+    unsigned int hist[256];
 };
 
-__global__ void k_floor(const double *__restrict__ p, long long n, double total, long long *__restrict__ ni,
-                        unsigned long long *__restrict__ key, SelectState *st) {
+// floor(p N), remainder keys, sum of floors; the last block to finish also
+// initialises the selection (residue R = N - sum floor).
+__global__ void k_floor(const double *__restrict__ p, long long n, double total, long long n_walks,
+                        long long *__restrict__ ni, unsigned long long *__restrict__ key, SelectState *st) {
+    __shared__ bool last;
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long got = 0;
     if (i < n) {
@@ -31,51 +35,68 @@ __global__ void k_floor(const double *__restrict__ p, long long n, double total,
     }
     got = warp_sum_ll(got);
     if ((threadIdx.x & 31) == 0 && got) atomicAdd(&st->total_floor, (unsigned long long)got);
-}
-
-__global__ void k_select_init(SelectState *st, long long n_walks) {
-    st->left = n_walks - (long long)st->total_floor;
-    st->k = st->left;
-    st->prefix = 0;
-    st->mask = 0;
-    for (int b = 0; b < 256; ++b) st->hist[b] = 0;
-}
-
-__global__ void k_hist(const unsigned long long *__restrict__ key, long long n, int shift, SelectState *st) {
-    __shared__ unsigned int h[256];
-    if (st->k <= 0) return;
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+    __threadfence();
     __syncthreads();
-    unsigned long long pre = st->prefix, msk = st->mask;
+    if (threadIdx.x == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        st->left = n_walks - (long long)atomicAdd(&st->total_floor, 0ull);
+        st->k = st->left;
+        st->prefix = 0;
+        st->mask = 0;
+        st->done = 0;
+    }
+}
+
+// One radix-select pass: histogram of the 8-bit digit at `shift` over keys
+// that match the current prefix; the last block picks the bucket holding the
+// k-th largest key (parallel suffix scan over the 256 bins).
+__global__ void __launch_bounds__(256) k_select_pass(const unsigned long long *__restrict__ key, long long n,
+                                                     int shift, SelectState *st) {
+    __shared__ unsigned int h[256];
+    __shared__ bool last;
+    if (st->k <= 0) return;  // uniform across the grid
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long pre = st->prefix, msk = st->mask;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         unsigned long long k = key[i];
         if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255u], 1u);
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < 256; b += blockDim.x)
-        if (h[b]) atomicAdd(&st->hist[b], (unsigned long long)h[b]);
-}
-
-__global__ void k_pick(int shift, SelectState *st) {
-    if (st->k <= 0) return;
-    long long k = st->k;
-    for (int b = 255; b >= 0; --b) {
-        long long c = (long long)st->hist[b];
-        if (k <= c) {
-            st->prefix |= (unsigned long long)b << shift;
-            st->mask |= 255ull << shift;
-            break;
-        }
-        k -= c;
+    if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // thread t looks at bin 255 - t: inclusive scan of counts from the top
+    const int b = 255 - threadIdx.x;
+    const long long c = (long long)atomicAdd(&st->hist[b], 0u);
+    __shared__ long long wsum[8];
+    long long x = c;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(MCF_FULL, x, o);
+        if (lane >= o) x += y;
     }
-    st->k = k;
-    for (int b = 0; b < 256; ++b) st->hist[b] = 0;
-}
-
-__global__ void k_tie_flags(const unsigned long long *__restrict__ key, long long n, const SelectState *st,
-                            long long *__restrict__ flag) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = (st->left > 0 && key[i] == st->prefix) ? 1 : 0;
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    long long before = 0;
+    for (int j = 0; j < w; ++j) before += wsum[j];
+    const long long incl = before + x;
+    const long long k = st->k;
+    __syncthreads();
+    if (incl - c < k && k <= incl) {
+        st->prefix = pre | ((unsigned long long)b << shift);
+        st->mask = msk | (255ull << shift);
+        st->k = k - (incl - c);
+    }
+    st->hist[b] = 0;
+    if (threadIdx.x == 0) st->done = 0;
 }
 
 __global__ void k_final(const unsigned long long *__restrict__ key, long long n, const SelectState *st,
@@ -93,37 +114,33 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     long long n = g->n;
     SelectState *st = nullptr;
     unsigned long long *key = nullptr;
-    long long *tmp = nullptr;
+    long long *rank = nullptr;
     MCF_CUDA(cudaMallocAsync(&st, sizeof(SelectState), s));
     MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * n, s));
-    MCF_CUDA(cudaMallocAsync(&tmp, sizeof(long long) * (2 * n + 1), s));
+    MCF_CUDA(cudaMallocAsync(&rank, sizeof(long long) * (n + 1), s));
     MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(SelectState), s));
     unsigned nb = (unsigned)((n + 255) / 256);
-    k_floor<<<nb, 256, 0, s>>>(g->init_prob, n, (double)n_walks, ni, key, st);
+    k_floor<<<nb, 256, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, ni, key, st);
     mcf::note_launch();
-    k_select_init<<<1, 1, 0, s>>>(st, n_walks);
-    mcf::note_launch();
-    int hb = sm_count() * 4;
+    long long want_blocks = (n + 2047) / 2048;
+    int hb = (int)(want_blocks < sm_count() * 2 ? (want_blocks > 0 ? want_blocks : 1) : sm_count() * 2);
     for (int pass = 0; pass < 8; ++pass) {
-        int shift = 56 - 8 * pass;
-        k_hist<<<hb, 256, 0, s>>>(key, n, shift, st);
-        mcf::note_launch();
-        k_pick<<<1, 1, 0, s>>>(shift, st);
+        k_select_pass<<<hb, 256, 0, s>>>(key, n, 56 - 8 * pass, st);
         mcf::note_launch();
     }
-    k_tie_flags<<<nb, 256, 0, s>>>(key, n, st, tmp);
-    mcf::note_launch();
     MCF_LAUNCHED("allocate");
-    int rc = exclusive_scan_i64(tmp, tmp + n, n, s);
+    // rank of each tied key among the ties (index order) = the stable argsort tie-break
+    ScanSrc ties{nullptr, key, &st->prefix};
+    int rc = scan_src(ties, rank, n, s);
     if (rc) return rc;
-    k_final<<<nb, 256, 0, s>>>(key, n, st, tmp + n, ni);
+    k_final<<<nb, 256, 0, s>>>(key, n, st, rank, ni);
     mcf::note_launch();
     MCF_LAUNCHED("k_final");
     rc = exclusive_scan_i64(ni, walk_pre, n, s);
     if (rc) return rc;
     MCF_CUDA(cudaFreeAsync(st, s));
     MCF_CUDA(cudaFreeAsync(key, s));
-    MCF_CUDA(cudaFreeAsync(tmp, s));
+    MCF_CUDA(cudaFreeAsync(rank, s));
     return MCF_OK;
 }
 

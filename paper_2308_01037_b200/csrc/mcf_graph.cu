@@ -76,6 +76,13 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
     }
 }
 
+// Rows longer than LONG_ROW, compacted (order irrelevant: each is reduced alone).
+__global__ void k_long_rows(const long long *__restrict__ row_ptr, long long n, int *__restrict__ out,
+                            unsigned long long *count) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && row_ptr[i + 1] - row_ptr[i] > LONG_ROW) out[atomicAdd(count, 1ull)] = (int)i;
+}
+
 // Packed column ids with the sign of a in bit 31 (only built if some a < 0).
 __global__ void k_ecol(const int *__restrict__ col_ids, const double *__restrict__ vals, long long nnz,
                        int *__restrict__ ecol) {
@@ -259,6 +266,7 @@ static void release(mcf_graph *g) {
     cudaFree(g->col_norm);
     cudaFree(g->init_prob);
     cudaFree(g->csr2csc);
+    cudaFree(g->long_rows);
     delete g;
 }
 
@@ -311,6 +319,24 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     g->info.n_negative = (int64_t)hc.n_negative;
     g->info.max_degree = (int64_t)hc.max_degree;
     memcpy(&g->info.max_row_abs_sum, &hc.max_rsum_bits, sizeof(double));
+    if (hc.max_degree > (unsigned long long)LONG_ROW) {  // hub rows get their own SpMV bin
+        unsigned long long *lc = nullptr, nl = 0;
+        if ((e = cudaMalloc(&lc, sizeof(unsigned long long))) != cudaSuccess) return fail(cuda_status(e, "long"));
+        cudaMemsetAsync(lc, 0, sizeof(unsigned long long), s);
+        int *tmp = nullptr;
+        if ((e = cudaMalloc(&tmp, sizeof(int) * g->n)) != cudaSuccess) return fail(cuda_status(e, "long rows"));
+        k_long_rows<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->n, tmp, lc);
+        mcf::note_launch();
+        cudaMemcpyAsync(&nl, lc, sizeof(nl), cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_status(e, "long rows"));
+        g->n_long_rows = (long long)nl;
+        if ((e = cudaMalloc(&g->long_rows, sizeof(int) * (nl ? nl : 1))) != cudaSuccess)
+            return fail(cuda_status(e, "long rows"));
+        cudaMemcpyAsync(g->long_rows, tmp, sizeof(int) * nl, cudaMemcpyDeviceToDevice, s);
+        cudaStreamSynchronize(s);
+        cudaFree(tmp);
+        cudaFree(lc);
+    }
     if (hc.n_negative) {
         if ((e = cudaMalloc(&g->ecol, sizeof(int) * g->nnz)) != cudaSuccess) return fail(cuda_status(e, "ecol"));
         g->ecol_owned = true;

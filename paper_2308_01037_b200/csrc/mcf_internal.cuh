@@ -83,6 +83,8 @@ struct mcf_graph {
     double *col_norm = nullptr;      // n
     double *init_prob = nullptr;     // n
     int64_t *csr2csc = nullptr;      // nnz, lazily built for diag
+    int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
+    long long n_long_rows = 0;
     mcf_graph_info info{};
     int device = 0;
     // optional per-launch timing of the dominant kernels (MCF_FLAG_TIME_KERNELS)
@@ -151,6 +153,9 @@ __device__ __forceinline__ NodeHdr load_hdr(const NodeHdr *h) {
     return r;
 }
 
+// rows longer than this get a CTA each in SpMV (load balance on hub rows)
+constexpr int LONG_ROW = 64;
+
 // column of global walk g: blk_col[g >> WALK_BLK_SHIFT] brackets the search
 constexpr int WALK_BLK_SHIFT = 6;
 
@@ -175,6 +180,13 @@ __device__ __forceinline__ int column_of_walk(long long g, long long g_rel, long
 // host helpers implemented in mcf_util.cu
 // ---------------------------------------------------------------------------
 int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s);
+// single-pass scan over a device functor: out[i] = sum_{j<i} f(j), out[n] = total
+struct ScanSrc {
+    const long long *in;                       // plain input, or
+    const unsigned long long *key;             // key[j] == *match ? 1 : 0
+    const unsigned long long *match;
+};
+int scan_src(ScanSrc src, long long *out, long long n, cudaStream_t s);
 int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end, long long capacity,
                   int **blk_col, cudaStream_t s);
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);

@@ -64,11 +64,14 @@ int sm_count() {
 }
 
 // ---------------------------------------------------------------------------
-// exclusive scan of int64: out[0..n] (out[n] = total); reduce-then-scan
+// exclusive scan of int64, single pass (decoupled look-back):
+// out[0..n] with out[n] = total.  Tiles take ids from a counter so every
+// predecessor a tile waits on has already started.
 // ---------------------------------------------------------------------------
 constexpr int SCAN_T = 512;
 constexpr int SCAN_I = 8;
 constexpr int SCAN_TILE = SCAN_T * SCAN_I;
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
 
 __device__ __forceinline__ long long block_excl_scan(long long v, long long *total) {
     __shared__ long long warp_tot[SCAN_T / 32];
@@ -97,65 +100,77 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long *tot
     return before;
 }
 
-__global__ void k_tile_sums(const long long *__restrict__ in, long long n, long long *__restrict__ bsum) {
-    long long base = (long long)blockIdx.x * SCAN_TILE;
-    long long s = 0;
-    for (int i = threadIdx.x; i < SCAN_TILE; i += SCAN_T) {
-        long long j = base + i;
-        if (j < n) s += in[j];
-    }
-    long long tot;
-    block_excl_scan(s, &tot);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+__device__ __forceinline__ long long scan_item(const ScanSrc &src, long long j) {
+    if (src.in) return src.in[j];
+    return src.key[j] == *src.match ? 1 : 0;
 }
 
-__global__ void k_tile_scan(const long long *__restrict__ in, long long n, const long long *__restrict__ boff,
-                            long long *__restrict__ out) {
-    long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_I;
+__global__ void __launch_bounds__(SCAN_T) k_scan(ScanSrc src, long long n, long long *__restrict__ out,
+                                                 unsigned long long *status, unsigned int *tile_ctr) {
+    __shared__ unsigned int s_tile;
+    __shared__ long long s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const long long tile = s_tile;
+    const long long base = tile * SCAN_TILE + (long long)threadIdx.x * SCAN_I;
     long long v[SCAN_I];
-    long long s = 0;
+    long long sum = 0;
 #pragma unroll
     for (int i = 0; i < SCAN_I; ++i) {
         long long j = base + i;
-        v[i] = (j < n) ? in[j] : 0;
-        s += v[i];
+        v[i] = (j < n) ? scan_item(src, j) : 0;
+        sum += v[i];
     }
-    long long tot;
-    long long run = block_excl_scan(s, &tot) + (boff ? boff[blockIdx.x] : 0);
+    long long agg;
+    long long local = block_excl_scan(sum, &agg);
+    if (threadIdx.x == 0) {
+        long long prefix = 0;
+        if (tile == 0) {
+            atomicExch(&status[0], ST_PRE | (unsigned long long)agg);
+        } else {
+            atomicExch(&status[tile], ST_AGG | (unsigned long long)agg);
+            for (long long t = tile - 1; t >= 0;) {
+                unsigned long long st = atomicAdd(&status[t], 0ull);
+                if (!(st & ~ST_VAL)) continue;  // predecessor not published yet
+                prefix += (long long)(st & ST_VAL);
+                if (st & ST_PRE) break;
+                --t;
+            }
+            atomicExch(&status[tile], ST_PRE | (unsigned long long)(prefix + agg));
+        }
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    long long run = s_prefix + local;
 #pragma unroll
     for (int i = 0; i < SCAN_I; ++i) {
         long long j = base + i;
         if (j < n) out[j] = run;
         run += v[i];
+        if (j == n - 1) out[n] = run;
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == SCAN_T - 1) out[n] = run;
 }
 
-int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s) {
+int scan_src(ScanSrc src, long long *out, long long n, cudaStream_t s) {
     if (n <= 0) {
         MCF_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), s));
         return MCF_OK;
     }
     long long nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (nb == 1) {
-        k_tile_scan<<<1, SCAN_T, 0, s>>>(in, n, nullptr, out);
-        mcf::note_launch();
-        MCF_LAUNCHED("k_tile_scan");
-        return MCF_OK;
-    }
-    long long *bsum = nullptr, *boff = nullptr;
-    MCF_CUDA(cudaMallocAsync(&bsum, sizeof(long long) * (2 * nb + 1), s));
-    boff = bsum + nb;
-    k_tile_sums<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, bsum);
+    unsigned long long *status = nullptr;
+    MCF_CUDA(cudaMallocAsync(&status, sizeof(unsigned long long) * nb + 16, s));
+    unsigned int *ctr = reinterpret_cast<unsigned int *>(status + nb);
+    MCF_CUDA(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * nb + 16, s));
+    k_scan<<<(unsigned)nb, SCAN_T, 0, s>>>(src, n, out, status, ctr);
     mcf::note_launch();
-    MCF_LAUNCHED("k_tile_sums");
-    int rc = exclusive_scan_i64(bsum, boff, nb, s);
-    if (rc) return rc;
-    k_tile_scan<<<(unsigned)nb, SCAN_T, 0, s>>>(in, n, boff, out);
-    mcf::note_launch();
-    MCF_LAUNCHED("k_tile_scan");
-    MCF_CUDA(cudaFreeAsync(bsum, s));
+    MCF_LAUNCHED("k_scan");
+    MCF_CUDA(cudaFreeAsync(status, s));
     return MCF_OK;
+}
+
+int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s) {
+    ScanSrc src{in, nullptr, nullptr};
+    return scan_src(src, out, n, s);
 }
 
 // ---------------------------------------------------------------------------

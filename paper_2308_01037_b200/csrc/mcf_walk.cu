@@ -289,7 +289,9 @@ __global__ void k_col_reduce(const long long *__restrict__ walk_pre, long long c
     }
 }
 
-// y = alpha v + beta r + A x; G lanes per row, fixed reduction order.
+// y = alpha v + beta r + A x, rows binned by length so hub rows do not
+// serialise a few lanes: rows with degree <= LONG_ROW use G lanes each,
+// longer rows (graph->long_rows) one CTA each.  Fixed reduction order.
 template <int G>
 __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
                        const double *__restrict__ vals, double alpha, const double *__restrict__ v, double beta,
@@ -299,10 +301,14 @@ __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restr
     int sub = threadIdx.x % G;
     bool in = i < row_end;
     double s = 0.0;
+    long long e0 = 0, e1 = 0;
     if (in) {
-        long long e1 = row_ptr[i + 1];
-        for (long long e = row_ptr[i] + sub; e < e1; e += G) s = fma(__ldg(vals + e), __ldg(x + __ldg(col_ids + e)), s);
+        e0 = row_ptr[i];
+        e1 = row_ptr[i + 1];
+        in = (e1 - e0) <= LONG_ROW;
     }
+    if (in)
+        for (long long e = e0 + sub; e < e1; e += G) s = fma(__ldg(vals + e), __ldg(x + __ldg(col_ids + e)), s);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, G);
     if (in && sub == 0) {
@@ -310,6 +316,36 @@ __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restr
         if (v) h = alpha * v[i];
         if (r) h += beta * r[i];
         y[i] = h + s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_rows, long long n_long,
+                                                   const long long *__restrict__ row_ptr,
+                                                   const int *__restrict__ col_ids, const double *__restrict__ vals,
+                                                   double alpha, const double *__restrict__ v, double beta,
+                                                   const double *__restrict__ r, const double *__restrict__ x,
+                                                   double *__restrict__ y, long long row_begin, long long row_end) {
+    __shared__ double part[8];
+    for (long long li = blockIdx.x; li < n_long; li += gridDim.x) {
+        const long long i = long_rows[li];
+        if (i < row_begin || i >= row_end) continue;
+        double s = 0.0;
+        for (long long e = row_ptr[i] + threadIdx.x; e < row_ptr[i + 1]; e += 256)
+            s = fma(__ldg(vals + e), __ldg(x + __ldg(col_ids + e)), s);
+        s = warp_sum(s);
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = threadIdx.x < 8 ? part[threadIdx.x] : 0.0;
+            t = warp_sum(t);
+            if (threadIdx.x == 0) {
+                double h = 0.0;
+                if (v) h = alpha * v[i];
+                if (r) h += beta * r[i];
+                y[i] = h + t;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -324,11 +360,14 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
     if (avg <= 8) {
         k_spmv<4><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
         mcf::note_launch();
-    } else if (avg <= 32) {
+    } else {
         k_spmv<8><<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
         mcf::note_launch();
-    } else {
-        k_spmv<32><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
+    }
+    if (g->n_long_rows > 0) {
+        long long grid = g->n_long_rows < 4 * sm_count() ? g->n_long_rows : 4 * sm_count();
+        k_spmv_long<<<(unsigned)grid, 256, 0, s>>>(g->long_rows, g->n_long_rows, rp, g->col_ids, g->vals, alpha, v,
+                                                   beta, r, x, y, rb, re);
         mcf::note_launch();
     }
     MCF_LAUNCHED("k_spmv");
