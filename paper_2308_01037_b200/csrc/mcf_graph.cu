@@ -20,50 +20,21 @@ struct BuildCounters {
     unsigned long long n_uniform, n_empty, n_negative;
     unsigned long long max_degree;
     unsigned long long max_rsum_bits;  // rsum >= 0: IEEE bits order like the values
+    unsigned long long n_long_rows, n_long_cols;
 };
 
-// One thread per row.  Row |a| sums are accumulated sequentially in CSR order,
-// which is what np.add.at does for row_abs_sums (sparsemat.py:355-360), so the
-// weight ratios a/t = copysign(rsum, a) (walker.py:124-125) match bit for bit.
-__global__ void k_rows(const long long *__restrict__ row_ptr, const double *__restrict__ vals, long long n,
-                       NodeHdr *__restrict__ hdr, BuildCounters *__restrict__ cnt) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long uni = 0, emp = 0, neg = 0, maxdeg = 0, maxr = 0;
-    if (i < n) {
-        long long s = row_ptr[i], e = row_ptr[i + 1];
-        double acc = 0.0;
-        bool uniform = true;
-        double first = (e > s) ? fabs(vals[s]) : 0.0;
-        for (long long j = s; j < e; ++j) {
-            double v = vals[j];
-            double a = fabs(v);
-            acc = __dadd_rn(acc, a);
-            uniform &= (a == first);
-            neg += (v < 0.0);
-        }
-        uint32_t flags = 0;
-        if (uniform) flags |= HDR_UNIFORM;
-        if (neg) flags |= HDR_HAS_NEG;
-        NodeHdr h;
-        h.start = s;
-        h.deg = (int)(e - s);
-        h.flags = flags;
-        h.rsum = acc;
-        h.aux = 0.0;
-        hdr[i] = h;
-        uni = (uniform && e > s);
-        emp = (e == s);
-        maxdeg = (unsigned long long)(e - s);
-        maxr = (unsigned long long)__double_as_longlong(acc);
-    }
-    // block-aggregate then one atomic per warp
-    uni = warp_sum_ll((long long)uni);
-    emp = warp_sum_ll((long long)emp);
-    neg = warp_sum_ll((long long)neg);
+constexpr int LONG_COL = 256;   // columns longer than this get a warp in k_colnorm_long
+constexpr int LEAFCAP = 2048;   // leaves of the pairwise tree a warp keeps in smem
+
+__device__ __forceinline__ void add_row_stats(BuildCounters *cnt, unsigned long long uni, unsigned long long emp,
+                                              unsigned long long neg, unsigned long long maxdeg,
+                                              unsigned long long maxr, unsigned mask = MCF_FULL) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long a = __shfl_xor_sync(MCF_FULL, maxdeg, o);
-        unsigned long long b = __shfl_xor_sync(MCF_FULL, maxr, o);
+        uni += __shfl_xor_sync(mask, uni, o);
+        emp += __shfl_xor_sync(mask, emp, o);
+        neg += __shfl_xor_sync(mask, neg, o);
+        unsigned long long a = __shfl_xor_sync(mask, maxdeg, o), b = __shfl_xor_sync(mask, maxr, o);
         maxdeg = a > maxdeg ? a : maxdeg;
         maxr = b > maxr ? b : maxr;
     }
@@ -76,11 +47,93 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
     }
 }
 
-// Rows longer than LONG_ROW, compacted (order irrelevant: each is reduced alone).
-__global__ void k_long_rows(const long long *__restrict__ row_ptr, long long n, int *__restrict__ out,
+__device__ __forceinline__ NodeHdr make_hdr(long long s, long long e, double acc, bool uniform, bool neg) {
+    NodeHdr h;
+    h.start = s;
+    h.deg = (int)(e - s);
+    h.flags = (uniform ? HDR_UNIFORM : 0u) | (neg ? HDR_HAS_NEG : 0u);
+    h.rsum = acc;
+    h.aux = 0.0;
+    return h;
+}
+
+// Rows (or columns) longer than `thr`, compacted (order irrelevant).
+__global__ void k_mark_long(const long long *__restrict__ ptr, long long n, long long thr, int *__restrict__ out,
                             unsigned long long *count) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && row_ptr[i + 1] - row_ptr[i] > LONG_ROW) out[atomicAdd(count, 1ull)] = (int)i;
+    if (i < n && ptr[i + 1] - ptr[i] > thr) out[atomicAdd(count, 1ull)] = (int)i;
+}
+
+// One thread per row of degree <= LONG_ROW.  Row |a| sums are accumulated
+// sequentially in CSR order, which is what np.add.at does for row_abs_sums
+// (sparsemat.py:355-360), so the weight ratios a/t = copysign(rsum, a)
+// (walker.py:124-125) match bit for bit.  Loads are batched 8 at a time.
+__global__ void k_rows(const long long *__restrict__ row_ptr, const double *__restrict__ vals, long long n,
+                       NodeHdr *__restrict__ hdr, BuildCounters *__restrict__ cnt) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long uni = 0, emp = 0, neg = 0, maxdeg = 0, maxr = 0;
+    if (i < n) {
+        const long long s = row_ptr[i], e = row_ptr[i + 1];
+        if (e - s <= LONG_ROW) {
+            double acc = 0.0;
+            bool uniform = true;
+            const double first = (e > s) ? fabs(vals[s]) : 0.0;
+            for (long long j = s; j < e; j += 8) {
+                double v[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) v[t] = (j + t < e) ? vals[j + t] : 0.0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    if (j + t < e) {
+                        const double a = fabs(v[t]);
+                        acc = __dadd_rn(acc, a);
+                        uniform &= (a == first);
+                        neg += (v[t] < 0.0);
+                    }
+                }
+            }
+            hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+            uni = (uniform && e > s);
+            emp = (e == s);
+            maxdeg = (unsigned long long)(e - s);
+            maxr = (unsigned long long)__double_as_longlong(acc);
+        }
+    }
+    add_row_stats(cnt, uni, emp, neg, maxdeg, maxr);
+}
+
+// One warp per long row: 32 coalesced loads, then the sequential sum in CSR
+// order through shuffles (same bits as the one-thread loop).
+__global__ void k_rows_long(const int *__restrict__ rows, const unsigned long long *count,
+                            const long long *__restrict__ row_ptr, const double *__restrict__ vals,
+                            NodeHdr *__restrict__ hdr, BuildCounters *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long nl = (long long)*count;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long li = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += warps) {
+        const int i = rows[li];
+        const long long s = row_ptr[i], e = row_ptr[i + 1];
+        const double first = fabs(vals[s]);
+        double acc = 0.0;
+        bool uniform = true;
+        unsigned long long neg = 0;
+        for (long long j = s; j < e; j += 32) {
+            const long long jj = j + lane;
+            const double v = jj < e ? vals[jj] : 0.0;
+            const double a = fabs(v);
+            uniform &= __all_sync(MCF_FULL, jj >= e || a == first);
+            neg += __popc(__ballot_sync(MCF_FULL, jj < e && v < 0.0));
+            const int m = (int)(e - j < 32 ? e - j : 32);
+            for (int t = 0; t < m; ++t) acc = __dadd_rn(acc, __shfl_sync(MCF_FULL, a, t));
+        }
+        if (lane == 0) hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+        if (lane == 0) {
+            if (uniform) atomicAdd(&cnt->n_uniform, 1ull);
+            if (neg) atomicAdd(&cnt->n_negative, neg);
+            atomicMax(&cnt->max_degree, (unsigned long long)(e - s));
+            atomicMax(&cnt->max_rsum_bits, (unsigned long long)__double_as_longlong(acc));
+        }
+    }
 }
 
 // Packed column ids with the sign of a in bit 31 (only built if some a < 0).
@@ -137,17 +190,18 @@ __device__ double pw_block(const double *a, long long n) {
     return res;
 }
 
-// The recursion of pairwise_sum evaluated with an explicit stack (device
-// recursion is avoided): frame state 0 = descend left, 1 = left done -> descend
-// right, 2 = both done -> combine and pop.  `ret` carries the value of the
-// child that just finished.
-template <bool SQUARE>
-__device__ double pw_sum(const double *a, long long n) {
-    if (n <= 128) return pw_block<SQUARE>(a, n);
+// The recursion of pairwise_sum evaluated with an explicit stack (no device
+// recursion): frame state 0 = descend left, 1 = left done -> descend right,
+// 2 = both done -> combine and pop.  `ret` carries the value of the child that
+// just finished.  leaf(k, off, len) supplies the value of the k-th leaf
+// (<= 128 terms) in recursion order.
+template <class LeafFn>
+__device__ double pw_eval(long long n, LeafFn leaf) {
+    if (n <= 128) return leaf(0, 0ll, n);
     long long off[28], len[28];  // depth <= 25 for n < 2^31
     double left[28];
     unsigned char st[28];
-    int sp = 0;
+    int sp = 0, k = 0;
     off[0] = 0;
     len[0] = n;
     st[0] = 0;
@@ -155,7 +209,7 @@ __device__ double pw_sum(const double *a, long long n) {
     while (sp >= 0) {
         const long long L = len[sp];
         if (L <= 128) {
-            ret = pw_block<SQUARE>(a + off[sp], L);
+            ret = leaf(k++, off[sp], L);
             --sp;
             continue;
         }
@@ -182,6 +236,17 @@ __device__ double pw_sum(const double *a, long long n) {
     return ret;
 }
 
+template <bool SQUARE>
+__device__ double pw_sum(const double *a, long long n) {
+    return pw_eval(n, [&](int, long long off, long long len) { return pw_block<SQUARE>(a + off, len); });
+}
+
+__device__ long long pw_leaf_count(long long n) {
+    long long c = 0;
+    pw_eval(n, [&](int, long long, long long) { ++c; return 0.0; });
+    return c;
+}
+
 // ||C_j||_2 exactly as scipy computes csc.multiply(csc).sum(axis=0) then sqrt
 // (walker.py:127): np.add.reduceat over the column = first + pairwise(rest).
 __global__ void k_colnorm(const long long *__restrict__ csc_ptr, const double *__restrict__ csc_vals, long long n,
@@ -189,12 +254,45 @@ __global__ void k_colnorm(const long long *__restrict__ csc_ptr, const double *_
     long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     long long s = csc_ptr[j], e = csc_ptr[j + 1];
+    if (e - s > LONG_COL) return;  // k_colnorm_long
     double sq = 0.0;
     if (e > s) {
         sq = __dmul_rn(csc_vals[s], csc_vals[s]);
         if (e - s > 1) sq = __dadd_rn(sq, pw_sum<true>(csc_vals + s + 1, e - s - 1));
     }
     col_norm[j] = __dsqrt_rn(sq);
+}
+
+// One warp per long column: lanes evaluate the leaves of the pairwise tree
+// (round robin), lane 0 combines them in the recursion order -> same bits.
+__global__ void __launch_bounds__(64) k_colnorm_long(const int *__restrict__ cols, const unsigned long long *count,
+                                                      const long long *__restrict__ csc_ptr,
+                                                      const double *__restrict__ csc_vals, double *__restrict__ col_norm) {
+    __shared__ double leafbuf[2][LEAFCAP];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *buf = leafbuf[w];
+    const long long nl = (long long)*count;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long li = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += warps) {
+        const int j = cols[li];
+        const long long s = csc_ptr[j], e = csc_ptr[j + 1];
+        const double *a = csc_vals + s + 1;
+        const long long m = e - s - 1;
+        const long long nleaf = pw_leaf_count(m);
+        double tail = 0.0;
+        if (nleaf > LEAFCAP) {
+            if (lane == 0) tail = pw_sum<true>(a, m);
+        } else {
+            pw_eval(m, [&](int k, long long off, long long len) {
+                if ((k & 31) == lane) buf[k] = pw_block<true>(a + off, len);
+                return 0.0;
+            });
+            __syncwarp();
+            if (lane == 0) tail = pw_eval(m, [&](int k, long long, long long) { return buf[k]; });
+        }
+        if (lane == 0) col_norm[j] = __dsqrt_rn(__dadd_rn(__dmul_rn(csc_vals[s], csc_vals[s]), tail));
+        __syncwarp();
+    }
 }
 
 __global__ void k_leaf_sums(const double *__restrict__ a, const long long *__restrict__ leaf_off,
@@ -231,45 +329,38 @@ static double pw_combine(long long n, const double *leaf, size_t &k) {
     return a + b;
 }
 
-static int numpy_sum(const double *dev, long long n, cudaStream_t s, double *out) {
-    std::vector<long long> lo;
-    std::vector<int> ln;
-    pw_leaves(0, n, lo, ln);
-    int nl = (int)lo.size();
-    long long *d_lo = nullptr;
-    int *d_ln = nullptr;
-    double *d_sum = nullptr;
-    MCF_CUDA(cudaMallocAsync(&d_lo, sizeof(long long) * nl, s));
-    MCF_CUDA(cudaMallocAsync(&d_ln, sizeof(int) * nl, s));
-    MCF_CUDA(cudaMallocAsync(&d_sum, sizeof(double) * nl, s));
-    MCF_CUDA(cudaMemcpyAsync(d_lo, lo.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, s));
-    MCF_CUDA(cudaMemcpyAsync(d_ln, ln.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s));
-    k_leaf_sums<<<(nl + 255) / 256, 256, 0, s>>>(dev, d_lo, d_ln, nl, d_sum);
-    mcf::note_launch();
-    MCF_LAUNCHED("k_leaf_sums");
-    std::vector<double> h(nl);
-    MCF_CUDA(cudaMemcpyAsync(h.data(), d_sum, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
-    MCF_CUDA(cudaStreamSynchronize(s));
-    size_t k = 0;
-    *out = pw_combine(n, h.data(), k);
-    cudaFreeAsync(d_lo, s);
-    cudaFreeAsync(d_ln, s);
-    cudaFreeAsync(d_sum, s);
-    return MCF_OK;
-}
-
 static void release(mcf_graph *g) {
     if (!g) return;
-    cudaFree(g->hdr);
-    if (g->ecol_owned) cudaFree(g->ecol);
-    cudaFree(g->cdf);
-    cudaFree(g->col_norm);
-    cudaFree(g->init_prob);
-    cudaFree(g->csr2csc);
-    cudaFree(g->long_rows);
+    cudaDeviceSynchronize();
+    if (g->hdr) cudaFreeAsync(g->hdr, 0);
+    if (g->ecol_owned) cudaFreeAsync(g->ecol, 0);
+    if (g->cdf) cudaFreeAsync(g->cdf, 0);
+    if (g->col_norm) cudaFreeAsync(g->col_norm, 0);
+    if (g->csr2csc) cudaFreeAsync(g->csr2csc, 0);
+    if (g->long_rows) cudaFreeAsync(g->long_rows, 0);
+    if (g->scratch) cudaFreeAsync(g->scratch, 0);
+    for (auto &p : g->ev_walk) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto &p : g->ev_q) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     delete g;
 }
 
+// keep freed stream-ordered memory in the pool (graph handles come and go)
+static void tune_pool() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
+// Device tables in one pass with a single host synchronisation (counters +
+// the leaves of sum_j ||C_j|| come back together; the host finishes numpy's
+// pairwise tree over the leaves and the rest is launched asynchronously).
 static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     MCF_ARG(c && out, "mcf_graph_create: null argument");
     MCF_ARG(c->n > 0, "matrix dimension must be positive");
@@ -280,6 +371,7 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     }
     MCF_ARG(c->row_ptr && c->col_ids && c->vals && c->csc_ptr && c->csc_rows && c->csc_vals,
             "mcf_graph_create: null CSR/CSC array");
+    tune_pool();
     mcf_graph *g = new mcf_graph();
     g->n = c->n;
     g->nnz = c->nnz;
@@ -290,75 +382,89 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     g->csc_rows = c->csc_rows;
     g->csc_vals = c->csc_vals;
     cudaGetDevice(&g->device);
-    int rc = MCF_OK;
+    const long long n = g->n;
     auto fail = [&](int code) {
         release(g);
         return code;
     };
-    BuildCounters *cnt = nullptr;
     cudaError_t e;
-    if ((e = cudaMalloc(&g->hdr, sizeof(NodeHdr) * g->n)) != cudaSuccess) return fail(cuda_status(e, "hdr"));
-    if ((e = cudaMalloc(&g->col_norm, sizeof(double) * g->n)) != cudaSuccess) return fail(cuda_status(e, "col_norm"));
-    if ((e = cudaMalloc(&g->init_prob, sizeof(double) * g->n)) != cudaSuccess) return fail(cuda_status(e, "init_prob"));
-    if ((e = cudaMallocAsync(&cnt, sizeof(BuildCounters), s)) != cudaSuccess) return fail(cuda_status(e, "counters"));
+    // leaves of the pairwise tree over the n column norms (host-enumerated)
+    std::vector<long long> lo;
+    std::vector<int> ln;
+    pw_leaves(0, n, lo, ln);
+    const int nl = (int)lo.size();
+    // one scratch block: counters | long-col list | leaf offsets | leaf lengths | leaf sums
+    size_t sz = sizeof(BuildCounters) + sizeof(int) * n + sizeof(long long) * nl + sizeof(int) * nl +
+                sizeof(double) * nl + 64;
+    char *scr = nullptr;
+    if ((e = cudaMallocAsync(&g->hdr, sizeof(NodeHdr) * n, s)) != cudaSuccess) return fail(cuda_status(e, "hdr"));
+    if ((e = cudaMallocAsync(&g->col_norm, sizeof(double) * 2 * n, s)) != cudaSuccess)
+        return fail(cuda_status(e, "col_norm"));
+    g->init_prob = g->col_norm + n;
+    if ((e = cudaMallocAsync(&g->long_rows, sizeof(int) * n + sizeof(unsigned long long), s)) != cudaSuccess)
+        return fail(cuda_status(e, "long_rows"));
+    if ((e = cudaMallocAsync(&scr, sz, s)) != cudaSuccess) return fail(cuda_status(e, "scratch"));
+    BuildCounters *cnt = reinterpret_cast<BuildCounters *>(scr);
+    int *long_cols = reinterpret_cast<int *>(scr + sizeof(BuildCounters));
+    long long *d_lo = reinterpret_cast<long long *>(((uintptr_t)(long_cols + n) + 15) & ~(uintptr_t)15);
+    int *d_ln = reinterpret_cast<int *>(d_lo + nl);
+    double *d_leaf = reinterpret_cast<double *>(((uintptr_t)(d_ln + nl) + 15) & ~(uintptr_t)15);
+    unsigned long long *lr_count = reinterpret_cast<unsigned long long *>(g->long_rows + n);
     cudaMemsetAsync(cnt, 0, sizeof(BuildCounters), s);
-    unsigned nb = (unsigned)((g->n + 255) / 256);
-    k_rows<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->vals, g->n, g->hdr, cnt);
+    cudaMemsetAsync(lr_count, 0, sizeof(unsigned long long), s);
+    cudaMemcpyAsync(d_lo, lo.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_ln, ln.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s);
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    const int wgrid = sm_count() * 8;
+    const long long *rp = (const long long *)g->row_ptr, *cp = (const long long *)g->csc_ptr;
+    k_mark_long<<<nb, 256, 0, s>>>(rp, n, LONG_ROW, g->long_rows, lr_count);
     mcf::note_launch();
-    k_colnorm<<<nb, 256, 0, s>>>((const long long *)g->csc_ptr, g->csc_vals, g->n, g->col_norm);
+    k_mark_long<<<nb, 256, 0, s>>>(cp, n, LONG_COL, long_cols, &cnt->n_long_cols);
     mcf::note_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "k_rows/k_colnorm"));
+    k_rows<<<nb, 256, 0, s>>>(rp, g->vals, n, g->hdr, cnt);
+    mcf::note_launch();
+    k_rows_long<<<wgrid, 256, 0, s>>>(g->long_rows, lr_count, rp, g->vals, g->hdr, cnt);
+    mcf::note_launch();
+    k_colnorm<<<nb, 256, 0, s>>>(cp, g->csc_vals, n, g->col_norm);
+    mcf::note_launch();
+    k_colnorm_long<<<wgrid, 64, 0, s>>>(long_cols, &cnt->n_long_cols, cp, g->csc_vals, g->col_norm);
+    mcf::note_launch();
+    k_leaf_sums<<<(nl + 255) / 256, 256, 0, s>>>(g->col_norm, d_lo, d_ln, nl, d_leaf);
+    mcf::note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "graph build kernels"));
     BuildCounters hc;
+    std::vector<double> leaf(nl);
     cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&g->n_long_rows, lr_count, sizeof(long long), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(leaf.data(), d_leaf, sizeof(double) * nl, cudaMemcpyDeviceToHost, s);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_status(e, "graph build"));
-    cudaFreeAsync(cnt, s);
-    g->info.n = g->n;
+    size_t k = 0;
+    const double total = pw_combine(n, leaf.data(), k);  // np.sum(col_norms) (walker.py:128)
+    g->info.n = n;
     g->info.nnz = g->nnz;
     g->info.n_uniform_rows = (int64_t)hc.n_uniform;
     g->info.n_empty_rows = (int64_t)hc.n_empty;
     g->info.n_negative = (int64_t)hc.n_negative;
     g->info.max_degree = (int64_t)hc.max_degree;
     memcpy(&g->info.max_row_abs_sum, &hc.max_rsum_bits, sizeof(double));
-    if (hc.max_degree > (unsigned long long)LONG_ROW) {  // hub rows get their own SpMV bin
-        unsigned long long *lc = nullptr, nl = 0;
-        if ((e = cudaMalloc(&lc, sizeof(unsigned long long))) != cudaSuccess) return fail(cuda_status(e, "long"));
-        cudaMemsetAsync(lc, 0, sizeof(unsigned long long), s);
-        int *tmp = nullptr;
-        if ((e = cudaMalloc(&tmp, sizeof(int) * g->n)) != cudaSuccess) return fail(cuda_status(e, "long rows"));
-        k_long_rows<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->n, tmp, lc);
-        mcf::note_launch();
-        cudaMemcpyAsync(&nl, lc, sizeof(nl), cudaMemcpyDeviceToHost, s);
-        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_status(e, "long rows"));
-        g->n_long_rows = (long long)nl;
-        if ((e = cudaMalloc(&g->long_rows, sizeof(int) * (nl ? nl : 1))) != cudaSuccess)
-            return fail(cuda_status(e, "long rows"));
-        cudaMemcpyAsync(g->long_rows, tmp, sizeof(int) * nl, cudaMemcpyDeviceToDevice, s);
-        cudaStreamSynchronize(s);
-        cudaFree(tmp);
-        cudaFree(lc);
-    }
+    g->info.col_norm_total = total;
     if (hc.n_negative) {
-        if ((e = cudaMalloc(&g->ecol, sizeof(int) * g->nnz)) != cudaSuccess) return fail(cuda_status(e, "ecol"));
+        if ((e = cudaMallocAsync(&g->ecol, sizeof(int) * g->nnz, s)) != cudaSuccess) return fail(cuda_status(e, "ecol"));
         g->ecol_owned = true;
         k_ecol<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>(g->col_ids, g->vals, g->nnz, g->ecol);
         mcf::note_launch();
     } else {
         g->ecol = const_cast<int32_t *>(g->col_ids);
     }
-    if (hc.n_uniform + hc.n_empty < (unsigned long long)g->n) {
-        if ((e = cudaMalloc(&g->cdf, sizeof(double) * g->nnz)) != cudaSuccess) return fail(cuda_status(e, "cdf"));
-        k_cdf<<<nb, 256, 0, s>>>(g->hdr, g->vals, g->n, g->cdf);
+    if (hc.n_uniform + hc.n_empty < (unsigned long long)n) {
+        if ((e = cudaMallocAsync(&g->cdf, sizeof(double) * g->nnz, s)) != cudaSuccess) return fail(cuda_status(e, "cdf"));
+        k_cdf<<<nb, 256, 0, s>>>(g->hdr, g->vals, n, g->cdf);
         mcf::note_launch();
     }
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "k_ecol/k_cdf"));
-    double total = 0.0;
-    rc = numpy_sum(g->col_norm, g->n, s, &total);
-    if (rc) return fail(rc);
-    g->info.col_norm_total = total;
-    k_divide<<<nb, 256, 0, s>>>(g->col_norm, total, g->n, g->init_prob);
+    k_divide<<<nb, 256, 0, s>>>(g->col_norm, total, n, g->init_prob);  // p_j (walker.py:129)
     mcf::note_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "k_divide"));
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_status(e, "graph build"));
+    cudaFreeAsync(scr, s);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail(cuda_status(e, "graph build tail"));
     *out = g;
     return MCF_OK;
 }
@@ -372,7 +478,6 @@ int mcf_graph_create(const mcf_csr *csr, void *stream, mcf_graph **out) {
 }
 
 int mcf_graph_destroy(mcf_graph *g) {
-    if (g) cudaDeviceSynchronize();
     mcf::release(g);
     return MCF_OK;
 }

@@ -85,6 +85,7 @@ struct mcf_graph {
     int64_t *csr2csc = nullptr;      // nnz, lazily built for diag
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;
+    void *scratch = nullptr;
     mcf_graph_info info{};
     int device = 0;
     // optional per-launch timing of the dominant kernels (MCF_FLAG_TIME_KERNELS)

@@ -36,6 +36,12 @@ def _same_storage(csr, csc) -> bool:
             and np.array_equal(csc.data, csr.data))
 
 
+def _upload(arr, dtype, dev) -> torch.Tensor:
+    """Host array -> device tensor (one H2D copy; page-locked sources DMA directly)."""
+    a = np.ascontiguousarray(arr, dtype=dtype)
+    return torch.from_numpy(a).to(dev, non_blocking=False)
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -80,18 +86,18 @@ class DeviceGraph:
         if not csr.has_sorted_indices:
             csr = csr.sorted_indices()
         dev = self.device
-        self.row_ptr = torch.from_numpy(np.ascontiguousarray(csr.indptr, dtype=np.int64)).to(dev)
-        self.col_ids = torch.from_numpy(np.ascontiguousarray(csr.indices, dtype=np.int32)).to(dev)
-        self.vals = torch.from_numpy(np.ascontiguousarray(csr.data, dtype=np.float64)).to(dev)
+        self.row_ptr = _upload(csr.indptr, np.int64, dev)
+        self.col_ids = _upload(csr.indices, np.int32, dev)
+        self.vals = _upload(csr.data, np.float64, dev)
         same = self.symmetric_hint and _same_storage(csr, csc)
         if same:
             self.csc_ptr, self.csc_rows, self.csc_vals = self.row_ptr, self.col_ids, self.vals
         else:
             if not csc.has_sorted_indices:
                 csc = csc.sorted_indices()
-            self.csc_ptr = torch.from_numpy(np.ascontiguousarray(csc.indptr, dtype=np.int64)).to(dev)
-            self.csc_rows = torch.from_numpy(np.ascontiguousarray(csc.indices, dtype=np.int32)).to(dev)
-            self.csc_vals = torch.from_numpy(np.ascontiguousarray(csc.data, dtype=np.float64)).to(dev)
+            self.csc_ptr = _upload(csc.indptr, np.int64, dev)
+            self.csc_rows = _upload(csc.indices, np.int32, dev)
+            self.csc_vals = _upload(csc.data, np.float64, dev)
         if self.gamma != 1.0:  # scale() on the device: every stored value times gamma
             self.vals = self.vals * self.gamma
             self.csc_vals = self.vals if same else self.csc_vals * self.gamma

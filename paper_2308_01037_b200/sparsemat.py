@@ -63,12 +63,18 @@ class SparseMatrix:
 
     @classmethod
     def from_csr_arrays(cls, n, row_ptr, col_ids, vals, symmetric_hint=False, meta=None):
-        """Wrap already sorted, duplicate-free CSR arrays (generators use this)."""
-        a_csr = sparse.csr_array((np.asarray(vals, np.float64), np.asarray(col_ids), np.asarray(row_ptr)),
-                                 shape=(n, n))
+        """Wrap already sorted, duplicate-free CSR arrays without copying them
+        (generators use this; pinned host buffers stay pinned)."""
+        rp = np.asarray(row_ptr)
+        ci = np.asarray(col_ids)
+        va = np.asarray(vals, dtype=np.float64)
+        a_csr = sparse.csr_array((n, n))
+        a_csr.indptr, a_csr.indices, a_csr.data = rp, ci, va
         a_csr.has_sorted_indices = True
-        if symmetric_hint:  # A == A^T: the CSC arrays are the CSR arrays
-            a_csc = sparse.csc_array((a_csr.data, a_csr.indices, a_csr.indptr), shape=(n, n))
+        if symmetric_hint:  # A == A^T: the CSC view shares the CSR arrays
+            a_csc = sparse.csc_array((n, n))
+            a_csc.indptr, a_csc.indices, a_csc.data = rp, ci, va
+            a_csc.has_sorted_indices = True
         else:
             a_csc = a_csr.tocsc()
             a_csc.sort_indices()
