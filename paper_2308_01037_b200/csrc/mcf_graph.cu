@@ -401,7 +401,8 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     if ((e = cudaMallocAsync(&g->col_norm, sizeof(double) * 2 * n, s)) != cudaSuccess)
         return fail(cuda_status(e, "col_norm"));
     g->init_prob = g->col_norm + n;
-    if ((e = cudaMallocAsync(&g->long_rows, sizeof(int) * n + sizeof(unsigned long long), s)) != cudaSuccess)
+    const long long n_even = (n + 1) & ~1ll;  // 8-byte aligned counter after the list
+    if ((e = cudaMallocAsync(&g->long_rows, sizeof(int) * n_even + sizeof(unsigned long long), s)) != cudaSuccess)
         return fail(cuda_status(e, "long_rows"));
     if ((e = cudaMallocAsync(&scr, sz, s)) != cudaSuccess) return fail(cuda_status(e, "scratch"));
     BuildCounters *cnt = reinterpret_cast<BuildCounters *>(scr);
@@ -409,7 +410,7 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     long long *d_lo = reinterpret_cast<long long *>(((uintptr_t)(long_cols + n) + 15) & ~(uintptr_t)15);
     int *d_ln = reinterpret_cast<int *>(d_lo + nl);
     double *d_leaf = reinterpret_cast<double *>(((uintptr_t)(d_ln + nl) + 15) & ~(uintptr_t)15);
-    unsigned long long *lr_count = reinterpret_cast<unsigned long long *>(g->long_rows + n);
+    unsigned long long *lr_count = reinterpret_cast<unsigned long long *>(g->long_rows + n_even);
     cudaMemsetAsync(cnt, 0, sizeof(BuildCounters), s);
     cudaMemsetAsync(lr_count, 0, sizeof(unsigned long long), s);
     cudaMemcpyAsync(d_lo, lo.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, s);

@@ -247,3 +247,38 @@ def test_katz_resolvent_statistics(mc):
     assert rep.gamma == pytest.approx(gam, rel=1e-15)
     z = (rep.scores - exact) / rep.result.stderr
     assert np.max(np.abs(z)) < 5
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_device_tables_bitwise_hub_rows(mc, seed):
+    """Rows/columns far longer than the warp-per-row thresholds (64 / 256),
+    random signed weights, non-symmetric: tables still equal the oracle's
+    (which is pinned to the reference) bit for bit, and so do the budgets."""
+    import torch
+    rng = np.random.default_rng(seed)
+    n = 3001
+    rows, cols = [], []
+    for hub, deg in ((0, 3000), (7, 1500), (100, 300), (2999, 70)):
+        nb = rng.choice(n, deg, replace=False)
+        rows += [hub] * deg
+        cols += list(nb)
+        rows += list(nb)
+        cols += [hub] * deg
+    r = rng.integers(0, n, 20000)
+    c = rng.integers(0, n, 20000)
+    m = sparse.coo_array((rng.normal(size=len(rows) + r.size), (np.r_[rows, r], np.r_[cols, c])), shape=(n, n)).tocsr()
+    m.sum_duplicates()
+    m.data[m.data == 0] = 0.5
+    m.sort_indices()
+    a = port.Csr.from_any(m)
+    t = port.transition_tables(a)
+    g = mc.DeviceGraph(as_matrix(a))
+    d = {k: v.cpu().numpy() for k, v in g.tables().items()}
+    assert np.array_equal(d["row_abs_sum"], t.rsum)
+    assert np.array_equal(d["col_norms"], t.col_norms)
+    assert np.array_equal(d["init_prob"], t.init_prob)
+    for ns in (1000, 77777):
+        assert np.array_equal(g.allocate(ns)[0].cpu().numpy(), port.allocate(t, ns))
+    x = rng.normal(size=n)
+    y = g.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+    np.testing.assert_allclose(y, m @ x, rtol=1e-12, atol=1e-12)
