@@ -49,8 +49,9 @@ __device__ __forceinline__ void add_row_stats(BuildCounters *cnt, unsigned long 
 
 __device__ __forceinline__ NodeHdr make_hdr(long long s, long long e, double acc, bool uniform, bool neg) {
     NodeHdr h;
-    h.start = s;
+    h.start = (int)s;
     h.deg = (int)(e - s);
+    h.pad = 0;
     h.flags = (uniform ? HDR_UNIFORM : 0u) | (neg ? HDR_HAS_NEG : 0u);
     h.rsum = acc;
     h.aux = 0.0;

@@ -56,9 +56,10 @@ enum : uint32_t {
 };
 
 struct __align__(32) NodeHdr {
-    long long start;  // row_ptr[i]
+    int start;        // row_ptr[i]  (nnz < 2^31)
     int deg;          // row_ptr[i+1] - row_ptr[i]
     uint32_t flags;
+    uint32_t pad;
     double rsum;      // sum_j |a_ij| in CSR order (= a/t magnitude, walker.py:124-125)
     double aux;       // per-call payload: r_i = (A v)_i for action walks
 };
@@ -146,9 +147,10 @@ __device__ __forceinline__ NodeHdr load_hdr(const NodeHdr *h) {
     const int4 *p = reinterpret_cast<const int4 *>(h);
     int4 a = __ldg(p), b = __ldg(p + 1);
     NodeHdr r;
-    r.start = ((long long)(unsigned)a.y << 32) | (unsigned)a.x;
-    r.deg = a.z;
-    r.flags = (uint32_t)a.w;
+    r.start = a.x;
+    r.deg = a.y;
+    r.flags = (uint32_t)a.z;
+    r.pad = 0;
     r.rsum = __hiloint2double(b.y, b.x);
     r.aux = __hiloint2double(b.w, b.z);
     return r;

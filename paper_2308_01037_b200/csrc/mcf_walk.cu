@@ -14,6 +14,8 @@
 // Per-walk contributions are written to a buffer and summed per column in a
 // fixed order, so q does not depend on scheduling, on the number of GPUs or on
 // how the column range is split.
+#include <cstdlib>
+
 #include "mcf_internal.cuh"
 
 namespace mcf {
@@ -50,17 +52,6 @@ __device__ __forceinline__ int cdf_pick(const double *__restrict__ cdf, int deg,
     return lo;
 }
 
-// Draw the next CSR entry of row h for step k of walk (c, wl).
-__device__ __forceinline__ long long draw_entry(const WalkCommon &a, const NodeHdr &h, long long k, long long wl,
-                                                int c) {
-    U4 r = philox4x32_10(U4{(uint32_t)k, (uint32_t)wl, (uint32_t)c, PHILOX_SALT}, a.key0, a.key1);
-    if (h.flags & HDR_UNIFORM) {
-        uint64_t x = ((uint64_t)r.x << 32) | r.y;
-        return h.start + (long long)__umul64hi(x, (uint64_t)h.deg);
-    }
-    return h.start + cdf_pick(a.cdf + h.start, h.deg, u53(r.z, r.w));
-}
-
 __device__ __forceinline__ void flush_stats(long long *stats, long long walks, long long em, long long tr,
                                             long long ab) {
     walks = warp_sum_ll(walks);
@@ -75,13 +66,14 @@ __device__ __forceinline__ void flush_stats(long long *stats, long long walks, l
     }
 }
 
-// Walk state of one lane.
+// Walk state of one lane (one walk slot).
 struct Lane {
     long long g;  // global walk index; -1 wants a walk, -2 no walks left
-    long long wl, k;
-    int c, state;
-    double w, thr;
     long long epos, eend;  // replay cursor
+    double w, thr, x;      // weight, cutoff threshold, per-walk accumulator
+    unsigned wl;           // walk index inside its column
+    int k, c, state;
+    uint32_t r0, r1;       // second half of the Philox block (odd steps)
 };
 
 // Warp-aggregated refill of lanes that finished their walk.
@@ -103,11 +95,12 @@ __device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long l
                 long long nc = __ldg(a.walk_pre + c + 1) - pre;
                 L.g = g;
                 L.c = c;
-                L.wl = g - pre;
+                L.wl = (unsigned)(g - pre);
                 L.k = 0;
                 L.state = c;
                 L.w = 1.0 / (double)nc;       // W0 = 1/N_c (walker.py:263)
                 L.thr = a.cutoff * L.w;       // strict cutoff W_c * W0 (walker.py:264)
+                L.x = 0.0;
                 if (REPLAY) {
                     L.epos = __ldg(a.walk_off + g);
                     L.eend = __ldg(a.walk_off + g + 1);
@@ -121,30 +114,56 @@ __device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long l
     return !__all_sync(MCF_FULL, L.g == -2);
 }
 
-// One step of walker.py:270-288 for one lane: the emission at step k has
-// already been consumed by the caller; this draws, updates W and the state
-// and applies the termination rules.  Returns true when the walk ended.
+constexpr long long PICK_END = -1;   // walk ends at this emission (absorbed, or bad replay stream)
+constexpr long long PICK_LAST = -2;  // final draw: only |W| matters, and |a/t| = row sum for every entry
+
+// First half of a step (walker.py:274-281): choose the CSR entry to take from
+// the current row h.  Philox-4x32-10 yields 128 bits per (step pair, walk,
+// column): even steps use the first 64, odd steps the second.
 template <bool REPLAY>
-__device__ __forceinline__ bool advance(const WalkCommon &a, Lane &L, const NodeHdr &h, long long &tr, long long &ab) {
+__device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, const NodeHdr &h, long long &ab) {
     if (h.deg == 0) {  // absorbing row (walker.py:274-278)
         ++ab;
-        return true;
+        return PICK_END;
     }
-    long long e;
     if (REPLAY) {
         if (L.epos >= L.eend) {
             atomicOr(a.err, 1);
-            return true;
+            return PICK_END;
         }
-        e = __ldg(a.entries + L.epos);
+        long long e = __ldg(a.entries + L.epos);
         ++L.epos;
-        if (e < h.start || e >= h.start + h.deg) atomicOr(a.err, 2);
-    } else {
-        e = draw_entry(a, h, L.k, L.wl, L.c);
+        if (e < h.start || e >= h.start + h.deg) {
+            atomicOr(a.err, 2);
+            return PICK_END;
+        }
+        return e;
     }
-    int pc = __ldg(a.ecol + e);
-    L.w *= (pc < 0) ? -h.rsum : h.rsum;  // a/t = copysign(rowsum, a) (walker.py:124-125, :282)
-    L.state = pc & 0x7fffffff;
+    if (L.k + 1 >= a.max_steps) return PICK_LAST;
+    uint64_t r;
+    if ((L.k & 1) == 0) {
+        U4 p = philox4x32_10(U4{(uint32_t)(L.k >> 1), L.wl, (uint32_t)L.c, PHILOX_SALT}, a.key0, a.key1);
+        r = ((uint64_t)p.x << 32) | p.y;
+        L.r0 = p.z;
+        L.r1 = p.w;
+    } else {
+        r = ((uint64_t)L.r0 << 32) | L.r1;
+    }
+    if (h.flags & HDR_UNIFORM) return h.start + (long long)__umul64hi(r, (uint64_t)h.deg);
+    return h.start + cdf_pick(a.cdf + h.start, h.deg, (double)(r >> 11) * 0x1.0p-53);
+}
+
+// Second half (walker.py:282-288): weight update a/t = copysign(rowsum, a)
+// (walker.py:124-125), move, then the strict cutoff and the step cap.
+// Returns true when the walk ended.
+__device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, const NodeHdr &h, long long e, int pc,
+                                      long long &tr) {
+    if (e == PICK_LAST) {
+        L.w *= h.rsum;
+    } else {
+        L.w *= (pc < 0) ? -h.rsum : h.rsum;
+        L.state = pc & 0x7fffffff;
+    }
     ++L.k;
     if (!(fabs(L.w) > L.thr)) return true;  // walker.py:286-288
     if (L.k >= a.max_steps) {               // step cap: truncated (walker.py:270, :289)
@@ -154,23 +173,48 @@ __device__ __forceinline__ bool advance(const WalkCommon &a, Lane &L, const Node
     return false;
 }
 
-template <bool REPLAY>
-__global__ void __launch_bounds__(256) k_walk_action(WalkCommon a, double *__restrict__ xw) {
+// NW walks per lane, stepped together so their dependent loads overlap.
+template <int NW>
+struct WalkOcc {  // resident CTAs per SM the register budget is tuned for
+    static constexpr int v = NW == 1 ? 5 : (NW == 2 ? 3 : 2);
+};
+
+template <bool REPLAY, int NW>
+__global__ void __launch_bounds__(256, WalkOcc<NW>::v) k_walk_action(WalkCommon a, double *__restrict__ xw) {
     const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
-    Lane L;
-    L.g = -1;
-    double x = 0.0;
+    Lane L[NW];
+#pragma unroll
+    for (int s = 0; s < NW; ++s) L[s].g = -1;
     long long n_walks = 0, em = 0, tr = 0, ab = 0;
-    while (refill<REPLAY>(a, wb, we, L, n_walks)) {
-        if (L.g < 0) continue;
-        if (L.k == 0) x = 0.0;
-        NodeHdr h = load_hdr(a.hdr + L.state);
-        x = fma(__ldg(a.zeta + L.k + 2) * L.w, h.aux, x);  // q_c += zeta_{k+2} W r[l]
-        ++em;
-        if (advance<REPLAY>(a, L, h, tr, ab)) {
-            if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
-            xw[L.g - wb] = x;
-            L.g = -1;
+    while (true) {
+        bool more = false;
+#pragma unroll
+        for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, we, L[s], n_walks);
+        if (!more) break;
+        NodeHdr h[NW];
+        long long e[NW];
+        int pc[NW];
+#pragma unroll
+        for (int s = 0; s < NW; ++s)
+            if (L[s].g >= 0) h[s] = load_hdr(a.hdr + L[s].state);
+#pragma unroll
+        for (int s = 0; s < NW; ++s) {
+            if (L[s].g < 0) continue;
+            L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, h[s].aux, L[s].x);  // q_c += zeta W r[l]
+            ++em;
+            e[s] = pick<REPLAY>(a, L[s], h[s], ab);
+        }
+#pragma unroll
+        for (int s = 0; s < NW; ++s)
+            if (L[s].g >= 0 && e[s] >= 0) pc[s] = __ldg(a.ecol + e[s]);
+#pragma unroll
+        for (int s = 0; s < NW; ++s) {
+            if (L[s].g < 0) continue;
+            if (e[s] == PICK_END || apply(a, L[s], h[s], e[s], pc[s], tr)) {
+                if (REPLAY && L[s].epos != L[s].eend) atomicOr(a.err, 4);
+                xw[L[s].g - wb] = L[s].x;
+                L[s].g = -1;
+            }
         }
     }
     flush_stats(a.stats, n_walks, em, tr, ab);
@@ -217,8 +261,10 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
             ewt[sb + L.k] = __ldg(a.zeta + L.k + 2) * L.w;
         }
         ++em;
-        long long emitted = L.k + 1;
-        if (advance<REPLAY>(a, L, h, tr, ab)) {
+        const long long emitted = L.k + 1;
+        const long long e = pick<REPLAY>(a, L, h, ab);
+        const int pc = e >= 0 ? __ldg(a.ecol + e) : 0;
+        if (e == PICK_END || apply(a, L, h, e, pc, tr)) {
             if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
             if (MODE == EMIT_COUNT) eaux[rel] = emitted;
             else
@@ -428,6 +474,17 @@ int walk_capacity(const mcf_walk_params *p, const long long *walk_pre, long long
     return rc;
 }
 
+// walks stepped together per lane (MCF_WALKS_PER_LANE = 1, 2 or 4; default 2)
+static int walks_per_lane() {
+    static int v = 0;
+    if (!v) {
+        const char *e = getenv("MCF_WALKS_PER_LANE");
+        v = e ? atoi(e) : 2;
+        if (v != 1 && v != 4) v = 2;
+    }
+    return v;
+}
+
 template <typename K>
 int walk_grid(K kernel, int threads, size_t smem) {
     int per_sm = 0;
@@ -514,12 +571,15 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
         rc = timed_begin(g, timed, g->ev_walk, s);
         if (rc) return rc;
         if (replay) {
-            k_walk_action<true><<<walk_grid(k_walk_action<true>, 256, 0), 256, 0, s>>>(a, xw);
-            mcf::note_launch();
+            k_walk_action<true, 1><<<walk_grid(k_walk_action<true, 1>, 256, 0), 256, 0, s>>>(a, xw);
         } else {
-            k_walk_action<false><<<walk_grid(k_walk_action<false>, 256, 0), 256, 0, s>>>(a, xw);
-            mcf::note_launch();
+            switch (walks_per_lane()) {
+                case 1: k_walk_action<false, 1><<<walk_grid(k_walk_action<false, 1>, 256, 0), 256, 0, s>>>(a, xw); break;
+                case 4: k_walk_action<false, 4><<<walk_grid(k_walk_action<false, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                default: k_walk_action<false, 2><<<walk_grid(k_walk_action<false, 2>, 256, 0), 256, 0, s>>>(a, xw);
+            }
         }
+        mcf::note_launch();
         MCF_LAUNCHED("k_walk_action");
         rc = timed_end(timed, g->ev_walk, s);
         if (rc) return rc;
