@@ -60,9 +60,16 @@ __global__ void __launch_bounds__(256) k_select_pass(const unsigned long long *_
     h[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long pre = st->prefix, msk = st->mask;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        unsigned long long k = key[i];
-        if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255u], 1u);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {  // warp-uniform trip count
+        const long long i = base + threadIdx.x;
+        const unsigned long long k = i < n ? key[i] : ~0ull;
+        const bool in = i < n && (k & msk) == pre;
+        const unsigned dig = in ? (unsigned)((k >> shift) & 255u) : 256u;
+        // equal digits in a warp (ties are common: equal-degree nodes share p)
+        // are added once per distinct digit
+        const unsigned grp = __match_any_sync(MCF_FULL, dig);
+        if (in && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&h[dig], (unsigned)__popc(grp));
     }
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);

@@ -21,6 +21,7 @@ struct BuildCounters {
     unsigned long long max_degree;
     unsigned long long max_rsum_bits;  // rsum >= 0: IEEE bits order like the values
     unsigned long long n_long_rows, n_long_cols;
+    unsigned long long min_abs_bits, max_abs_bits;  // over all stored |a| (uniform-value graphs)
 };
 
 constexpr int LONG_COL = 256;   // columns longer than this get a warp in k_colnorm_long
@@ -76,7 +77,7 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
     if (i < n) {
         const long long s = row_ptr[i], e = row_ptr[i + 1];
         if (e - s <= LONG_ROW) {
-            double acc = 0.0;
+            double acc = 0.0, mn = INFINITY, mx = 0.0;
             bool uniform = true;
             const double first = (e > s) ? fabs(vals[s]) : 0.0;
             for (long long j = s; j < e; j += 8) {
@@ -90,10 +91,16 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
                         acc = __dadd_rn(acc, a);
                         uniform &= (a == first);
                         neg += (v[t] < 0.0);
+                        mn = fmin(mn, a);
+                        mx = fmax(mx, a);
                     }
                 }
             }
             hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+            if (e > s) {
+                atomicMin(&cnt->min_abs_bits, (unsigned long long)__double_as_longlong(mn));
+                atomicMax(&cnt->max_abs_bits, (unsigned long long)__double_as_longlong(mx));
+            }
             uni = (uniform && e > s);
             emp = (e == s);
             maxdeg = (unsigned long long)(e - s);
@@ -115,7 +122,7 @@ __global__ void k_rows_long(const int *__restrict__ rows, const unsigned long lo
         const int i = rows[li];
         const long long s = row_ptr[i], e = row_ptr[i + 1];
         const double first = fabs(vals[s]);
-        double acc = 0.0;
+        double acc = 0.0, mn = INFINITY, mx = 0.0;
         bool uniform = true;
         unsigned long long neg = 0;
         for (long long j = s; j < e; j += 32) {
@@ -123,11 +130,24 @@ __global__ void k_rows_long(const int *__restrict__ rows, const unsigned long lo
             const double v = jj < e ? vals[jj] : 0.0;
             const double a = fabs(v);
             uniform &= __all_sync(MCF_FULL, jj >= e || a == first);
+            if (jj < e) {
+                mn = fmin(mn, a);
+                mx = fmax(mx, a);
+            }
             neg += __popc(__ballot_sync(MCF_FULL, jj < e && v < 0.0));
             const int m = (int)(e - j < 32 ? e - j : 32);
             for (int t = 0; t < m; ++t) acc = __dadd_rn(acc, __shfl_sync(MCF_FULL, a, t));
         }
         if (lane == 0) hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fmin(mn, __shfl_xor_sync(MCF_FULL, mn, o));
+            mx = fmax(mx, __shfl_xor_sync(MCF_FULL, mx, o));
+        }
+        if (lane == 0) {
+            atomicMin(&cnt->min_abs_bits, (unsigned long long)__double_as_longlong(mn));
+            atomicMax(&cnt->max_abs_bits, (unsigned long long)__double_as_longlong(mx));
+        }
         if (lane == 0) {
             if (uniform) atomicAdd(&cnt->n_uniform, 1ull);
             if (neg) atomicAdd(&cnt->n_negative, neg);
@@ -413,6 +433,7 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     double *d_leaf = reinterpret_cast<double *>(((uintptr_t)(d_ln + nl) + 15) & ~(uintptr_t)15);
     unsigned long long *lr_count = reinterpret_cast<unsigned long long *>(g->long_rows + n_even);
     cudaMemsetAsync(cnt, 0, sizeof(BuildCounters), s);
+    cudaMemsetAsync(&cnt->min_abs_bits, 0xff, sizeof(unsigned long long), s);
     cudaMemsetAsync(lr_count, 0, sizeof(unsigned long long), s);
     cudaMemcpyAsync(d_lo, lo.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_ln, ln.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, s);
@@ -450,6 +471,10 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     g->info.max_degree = (int64_t)hc.max_degree;
     memcpy(&g->info.max_row_abs_sum, &hc.max_rsum_bits, sizeof(double));
     g->info.col_norm_total = total;
+    if (hc.n_negative == 0 && hc.min_abs_bits == hc.max_abs_bits) {  // every stored value equal
+        g->uniform_value = true;
+        memcpy(&g->value, &hc.min_abs_bits, sizeof(double));
+    }
     if (hc.n_negative) {
         if ((e = cudaMallocAsync(&g->ecol, sizeof(int) * g->nnz, s)) != cudaSuccess) return fail(cuda_status(e, "ecol"));
         g->ecol_owned = true;

@@ -87,6 +87,8 @@ struct mcf_graph {
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;
     void *scratch = nullptr;
+    bool uniform_value = false;      // all stored values equal `value` (0/1 graphs scaled by gamma)
+    double value = 0.0;
     mcf_graph_info info{};
     int device = 0;
     // optional per-launch timing of the dominant kernels (MCF_FLAG_TIME_KERNELS)

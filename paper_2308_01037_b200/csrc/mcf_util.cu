@@ -123,22 +123,35 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(ScanSrc src, long long n, long 
     }
     long long agg;
     long long local = block_excl_scan(sum, &agg);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 tiles at a time
+        const int lane = threadIdx.x;
         long long prefix = 0;
         if (tile == 0) {
-            atomicExch(&status[0], ST_PRE | (unsigned long long)agg);
+            if (lane == 0) atomicExch(&status[0], ST_PRE | (unsigned long long)agg);
         } else {
-            atomicExch(&status[tile], ST_AGG | (unsigned long long)agg);
-            for (long long t = tile - 1; t >= 0;) {
-                unsigned long long st = atomicAdd(&status[t], 0ull);
-                if (!(st & ~ST_VAL)) continue;  // predecessor not published yet
-                prefix += (long long)(st & ST_VAL);
-                if (st & ST_PRE) break;
-                --t;
+            if (lane == 0) atomicExch(&status[tile], ST_AGG | (unsigned long long)agg);
+            long long t = tile - 1;
+            while (true) {
+                const long long mine = t - lane;
+                unsigned long long st = 0;
+                if (mine >= 0) {
+                    do {
+                        st = atomicAdd(&status[mine], 0ull);
+                    } while (!(st & ~ST_VAL));
+                }
+                const unsigned pre = __ballot_sync(MCF_FULL, mine >= 0 && (st & ST_PRE));
+                // sum values of tiles t .. nearest PREFIX tile (inclusive)
+                const int stop = pre ? __ffs(pre) - 1 : 31;
+                long long v = (lane <= stop && mine >= 0) ? (long long)(st & ST_VAL) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MCF_FULL, v, o);
+                prefix += v;
+                if (pre || t - 32 < 0) break;
+                t -= 32;
             }
-            atomicExch(&status[tile], ST_PRE | (unsigned long long)(prefix + agg));
+            if (lane == 0) atomicExch(&status[tile], ST_PRE | (unsigned long long)(prefix + agg));
         }
-        s_prefix = prefix;
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
     long long run = s_prefix + local;

@@ -337,11 +337,35 @@ __global__ void k_col_reduce(const long long *__restrict__ walk_pre, long long c
 
 // y = alpha v + beta r + A x, rows binned by length so hub rows do not
 // serialise a few lanes: rows with degree <= LONG_ROW use G lanes each,
-// longer rows (graph->long_rows) one CTA each.  Fixed reduction order.
-template <int G>
+// longer rows (graph->long_rows) one warp each (one CTA above HUGE_ROW).
+// UNI: every stored value equals `uval` (0/1 graph times gamma), so the value
+// array is not read: y = h + uval * sum_j x_j.  Fixed reduction order.
+constexpr int HUGE_ROW = 4096;
+
+template <int G, bool UNI>
+__device__ __forceinline__ double row_dot(const long long e0, const long long e1, int sub,
+                                          const int *__restrict__ col_ids, const double *__restrict__ vals,
+                                          const double *__restrict__ x) {
+    double s = 0.0;
+    for (long long e = e0 + sub; e < e1; e += G) {
+        const double xv = __ldg(x + __ldg(col_ids + e));
+        s = UNI ? s + xv : fma(__ldg(vals + e), xv, s);
+    }
+    return s;
+}
+
+__device__ __forceinline__ double combine_out(double alpha, const double *v, double beta, const double *r, long long i,
+                                              double s) {
+    double h = 0.0;
+    if (v) h = alpha * v[i];
+    if (r) h += beta * r[i];
+    return h + s;
+}
+
+template <int G, bool UNI>
 __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
-                       const double *__restrict__ vals, double alpha, const double *__restrict__ v, double beta,
-                       const double *__restrict__ r, const double *__restrict__ x, double *__restrict__ y,
+                       const double *__restrict__ vals, double uval, double alpha, const double *__restrict__ v,
+                       double beta, const double *__restrict__ r, const double *__restrict__ x, double *__restrict__ y,
                        long long row_begin, long long row_end) {
     long long i = row_begin + (((long long)blockIdx.x * blockDim.x + threadIdx.x) / G);
     int sub = threadIdx.x % G;
@@ -353,45 +377,60 @@ __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restr
         e1 = row_ptr[i + 1];
         in = (e1 - e0) <= LONG_ROW;
     }
-    if (in)
-        for (long long e = e0 + sub; e < e1; e += G) s = fma(__ldg(vals + e), __ldg(x + __ldg(col_ids + e)), s);
+    if (in) s = row_dot<G, UNI>(e0, e1, sub, col_ids, vals, x);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, G);
-    if (in && sub == 0) {
-        double h = 0.0;
-        if (v) h = alpha * v[i];
-        if (r) h += beta * r[i];
-        y[i] = h + s;
-    }
+    if (in && sub == 0) y[i] = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
 }
 
+template <bool UNI>
 __global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_rows, long long n_long,
                                                    const long long *__restrict__ row_ptr,
                                                    const int *__restrict__ col_ids, const double *__restrict__ vals,
-                                                   double alpha, const double *__restrict__ v, double beta,
+                                                   double uval, double alpha, const double *__restrict__ v, double beta,
                                                    const double *__restrict__ r, const double *__restrict__ x,
                                                    double *__restrict__ y, long long row_begin, long long row_end) {
     __shared__ double part[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // warps take rows of up to HUGE_ROW entries; the CTA takes the hub rows
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long li = gw; li < n_long; li += nw) {
+        const long long i = long_rows[li];
+        const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
+        if (i < row_begin || i >= row_end || e1 - e0 > HUGE_ROW) continue;
+        double s = warp_sum(row_dot<32, UNI>(e0, e1, lane, col_ids, vals, x));
+        if (lane == 0) y[i] = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
+    }
     for (long long li = blockIdx.x; li < n_long; li += gridDim.x) {
         const long long i = long_rows[li];
-        if (i < row_begin || i >= row_end) continue;
-        double s = 0.0;
-        for (long long e = row_ptr[i] + threadIdx.x; e < row_ptr[i + 1]; e += 256)
-            s = fma(__ldg(vals + e), __ldg(x + __ldg(col_ids + e)), s);
-        s = warp_sum(s);
-        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+        const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
+        if (i < row_begin || i >= row_end || e1 - e0 <= HUGE_ROW) continue;
+        double s = warp_sum(row_dot<256, UNI>(e0, e1, threadIdx.x, col_ids, vals, x));
+        if (lane == 0) part[w] = s;
         __syncthreads();
         if (threadIdx.x < 32) {
-            double t = threadIdx.x < 8 ? part[threadIdx.x] : 0.0;
-            t = warp_sum(t);
-            if (threadIdx.x == 0) {
-                double h = 0.0;
-                if (v) h = alpha * v[i];
-                if (r) h += beta * r[i];
-                y[i] = h + t;
-            }
+            double t = warp_sum(threadIdx.x < 8 ? part[threadIdx.x] : 0.0);
+            if (threadIdx.x == 0) y[i] = combine_out(alpha, v, beta, r, i, UNI ? uval * t : t);
         }
         __syncthreads();
+    }
+}
+
+template <int G, bool UNI>
+static void launch_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x,
+                        double *y, long long rb, long long re, cudaStream_t s) {
+    const long long rows = re - rb;
+    const long long *rp = (const long long *)g->row_ptr;
+    k_spmv<G, UNI><<<(unsigned)((rows * G + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta,
+                                                                     r, x, y, rb, re);
+    mcf::note_launch();
+    if (g->n_long_rows > 0) {
+        long long grid = (g->n_long_rows + 7) / 8;
+        if (grid > 8 * sm_count()) grid = 8 * sm_count();
+        k_spmv_long<UNI><<<(unsigned)grid, 256, 0, s>>>(g->long_rows, g->n_long_rows, rp, g->col_ids, g->vals, g->value,
+                                                       alpha, v, beta, r, x, y, rb, re);
+        mcf::note_launch();
     }
 }
 
@@ -400,21 +439,13 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
     MCF_ARG(g && x && y, "mcf_spmv: null argument");
     MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv: bad row range");
     if (re == rb) return MCF_OK;
-    long long avg = g->nnz / g->n;
-    long long rows = re - rb;
-    const long long *rp = (const long long *)g->row_ptr;
-    if (avg <= 8) {
-        k_spmv<4><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
-        mcf::note_launch();
+    const bool small = g->nnz / g->n <= 8;
+    if (g->uniform_value) {
+        if (small) launch_spmv<4, true>(g, alpha, v, beta, r, x, y, rb, re, s);
+        else launch_spmv<8, true>(g, alpha, v, beta, r, x, y, rb, re, s);
     } else {
-        k_spmv<8><<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, alpha, v, beta, r, x, y, rb, re);
-        mcf::note_launch();
-    }
-    if (g->n_long_rows > 0) {
-        long long grid = g->n_long_rows < 4 * sm_count() ? g->n_long_rows : 4 * sm_count();
-        k_spmv_long<<<(unsigned)grid, 256, 0, s>>>(g->long_rows, g->n_long_rows, rp, g->col_ids, g->vals, alpha, v,
-                                                   beta, r, x, y, rb, re);
-        mcf::note_launch();
+        if (small) launch_spmv<4, false>(g, alpha, v, beta, r, x, y, rb, re, s);
+        else launch_spmv<8, false>(g, alpha, v, beta, r, x, y, rb, re, s);
     }
     MCF_LAUNCHED("k_spmv");
     return MCF_OK;
@@ -474,13 +505,14 @@ int walk_capacity(const mcf_walk_params *p, const long long *walk_pre, long long
     return rc;
 }
 
-// walks stepped together per lane (MCF_WALKS_PER_LANE = 1, 2 or 4; default 2)
+// walks stepped together per lane (MCF_WALKS_PER_LANE = 1, 2 or 4; default 1:
+// on the L2-resident config-2 graph the register cost of 2 or 4 slots loses)
 static int walks_per_lane() {
     static int v = 0;
     if (!v) {
         const char *e = getenv("MCF_WALKS_PER_LANE");
-        v = e ? atoi(e) : 2;
-        if (v != 1 && v != 4) v = 2;
+        v = e ? atoi(e) : 1;
+        if (v != 2 && v != 4) v = 1;
     }
     return v;
 }
