@@ -66,10 +66,14 @@ __global__ void __launch_bounds__(256) k_select_pass(const unsigned long long *_
         const unsigned long long k = i < n ? key[i] : ~0ull;
         const bool in = i < n && (k & msk) == pre;
         const unsigned dig = in ? (unsigned)((k >> shift) & 255u) : 256u;
-        // equal digits in a warp (ties are common: equal-degree nodes share p)
-        // are added once per distinct digit
-        const unsigned grp = __match_any_sync(MCF_FULL, dig);
-        if (in && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&h[dig], (unsigned)__popc(grp));
+        // ties are common (equal-degree nodes share p): a warp whose keys all
+        // fall in one bin adds once
+        const unsigned d0 = __shfl_sync(MCF_FULL, dig, 0);
+        if (__all_sync(MCF_FULL, dig == d0)) {
+            if ((threadIdx.x & 31) == 0 && d0 < 256u) atomicAdd(&h[d0], 32u);
+        } else if (in) {
+            atomicAdd(&h[dig], 1u);
+        }
     }
     __syncthreads();
     if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);

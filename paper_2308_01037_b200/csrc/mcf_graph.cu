@@ -73,7 +73,7 @@ __global__ void k_mark_long(const long long *__restrict__ ptr, long long n, long
 __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__restrict__ vals, long long n,
                        NodeHdr *__restrict__ hdr, BuildCounters *__restrict__ cnt) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long uni = 0, emp = 0, neg = 0, maxdeg = 0, maxr = 0;
+    unsigned long long uni = 0, emp = 0, neg = 0, maxdeg = 0, maxr = 0, minb = ~0ull, maxb = 0;
     if (i < n) {
         const long long s = row_ptr[i], e = row_ptr[i + 1];
         if (e - s <= LONG_ROW) {
@@ -98,8 +98,8 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
             }
             hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
             if (e > s) {
-                atomicMin(&cnt->min_abs_bits, (unsigned long long)__double_as_longlong(mn));
-                atomicMax(&cnt->max_abs_bits, (unsigned long long)__double_as_longlong(mx));
+                minb = (unsigned long long)__double_as_longlong(mn);
+                maxb = (unsigned long long)__double_as_longlong(mx);
             }
             uni = (uniform && e > s);
             emp = (e == s);
@@ -108,6 +108,16 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
         }
     }
     add_row_stats(cnt, uni, emp, neg, maxdeg, maxr);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(MCF_FULL, minb, o), b = __shfl_xor_sync(MCF_FULL, maxb, o);
+        minb = a < minb ? a : minb;
+        maxb = b > maxb ? b : maxb;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (minb != ~0ull) atomicMin(&cnt->min_abs_bits, minb);
+        if (maxb) atomicMax(&cnt->max_abs_bits, maxb);
+    }
 }
 
 // One warp per long row: 32 coalesced loads, then the sequential sum in CSR
