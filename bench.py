@@ -40,6 +40,10 @@ CONFIGS = {
     1: dict(workload="config1: subgraph centrality diag(exp(beta A)), Erdos-Renyi n=1e4 mean degree 8 (LCC), "
                      "beta=1/lambda_max, 30 Taylor terms, 1000 walks per node",
             kind="diag", graph="er", n=10_000, deg=8, walks_per_node=1000, max_steps=28, cutoff=1e-300, seed=0),
+    4: dict(workload="config4: Katz resolvent (I - gamma A)^-1 1, symmetrised R-MAT scale 24 edge factor 16 "
+                     "(.57,.19,.19,.05), no loops/duplicates, gamma=0.85/lambda_max, W_c=1e-8, 100 walks per node",
+            kind="action", graph="rmat", scale=24, ef=16, walks_per_node=100, max_steps=10_000, cutoff=1e-8, seed=0,
+            func="resolvent", gamma_frac=0.85),
 }
 
 
@@ -47,15 +51,43 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def make_graph(cfg, pinned=False):
+def make_graph(cfg, pinned=False, scale=None):
+    """Host SparseMatrix (for the e2e leg), the scale factor (beta, or the Katz
+    gamma) and N_s.  R-MAT configs are generated on the GPU and copied to
+    pinned host memory once (setup, untimed)."""
     from paper_2308_01037_b200 import graphs
-    if cfg["graph"] == "ba":
+    if cfg["graph"] == "rmat":
+        import torch
+        from paper_2308_01037_b200.device import DeviceGraph
+        from paper_2308_01037_b200.sparsemat import SparseMatrix
+        sc = scale or cfg["scale"]
+        n, rp, ci = graphs.rmat_device(sc, cfg["ef"], seed=cfg["seed"])
+        g1 = DeviceGraph.from_device_arrays(n, rp, ci, torch.ones(ci.numel(), dtype=torch.float64, device=rp.device))
+        lam = graphs.lambda_max_device(g1)
+        g1.close()
+        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (rp, ci)]
+        host[0].copy_(rp)
+        host[1].copy_(ci)
+        vals = torch.ones(ci.numel(), dtype=torch.float64, pin_memory=True)
+        a = SparseMatrix.from_csr_arrays(n, host[0].numpy(), host[1].numpy(), vals.numpy(), symmetric_hint=True,
+                                         meta={"generator": "rmat", "scale": sc, "lambda_max": lam})
+        a._pinned = (host, vals)
+        del rp, ci
+        torch.cuda.empty_cache()
+        scale_factor = cfg.get("gamma_frac", 1.0) / lam
+    elif cfg["graph"] == "ba":
         a = graphs.barabasi_albert(cfg["n"], cfg["m"], seed=cfg["seed"], pinned=pinned)
+        scale_factor = 1.0 / graphs.lambda_max(a)
     else:
         a = graphs.erdos_renyi_lcc(cfg["n"], cfg["deg"], seed=cfg["seed"])
-    beta = 1.0 / graphs.lambda_max(a)
+        scale_factor = 1.0 / graphs.lambda_max(a)
     n_walks = cfg.get("n_walks") or cfg["walks_per_node"] * a.n
-    return a, beta, n_walks
+    return a, scale_factor, n_walks
+
+
+def coeff_stream(cfg):
+    import paper_2308_01037_b200 as mc
+    return mc.RESOLVENT if cfg.get("func") == "resolvent" else mc.EXPONENTIAL
 
 
 def measured_peak():
@@ -161,7 +193,7 @@ class CpuBaseline:
         A = port.Csr.from_any(a).scaled(beta)
         t = port.transition_tables(A)
         ni = port.allocate(t, n_walks)
-        z = port.zeta_prefix("exponential", cfg["max_steps"] + 2)
+        z = port.zeta_prefix(cfg.get("func", "exponential"), cfg["max_steps"] + 2)
         _CPU.update(kind=cfg["kind"], t=t, A=A, ni=ni, z=z, r=A.scipy_csr() @ np.ones(A.n),
                     max_steps=cfg["max_steps"], cutoff=cfg["cutoff"], seed=cfg["seed"])
         self.setup_s = time.perf_counter() - t0
@@ -201,6 +233,10 @@ def run_reference(args, cfg):
     if rank != 0:
         return 0
     a, beta, n_walks = make_graph(cfg)
+    if cfg["graph"] == "rmat":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference CPU algorithm needs ~80 GB of host RAM "
+                                                              "for this R-MAT graph's numpy tables"}), flush=True)
+        return 0
     cpu = CpuBaseline(a, beta, n_walks, cfg)
     per_step = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
@@ -246,10 +282,11 @@ def run_device(args, cfg):
     lib = _native.lib()
 
     t0 = time.perf_counter()
-    a, beta, n_walks = make_graph(cfg, pinned=True)
+    a, beta, n_walks = make_graph(cfg, pinned=True, scale=args.scale)
+    coeffs = coeff_stream(cfg)
     log(f"[bench] graph n={a.n} nnz={a.nnz} beta={beta:.6e} walks={n_walks} ({time.perf_counter() - t0:.1f}s)")
     wcfg = mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"], cfg["seed"])
-    z = mc.EXPONENTIAL.prefix(cfg["max_steps"] + 2)
+    z = coeffs.prefix(cfg["max_steps"] + 2)
     params = WalkParams(wcfg, z)
     g = DeviceGraph(a, gamma=beta)
     v = torch.ones(g.n, dtype=torch.float64, device=g.device)
@@ -257,8 +294,8 @@ def run_device(args, cfg):
 
     def step():
         if cfg["kind"] == "action":
-            return parallel.sharded_action(g, mc.EXPONENTIAL, v, wcfg, params=params)
-        return parallel.sharded_diag(g, mc.EXPONENTIAL, wcfg, params=params)
+            return parallel.sharded_action(g, coeffs, v, wcfg, params=params)
+        return parallel.sharded_diag(g, coeffs, wcfg, params=params)
 
     clocks = Clocks(local) if rank == 0 else None
     for _ in range(max(args.warmup, 0)):
@@ -376,9 +413,9 @@ def run_device(args, cfg):
             ge = DeviceGraph(a, gamma=beta)
             ve = torch.ones(ge.n, dtype=torch.float64, device=ge.device)
             if cfg["kind"] == "action":
-                y, _ = parallel.sharded_action(ge, mc.EXPONENTIAL, ve, wcfg)
+                y, _ = parallel.sharded_action(ge, coeffs, ve, wcfg)
             else:
-                y, _ = parallel.sharded_diag(ge, mc.EXPONENTIAL, wcfg)
+                y, _ = parallel.sharded_diag(ge, coeffs, wcfg)
             host = y.cpu().numpy()
             torch.cuda.synchronize()
             dt = time.perf_counter() - t1
@@ -398,7 +435,10 @@ def run_device(args, cfg):
 
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if cfg["graph"] == "rmat":
+        cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": "not run: the oracle's numpy tables for this graph need ~80 GB of host RAM (SURVEY §8c)"}
+    elif rank == 0 and world == 1 and not args.no_cpu:
         cb = CpuBaseline(a, beta, n_walks, cfg)
         em, wall, k = cb.run(args.cpu_seconds)
         cpu = {"value": em / wall, "unit": "steps/s", "cores": cb.cores, "kind": "port", "sample": cb.describe(k)}
@@ -438,8 +478,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale (config 4)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.scale and cfg["graph"] == "rmat":
+        cfg["scale"] = args.scale
+        cfg["workload"] = cfg["workload"].replace("scale 24", f"scale {args.scale}")
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_device(args, cfg)

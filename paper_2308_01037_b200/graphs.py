@@ -81,3 +81,68 @@ def lambda_max(a) -> float:
     if m.shape[0] <= 512:
         return float(np.linalg.eigvalsh(m.toarray())[-1])
     return float(eigsh(m, k=1, which="LA", v0=np.ones(m.shape[0]), tol=1e-12)[0][0])
+
+
+# --------------------------------------------------------------------------
+# device generators (large configs; torch is plumbing here, the estimator
+# kernels never see these code paths)
+# --------------------------------------------------------------------------
+def _csr_from_sorted_keys(keys, scale: int, n: int):
+    import torch
+    rows = keys >> scale
+    cols = (keys & (n - 1)).to(torch.int32)
+    counts = torch.bincount(rows, minlength=n)
+    row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=keys.device)
+    torch.cumsum(counts, 0, out=row_ptr[1:])
+    return row_ptr, cols
+
+
+def rmat_device(scale: int, edge_factor: int = 16, pa: float = 0.57, pb: float = 0.19, pc: float = 0.19,
+                seed: int = 0, device="cuda", chunk: int = 1 << 26):
+    """Symmetrised R-MAT on the GPU (BASELINE configs 3-4): edge_factor * 2^scale
+    draws, one uniform per level with the reference's quadrant rule
+    (graphgen.py:138-143: row bit r >= pa+pb, column bit r in [pa, pa+pb) or
+    r >= pa+pb+pc), then both directions, loops and duplicates removed.  No
+    isolated-node compaction: n = 2^scale rows as generated.
+    Returns (n, row_ptr int64, col_ids int32) on the device."""
+    import torch
+    n = 1 << scale
+    draws = edge_factor << scale
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    ab, abc = pa + pb, pa + pb + pc
+    keys = []
+    for lo in range(0, draws, chunk):
+        m = min(chunk, draws - lo)
+        u = torch.zeros(m, dtype=torch.int64, device=device)
+        v = torch.zeros(m, dtype=torch.int64, device=device)
+        for _ in range(scale):
+            r = torch.rand(m, generator=gen, dtype=torch.float64, device=device)
+            rb = r >= ab
+            cb = ((r >= pa) & ~rb) | (r >= abc)
+            u = (u << 1) | rb
+            v = (v << 1) | cb
+        keep = u != v
+        u, v = u[keep], v[keep]
+        keys.append((u << scale) | v)
+        keys.append((v << scale) | u)
+    k = torch.cat(keys)
+    del keys
+    k = torch.unique(k, sorted=True)
+    row_ptr, cols = _csr_from_sorted_keys(k, scale, n)
+    return n, row_ptr, cols
+
+
+def lambda_max_device(g, iters: int = 300) -> float:
+    """Largest eigenvalue of a symmetric nonnegative matrix on the device:
+    power iteration on A + I (the +1 shift keeps -lambda_max away) with the
+    library SpMV, Rayleigh quotient at the end."""
+    import torch
+    x = torch.ones(g.n, dtype=torch.float64, device=g.device)
+    x /= torch.linalg.norm(x)
+    y = torch.empty_like(x)
+    for _ in range(iters):
+        g.spmv(x, alpha=1.0, v=x, out=y)
+        x, y = y / torch.linalg.norm(y), x
+    g.spmv(x, out=y)
+    return float((x @ y) / (x @ x))
