@@ -77,6 +77,9 @@ typedef struct {
     int64_t max_degree;
     double max_row_abs_sum;   /* sqrt(alpha_diagnostic) (walker.py:293-302) */
     double col_norm_total;    /* sum_j ||C_j||_2 (walker.py:128) */
+    int64_t walk_layout;      /* 0: compact (entry id, then the target's 32-B header: two random
+                                 sectors per step); 1: fat (target header copied into every
+                                 entry: one random sector per step, 32 B x nnz) */
 } mcf_graph_info;
 
 /* Walk termination and RNG (WalkConfig, walker.py:44-67) plus the series. */

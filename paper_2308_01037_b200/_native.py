@@ -29,7 +29,7 @@ class McfCsr(C.Structure):
 class McfGraphInfo(C.Structure):
     _fields_ = [("n", I64), ("nnz", I64), ("n_uniform_rows", I64), ("n_empty_rows", I64),
                 ("n_negative", I64), ("max_degree", I64), ("max_row_abs_sum", C.c_double),
-                ("col_norm_total", C.c_double)]
+                ("col_norm_total", C.c_double), ("walk_layout", I64)]
 
 
 class McfWalkParams(C.Structure):

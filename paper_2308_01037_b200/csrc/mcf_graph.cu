@@ -9,6 +9,7 @@
 //   col_norm[n], init_prob[n]  start distribution, bit-identical to the
 //               reference (numpy pairwise summation order reproduced).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -165,6 +166,18 @@ __global__ void k_rows_long(const int *__restrict__ rows, const unsigned long lo
             atomicMax(&cnt->max_rsum_bits, (unsigned long long)__double_as_longlong(acc));
         }
     }
+}
+
+// Fat walk entries: went[e] = hdr[col[e]], pad = col[e], sign of a_e in flags.
+__global__ void k_build_went(const NodeHdr *__restrict__ hdr, const int *__restrict__ col_ids,
+                             const double *__restrict__ vals, long long nnz, NodeHdr *__restrict__ went) {
+    long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int c = col_ids[e];
+    NodeHdr h = hdr[c];
+    h.pad = (uint32_t)c;
+    if (vals[e] < 0.0) h.flags |= HDR_NEG_EDGE;
+    went[e] = h;
 }
 
 // Packed column ids with the sign of a in bit 31 (only built if some a < 0).
@@ -369,6 +382,7 @@ static void release(mcf_graph *g) {
     if (g->col_norm) cudaFreeAsync(g->col_norm, 0);
     if (g->csr2csc) cudaFreeAsync(g->csr2csc, 0);
     if (g->long_rows) cudaFreeAsync(g->long_rows, 0);
+    if (g->went) cudaFreeAsync(g->went, 0);
     if (g->scratch) cudaFreeAsync(g->scratch, 0);
     for (auto &p : g->ev_walk) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto &p : g->ev_q) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -497,6 +511,26 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
         if ((e = cudaMallocAsync(&g->cdf, sizeof(double) * g->nnz, s)) != cudaSuccess) return fail(cuda_status(e, "cdf"));
         k_cdf<<<nb, 256, 0, s>>>(g->hdr, g->vals, n, g->cdf);
         mcf::note_launch();
+    }
+    // walk layout: fat entries when the compact tables (32 n + 4 nnz bytes)
+    // would not stay resident in L2 (MCF_WALK_LAYOUT=fat|compact overrides)
+    {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+        const double compact_bytes = 32.0 * n + 4.0 * g->nnz;
+        bool fat = compact_bytes > 0.75 * (double)l2;
+        const char *env = getenv("MCF_WALK_LAYOUT");
+        if (env && !strcmp(env, "fat")) fat = true;
+        if (env && !strcmp(env, "compact")) fat = false;
+        if (fat && cudaMallocAsync(&g->went, sizeof(NodeHdr) * g->nnz, s) == cudaSuccess) {
+            k_build_went<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>(g->hdr, g->col_ids, g->vals, g->nnz,
+                                                                          g->went);
+            mcf::note_launch();
+        } else {
+            cudaGetLastError();  // no room for 32 B x nnz: stay compact
+            g->went = nullptr;
+        }
+        g->info.walk_layout = g->went ? 1 : 0;
     }
     k_divide<<<nb, 256, 0, s>>>(g->col_norm, total, n, g->init_prob);  // p_j (walker.py:129)
     mcf::note_launch();

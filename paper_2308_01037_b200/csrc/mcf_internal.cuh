@@ -53,13 +53,14 @@ namespace mcf {
 enum : uint32_t {
     HDR_UNIFORM = 1u,   // all |a_ij| of the row equal -> sample by index
     HDR_HAS_NEG = 2u,   // row holds a negative value -> sign packed in ecol
+    HDR_NEG_EDGE = 4u,  // walk-entry copy only: the entry's own value a_e < 0
 };
 
 struct __align__(32) NodeHdr {
     int start;        // row_ptr[i]  (nnz < 2^31)
     int deg;          // row_ptr[i+1] - row_ptr[i]
     uint32_t flags;
-    uint32_t pad;
+    uint32_t pad;     // walk-entry copy: the node id itself
     double rsum;      // sum_j |a_ij| in CSR order (= a/t magnitude, walker.py:124-125)
     double aux;       // per-call payload: r_i = (A v)_i for action walks
 };
@@ -84,6 +85,11 @@ struct mcf_graph {
     double *col_norm = nullptr;      // n
     double *init_prob = nullptr;     // n
     int64_t *csr2csc = nullptr;      // nnz, lazily built for diag
+    // "fat" walk layout: went[e] = hdr[col[e]] with pad = col[e] and the
+    // entry's sign in flags, so a step reads ONE random 32-B sector instead of
+    // two (entry, then the target's header).  32 B x nnz; used when the
+    // compact tables would not stay in L2.
+    mcf::NodeHdr *went = nullptr;
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;
     void *scratch = nullptr;

@@ -24,6 +24,7 @@ constexpr uint32_t PHILOX_SALT = 0x6d636621u;  // "mcf!"
 
 struct WalkCommon {
     const NodeHdr *__restrict__ hdr;
+    const NodeHdr *__restrict__ went;  // fat layout (nullptr: compact)
     const int *__restrict__ ecol;
     const double *__restrict__ cdf;
     const double *__restrict__ zeta;
@@ -71,6 +72,7 @@ struct Lane {
     long long g;  // global walk index; -1 wants a walk, -2 no walks left
     long long epos, eend;  // replay cursor
     double w, thr, x;      // weight, cutoff threshold, per-walk accumulator
+    NodeHdr h;             // header of the current state (aux = r[state])
     unsigned wl;           // walk index inside its column
     int k, c, state;
     uint32_t r0, r1;       // second half of the Philox block (odd steps)
@@ -98,6 +100,7 @@ __device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long l
                 L.wl = (unsigned)(g - pre);
                 L.k = 0;
                 L.state = c;
+                L.h = load_hdr(a.hdr + c);
                 L.w = 1.0 / (double)nc;       // W0 = 1/N_c (walker.py:263)
                 L.thr = a.cutoff * L.w;       // strict cutoff W_c * W0 (walker.py:264)
                 L.x = 0.0;
@@ -118,10 +121,11 @@ constexpr long long PICK_END = -1;   // walk ends at this emission (absorbed, or
 constexpr long long PICK_LAST = -2;  // final draw: only |W| matters, and |a/t| = row sum for every entry
 
 // First half of a step (walker.py:274-281): choose the CSR entry to take from
-// the current row h.  Philox-4x32-10 yields 128 bits per (step pair, walk,
+// the current row.  Philox-4x32-10 yields 128 bits per (step pair, walk,
 // column): even steps use the first 64, odd steps the second.
 template <bool REPLAY>
-__device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, const NodeHdr &h, long long &ab) {
+__device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, long long &ab) {
+    const NodeHdr &h = L.h;
     if (h.deg == 0) {  // absorbing row (walker.py:274-278)
         ++ab;
         return PICK_END;
@@ -133,7 +137,7 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, const No
         }
         long long e = __ldg(a.entries + L.epos);
         ++L.epos;
-        if (e < h.start || e >= h.start + h.deg) {
+        if (e < h.start || e >= (long long)h.start + h.deg) {
             atomicOr(a.err, 2);
             return PICK_END;
         }
@@ -153,16 +157,30 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, const No
     return h.start + cdf_pick(a.cdf + h.start, h.deg, (double)(r >> 11) * 0x1.0p-53);
 }
 
-// Second half (walker.py:282-288): weight update a/t = copysign(rowsum, a)
-// (walker.py:124-125), move, then the strict cutoff and the step cap.
-// Returns true when the walk ended.
-__device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, const NodeHdr &h, long long e, int pc,
-                                      long long &tr) {
+// The header of the entry's target, with pad = target id and HDR_NEG_EDGE =
+// sign of a_e.  Fat layout: one 32-B sector; compact: the entry's packed
+// column id, then the target's header (two dependent sectors).
+template <bool FAT>
+__device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) {
+    if (FAT) return load_hdr(a.went + e);
+    const int pc = __ldg(a.ecol + e);
+    const int nxt = pc & 0x7fffffff;
+    NodeHdr h = load_hdr(a.hdr + nxt);
+    h.pad = (uint32_t)nxt;
+    if (pc < 0) h.flags |= HDR_NEG_EDGE;
+    return h;
+}
+
+// Second half (walker.py:282-288): weight update a/t = copysign(rowsum, a_e)
+// of the CURRENT row (walker.py:124-125), move, then the strict cutoff and
+// the step cap.  Returns true when the walk ended.
+__device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, long long e, const NodeHdr &nh, long long &tr) {
     if (e == PICK_LAST) {
-        L.w *= h.rsum;
+        L.w *= L.h.rsum;
     } else {
-        L.w *= (pc < 0) ? -h.rsum : h.rsum;
-        L.state = pc & 0x7fffffff;
+        L.w *= (nh.flags & HDR_NEG_EDGE) ? -L.h.rsum : L.h.rsum;
+        L.state = (int)nh.pad;
+        L.h = nh;
     }
     ++L.k;
     if (!(fabs(L.w) > L.thr)) return true;  // walker.py:286-288
@@ -173,13 +191,13 @@ __device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, const NodeHd
     return false;
 }
 
-// NW walks per lane, stepped together so their dependent loads overlap.
 template <int NW>
 struct WalkOcc {  // resident CTAs per SM the register budget is tuned for
     static constexpr int v = NW == 1 ? 5 : (NW == 2 ? 3 : 2);
 };
 
-template <bool REPLAY, int NW>
+// NW walks per lane, stepped together so their dependent loads overlap.
+template <bool REPLAY, bool FAT, int NW>
 __global__ void __launch_bounds__(256, WalkOcc<NW>::v) k_walk_action(WalkCommon a, double *__restrict__ xw) {
     const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
     Lane L[NW];
@@ -191,26 +209,22 @@ __global__ void __launch_bounds__(256, WalkOcc<NW>::v) k_walk_action(WalkCommon 
 #pragma unroll
         for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, we, L[s], n_walks);
         if (!more) break;
-        NodeHdr h[NW];
         long long e[NW];
-        int pc[NW];
-#pragma unroll
-        for (int s = 0; s < NW; ++s)
-            if (L[s].g >= 0) h[s] = load_hdr(a.hdr + L[s].state);
+        NodeHdr nh[NW];
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
             if (L[s].g < 0) continue;
-            L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, h[s].aux, L[s].x);  // q_c += zeta W r[l]
+            L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, L[s].h.aux, L[s].x);  // q_c += zeta W r[l]
             ++em;
-            e[s] = pick<REPLAY>(a, L[s], h[s], ab);
+            e[s] = pick<REPLAY>(a, L[s], ab);
         }
 #pragma unroll
         for (int s = 0; s < NW; ++s)
-            if (L[s].g >= 0 && e[s] >= 0) pc[s] = __ldg(a.ecol + e[s]);
+            if (L[s].g >= 0 && e[s] >= 0) nh[s] = fetch_next<FAT>(a, e[s]);
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
             if (L[s].g < 0) continue;
-            if (e[s] == PICK_END || apply(a, L[s], h[s], e[s], pc[s], tr)) {
+            if (e[s] == PICK_END || apply(a, L[s], e[s], nh[s], tr)) {
                 if (REPLAY && L[s].epos != L[s].eend) atomicOr(a.err, 4);
                 xw[L[s].g - wb] = L[s].x;
                 L[s].g = -1;
@@ -230,7 +244,7 @@ __global__ void __launch_bounds__(256, WalkOcc<NW>::v) k_walk_action(WalkCommon 
 // walk are marked -1.
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
-template <int MODE>
+template <int MODE, bool FAT>
 __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_len, long long off_base,
                                                    long long *__restrict__ eaux, int *__restrict__ est,
                                                    double *__restrict__ ewt) {
@@ -255,16 +269,16 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
                 scap = eaux[rel + 1] - sb;
             }
         }
-        NodeHdr h = load_hdr(a.hdr + L.state);
         if (MODE != EMIT_COUNT) {
             est[sb + L.k] = L.state;
             ewt[sb + L.k] = __ldg(a.zeta + L.k + 2) * L.w;
         }
         ++em;
         const long long emitted = L.k + 1;
-        const long long e = pick<REPLAY>(a, L, h, ab);
-        const int pc = e >= 0 ? __ldg(a.ecol + e) : 0;
-        if (e == PICK_END || apply(a, L, h, e, pc, tr)) {
+        const long long e = pick<REPLAY>(a, L, ab);
+        NodeHdr nh;
+        if (e >= 0) nh = fetch_next<FAT>(a, e);
+        if (e == PICK_END || apply(a, L, e, nh, tr)) {
             if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
             if (MODE == EMIT_COUNT) eaux[rel] = emitted;
             else
@@ -279,6 +293,12 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
 __global__ void k_set_aux(NodeHdr *__restrict__ hdr, const double *__restrict__ r, long long n) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) hdr[i].aux = r[i];
+}
+
+// fat layout: went[e].aux = r[target of e]
+__global__ void k_set_aux_fat(NodeHdr *__restrict__ went, const double *__restrict__ r, long long nnz) {
+    long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < nnz) went[e].aux = __ldg(r + went[e].pad);
 }
 
 // q[c] = sum of the per-walk contributions of column c, fixed order; optional
@@ -475,6 +495,7 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     int rc = build_blk_col(walk_pre, cb, ce, capacity, blk, s);
     if (rc) return rc;
     a.hdr = g->hdr;
+    a.went = g->went;
     a.ecol = g->ecol;
     a.cdf = g->cdf;
     a.zeta = p->zeta;
@@ -544,23 +565,22 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0 && mode != EMIT_COUNT;
     rc = timed_begin(g, timed, g->ev_walk, s);
     if (rc) return rc;
-    switch (mode) {
-        case EMIT_FIXED:
-            k_walk_emit<EMIT_FIXED><<<walk_grid(k_walk_emit<EMIT_FIXED>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt);
-            mcf::note_launch();
-            break;
-        case EMIT_REPLAY:
-            k_walk_emit<EMIT_REPLAY><<<walk_grid(k_walk_emit<EMIT_REPLAY>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt);
-            mcf::note_launch();
-            break;
-        case EMIT_COUNT:
-            k_walk_emit<EMIT_COUNT><<<walk_grid(k_walk_emit<EMIT_COUNT>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
-            mcf::note_launch();
-            break;
-        default:
-            k_walk_emit<EMIT_EXPLICIT><<<walk_grid(k_walk_emit<EMIT_EXPLICIT>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
-            mcf::note_launch();
+    if (g->went) {
+        switch (mode) {
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, true><<<walk_grid(k_walk_emit<EMIT_FIXED, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, true><<<walk_grid(k_walk_emit<EMIT_REPLAY, true>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, true><<<walk_grid(k_walk_emit<EMIT_COUNT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, true><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+        }
+    } else {
+        switch (mode) {
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false><<<walk_grid(k_walk_emit<EMIT_FIXED, false>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, false><<<walk_grid(k_walk_emit<EMIT_REPLAY, false>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false><<<walk_grid(k_walk_emit<EMIT_COUNT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, false><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+        }
     }
+    mcf::note_launch();
     MCF_LAUNCHED("k_walk_emit");
     rc = timed_end(timed, g->ev_walk, s);
     if (rc) return rc;
@@ -597,18 +617,34 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     a.entries = entries;
     k_set_aux<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, r, g->n);
     mcf::note_launch();
+    if (g->went) {
+        k_set_aux_fat<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>(g->went, r, g->nnz);
+        mcf::note_launch();
+    }
     MCF_LAUNCHED("k_set_aux");
     const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0;
     if (nw > 0) {
         rc = timed_begin(g, timed, g->ev_walk, s);
         if (rc) return rc;
-        if (replay) {
-            k_walk_action<true, 1><<<walk_grid(k_walk_action<true, 1>, 256, 0), 256, 0, s>>>(a, xw);
+        if (g->went) {
+            if (replay) {
+                k_walk_action<true, true, 1><<<walk_grid(k_walk_action<true, true, 1>, 256, 0), 256, 0, s>>>(a, xw);
+            } else {
+                switch (walks_per_lane()) {
+                    case 2: k_walk_action<false, true, 2><<<walk_grid(k_walk_action<false, true, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 4: k_walk_action<false, true, 4><<<walk_grid(k_walk_action<false, true, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    default: k_walk_action<false, true, 1><<<walk_grid(k_walk_action<false, true, 1>, 256, 0), 256, 0, s>>>(a, xw);
+                }
+            }
         } else {
-            switch (walks_per_lane()) {
-                case 1: k_walk_action<false, 1><<<walk_grid(k_walk_action<false, 1>, 256, 0), 256, 0, s>>>(a, xw); break;
-                case 4: k_walk_action<false, 4><<<walk_grid(k_walk_action<false, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
-                default: k_walk_action<false, 2><<<walk_grid(k_walk_action<false, 2>, 256, 0), 256, 0, s>>>(a, xw);
+            if (replay) {
+                k_walk_action<true, false, 1><<<walk_grid(k_walk_action<true, false, 1>, 256, 0), 256, 0, s>>>(a, xw);
+            } else {
+                switch (walks_per_lane()) {
+                    case 2: k_walk_action<false, false, 2><<<walk_grid(k_walk_action<false, false, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 4: k_walk_action<false, false, 4><<<walk_grid(k_walk_action<false, false, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    default: k_walk_action<false, false, 1><<<walk_grid(k_walk_action<false, false, 1>, 256, 0), 256, 0, s>>>(a, xw);
+                }
             }
         }
         mcf::note_launch();

@@ -42,6 +42,6 @@ def test_only_mcf_symbols_exported():
 def test_struct_layouts():
     # offsets must match the C structs in include/mcfunm_cuda.h
     assert ctypes.sizeof(_native.McfCsr) == 8 * 8
-    assert ctypes.sizeof(_native.McfGraphInfo) == 8 * 8
+    assert ctypes.sizeof(_native.McfGraphInfo) == 9 * 8
     assert _native.McfWalkParams.zeta.offset == 24 and _native.McfWalkParams.flags.offset == 40
     assert ctypes.sizeof(_native.McfWalkParams) == 48

@@ -16,6 +16,19 @@ pytestmark = pytest.mark.gpu
 REL = 1e-10  # replay tolerance stated by the north star
 
 
+@pytest.fixture(scope="module", params=["compact", "fat"])
+def layout(request):
+    """Both walk layouts (MCF_WALK_LAYOUT is read when a graph is built)."""
+    import os
+    old = os.environ.get("MCF_WALK_LAYOUT")
+    os.environ["MCF_WALK_LAYOUT"] = request.param
+    yield request.param
+    if old is None:
+        os.environ.pop("MCF_WALK_LAYOUT", None)
+    else:
+        os.environ["MCF_WALK_LAYOUT"] = old
+
+
 @pytest.fixture(scope="module")
 def mc():
     import torch
@@ -63,9 +76,10 @@ def test_device_allocation_bitwise(mc, name):
 
 
 @pytest.mark.parametrize("name", golden_io.CASES)
-def test_replay_matches_reference(mc, name):
+def test_replay_matches_reference(mc, layout, name):
     c = golden_io.load(name)
     g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
+    assert g.info["walk_layout"] == (1 if layout == "fat" else 0)
     for j, r in enumerate(c.runs):
         p = f"r{j}_"
         cfg = mc.WalkConfig(r["n_walks"], r["cutoff"], r["max_steps"], r["seed"])
@@ -171,6 +185,22 @@ def test_degenerate_and_argument_errors(mc):
         mc.subgraph_centrality(mc.SparseMatrix.from_dense([[0, 1], [0, 0]]), 0.1, mc.WalkConfig(10))
 
 
+def test_fat_and_compact_layouts_agree_bitwise(mc):
+    """The layout changes which memory a step reads, never the walk."""
+    import os
+    c = golden_io.load("ba400")
+    out = {}
+    for lay in ("compact", "fat"):
+        os.environ["MCF_WALK_LAYOUT"] = lay
+        g = mc.DeviceGraph(as_matrix(c.sa, True))
+        cfg = mc.WalkConfig(50_000, 1e-6, 28, 3)
+        out[lay] = (mc.rand_funm_action(g, mc.EXPONENTIAL, np.linspace(0, 1, c.n), cfg).values,
+                    mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values)
+    os.environ.pop("MCF_WALK_LAYOUT", None)
+    assert np.array_equal(out["compact"][0], out["fat"][0])
+    assert np.array_equal(out["compact"][1], out["fat"][1])
+
+
 def test_determinism_and_partition_invariance(mc):
     import torch
     c = golden_io.load("kron8")
@@ -202,7 +232,7 @@ def _z_check(z, n):
     assert abs(np.mean(z)) < 0.15 and 0.8 < np.std(z) < 1.2, (np.mean(z), np.std(z))
 
 
-def test_device_rng_action_statistics(mc):
+def test_device_rng_action_statistics(mc, layout):
     """Device RNG vs exact 30-term Taylor action (SURVEY.md §4 z-test recipe)."""
     c = golden_io.load("ba400")
     g = mc.DeviceGraph(as_matrix(c.sa, True))
@@ -224,7 +254,7 @@ def test_device_rng_diag_statistics(mc):
     assert abs(np.mean(z)) < 0.3
 
 
-def test_device_rng_weighted_signed_rows(mc):
+def test_device_rng_weighted_signed_rows(mc, layout):
     """Non-uniform rows (inverse-CDF path) and negative values (packed signs)."""
     c = golden_io.load("signed6")
     g = mc.DeviceGraph(as_matrix(c.sa))
