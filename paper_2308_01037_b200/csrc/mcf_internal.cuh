@@ -158,7 +158,7 @@ __device__ __forceinline__ NodeHdr load_hdr(const NodeHdr *h) {
     r.start = a.x;
     r.deg = a.y;
     r.flags = (uint32_t)a.z;
-    r.pad = 0;
+    r.pad = (uint32_t)a.w;
     r.rsum = __hiloint2double(b.y, b.x);
     r.aux = __hiloint2double(b.w, b.z);
     return r;

@@ -78,19 +78,42 @@ struct Lane {
     uint32_t r0, r1;       // second half of the Philox block (odd steps)
 };
 
-// Warp-aggregated refill of lanes that finished their walk.
+// Warp-level walk pool: a warp takes `chunk` consecutive walks from the
+// global counter at a time and hands them to its lanes as they finish, so the
+// single counter sees one atomic per chunk (a per-refill atomic serialised
+// short Katz walks on the counter's L2 slice).  pool/pool_end are warp-uniform.
+struct WarpPool {
+    long long next, end, chunk;
+};
+
+__device__ __forceinline__ WarpPool make_pool(long long nw_total) {
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    long long c = nw_total / (warps * 8);
+    c = c < 32 ? 32 : (c > 256 ? 256 : c);
+    return WarpPool{0, 0, c & ~31ll};
+}
+
 template <bool REPLAY>
-__device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long long we, Lane &L, long long &n_walks) {
-    unsigned need = __ballot_sync(MCF_FULL, L.g == -1);
+__device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long long we, Lane &L, long long &n_walks,
+                                       WarpPool &P) {
+    const unsigned need = __ballot_sync(MCF_FULL, L.g == -1);
     if (need) {
-        int lane = threadIdx.x & 31;
-        int leader = __ffs(need) - 1;
-        unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(a.counter, (unsigned long long)__popc(need));
-        base = __shfl_sync(MCF_FULL, base, leader);
+        const int rank = __popc(need & lanemask_lt());
+        const long long cnt = __popc(need);
+        const long long avail = P.end - P.next;
+        long long rel = P.next + rank;
+        if (cnt > avail) {  // pool runs dry: one atomic for the next chunk
+            unsigned long long base = 0;
+            if ((threadIdx.x & 31) == 0) base = atomicAdd(a.counter, (unsigned long long)P.chunk);
+            base = __shfl_sync(MCF_FULL, base, 0);
+            if (rank >= avail) rel = (long long)base + (rank - avail);
+            P.next = (long long)base + (cnt - avail);
+            P.end = (long long)base + P.chunk;
+        } else {
+            P.next += cnt;
+        }
         if (L.g == -1) {
-            long long rel = (long long)base + __popc(need & lanemask_lt());
-            long long g = wb + rel;
+            const long long g = wb + rel;
             if (g < we) {
                 int c = column_of_walk(g, rel, we - wb, a.walk_pre, a.blk_col, a.col_last);
                 long long pre = __ldg(a.walk_pre + c);
@@ -203,11 +226,12 @@ __global__ void __launch_bounds__(256, WalkOcc<NW>::v) k_walk_action(WalkCommon 
     Lane L[NW];
 #pragma unroll
     for (int s = 0; s < NW; ++s) L[s].g = -1;
+    WarpPool P = make_pool(we - wb);
     long long n_walks = 0, em = 0, tr = 0, ab = 0;
     while (true) {
         bool more = false;
 #pragma unroll
-        for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, we, L[s], n_walks);
+        for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, we, L[s], n_walks, P);
         if (!more) break;
         long long e[NW];
         NodeHdr nh[NW];
@@ -252,9 +276,10 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
     const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
     Lane L;
     L.g = -1;
+    WarpPool P = make_pool(we - wb);
     long long n_walks = 0, em = 0, tr = 0, ab = 0;
     long long sb = 0, scap = 0;
-    while (refill<REPLAY>(a, wb, we, L, n_walks)) {
+    while (refill<REPLAY>(a, wb, we, L, n_walks, P)) {
         if (L.g < 0) continue;
         const long long rel = L.g - wb;
         if (L.k == 0) {

@@ -28,6 +28,33 @@ __global__ void k_init(Rec *r, unsigned long long n, unsigned long long mult, un
     }
 }
 
+enum { LD_NC = 0, LD_CA = 1, LD_CG = 2, LD_CS = 3, LD_V4NC = 4, LD_V4CG = 5 };
+
+template <int MODE>
+__device__ __forceinline__ unsigned ld(const Rec *p) {
+    unsigned v;
+    if (MODE == LD_NC) return __ldg(&p->next);
+    if (MODE == LD_CA) asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(&p->next));
+    if (MODE == LD_CG) asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(&p->next));
+    if (MODE == LD_CS) asm volatile("ld.global.cs.u32 %0, [%1];" : "=r"(v) : "l"(&p->next));
+    if (MODE == LD_V4NC) { int4 a = __ldg(reinterpret_cast<const int4 *>(p)); int4 b = __ldg(reinterpret_cast<const int4 *>(p) + 1); v = a.x + b.w; }
+    if (MODE == LD_V4CG) {
+        int4 a, b;
+        asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p));
+        asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4+16];" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p));
+        v = a.x + b.w;
+    }
+    return v;
+}
+
+template <int MODE>
+__global__ void k_chain_mode(const Rec *r, unsigned long long n, int steps, unsigned *out) {
+    unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    unsigned p = (unsigned)(mix(t) & (n - 1));
+    for (int s = 0; s < steps; ++s) p = ld<MODE>(&r[p]) & (unsigned)(n - 1);
+    if (p == 0x12345678u) out[0] = p;
+}
+
 template <int K>
 __global__ void k_indep(const Rec *r, unsigned long long n, int iters, unsigned *out) {
     unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
@@ -100,6 +127,18 @@ int main() {
             double st = (double)th * steps;
             printf("%6llu MB chain thr/SM=%d: NW=1 %6.2f  NW=2 %6.2f  NW=4 %6.2f  G dependent loads/s\n", bytes >> 20,
                    occ, st / m1 / 1e6, 2 * st / m2 / 1e6, 4 * st / m4 / 1e6);
+        }
+        {
+            int th = sms * 2048, steps = 256;
+            double st = (double)th * steps;
+            float a0 = timeit([&] { k_chain_mode<LD_NC><<<th / 256, 256>>>(r, n, steps, out); });
+            float a1 = timeit([&] { k_chain_mode<LD_CA><<<th / 256, 256>>>(r, n, steps, out); });
+            float a2 = timeit([&] { k_chain_mode<LD_CG><<<th / 256, 256>>>(r, n, steps, out); });
+            float a3 = timeit([&] { k_chain_mode<LD_CS><<<th / 256, 256>>>(r, n, steps, out); });
+            float a4 = timeit([&] { k_chain_mode<LD_V4NC><<<th / 256, 256>>>(r, n, steps, out); });
+            float a5 = timeit([&] { k_chain_mode<LD_V4CG><<<th / 256, 256>>>(r, n, steps, out); });
+            printf("%6llu MB chain by load kind (G loads/s): nc %.2f  ca %.2f  cg %.2f  cs %.2f  2xv4.nc %.2f  2xv4.cg %.2f\n",
+                   bytes >> 20, st / a0 / 1e6, st / a1 / 1e6, st / a2 / 1e6, st / a3 / 1e6, st / a4 / 1e6, st / a5 / 1e6);
         }
         cudaFree(r);
     }
