@@ -37,7 +37,7 @@ struct WalkCommon {
     uint32_t key0, key1;
     const long long *__restrict__ walk_off;  // replay only
     const int *__restrict__ entries;          // replay only
-    unsigned long long *counter;
+    unsigned *counter;  // walks handed out (chunked, relative to the range start)
     long long *stats;
     int *err;
 };
@@ -53,8 +53,9 @@ __device__ __forceinline__ int cdf_pick(const double *__restrict__ cdf, int deg,
     return lo;
 }
 
-__device__ __forceinline__ void flush_stats(long long *stats, long long walks, long long em, long long tr,
-                                            long long ab) {
+__device__ __forceinline__ void flush_stats(long long *stats, unsigned walks_, unsigned em_, unsigned tr_,
+                                            unsigned ab_) {
+    long long walks = walks_, em = em_, tr = tr_, ab = ab_;
     walks = warp_sum_ll(walks);
     em = warp_sum_ll(em);
     tr = warp_sum_ll(tr);
@@ -69,13 +70,13 @@ __device__ __forceinline__ void flush_stats(long long *stats, long long walks, l
 
 // Walk state of one lane (one walk slot).
 struct Lane {
-    long long g;  // global walk index; -1 wants a walk, -2 no walks left
-    long long epos, eend;  // replay cursor
-    double w, thr, x;      // weight, cutoff threshold, per-walk accumulator
-    NodeHdr h;             // header of the current state (aux = r[state])
+    int rel;               // walk index relative to the range start; -1 wants a walk, -2 none left
+    int k, c;              // step, start column
     unsigned wl;           // walk index inside its column
-    int k, c, state;
+    double w, thr, x;      // weight, cutoff threshold, per-walk accumulator
+    NodeHdr h;             // header of the current state; h.pad = the state's node id
     uint32_t r0, r1;       // second half of the Philox block (odd steps)
+    long long epos, eend;  // replay cursor
 };
 
 // Warp-level walk pool: a warp takes `chunk` consecutive walks from the
@@ -83,47 +84,47 @@ struct Lane {
 // single counter sees one atomic per chunk (a per-refill atomic serialised
 // short Katz walks on the counter's L2 slice).  pool/pool_end are warp-uniform.
 struct WarpPool {
-    long long next, end, chunk;
+    int next, end, chunk;
 };
 
-__device__ __forceinline__ WarpPool make_pool(long long nw_total) {
-    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
-    long long c = nw_total / (warps * 8);
+__device__ __forceinline__ WarpPool make_pool(int nw_total) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    int c = nw_total / (warps * 8);
     c = c < 32 ? 32 : (c > 256 ? 256 : c);
-    return WarpPool{0, 0, c & ~31ll};
+    return WarpPool{0, 0, c & ~31};
 }
 
 template <bool REPLAY>
-__device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long long we, Lane &L, long long &n_walks,
+__device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, int nw, Lane &L, unsigned &n_walks,
                                        WarpPool &P) {
-    const unsigned need = __ballot_sync(MCF_FULL, L.g == -1);
+    const unsigned need = __ballot_sync(MCF_FULL, L.rel == -1);
     if (need) {
         const int rank = __popc(need & lanemask_lt());
-        const long long cnt = __popc(need);
-        const long long avail = P.end - P.next;
-        long long rel = P.next + rank;
+        const int cnt = __popc(need);
+        const int avail = P.end - P.next;
+        int rel = P.next + rank;
         if (cnt > avail) {  // pool runs dry: one atomic for the next chunk
-            unsigned long long base = 0;
-            if ((threadIdx.x & 31) == 0) base = atomicAdd(a.counter, (unsigned long long)P.chunk);
+            unsigned base = 0;
+            if ((threadIdx.x & 31) == 0) base = atomicAdd(a.counter, (unsigned)P.chunk);
             base = __shfl_sync(MCF_FULL, base, 0);
-            if (rank >= avail) rel = (long long)base + (rank - avail);
-            P.next = (long long)base + (cnt - avail);
-            P.end = (long long)base + P.chunk;
+            if (rank >= avail) rel = (int)base + (rank - avail);
+            P.next = (int)base + (cnt - avail);
+            P.end = (int)base + P.chunk;
         } else {
             P.next += cnt;
         }
-        if (L.g == -1) {
+        if (L.rel == -1) {
             const long long g = wb + rel;
-            if (g < we) {
-                int c = column_of_walk(g, rel, we - wb, a.walk_pre, a.blk_col, a.col_last);
+            if (rel < nw) {
+                int c = column_of_walk(g, rel, nw, a.walk_pre, a.blk_col, a.col_last);
                 long long pre = __ldg(a.walk_pre + c);
                 long long nc = __ldg(a.walk_pre + c + 1) - pre;
-                L.g = g;
+                L.rel = (int)rel;
                 L.c = c;
                 L.wl = (unsigned)(g - pre);
                 L.k = 0;
-                L.state = c;
                 L.h = load_hdr(a.hdr + c);
+                L.h.pad = (uint32_t)c;
                 L.w = 1.0 / (double)nc;       // W0 = 1/N_c (walker.py:263)
                 L.thr = a.cutoff * L.w;       // strict cutoff W_c * W0 (walker.py:264)
                 L.x = 0.0;
@@ -133,11 +134,11 @@ __device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, long l
                 }
                 ++n_walks;
             } else {
-                L.g = -2;
+                L.rel = -2;
             }
         }
     }
-    return !__all_sync(MCF_FULL, L.g == -2);
+    return !__all_sync(MCF_FULL, L.rel == -2);
 }
 
 constexpr long long PICK_END = -1;   // walk ends at this emission (absorbed, or bad replay stream)
@@ -147,7 +148,7 @@ constexpr long long PICK_LAST = -2;  // final draw: only |W| matters, and |a/t| 
 // the current row.  Philox-4x32-10 yields 128 bits per (step pair, walk,
 // column): even steps use the first 64, odd steps the second.
 template <bool REPLAY>
-__device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, long long &ab) {
+__device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned &ab) {
     const NodeHdr &h = L.h;
     if (h.deg == 0) {  // absorbing row (walker.py:274-278)
         ++ab;
@@ -197,12 +198,11 @@ __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) 
 // Second half (walker.py:282-288): weight update a/t = copysign(rowsum, a_e)
 // of the CURRENT row (walker.py:124-125), move, then the strict cutoff and
 // the step cap.  Returns true when the walk ended.
-__device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, long long e, const NodeHdr &nh, long long &tr) {
+__device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, long long e, const NodeHdr &nh, unsigned &tr) {
     if (e == PICK_LAST) {
         L.w *= L.h.rsum;
     } else {
         L.w *= (nh.flags & HDR_NEG_EDGE) ? -L.h.rsum : L.h.rsum;
-        L.state = (int)nh.pad;
         L.h = nh;
     }
     ++L.k;
@@ -214,44 +214,47 @@ __device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, long long e,
     return false;
 }
 
-template <int NW>
+template <int NW, int OCC>
 struct WalkOcc {  // resident CTAs per SM the register budget is tuned for
-    static constexpr int v = NW == 1 ? 5 : (NW == 2 ? 3 : 2);
+    static constexpr int v = NW == 1 ? OCC : (NW == 2 ? 3 : 2);
 };
 
 // NW walks per lane, stepped together so their dependent loads overlap.
-template <bool REPLAY, bool FAT, int NW>
-__global__ void __launch_bounds__(256, WalkOcc<NW>::v) k_walk_action(WalkCommon a, double *__restrict__ xw) {
-    const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
+// OCC: CTAs per SM the one-walk variant is register-tuned for (4: no spills,
+// 5: more warps with a few spilled registers).
+template <bool REPLAY, bool FAT, int NW, int OCC = 5>
+__global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(WalkCommon a, double *__restrict__ xw) {
+    const long long wb = __ldg(a.walk_pre + a.col_begin);
+    const int nw = (int)(__ldg(a.walk_pre + a.col_end) - wb);
     Lane L[NW];
 #pragma unroll
-    for (int s = 0; s < NW; ++s) L[s].g = -1;
-    WarpPool P = make_pool(we - wb);
-    long long n_walks = 0, em = 0, tr = 0, ab = 0;
+    for (int s = 0; s < NW; ++s) L[s].rel = -1;
+    WarpPool P = make_pool(nw);
+    unsigned n_walks = 0, em = 0, tr = 0, ab = 0;
     while (true) {
         bool more = false;
 #pragma unroll
-        for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, we, L[s], n_walks, P);
+        for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, nw, L[s], n_walks, P);
         if (!more) break;
         long long e[NW];
         NodeHdr nh[NW];
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
-            if (L[s].g < 0) continue;
+            if (L[s].rel < 0) continue;
             L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, L[s].h.aux, L[s].x);  // q_c += zeta W r[l]
             ++em;
             e[s] = pick<REPLAY>(a, L[s], ab);
         }
 #pragma unroll
         for (int s = 0; s < NW; ++s)
-            if (L[s].g >= 0 && e[s] >= 0) nh[s] = fetch_next<FAT>(a, e[s]);
+            if (L[s].rel >= 0 && e[s] >= 0) nh[s] = fetch_next<FAT>(a, e[s]);
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
-            if (L[s].g < 0) continue;
+            if (L[s].rel < 0) continue;
             if (e[s] == PICK_END || apply(a, L[s], e[s], nh[s], tr)) {
                 if (REPLAY && L[s].epos != L[s].eend) atomicOr(a.err, 4);
-                xw[L[s].g - wb] = L[s].x;
-                L[s].g = -1;
+                xw[L[s].rel] = L[s].x;
+                L[s].rel = -1;
             }
         }
     }
@@ -273,15 +276,16 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
                                                    long long *__restrict__ eaux, int *__restrict__ est,
                                                    double *__restrict__ ewt) {
     constexpr bool REPLAY = MODE == EMIT_REPLAY;
-    const long long wb = __ldg(a.walk_pre + a.col_begin), we = __ldg(a.walk_pre + a.col_end);
+    const long long wb = __ldg(a.walk_pre + a.col_begin);
+    const int nw = (int)(__ldg(a.walk_pre + a.col_end) - wb);
     Lane L;
-    L.g = -1;
-    WarpPool P = make_pool(we - wb);
-    long long n_walks = 0, em = 0, tr = 0, ab = 0;
+    L.rel = -1;
+    WarpPool P = make_pool(nw);
+    unsigned n_walks = 0, em = 0, tr = 0, ab = 0;
     long long sb = 0, scap = 0;
-    while (refill<REPLAY>(a, wb, we, L, n_walks, P)) {
-        if (L.g < 0) continue;
-        const long long rel = L.g - wb;
+    while (refill<REPLAY>(a, wb, nw, L, n_walks, P)) {
+        if (L.rel < 0) continue;
+        const long long rel = L.rel;
         if (L.k == 0) {
             if (MODE == EMIT_REPLAY) {
                 sb = L.epos - off_base + rel;
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
             }
         }
         if (MODE != EMIT_COUNT) {
-            est[sb + L.k] = L.state;
+            est[sb + L.k] = (int)L.h.pad;
             ewt[sb + L.k] = __ldg(a.zeta + L.k + 2) * L.w;
         }
         ++em;
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
             if (MODE == EMIT_COUNT) eaux[rel] = emitted;
             else
                 for (long long t = emitted; t < scap; ++t) est[sb + t] = -1;
-            L.g = -1;
+            L.rel = -1;
         }
     }
     if (MODE != EMIT_COUNT) flush_stats(a.stats, n_walks, em, tr, ab);
@@ -558,7 +562,7 @@ static int walks_per_lane() {
     if (!v) {
         const char *e = getenv("MCF_WALKS_PER_LANE");
         v = e ? atoi(e) : 1;
-        if (v != 2 && v != 4) v = 1;
+        if (v != 2 && v != 4 && v != 14) v = 1;  // 14 = one walk, 4 CTAs/SM
     }
     return v;
 }
@@ -579,7 +583,7 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     int *blk = nullptr;
     int rc = setup_common(g, p, walk_pre, cb, ce, nwalks, a, &blk, s);
     if (rc) return rc;
-    unsigned long long *counter = nullptr;
+    unsigned *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     a.counter = counter;
@@ -628,12 +632,13 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     if (rc) return rc;
     rc = setup_common(g, p, walk_pre, cb, ce, nw, a, &blk, s);
     if (rc) return rc;
+    MCF_ARG(nw < (1ll << 31) - 4096, "walks per call must be below 2^31 (split the column range)");
     double *xw = nullptr;
-    unsigned long long *counter = nullptr;
+    unsigned *counter = nullptr;
     int *err = nullptr;
     MCF_CUDA(cudaMallocAsync(&xw, sizeof(double) * (nw > 0 ? nw : 1), s));
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) + sizeof(int) * 2, s));
-    err = (int *)(counter + 1);
+    err = (int *)(counter + 2);
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
     a.counter = counter;
     a.err = err;
@@ -658,6 +663,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
                 switch (walks_per_lane()) {
                     case 2: k_walk_action<false, true, 2><<<walk_grid(k_walk_action<false, true, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 4: k_walk_action<false, true, 4><<<walk_grid(k_walk_action<false, true, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 14: k_walk_action<false, true, 1, 4><<<walk_grid(k_walk_action<false, true, 1, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     default: k_walk_action<false, true, 1><<<walk_grid(k_walk_action<false, true, 1>, 256, 0), 256, 0, s>>>(a, xw);
                 }
             }
@@ -668,6 +674,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
                 switch (walks_per_lane()) {
                     case 2: k_walk_action<false, false, 2><<<walk_grid(k_walk_action<false, false, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 4: k_walk_action<false, false, 4><<<walk_grid(k_walk_action<false, false, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 14: k_walk_action<false, false, 1, 4><<<walk_grid(k_walk_action<false, false, 1, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     default: k_walk_action<false, false, 1><<<walk_grid(k_walk_action<false, false, 1>, 256, 0), 256, 0, s>>>(a, xw);
                 }
             }
