@@ -555,14 +555,16 @@ int walk_capacity(const mcf_walk_params *p, const long long *walk_pre, long long
     return rc;
 }
 
-// walks stepped together per lane (MCF_WALKS_PER_LANE = 1, 2 or 4; default 1:
-// on the L2-resident config-2 graph the register cost of 2 or 4 slots loses)
+// walks stepped together per lane (MCF_WALKS_PER_LANE = 1, 2 or 4; 14 = one
+// walk at 4 CTAs/SM).  Measured on B200 (r01): one walk per lane at 4 CTAs/SM
+// is fastest on both the L2-resident config 2 and the HBM-bound config 4 --
+// the walk is bound by the random-sector rate, not by per-lane latency.
 static int walks_per_lane() {
     static int v = 0;
     if (!v) {
         const char *e = getenv("MCF_WALKS_PER_LANE");
-        v = e ? atoi(e) : 1;
-        if (v != 2 && v != 4 && v != 14) v = 1;  // 14 = one walk, 4 CTAs/SM
+        v = e ? atoi(e) : 14;
+        if (v != 1 && v != 2 && v != 4) v = 14;  // 14 = one walk, 4 CTAs/SM (no spills): best measured
     }
     return v;
 }
