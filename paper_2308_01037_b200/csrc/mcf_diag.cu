@@ -54,7 +54,7 @@ struct QArgs {
     long long col_begin, col_end;
     double *__restrict__ pcol;
     int *gkeys;
-    double *gvals;
+    long long *gvals;
     long long gcap;
     unsigned long long *counter;
 };
@@ -82,28 +82,39 @@ __device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key)
     }
 }
 
-__device__ __forceinline__ double lookup(const int *keys, const double *vals, uint32_t mask, int key) {
+__device__ __forceinline__ long long lookup(const int *keys, const long long *vals, uint32_t mask, int key) {
     uint32_t s = hash_slot(key, mask);
     while (true) {
         int k = keys[s];
         if (k == key) return vals[s];
-        if (k == EMPTY_KEY) return 0.0;
+        if (k == EMPTY_KEY) return 0;
         s = (s + 1) & mask;
     }
 }
 
+// Q_c is accumulated in fixed point: every weight is scaled by 2^E (E from the
+// column's largest |weight| and its emission count, so no sum can exceed
+// 2^62) and rounded to int64; integer adds commute, so Q_c -- and therefore d
+// -- does not depend on the order in which threads add (deterministic), and
+// plain shared-memory atomics replace any ordering barriers.  The quantum is
+// 2^-E <= 2^-61 * M * max|w| (M emissions), orders of magnitude below the
+// 1e-10 replay tolerance and the Monte Carlo error.
 __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *svals = reinterpret_cast<double *>(smem_raw);
+    long long *svals = reinterpret_cast<long long *>(smem_raw);
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     __shared__ long long s_col;
+    __shared__ unsigned long long s_maxbits;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
-    double *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
+    long long *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
 
     while (true) {
         __syncthreads();
-        if (tid == 0) s_col = a.col_begin + (long long)atomicAdd(a.counter, 1ull);
+        if (tid == 0) {
+            s_col = a.col_begin + (long long)atomicAdd(a.counter, 1ull);
+            s_maxbits = 0;
+        }
         __syncthreads();
         const long long c = s_col;
         if (c >= a.col_end) break;
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         uint32_t cap = 32;
         while ((long long)cap * 3 < need * 4 + 4) cap <<= 1;  // load factor <= 3/4
         int *keys;
-        double *vals;
+        long long *vals;
         if (cap <= (uint32_t)SCAP) {
             keys = skeys;
             vals = svals;
@@ -123,34 +134,31 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             vals = gvals;
         }
         const uint32_t mask = cap - 1;
+        // pass 1: clear the table, find max |w| over the column's emissions
+        double mx = 0.0;
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
             keys[t] = EMPTY_KEY;
-            vals[t] = 0.0;
+            vals[t] = 0;
+        }
+        for (long long i = tid; i < m; i += Q_THREADS)
+            if (a.est[s0 + i] >= 0) mx = fmax(mx, fabs(a.ewt[s0 + i]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(MCF_FULL, mx, o));
+        if (lane == 0 && mx > 0.0) atomicMax(&s_maxbits, (unsigned long long)__double_as_longlong(mx));
+        __syncthreads();
+        const double maxw = __longlong_as_double((long long)s_maxbits);
+        int lg_m = 0;
+        while ((1ll << lg_m) < m) ++lg_m;
+        const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // sum of m terms < 2^62
+        // pass 2: Q_c[j] += round(w 2^E)   (Alg. 2 line "q_{i l_k} += zeta W")
+        for (long long i = tid; i < m; i += Q_THREADS) {
+            const int s = a.est[s0 + i];
+            if (s < 0) continue;
+            const long long q = __double2ll_rn(ldexp(a.ewt[s0 + i], E));
+            const int slot = find_or_insert(keys, mask, s);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&vals[slot]), (unsigned long long)q);
         }
         __syncthreads();
-
-        // Q_c[j] += zeta_{k+2} W over visits (Alg. 2 line "q_{i l_k} += ...")
-        for (long long base = 0; base < m; base += Q_THREADS) {
-            long long i = base + tid;
-            int s = (i < m) ? a.est[s0 + i] : EMPTY_KEY;
-            double w = (s >= 0) ? a.ewt[s0 + i] : 0.0;
-            unsigned grp = __match_any_sync(MCF_FULL, s);
-            int leader = __ffs(grp) - 1;
-            double sum = w;
-            if (!__all_sync(MCF_FULL, __popc(grp) == 1)) {  // equal states in this warp: sum in lane order
-                sum = 0.0;
-                for (int src = 0; src < 32; ++src) {
-                    double o = __shfl_sync(MCF_FULL, w, src);
-                    if ((grp >> src) & 1u) sum += o;
-                }
-            }
-            int slot = -1;
-            if (s >= 0 && lane == leader) slot = find_or_insert(keys, mask, s);
-            for (int ph = 0; ph < Q_WARPS; ++ph) {  // warps add in index order -> fixed summation order
-                if (warp == ph && slot >= 0) vals[slot] += sum;
-                __syncthreads();
-            }
-        }
 
         // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
@@ -160,8 +168,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
             double acc = 0.0;
             for (long long e = ilo + lane; e < ihi; e += 32) {
-                double qv = lookup(keys, vals, mask, __ldg(a.csc_rows + e));
-                acc = fma(__ldg(a.csc_vals + e), qv, acc);
+                const long long qi = lookup(keys, vals, mask, __ldg(a.csc_rows + e));
+                acc = fma(__ldg(a.csc_vals + e), ldexp((double)qi, -E), acc);
             }
             acc = warp_sum(acc);
             if (lane == 0) a.pcol[cs + t] = aic * acc;
@@ -261,14 +269,14 @@ static int run_q(bool timed, mcf_graph *g, const long long *walk_pre, long long 
     if (cap > SCAP) {
         q.gcap = cap;
         MCF_CUDA(cudaMallocAsync(&gbuf, (size_t)grid * cap * (sizeof(int) + sizeof(double)), s));
-        q.gvals = reinterpret_cast<double *>(gbuf);
+        q.gvals = reinterpret_cast<long long *>(gbuf);
         q.gkeys = reinterpret_cast<int *>(q.gvals + (size_t)grid * cap);
     }
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     q.counter = counter;
-    size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(double));
+    size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(long long));
     MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;

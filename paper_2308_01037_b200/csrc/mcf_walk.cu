@@ -262,13 +262,15 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
 }
 
 // Diagonal-mode walks.  Slot layout of the emission buffer per MODE:
-//   EMIT_FIXED     walk rel owns slots [rel*L, rel*L + L)
+//   EMIT_FIXED     column c owns slots [(pre_c - wb) L, (pre_{c+1} - wb) L),
+//                  step-major inside: emission k of the column's walk w is at
+//                  + k N_c + w, so lanes holding consecutive walks write
+//                  consecutive addresses
 //   EMIT_REPLAY    walk g owns walk_off[g]-off_base+rel .. + draws+1
 //   EMIT_COUNT     no emission written; elen[rel] = number of emissions
 //   EMIT_EXPLICIT  walk rel owns [eoff[rel], eoff[rel+1]) (exclusive scan of a
 //                  previous EMIT_COUNT pass over the same Philox stream)
-// Each emission (state, zeta_{k+2} W_k) goes to slot sb + k; unused slots of a
-// walk are marked -1.
+// Each emission is (state, zeta_{k+2} W_k); unused slots of a walk hold -1.
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
 template <int MODE, bool FAT>
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
     L.rel = -1;
     WarpPool P = make_pool(nw);
     unsigned n_walks = 0, em = 0, tr = 0, ab = 0;
-    long long sb = 0, scap = 0;
+    long long sb = 0, scap = 0, stride = 1;
     while (refill<REPLAY>(a, wb, nw, L, n_walks, P)) {
         if (L.rel < 0) continue;
         const long long rel = L.rel;
@@ -291,7 +293,9 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
                 sb = L.epos - off_base + rel;
                 scap = L.eend - L.epos + 1;
             } else if (MODE == EMIT_FIXED) {
-                sb = rel * slot_len;
+                const long long pre = __ldg(a.walk_pre + L.c);
+                stride = __ldg(a.walk_pre + L.c + 1) - pre;
+                sb = (pre - wb) * slot_len + L.wl;
                 scap = slot_len;
             } else if (MODE == EMIT_EXPLICIT) {
                 sb = eaux[rel];
@@ -299,8 +303,8 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
             }
         }
         if (MODE != EMIT_COUNT) {
-            est[sb + L.k] = (int)L.h.pad;
-            ewt[sb + L.k] = __ldg(a.zeta + L.k + 2) * L.w;
+            est[sb + L.k * stride] = (int)L.h.pad;
+            ewt[sb + L.k * stride] = __ldg(a.zeta + L.k + 2) * L.w;
         }
         ++em;
         const long long emitted = L.k + 1;
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
             if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
             if (MODE == EMIT_COUNT) eaux[rel] = emitted;
             else
-                for (long long t = emitted; t < scap; ++t) est[sb + t] = -1;
+                for (long long t = emitted; t < scap; ++t) est[sb + t * stride] = -1;
             L.rel = -1;
         }
     }
