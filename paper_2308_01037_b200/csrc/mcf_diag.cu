@@ -25,8 +25,8 @@ namespace mcf {
 int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce);
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                      long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
-                     long long off_base, long long *eaux, int *est, double *ewt, long long *stats, int *err,
-                     cudaStream_t s);
+                     long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
+                     long long *stats, int *err, cudaStream_t s);
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
 }  // namespace mcf
@@ -53,6 +53,7 @@ struct QArgs {
     long long n;
     long long col_begin, col_end;
     double *__restrict__ pcol;
+    const unsigned long long *__restrict__ colmax;  // per-column max |weight| bits (from the walk kernel)
     int *gkeys;
     long long *gvals;
     long long gcap;
@@ -104,7 +105,6 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     long long *svals = reinterpret_cast<long long *>(smem_raw);
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     __shared__ long long s_col;
-    __shared__ unsigned long long s_maxbits;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
     long long *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
@@ -113,7 +113,6 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         __syncthreads();
         if (tid == 0) {
             s_col = a.col_begin + (long long)atomicAdd(a.counter, 1ull);
-            s_maxbits = 0;
         }
         __syncthreads();
         const long long c = s_col;
@@ -134,19 +133,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             vals = gvals;
         }
         const uint32_t mask = cap - 1;
-        // pass 1: clear the table, find max |w| over the column's emissions
-        double mx = 0.0;
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
             keys[t] = EMPTY_KEY;
             vals[t] = 0;
         }
-        for (long long i = tid; i < m; i += Q_THREADS)
-            if (a.est[s0 + i] >= 0) mx = fmax(mx, fabs(a.ewt[s0 + i]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(MCF_FULL, mx, o));
-        if (lane == 0 && mx > 0.0) atomicMax(&s_maxbits, (unsigned long long)__double_as_longlong(mx));
         __syncthreads();
-        const double maxw = __longlong_as_double((long long)s_maxbits);
+        const double maxw = __longlong_as_double((long long)a.colmax[c]);
         int lg_m = 0;
         while ((1ll << lg_m) < m) ++lg_m;
         const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // sum of m terms < 2^62
@@ -228,19 +220,20 @@ __global__ void k_max_walks(const long long *__restrict__ walk_pre, long long cb
     if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
 }
 
-// default emission-buffer budget (slots of 12 B): 2^28 -> 3 GiB
+// default emission-buffer budget (slots of 12 B): 2^30 -> 12 GiB of the 180 GB
 static long long emission_budget() {
     static long long v = 0;
     if (!v) {
         const char *e = getenv("MCF_EMISSION_SLOTS");
-        v = e ? atoll(e) : (1ll << 28);
+        v = e ? atoll(e) : (1ll << 30);
         if (v < (1ll << 16)) v = 1ll << 16;
     }
     return v;
 }
 
-static int run_q(bool timed, mcf_graph *g, const long long *walk_pre, long long cb, long long ce, long long wb, long long slot_len,
-                 const long long *eoff, const long long *walk_off, long long off_base, const int *est, const double *ewt, double *pcol,
+static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre, long long cb,
+                 long long ce, long long wb, long long slot_len, const long long *eoff, const long long *walk_off,
+                 long long off_base, const int *est, const double *ewt, double *pcol,
                  long long max_slots_per_col, cudaStream_t s) {
     QArgs q;
     q.walk_pre = walk_pre;
@@ -258,6 +251,7 @@ static int run_q(bool timed, mcf_graph *g, const long long *walk_pre, long long 
     q.col_begin = cb;
     q.col_end = ce;
     q.pcol = pcol;
+    q.colmax = colmax;
     q.gkeys = nullptr;
     q.gvals = nullptr;
     q.gcap = 0;
@@ -313,6 +307,9 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     unsigned long long hmax = 0;
     MCF_CUDA(cudaMemcpyAsync(&hmax, maxw, sizeof(hmax), cudaMemcpyDeviceToHost, s));
     MCF_CUDA(cudaStreamSynchronize(s));
+    unsigned long long *colmax = nullptr;  // per-column max |emission| for the fixed-point scale
+    MCF_CUDA(cudaMallocAsync(&colmax, sizeof(unsigned long long) * g->n, s));
+    MCF_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * g->n, s));
 
     if (replay) {
         long long hoff[2];
@@ -325,10 +322,10 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * slots, s));
         MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * slots, s));
         rc = launch_walk_emit(g, p, walk_pre, cb, ce, we - wb, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est, ewt,
-                              stats, err, s);
+                              colmax, stats, err, s);
         if (rc) return rc;
         // table size is bounded by min(slots, n) per column
-        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
+        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, colmax, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
         if (rc) return rc;
         int herr = 0;
         MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -336,6 +333,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         cudaFreeAsync(est, s);
         cudaFreeAsync(ewt, s);
         cudaFreeAsync(err, s);
+        cudaFreeAsync(colmax, s);
         if (herr) {
             set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) + ")");
             return MCF_ERR_ARGUMENT;
@@ -371,10 +369,10 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         if (rc) break;
         if (bw1 == bw0) continue;
         if (fixed) {
-            rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, stats,
-                                  err, s);
+            rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, colmax,
+                                  stats, err, s);
             if (rc) break;
-            rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
+            rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, colmax, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
             if (rc) break;
             continue;
         }
@@ -384,7 +382,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         MCF_CUDA(cudaMallocAsync(&elen, sizeof(long long) * (2 * nwb + 1), s));
         long long *eoff = elen + nwb;
         rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
-                              stats, err, s);
+                              nullptr, stats, err, s);
         if (rc) break;
         rc = exclusive_scan_i64(elen, eoff, nwb, s);
         if (rc) break;
@@ -398,14 +396,15 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
             MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * buf_slots, s));
             MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s));
         }
-        rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, stats,
-                              err, s);
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, colmax,
+                              stats, err, s);
         if (rc) break;
-        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
+        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, colmax, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
         cudaFreeAsync(elen, s);
         if (rc) break;
     }
     delete[] hb;
+    cudaFreeAsync(colmax, s);
     cudaFreeAsync(est, s);
     cudaFreeAsync(ewt, s);
     cudaFreeAsync(dbounds, s);

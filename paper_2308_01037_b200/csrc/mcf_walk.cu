@@ -38,6 +38,7 @@ struct WalkCommon {
     const long long *__restrict__ walk_off;  // replay only
     const int *__restrict__ entries;          // replay only
     unsigned *counter;  // walks handed out (chunked, relative to the range start)
+    unsigned long long *colmax;  // diag: per-column max |emission| (IEEE bits), or null
     long long *stats;
     int *err;
 };
@@ -285,10 +286,12 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
     WarpPool P = make_pool(nw);
     unsigned n_walks = 0, em = 0, tr = 0, ab = 0;
     long long sb = 0, scap = 0, stride = 1;
+    double wmax = 0.0;  // this walk's largest |emission| -> per-column max (fixed-point scale of k_diag_q)
     while (refill<REPLAY>(a, wb, nw, L, n_walks, P)) {
         if (L.rel < 0) continue;
         const long long rel = L.rel;
         if (L.k == 0) {
+            wmax = 0.0;
             if (MODE == EMIT_REPLAY) {
                 sb = L.epos - off_base + rel;
                 scap = L.eend - L.epos + 1;
@@ -303,8 +306,10 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
             }
         }
         if (MODE != EMIT_COUNT) {
+            const double om = __ldg(a.zeta + L.k + 2) * L.w;
             est[sb + L.k * stride] = (int)L.h.pad;
-            ewt[sb + L.k * stride] = __ldg(a.zeta + L.k + 2) * L.w;
+            ewt[sb + L.k * stride] = om;
+            wmax = fmax(wmax, fabs(om));
         }
         ++em;
         const long long emitted = L.k + 1;
@@ -313,9 +318,12 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
         if (e >= 0) nh = fetch_next<FAT>(a, e);
         if (e == PICK_END || apply(a, L, e, nh, tr)) {
             if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
-            if (MODE == EMIT_COUNT) eaux[rel] = emitted;
-            else
+            if (MODE == EMIT_COUNT) {
+                eaux[rel] = emitted;
+            } else {
                 for (long long t = emitted; t < scap; ++t) est[sb + t * stride] = -1;
+                if (wmax > 0.0) atomicMax(a.colmax + L.c, (unsigned long long)__double_as_longlong(wmax));
+            }
             L.rel = -1;
         }
     }
@@ -543,6 +551,7 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.key1 = (uint32_t)(p->seed >> 32);
     a.walk_off = nullptr;
     a.entries = nullptr;
+    a.colmax = nullptr;
     return MCF_OK;
 }
 
@@ -583,8 +592,8 @@ int walk_grid(K kernel, int threads, size_t smem) {
 
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                      long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
-                     long long off_base, long long *eaux, int *est, double *ewt, long long *stats, int *err,
-                     cudaStream_t s) {
+                     long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
+                     long long *stats, int *err, cudaStream_t s) {
     WalkCommon a;
     int *blk = nullptr;
     int rc = setup_common(g, p, walk_pre, cb, ce, nwalks, a, &blk, s);
@@ -597,6 +606,7 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     a.stats = stats;
     a.walk_off = walk_off;
     a.entries = entries;
+    a.colmax = colmax;
     const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0 && mode != EMIT_COUNT;
     rc = timed_begin(g, timed, g->ev_walk, s);
     if (rc) return rc;
