@@ -143,12 +143,23 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         while ((1ll << lg_m) < m) ++lg_m;
         const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // sum of m terms < 2^62
         // pass 2: Q_c[j] += round(w 2^E)   (Alg. 2 line "q_{i l_k} += zeta W")
-        for (long long i = tid; i < m; i += Q_THREADS) {
-            const int s = a.est[s0 + i];
-            if (s < 0) continue;
-            const long long q = __double2ll_rn(ldexp(a.ewt[s0 + i], E));
-            const int slot = find_or_insert(keys, mask, s);
-            atomicAdd(reinterpret_cast<unsigned long long *>(&vals[slot]), (unsigned long long)q);
+        constexpr int U = 4;  // emissions in flight per thread (streaming loads ahead of the smem work)
+        for (long long base = 0; base < m; base += (long long)U * Q_THREADS) {
+            int sv[U];
+            double wv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long i = base + (long long)u * Q_THREADS + tid;
+                sv[u] = i < m ? __ldcs(a.est + s0 + i) : EMPTY_KEY;
+                wv[u] = i < m ? __ldcs(a.ewt + s0 + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (sv[u] < 0) continue;
+                const long long q = __double2ll_rn(ldexp(wv[u], E));
+                const int slot = find_or_insert(keys, mask, sv[u]);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&vals[slot]), (unsigned long long)q);
+            }
         }
         __syncthreads();
 
