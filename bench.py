@@ -40,6 +40,12 @@ CONFIGS = {
     1: dict(workload="config1: subgraph centrality diag(exp(beta A)), Erdos-Renyi n=1e4 mean degree 8 (LCC), "
                      "beta=1/lambda_max, 30 Taylor terms, 1000 walks per node",
             kind="diag", graph="er", n=10_000, deg=8, walks_per_node=1000, max_steps=28, cutoff=1e-300, seed=0),
+    3: dict(workload="config3: subgraph centrality diag(exp(beta A)), symmetrised R-MAT scale 22 edge factor 16 "
+                     "(.57,.19,.19,.05), no loops/duplicates, beta=1/lambda_max, 25 Taylor terms, 200 walks per node",
+            kind="diag", graph="rmat", scale=22, ef=16, walks_per_node=200, max_steps=23, cutoff=1e-300, seed=0),
+    5: dict(workload="config5: subgraph centrality diag(exp(beta A)), Chung-Lu n=1.6e7 exponent 2.1 mean degree 20 "
+                     "max degree 1e5, beta=1/lambda_max, 25 Taylor terms, 100 walks per node",
+            kind="diag", graph="chunglu", n=16_000_000, walks_per_node=100, max_steps=23, cutoff=1e-300, seed=0),
     4: dict(workload="config4: Katz resolvent (I - gamma A)^-1 1, symmetrised R-MAT scale 24 edge factor 16 "
                      "(.57,.19,.19,.05), no loops/duplicates, gamma=0.85/lambda_max, W_c=1e-8, 100 walks per node",
             kind="action", graph="rmat", scale=24, ef=16, walks_per_node=100, max_steps=10_000, cutoff=1e-8, seed=0,
@@ -56,12 +62,15 @@ def make_graph(cfg, pinned=False, scale=None):
     gamma) and N_s.  R-MAT configs are generated on the GPU and copied to
     pinned host memory once (setup, untimed)."""
     from paper_2308_01037_b200 import graphs
-    if cfg["graph"] == "rmat":
+    if cfg["graph"] in ("rmat", "chunglu"):
         import torch
         from paper_2308_01037_b200.device import DeviceGraph
         from paper_2308_01037_b200.sparsemat import SparseMatrix
-        sc = scale or cfg["scale"]
-        n, rp, ci = graphs.rmat_device(sc, cfg["ef"], seed=cfg["seed"])
+        sc = scale or cfg.get("scale")
+        if cfg["graph"] == "rmat":
+            n, rp, ci = graphs.rmat_device(sc, cfg["ef"], seed=cfg["seed"])
+        else:
+            n, rp, ci = graphs.chung_lu_device(cfg["n"], seed=cfg["seed"])
         g1 = DeviceGraph.from_device_arrays(n, rp, ci, torch.ones(ci.numel(), dtype=torch.float64, device=rp.device))
         lam = graphs.lambda_max_device(g1)
         g1.close()
@@ -70,7 +79,7 @@ def make_graph(cfg, pinned=False, scale=None):
         host[1].copy_(ci)
         vals = torch.ones(ci.numel(), dtype=torch.float64, pin_memory=True)
         a = SparseMatrix.from_csr_arrays(n, host[0].numpy(), host[1].numpy(), vals.numpy(), symmetric_hint=True,
-                                         meta={"generator": "rmat", "scale": sc, "lambda_max": lam})
+                                         meta={"generator": cfg["graph"], "scale": sc, "lambda_max": lam})
         a._pinned = (host, vals)
         del rp, ci
         torch.cuda.empty_cache()
@@ -233,7 +242,7 @@ def run_reference(args, cfg):
     if rank != 0:
         return 0
     a, beta, n_walks = make_graph(cfg)
-    if cfg["graph"] == "rmat":
+    if cfg["graph"] in ("rmat", "chunglu"):
         print(json.dumps({"impl": "reference", "unavailable": "the reference CPU algorithm needs ~80 GB of host RAM "
                                                               "for this R-MAT graph's numpy tables"}), flush=True)
         return 0
@@ -435,9 +444,9 @@ def run_device(args, cfg):
 
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     cpu = None
-    if cfg["graph"] == "rmat":
+    if cfg["graph"] in ("rmat", "chunglu"):
         cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": "not run: the oracle's numpy tables for this graph need ~80 GB of host RAM (SURVEY §8c)"}
+               "sample": "not run: the oracle's numpy tables for this graph need tens of GB of host RAM (SURVEY §8c)"}
     elif rank == 0 and world == 1 and not args.no_cpu:
         cb = CpuBaseline(a, beta, n_walks, cfg)
         em, wall, k = cb.run(args.cpu_seconds)

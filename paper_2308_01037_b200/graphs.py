@@ -146,3 +146,53 @@ def lambda_max_device(g, iters: int = 300) -> float:
         x, y = y / torch.linalg.norm(y), x
     g.spmv(x, out=y)
     return float((x @ y) / (x @ x))
+
+
+def chung_lu_device(n: int, exponent: float = 2.1, mean_degree: float = 20.0, max_degree: float = 1e5,
+                    seed: int = 0, device="cuda", chunk: int = 1 << 26):
+    """Chung-Lu power-law graph on the GPU (BASELINE config 5): expected
+    degrees w_i from a truncated Pareto(exponent) on [w_min, max_degree] with
+    w_min solved for the requested mean (deterministic quantiles, hubs first),
+    n*mean/2 edges with both endpoints drawn proportionally to w, then both
+    directions, loops and duplicates removed.  Returns (n, row_ptr, col_ids)."""
+    import math
+
+    import torch
+    a = exponent - 1.0
+
+    def weights(wmin):
+        u = (torch.arange(n, dtype=torch.float64, device=device) + 0.5) / n
+        r = (wmin / max_degree) ** a
+        return wmin * (1.0 - u * (1.0 - r)) ** (-1.0 / a)
+
+    lo, hi = 1e-3, mean_degree
+    for _ in range(60):  # bisection on w_min for the mean degree
+        mid = 0.5 * (lo + hi)
+        if float(weights(mid).mean()) < mean_degree:
+            lo = mid
+        else:
+            hi = mid
+    w = torch.flip(weights(0.5 * (lo + hi)), [0])  # node 0 = largest expected degree
+    cdf = torch.cumsum(w, 0)
+    cdf /= cdf[-1].clone()
+    m = int(round(n * mean_degree / 2))
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    scale = int(math.ceil(math.log2(n)))
+    keys = []
+    for lo_ in range(0, m, chunk):
+        k = min(chunk, m - lo_)
+        u = torch.searchsorted(cdf, torch.rand(k, generator=gen, dtype=torch.float64, device=device)).clamp_(max=n - 1)
+        v = torch.searchsorted(cdf, torch.rand(k, generator=gen, dtype=torch.float64, device=device)).clamp_(max=n - 1)
+        keep = u != v
+        u, v = u[keep], v[keep]
+        keys.append((u << scale) | v)
+        keys.append((v << scale) | u)
+    kk = torch.unique(torch.cat(keys), sorted=True)
+    del keys
+    rows = kk >> scale
+    cols = (kk & ((1 << scale) - 1)).to(torch.int32)
+    counts = torch.bincount(rows, minlength=n)
+    row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=row_ptr[1:])
+    return n, row_ptr, cols
