@@ -36,6 +36,7 @@ namespace mcf {
 constexpr int Q_THREADS = 512;
 constexpr int Q_WARPS = Q_THREADS / 32;
 constexpr int SCAP = 16384;  // shared table slots: 16384 * (4 + 8) B = 192 KB
+constexpr int FILTER_WORDS = 8192;  // 32 KB Bloom filter (262144 bits) in front of every combine lookup
 constexpr int EMPTY_KEY = -1;
 
 struct QArgs {
@@ -53,6 +54,8 @@ struct QArgs {
     long long n;
     long long col_begin, col_end;
     double *__restrict__ pcol;
+    int uniform;   // every stored value equals `value`: the combine skips csc_vals
+    double value;
     const unsigned long long *__restrict__ colmax;  // per-column max |weight| bits (from the walk kernel)
     int *gkeys;
     long long *gvals;
@@ -83,15 +86,20 @@ __device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key)
     }
 }
 
-__device__ __forceinline__ long long lookup(const int *keys, const long long *vals, uint32_t mask, int key) {
+__device__ __forceinline__ double lookup(const int *keys, const double *vals, uint32_t mask, int key) {
     uint32_t s = hash_slot(key, mask);
     while (true) {
         int k = keys[s];
         if (k == key) return vals[s];
-        if (k == EMPTY_KEY) return 0;
+        if (k == EMPTY_KEY) return 0.0;
         s = (s + 1) & mask;
     }
 }
+
+// Bloom bit of a key (independent of the table hash).  Most combine lookups
+// miss (C_i entries no walk from c visited): the filter answers them with one
+// shared-memory word instead of a linear-probing chain.
+__device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key * 0x85EBCA6Bu) >> 14; }
 
 // Q_c is accumulated in fixed point: every weight is scaled by 2^E (E from the
 // column's largest |weight| and its emission count, so no sum can exceed
@@ -104,6 +112,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     long long *svals = reinterpret_cast<long long *>(smem_raw);
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
+    unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
     __shared__ long long s_col;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
@@ -162,20 +171,37 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             }
         }
         __syncthreads();
+        // fixed point -> double in place, and the Bloom filter of the keys
+        double *qv = reinterpret_cast<double *>(vals);
+        for (int t = tid; t < FILTER_WORDS; t += Q_THREADS) filt[t] = 0u;
+        __syncthreads();
+        for (uint32_t t = tid; t < cap; t += Q_THREADS) {
+            const int key = keys[t];
+            if (key != EMPTY_KEY) {
+                qv[t] = ldexp((double)vals[t], -E);
+                const uint32_t b = filter_bit(key);
+                atomicOr(&filt[b >> 5], 1u << (b & 31));
+            }
+        }
+        __syncthreads();
 
         // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
         for (long long t = warp; t < cn; t += Q_WARPS) {
-            int i = a.csc_rows[cs + t];
-            double aic = a.csc_vals[cs + t];
-            long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+            const int i = a.csc_rows[cs + t];
+            const double aic = a.csc_vals[cs + t];
+            const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
             double acc = 0.0;
             for (long long e = ilo + lane; e < ihi; e += 32) {
-                const long long qi = lookup(keys, vals, mask, __ldg(a.csc_rows + e));
-                acc = fma(__ldg(a.csc_vals + e), ldexp((double)qi, -E), acc);
+                const int j = __ldg(a.csc_rows + e);
+                const uint32_t b = filter_bit(j);
+                if (filt[b >> 5] & (1u << (b & 31))) {
+                    const double qj = lookup(keys, qv, mask, j);
+                    acc = a.uniform ? acc + qj : fma(__ldg(a.csc_vals + e), qj, acc);
+                }
             }
             acc = warp_sum(acc);
-            if (lane == 0) a.pcol[cs + t] = aic * acc;
+            if (lane == 0) a.pcol[cs + t] = aic * (a.uniform ? a.value * acc : acc);
         }
     }
 }
@@ -262,6 +288,8 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.col_begin = cb;
     q.col_end = ce;
     q.pcol = pcol;
+    q.uniform = g->uniform_value ? 1 : 0;
+    q.value = g->value;
     q.colmax = colmax;
     q.gkeys = nullptr;
     q.gvals = nullptr;
@@ -281,7 +309,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     q.counter = counter;
-    size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(long long));
+    size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(long long)) + FILTER_WORDS * sizeof(unsigned);
     MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
