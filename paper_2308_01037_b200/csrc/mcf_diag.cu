@@ -61,7 +61,24 @@ struct QArgs {
     long long *gvals;
     long long gcap;
     unsigned long long *counter;
+    // big columns (combine work > BIG_WORK probes): Q_c handed to k_diag_big
+    struct BigRec *big;         // records
+    unsigned *n_big;            // record counter
+    unsigned max_big;
+    int *pool_keys;             // persisted tables
+    double *pool_vals;
+    unsigned long long *pool_used, pool_cap;
+    unsigned *pool_filt;        // FILTER_WORDS per record
 };
+
+struct BigRec {
+    long long c;      // column
+    long long off;    // table offset in the pool
+    unsigned cap;     // table slots (power of two)
+    unsigned cn;      // entries of C_c
+};
+
+constexpr long long BIG_WORK = 1ll << 20;  // combine probes above which a column's Q_c is shared GPU-wide
 
 __device__ __forceinline__ long long slot_of(const QArgs &a, long long g) {
     if (a.slot_len > 0) return (g - a.wb) * a.slot_len;
@@ -113,7 +130,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     long long *svals = reinterpret_cast<long long *>(smem_raw);
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
-    __shared__ long long s_col;
+    __shared__ long long s_col, s_work, s_slot, s_off;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
     long long *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
@@ -185,8 +202,45 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         }
         __syncthreads();
 
-        // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
+        // combine work of this column: sum of deg(i) over the entries (i, c)
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        long long work = 0;
+        for (long long t = tid; t < cn; t += Q_THREADS) {
+            const int i = a.csc_rows[cs + t];
+            work += a.csc_ptr[i + 1] - a.csc_ptr[i];
+        }
+        work = warp_sum_ll(work);
+        if (tid == 0) s_work = 0;
+        __syncthreads();
+        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_work), (unsigned long long)work);
+        __syncthreads();
+        if (s_work > BIG_WORK && a.big) {
+            // hand Q_c to k_diag_big: all warps of the GPU share the combine
+            if (tid == 0) {
+                s_slot = -1;
+                const unsigned long long off = atomicAdd(a.pool_used, (unsigned long long)cap);
+                if (off + cap <= a.pool_cap) {
+                    const unsigned r = atomicAdd(a.n_big, 1u);
+                    if (r < a.max_big) {
+                        a.big[r] = BigRec{c, (long long)off, cap, (unsigned)cn};
+                        s_slot = (long long)r;
+                        s_off = (long long)off;
+                    }
+                }
+            }
+            __syncthreads();
+            if (s_slot >= 0) {
+                for (uint32_t t = tid; t < cap; t += Q_THREADS) {
+                    a.pool_keys[s_off + t] = keys[t];
+                    a.pool_vals[s_off + t] = qv[t];
+                }
+                for (int t = tid; t < FILTER_WORDS; t += Q_THREADS)
+                    a.pool_filt[s_slot * FILTER_WORDS + t] = filt[t];
+                continue;  // the loop-top barrier orders these copies before the table is reused
+            }
+        }
+
+        // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
         for (long long t = warp; t < cn; t += Q_WARPS) {
             const int i = a.csc_rows[cs + t];
             const double aic = a.csc_vals[cs + t];
@@ -204,6 +258,49 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             if (lane == 0) a.pcol[cs + t] = aic * (a.uniform ? a.value * acc : acc);
         }
     }
+}
+
+// Combine of the big columns: the (column, entry) pairs of all records are
+// flattened (prefix over cn) and spread over every warp of the GPU; each pair
+// is still reduced by one warp in a fixed order.
+__global__ void __launch_bounds__(256) k_diag_big(QArgs a, const long long *__restrict__ item_pre, unsigned nrec) {
+    const int lane = threadIdx.x & 31;
+    const long long total = item_pre[nrec];
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long x = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < total; x += nw) {
+        unsigned lo = 0, hi = nrec - 1;  // record b with item_pre[b] <= x < item_pre[b+1]
+        while (lo < hi) {
+            const unsigned mid = (lo + hi + 1) >> 1;
+            if (item_pre[mid] <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        const BigRec r = a.big[lo];
+        const long long t = x - item_pre[lo];
+        const int *keys = a.pool_keys + r.off;
+        const double *qv = a.pool_vals + r.off;
+        const unsigned *filt = a.pool_filt + (long long)lo * FILTER_WORDS;
+        const uint32_t mask = r.cap - 1;
+        const long long cs = a.csc_ptr[r.c];
+        const int i = a.csc_rows[cs + t];
+        const double aic = a.csc_vals[cs + t];
+        const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+        double acc = 0.0;
+        for (long long e = ilo + lane; e < ihi; e += 32) {
+            const int j = __ldg(a.csc_rows + e);
+            const uint32_t b = filter_bit(j);
+            if (__ldg(filt + (b >> 5)) & (1u << (b & 31))) {
+                const double qj = lookup(keys, qv, mask, j);
+                acc = a.uniform ? acc + qj : fma(__ldg(a.csc_vals + e), qj, acc);
+            }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) a.pcol[cs + t] = aic * (a.uniform ? a.value * acc : acc);
+    }
+}
+
+__global__ void k_big_counts(const BigRec *__restrict__ big, unsigned nrec, long long *__restrict__ cnt) {
+    unsigned b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nrec) cnt[b] = big[b].cn;
 }
 
 // d_i = zeta_0 + zeta_1 a_ii + sum over row i of pcol[csr2csc[e]] (4 lanes per row)
@@ -306,9 +403,30 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.gkeys = reinterpret_cast<int *>(q.gvals + (size_t)grid * cap);
     }
     unsigned long long *counter = nullptr;
-    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
-    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));
+    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) * 4, s));
     q.counter = counter;
+    q.n_big = reinterpret_cast<unsigned *>(counter + 1);
+    q.pool_used = counter + 2;
+    // pool for the tables of big columns (shared GPU-wide by k_diag_big)
+    const unsigned max_big = 32768;
+    const unsigned long long pool_cap = 1ull << 27;  // 1.5 GiB of (key, value) slots
+    unsigned char *pool = nullptr;
+    if (cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(double)) + (size_t)max_big * FILTER_WORDS * 4 +
+                                       sizeof(BigRec) * max_big,
+                        s) == cudaSuccess) {
+        q.pool_vals = reinterpret_cast<double *>(pool);
+        q.pool_keys = reinterpret_cast<int *>(q.pool_vals + pool_cap);
+        q.pool_filt = reinterpret_cast<unsigned *>(q.pool_keys + pool_cap);
+        q.big = reinterpret_cast<BigRec *>(q.pool_filt + (size_t)max_big * FILTER_WORDS);
+        q.max_big = max_big;
+        q.pool_cap = pool_cap;
+    } else {
+        cudaGetLastError();
+        q.big = nullptr;
+        q.max_big = 0;
+        q.pool_cap = 0;
+    }
     size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(long long)) + FILTER_WORDS * sizeof(unsigned);
     MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int rc = timed_begin(g, timed, g->ev_q, s);
@@ -316,6 +434,25 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
     mcf::note_launch();
     MCF_LAUNCHED("k_diag_q");
+    if (q.big) {
+        unsigned nrec = 0;
+        MCF_CUDA(cudaMemcpyAsync(&nrec, q.n_big, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        if (nrec > max_big) nrec = max_big;
+        if (nrec > 0) {
+            long long *cnt = nullptr;
+            MCF_CUDA(cudaMallocAsync(&cnt, sizeof(long long) * (2 * (size_t)nrec + 1), s));
+            k_big_counts<<<(nrec + 255) / 256, 256, 0, s>>>(q.big, nrec, cnt);
+            mcf::note_launch();
+            rc = exclusive_scan_i64(cnt, cnt + nrec, nrec, s);
+            if (rc) return rc;
+            k_diag_big<<<sm_count() * 8, 256, 0, s>>>(q, cnt + nrec, nrec);
+            mcf::note_launch();
+            MCF_LAUNCHED("k_diag_big");
+            cudaFreeAsync(cnt, s);
+        }
+        cudaFreeAsync(pool, s);
+    }
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
     cudaFreeAsync(counter, s);
