@@ -86,8 +86,11 @@ __device__ __forceinline__ long long slot_of(const QArgs &a, long long g) {
     return a.walk_off[g] - a.off_base + (g - a.wb);
 }
 
+// Fibonacci hashing: the HIGH bits of key * 2^32/phi (the low bits of the
+// product depend only on the key's low bits, so keys equal mod the table size
+// would share a probe chain).  mask = cap - 1, cap a power of two >= 32.
 __device__ __forceinline__ uint32_t hash_slot(int key, uint32_t mask) {
-    return ((uint32_t)key * 0x9E3779B1u) & mask;
+    return (uint32_t)(((uint64_t)((uint32_t)key * 0x9E3779B1u) * (uint64_t)(mask + 1)) >> 32);
 }
 
 __device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key) {
@@ -148,7 +151,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         const long long s0 = slot_of(a, g0), m = slot_of(a, g1) - s0;
         long long need = m < a.n ? m : a.n;
         uint32_t cap = 32;
-        while ((long long)cap * 3 < need * 4 + 4) cap <<= 1;  // load factor <= 3/4
+        while ((long long)cap < need * 2 && cap < (uint32_t)SCAP) cap <<= 1;  // load factor <= 1/2 if it fits smem
+        while ((long long)cap * 3 < need * 4 + 4) cap <<= 1;                 // and <= 3/4 always
         int *keys;
         long long *vals;
         if (cap <= (uint32_t)SCAP) {
