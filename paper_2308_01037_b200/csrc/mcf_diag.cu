@@ -33,7 +33,7 @@ enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
 namespace mcf {
 
-constexpr int Q_THREADS = 512;
+constexpr int Q_THREADS = 1024;  // one CTA per SM (the 224-KB table): 32 warps hide the combine's latency
 constexpr int Q_WARPS = Q_THREADS / 32;
 constexpr int SCAP = 16384;  // shared table slots: 16384 * (4 + 8) B = 192 KB
 constexpr int FILTER_WORDS = 8192;  // 32 KB Bloom filter (262144 bits) in front of every combine lookup
@@ -250,7 +250,20 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             const double aic = a.csc_vals[cs + t];
             const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
             double acc = 0.0;
-            for (long long e = ilo + lane; e < ihi; e += 32) {
+            long long e = ilo + lane;
+            for (; e + 32 < ihi; e += 64) {  // two row ids in flight per lane
+                const int j0 = __ldg(a.csc_rows + e), j1 = __ldg(a.csc_rows + e + 32);
+                const uint32_t b0 = filter_bit(j0), b1 = filter_bit(j1);
+                if (filt[b0 >> 5] & (1u << (b0 & 31))) {
+                    const double q0 = lookup(keys, qv, mask, j0);
+                    acc = a.uniform ? acc + q0 : fma(__ldg(a.csc_vals + e), q0, acc);
+                }
+                if (filt[b1 >> 5] & (1u << (b1 & 31))) {
+                    const double q1 = lookup(keys, qv, mask, j1);
+                    acc = a.uniform ? acc + q1 : fma(__ldg(a.csc_vals + e + 32), q1, acc);
+                }
+            }
+            if (e < ihi) {
                 const int j = __ldg(a.csc_rows + e);
                 const uint32_t b = filter_bit(j);
                 if (filt[b >> 5] & (1u << (b & 31))) {
