@@ -5,6 +5,7 @@
 //           permutation of 32-B records (a walk step is such a dependency)
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/gups tools/gups.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -101,7 +102,14 @@ float timeit(F f) {
     return ms;
 }
 
-int main() {
+int main(int argc, char **argv) {
+    if (argc > 1) {  // L2 fetch granularity hint in bytes (32, 64, 128)
+        size_t gran = (size_t)atoi(argv[1]);
+        cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+        size_t got = 0;
+        cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+        printf("L2 fetch granularity: requested %zu -> %s, now %zu\n", gran, cudaGetErrorString(e), got);
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     unsigned *out;
