@@ -403,8 +403,11 @@ def run_device(args, cfg):
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "bytes_per_step": BYTES_PER_STEP,
                 "kernel_ms_avg": walk_avg_ms, "kernel_share_of_step": (walk_ms_tot / ms) if ms else None,
-                "note": "algorithmic bytes = 64 B x emissions per launch; config-2 tables (~70 MB touched) fit in "
-                        "the 126 MB L2 after the flush, so frac can exceed the HBM roofline"}
+                "random_sector_ceiling_gsteps": 37.8,
+                "note": "algorithmic bytes = 64 B x emissions (row header + sampled entry, SURVEY 8d); the fat "
+                        "layout serves them with one random 32-B sector per step. Random HBM sectors top out at "
+                        "~37.8 G/s on this B200 (tools/gups, profiles/r01/gups.txt); L2-resident graphs (config 2) "
+                        "exceed it"}
     if cfg["kind"] == "diag":
         roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
 
