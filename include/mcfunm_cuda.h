@@ -49,6 +49,8 @@ extern "C" {
 #define MCF_FLAG_NONE 0
 #define MCF_FLAG_TIME_KERNELS 1 /* bracket the walk / Q-build kernels with CUDA events
                                    (read with mcf_graph_kernel_times) */
+#define MCF_FLAG_RETURN_ONLY 2  /* action walks accumulate zeta W only at emissions where the walk is
+                                   back at its start node (classic MC diagonal, Alg. 1) */
 
 typedef struct mcf_graph mcf_graph;
 

@@ -570,3 +570,89 @@ def diag_columns(a: Csr, t: Tables, z: np.ndarray, ni: np.ndarray, cols, max_ste
             ilo, ihi = a.csc_ptr[i], a.csc_ptr[i + 1]
             contrib[int(i)] = contrib.get(int(i), 0.0) + aic * (qrow[a.csc_rows[ilo:ihi]] @ a.csc_vals[ilo:ihi])
     return contrib, em
+
+
+# --------------------------------------------------------------------------
+# single-entry estimator and the classic MC baseline (SPEC-only in the
+# reference: Alg. 1 :93-117 and §4.3 :636-649)
+# --------------------------------------------------------------------------
+def entry_budgets(t: Tables, a: Csr, i: int, n_walks: int) -> np.ndarray:
+    """walks only from the columns j with a_ij != 0, the start
+    distribution renormalised over that support, largest-remainder rounding."""
+    lo, hi = a.row_ptr[i], a.row_ptr[i + 1]
+    cols = a.col_ids[lo:hi]
+    ni = np.zeros(a.n, dtype=np.int64)
+    if hi > lo:
+        p = t.init_prob[cols]
+        if p.sum() > 0:
+            ni[cols] = largest_remainder(p / p.sum(), n_walks)
+    return ni
+
+
+def funm_entry(a: Csr, tag: str, v: np.ndarray, i: int, n_walks: int, cutoff: float = 1e-6,
+               max_steps: int = 10_000, seed: int = 0, record: bool = False) -> Run:
+    """y_i = zeta_0 v_i + zeta_1 r_i + <A_i, q> with q from walks launched only
+    from row i's support."""
+    v = np.asarray(v, dtype=np.float64)
+    z = zeta_prefix(tag, max_steps + 2)
+    lo, hi = a.row_ptr[i], a.row_ptr[i + 1]
+    if hi == lo:  # empty row: zeta_0 v_i exactly, no walk
+        return Run(np.array([z[0] * v[i]]), np.zeros(a.n, dtype=np.int64))
+    t = transition_tables(a)
+    ni = entry_budgets(t, a, i, n_walks)
+    A = a.scipy_csr()
+    r = A @ v
+    rec = _Recorder(ni) if record else None
+    q = np.zeros(a.n)
+    em = tr = 0
+    for c in np.flatnonzero(ni):
+        acc = [0.0]
+
+        def on_step(k, s, w, ids, acc=acc):
+            acc[0] += z[k + 2] * (w * r[s]).sum()
+        e, tt = batch_walks(t, int(c), int(ni[c]), max_steps, cutoff, column_stream(seed, int(c)), on_step,
+                            rec.hook(c) if rec else None)
+        q[c] = acc[0]
+        em += e
+        tr += tt
+    yi = z[0] * v[i] + z[1] * r[i] + a.vals[lo:hi] @ q[a.col_ids[lo:hi]]
+    out = Run(np.array([yi]), ni, em, tr, int(ni.sum()), {"q": q, "r": r})
+    if rec:
+        out.record = rec.finish()
+    return out
+
+
+def mc_baseline(a: Csr, tag: str, walks_per_row: int, cutoff: float = 1e-6, max_steps: int = 10_000,
+                seed: int = 0, mode: str = "diag", v: np.ndarray | None = None, rows=None,
+                record: bool = False) -> Run:
+    """Alg. 1: N_s walks from every row i, W0 = 1/N_s,
+    f_{i,l_k} += zeta_k W_k.  diag keeps f_ii (walks back at i); action
+    accumulates y_i += zeta_k W_k v[l_k]; ``rows`` restricts the start rows
+    (entry mode).  Walks use the same per-row substreams and batch driver."""
+    z = zeta_prefix(tag, max_steps + 1)
+    t = transition_tables(a)
+    rows = np.arange(a.n) if rows is None else np.asarray(rows)
+    ni = np.zeros(a.n, dtype=np.int64)
+    ni[rows] = walks_per_row
+    rec = _Recorder(ni) if record else None
+    out = np.zeros(a.n)
+    if mode == "action":
+        v = np.asarray(v, dtype=np.float64)
+    em = tr = 0
+    for i in rows:
+        acc = [0.0]
+
+        def on_step(k, s, w, ids, acc=acc, i=int(i)):
+            if mode == "action":
+                acc[0] += z[k] * (w * v[s]).sum()
+            else:
+                acc[0] += z[k] * w[s == i].sum()
+        e, tt = batch_walks(t, int(i), int(walks_per_row), max_steps, cutoff, column_stream(seed, int(i)), on_step,
+                            rec.hook(i) if rec else None)
+        out[i] = acc[0]
+        em += e
+        tr += tt
+    res = Run(out, ni, em, tr, int(ni.sum()))
+    if rec:
+        res.record = rec.finish()
+    return res

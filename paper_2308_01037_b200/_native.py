@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("MCFUNM_CUDA_LIB", os.path.join(_HERE, "lib", "libmcfu
 
 MCF_STATS_LEN = 4
 MCF_FLAG_TIME_KERNELS = 1
+MCF_FLAG_RETURN_ONLY = 2
 
 P = C.c_void_p
 I64 = C.c_int64

@@ -39,6 +39,7 @@ struct WalkCommon {
     const int *__restrict__ entries;          // replay only
     unsigned *counter;  // walks handed out (chunked, relative to the range start)
     unsigned long long *colmax;  // diag: per-column max |emission| (IEEE bits), or null
+    int return_only;             // MCF_FLAG_RETURN_ONLY
     long long *stats;
     int *err;
 };
@@ -242,7 +243,9 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
             if (L[s].rel < 0) continue;
-            L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, L[s].h.aux, L[s].x);  // q_c += zeta W r[l]
+            // q_c += zeta W r[l]; classic MC diagonal: only back at the start (Alg. 1)
+            const double pay = a.return_only ? ((int)L[s].h.pad == L[s].c ? 1.0 : 0.0) : L[s].h.aux;
+            L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, pay, L[s].x);
             ++em;
             e[s] = pick<REPLAY>(a, L[s], ab);
         }
@@ -552,6 +555,7 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.walk_off = nullptr;
     a.entries = nullptr;
     a.colmax = nullptr;
+    a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
     return MCF_OK;
 }
 

@@ -164,3 +164,119 @@ def rand_funm_diag(a, coeffs, config, *, replay=None, budgets=None, device=None,
     _stats(res, st)
     res.aux = {"pcol": pcol, "ni": ni, "walk_pre": pre}
     return res
+
+
+def _row(g: DeviceGraph, i: int):
+    lo, hi = (int(x) for x in g.row_ptr[i:i + 2].cpu())
+    return lo, hi, g.col_ids[lo:hi].to(torch.int64), g.vals[lo:hi]
+
+
+def rand_funm_entry(a, coeffs, v, i: int, config, *, replay=None, device=None) -> FunmResult:
+    """(f(A) v)_i alone (§4.3 :636-649):
+    y_i = zeta_0 v_i + zeta_1 r_i + <A_i, q>, with walks launched only from the
+    columns j where a_ij != 0 and the start distribution renormalised over that
+    support (largest-remainder rounding, as allocate_walks)."""
+    from .walker import largest_remainder
+    cfg = check_config(config)
+    coeffs = as_stream(coeffs)
+    n, nnz = _n_nnz(a)
+    if not 0 <= int(i) < n:
+        raise ArgumentError(f"entry index {i} outside [0, {n})")
+    v_np = v.cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v, dtype=np.float64)
+    if v_np.shape != (n,):
+        raise ArgumentError(f"v must have length {n}")
+    z = coeffs.prefix(cfg.max_steps + 2)
+    mode = "replay" if replay is not None else "philox"
+    empty = FunmResult(np.array([z[0] * v_np[i]]), "entry", config=_cfg_echo(cfg, coeffs, mode))
+    if nnz == 0:
+        return empty
+    g = _graph(a, device)
+    lo, hi, cols, vals = _row(g, int(i))
+    if hi == lo:  # empty row: y_i = zeta_0 v_i exactly, no walk (SPEC.md:383)
+        return empty
+    if replay is not None:
+        ni, pre = _budgets(g, cfg, replay, None)
+    else:
+        p = g.tables()["init_prob"][cols].cpu().numpy()
+        nib = np.zeros(n, dtype=np.int64)
+        if p.sum() > 0:
+            nib[cols.cpu().numpy()] = largest_remainder(p / p.sum(), cfg.n_walks)
+        ni, pre = g.budgets(nib)
+    vd = torch.from_numpy(np.ascontiguousarray(v_np)).to(g.device)
+    params = WalkParams(cfg, z, g.device)
+    r = g.spmv(vd)
+    q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
+    st = g.new_stats()
+    if replay is None:
+        g.walk_action(params, pre, r, q, stats=st)
+    else:
+        off, ent = _replay_tensors(g, replay)
+        g.replay_action(params, pre, off, ent, r, q, stats=st)
+    yi = float(z[0] * vd[i] + z[1] * r[i] + (vals * q[cols]).sum())
+    res = FunmResult(np.array([yi]), "entry", config=_cfg_echo(cfg, coeffs, mode))
+    _stats(res, st)
+    res.aux = {"q": q, "r": r, "ni": ni}
+    return res
+
+
+def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None = None, replay=None,
+                device=None) -> FunmResult:
+    """Classic Monte Carlo (Alg. 1 :93-117) on the same
+    device walk engine: ``config.n_walks`` walks from EVERY row (Alg. 1's per-row
+    N_s; total n N_s), W0 = 1/N_s, each step adds zeta_k W_k (from k = 0).
+    mode "diag": f_ii (only emissions back at i); "action": y_i = sum zeta_k
+    W_k v[l_k]; "entry": the action of row i only.  ("full" f(A) is not
+    supported: n^2 output.)"""
+    cfg = check_config(config)
+    coeffs = as_stream(coeffs)
+    if mode not in ("diag", "action", "entry"):
+        raise ArgumentError(f"mc_baseline mode must be diag, action or entry (got '{mode}')")
+    n, nnz = _n_nnz(a)
+    z = coeffs.prefix(cfg.max_steps + 1)
+    zs = np.concatenate([[0.0, 0.0], z])  # the kernel reads zeta[k + 2]: shift Alg. 1's zeta_k by two
+    if mode in ("action", "entry"):
+        if v is None:
+            raise ArgumentError("action/entry mode needs v")
+        v_np = v.cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v, dtype=np.float64)
+        if v_np.shape != (n,):
+            raise ArgumentError(f"v must have length {n}")
+    if mode == "entry" and (i is None or not 0 <= int(i) < n):
+        raise ArgumentError("entry mode needs a row index i in [0, n)")
+    smode = "replay" if replay is not None else "philox"
+    if nnz == 0:  # A = 0: f = zeta_0 I
+        vals = np.full(n, z[0]) if mode == "diag" else z[0] * v_np
+        return FunmResult(vals if mode != "entry" else np.array([vals[i]]), "mc-" + mode,
+                          config=_cfg_echo(cfg, coeffs, smode))
+    g = _graph(a, device)
+    rows = [int(i)] if mode == "entry" else None
+    if replay is not None:
+        ni, pre = _budgets(g, cfg, replay, None)
+    else:
+        nib = np.zeros(n, dtype=np.int64)
+        nib[rows if rows is not None else slice(None)] = cfg.n_walks
+        ni, pre = g.budgets(nib)
+    from . import _native as N
+    from .walker import WalkConfig
+    pcfg = WalkConfig(max(1, cfg.n_walks * (1 if rows else n)), cfg.weight_cutoff, cfg.max_steps, cfg.seed)
+    params = WalkParams(pcfg, zs, g.device)
+    payload = (torch.from_numpy(np.ascontiguousarray(v_np)).to(g.device) if mode != "diag"
+               else torch.zeros(g.n, dtype=torch.float64, device=g.device))
+    if mode == "diag":
+        params.c.flags |= N.MCF_FLAG_RETURN_ONLY
+    q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
+    st = g.new_stats()
+    if replay is None:
+        # < 2^31 walks per launch: chunk the start rows
+        per = max(1, (1 << 30) // max(1, cfg.n_walks))
+        ranges = [(int(i), int(i) + 1)] if rows else [(lo, min(n, lo + per)) for lo in range(0, n, per)]
+        for lo, hi in ranges:
+            params.c.walk_capacity = cfg.n_walks * (hi - lo)
+            g.walk_action(params, pre, payload, q, cols=(lo, hi), stats=st)
+    else:
+        off, ent = _replay_tensors(g, replay)
+        g.replay_action(params, pre, off, ent, payload, q, stats=st)
+    out = q.cpu().numpy()
+    res = FunmResult(out if mode != "entry" else np.array([out[int(i)]]), "mc-" + mode,
+                     config=_cfg_echo(cfg, coeffs, smode))
+    _stats(res, st)
+    return res

@@ -52,3 +52,18 @@ def alpha_diagnostic(a) -> float:
     s = np.zeros(a.csr.shape[0])
     np.add.at(s, rows, np.abs(a.csr.data))
     return float(s.max() ** 2)
+
+
+def largest_remainder(probs, total: int) -> np.ndarray:
+    """floor(p N) plus one for the largest remainders, ties by ascending index,
+    p == 0 never selected (reference walker.py:148-162 contract).  Host-side,
+    for small supports (rand_funm_entry); the full allocation runs on the GPU."""
+    p = np.asarray(probs, dtype=np.float64)
+    want = p * total
+    got = np.floor(want).astype(np.int64)
+    left = int(total - got.sum())
+    if left > 0:
+        rem = want - got
+        rem[p == 0.0] = -1.0
+        got[np.argsort(-rem, kind="stable")[:left]] += 1
+    return got

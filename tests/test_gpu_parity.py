@@ -312,3 +312,47 @@ def test_device_tables_bitwise_hub_rows(mc, seed):
     x = rng.normal(size=n)
     y = g.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
     np.testing.assert_allclose(y, m @ x, rtol=1e-12, atol=1e-12)
+
+
+def test_entry_and_mc_replay_parity(mc):
+    """rand_funm_entry and mc_baseline replaying oracle-recorded streams."""
+    c = golden_io.load("ba400")
+    g = mc.DeviceGraph(as_matrix(c.sa, True))
+    hub = int(np.argmax(np.diff(c.sa.row_ptr)))
+    v = np.linspace(0.5, 1.5, c.n)
+    run = port.funm_entry(c.sa, "exponential", v, hub, 20_000, 1e-6, 28, 4, record=True)
+    out = mc.rand_funm_entry(g, mc.EXPONENTIAL, v, hub, mc.WalkConfig(20_000, 1e-6, 28, 4), replay=run.record)
+    assert rel_err(out.values, run.payload) < REL and out.emissions == run.emissions
+    for mode in ("diag", "action"):
+        run = port.mc_baseline(c.sa, "exponential", 20, 1e-6, 28, 5, mode, v=v, record=True)
+        out = mc.mc_baseline(g, mc.EXPONENTIAL, mc.WalkConfig(20, 1e-6, 28, 5), mode, v=v, replay=run.record)
+        assert rel_err(out.values, run.payload) < REL
+        assert out.emissions == run.emissions
+
+
+def test_entry_device_rng_matches_exact(mc):
+    c = golden_io.load("er300")
+    g = mc.DeviceGraph(as_matrix(c.sa, True))
+    exact = port.taylor_action(c.sa, "exponential", np.ones(c.n), 29)
+    for i in (0, 17, 123):
+        ys = [mc.rand_funm_entry(g, mc.EXPONENTIAL, np.ones(c.n), i, mc.WalkConfig(200_000, 1e-300, 28, s)).values[0]
+              for s in range(8)]
+        z = (np.mean(ys) - exact[i]) / (np.std(ys, ddof=1) / np.sqrt(8))
+        assert abs(z) < 5, (i, z)
+    e = mc.rand_funm_entry(g, mc.EXPONENTIAL, np.ones(c.n), 5, mc.WalkConfig(1000))
+    assert e.walks == 1000
+
+
+def test_mc_baseline_dominated_by_rand_funm_diag(mc):
+    """SPEC acceptance 6 (§4.2 claim): at equal global walk budget on a 64-node
+    small world, rand_funm_diag beats mc_baseline(diag) in l_inf error in >= 8/10 seeds."""
+    c = golden_io.load("sw64_katz")
+    a = c.a.scaled(1e-1)
+    g = mc.DeviceGraph(as_matrix(a, True))
+    exact = np.diag(port.dense_funm(a, "exponential", 40))
+    wins = 0
+    for s in range(10):
+        d1 = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(64 * 1000, 1e-10, 100, s)).values
+        d0 = mc.mc_baseline(g, mc.EXPONENTIAL, mc.WalkConfig(1000, 1e-10, 100, s), "diag").values
+        wins += np.max(np.abs(d1 - exact)) < np.max(np.abs(d0 - exact))
+    assert wins >= 8
