@@ -66,7 +66,12 @@ struct QArgs {
     unsigned *n_big;            // record counter
     unsigned max_big;
     int *pool_keys;             // persisted tables
-    double *pool_vals;
+    long long *pool_vals;
+    int *pool_E;                // fixed-point exponent per record
+    // hub-row bitmaps (uniform-value graphs): hub_of[i] = bitmap index or -1
+    const int *hub_of;
+    const unsigned *hub_bits;
+    long long hub_words;
     unsigned long long *pool_used, pool_cap;
     unsigned *pool_filt;        // FILTER_WORDS per record
 };
@@ -106,12 +111,12 @@ __device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key)
     }
 }
 
-__device__ __forceinline__ double lookup(const int *keys, const double *vals, uint32_t mask, int key) {
+__device__ __forceinline__ long long lookup(const int *keys, const long long *vals, uint32_t mask, int key) {
     uint32_t s = hash_slot(key, mask);
     while (true) {
         int k = keys[s];
         if (k == key) return vals[s];
-        if (k == EMPTY_KEY) return 0.0;
+        if (k == EMPTY_KEY) return 0;
         s = (s + 1) & mask;
     }
 }
@@ -120,6 +125,52 @@ __device__ __forceinline__ double lookup(const int *keys, const double *vals, ui
 // miss (C_i entries no walk from c visited): the filter answers them with one
 // shared-memory word instead of a linear-probing chain.
 __device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key * 0x85EBCA6Bu) >> 14; }
+
+// Contribution of the stored entry (i, c): a_ic <Q_c, C_i>, one warp.
+//   pull: scan C_i (coalesced row ids), Bloom filter, hash lookup;
+//   push: for a hub row i longer than the table, scan the table's slots and
+//         test membership in i's bitmap (cost min(deg i, cap) instead of deg i).
+// On uniform-value graphs both paths add the fixed-point integers exactly, so
+// the value does not depend on the path or on any order (deterministic).
+__device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, const long long *vals, uint32_t mask,
+                                             uint32_t cap, const unsigned *filt, int E, int i, double aic,
+                                             int lane) {
+    const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+    if (a.uniform) {
+        long long acc = 0;
+        const int h = a.hub_of ? __ldg(a.hub_of + i) : -1;
+        if (h >= 0 && ihi - ilo > (long long)cap) {
+            const unsigned *bits = a.hub_bits + (long long)h * a.hub_words;
+            for (uint32_t t = lane; t < cap; t += 32) {
+                const int k = keys[t];
+                if (k != EMPTY_KEY && ((__ldg(bits + (k >> 5)) >> (k & 31)) & 1u)) acc += vals[t];
+            }
+        } else {
+            long long e = ilo + lane;
+            for (; e + 32 < ihi; e += 64) {  // two row ids in flight per lane
+                const int j0 = __ldg(a.csc_rows + e), j1 = __ldg(a.csc_rows + e + 32);
+                const uint32_t b0 = filter_bit(j0), b1 = filter_bit(j1);
+                if (filt[b0 >> 5] & (1u << (b0 & 31))) acc += lookup(keys, vals, mask, j0);
+                if (filt[b1 >> 5] & (1u << (b1 & 31))) acc += lookup(keys, vals, mask, j1);
+            }
+            if (e < ihi) {
+                const int j = __ldg(a.csc_rows + e);
+                const uint32_t b = filter_bit(j);
+                if (filt[b >> 5] & (1u << (b & 31))) acc += lookup(keys, vals, mask, j);
+            }
+        }
+        acc = warp_sum_ll(acc);
+        return aic * (a.value * ldexp((double)acc, -E));
+    }
+    double acc = 0.0;
+    for (long long e = ilo + lane; e < ihi; e += 32) {
+        const int j = __ldg(a.csc_rows + e);
+        const uint32_t b = filter_bit(j);
+        if (filt[b >> 5] & (1u << (b & 31)))
+            acc = fma(__ldg(a.csc_vals + e), ldexp((double)lookup(keys, vals, mask, j), -E), acc);
+    }
+    return aic * warp_sum(acc);
+}
 
 // Q_c is accumulated in fixed point: every weight is scaled by 2^E (E from the
 // column's largest |weight| and its emission count, so no sum can exceed
@@ -192,14 +243,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             }
         }
         __syncthreads();
-        // fixed point -> double in place, and the Bloom filter of the keys
-        double *qv = reinterpret_cast<double *>(vals);
+        // Bloom filter of the keys
         for (int t = tid; t < FILTER_WORDS; t += Q_THREADS) filt[t] = 0u;
         __syncthreads();
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
             const int key = keys[t];
             if (key != EMPTY_KEY) {
-                qv[t] = ldexp((double)vals[t], -E);
                 const uint32_t b = filter_bit(key);
                 atomicOr(&filt[b >> 5], 1u << (b & 31));
             }
@@ -227,6 +276,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     const unsigned r = atomicAdd(a.n_big, 1u);
                     if (r < a.max_big) {
                         a.big[r] = BigRec{c, (long long)off, cap, (unsigned)cn};
+                        a.pool_E[r] = E;
                         s_slot = (long long)r;
                         s_off = (long long)off;
                     }
@@ -236,7 +286,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             if (s_slot >= 0) {
                 for (uint32_t t = tid; t < cap; t += Q_THREADS) {
                     a.pool_keys[s_off + t] = keys[t];
-                    a.pool_vals[s_off + t] = qv[t];
+                    a.pool_vals[s_off + t] = vals[t];
                 }
                 for (int t = tid; t < FILTER_WORDS; t += Q_THREADS)
                     a.pool_filt[s_slot * FILTER_WORDS + t] = filt[t];
@@ -246,33 +296,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
 
         // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
         for (long long t = warp; t < cn; t += Q_WARPS) {
-            const int i = a.csc_rows[cs + t];
-            const double aic = a.csc_vals[cs + t];
-            const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
-            double acc = 0.0;
-            long long e = ilo + lane;
-            for (; e + 32 < ihi; e += 64) {  // two row ids in flight per lane
-                const int j0 = __ldg(a.csc_rows + e), j1 = __ldg(a.csc_rows + e + 32);
-                const uint32_t b0 = filter_bit(j0), b1 = filter_bit(j1);
-                if (filt[b0 >> 5] & (1u << (b0 & 31))) {
-                    const double q0 = lookup(keys, qv, mask, j0);
-                    acc = a.uniform ? acc + q0 : fma(__ldg(a.csc_vals + e), q0, acc);
-                }
-                if (filt[b1 >> 5] & (1u << (b1 & 31))) {
-                    const double q1 = lookup(keys, qv, mask, j1);
-                    acc = a.uniform ? acc + q1 : fma(__ldg(a.csc_vals + e + 32), q1, acc);
-                }
-            }
-            if (e < ihi) {
-                const int j = __ldg(a.csc_rows + e);
-                const uint32_t b = filter_bit(j);
-                if (filt[b >> 5] & (1u << (b & 31))) {
-                    const double qj = lookup(keys, qv, mask, j);
-                    acc = a.uniform ? acc + qj : fma(__ldg(a.csc_vals + e), qj, acc);
-                }
-            }
-            acc = warp_sum(acc);
-            if (lane == 0) a.pcol[cs + t] = aic * (a.uniform ? a.value * acc : acc);
+            const double v = pair_value(a, keys, vals, mask, cap, filt, E, a.csc_rows[cs + t], a.csc_vals[cs + t], lane);
+            if (lane == 0) a.pcol[cs + t] = v;
         }
     }
 }
@@ -294,24 +319,12 @@ __global__ void __launch_bounds__(256) k_diag_big(QArgs a, const long long *__re
         const BigRec r = a.big[lo];
         const long long t = x - item_pre[lo];
         const int *keys = a.pool_keys + r.off;
-        const double *qv = a.pool_vals + r.off;
+        const long long *vals = a.pool_vals + r.off;
         const unsigned *filt = a.pool_filt + (long long)lo * FILTER_WORDS;
-        const uint32_t mask = r.cap - 1;
         const long long cs = a.csc_ptr[r.c];
-        const int i = a.csc_rows[cs + t];
-        const double aic = a.csc_vals[cs + t];
-        const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
-        double acc = 0.0;
-        for (long long e = ilo + lane; e < ihi; e += 32) {
-            const int j = __ldg(a.csc_rows + e);
-            const uint32_t b = filter_bit(j);
-            if (__ldg(filt + (b >> 5)) & (1u << (b & 31))) {
-                const double qj = lookup(keys, qv, mask, j);
-                acc = a.uniform ? acc + qj : fma(__ldg(a.csc_vals + e), qj, acc);
-            }
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) a.pcol[cs + t] = aic * (a.uniform ? a.value * acc : acc);
+        const double v = pair_value(a, keys, vals, r.cap - 1, r.cap, filt, a.pool_E[lo], a.csc_rows[cs + t],
+                                    a.csc_vals[cs + t], lane);
+        if (lane == 0) a.pcol[cs + t] = v;
     }
 }
 
@@ -402,6 +415,9 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.col_begin = cb;
     q.col_end = ce;
     q.pcol = pcol;
+    q.hub_of = g->hub_of;
+    q.hub_bits = g->hub_bits;
+    q.hub_words = g->hub_words;
     q.uniform = g->uniform_value ? 1 : 0;
     q.value = g->value;
     q.colmax = colmax;
@@ -429,13 +445,14 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     const unsigned max_big = 32768;
     const unsigned long long pool_cap = 1ull << 27;  // 1.5 GiB of (key, value) slots
     unsigned char *pool = nullptr;
-    if (cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(double)) + (size_t)max_big * FILTER_WORDS * 4 +
-                                       sizeof(BigRec) * max_big,
+    if (cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(long long)) + (size_t)max_big * FILTER_WORDS * 4 +
+                                       sizeof(BigRec) * max_big + sizeof(int) * max_big,
                         s) == cudaSuccess) {
-        q.pool_vals = reinterpret_cast<double *>(pool);
+        q.pool_vals = reinterpret_cast<long long *>(pool);
         q.pool_keys = reinterpret_cast<int *>(q.pool_vals + pool_cap);
         q.pool_filt = reinterpret_cast<unsigned *>(q.pool_keys + pool_cap);
         q.big = reinterpret_cast<BigRec *>(q.pool_filt + (size_t)max_big * FILTER_WORDS);
+        q.pool_E = reinterpret_cast<int *>(q.big + max_big);
         q.max_big = max_big;
         q.pool_cap = pool_cap;
     } else {
@@ -483,6 +500,8 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(pcol && stats, "diag walk: null pcol/stats");
+    rc = ensure_hub_bitmaps(g, s);
+    if (rc) return rc;
     if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
     long long wb = 0, we = 0;
     rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);

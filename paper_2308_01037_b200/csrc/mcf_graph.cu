@@ -383,6 +383,8 @@ static void release(mcf_graph *g) {
     if (g->csr2csc) cudaFreeAsync(g->csr2csc, 0);
     if (g->long_rows) cudaFreeAsync(g->long_rows, 0);
     if (g->went) cudaFreeAsync(g->went, 0);
+    if (g->hub_of) cudaFreeAsync(g->hub_of, 0);
+    if (g->hub_bits) cudaFreeAsync(g->hub_bits, 0);
     if (g->scratch) cudaFreeAsync(g->scratch, 0);
     for (auto &p : g->ev_walk) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto &p : g->ev_q) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }

@@ -93,6 +93,11 @@ struct mcf_graph {
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;
     void *scratch = nullptr;
+    // hub-row bitmaps for the diag combine (uniform-value graphs, built lazily)
+    int *hub_of = nullptr;           // n: bitmap index of row i, or -1
+    unsigned *hub_bits = nullptr;    // n_hubs x hub_words
+    long long hub_words = 0;
+    bool hubs_ready = false;
     bool uniform_value = false;      // all stored values equal `value` (0/1 graphs scaled by gamma)
     double value = 0.0;
     mcf_graph_info info{};
@@ -201,6 +206,7 @@ int scan_src(ScanSrc src, long long *out, long long n, cudaStream_t s);
 int build_blk_col(const long long *walk_pre, long long col_begin, long long col_end, long long capacity,
                   int **blk_col, cudaStream_t s);
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
+int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s);
 int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end,
                     long long *wb, long long *we, cudaStream_t s);
 int sm_count();

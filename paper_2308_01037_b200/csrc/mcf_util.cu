@@ -2,6 +2,7 @@
 // index, coefficient upload, CSR -> CSC entry map.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "mcf_internal.cuh"
@@ -255,6 +256,93 @@ int ensure_csr2csc(mcf_graph *g, cudaStream_t s) {
                                                (long long *)g->csr2csc);
     mcf::note_launch();
     MCF_LAUNCHED("k_csr2csc");
+    return MCF_OK;
+}
+
+}  // namespace mcf
+
+// ---------------------------------------------------------------------------
+// hub-row bitmaps (diag combine push path; uniform-value graphs)
+// ---------------------------------------------------------------------------
+namespace mcf {
+
+__global__ void k_deg_hist(const long long *__restrict__ row_ptr, long long n, unsigned long long *hist) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long d = row_ptr[i + 1] - row_ptr[i];
+    if (d > 0) atomicAdd(&hist[63 - __clzll(d)], 1ull);  // bin b: 2^b <= deg < 2^(b+1)
+}
+
+__global__ void k_mark_hubs(const long long *__restrict__ row_ptr, long long n, long long min_deg, int max_hubs,
+                            int *__restrict__ hub_of, unsigned *count) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int h = -1;
+    if (row_ptr[i + 1] - row_ptr[i] >= min_deg) {
+        unsigned k = atomicAdd(count, 1u);
+        if ((int)k < max_hubs) h = (int)k;
+    }
+    hub_of[i] = h;
+}
+
+__global__ void k_hub_bits(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                           const int *__restrict__ hub_of, long long n, long long words, unsigned *__restrict__ bits) {
+    for (long long i = blockIdx.x; i < n; i += gridDim.x) {
+        const int h = hub_of[i];
+        if (h < 0) continue;
+        unsigned *b = bits + (long long)h * words;
+        for (long long e = row_ptr[i] + threadIdx.x; e < row_ptr[i + 1]; e += blockDim.x) {
+            const int c = col_ids[e];
+            atomicOr(b + (c >> 5), 1u << (c & 31));
+        }
+    }
+}
+
+constexpr long long HUB_MIN_DEG = 2048;
+
+int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s) {
+    if (g->hubs_ready) return MCF_OK;
+    g->hubs_ready = true;
+    if (!g->uniform_value || g->info.max_degree < HUB_MIN_DEG) return MCF_OK;
+    const char *env = getenv("MCF_HUB_BITMAP_MB");
+    const long long budget = (env ? atoll(env) : 4096ll) << 20;
+    const long long words = (g->n + 31) / 32;
+    const long long max_hubs = budget / (words * 4);
+    if (max_hubs < 1) return MCF_OK;
+    unsigned long long *hist = nullptr;
+    MCF_CUDA(cudaMallocAsync(&hist, sizeof(unsigned long long) * 64 + 16, s));
+    MCF_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 64 + 16, s));
+    const unsigned nb = (unsigned)((g->n + 255) / 256);
+    k_deg_hist<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->n, hist);
+    mcf::note_launch();
+    unsigned long long h[64];
+    MCF_CUDA(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    // smallest power-of-two threshold >= HUB_MIN_DEG whose hub count fits the budget
+    int b0 = 63 - __builtin_clzll((unsigned long long)HUB_MIN_DEG);
+    long long above = 0;
+    int bsel = 64;
+    for (int b = 63; b >= b0; --b) {
+        if (above + (long long)h[b] > max_hubs) break;
+        above += (long long)h[b];
+        bsel = b;
+    }
+    if (bsel == 64 || above == 0) {
+        cudaFreeAsync(hist, s);
+        return MCF_OK;
+    }
+    MCF_CUDA(cudaMallocAsync(&g->hub_of, sizeof(int) * g->n, s));
+    MCF_CUDA(cudaMallocAsync(&g->hub_bits, sizeof(unsigned) * words * above, s));
+    MCF_CUDA(cudaMemsetAsync(g->hub_bits, 0, sizeof(unsigned) * words * above, s));
+    unsigned *cnt = reinterpret_cast<unsigned *>(hist + 64);
+    k_mark_hubs<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->n, 1ll << bsel, (int)above, g->hub_of, cnt);
+    mcf::note_launch();
+    k_hub_bits<<<sm_count() * 4, 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->hub_of, g->n, words,
+                                            g->hub_bits);
+    mcf::note_launch();
+    MCF_LAUNCHED("hub bitmaps");
+    g->hub_words = words;
+    cudaFreeAsync(hist, s);
     return MCF_OK;
 }
 

@@ -356,3 +356,43 @@ def test_mc_baseline_dominated_by_rand_funm_diag(mc):
         d0 = mc.mc_baseline(g, mc.EXPONENTIAL, mc.WalkConfig(1000, 1e-10, 100, s), "diag").values
         wins += np.max(np.abs(d1 - exact)) < np.max(np.abs(d0 - exact))
     assert wins >= 8
+
+
+def _hub_graph(seed=0, n=5000, hub_deg=4000):
+    rng = np.random.default_rng(seed)
+    nb = rng.choice(np.arange(1, n), hub_deg, replace=False)
+    u = np.r_[np.zeros(hub_deg, dtype=np.int64), rng.integers(0, n, 6 * n)]
+    v = np.r_[nb, rng.integers(0, n, 6 * n)]
+    keep = u != v
+    m = sparse.coo_array((np.ones(2 * keep.sum()), (np.r_[u[keep], v[keep]], np.r_[v[keep], u[keep]])), shape=(n, n))
+    m = sparse.csr_array(m)
+    m.sum_duplicates()
+    m.data[:] = 1.0
+    a = port.Csr.from_any(m)
+    lam = float(np.max(np.linalg.eigvalsh(m.toarray()))) if n <= 3000 else float(
+        __import__("scipy.sparse.linalg", fromlist=["eigsh"]).eigsh(m.astype(float), k=1, which="LA",
+                                                                      v0=np.ones(n))[0][0])
+    return a.scaled(1.0 / lam)
+
+
+def test_diag_hub_push_path_bitwise_and_replay(mc):
+    """Hub rows (degree >= 2048) take the bitmap push path on uniform-value
+    graphs; fixed-point sums make it bitwise equal to the pull path, and replay
+    still matches the oracle to 1e-10."""
+    import os
+    a = _hub_graph()
+    cfg = mc.WalkConfig(5000 * 30, 1e-300, 20, 2)
+    outs = []
+    for mb in (None, "0"):
+        if mb is None:
+            os.environ.pop("MCF_HUB_BITMAP_MB", None)
+        else:
+            os.environ["MCF_HUB_BITMAP_MB"] = mb
+        g = mc.DeviceGraph(as_matrix(a, True))
+        outs.append(mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values)
+    os.environ.pop("MCF_HUB_BITMAP_MB", None)
+    assert np.array_equal(outs[0], outs[1])
+    run = port.funm_diag(a, "exponential", 5000 * 4, 1e-300, 20, 3, record=True)
+    g = mc.DeviceGraph(as_matrix(a, True))
+    out = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(5000 * 4, 1e-300, 20, 3), replay=run.record)
+    assert rel_err(out.values, run.payload) < REL
