@@ -68,6 +68,10 @@ struct QArgs {
     int *pool_keys;             // persisted tables
     long long *pool_vals;
     int *pool_E;                // fixed-point exponent per record
+    int *lkeys;                 // per-CTA support list of Q_c (push path), gcap_l entries per CTA
+    long long *lvals;
+    long long lcap;
+    int *pool_nsupp;            // support-list length per big record (lists live after the table in the pool)
     // hub-row bitmaps (uniform-value graphs): hub_of[i] = bitmap index or -1
     const int *hub_of;
     const unsigned *hub_bits;
@@ -133,17 +137,17 @@ __device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key 
 // On uniform-value graphs both paths add the fixed-point integers exactly, so
 // the value does not depend on the path or on any order (deterministic).
 __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, const long long *vals, uint32_t mask,
-                                             uint32_t cap, const unsigned *filt, int E, int i, double aic,
-                                             int lane) {
+                                             const int *lkeys, const long long *lvals, int nsupp,
+                                             const unsigned *filt, int E, int i, double aic, int lane) {
     const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
     if (a.uniform) {
         long long acc = 0;
         const int h = a.hub_of ? __ldg(a.hub_of + i) : -1;
-        if (h >= 0 && ihi - ilo > (long long)cap) {
+        if (h >= 0 && ihi - ilo > 4ll * nsupp) {  // push: the support list against i's bitmap
             const unsigned *bits = a.hub_bits + (long long)h * a.hub_words;
-            for (uint32_t t = lane; t < cap; t += 32) {
-                const int k = keys[t];
-                if (k != EMPTY_KEY && ((__ldg(bits + (k >> 5)) >> (k & 31)) & 1u)) acc += vals[t];
+            for (int t = lane; t < nsupp; t += 32) {
+                const int k = lkeys[t];
+                if ((__ldg(bits + (k >> 5)) >> (k & 31)) & 1u) acc += lvals[t];
             }
         } else {
             long long e = ilo + lane;
@@ -185,6 +189,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
     __shared__ long long s_col, s_work, s_slot, s_off;
+    __shared__ int s_nsupp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
     long long *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
@@ -243,17 +248,28 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             }
         }
         __syncthreads();
-        // Bloom filter of the keys
+        // Bloom filter of the keys and the compact support list (push path)
         for (int t = tid; t < FILTER_WORDS; t += Q_THREADS) filt[t] = 0u;
+        if (tid == 0) s_nsupp = 0;
         __syncthreads();
+        int *lkeys = a.lkeys + (long long)blockIdx.x * a.lcap;
+        long long *lvals = a.lvals + (long long)blockIdx.x * a.lcap;
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
             const int key = keys[t];
             if (key != EMPTY_KEY) {
                 const uint32_t b = filter_bit(key);
                 atomicOr(&filt[b >> 5], 1u << (b & 31));
+                if (a.uniform) {
+                    const int p = atomicAdd(&s_nsupp, 1);
+                    if (p < a.lcap) {
+                        lkeys[p] = key;
+                        lvals[p] = vals[t];
+                    }
+                }
             }
         }
         __syncthreads();
+        const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
 
         // combine work of this column: sum of deg(i) over the entries (i, c)
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
@@ -271,8 +287,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             // hand Q_c to k_diag_big: all warps of the GPU share the combine
             if (tid == 0) {
                 s_slot = -1;
-                const unsigned long long off = atomicAdd(a.pool_used, (unsigned long long)cap);
-                if (off + cap <= a.pool_cap) {
+                const unsigned long long off = atomicAdd(a.pool_used, 2ull * cap);
+                if (off + 2ull * cap <= a.pool_cap) {
                     const unsigned r = atomicAdd(a.n_big, 1u);
                     if (r < a.max_big) {
                         a.big[r] = BigRec{c, (long long)off, cap, (unsigned)cn};
@@ -288,6 +304,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     a.pool_keys[s_off + t] = keys[t];
                     a.pool_vals[s_off + t] = vals[t];
                 }
+                // support list after the table (nsupp <= cap / 2 by the load factor)
+                for (int t = tid; t < nsupp && nsupp <= (int)cap; t += Q_THREADS) {
+                    a.pool_keys[s_off + cap + t] = lkeys[t];
+                    a.pool_vals[s_off + cap + t] = lvals[t];
+                }
+                if (tid == 0) a.pool_nsupp[s_slot] = nsupp <= (int)cap ? nsupp : 0x3fffffff;
                 for (int t = tid; t < FILTER_WORDS; t += Q_THREADS)
                     a.pool_filt[s_slot * FILTER_WORDS + t] = filt[t];
                 continue;  // the loop-top barrier orders these copies before the table is reused
@@ -296,7 +318,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
 
         // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
         for (long long t = warp; t < cn; t += Q_WARPS) {
-            const double v = pair_value(a, keys, vals, mask, cap, filt, E, a.csc_rows[cs + t], a.csc_vals[cs + t], lane);
+            const double v = pair_value(a, keys, vals, mask, lkeys, lvals, nsupp, filt, E, a.csc_rows[cs + t],
+                                        a.csc_vals[cs + t], lane);
             if (lane == 0) a.pcol[cs + t] = v;
         }
     }
@@ -322,8 +345,8 @@ __global__ void __launch_bounds__(256) k_diag_big(QArgs a, const long long *__re
         const long long *vals = a.pool_vals + r.off;
         const unsigned *filt = a.pool_filt + (long long)lo * FILTER_WORDS;
         const long long cs = a.csc_ptr[r.c];
-        const double v = pair_value(a, keys, vals, r.cap - 1, r.cap, filt, a.pool_E[lo], a.csc_rows[cs + t],
-                                    a.csc_vals[cs + t], lane);
+        const double v = pair_value(a, keys, vals, r.cap - 1, keys + r.cap, vals + r.cap, a.pool_nsupp[lo], filt,
+                                    a.pool_E[lo], a.csc_rows[cs + t], a.csc_vals[cs + t], lane);
         if (lane == 0) a.pcol[cs + t] = v;
     }
 }
@@ -435,6 +458,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.gvals = reinterpret_cast<long long *>(gbuf);
         q.gkeys = reinterpret_cast<int *>(q.gvals + (size_t)grid * cap);
     }
+    // per-CTA support lists (push path): up to half the largest table
+    q.lcap = (cap > SCAP ? cap : SCAP) / 2;
+    unsigned char *lbuf = nullptr;
+    MCF_CUDA(cudaMallocAsync(&lbuf, (size_t)grid * q.lcap * (sizeof(int) + sizeof(long long)), s));
+    q.lvals = reinterpret_cast<long long *>(lbuf);
+    q.lkeys = reinterpret_cast<int *>(q.lvals + (size_t)grid * q.lcap);
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) * 4, s));
@@ -446,13 +475,14 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     const unsigned long long pool_cap = 1ull << 27;  // 1.5 GiB of (key, value) slots
     unsigned char *pool = nullptr;
     if (cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(long long)) + (size_t)max_big * FILTER_WORDS * 4 +
-                                       sizeof(BigRec) * max_big + sizeof(int) * max_big,
+                                       sizeof(BigRec) * max_big + 2 * sizeof(int) * max_big,
                         s) == cudaSuccess) {
         q.pool_vals = reinterpret_cast<long long *>(pool);
         q.pool_keys = reinterpret_cast<int *>(q.pool_vals + pool_cap);
         q.pool_filt = reinterpret_cast<unsigned *>(q.pool_keys + pool_cap);
         q.big = reinterpret_cast<BigRec *>(q.pool_filt + (size_t)max_big * FILTER_WORDS);
         q.pool_E = reinterpret_cast<int *>(q.big + max_big);
+        q.pool_nsupp = q.pool_E + max_big;
         q.max_big = max_big;
         q.pool_cap = pool_cap;
     } else {
@@ -490,6 +520,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
     cudaFreeAsync(counter, s);
+    cudaFreeAsync(lbuf, s);
     if (gbuf) cudaFreeAsync(gbuf, s);
     return MCF_OK;
 }
