@@ -9,86 +9,95 @@
 
 namespace mcf {
 
-struct SelectState {
+// Largest-remainder selection in five kernels, without a sort:
+//   1 k_alloc_floor  N_i = floor(p_i N), remainder key, Sum N_i and a 1024-bucket
+//                    histogram of the remainders (floor(rem * 1024)); the last
+//                    block finds the bucket b* that holds the R-th largest.
+//   2 k_alloc_cands  compacts the keys of bucket b* (with their index).
+//   3 k_alloc_select one CTA: exact radix select of the threshold key T among
+//                    the candidates, then -- among the keys equal to T -- the
+//                    index threshold I (ties go to the lowest indices, the
+//                    reference's stable argsort).
+//   4 k_alloc_final  N_i += key > T || (key == T && i <= I).
+//   5 scan           walk_pre.
+// p_i = 0 keys (0) sit below every positive remainder; they are only reached
+// when R exceeds the number of positive p_i (then b* = -1 covers them).
+constexpr int NBUCKET = 1024;
+
+struct AllocState {
     unsigned long long total_floor;  // sum of floor(p N)
-    unsigned long long prefix, mask;
-    long long k;     // still to select inside the current prefix bucket
-    long long left;  // residue R
-    unsigned int done;
-    unsigned int hist[256];
+    unsigned long long n_pos;        // entries with p > 0
+    long long left;                  // residue R
+    long long need;                  // to take inside bucket b*
+    int bstar;                       // bucket holding the R-th largest (-1: the p == 0 keys)
+    unsigned done;
+    unsigned ncand;
+    unsigned long long T;            // threshold key
+    long long I;                     // index threshold among keys == T
+    unsigned hist[NBUCKET];
 };
 
-// floor(p N), remainder keys, sum of floors; the last block to finish also
-// initialises the selection (residue R = N - sum floor).
-__global__ void k_floor(const double *__restrict__ p, long long n, double total, long long n_walks,
-                        long long *__restrict__ ni, unsigned long long *__restrict__ key, SelectState *st) {
-    __shared__ bool last;
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    long long got = 0;
-    if (i < n) {
-        double pi = p[i];
-        double want = __dmul_rn(pi, total);
-        double fl = floor(want);
-        got = (long long)fl;
-        ni[i] = got;
-        key[i] = (pi == 0.0) ? 0ull : (unsigned long long)__double_as_longlong(__dsub_rn(want, fl)) + 1ull;
-    }
-    got = warp_sum_ll(got);
-    if ((threadIdx.x & 31) == 0 && got) atomicAdd(&st->total_floor, (unsigned long long)got);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
-        st->left = n_walks - (long long)atomicAdd(&st->total_floor, 0ull);
-        st->k = st->left;
-        st->prefix = 0;
-        st->mask = 0;
-        st->done = 0;
-    }
+__device__ __forceinline__ int rem_bucket(unsigned long long key) {
+    if (key == 0) return -1;
+    const double rem = __longlong_as_double((long long)(key - 1));
+    const int b = (int)(rem * NBUCKET);
+    return b < NBUCKET ? b : NBUCKET - 1;
 }
 
-// One radix-select pass: histogram of the 8-bit digit at `shift` over keys
-// that match the current prefix; the last block picks the bucket holding the
-// k-th largest key (parallel suffix scan over the 256 bins).
-__global__ void __launch_bounds__(256) k_select_pass(const unsigned long long *__restrict__ key, long long n,
-                                                     int shift, SelectState *st) {
-    __shared__ unsigned int h[256];
+// block-parallel search from the top bucket: thread t holds bucket NBUCKET-1-t*4..; finds b with
+// count(above b) < R <= count(above b) + hist[b]
+__global__ void __launch_bounds__(256) k_alloc_floor(const double *__restrict__ p, long long n, double total,
+                                                     long long n_walks, long long *__restrict__ ni,
+                                                     unsigned long long *__restrict__ key, AllocState *st) {
+    __shared__ unsigned h[NBUCKET];
     __shared__ bool last;
-    if (st->k <= 0) return;  // uniform across the grid
-    h[threadIdx.x] = 0;
+    __shared__ long long wsum[8];
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    const unsigned long long pre = st->prefix, msk = st->mask;
+    long long got_sum = 0, pos = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {  // warp-uniform trip count
-        const long long i = base + threadIdx.x;
-        const unsigned long long k = i < n ? key[i] : ~0ull;
-        const bool in = i < n && (k & msk) == pre;
-        const unsigned dig = in ? (unsigned)((k >> shift) & 255u) : 256u;
-        // ties are common (equal-degree nodes share p): a warp whose keys all
-        // fall in one bin adds once
-        const unsigned d0 = __shfl_sync(MCF_FULL, dig, 0);
-        if (__all_sync(MCF_FULL, dig == d0)) {
-            if ((threadIdx.x & 31) == 0 && d0 < 256u) atomicAdd(&h[d0], 32u);
-        } else if (in) {
-            atomicAdd(&h[dig], 1u);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double pi = p[i];
+        const double want = __dmul_rn(pi, total);
+        const double fl = floor(want);
+        const long long got = (long long)fl;
+        ni[i] = got;
+        got_sum += got;
+        unsigned long long k = 0;
+        if (pi != 0.0) {
+            k = (unsigned long long)__double_as_longlong(__dsub_rn(want, fl)) + 1ull;
+            ++pos;
+            atomicAdd(&h[rem_bucket(k)], 1u);
         }
+        key[i] = k;
+    }
+    got_sum = warp_sum_ll(got_sum);
+    pos = warp_sum_ll(pos);
+    if ((threadIdx.x & 31) == 0) {
+        if (got_sum) atomicAdd(&st->total_floor, (unsigned long long)got_sum);
+        if (pos) atomicAdd(&st->n_pos, (unsigned long long)pos);
     }
     __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], h[threadIdx.x]);
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x)
+        if (h[b]) atomicAdd(&st->hist[b], h[b]);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // thread t looks at bin 255 - t: inclusive scan of counts from the top
-    const int b = 255 - threadIdx.x;
-    const long long c = (long long)atomicAdd(&st->hist[b], 0u);
-    __shared__ long long wsum[8];
-    long long x = c;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long R = n_walks - (long long)atomicAdd(&st->total_floor, 0ull);
+    const long long npos = (long long)atomicAdd(&st->n_pos, 0ull);
+    // suffix counts: thread t owns buckets [NBUCKET-4(t+1), NBUCKET-4t) (4 per thread, top first)
+    const int t = threadIdx.x;
+    long long c4[4], own = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        c4[u] = (long long)atomicAdd(&st->hist[NBUCKET - 1 - (4 * t + u)], 0u);
+        own += c4[u];
+    }
+    long long x = own;
+    const int lane = t & 31, w = t >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         long long y = __shfl_up_sync(MCF_FULL, x, o);
@@ -96,62 +105,158 @@ __global__ void __launch_bounds__(256) k_select_pass(const unsigned long long *_
     }
     if (lane == 31) wsum[w] = x;
     __syncthreads();
-    long long before = 0;
-    for (int j = 0; j < w; ++j) before += wsum[j];
-    const long long incl = before + x;
-    const long long k = st->k;
-    __syncthreads();
-    if (incl - c < k && k <= incl) {
-        st->prefix = pre | ((unsigned long long)b << shift);
-        st->mask = msk | (255ull << shift);
-        st->k = k - (incl - c);
+    long long above = x - own;
+    for (int j = 0; j < w; ++j) above += wsum[j];
+    if (t == 0) {
+        st->left = R;
+        st->bstar = -2;  // nothing to select
+        st->need = 0;
+        st->done = 0;
+        st->ncand = 0;
+        if (R > npos) {  // every positive key, plus the lowest-index p == 0 entries
+            st->bstar = -1;
+            st->need = R - npos;
+        }
     }
-    st->hist[b] = 0;
-    if (threadIdx.x == 0) st->done = 0;
+    __syncthreads();
+    if (R > 0 && R <= npos) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (above < R && R <= above + c4[u]) {
+                st->bstar = NBUCKET - 1 - (4 * t + u);
+                st->need = R - above;
+            }
+            above += c4[u];
+        }
+    }
 }
 
-__global__ void k_final(const unsigned long long *__restrict__ key, long long n, const SelectState *st,
-                        const long long *__restrict__ tie_rank, long long *__restrict__ ni) {
+__global__ void k_alloc_cands(const unsigned long long *__restrict__ key, long long n, AllocState *st,
+                              unsigned long long *__restrict__ ckey, int *__restrict__ cidx) {
+    const int bstar = st->bstar;
+    if (bstar == -2) return;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const long long i = base + threadIdx.x;
+        const bool in = i < n && rem_bucket(key[i]) == bstar;
+        const unsigned m = __ballot_sync(MCF_FULL, in);
+        if (!m) continue;
+        unsigned pos = 0;
+        if ((threadIdx.x & 31) == 0) pos = atomicAdd(&st->ncand, (unsigned)__popc(m));
+        pos = __shfl_sync(MCF_FULL, pos, 0);
+        if (in) {
+            const unsigned r = pos + __popc(m & lanemask_lt());
+            ckey[r] = key[i];
+            cidx[r] = (int)i;
+        }
+    }
+}
+
+// Exact k-th largest key among C candidates (MSB-first 8-bit radix), then the
+// k'-th smallest index among the candidates equal to it.
+__global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long *__restrict__ ckey,
+                                                       const int *__restrict__ cidx, AllocState *st) {
+    __shared__ unsigned h[256];
+    __shared__ unsigned long long s_pre, s_mask;
+    __shared__ long long s_k;
+    __shared__ long long wsum[32];
+    const int bstar = st->bstar;
+    if (bstar == -2) return;
+    const unsigned C = st->ncand;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) {
+        s_pre = 0;
+        s_mask = 0;
+        s_k = st->need;  // k-th largest inside the bucket
+    }
+    // pass over the key bits (largest first), then over the index bits (smallest first)
+    for (int phase = 0; phase < 2; ++phase) {
+        const int nbits = phase == 0 ? 64 : 32;
+        for (int shift = nbits - 8; shift >= 0; shift -= 8) {
+            if (t < 256) h[t] = 0;
+            __syncthreads();
+            const unsigned long long pre = s_pre, msk = s_mask;
+            for (unsigned c = t; c < C; c += blockDim.x) {
+                const unsigned long long k = ckey[c];
+                if (phase == 0) {
+                    if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255u], 1u);
+                } else if (k == st->T) {
+                    const unsigned long long ix = (unsigned)cidx[c];
+                    if ((ix & msk) == pre) atomicAdd(&h[(ix >> shift) & 255u], 1u);
+                }
+            }
+            __syncthreads();
+            // phase 0: bins from the top (largest keys); phase 1: from the bottom (smallest index)
+            long long own = 0;
+            if (t < 256) own = h[phase == 0 ? 255 - t : t];
+            long long x = own;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                long long y = __shfl_up_sync(MCF_FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[w] = x;
+            __syncthreads();
+            long long before = x - own;
+            for (int j = 0; j < w; ++j) before += wsum[j];
+            const long long k = s_k;
+            __syncthreads();
+            if (t < 256 && before < k && k <= before + own) {
+                const unsigned bin = phase == 0 ? 255 - t : t;
+                s_pre = pre | ((unsigned long long)bin << shift);
+                s_mask = msk | (255ull << shift);
+                s_k = k - before;
+            }
+            __syncthreads();
+        }
+        if (t == 0) {
+            if (phase == 0) {
+                st->T = s_pre;  // threshold key; s_k = how many of the ties to take
+                s_pre = 0;
+                s_mask = 0;
+            } else {
+                st->I = (long long)s_pre;  // largest selected index among the ties
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_alloc_final(const unsigned long long *__restrict__ key, long long n, const AllocState *st,
+                              long long *__restrict__ ni) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || st->left <= 0) return;
-    unsigned long long k = key[i], t = st->prefix;
-    if (k > t || (k == t && tie_rank[i] < st->k)) ni[i] += 1;
+    if (i >= n || st->bstar == -2) return;
+    const unsigned long long k = key[i], T = st->T;
+    if (k > T || (k == T && i <= st->I)) ni[i] += 1;
 }
 
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, cudaStream_t s) {
     MCF_ARG(g && ni && walk_pre, "mcf_allocate_walks: null argument");
     MCF_ARG(n_walks >= 1, "n_walks must be at least 1");  // walker.py:168-169
     MCF_ARG(n_walks < (1ll << 53), "n_walks must be below 2^53");
-    long long n = g->n;
-    SelectState *st = nullptr;
-    unsigned long long *key = nullptr;
-    long long *rank = nullptr;
-    MCF_CUDA(cudaMallocAsync(&st, sizeof(SelectState), s));
-    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * n, s));
-    MCF_CUDA(cudaMallocAsync(&rank, sizeof(long long) * (n + 1), s));
-    MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(SelectState), s));
-    unsigned nb = (unsigned)((n + 255) / 256);
-    k_floor<<<nb, 256, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, ni, key, st);
+    const long long n = g->n;
+    AllocState *st = nullptr;
+    unsigned long long *key = nullptr, *ckey = nullptr;
+    int *cidx = nullptr;
+    MCF_CUDA(cudaMallocAsync(&st, sizeof(AllocState), s));
+    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * n * 2 + sizeof(int) * n, s));
+    ckey = key + n;
+    cidx = reinterpret_cast<int *>(ckey + n);
+    MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(AllocState), s));
+    const int grid = sm_count() * 4;
+    k_alloc_floor<<<grid, 256, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, ni, key, st);
     mcf::note_launch();
-    long long want_blocks = (n + 2047) / 2048;
-    int hb = (int)(want_blocks < sm_count() * 2 ? (want_blocks > 0 ? want_blocks : 1) : sm_count() * 2);
-    for (int pass = 0; pass < 8; ++pass) {
-        k_select_pass<<<hb, 256, 0, s>>>(key, n, 56 - 8 * pass, st);
-        mcf::note_launch();
-    }
+    k_alloc_cands<<<grid, 256, 0, s>>>(key, n, st, ckey, cidx);
+    mcf::note_launch();
+    k_alloc_select<<<1, 1024, 0, s>>>(ckey, cidx, st);
+    mcf::note_launch();
+    k_alloc_final<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, n, st, ni);
+    mcf::note_launch();
     MCF_LAUNCHED("allocate");
-    // rank of each tied key among the ties (index order) = the stable argsort tie-break
-    ScanSrc ties{nullptr, key, &st->prefix};
-    int rc = scan_src(ties, rank, n, s);
-    if (rc) return rc;
-    k_final<<<nb, 256, 0, s>>>(key, n, st, rank, ni);
-    mcf::note_launch();
-    MCF_LAUNCHED("k_final");
-    rc = exclusive_scan_i64(ni, walk_pre, n, s);
+    int rc = exclusive_scan_i64(ni, walk_pre, n, s);
     if (rc) return rc;
     MCF_CUDA(cudaFreeAsync(st, s));
     MCF_CUDA(cudaFreeAsync(key, s));
-    MCF_CUDA(cudaFreeAsync(rank, s));
     return MCF_OK;
 }
 
