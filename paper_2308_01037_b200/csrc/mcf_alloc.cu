@@ -15,11 +15,11 @@ namespace mcf {
 //                    block finds the bucket b* that holds the R-th largest.
 //   2 k_alloc_cands  compacts the keys of bucket b* (with their index).
 //   3 k_alloc_select one CTA: exact radix select of the threshold key T among
-//                    the candidates, then -- among the keys equal to T -- the
-//                    index threshold I (ties go to the lowest indices, the
-//                    reference's stable argsort).
-//   4 k_alloc_final  N_i += key > T || (key == T && i <= I).
-//   5 scan           walk_pre.
+//                    the candidates (one distinct value: read off min/max)
+//   4 scan           rank of each key equal to T among those, in index order
+//   5 k_alloc_final  N_i += key > T || (key == T && rank < ties to take)
+//                    (ties go to the lowest indices, the reference's stable argsort)
+//   6 scan           walk_pre.
 // p_i = 0 keys (0) sit below every positive remainder; they are only reached
 // when R exceeds the number of positive p_i (then b* = -1 covers them).
 constexpr int NBUCKET = 1024;
@@ -33,7 +33,8 @@ struct AllocState {
     unsigned done;
     unsigned ncand;
     unsigned long long T;            // threshold key
-    long long I;                     // index threshold among keys == T
+    long long I;                     // how many of the keys == T to take (lowest indices)
+    unsigned long long cmin, cmax;   // smallest / largest candidate key
     unsigned hist[NBUCKET];
 };
 
@@ -144,90 +145,99 @@ __global__ void k_alloc_cands(const unsigned long long *__restrict__ key, long l
         unsigned pos = 0;
         if ((threadIdx.x & 31) == 0) pos = atomicAdd(&st->ncand, (unsigned)__popc(m));
         pos = __shfl_sync(MCF_FULL, pos, 0);
+        unsigned long long kk = in ? key[i] : 0ull;
+        unsigned long long mn = in ? kk : ~0ull, mx = kk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(MCF_FULL, mn, o), b = __shfl_xor_sync(MCF_FULL, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&st->cmin, mn);
+            atomicMax(&st->cmax, mx);
+        }
         if (in) {
             const unsigned r = pos + __popc(m & lanemask_lt());
-            ckey[r] = key[i];
+            ckey[r] = kk;
             cidx[r] = (int)i;
         }
     }
 }
 
-// Exact k-th largest key among C candidates (MSB-first 8-bit radix), then the
-// k'-th smallest index among the candidates equal to it.
-__global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long *__restrict__ ckey,
-                                                       const int *__restrict__ cidx, AllocState *st) {
+// Exact k-th largest key among the C candidates (MSB-first 8-bit radix).
+// Ties are the common case (equal-degree nodes share p): a bucket holding one
+// distinct value is answered from the min/max, and warps whose keys share a
+// digit add once.  The index tie-break is a scan afterwards.
+__global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long *__restrict__ ckey, AllocState *st) {
     __shared__ unsigned h[256];
     __shared__ unsigned long long s_pre, s_mask;
     __shared__ long long s_k;
     __shared__ long long wsum[32];
-    const int bstar = st->bstar;
-    if (bstar == -2) return;
-    const unsigned C = st->ncand;
+    if (st->bstar == -2) return;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (st->cmin == st->cmax) {  // a single distinct value: it is the threshold
+        if (t == 0) {
+            st->T = st->cmin;
+            st->I = st->need;
+        }
+        return;
+    }
+    const unsigned C = st->ncand;
     if (t == 0) {
         s_pre = 0;
         s_mask = 0;
-        s_k = st->need;  // k-th largest inside the bucket
+        s_k = st->need;
     }
-    // pass over the key bits (largest first), then over the index bits (smallest first)
-    for (int phase = 0; phase < 2; ++phase) {
-        const int nbits = phase == 0 ? 64 : 32;
-        for (int shift = nbits - 8; shift >= 0; shift -= 8) {
-            if (t < 256) h[t] = 0;
-            __syncthreads();
-            const unsigned long long pre = s_pre, msk = s_mask;
-            for (unsigned c = t; c < C; c += blockDim.x) {
-                const unsigned long long k = ckey[c];
-                if (phase == 0) {
-                    if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255u], 1u);
-                } else if (k == st->T) {
-                    const unsigned long long ix = (unsigned)cidx[c];
-                    if ((ix & msk) == pre) atomicAdd(&h[(ix >> shift) & 255u], 1u);
-                }
-            }
-            __syncthreads();
-            // phase 0: bins from the top (largest keys); phase 1: from the bottom (smallest index)
-            long long own = 0;
-            if (t < 256) own = h[phase == 0 ? 255 - t : t];
-            long long x = own;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                long long y = __shfl_up_sync(MCF_FULL, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) wsum[w] = x;
-            __syncthreads();
-            long long before = x - own;
-            for (int j = 0; j < w; ++j) before += wsum[j];
-            const long long k = s_k;
-            __syncthreads();
-            if (t < 256 && before < k && k <= before + own) {
-                const unsigned bin = phase == 0 ? 255 - t : t;
-                s_pre = pre | ((unsigned long long)bin << shift);
-                s_mask = msk | (255ull << shift);
-                s_k = k - before;
-            }
-            __syncthreads();
-        }
-        if (t == 0) {
-            if (phase == 0) {
-                st->T = s_pre;  // threshold key; s_k = how many of the ties to take
-                s_pre = 0;
-                s_mask = 0;
-            } else {
-                st->I = (long long)s_pre;  // largest selected index among the ties
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        if (t < 256) h[t] = 0;
+        __syncthreads();
+        const unsigned long long pre = s_pre, msk = s_mask;
+        for (unsigned base = 0; base < C; base += blockDim.x) {  // warp-uniform trip count
+            const unsigned c = base + t;
+            const unsigned long long k = c < C ? ckey[c] : ~0ull;
+            const bool in = c < C && (k & msk) == pre;
+            const unsigned dig = in ? (unsigned)((k >> shift) & 255u) : 256u;
+            const unsigned d0 = __shfl_sync(MCF_FULL, dig, 0);
+            if (__all_sync(MCF_FULL, dig == d0)) {
+                if (lane == 0 && d0 < 256u) atomicAdd(&h[d0], 32u);
+            } else if (in) {
+                atomicAdd(&h[dig], 1u);
             }
         }
         __syncthreads();
+        long long own = t < 256 ? h[255 - t] : 0;  // bins from the top (largest keys first)
+        long long x = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(MCF_FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        long long before = x - own;
+        for (int j = 0; j < w; ++j) before += wsum[j];
+        const long long k = s_k;
+        __syncthreads();
+        if (t < 256 && before < k && k <= before + own) {
+            s_pre = pre | ((unsigned long long)(255 - t) << shift);
+            s_mask = msk | (255ull << shift);
+            s_k = k - before;
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        st->T = s_pre;
+        st->I = s_k;  // ties (key == T) to take, lowest indices first
     }
 }
 
 __global__ void k_alloc_final(const unsigned long long *__restrict__ key, long long n, const AllocState *st,
-                              long long *__restrict__ ni) {
+                              const long long *__restrict__ tie_rank, long long *__restrict__ ni) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || st->bstar == -2) return;
     const unsigned long long k = key[i], T = st->T;
-    if (k > T || (k == T && i <= st->I)) ni[i] += 1;
+    if (k > T || (k == T && tie_rank[i] < st->I)) ni[i] += 1;
 }
 
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, cudaStream_t s) {
@@ -239,18 +249,23 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     unsigned long long *key = nullptr, *ckey = nullptr;
     int *cidx = nullptr;
     MCF_CUDA(cudaMallocAsync(&st, sizeof(AllocState), s));
-    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * n * 2 + sizeof(int) * n, s));
+    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * n * 3 + 8 + sizeof(int) * n, s));
     ckey = key + n;
-    cidx = reinterpret_cast<int *>(ckey + n);
+    long long *rank = reinterpret_cast<long long *>(ckey + n);
+    cidx = reinterpret_cast<int *>(rank + n + 1);
     MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(AllocState), s));
+    MCF_CUDA(cudaMemsetAsync(&st->cmin, 0xff, sizeof(unsigned long long), s));
     const int grid = sm_count() * 4;
     k_alloc_floor<<<grid, 256, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, ni, key, st);
     mcf::note_launch();
     k_alloc_cands<<<grid, 256, 0, s>>>(key, n, st, ckey, cidx);
     mcf::note_launch();
-    k_alloc_select<<<1, 1024, 0, s>>>(ckey, cidx, st);
+    k_alloc_select<<<1, 1024, 0, s>>>(ckey, st);
     mcf::note_launch();
-    k_alloc_final<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, n, st, ni);
+    ScanSrc ties{nullptr, key, &st->T};  // rank among the keys equal to T (index order)
+    int rc0 = scan_src(ties, rank, n, s);
+    if (rc0) return rc0;
+    k_alloc_final<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, n, st, rank, ni);
     mcf::note_launch();
     MCF_LAUNCHED("allocate");
     int rc = exclusive_scan_i64(ni, walk_pre, n, s);
