@@ -184,6 +184,68 @@ __global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long 
         return;
     }
     const unsigned C = st->ncand;
+    // (1) distinct values with their counts in a shared hash (ties are few, large groups)
+    constexpr int HS = 2048;
+    __shared__ unsigned long long hk[HS];
+    __shared__ unsigned hc[HS];
+    __shared__ unsigned s_nd;
+    __shared__ int s_over;
+    for (int j = t; j < HS; j += blockDim.x) {
+        hk[j] = ~0ull;
+        hc[j] = 0;
+    }
+    if (t == 0) {
+        s_nd = 0;
+        s_over = 0;
+    }
+    __syncthreads();
+    for (unsigned base = 0; base < C && !s_over; base += blockDim.x) {
+        const unsigned c = base + t;
+        const bool valid = c < C;
+        const unsigned long long k = valid ? ckey[c] : 0ull;
+        const unsigned m = __ballot_sync(MCF_FULL, valid);
+        const unsigned long long d0 = __shfl_sync(MCF_FULL, k, 0);
+        const bool same = __all_sync(MCF_FULL, !valid || k == d0);
+        if (same ? (lane == 0) : valid) {
+            const unsigned cnt = same ? (unsigned)__popc(m) : 1u;
+            const unsigned long long kk = same ? d0 : k;
+            unsigned slot = (unsigned)((kk * 0x9E3779B97F4A7C15ull) >> 53);  // 11 bits
+            for (int probe = 0; probe < HS; ++probe) {
+                unsigned long long cur = hk[slot];
+                if (cur == ~0ull) {
+                    cur = atomicCAS(&hk[slot], ~0ull, kk);
+                    if (cur == ~0ull) {
+                        if (atomicAdd(&s_nd, 1u) >= HS / 2) s_over = 1;
+                        cur = kk;
+                    }
+                }
+                if (cur == kk) {
+                    atomicAdd(&hc[slot], cnt);
+                    break;
+                }
+                slot = (slot + 1) & (HS - 1);
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (!s_over) {
+        // the k-th largest: count above each distinct value (distinct values <= HS/2)
+        const long long need = st->need;
+        for (int j = t; j < HS; j += blockDim.x) {
+            const unsigned long long v = hk[j];
+            if (v == ~0ull) continue;
+            long long above = 0;
+            for (int f = 0; f < HS; ++f)
+                if (hk[f] != ~0ull && hk[f] > v) above += hc[f];
+            if (above < need && need <= above + (long long)hc[j]) {
+                st->T = v;
+                st->I = need - above;
+            }
+        }
+        return;
+    }
+    // (2) fallback: exact MSB-first radix over the candidates
     if (t == 0) {
         s_pre = 0;
         s_mask = 0;
