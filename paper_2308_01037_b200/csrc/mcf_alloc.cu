@@ -35,7 +35,11 @@ struct AllocState {
     unsigned long long T;            // threshold key
     long long I;                     // how many of the keys == T to take (lowest indices)
     unsigned long long cmin, cmax;   // smallest / largest candidate key
+    int b2;                          // sub-bucket of b* holding the R-th largest (-1: none / not refined)
+    int resolved;                    // T and the tie count are known (no candidate pass needed)
     unsigned hist[NBUCKET];
+    unsigned hist2[NBUCKET];
+    unsigned long long min2[NBUCKET], max2[NBUCKET];
 };
 
 __device__ __forceinline__ int rem_bucket(unsigned long long key) {
@@ -43,6 +47,45 @@ __device__ __forceinline__ int rem_bucket(unsigned long long key) {
     const double rem = __longlong_as_double((long long)(key - 1));
     const int b = (int)(rem * NBUCKET);
     return b < NBUCKET ? b : NBUCKET - 1;
+}
+
+// second level: position inside bucket b (monotone in the remainder)
+__device__ __forceinline__ int rem_sub(unsigned long long key, int b) {
+    const double rem = __longlong_as_double((long long)(key - 1));
+    const int s = (int)((rem * NBUCKET - b) * NBUCKET);
+    return s < 0 ? 0 : (s < NBUCKET ? s : NBUCKET - 1);
+}
+
+// top-down search over 1024 counts held 4 per thread (256 threads): the bin
+// with count(above) < R <= count(above) + count(bin); returns via *bin/*need
+__device__ void find_bin(const unsigned *cnt, long long R, int *bin, long long *need) {
+    __shared__ long long wsum[8];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    long long c4[4], own = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        c4[u] = (long long)atomicAdd(const_cast<unsigned *>(&cnt[NBUCKET - 1 - (4 * t + u)]), 0u);
+        own += c4[u];
+    }
+    long long x = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(MCF_FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    long long above = x - own;
+    for (int j = 0; j < w; ++j) above += wsum[j];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if (above < R && R <= above + c4[u]) {
+            *bin = NBUCKET - 1 - (4 * t + u);
+            *need = R - above;
+        }
+        above += c4[u];
+    }
+    __syncthreads();
 }
 
 // block-parallel search from the top bucket: thread t holds bucket NBUCKET-1-t*4..; finds b with
@@ -89,57 +132,105 @@ __global__ void __launch_bounds__(256) k_alloc_floor(const double *__restrict__ 
     __threadfence();
     const long long R = n_walks - (long long)atomicAdd(&st->total_floor, 0ull);
     const long long npos = (long long)atomicAdd(&st->n_pos, 0ull);
-    // suffix counts: thread t owns buckets [NBUCKET-4(t+1), NBUCKET-4t) (4 per thread, top first)
-    const int t = threadIdx.x;
-    long long c4[4], own = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        c4[u] = (long long)atomicAdd(&st->hist[NBUCKET - 1 - (4 * t + u)], 0u);
-        own += c4[u];
-    }
-    long long x = own;
-    const int lane = t & 31, w = t >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        long long y = __shfl_up_sync(MCF_FULL, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    long long above = x - own;
-    for (int j = 0; j < w; ++j) above += wsum[j];
-    if (t == 0) {
+    if (threadIdx.x == 0) {
         st->left = R;
         st->bstar = -2;  // nothing to select
         st->need = 0;
         st->done = 0;
         st->ncand = 0;
+        st->b2 = -1;
+        st->resolved = 0;
         if (R > npos) {  // every positive key, plus the lowest-index p == 0 entries
             st->bstar = -1;
             st->need = R - npos;
+            st->T = 0;
+            st->I = R - npos;
+            st->resolved = 1;
         }
     }
     __syncthreads();
-    if (R > 0 && R <= npos) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (above < R && R <= above + c4[u]) {
-                st->bstar = NBUCKET - 1 - (4 * t + u);
-                st->need = R - above;
+    if (R > 0 && R <= npos) find_bin(st->hist, R, &st->bstar, &st->need);
+}
+
+// Level 2: histogram of bucket b* into 1024 sub-buckets with per-sub-bucket
+// min/max key; the last block picks the sub-bucket, and if it holds a single
+// distinct value (the usual case: equal-degree ties) T is resolved here.
+__global__ void __launch_bounds__(256) k_alloc_level2(const unsigned long long *__restrict__ key, long long n,
+                                                      AllocState *st) {
+    __shared__ unsigned h[NBUCKET];
+    __shared__ unsigned long long mn[NBUCKET], mx[NBUCKET];
+    __shared__ bool last;
+    const int bstar = st->bstar;
+    if (bstar < 0) return;
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) {
+        h[b] = 0;
+        mn[b] = ~0ull;
+        mx[b] = 0;
+    }
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const long long i = base + threadIdx.x;
+        const unsigned long long k = i < n ? key[i] : 0ull;
+        const bool in = i < n && rem_bucket(k) == bstar;
+        const int sb = in ? rem_sub(k, bstar) : -1;
+        const int s0 = __shfl_sync(MCF_FULL, sb, 0);
+        const unsigned long long k0 = __shfl_sync(MCF_FULL, k, 0);
+        if (__all_sync(MCF_FULL, in && k == k0)) {  // one tied key across the warp
+            if ((threadIdx.x & 31) == 0) {
+                atomicAdd(&h[s0], 32u);
+                atomicMin(&mn[s0], k0);
+                atomicMax(&mx[s0], k0);
             }
-            above += c4[u];
+        } else if (in) {
+            atomicAdd(&h[sb], 1u);
+            atomicMin(&mn[sb], k);
+            atomicMax(&mx[sb], k);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) {
+        if (h[b]) {
+            atomicAdd(&st->hist2[b], h[b]);
+            atomicMin(&st->min2[b], mn[b]);
+            atomicMax(&st->max2[b], mx[b]);
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    int b2 = -1;
+    long long need2 = 0;
+    __shared__ int s_b2;
+    __shared__ long long s_need2;
+    if (threadIdx.x == 0) s_b2 = -1;
+    __syncthreads();
+    find_bin(st->hist2, st->need, &s_b2, &s_need2);
+    b2 = s_b2;
+    need2 = s_need2;
+    if (threadIdx.x == 0) {
+        st->b2 = b2;
+        st->need = need2;
+        const unsigned long long lo = atomicAdd(&st->min2[b2], 0ull), hi = atomicMax(&st->max2[b2], 0ull);
+        if (lo == hi) {  // single distinct value: it is the threshold
+            st->T = lo;
+            st->I = need2;
+            st->resolved = 1;
         }
     }
 }
 
 __global__ void k_alloc_cands(const unsigned long long *__restrict__ key, long long n, AllocState *st,
                               unsigned long long *__restrict__ ckey, int *__restrict__ cidx) {
-    const int bstar = st->bstar;
-    if (bstar == -2) return;
+    const int bstar = st->bstar, b2 = st->b2;
+    if (bstar < 0 || st->resolved) return;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
         const long long i = base + threadIdx.x;
-        const bool in = i < n && rem_bucket(key[i]) == bstar;
+        const bool in = i < n && rem_bucket(key[i]) == bstar && rem_sub(key[i], bstar) == b2;
         const unsigned m = __ballot_sync(MCF_FULL, in);
         if (!m) continue;
         unsigned pos = 0;
@@ -174,7 +265,7 @@ __global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long 
     __shared__ unsigned long long s_pre, s_mask;
     __shared__ long long s_k;
     __shared__ long long wsum[32];
-    if (st->bstar == -2) return;
+    if (st->bstar == -2 || st->resolved) return;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (st->cmin == st->cmax) {  // a single distinct value: it is the threshold
         if (t == 0) {
@@ -317,8 +408,11 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     cidx = reinterpret_cast<int *>(rank + n + 1);
     MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(AllocState), s));
     MCF_CUDA(cudaMemsetAsync(&st->cmin, 0xff, sizeof(unsigned long long), s));
+    MCF_CUDA(cudaMemsetAsync(st->min2, 0xff, sizeof(st->min2), s));
     const int grid = sm_count() * 4;
     k_alloc_floor<<<grid, 256, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, ni, key, st);
+    mcf::note_launch();
+    k_alloc_level2<<<grid, 256, 0, s>>>(key, n, st);
     mcf::note_launch();
     k_alloc_cands<<<grid, 256, 0, s>>>(key, n, st, ckey, cidx);
     mcf::note_launch();
