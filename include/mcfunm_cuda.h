@@ -172,6 +172,14 @@ MCF_API int mcf_replay_diag(mcf_graph *g, const mcf_walk_params *p, const int64_
                     int64_t col_begin, int64_t col_end, const int64_t *walk_off,
                     const int32_t *entries, double *pcol, int64_t *stats, void *stream);
 
+/* Dense rows of Q for the full estimator (Alg. 2,
+ * Eq. 18-19): Q[(c - col_begin) * ldq + j] = sum over visits of j by the walks
+ * from column c of zeta_{k+2} W_k, for c in [col_begin, col_end).  The caller
+ * forms f(A) ~ zeta_0 I + zeta_1 A + A Q A block by block (dense GEMMs).
+ * Needs n <= 16384 (else MCF_ERR_RESOURCE); synchronises `stream`. */
+MCF_API int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin,
+                            int64_t col_end, double *Q, int64_t ldq, int64_t *stats, void *stream);
+
 /* d_i = zeta_0 + zeta_1 a_ii + sum_{c} pcol[(i,c)] for rows [row_begin, row_end)
  * (Eq. 20 final sum), fixed summation order. */
 MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d,

@@ -16,7 +16,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-dependent parts load lazily so host-only use stays cheap
-    if name in ("rand_funm_diag", "rand_funm_action", "rand_funm_entry", "mc_baseline", "FunmResult"):
+    if name in ("rand_funm", "rand_funm_diag", "rand_funm_action", "rand_funm_entry", "mc_baseline", "FunmResult"):
         from . import estimators
         return getattr(estimators, name)
     if name in ("subgraph_centrality", "total_communicability", "katz_centrality", "estrada_index",

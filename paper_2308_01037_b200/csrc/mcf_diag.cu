@@ -655,6 +655,95 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     return rc;
 }
 
+// Dense rows of Q for the full estimator (rand_funm): one
+// CTA per column c, Q_c accumulated in a shared dense int64 row in fixed point
+// (scale from the walk kernel's per-column max: deterministic), then written
+// as fp64 to Q[(c - cb) * ldq + j].
+constexpr int QDENSE_MAX_N = 16384;  // 128 KB shared row
+
+__global__ void __launch_bounds__(512) k_qdense(const long long *__restrict__ walk_pre, long long cb, long long ce,
+                                                long long wb, const long long *__restrict__ eoff,
+                                                const int *__restrict__ est, const double *__restrict__ ewt,
+                                                const unsigned long long *__restrict__ colmax, long long n,
+                                                double *__restrict__ Q, long long ldq) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    long long *row = reinterpret_cast<long long *>(smem_raw);
+    for (long long c = cb + blockIdx.x; c < ce; c += gridDim.x) {
+        for (long long j = threadIdx.x; j < n; j += blockDim.x) row[j] = 0;
+        __syncthreads();
+        const long long g0 = walk_pre[c], g1 = walk_pre[c + 1];
+        const long long s0 = eoff[g0 - wb], m = eoff[g1 - wb] - s0;
+        const double maxw = __longlong_as_double((long long)colmax[c]);
+        int lg_m = 0;
+        while ((1ll << lg_m) < m) ++lg_m;
+        const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;
+        for (long long i = threadIdx.x; i < m; i += blockDim.x) {
+            const int s = est[s0 + i];
+            if (s >= 0)
+                atomicAdd(reinterpret_cast<unsigned long long *>(&row[s]),
+                          (unsigned long long)__double2ll_rn(ldexp(ewt[s0 + i], E)));
+        }
+        __syncthreads();
+        double *out = Q + (c - cb) * ldq;
+        for (long long j = threadIdx.x; j < n; j += blockDim.x) out[j] = ldexp((double)row[j], -E);
+        __syncthreads();
+    }
+}
+
+static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                  double *Q, long long ldq, long long *stats, cudaStream_t s) {
+    int rc = check_params(g, p, walk_pre, cb, ce);
+    if (rc) return rc;
+    MCF_ARG(Q && stats && ldq >= g->n, "mcf_walk_qdense: null Q/stats or ldq < n");
+    if (g->n > QDENSE_MAX_N) {
+        set_error("dense Q rows need n <= 16384 (use rand_funm_diag / rand_funm_action for larger graphs)");
+        return MCF_ERR_RESOURCE;
+    }
+    long long wb = 0, we = 0;
+    rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
+    if (rc) return rc;
+    MCF_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * ldq * (ce - cb), s));
+    if (we == wb) return MCF_OK;
+    const long long nw = we - wb;
+    unsigned long long *colmax = nullptr;
+    long long *elen = nullptr;
+    int *err = nullptr;
+    MCF_CUDA(cudaMallocAsync(&colmax, sizeof(unsigned long long) * g->n, s));
+    MCF_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * g->n, s));
+    MCF_CUDA(cudaMallocAsync(&elen, sizeof(long long) * (2 * nw + 1) + 16, s));
+    long long *eoff = elen + nw;
+    err = reinterpret_cast<int *>(eoff + nw + 1);
+    MCF_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+    rc = launch_walk_emit(g, p, walk_pre, cb, ce, nw, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
+                          nullptr, stats, err, s);
+    if (rc) return rc;
+    rc = exclusive_scan_i64(elen, eoff, nw, s);
+    if (rc) return rc;
+    long long total = 0;
+    MCF_CUDA(cudaMemcpyAsync(&total, eoff + nw, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    MCF_ARG(total <= 4 * emission_budget(), "too many emissions for one dense-Q call (split the column range)");
+    int *est = nullptr;
+    double *ewt = nullptr;
+    MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * (total > 0 ? total : 1), s));
+    MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * (total > 0 ? total : 1), s));
+    rc = launch_walk_emit(g, p, walk_pre, cb, ce, nw, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, colmax,
+                          stats, err, s);
+    if (rc) return rc;
+    const size_t smem = sizeof(long long) * g->n;
+    MCF_CUDA(cudaFuncSetAttribute(k_qdense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    long long nc = ce - cb;
+    int grid = (int)(nc < 4 * sm_count() ? nc : 4 * sm_count());
+    k_qdense<<<grid, 512, smem, s>>>(walk_pre, cb, ce, wb, eoff, est, ewt, colmax, g->n, Q, ldq);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_qdense");
+    cudaFreeAsync(est, s);
+    cudaFreeAsync(ewt, s);
+    cudaFreeAsync(elen, s);
+    cudaFreeAsync(colmax, s);
+    return MCF_OK;
+}
+
 static int diag_combine(mcf_graph *g, double z0, double z1, const double *pcol, double *d, long long rb, long long re,
                         cudaStream_t s) {
     MCF_ARG(g && pcol && d, "mcf_diag_combine: null argument");
@@ -685,6 +774,12 @@ int mcf_replay_diag(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_
                     void *stream) {
     return mcf::diag(g, p, (const long long *)walk_pre, col_begin, col_end, (const long long *)walk_off, entries, pcol,
                      (long long *)stats, (cudaStream_t)stream, true);
+}
+
+int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin,
+                    int64_t col_end, double *Q, int64_t ldq, int64_t *stats, void *stream) {
+    return mcf::qdense(g, p, (const long long *)walk_pre, col_begin, col_end, Q, ldq, (long long *)stats,
+                       (cudaStream_t)stream);
 }
 
 int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d, int64_t row_begin,

@@ -245,6 +245,13 @@ class DeviceGraph:
                                         _ptr(walk_off), _ptr(entries), _ptr(pcol), _ptr(stats), self.stream),
                 "mcf_replay_diag")
 
+    def walk_qdense(self, params: WalkParams, walk_pre, Q, cols, stats=None):
+        """Dense rows Q[c - cols[0], :] of the walk matrix for c in cols."""
+        cb, ce = cols
+        N.check(N.lib().mcf_walk_qdense(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce), _ptr(Q),
+                                        int(Q.stride(0)), _ptr(stats), self.stream), "mcf_walk_qdense")
+        return Q
+
     def diag_combine(self, z0, z1, pcol, d=None, rows=None):
         d = self._f64() if d is None else d
         rb, re = (0, self.n) if rows is None else rows

@@ -280,3 +280,39 @@ def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None 
                      config=_cfg_echo(cfg, coeffs, smode))
     _stats(res, st)
     return res
+
+
+def rand_funm(a, coeffs, config, *, block: int = 1024, device=None, as_tensor: bool = False) -> FunmResult:
+    """Full matrix estimate F ~ f(A) = zeta_0 I + zeta_1 A + A Q A (PAPER.md
+    Alg. 2 / Eq. 19), Q assembled in row blocks of ``block``
+    columns so one block of Q is live at a time.  The walks and Q rows run in
+    libmcfunm_cuda; the two products per block are dense fp64 GEMMs (cuBLAS).
+    Dense output: n <= 16384 (ResourceError otherwise, advising the diag or
+    action estimators)."""
+    from .errors import ResourceError
+    cfg = check_config(config)
+    coeffs = as_stream(coeffs)
+    n, nnz = _n_nnz(a)
+    z = coeffs.prefix(cfg.max_steps + 2)
+    if n > 16384:
+        raise ResourceError(f"the dense estimate needs n <= 16384 (got n={n}): use rand_funm_diag / rand_funm_action")
+    if nnz == 0:  # A = 0 -> zeta_0 I exactly (SPEC.md:354)
+        return FunmResult(z[0] * np.eye(n), "full", config=_cfg_echo(cfg, coeffs, "philox"))
+    g = _graph(a, device)
+    params = WalkParams(cfg, z, g.device)
+    ni, pre = g.allocate(cfg.n_walks)
+    A = torch.zeros((n, n), dtype=torch.float64, device=g.device)
+    rows = torch.repeat_interleave(torch.arange(n, device=g.device), g.row_ptr.diff())
+    A[rows, g.col_ids.to(torch.int64)] = g.vals
+    F = z[0] * torch.eye(n, dtype=torch.float64, device=g.device) + z[1] * A
+    st = g.new_stats()
+    Qb = torch.empty((min(block, n), n), dtype=torch.float64, device=g.device)
+    for cb in range(0, n, block):
+        ce = min(n, cb + block)
+        q = Qb[: ce - cb]
+        g.walk_qdense(params, pre, q, (cb, ce), stats=st)
+        F += A[:, cb:ce] @ (q @ A)  # C_c Q_c A summed over the block's columns (Eq. 19)
+    res = FunmResult(F if as_tensor else F.cpu().numpy(), "full", config=_cfg_echo(cfg, coeffs, "philox"))
+    _stats(res, st)
+    res.aux = {"ni": ni, "walk_pre": pre}
+    return res

@@ -396,3 +396,26 @@ def test_diag_hub_push_path_bitwise_and_replay(mc):
     g = mc.DeviceGraph(as_matrix(a, True))
     out = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(5000 * 4, 1e-300, 20, 3), replay=run.record)
     assert rel_err(out.values, run.payload) < REL
+
+
+def test_rand_funm_full_consistency_and_closed_form(mc):
+    """SPEC acceptance 4: diag(rand_funm) == rand_funm_diag (shared seed) to
+    1e-12 relative on 16-node instances; SPEC.md:352 closed form; A = 0."""
+    rng = np.random.default_rng(1)
+    for trial in range(3):
+        d = (rng.random((16, 16)) < 0.3).astype(float)
+        d = np.triu(d, 1)
+        d = d + d.T
+        a = mc.SparseMatrix.from_dense(d * 0.2, True)
+        cfg = mc.WalkConfig(20_000, 1e-10, 60, trial)
+        full = mc.rand_funm(a, mc.EXPONENTIAL, cfg, block=5).values
+        diag = mc.rand_funm_diag(a, mc.EXPONENTIAL, cfg).values
+        np.testing.assert_allclose(np.diag(full), diag, rtol=1e-12)
+        exact = port.dense_funm(port.Csr.from_dense(d * 0.2), "exponential", 64)
+        assert np.max(np.abs(full - exact)) < 5e-2
+    a2 = mc.SparseMatrix.from_dense([[0, 0.1], [0.1, 0]], True)
+    f2 = mc.rand_funm(a2, mc.EXPONENTIAL, mc.WalkConfig(10**6, 1e-10, 10_000, 0)).values
+    np.testing.assert_allclose(f2, [[np.cosh(0.1), np.sinh(0.1)], [np.sinh(0.1), np.cosh(0.1)]], atol=5e-3)
+    z = mc.rand_funm(mc.SparseMatrix(sparse.csr_array((3, 3)), sparse.csc_array((3, 3))), mc.EXPONENTIAL,
+                     mc.WalkConfig(10)).values
+    assert np.array_equal(z, np.eye(3))
