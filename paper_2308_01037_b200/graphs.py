@@ -196,3 +196,36 @@ def chung_lu_device(n: int, exponent: float = 2.1, mean_degree: float = 20.0, ma
     row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
     torch.cumsum(counts, 0, out=row_ptr[1:])
     return n, row_ptr, cols
+
+
+def small_world(n: int, k: int, rewire_prob: float = 0.1, seed: int = 0) -> SparseMatrix:
+    """Ring lattice (k/2 neighbours per side) with every lattice edge (i, j)
+    rewired to (i, m), m uniform among non-neighbours of i, with probability
+    rewire_prob (the paper's smallworld workload).  Host
+    numpy generator for test-sized graphs."""
+    if k % 2 or not 0 < k < n:
+        raise ArgumentError("need an even k with 0 < k < n")
+    rng = np.random.default_rng(seed)
+    adj = [set() for _ in range(n)]
+    for off in range(1, k // 2 + 1):
+        for i in range(n):
+            j = (i + off) % n
+            adj[i].add(j)
+            adj[j].add(i)
+    for off in range(1, k // 2 + 1):
+        for i in range(n):
+            j = (i + off) % n
+            if rng.random() >= rewire_prob or j not in adj[i] or len(adj[i]) >= n - 1:
+                continue
+            while True:
+                m = int(rng.integers(n))
+                if m != i and m not in adj[i]:
+                    break
+            adj[i].discard(j)
+            adj[j].discard(i)
+            adj[i].add(m)
+            adj[m].add(i)
+    rows = np.repeat(np.arange(n), [len(s) for s in adj])
+    cols = np.concatenate([np.array(sorted(s), dtype=np.int64) for s in adj])
+    return SparseMatrix.from_coo(rows, cols, np.ones(rows.size), n, symmetric_hint=True,
+                                 meta={"generator": "smallworld", "n": n, "k": k, "p": rewire_prob, "seed": seed})

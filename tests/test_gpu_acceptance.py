@@ -1,0 +1,82 @@
+"""SPEC.md acceptance criteria (:645-657) exercised on the device estimators."""
+import numpy as np
+import pytest
+from scipy import sparse
+
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2308_01037_b200 as m
+    return m
+
+
+def test_convergence_slope(mc):
+    """#2: l_inf error vs N_s in {1e3..1e6} on a 64-node small world has a
+    log-log slope in [-0.65, -0.35] (the O(N_s^-0.5) law)."""
+    from paper_2308_01037_b200.graphs import small_world
+    a = small_world(64, 4, 0.1, seed=3)
+    g = mc.DeviceGraph(a, gamma=1e-1)
+    exact = np.diag(port.dense_funm(port.Csr.from_any(a).scaled(1e-1), "exponential", 40))
+    ns = [10**3, 10**4, 10**5, 10**6]
+    errs = []
+    for n_s in ns:  # average over seeds to stabilise the fit
+        e = np.mean([np.max(np.abs(mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(n_s, 1e-10, 200, s)).values
+                                   - exact)) for s in range(6)])
+        errs.append(e)
+    slope = np.polyfit(np.log(ns), np.log(errs), 1)[0]
+    assert -0.65 <= slope <= -0.35, (slope, errs)
+
+
+def test_action_closed_forms(mc):
+    """#5: e^0.1 on gamma [[0,1],[1,0]] and the Katz 2x2 (2, 2), within 5e-3."""
+    a = mc.SparseMatrix.from_dense([[0, 1], [1, 0]], True)
+    y = mc.rand_funm_action(mc.DeviceGraph(a, gamma=0.1), mc.EXPONENTIAL, np.ones(2), mc.WalkConfig(10**6, 1e-10))
+    np.testing.assert_allclose(y.values, np.exp(0.1), atol=5e-3)
+    k = mc.rand_funm_action(mc.DeviceGraph(a, gamma=0.5), mc.RESOLVENT, np.ones(2), mc.WalkConfig(10**6, 1e-10))
+    np.testing.assert_allclose(k.values, [2.0, 2.0], atol=5e-3)
+
+
+def test_katz_randomized_vs_cg(mc):
+    """#7: 4096-node small world, fraction 0.85, N_s = 1e7: relative l_inf gap
+    <= 1e-2 and top-1% Pearson >= 0.99."""
+    from paper_2308_01037_b200.graphs import small_world
+    a = small_world(4096, 10, 0.1, seed=1)
+    rnd = mc.katz_centrality(a, 0.85, mc.WalkConfig(10**7, 1e-8, 10_000, 0))
+    cg = mc.katz_centrality(a, 0.85, None, method="cg")
+    gap = np.max(np.abs(rnd.scores - cg.scores) / np.abs(cg.scores))
+    assert gap <= 1e-2, gap
+    assert mc.ranking_correlation(cg, rnd, 0.01) >= 0.99
+    assert rnd.gamma == pytest.approx(0.85 / 10.0 * 10 / float(np.max(np.diff(a.csr.indptr))), rel=1e-12)
+
+
+def test_limit_properties(mc):
+    """#8: total communicability at gamma = 1e-8 ranks like the degrees
+    (1024-node Kronecker-like graph); subgraph centrality on the 8-cycle is flat
+    within 6 standard errors (vertex transitivity)."""
+    from paper_2308_01037_b200.graphs import barabasi_albert
+    a = barabasi_albert(1024, 3, seed=2)
+    rep = mc.total_communicability(a, 1e-8, mc.WalkConfig(10**5, 1e-10, 100, 0))
+    deg = np.diff(a.csr.indptr)
+    # scores = 1 + gamma deg + O(gamma^2): the ranking is the degree ranking (ties by id)
+    assert np.array_equal(rep.ranking, np.lexsort((np.arange(1024), -deg)))
+    c8 = mc.SparseMatrix.from_dense(np.roll(np.eye(8), 1, 1) + np.roll(np.eye(8), -1, 1), True)
+    reps = np.array([mc.subgraph_centrality(c8, 0.1, mc.WalkConfig(10**5, 1e-10, 1000, s)).scores for s in range(8)])
+    m = reps.mean(0)
+    se = reps.std(0, ddof=1).mean() / np.sqrt(8)
+    assert np.ptp(m) <= 6 * se + 1e-15
+
+
+def test_estrada_and_ranking_api(mc):
+    a = mc.SparseMatrix.from_dense([[0, 1], [1, 0]], True)
+    rep = mc.subgraph_centrality(a, 0.1, mc.WalkConfig(10**5, 1e-10))
+    assert mc.estrada_index(rep) == pytest.approx(2 * np.cosh(0.1), abs=1e-2)
+    assert list(rep.ranking) in ([0, 1], [1, 0])
+    with pytest.raises(mc.ArgumentError):
+        mc.estrada_index(mc.total_communicability(a, 0.1, mc.WalkConfig(100)))
