@@ -64,8 +64,9 @@ def test_limit_properties(mc):
     a = barabasi_albert(1024, 3, seed=2)
     rep = mc.total_communicability(a, 1e-8, mc.WalkConfig(10**5, 1e-10, 100, 0))
     deg = np.diff(a.csr.indptr)
-    # scores = 1 + gamma deg + O(gamma^2): the ranking is the degree ranking (ties by id)
-    assert np.array_equal(rep.ranking, np.lexsort((np.arange(1024), -deg)))
+    # scores = 1 + gamma deg + O(gamma^2): the ranking is a degree ranking (equal
+    # degrees may order either way at second order)
+    assert np.all(np.diff(deg[rep.ranking]) <= 0)
     c8 = mc.SparseMatrix.from_dense(np.roll(np.eye(8), 1, 1) + np.roll(np.eye(8), -1, 1), True)
     reps = np.array([mc.subgraph_centrality(c8, 0.1, mc.WalkConfig(10**5, 1e-10, 1000, s)).scores for s in range(8)])
     m = reps.mean(0)
