@@ -280,7 +280,7 @@ def run_device(args, cfg):
 
     import paper_2308_01037_b200 as mc
     from paper_2308_01037_b200 import _native, parallel
-    from paper_2308_01037_b200.device import DeviceGraph, WalkParams
+    from paper_2308_01037_b200.device import DeviceGraph, WalkParams, to_host
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -428,7 +428,7 @@ def run_device(args, cfg):
                 y, _ = parallel.sharded_action(ge, coeffs, ve, wcfg)
             else:
                 y, _ = parallel.sharded_diag(ge, coeffs, wcfg)
-            host = y.cpu().numpy()
+            host = to_host(y)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t1
             ge.close()
@@ -443,7 +443,7 @@ def run_device(args, cfg):
         e2e = {"value": em_per_step * len(e2e_ms) / (e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / len(e2e_ms),
                "nodes_per_s": g.n * len(e2e_ms) / (e_ms / 1e3),
-               "path": "DeviceGraph(host SparseMatrix, gamma) + estimator + y.cpu(): pinned H2D of CSR, D2H of y"}
+               "path": "DeviceGraph(host SparseMatrix, gamma) + estimator + y to host: pinned H2D of CSR, pinned D2H of y"}
 
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     cpu = None

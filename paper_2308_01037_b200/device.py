@@ -27,6 +27,15 @@ def require_cuda(device=None) -> torch.device:
     return dev
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy through a page-locked buffer (the copy runs at
+    PCIe DMA speed instead of staging through pageable memory)."""
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return out.numpy()
+
+
 def _same_storage(csr, csc) -> bool:
     """CSC arrays of a symmetric matrix that are (or equal) the CSR arrays."""
     if csc.indptr is csr.indptr and csc.indices is csr.indices and csc.data is csr.data:

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .device import DeviceGraph, WalkParams
+from .device import DeviceGraph, WalkParams, to_host
 from .errors import ArgumentError
 from .series import as_stream
 from .walker import check_config
@@ -123,7 +123,7 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
         off, ent = _replay_tensors(g, replay)
         g.replay_action(params, pre, off, ent, r, q, stats=st)
     y = g.spmv(q, alpha=z[0], v=vd, beta=z[1], r=r)   # y = z0 v + z1 r + A q
-    res = FunmResult(y if as_tensor else y.cpu().numpy(), "action", config=_cfg_echo(cfg, coeffs, mode))
+    res = FunmResult(y if as_tensor else to_host(y), "action", config=_cfg_echo(cfg, coeffs, mode))
     _stats(res, st)
     res.aux = {"q": q, "r": r, "ni": ni, "walk_pre": pre}
     if stderr:
@@ -160,7 +160,7 @@ def rand_funm_diag(a, coeffs, config, *, replay=None, budgets=None, device=None,
         off, ent = _replay_tensors(g, replay)
         g.replay_diag(params, pre, off, ent, pcol, stats=st)
     d = g.diag_combine(z[0], z[1], pcol)
-    res = FunmResult(d if as_tensor else d.cpu().numpy(), "diag", config=_cfg_echo(cfg, coeffs, mode))
+    res = FunmResult(d if as_tensor else to_host(d), "diag", config=_cfg_echo(cfg, coeffs, mode))
     _stats(res, st)
     res.aux = {"pcol": pcol, "ni": ni, "walk_pre": pre}
     return res
@@ -275,7 +275,7 @@ def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None 
     else:
         off, ent = _replay_tensors(g, replay)
         g.replay_action(params, pre, off, ent, payload, q, stats=st)
-    out = q.cpu().numpy()
+    out = to_host(q)
     res = FunmResult(out if mode != "entry" else np.array([out[int(i)]]), "mc-" + mode,
                      config=_cfg_echo(cfg, coeffs, smode))
     _stats(res, st)
@@ -312,7 +312,7 @@ def rand_funm(a, coeffs, config, *, block: int = 1024, device=None, as_tensor: b
         q = Qb[: ce - cb]
         g.walk_qdense(params, pre, q, (cb, ce), stats=st)
         F += A[:, cb:ce] @ (q @ A)  # C_c Q_c A summed over the block's columns (Eq. 19)
-    res = FunmResult(F if as_tensor else F.cpu().numpy(), "full", config=_cfg_echo(cfg, coeffs, "philox"))
+    res = FunmResult(F if as_tensor else to_host(F), "full", config=_cfg_echo(cfg, coeffs, "philox"))
     _stats(res, st)
     res.aux = {"ni": ni, "walk_pre": pre}
     return res

@@ -42,7 +42,8 @@ def main(config=2, reps=3):
             y, st = parallel.sharded_diag(g, mc.EXPONENTIAL, wcfg)
         t3 = t()
         ph["estimate"] = t3 - t2
-        host = y.cpu().numpy()
+        from paper_2308_01037_b200.device import to_host
+        host = to_host(y)
         t4 = t()
         ph["d2h"] = t4 - t3
         g.close()
