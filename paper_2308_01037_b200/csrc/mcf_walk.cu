@@ -404,7 +404,7 @@ __global__ void k_col_reduce(const long long *__restrict__ walk_pre, long long c
 // longer rows (graph->long_rows) one warp each (one CTA above HUGE_ROW).
 // UNI: every stored value equals `uval` (0/1 graph times gamma), so the value
 // array is not read: y = h + uval * sum_j x_j.  Fixed reduction order.
-constexpr int HUGE_ROW = 4096;
+constexpr int HUGE_ROW = 1024;
 
 template <int G, bool UNI>
 __device__ __forceinline__ double row_dot(const long long e0, const long long e1, int sub,
@@ -430,7 +430,7 @@ template <int G, bool UNI>
 __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
                        const double *__restrict__ vals, double uval, double alpha, const double *__restrict__ v,
                        double beta, const double *__restrict__ r, const double *__restrict__ x, double *__restrict__ y,
-                       long long row_begin, long long row_end) {
+                       long long row_begin, long long row_end, NodeHdr *__restrict__ aux) {
     long long i = row_begin + (((long long)blockIdx.x * blockDim.x + threadIdx.x) / G);
     int sub = threadIdx.x % G;
     bool in = i < row_end;
@@ -444,7 +444,11 @@ __global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restr
     if (in) s = row_dot<G, UNI>(e0, e1, sub, col_ids, vals, x);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, G);
-    if (in && sub == 0) y[i] = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
+    if (in && sub == 0) {
+        const double out = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
+        y[i] = out;
+        if (aux) aux[i].aux = out;  // r = A v lands in the walk headers too
+    }
 }
 
 template <bool UNI>
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_
                                                    const int *__restrict__ col_ids, const double *__restrict__ vals,
                                                    double uval, double alpha, const double *__restrict__ v, double beta,
                                                    const double *__restrict__ r, const double *__restrict__ x,
-                                                   double *__restrict__ y, long long row_begin, long long row_end) {
+                                                   double *__restrict__ y, long long row_begin, long long row_end,
+                                                   NodeHdr *__restrict__ aux) {
     __shared__ double part[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // warps take rows of up to HUGE_ROW entries; the CTA takes the hub rows
@@ -464,7 +469,11 @@ __global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_
         const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
         if (i < row_begin || i >= row_end || e1 - e0 > HUGE_ROW) continue;
         double s = warp_sum(row_dot<32, UNI>(e0, e1, lane, col_ids, vals, x));
-        if (lane == 0) y[i] = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
+        if (lane == 0) {
+            const double out = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
+            y[i] = out;
+            if (aux) aux[i].aux = out;
+        }
     }
     for (long long li = blockIdx.x; li < n_long; li += gridDim.x) {
         const long long i = long_rows[li];
@@ -475,7 +484,11 @@ __global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_
         __syncthreads();
         if (threadIdx.x < 32) {
             double t = warp_sum(threadIdx.x < 8 ? part[threadIdx.x] : 0.0);
-            if (threadIdx.x == 0) y[i] = combine_out(alpha, v, beta, r, i, UNI ? uval * t : t);
+            if (threadIdx.x == 0) {
+                const double out = combine_out(alpha, v, beta, r, i, UNI ? uval * t : t);
+                y[i] = out;
+                if (aux) aux[i].aux = out;
+            }
         }
         __syncthreads();
     }
@@ -483,33 +496,33 @@ __global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_
 
 template <int G, bool UNI>
 static void launch_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x,
-                        double *y, long long rb, long long re, cudaStream_t s) {
+                        double *y, long long rb, long long re, cudaStream_t s, NodeHdr *aux) {
     const long long rows = re - rb;
     const long long *rp = (const long long *)g->row_ptr;
     k_spmv<G, UNI><<<(unsigned)((rows * G + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta,
-                                                                     r, x, y, rb, re);
+                                                                     r, x, y, rb, re, aux);
     mcf::note_launch();
     if (g->n_long_rows > 0) {
         long long grid = (g->n_long_rows + 7) / 8;
         if (grid > 8 * sm_count()) grid = 8 * sm_count();
         k_spmv_long<UNI><<<(unsigned)grid, 256, 0, s>>>(g->long_rows, g->n_long_rows, rp, g->col_ids, g->vals, g->value,
-                                                       alpha, v, beta, r, x, y, rb, re);
+                                                       alpha, v, beta, r, x, y, rb, re, aux);
         mcf::note_launch();
     }
 }
 
 int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,
-         long long rb, long long re, cudaStream_t s) {
+         long long rb, long long re, cudaStream_t s, NodeHdr *aux = nullptr) {
     MCF_ARG(g && x && y, "mcf_spmv: null argument");
     MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv: bad row range");
     if (re == rb) return MCF_OK;
     const bool small = g->nnz / g->n <= 8;
     if (g->uniform_value) {
-        if (small) launch_spmv<4, true>(g, alpha, v, beta, r, x, y, rb, re, s);
-        else launch_spmv<8, true>(g, alpha, v, beta, r, x, y, rb, re, s);
+        if (small) launch_spmv<4, true>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
+        else launch_spmv<8, true>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
     } else {
-        if (small) launch_spmv<4, false>(g, alpha, v, beta, r, x, y, rb, re, s);
-        else launch_spmv<8, false>(g, alpha, v, beta, r, x, y, rb, re, s);
+        if (small) launch_spmv<4, false>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
+        else launch_spmv<8, false>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
     }
     MCF_LAUNCHED("k_spmv");
     return MCF_OK;
@@ -640,7 +653,7 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
 
 static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                   const long long *walk_off, const int *entries, const double *r, double *q, double *qvar,
-                  long long *stats, cudaStream_t s, bool replay) {
+                  long long *stats, cudaStream_t s, bool replay, bool aux_ready = false) {
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(r && q && stats, "action walk: null r/q/stats");
@@ -665,8 +678,10 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     a.stats = stats;
     a.walk_off = walk_off;
     a.entries = entries;
-    k_set_aux<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, r, g->n);
-    mcf::note_launch();
+    if (!aux_ready) {
+        k_set_aux<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, r, g->n);
+        mcf::note_launch();
+    }
     if (g->went) {
         k_set_aux_fat<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>(g->went, r, g->nnz);
         mcf::note_launch();
@@ -727,9 +742,28 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     return MCF_OK;
 }
 
+// The whole RandFunmAction estimate for one process (Alg. 3): r = A v (the
+// SpMV writes r into the walk headers directly), walks, per-column
+// reduction, y = z0 v + z1 r + A q.  No host synchronisation.
+static int funm_action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, const double *v, double z0,
+                       double z1, double *r, double *q, double *qvar, double *y, long long *stats, cudaStream_t s) {
+    MCF_ARG(g && v && r && q && y, "mcf_funm_action: null argument");
+    int rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+    if (rc) return rc;
+    rc = action(g, p, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true);
+    if (rc) return rc;
+    return spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
+}
+
 }  // namespace mcf
 
 extern "C" {
+
+int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, const double *v, double zeta0,
+                    double zeta1, double *r, double *q, double *q_var, double *y, int64_t *stats, void *stream) {
+    return mcf::funm_action(g, p, (const long long *)walk_pre, v, zeta0, zeta1, r, q, q_var, y, (long long *)stats,
+                            (cudaStream_t)stream);
+}
 
 int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,
              int64_t row_begin, int64_t row_end, void *stream) {

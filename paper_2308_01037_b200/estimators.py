@@ -113,16 +113,17 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
     vd = v.to(g.device, torch.float64) if isinstance(v, torch.Tensor) else torch.from_numpy(v_np).to(g.device)
     params = WalkParams(cfg, z, g.device)
     ni, pre = _budgets(g, cfg, replay, budgets)
-    r = g.spmv(vd)                       # r = A v
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
     qvar = torch.zeros_like(q) if stderr else None
     st = g.new_stats()
-    if replay is None:
-        g.walk_action(params, pre, r, q, qvar, stats=st)
+    if replay is None:  # r = A v, walks, q, y = z0 v + z1 r + A q in one library call
+        r = torch.empty_like(q)
+        y = g.funm_action(params, pre, vd, z[0], z[1], r, q, torch.empty_like(q), qvar, st)
     else:
+        r = g.spmv(vd)                       # r = A v
         off, ent = _replay_tensors(g, replay)
         g.replay_action(params, pre, off, ent, r, q, stats=st)
-    y = g.spmv(q, alpha=z[0], v=vd, beta=z[1], r=r)   # y = z0 v + z1 r + A q
+        y = g.spmv(q, alpha=z[0], v=vd, beta=z[1], r=r)   # y = z0 v + z1 r + A q
     res = FunmResult(y if as_tensor else to_host(y), "action", config=_cfg_echo(cfg, coeffs, mode))
     _stats(res, st)
     res.aux = {"q": q, "r": r, "ni": ni, "walk_pre": pre}

@@ -67,11 +67,15 @@ def sharded_action(g: DeviceGraph, coeffs, v: torch.Tensor, config, *, params=No
     z = coeffs.prefix(cfg.max_steps + 2)
     params = params or WalkParams(cfg, z, g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
-    cols = column_shards(pre, size)[rank] if size > 1 else (0, g.n)
-    rows = row_shards(g.n, size)[rank] if size > 1 else (0, g.n)
+    st = g.new_stats()
+    if size == 1:  # the whole pass in one library call
+        q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
+        r, y = torch.empty_like(q), torch.empty_like(q)
+        return g.funm_action(params, pre, v, z[0], z[1], r, q, y, stats=st), st
+    cols = column_shards(pre, size)[rank]
+    rows = row_shards(g.n, size)[rank]
     r = g.spmv(v)
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
-    st = g.new_stats()
     g.walk_action(params, pre, r, q, cols=cols, stats=st)
     assemble(q, group)
     y = torch.zeros(g.n, dtype=torch.float64, device=g.device) if size > 1 else None
