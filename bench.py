@@ -300,6 +300,17 @@ def run_device(args, cfg):
     g = DeviceGraph(a, gamma=beta)
     v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=g.device)  # > 126 MB L2
+    # The write leaves L2 full of DIRTY lines whose write-back would otherwise
+    # land inside the next timed step; reading a second buffer of the same size
+    # (untimed) evicts them, so each step starts with no input cached and a
+    # clean L2 ("write": the write alone).
+    sweep = torch.zeros(32 << 20, dtype=torch.int64, device=g.device) if args.flush == "write+read" else None
+    sweep_out = torch.empty((), dtype=torch.int64, device=g.device)
+
+    def flush_l2():
+        flush.zero_()
+        if sweep is not None:
+            torch.sum(sweep, dim=0, out=sweep_out)
 
     def step():
         if cfg["kind"] == "action":
@@ -349,7 +360,7 @@ def run_device(args, cfg):
     torch.cuda.synchronize()
     t_wall0 = time.time()
     for i in range(args.steps):
-        flush.zero_()
+        flush_l2()
         ev[i][0].record()
         if graph is not None:
             graph.replay()
@@ -417,7 +428,8 @@ def run_device(args, cfg):
         h2d = int(a.csr.indptr.nbytes + a.csr.indices.nbytes + a.csr.data.nbytes)
         d2h = 8 * a.n
         e2e_ms = []
-        for i in range(max(1, args.steps) + 1):
+        e2e_warm = max(1, args.warmup)  # first calls warm the pinned/device allocators
+        for i in range(max(1, args.steps) + e2e_warm):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -432,7 +444,7 @@ def run_device(args, cfg):
             torch.cuda.synchronize()
             dt = time.perf_counter() - t1
             ge.close()
-            if i > 0:  # first call warms the allocator
+            if i >= e2e_warm:
                 e2e_ms.append(dt * 1e3)
             assert np.isfinite(host).all()
         e_ms = sum(e2e_ms)
@@ -466,7 +478,9 @@ def run_device(args, cfg):
             "config": {"workload": cfg["workload"], "n": g.n, "nnz": g.nnz, "n_walks": int(n_walks),
                        "emissions_per_step": em_per_step, "beta": beta, "max_steps": cfg["max_steps"],
                        "weight_cutoff": cfg["cutoff"], "seed": cfg["seed"], "sampling": "philox (device RNG)",
-                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "l2": ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read of another "
+                              "buffer to evict the dirty lines" if args.flush == "write+read" else
+                              "flushed between timed steps (256 MiB write, untimed)"),
                        "parallelism": f"start-column shards x{world}, graph replicated"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "timing": "CUDA-graph replay of one full estimator pass" if graph is not None else "eager steps",
@@ -487,6 +501,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="mcfunm", choices=["mcfunm", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--flush", choices=["write", "write+read"], default="write")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -148,14 +148,15 @@ MCF_API int mcf_walk_action(mcf_graph *g, const mcf_walk_params *p, const int64_
                     double *q_var, int64_t *stats, void *stream);
 
 /* The whole RandFunmAction estimate in one call (Alg. 3, PAPER.md:337-367,
- * SPEC.md:369-377): r = A v, the walks of every column (budgets walk_pre),
- * q, optional q_var, and y = zeta0 v + zeta1 r + A q ([dev] n each).  Single
- * process (the multi-GPU path composes mcf_spmv / mcf_walk_action with an
- * exchange of q).  No host synchronisation (capturable in a CUDA graph when
- * p->walk_capacity > 0). */
-MCF_API int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, const double *v,
-                            double zeta0, double zeta1, double *r, double *q, double *q_var, double *y,
-                            int64_t *stats, void *stream);
+ * SPEC.md:369-377): the budgets for n_walks (-> ni[n], walk_pre[n+1], as
+ * mcf_allocate_walks, computed on an internal stream concurrently with
+ * r = A v), the walks of every column, q, optional q_var, and
+ * y = zeta0 v + zeta1 r + A q ([dev] n each).  Single process (the multi-GPU
+ * path composes mcf_spmv / mcf_walk_action with an exchange of q).  No host
+ * synchronisation: capturable in a CUDA graph (set p->walk_capacity). */
+MCF_API int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, int64_t n_walks, int64_t *ni,
+                            int64_t *walk_pre, const double *v, double zeta0, double zeta1, double *r, double *q,
+                            double *q_var, double *y, int64_t *stats, void *stream);
 
 /* Same as mcf_walk_action, but every draw is taken from a recorded entry stream instead of the
  * RNG: walk g = walk_pre[c] + w consumes entries[walk_off[g] .. walk_off[g+1])

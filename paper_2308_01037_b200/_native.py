@@ -51,7 +51,7 @@ SIGNATURES = {
     "mcf_allocate_walks": (C.c_int, [P, I64, P, P, P]),
     "mcf_spmv": (C.c_int, [P, C.c_double, P, C.c_double, P, P, P, I64, I64, P]),
     "mcf_walk_action": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P, P, P]),
-    "mcf_funm_action": (C.c_int, [P, C.POINTER(McfWalkParams), P, P, C.c_double, C.c_double, P, P, P, P, P, P]),
+    "mcf_funm_action": (C.c_int, [P, C.POINTER(McfWalkParams), C.c_int64, P, P, P, C.c_double, C.c_double, P, P, P, P, P, P]),
     "mcf_replay_action": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P, P, P, P]),
     "mcf_walk_diag": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P]),
     "mcf_replay_diag": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P, P, P]),

@@ -9,17 +9,21 @@
 
 namespace mcf {
 
-// Largest-remainder selection in five kernels, without a sort:
+// Largest-remainder selection without a sort:
 //   1 k_alloc_floor  N_i = floor(p_i N), remainder key, Sum N_i and a 1024-bucket
 //                    histogram of the remainders (floor(rem * 1024)); the last
 //                    block finds the bucket b* that holds the R-th largest.
-//   2 k_alloc_cands  compacts the keys of bucket b* (with their index).
-//   3 k_alloc_select one CTA: exact radix select of the threshold key T among
-//                    the candidates (one distinct value: read off min/max)
-//   4 scan           rank of each key equal to T among those, in index order
-//   5 k_alloc_final  N_i += key > T || (key == T && rank < ties to take)
-//                    (ties go to the lowest indices, the reference's stable argsort)
-//   6 scan           walk_pre.
+//   2 k_alloc_level2 1024 sub-buckets of b* with min/max: usually pins the
+//                    threshold key T (a single distinct value) and the number
+//                    I of keys == T to take.
+//   3 k_alloc_cands + k_alloc_select (only when level 2 did not resolve T):
+//                    one CTA, exact select among the candidates.
+//   4 k_alloc_scan   one single-pass scan of the pair (a_i, b_i) =
+//                    (N_i + [key_i > T], [key_i == T]): ties go to the lowest
+//                    indices (the reference's stable argsort), so the final
+//                    N_i = a_i + [b_i and ties before i < I] and
+//                    walk_pre[i] = sum_{j<i} a_j + min(I, ties before i);
+//                    the same pass fills the walk-block -> column map.
 // p_i = 0 keys (0) sit below every positive remainder; they are only reached
 // when R exceeds the number of positive p_i (then b* = -1 covers them).
 constexpr int NBUCKET = 1024;
@@ -90,30 +94,46 @@ __device__ void find_bin(const unsigned *cnt, long long R, int *bin, long long *
 
 // block-parallel search from the top bucket: thread t holds bucket NBUCKET-1-t*4..; finds b with
 // count(above b) < R <= count(above b) + hist[b]
-__global__ void __launch_bounds__(256) k_alloc_floor(const double *__restrict__ p, long long n, double total,
+__global__ void __launch_bounds__(256, 4) k_alloc_floor(const double *__restrict__ p, long long n, double total,
                                                      long long n_walks, long long *__restrict__ ni,
                                                      unsigned long long *__restrict__ key, AllocState *st) {
     __shared__ unsigned h[NBUCKET];
     __shared__ bool last;
-    __shared__ long long wsum[8];
     for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) h[b] = 0;
     __syncthreads();
     long long got_sum = 0, pos = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double pi = p[i];
-        const double want = __dmul_rn(pi, total);
-        const double fl = floor(want);
-        const long long got = (long long)fl;
-        ni[i] = got;
-        got_sum += got;
-        unsigned long long k = 0;
-        if (pi != 0.0) {
-            k = (unsigned long long)__double_as_longlong(__dsub_rn(want, fl)) + 1ull;
-            ++pos;
-            atomicAdd(&h[rem_bucket(k)], 1u);
+    // warp-uniform trip count (the bucket vote below is warp-wide)
+    for (long long w0 = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); w0 < n; w0 += 4 * stride) {
+        const long long i0 = w0 + (threadIdx.x & 31);
+        double pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pv[u] = i0 + u * stride < n ? p[i0 + u * stride] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long i = i0 + u * stride;
+            const double pi = pv[u];
+            const double want = __dmul_rn(pi, total);
+            const double fl = floor(want);
+            const long long got = (long long)fl;
+            unsigned long long k = 0;
+            if (pi != 0.0) {
+                k = (unsigned long long)__double_as_longlong(__dsub_rn(want, fl)) + 1ull;
+                ++pos;
+            }
+            const int bk = k ? rem_bucket(k) : -1;
+            const int b0 = __shfl_sync(MCF_FULL, bk, 0);
+            if (__all_sync(MCF_FULL, bk == b0)) {  // equal-degree runs share a bucket
+                if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicAdd(&h[b0], 32u);
+            } else if (bk >= 0) {
+                atomicAdd(&h[bk], 1u);
+            }
+            if (i < n) {
+                ni[i] = got;
+                got_sum += got;
+                key[i] = k;
+            }
         }
-        key[i] = k;
     }
     got_sum = warp_sum_ll(got_sum);
     pos = warp_sum_ll(pos);
@@ -385,15 +405,52 @@ __global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long 
     }
 }
 
-__global__ void k_alloc_final(const unsigned long long *__restrict__ key, long long n, const AllocState *st,
-                              const long long *__restrict__ tie_rank, long long *__restrict__ ni) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || st->bstar == -2) return;
-    const unsigned long long k = key[i], T = st->T;
-    if (k > T || (k == T && tie_rank[i] < st->I)) ni[i] += 1;
+__global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const unsigned long long *__restrict__ key, long long n,
+                                                          const AllocState *st, long long *__restrict__ ni,
+                                                          long long *__restrict__ walk_pre, int *__restrict__ blk_col,
+                                                          unsigned long long *sa, unsigned long long *sb,
+                                                          unsigned *tile_ctr) {
+    __shared__ unsigned s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const long long tile = s_tile;
+    const bool select = st->bstar != -2;
+    const unsigned long long T = select ? st->T : 0ull;
+    const long long I = select ? st->I : 0;
+    const long long base = tile * SCAN_TILE + (long long)(threadIdx.x >> 5) * 32 * SCAN_I + (threadIdx.x & 31);
+    long long a[SCAN_I], b[SCAN_I], ea[SCAN_I], eb[SCAN_I];
+#pragma unroll
+    for (int k = 0; k < SCAN_I; ++k) {
+        const long long j = base + 32 * k;
+        a[k] = b[k] = 0;
+        if (j < n) {
+            const unsigned long long kj = key[j];
+            a[k] = ni[j] + ((select && kj > T) ? 1 : 0);
+            b[k] = (select && kj == T) ? 1 : 0;
+        }
+    }
+    tile_scan<true>(tile, a, b, ea, eb, sa, sb);
+    constexpr long long B = 1ll << WALK_BLK_SHIFT;
+#pragma unroll
+    for (int k = 0; k < SCAN_I; ++k) {
+        const long long j = base + 32 * k;
+        if (j < n) {
+            const long long nj = a[k] + ((b[k] && eb[k] < I) ? 1 : 0);
+            const long long w0 = ea[k] + (eb[k] < I ? eb[k] : I);
+            ni[j] = nj;
+            walk_pre[j] = w0;
+            if (blk_col)
+                for (long long blk = (w0 + B - 1) >> WALK_BLK_SHIFT; blk * B < w0 + nj; ++blk) blk_col[blk] = (int)j;
+            if (j == n - 1) {
+                const long long tb = eb[k] + b[k];
+                walk_pre[n] = ea[k] + a[k] + (tb < I ? tb : I);
+            }
+        }
+    }
 }
 
-static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, cudaStream_t s) {
+static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
+                    cudaStream_t s) {
     MCF_ARG(g && ni && walk_pre, "mcf_allocate_walks: null argument");
     MCF_ARG(n_walks >= 1, "n_walks must be at least 1");  // walker.py:168-169
     MCF_ARG(n_walks < (1ll << 53), "n_walks must be below 2^53");
@@ -402,10 +459,16 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     unsigned long long *key = nullptr, *ckey = nullptr;
     int *cidx = nullptr;
     MCF_CUDA(cudaMallocAsync(&st, sizeof(AllocState), s));
-    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * n * 3 + 8 + sizeof(int) * n, s));
+    if (n == 0) {
+        MCF_CUDA(cudaMemsetAsync(walk_pre, 0, sizeof(long long), s));
+        return MCF_OK;
+    }
+    const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * (2 * n + 2 * tiles + 1) + sizeof(int) * n, s));
     ckey = key + n;
-    long long *rank = reinterpret_cast<long long *>(ckey + n);
-    cidx = reinterpret_cast<int *>(rank + n + 1);
+    unsigned long long *sa = ckey + n, *sb = sa + tiles;  // look-back state of k_alloc_scan
+    unsigned *ctr = reinterpret_cast<unsigned *>(sb + tiles);
+    cidx = reinterpret_cast<int *>(ctr + 2);
     MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(AllocState), s));
     MCF_CUDA(cudaMemsetAsync(&st->cmin, 0xff, sizeof(unsigned long long), s));
     MCF_CUDA(cudaMemsetAsync(st->min2, 0xff, sizeof(st->min2), s));
@@ -418,21 +481,22 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     mcf::note_launch();
     k_alloc_select<<<1, 1024, 0, s>>>(ckey, st);
     mcf::note_launch();
-    ScanSrc ties{nullptr, key, &st->T};  // rank among the keys equal to T (index order)
-    int rc0 = scan_src(ties, rank, n, s);
-    if (rc0) return rc0;
-    k_alloc_final<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, n, st, rank, ni);
+    MCF_CUDA(cudaMemsetAsync(sa, 0, sizeof(unsigned long long) * (2 * tiles + 1), s));
+    k_alloc_scan<<<(unsigned)tiles, SCAN_T, 0, s>>>(key, n, st, ni, walk_pre, blk_col, sa, sb, ctr);
     mcf::note_launch();
     MCF_LAUNCHED("allocate");
-    int rc = exclusive_scan_i64(ni, walk_pre, n, s);
-    if (rc) return rc;
     MCF_CUDA(cudaFreeAsync(st, s));
     MCF_CUDA(cudaFreeAsync(key, s));
     return MCF_OK;
 }
 
+int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
+                   cudaStream_t s) {
+    return allocate(g, n_walks, ni, walk_pre, blk_col, s);
+}
+
 }  // namespace mcf
 
 extern "C" int mcf_allocate_walks(mcf_graph *g, int64_t n_walks, int64_t *ni, int64_t *walk_pre, void *stream) {
-    return mcf::allocate(g, (long long)n_walks, (long long *)ni, (long long *)walk_pre, (cudaStream_t)stream);
+    return mcf::allocate(g, (long long)n_walks, (long long *)ni, (long long *)walk_pre, nullptr, (cudaStream_t)stream);
 }

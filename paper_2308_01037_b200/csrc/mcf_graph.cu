@@ -386,6 +386,9 @@ static void release(mcf_graph *g) {
     if (g->hub_of) cudaFreeAsync(g->hub_of, 0);
     if (g->hub_bits) cudaFreeAsync(g->hub_bits, 0);
     if (g->scratch) cudaFreeAsync(g->scratch, 0);
+    if (g->side) cudaStreamDestroy(g->side);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    if (g->ev_join) cudaEventDestroy(g->ev_join);
     for (auto &p : g->ev_walk) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto &p : g->ev_q) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     delete g;

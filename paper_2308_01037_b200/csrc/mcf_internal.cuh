@@ -104,6 +104,9 @@ struct mcf_graph {
     int device = 0;
     // optional per-launch timing of the dominant kernels (MCF_FLAG_TIME_KERNELS)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_walk, ev_q;
+    // side stream + fork/join events (budgets computed concurrently with r = A v)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace mcf {
@@ -193,6 +196,137 @@ __device__ __forceinline__ int column_of_walk(long long g, long long g_rel, long
 }
 
 // ---------------------------------------------------------------------------
+// single-pass scans (decoupled look-back) without fences: each component of a
+// tile's state is one 64-bit word flag | value (62 bits), ST_AGG = the tile's
+// own total, ST_PRE = its inclusive prefix.  With two components (sa, sb) a
+// reader accepts a pair only when both flags agree -- flags only move
+// 0 -> AGG -> PRE and the value for each flag is fixed, so an agreeing pair is
+// consistent without any release/acquire ordering.  One warp looks back 32
+// tiles per round.  Tiles are warp-striped: element k of lane l
+// in warp w is item tile * SCAN_TILE + w * 32 * SCAN_I + k * 32 + l, so every
+// load and store is coalesced.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
+constexpr int SCAN_T = 512, SCAN_I = 8, SCAN_TILE = SCAN_T * SCAN_I, SCAN_W = SCAN_T / 32;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// inclusive warp scan
+__device__ __forceinline__ long long warp_incl_scan(long long x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(MCF_FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// warp 0 of tile `tile` (> 0): exclusive prefix (pa, pb) over tiles < tile.
+// 32 tiles per round (one per lane); a lane whose tile has not published yet
+// polls it with a short back-off, so the status words (a few L2 lines every
+// tile polls) are not flooded.
+template <bool HAS_B>
+__device__ __forceinline__ void lookback(long long tile, const unsigned long long *sa, const unsigned long long *sb,
+                                         long long &pa, long long &pb) {
+    const int lane = threadIdx.x & 31;
+    pa = 0;
+    pb = 0;
+    for (long long t = tile - 1;; t -= 32) {
+        const long long idx = t - lane;
+        unsigned long long xa = ST_PRE, xb = ST_PRE;  // idx < 0: nothing
+        if (idx >= 0) {
+            unsigned ns = 32;
+            while (true) {
+                xa = ld_relaxed_u64(sa + idx);
+                if (HAS_B) xb = ld_relaxed_u64(sb + idx);
+                if ((xa & ~ST_VAL) && (!HAS_B || (xa & ~ST_VAL) == (xb & ~ST_VAL))) break;
+                __nanosleep(ns);
+                if (ns < 512) ns <<= 1;
+            }
+        }
+        const unsigned pre = __ballot_sync(MCF_FULL, idx >= 0 && (xa & ST_PRE));
+        const int f = pre ? __ffs(pre) - 1 : 32;  // nearest tile holding an inclusive prefix
+        long long a = (idx >= 0 && lane <= f) ? (long long)(xa & ST_VAL) : 0;
+        long long b = (HAS_B && idx >= 0 && lane <= f) ? (long long)(xb & ST_VAL) : 0;
+        pa += warp_sum_ll(a);
+        if (HAS_B) pb += warp_sum_ll(b);
+        if (pre || t - 32 < 0) break;
+    }
+}
+
+// Tile-level exclusive scan of one or two components held warp-striped
+// (a[k], b[k] for k < SCAN_I).  On return ea[k] / eb[k] are the exclusive
+// prefixes of the item over the whole array.  Two barriers; every thread of
+// the SCAN_T-thread block calls it.
+template <bool HAS_B>
+__device__ __forceinline__ void tile_scan(long long tile, const long long (&a)[SCAN_I], const long long (&b)[SCAN_I],
+                                          long long (&ea)[SCAN_I], long long (&eb)[SCAN_I], unsigned long long *sa,
+                                          unsigned long long *sb) {
+    __shared__ long long s_wa[SCAN_W], s_wb[SCAN_W];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long ca = 0, cb = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_I; ++k) {
+        const long long xa = warp_incl_scan(a[k]);
+        ea[k] = ca + xa - a[k];
+        ca += __shfl_sync(MCF_FULL, xa, 31);
+        if (HAS_B) {
+            const long long xb = warp_incl_scan(b[k]);
+            eb[k] = cb + xb - b[k];
+            cb += __shfl_sync(MCF_FULL, xb, 31);
+        }
+    }
+    if (lane == 0) {
+        s_wa[w] = ca;
+        if (HAS_B) s_wb[w] = cb;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const long long va = lane < SCAN_W ? s_wa[lane] : 0, vb = (HAS_B && lane < SCAN_W) ? s_wb[lane] : 0;
+        const long long ia = warp_incl_scan(va), ib = HAS_B ? warp_incl_scan(vb) : 0;
+        const long long ta = __shfl_sync(MCF_FULL, ia, 31), tb = HAS_B ? __shfl_sync(MCF_FULL, ib, 31) : 0;
+        long long pa = 0, pb = 0;
+        if (tile == 0) {
+            if (lane == 0) {
+                st_relaxed_u64(sa, ST_PRE | (unsigned long long)ta);
+                if (HAS_B) st_relaxed_u64(sb, ST_PRE | (unsigned long long)tb);
+            }
+        } else {
+            if (lane == 0) {
+                st_relaxed_u64(sa + tile, ST_AGG | (unsigned long long)ta);
+                if (HAS_B) st_relaxed_u64(sb + tile, ST_AGG | (unsigned long long)tb);
+            }
+            lookback<HAS_B>(tile, sa, sb, pa, pb);
+            if (lane == 0) {
+                st_relaxed_u64(sa + tile, ST_PRE | (unsigned long long)(pa + ta));
+                if (HAS_B) st_relaxed_u64(sb + tile, ST_PRE | (unsigned long long)(pb + tb));
+            }
+        }
+        __syncwarp();
+        if (lane < SCAN_W) {  // exclusive warp offsets, including the tile prefix
+            s_wa[lane] = pa + ia - va;
+            if (HAS_B) s_wb[lane] = pb + ib - vb;
+        }
+    }
+    __syncthreads();
+    const long long oa = s_wa[w], ob = HAS_B ? s_wb[w] : 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_I; ++k) {
+        ea[k] += oa;
+        if (HAS_B) eb[k] += ob;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host helpers implemented in mcf_util.cu
 // ---------------------------------------------------------------------------
 int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s);
@@ -207,6 +341,8 @@ int build_blk_col(const long long *walk_pre, long long col_begin, long long col_
                   int **blk_col, cudaStream_t s);
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
 int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s);
+int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
+                   cudaStream_t s);
 int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end,
                     long long *wb, long long *we, cudaStream_t s);
 int sm_count();

@@ -65,103 +65,35 @@ int sm_count() {
 }
 
 // ---------------------------------------------------------------------------
-// exclusive scan of int64, single pass (decoupled look-back):
+// exclusive scan of int64, single pass (decoupled look-back, mcf_internal.cuh):
 // out[0..n] with out[n] = total.  Tiles take ids from a counter so every
 // predecessor a tile waits on has already started.
 // ---------------------------------------------------------------------------
-constexpr int SCAN_T = 512;
-constexpr int SCAN_I = 8;
-constexpr int SCAN_TILE = SCAN_T * SCAN_I;
-constexpr unsigned long long ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_VAL = (1ull << 62) - 1;
-
-__device__ __forceinline__ long long block_excl_scan(long long v, long long *total) {
-    __shared__ long long warp_tot[SCAN_T / 32];
-    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    long long x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        long long y = __shfl_up_sync(MCF_FULL, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        long long t = (lane < SCAN_T / 32) ? warp_tot[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            long long y = __shfl_up_sync(MCF_FULL, t, o);
-            if (lane >= o) t += y;
-        }
-        if (lane < SCAN_T / 32) warp_tot[lane] = t;  // inclusive
-    }
-    __syncthreads();
-    long long before = (wid > 0 ? warp_tot[wid - 1] : 0) + x - v;
-    *total = warp_tot[SCAN_T / 32 - 1];
-    __syncthreads();
-    return before;
-}
-
 __device__ __forceinline__ long long scan_item(const ScanSrc &src, long long j) {
     if (src.in) return src.in[j];
     return src.key[j] == *src.match ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan(ScanSrc src, long long n, long long *__restrict__ out,
-                                                 unsigned long long *status, unsigned int *tile_ctr) {
+__global__ void __launch_bounds__(SCAN_T, 2) k_scan(ScanSrc src, long long n, long long *__restrict__ out,
+                                                    unsigned long long *status, unsigned int *tile_ctr) {
     __shared__ unsigned int s_tile;
-    __shared__ long long s_prefix;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const long long tile = s_tile;
-    const long long base = tile * SCAN_TILE + (long long)threadIdx.x * SCAN_I;
-    long long v[SCAN_I];
-    long long sum = 0;
+    const long long base = tile * SCAN_TILE + (long long)(threadIdx.x >> 5) * 32 * SCAN_I + (threadIdx.x & 31);
+    long long v[SCAN_I], e[SCAN_I], none[SCAN_I], none2[SCAN_I];
 #pragma unroll
-    for (int i = 0; i < SCAN_I; ++i) {
-        long long j = base + i;
-        v[i] = (j < n) ? scan_item(src, j) : 0;
-        sum += v[i];
+    for (int k = 0; k < SCAN_I; ++k) {
+        const long long j = base + 32 * k;
+        v[k] = j < n ? scan_item(src, j) : 0;
+        none[k] = 0;
     }
-    long long agg;
-    long long local = block_excl_scan(sum, &agg);
-    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 tiles at a time
-        const int lane = threadIdx.x;
-        long long prefix = 0;
-        if (tile == 0) {
-            if (lane == 0) atomicExch(&status[0], ST_PRE | (unsigned long long)agg);
-        } else {
-            if (lane == 0) atomicExch(&status[tile], ST_AGG | (unsigned long long)agg);
-            long long t = tile - 1;
-            while (true) {
-                const long long mine = t - lane;
-                unsigned long long st = 0;
-                if (mine >= 0) {
-                    do {
-                        st = atomicAdd(&status[mine], 0ull);
-                    } while (!(st & ~ST_VAL));
-                }
-                const unsigned pre = __ballot_sync(MCF_FULL, mine >= 0 && (st & ST_PRE));
-                // sum values of tiles t .. nearest PREFIX tile (inclusive)
-                const int stop = pre ? __ffs(pre) - 1 : 31;
-                long long v = (lane <= stop && mine >= 0) ? (long long)(st & ST_VAL) : 0;
+    tile_scan<false>(tile, v, none, e, none2, status, nullptr);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MCF_FULL, v, o);
-                prefix += v;
-                if (pre || t - 32 < 0) break;
-                t -= 32;
-            }
-            if (lane == 0) atomicExch(&status[tile], ST_PRE | (unsigned long long)(prefix + agg));
-        }
-        if (lane == 0) s_prefix = prefix;
-    }
-    __syncthreads();
-    long long run = s_prefix + local;
-#pragma unroll
-    for (int i = 0; i < SCAN_I; ++i) {
-        long long j = base + i;
-        if (j < n) out[j] = run;
-        run += v[i];
-        if (j == n - 1) out[n] = run;
+    for (int k = 0; k < SCAN_I; ++k) {
+        const long long j = base + 32 * k;
+        if (j < n) out[j] = e[k];
+        if (j == n - 1) out[n] = e[k] + v[k];
     }
 }
 

@@ -406,108 +406,129 @@ __global__ void k_col_reduce(const long long *__restrict__ walk_pre, long long c
 // array is not read: y = h + uval * sum_j x_j.  Fixed reduction order.
 constexpr int HUGE_ROW = 1024;
 
-template <int G, bool UNI>
-__device__ __forceinline__ double row_dot(const long long e0, const long long e1, int sub,
-                                          const int *__restrict__ col_ids, const double *__restrict__ vals,
-                                          const double *__restrict__ x) {
-    double s = 0.0;
-    for (long long e = e0 + sub; e < e1; e += G) {
-        const double xv = __ldg(x + __ldg(col_ids + e));
-        s = UNI ? s + xv : fma(__ldg(vals + e), xv, s);
-    }
-    return s;
-}
+// Short rows (<= LONG_ROW entries): a warp takes 32 consecutive rows and walks
+// their entries as one flat, coalesced segment, up to SEG_CAP entries per pass
+// with every load of a pass in flight at once (the latency chain per row is
+// row_ptr -> col_ids -> x, paid once per warp instead of once per entry).
+// The products land in shared memory and each lane then sums its own row in
+// CSR order with separate multiply and add, so y matches a sequential CSR
+// matvec (scipy's) bit for bit on these rows.  Long rows take the blocks
+// in front of the grid (a warp each, or the whole CTA past HUGE_ROW).
+constexpr int SEG_CAP = 256;
+constexpr int SPMV_WARPS = 8;
 
-__device__ __forceinline__ double combine_out(double alpha, const double *v, double beta, const double *r, long long i,
-                                              double s) {
+__device__ __forceinline__ double combine_exact(double alpha, const double *v, double beta, const double *r,
+                                                long long i, double s) {
+    // ((alpha v) + (beta r)) + s, each operation rounded: the numpy expression
+    // z0 * v + z1 * r + A @ q evaluated elementwise
     double h = 0.0;
-    if (v) h = alpha * v[i];
-    if (r) h += beta * r[i];
-    return h + s;
-}
-
-template <int G, bool UNI>
-__global__ void k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
-                       const double *__restrict__ vals, double uval, double alpha, const double *__restrict__ v,
-                       double beta, const double *__restrict__ r, const double *__restrict__ x, double *__restrict__ y,
-                       long long row_begin, long long row_end, NodeHdr *__restrict__ aux) {
-    long long i = row_begin + (((long long)blockIdx.x * blockDim.x + threadIdx.x) / G);
-    int sub = threadIdx.x % G;
-    bool in = i < row_end;
-    double s = 0.0;
-    long long e0 = 0, e1 = 0;
-    if (in) {
-        e0 = row_ptr[i];
-        e1 = row_ptr[i + 1];
-        in = (e1 - e0) <= LONG_ROW;
-    }
-    if (in) s = row_dot<G, UNI>(e0, e1, sub, col_ids, vals, x);
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, G);
-    if (in && sub == 0) {
-        const double out = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
-        y[i] = out;
-        if (aux) aux[i].aux = out;  // r = A v lands in the walk headers too
-    }
+    if (v) h = __dmul_rn(alpha, v[i]);
+    if (r) h = v ? __dadd_rn(h, __dmul_rn(beta, r[i])) : __dmul_rn(beta, r[i]);
+    return (v || r) ? __dadd_rn(h, s) : s;
 }
 
 template <bool UNI>
-__global__ void __launch_bounds__(256) k_spmv_long(const int *__restrict__ long_rows, long long n_long,
-                                                   const long long *__restrict__ row_ptr,
-                                                   const int *__restrict__ col_ids, const double *__restrict__ vals,
-                                                   double uval, double alpha, const double *__restrict__ v, double beta,
-                                                   const double *__restrict__ r, const double *__restrict__ x,
-                                                   double *__restrict__ y, long long row_begin, long long row_end,
-                                                   NodeHdr *__restrict__ aux) {
-    __shared__ double part[8];
+__global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                                              const double *__restrict__ vals, double uval, double alpha,
+                                              const double *__restrict__ v, double beta, const double *__restrict__ r,
+                                              const double *__restrict__ x, double *__restrict__ y, long long row_begin,
+                                              long long row_end, NodeHdr *__restrict__ aux,
+                                              const int *__restrict__ long_rows, long long n_long, int long_blocks) {
+    __shared__ double prod[SPMV_WARPS][SEG_CAP];
+    __shared__ unsigned char rmap[SPMV_WARPS][SEG_CAP];
+    __shared__ long long delta[SPMV_WARPS][32];
+    __shared__ double part[SPMV_WARPS];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // warps take rows of up to HUGE_ROW entries; the CTA takes the hub rows
-    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long li = gw; li < n_long; li += nw) {
-        const long long i = long_rows[li];
-        const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
-        if (i < row_begin || i >= row_end || e1 - e0 > HUGE_ROW) continue;
-        double s = warp_sum(row_dot<32, UNI>(e0, e1, lane, col_ids, vals, x));
-        if (lane == 0) {
-            const double out = combine_out(alpha, v, beta, r, i, UNI ? uval * s : s);
-            y[i] = out;
-            if (aux) aux[i].aux = out;
-        }
-    }
-    for (long long li = blockIdx.x; li < n_long; li += gridDim.x) {
-        const long long i = long_rows[li];
-        const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
-        if (i < row_begin || i >= row_end || e1 - e0 <= HUGE_ROW) continue;
-        double s = warp_sum(row_dot<256, UNI>(e0, e1, threadIdx.x, col_ids, vals, x));
-        if (lane == 0) part[w] = s;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            double t = warp_sum(threadIdx.x < 8 ? part[threadIdx.x] : 0.0);
-            if (threadIdx.x == 0) {
-                const double out = combine_out(alpha, v, beta, r, i, UNI ? uval * t : t);
+    if ((int)blockIdx.x < long_blocks) {
+        // ---- long rows: a warp per row up to HUGE_ROW, the CTA beyond -------
+        const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const long long nw = ((long long)long_blocks * blockDim.x) >> 5;
+        for (long long li = gw; li < n_long; li += nw) {
+            const long long i = long_rows[li];
+            const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
+            if (i < row_begin || i >= row_end || e1 - e0 > HUGE_ROW) continue;
+            double s = 0.0;
+            for (long long e = e0 + lane; e < e1; e += 32)
+                s += __dmul_rn(UNI ? uval : __ldg(vals + e), __ldg(x + __ldg(col_ids + e)));
+            s = warp_sum(s);
+            if (lane == 0) {
+                const double out = combine_exact(alpha, v, beta, r, i, s);
                 y[i] = out;
                 if (aux) aux[i].aux = out;
             }
         }
-        __syncthreads();
+        for (long long li = blockIdx.x; li < n_long; li += long_blocks) {
+            const long long i = long_rows[li];
+            const long long e0 = row_ptr[i], e1 = row_ptr[i + 1];
+            if (i < row_begin || i >= row_end || e1 - e0 <= HUGE_ROW) continue;
+            double s = 0.0;
+            for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+                s += __dmul_rn(UNI ? uval : __ldg(vals + e), __ldg(x + __ldg(col_ids + e)));
+            s = warp_sum(s);
+            if (lane == 0) part[w] = s;
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const double t = warp_sum(threadIdx.x < SPMV_WARPS ? part[threadIdx.x] : 0.0);
+                if (threadIdx.x == 0) {
+                    const double out = combine_exact(alpha, v, beta, r, i, t);
+                    y[i] = out;
+                    if (aux) aux[i].aux = out;
+                }
+            }
+            __syncthreads();
+        }
+        return;
     }
-}
-
-template <int G, bool UNI>
-static void launch_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x,
-                        double *y, long long rb, long long re, cudaStream_t s, NodeHdr *aux) {
-    const long long rows = re - rb;
-    const long long *rp = (const long long *)g->row_ptr;
-    k_spmv<G, UNI><<<(unsigned)((rows * G + 255) / 256), 256, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta,
-                                                                     r, x, y, rb, re, aux);
-    mcf::note_launch();
-    if (g->n_long_rows > 0) {
-        long long grid = (g->n_long_rows + 7) / 8;
-        if (grid > 8 * sm_count()) grid = 8 * sm_count();
-        k_spmv_long<UNI><<<(unsigned)grid, 256, 0, s>>>(g->long_rows, g->n_long_rows, rp, g->col_ids, g->vals, g->value,
-                                                       alpha, v, beta, r, x, y, rb, re, aux);
-        mcf::note_launch();
+    // ---- short rows: 32 consecutive rows per warp ---------------------------
+    const long long i0 = row_begin + ((long long)(blockIdx.x - long_blocks) * SPMV_WARPS + w) * 32;
+    if (i0 >= row_end) return;
+    const long long i = i0 + lane;
+    const bool in = i < row_end;
+    long long e0 = 0, e1 = 0;
+    if (in) {
+        e0 = row_ptr[i];
+        e1 = row_ptr[i + 1];
+    }
+    const bool mine = in && e1 - e0 <= LONG_ROW;
+    const int len = mine ? (int)(e1 - e0) : 0;
+    int inc = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(MCF_FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    const int start = inc - len, total = __shfl_sync(MCF_FULL, inc, 31);
+    delta[w][lane] = e0 - start;
+    double s = 0.0;
+    for (int P = 0; P < total; P += SEG_CAP) {
+        const int lo = max(start, P), hi = min(start + len, P + SEG_CAP);
+        for (int t = lo; t < hi; ++t) rmap[w][t - P] = (unsigned char)lane;
+        __syncwarp();
+        const int cnt = min(SEG_CAP, total - P);
+        int c[SEG_CAP / 32];
+        double a[SEG_CAP / 32];
+#pragma unroll
+        for (int k = 0; k < SEG_CAP / 32; ++k) {
+            const int t = lane + 32 * k;
+            if (t < cnt) {
+                const long long e = P + t + delta[w][rmap[w][t]];
+                c[k] = __ldg(col_ids + e);
+                a[k] = UNI ? uval : __ldg(vals + e);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SEG_CAP / 32; ++k) {
+            const int t = lane + 32 * k;
+            if (t < cnt) prod[w][t] = __dmul_rn(a[k], __ldg(x + c[k]));
+        }
+        __syncwarp();
+        for (int t = lo; t < hi; ++t) s = __dadd_rn(s, prod[w][t - P]);
+        __syncwarp();
+    }
+    if (mine) {
+        const double out = combine_exact(alpha, v, beta, r, i, s);
+        y[i] = out;
+        if (aux) aux[i].aux = out;
     }
 }
 
@@ -516,14 +537,18 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
     MCF_ARG(g && x && y, "mcf_spmv: null argument");
     MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv: bad row range");
     if (re == rb) return MCF_OK;
-    const bool small = g->nnz / g->n <= 8;
-    if (g->uniform_value) {
-        if (small) launch_spmv<4, true>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
-        else launch_spmv<8, true>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
-    } else {
-        if (small) launch_spmv<4, false>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
-        else launch_spmv<8, false>(g, alpha, v, beta, r, x, y, rb, re, s, aux);
-    }
+    const long long *rp = (const long long *)g->row_ptr;
+    long long lb = g->n_long_rows > 0 ? (g->n_long_rows + SPMV_WARPS - 1) / SPMV_WARPS : 0;
+    if (lb > 2 * sm_count()) lb = 2 * sm_count();
+    const long long sb = (re - rb + 32 * SPMV_WARPS - 1) / (32 * SPMV_WARPS);
+    const unsigned grid = (unsigned)(lb + sb);
+    if (g->uniform_value)
+        k_spmv<true><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r, x, y, rb,
+                                                      re, aux, g->long_rows, g->n_long_rows, (int)lb);
+    else
+        k_spmv<false><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r, x, y, rb,
+                                                       re, aux, g->long_rows, g->n_long_rows, (int)lb);
+    mcf::note_launch();
     MCF_LAUNCHED("k_spmv");
     return MCF_OK;
 }
@@ -548,9 +573,13 @@ int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *
 // caller's upper bound `capacity` (so the whole call can be captured in a
 // CUDA graph).
 int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
-                 long long capacity, WalkCommon &a, int **blk, cudaStream_t s) {
-    int rc = build_blk_col(walk_pre, cb, ce, capacity, blk, s);
-    if (rc) return rc;
+                 long long capacity, WalkCommon &a, int **blk, cudaStream_t s, int *blk_ready = nullptr) {
+    if (blk_ready) {
+        *blk = blk_ready;  // filled by the budget scan (funm_action)
+    } else {
+        int rc = build_blk_col(walk_pre, cb, ce, capacity, blk, s);
+        if (rc) return rc;
+    }
     a.hdr = g->hdr;
     a.went = g->went;
     a.ecol = g->ecol;
@@ -653,7 +682,7 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
 
 static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                   const long long *walk_off, const int *entries, const double *r, double *q, double *qvar,
-                  long long *stats, cudaStream_t s, bool replay, bool aux_ready = false) {
+                  long long *stats, cudaStream_t s, bool replay, bool aux_ready = false, int *blk_ready = nullptr) {
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(r && q && stats, "action walk: null r/q/stats");
@@ -663,7 +692,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     long long nw = 0;
     rc = walk_capacity(p, walk_pre, cb, ce, &nw, s);
     if (rc) return rc;
-    rc = setup_common(g, p, walk_pre, cb, ce, nw, a, &blk, s);
+    rc = setup_common(g, p, walk_pre, cb, ce, nw, a, &blk, s, blk_ready);
     if (rc) return rc;
     MCF_ARG(nw < (1ll << 31) - 4096, "walks per call must be below 2^31 (split the column range)");
     double *xw = nullptr;
@@ -742,15 +771,34 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     return MCF_OK;
 }
 
-// The whole RandFunmAction estimate for one process (Alg. 3): r = A v (the
-// SpMV writes r into the walk headers directly), walks, per-column
-// reduction, y = z0 v + z1 r + A q.  No host synchronisation.
-static int funm_action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, const double *v, double z0,
-                       double z1, double *r, double *q, double *qvar, double *y, long long *stats, cudaStream_t s) {
-    MCF_ARG(g && v && r && q && y, "mcf_funm_action: null argument");
-    int rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+// The whole RandFunmAction estimate for one process (Alg. 3): the walk
+// budgets (largest remainder) on a side stream concurrently with r = A v (the
+// SpMV writes r into the walk headers directly), then walks, per-column
+// reduction, y = z0 v + z1 r + A q.  No host synchronisation; the fork/join
+// uses events, so the whole call captures into one CUDA graph.
+static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks, long long *ni, long long *walk_pre,
+                       const double *v, double z0, double z1, double *r, double *q, double *qvar, double *y,
+                       long long *stats, cudaStream_t s) {
+    MCF_ARG(g && v && r && q && y && ni && walk_pre, "mcf_funm_action: null argument");
+    if (!g->side) {
+        MCF_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+        MCF_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+        MCF_CUDA(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+    }
+    MCF_ARG(p && n_walks >= 1 && n_walks < (1ll << 31) - 4096, "mcf_funm_action: n_walks must be in [1, 2^31 - 4096)");
+    MCF_CUDA(cudaEventRecord(g->ev_fork, s));
+    MCF_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
+    int *blk = nullptr;
+    MCF_CUDA(cudaMallocAsync(&blk, sizeof(int) * ((n_walks + (1ll << WALK_BLK_SHIFT) - 1) >> WALK_BLK_SHIFT), g->side));
+    int rc = allocate_walks(g, n_walks, ni, walk_pre, blk, g->side);
     if (rc) return rc;
-    rc = action(g, p, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true);
+    MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
+    rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+    if (rc) return rc;
+    MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
+    mcf_walk_params pp = *p;
+    pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks
+    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk);
     if (rc) return rc;
     return spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
 }
@@ -759,10 +807,11 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, const long long *
 
 extern "C" {
 
-int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, const double *v, double zeta0,
-                    double zeta1, double *r, double *q, double *q_var, double *y, int64_t *stats, void *stream) {
-    return mcf::funm_action(g, p, (const long long *)walk_pre, v, zeta0, zeta1, r, q, q_var, y, (long long *)stats,
-                            (cudaStream_t)stream);
+int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, int64_t n_walks, int64_t *ni, int64_t *walk_pre,
+                    const double *v, double zeta0, double zeta1, double *r, double *q, double *q_var, double *y,
+                    int64_t *stats, void *stream) {
+    return mcf::funm_action(g, p, (long long)n_walks, (long long *)ni, (long long *)walk_pre, v, zeta0, zeta1, r, q,
+                            q_var, y, (long long *)stats, (cudaStream_t)stream);
 }
 
 int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,

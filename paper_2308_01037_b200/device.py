@@ -237,12 +237,17 @@ class DeviceGraph:
         N.check(N.lib().mcf_walk_action(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce), _ptr(r),
                                         _ptr(q), _ptr(qvar), _ptr(stats), self.stream), "mcf_walk_action")
 
-    def funm_action(self, params: WalkParams, walk_pre, v, z0, z1, r, q, y, qvar=None, stats=None):
-        """Whole single-process RandFunmAction pass in one library call."""
-        N.check(N.lib().mcf_funm_action(self.handle, C.byref(params.c), _ptr(walk_pre), _ptr(v), float(z0), float(z1),
-                                        _ptr(r), _ptr(q), _ptr(qvar), _ptr(y), _ptr(stats), self.stream),
-                "mcf_funm_action")
-        return y
+    def funm_action(self, params: WalkParams, n_walks: int, v, z0, z1, r, q, y, qvar=None, stats=None,
+                    ni=None, walk_pre=None):
+        """Whole single-process RandFunmAction pass in one library call: the
+        budgets for n_walks (computed concurrently with r = A v), walks, q and
+        y.  Returns (y, ni, walk_pre)."""
+        ni = torch.empty(self.n, dtype=torch.int64, device=self.device) if ni is None else ni
+        walk_pre = torch.empty(self.n + 1, dtype=torch.int64, device=self.device) if walk_pre is None else walk_pre
+        N.check(N.lib().mcf_funm_action(self.handle, C.byref(params.c), int(n_walks), _ptr(ni), _ptr(walk_pre),
+                                        _ptr(v), float(z0), float(z1), _ptr(r), _ptr(q), _ptr(qvar), _ptr(y),
+                                        _ptr(stats), self.stream), "mcf_funm_action")
+        return y, ni, walk_pre
 
     def replay_action(self, params: WalkParams, walk_pre, walk_off, entries, r, q, cols=None, stats=None):
         cb, ce = (0, self.n) if cols is None else cols

@@ -112,14 +112,20 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
     g = _graph(a, device)
     vd = v.to(g.device, torch.float64) if isinstance(v, torch.Tensor) else torch.from_numpy(v_np).to(g.device)
     params = WalkParams(cfg, z, g.device)
-    ni, pre = _budgets(g, cfg, replay, budgets)
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
     qvar = torch.zeros_like(q) if stderr else None
     st = g.new_stats()
-    if replay is None:  # r = A v, walks, q, y = z0 v + z1 r + A q in one library call
+    if replay is None and budgets is None:
+        # budgets, r = A v, walks, q, y = z0 v + z1 r + A q in one library call
         r = torch.empty_like(q)
-        y = g.funm_action(params, pre, vd, z[0], z[1], r, q, torch.empty_like(q), qvar, st)
+        y, ni, pre = g.funm_action(params, cfg.n_walks, vd, z[0], z[1], r, q, torch.empty_like(q), qvar, st)
+    elif replay is None:
+        ni, pre = _budgets(g, cfg, replay, budgets)
+        r = g.spmv(vd)
+        g.walk_action(params, pre, r, q, qvar, stats=st)
+        y = g.spmv(q, alpha=z[0], v=vd, beta=z[1], r=r)
     else:
+        ni, pre = _budgets(g, cfg, replay, budgets)
         r = g.spmv(vd)                       # r = A v
         off, ent = _replay_tensors(g, replay)
         g.replay_action(params, pre, off, ent, r, q, stats=st)

@@ -66,12 +66,12 @@ def sharded_action(g: DeviceGraph, coeffs, v: torch.Tensor, config, *, params=No
     coeffs = as_stream(coeffs)
     z = coeffs.prefix(cfg.max_steps + 2)
     params = params or WalkParams(cfg, z, g.device)
-    ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     st = g.new_stats()
-    if size == 1:  # the whole pass in one library call
+    if size == 1 and budgets is None:  # the whole pass in one library call
         q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
         r, y = torch.empty_like(q), torch.empty_like(q)
-        return g.funm_action(params, pre, v, z[0], z[1], r, q, y, stats=st), st
+        return g.funm_action(params, cfg.n_walks, v, z[0], z[1], r, q, y, stats=st)[0], st
+    ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     cols = column_shards(pre, size)[rank]
     rows = row_shards(g.n, size)[rank]
     r = g.spmv(v)

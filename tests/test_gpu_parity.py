@@ -419,3 +419,30 @@ def test_rand_funm_full_consistency_and_closed_form(mc):
     z = mc.rand_funm(mc.SparseMatrix(sparse.csr_array((3, 3)), sparse.csc_array((3, 3))), mc.EXPONENTIAL,
                      mc.WalkConfig(10)).values
     assert np.array_equal(z, np.eye(3))
+
+
+@pytest.mark.parametrize("uniform", [False, True])
+def test_spmv_short_rows_match_sequential_csr_bitwise(mc, uniform):
+    """Rows of <= 64 entries: y = z0 v + z1 r + A x equals numpy/scipy's
+    sequential CSR evaluation bit for bit (products and sums rounded
+    separately, in CSR order) -- the reference computes r = A @ v and
+    y = z[0] * v + z[1] * r + A @ q with exactly these operations."""
+    import torch
+    rng = np.random.default_rng(11)
+    n = 5000
+    lens = rng.integers(0, 65, n)
+    lens[::97] = 64
+    lens[::101] = 0
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.concatenate([rng.choice(n, k, replace=False) for k in lens])
+    vals = np.full(rows.size, 0.37) if uniform else rng.normal(size=rows.size)
+    m = sparse.csr_array((vals, (rows, cols)), shape=(n, n))
+    m.sort_indices()
+    a = port.Csr.from_any(m)
+    g = mc.DeviceGraph(as_matrix(a))
+    x, v, r = rng.normal(size=n), rng.normal(size=n), rng.normal(size=n)
+    t = lambda z: torch.from_numpy(z).cuda()  # noqa: E731
+    y = g.spmv(t(x)).cpu().numpy()
+    assert np.array_equal(y, m @ x)
+    y = g.spmv(t(x), alpha=0.75, v=t(v), beta=-1.25, r=t(r)).cpu().numpy()
+    assert np.array_equal(y, 0.75 * v + -1.25 * r + m @ x)
