@@ -38,13 +38,22 @@ struct AllocState {
     unsigned ncand;
     unsigned long long T;            // threshold key
     long long I;                     // how many of the keys == T to take (lowest indices)
-    unsigned long long cmin, cmax;   // smallest / largest candidate key
+    unsigned long long ncmin, cmax;  // ~(smallest candidate key), largest candidate key
     int b2;                          // sub-bucket of b* holding the R-th largest (-1: none / not refined)
     int resolved;                    // T and the tie count are known (no candidate pass needed)
     unsigned hist[NBUCKET];
     unsigned hist2[NBUCKET];
-    unsigned long long min2[NBUCKET], max2[NBUCKET];
+    unsigned long long nmin2[NBUCKET], max2[NBUCKET];  // ~min / max key per sub-bucket (zero-initialised)
 };
+
+// N_i = floor(p_i N) and the remainder key (IEEE bits of the remainder + 1;
+// 0 for p_i = 0), recomputed from p by every pass instead of stored
+__device__ __forceinline__ void floor_key(double pi, double total, long long &got, unsigned long long &k) {
+    const double want = __dmul_rn(pi, total);
+    const double fl = floor(want);
+    got = (long long)fl;
+    k = pi != 0.0 ? (unsigned long long)__double_as_longlong(__dsub_rn(want, fl)) + 1ull : 0ull;
+}
 
 __device__ __forceinline__ int rem_bucket(unsigned long long key) {
     if (key == 0) return -1;
@@ -95,8 +104,7 @@ __device__ void find_bin(const unsigned *cnt, long long R, int *bin, long long *
 // block-parallel search from the top bucket: thread t holds bucket NBUCKET-1-t*4..; finds b with
 // count(above b) < R <= count(above b) + hist[b]
 __global__ void __launch_bounds__(256, 4) k_alloc_floor(const double *__restrict__ p, long long n, double total,
-                                                     long long n_walks, long long *__restrict__ ni,
-                                                     unsigned long long *__restrict__ key, AllocState *st) {
+                                                        long long n_walks, AllocState *st) {
     __shared__ unsigned h[NBUCKET];
     __shared__ bool last;
     for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) h[b] = 0;
@@ -112,16 +120,10 @@ __global__ void __launch_bounds__(256, 4) k_alloc_floor(const double *__restrict
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const long long i = i0 + u * stride;
-            const double pi = pv[u];
-            const double want = __dmul_rn(pi, total);
-            const double fl = floor(want);
-            const long long got = (long long)fl;
-            unsigned long long k = 0;
-            if (pi != 0.0) {
-                k = (unsigned long long)__double_as_longlong(__dsub_rn(want, fl)) + 1ull;
-                ++pos;
-            }
-            const int bk = k ? rem_bucket(k) : -1;
+            long long got;
+            unsigned long long k;
+            floor_key(pv[u], total, got, k);
+            const int bk = (i < n && k) ? rem_bucket(k) : -1;
             const int b0 = __shfl_sync(MCF_FULL, bk, 0);
             if (__all_sync(MCF_FULL, bk == b0)) {  // equal-degree runs share a bucket
                 if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicAdd(&h[b0], 32u);
@@ -129,9 +131,8 @@ __global__ void __launch_bounds__(256, 4) k_alloc_floor(const double *__restrict
                 atomicAdd(&h[bk], 1u);
             }
             if (i < n) {
-                ni[i] = got;
                 got_sum += got;
-                key[i] = k;
+                pos += k ? 1 : 0;
             }
         }
     }
@@ -175,8 +176,8 @@ __global__ void __launch_bounds__(256, 4) k_alloc_floor(const double *__restrict
 // Level 2: histogram of bucket b* into 1024 sub-buckets with per-sub-bucket
 // min/max key; the last block picks the sub-bucket, and if it holds a single
 // distinct value (the usual case: equal-degree ties) T is resolved here.
-__global__ void __launch_bounds__(256) k_alloc_level2(const unsigned long long *__restrict__ key, long long n,
-                                                      AllocState *st) {
+__global__ void __launch_bounds__(256, 4) k_alloc_level2(const double *__restrict__ p, long long n, double total,
+                                                         AllocState *st) {
     __shared__ unsigned h[NBUCKET];
     __shared__ unsigned long long mn[NBUCKET], mx[NBUCKET];
     __shared__ bool last;
@@ -189,30 +190,40 @@ __global__ void __launch_bounds__(256) k_alloc_level2(const unsigned long long *
     }
     __syncthreads();
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
-        const long long i = base + threadIdx.x;
-        const unsigned long long k = i < n ? key[i] : 0ull;
-        const bool in = i < n && rem_bucket(k) == bstar;
-        const int sb = in ? rem_sub(k, bstar) : -1;
-        const int s0 = __shfl_sync(MCF_FULL, sb, 0);
-        const unsigned long long k0 = __shfl_sync(MCF_FULL, k, 0);
-        if (__all_sync(MCF_FULL, in && k == k0)) {  // one tied key across the warp
-            if ((threadIdx.x & 31) == 0) {
-                atomicAdd(&h[s0], 32u);
-                atomicMin(&mn[s0], k0);
-                atomicMax(&mx[s0], k0);
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += 4 * stride) {
+        double pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long i = base + u * stride + threadIdx.x;
+            pv[u] = i < n ? p[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            long long got;
+            unsigned long long k;
+            floor_key(pv[u], total, got, k);
+            const bool in = k && rem_bucket(k) == bstar;
+            const int sb = in ? rem_sub(k, bstar) : -1;
+            const int s0 = __shfl_sync(MCF_FULL, sb, 0);
+            const unsigned long long k0 = __shfl_sync(MCF_FULL, k, 0);
+            if (__all_sync(MCF_FULL, in && k == k0)) {  // one tied key across the warp
+                if ((threadIdx.x & 31) == 0) {
+                    atomicAdd(&h[s0], 32u);
+                    atomicMin(&mn[s0], k0);
+                    atomicMax(&mx[s0], k0);
+                }
+            } else if (in) {
+                atomicAdd(&h[sb], 1u);
+                atomicMin(&mn[sb], k);
+                atomicMax(&mx[sb], k);
             }
-        } else if (in) {
-            atomicAdd(&h[sb], 1u);
-            atomicMin(&mn[sb], k);
-            atomicMax(&mx[sb], k);
         }
     }
     __syncthreads();
     for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) {
         if (h[b]) {
             atomicAdd(&st->hist2[b], h[b]);
-            atomicMin(&st->min2[b], mn[b]);
+            atomicMax(&st->nmin2[b], ~mn[b]);
             atomicMax(&st->max2[b], mx[b]);
         }
     }
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(256) k_alloc_level2(const unsigned long long *
     if (threadIdx.x == 0) {
         st->b2 = b2;
         st->need = need2;
-        const unsigned long long lo = atomicAdd(&st->min2[b2], 0ull), hi = atomicMax(&st->max2[b2], 0ull);
+        const unsigned long long lo = ~atomicAdd(&st->nmin2[b2], 0ull), hi = atomicMax(&st->max2[b2], 0ull);
         if (lo == hi) {  // single distinct value: it is the threshold
             st->T = lo;
             st->I = need2;
@@ -243,21 +254,23 @@ __global__ void __launch_bounds__(256) k_alloc_level2(const unsigned long long *
     }
 }
 
-__global__ void k_alloc_cands(const unsigned long long *__restrict__ key, long long n, AllocState *st,
-                              unsigned long long *__restrict__ ckey, int *__restrict__ cidx) {
+__global__ void k_alloc_cands(const double *__restrict__ p, long long n, double total, AllocState *st,
+                              unsigned long long *__restrict__ ckey) {
     const int bstar = st->bstar, b2 = st->b2;
     if (bstar < 0 || st->resolved) return;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
         const long long i = base + threadIdx.x;
-        const bool in = i < n && rem_bucket(key[i]) == bstar && rem_sub(key[i], bstar) == b2;
+        long long got;
+        unsigned long long kk = 0;
+        if (i < n) floor_key(p[i], total, got, kk);
+        const bool in = kk && rem_bucket(kk) == bstar && rem_sub(kk, bstar) == b2;
         const unsigned m = __ballot_sync(MCF_FULL, in);
         if (!m) continue;
         unsigned pos = 0;
         if ((threadIdx.x & 31) == 0) pos = atomicAdd(&st->ncand, (unsigned)__popc(m));
         pos = __shfl_sync(MCF_FULL, pos, 0);
-        unsigned long long kk = in ? key[i] : 0ull;
-        unsigned long long mn = in ? kk : ~0ull, mx = kk;
+        unsigned long long mn = in ? kk : ~0ull, mx = in ? kk : 0ull;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long a = __shfl_xor_sync(MCF_FULL, mn, o), b = __shfl_xor_sync(MCF_FULL, mx, o);
@@ -265,14 +278,10 @@ __global__ void k_alloc_cands(const unsigned long long *__restrict__ key, long l
             mx = b > mx ? b : mx;
         }
         if ((threadIdx.x & 31) == 0) {
-            atomicMin(&st->cmin, mn);
+            atomicMax(&st->ncmin, ~mn);
             atomicMax(&st->cmax, mx);
         }
-        if (in) {
-            const unsigned r = pos + __popc(m & lanemask_lt());
-            ckey[r] = kk;
-            cidx[r] = (int)i;
-        }
+        if (in) ckey[pos + __popc(m & lanemask_lt())] = kk;
     }
 }
 
@@ -287,9 +296,9 @@ __global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long 
     __shared__ long long wsum[32];
     if (st->bstar == -2 || st->resolved) return;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    if (st->cmin == st->cmax) {  // a single distinct value: it is the threshold
+    if (~st->ncmin == st->cmax) {  // a single distinct value: it is the threshold
         if (t == 0) {
-            st->T = st->cmin;
+            st->T = st->cmax;
             st->I = st->need;
         }
         return;
@@ -405,7 +414,7 @@ __global__ void __launch_bounds__(1024) k_alloc_select(const unsigned long long 
     }
 }
 
-__global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const unsigned long long *__restrict__ key, long long n,
+__global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const double *__restrict__ p, long long n, double total,
                                                           const AllocState *st, long long *__restrict__ ni,
                                                           long long *__restrict__ walk_pre, int *__restrict__ blk_col,
                                                           unsigned long long *sa, unsigned long long *sb,
@@ -424,8 +433,10 @@ __global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const unsigned long lo
         const long long j = base + 32 * k;
         a[k] = b[k] = 0;
         if (j < n) {
-            const unsigned long long kj = key[j];
-            a[k] = ni[j] + ((select && kj > T) ? 1 : 0);
+            long long got;
+            unsigned long long kj;
+            floor_key(p[j], total, got, kj);
+            a[k] = got + ((select && kj > T) ? 1 : 0);
             b[k] = (select && kj == T) ? 1 : 0;
         }
     }
@@ -455,38 +466,36 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     MCF_ARG(n_walks >= 1, "n_walks must be at least 1");  // walker.py:168-169
     MCF_ARG(n_walks < (1ll << 53), "n_walks must be below 2^53");
     const long long n = g->n;
-    AllocState *st = nullptr;
-    unsigned long long *key = nullptr, *ckey = nullptr;
-    int *cidx = nullptr;
-    MCF_CUDA(cudaMallocAsync(&st, sizeof(AllocState), s));
     if (n == 0) {
         MCF_CUDA(cudaMemsetAsync(walk_pre, 0, sizeof(long long), s));
         return MCF_OK;
     }
+    // one zero-initialised block: selection state + the budget scan's look-back words
     const long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    MCF_CUDA(cudaMallocAsync(&key, sizeof(unsigned long long) * (2 * n + 2 * tiles + 1) + sizeof(int) * n, s));
-    ckey = key + n;
-    unsigned long long *sa = ckey + n, *sb = sa + tiles;  // look-back state of k_alloc_scan
+    const size_t state_bytes = (sizeof(AllocState) + 15) & ~size_t(15);
+    char *blk = nullptr;
+    unsigned long long *ckey = nullptr;
+    MCF_CUDA(cudaMallocAsync(&blk, state_bytes + sizeof(unsigned long long) * (2 * tiles + 2), s));
+    AllocState *st = reinterpret_cast<AllocState *>(blk);
+    unsigned long long *sa = reinterpret_cast<unsigned long long *>(blk + state_bytes), *sb = sa + tiles;
     unsigned *ctr = reinterpret_cast<unsigned *>(sb + tiles);
-    cidx = reinterpret_cast<int *>(ctr + 2);
-    MCF_CUDA(cudaMemsetAsync(st, 0, sizeof(AllocState), s));
-    MCF_CUDA(cudaMemsetAsync(&st->cmin, 0xff, sizeof(unsigned long long), s));
-    MCF_CUDA(cudaMemsetAsync(st->min2, 0xff, sizeof(st->min2), s));
-    const int grid = sm_count() * 4;
-    k_alloc_floor<<<grid, 256, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, ni, key, st);
+    MCF_CUDA(cudaMemsetAsync(blk, 0, state_bytes + sizeof(unsigned long long) * (2 * tiles + 2), s));
+    MCF_CUDA(cudaMallocAsync(&ckey, sizeof(unsigned long long) * n, s));  // candidates (rarely written)
+    const double total = (double)n_walks;
+    const int grid = sm_count() * 2;
+    k_alloc_floor<<<grid, 256, 0, s>>>(g->init_prob, n, total, n_walks, st);
     mcf::note_launch();
-    k_alloc_level2<<<grid, 256, 0, s>>>(key, n, st);
+    k_alloc_level2<<<grid, 256, 0, s>>>(g->init_prob, n, total, st);
     mcf::note_launch();
-    k_alloc_cands<<<grid, 256, 0, s>>>(key, n, st, ckey, cidx);
+    k_alloc_cands<<<grid, 256, 0, s>>>(g->init_prob, n, total, st, ckey);
     mcf::note_launch();
     k_alloc_select<<<1, 1024, 0, s>>>(ckey, st);
     mcf::note_launch();
-    MCF_CUDA(cudaMemsetAsync(sa, 0, sizeof(unsigned long long) * (2 * tiles + 1), s));
-    k_alloc_scan<<<(unsigned)tiles, SCAN_T, 0, s>>>(key, n, st, ni, walk_pre, blk_col, sa, sb, ctr);
+    k_alloc_scan<<<(unsigned)tiles, SCAN_T, 0, s>>>(g->init_prob, n, total, st, ni, walk_pre, blk_col, sa, sb, ctr);
     mcf::note_launch();
     MCF_LAUNCHED("allocate");
-    MCF_CUDA(cudaFreeAsync(st, s));
-    MCF_CUDA(cudaFreeAsync(key, s));
+    MCF_CUDA(cudaFreeAsync(ckey, s));
+    MCF_CUDA(cudaFreeAsync(blk, s));
     return MCF_OK;
 }
 

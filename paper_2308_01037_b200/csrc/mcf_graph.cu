@@ -536,6 +536,12 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
             g->went = nullptr;
         }
         g->info.walk_layout = g->went ? 1 : 0;
+        // L2-resident compact tables: the walk kernels stream them into L2
+        // with TMA bulk prefetches before walking (sequential HBM reads instead
+        // of one random sector fetch per first touch; MCF_L2_PREFETCH=0 off)
+        const double walk_bytes = compact_bytes + (g->cdf ? 8.0 * g->nnz : 0.0);
+        const char *pf = getenv("MCF_L2_PREFETCH");
+        g->l2_prefetch = !g->went && walk_bytes <= 0.6 * (double)l2 && !(pf && !strcmp(pf, "0"));
     }
     k_divide<<<nb, 256, 0, s>>>(g->col_norm, total, n, g->init_prob);  // p_j (walker.py:129)
     mcf::note_launch();

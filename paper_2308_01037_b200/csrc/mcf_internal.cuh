@@ -82,6 +82,7 @@ struct mcf_graph {
     int32_t *ecol = nullptr;         // nnz; col | (a<0)<<31 (aliases col_ids if no negatives)
     bool ecol_owned = false;
     double *cdf = nullptr;           // nnz within-row CDF (only if some row is non-uniform)
+    bool l2_prefetch = false;        // compact tables fit L2: walk kernels bulk-prefetch them first
     double *col_norm = nullptr;      // n
     double *init_prob = nullptr;     // n
     int64_t *csr2csc = nullptr;      // nnz, lazily built for diag
@@ -159,9 +160,14 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// One 256-bit load (sm_100 LDG.E.ENL2.256): a random 32-B record costs one
+// L1 wavefront instead of two for a pair of 128-bit loads -- the walk kernels
+// are bound by L1 wavefronts per step.
 __device__ __forceinline__ NodeHdr load_hdr(const NodeHdr *h) {
-    const int4 *p = reinterpret_cast<const int4 *>(h);
-    int4 a = __ldg(p), b = __ldg(p + 1);
+    int4 a, b;
+    asm("ld.global.nc.L2::evict_normal.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(h));
     NodeHdr r;
     r.start = a.x;
     r.deg = a.y;

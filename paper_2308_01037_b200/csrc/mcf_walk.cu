@@ -42,7 +42,36 @@ struct WalkCommon {
     int return_only;             // MCF_FLAG_RETURN_ONLY
     long long *stats;
     int *err;
+    // L2 bulk prefetch of the walk tables at kernel start (bytes 0: none)
+    const char *pf[3];
+    long long pf_bytes[3];
 };
+
+// Alternative (MCF_L2_PREFETCH=2): a streaming read of the tables by a
+// separate kernel (16-B loads cached in L2 only) right before the walk.
+__global__ void k_l2_touch(const uint4 *__restrict__ p, long long n16, unsigned *sink) {
+    uint32_t acc = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcg(p + i);
+        acc ^= v.x ^ v.w;
+    }
+    if (acc == 0x9e3779b9u && sink) *sink = acc;
+}
+
+// Each CTA streams its share of the walk tables into L2 with TMA bulk
+// prefetches (cp.async.bulk.prefetch.L2: no registers, no shared memory, the
+// copy engine does the sequential read) before its lanes start walking.
+__device__ __forceinline__ void l2_prefetch_tables(const WalkCommon &a) {
+    if (threadIdx.x >= 3 || a.pf_bytes[threadIdx.x] <= 0) return;
+    const long long bytes = a.pf_bytes[threadIdx.x];
+    const long long share = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ll;
+    const long long lo = share * blockIdx.x;
+    const long long hi = lo + share < bytes ? lo + share : bytes;
+    for (long long o = lo; o < hi; o += 32768) {
+        const unsigned len = (unsigned)((hi - o < 32768 ? hi - o : 32768) & ~15ll);
+        if (len) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf[threadIdx.x] + o), "r"(len) : "memory");
+    }
+}
 
 // Inverse-CDF draw inside one non-uniform row: first t with cdf[t] > u.
 __device__ __forceinline__ int cdf_pick(const double *__restrict__ cdf, int deg, double u) {
@@ -218,7 +247,7 @@ __device__ __forceinline__ bool apply(const WalkCommon &a, Lane &L, long long e,
 
 template <int NW, int OCC>
 struct WalkOcc {  // resident CTAs per SM the register budget is tuned for
-    static constexpr int v = NW == 1 ? OCC : (NW == 2 ? 3 : 2);
+    static constexpr int v = NW == 1 ? OCC : (NW == 2 ? (OCC == 4 ? 4 : 3) : 2);
 };
 
 // NW walks per lane, stepped together so their dependent loads overlap.
@@ -226,6 +255,7 @@ struct WalkOcc {  // resident CTAs per SM the register budget is tuned for
 // 5: more warps with a few spilled registers).
 template <bool REPLAY, bool FAT, int NW, int OCC = 5>
 __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(WalkCommon a, double *__restrict__ xw) {
+    l2_prefetch_tables(a);
     const long long wb = __ldg(a.walk_pre + a.col_begin);
     const int nw = (int)(__ldg(a.walk_pre + a.col_end) - wb);
     Lane L[NW];
@@ -282,6 +312,7 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
                                                    long long *__restrict__ eaux, int *__restrict__ est,
                                                    double *__restrict__ ewt) {
     constexpr bool REPLAY = MODE == EMIT_REPLAY;
+    if (MODE != EMIT_COUNT) l2_prefetch_tables(a);
     const long long wb = __ldg(a.walk_pre + a.col_begin);
     const int nw = (int)(__ldg(a.walk_pre + a.col_end) - wb);
     Lane L;
@@ -598,6 +629,32 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.entries = nullptr;
     a.colmax = nullptr;
     a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
+    for (int k = 0; k < 3; ++k) {
+        a.pf[k] = nullptr;
+        a.pf_bytes[k] = 0;
+    }
+    if (g->l2_prefetch) {
+        a.pf[0] = (const char *)g->hdr;
+        a.pf_bytes[0] = (long long)sizeof(NodeHdr) * g->n;
+        a.pf[1] = (const char *)g->ecol;
+        a.pf_bytes[1] = 4ll * g->nnz;
+        if (g->cdf) {
+            a.pf[2] = (const char *)g->cdf;
+            a.pf_bytes[2] = 8ll * g->nnz;
+        }
+        for (int k = 0; k < 3; ++k)  // bulk prefetch wants 16-B aligned ranges
+            if ((uintptr_t)a.pf[k] & 15) a.pf_bytes[k] = 0;
+        const char *mode = getenv("MCF_L2_PREFETCH");
+        if (mode && !strcmp(mode, "2")) {
+            for (int k = 0; k < 3; ++k) {
+                if (a.pf_bytes[k] > 0) {
+                    k_l2_touch<<<sm_count() * 4, 512, 0, s>>>((const uint4 *)a.pf[k], a.pf_bytes[k] / 16, nullptr);
+                    mcf::note_launch();
+                }
+                a.pf_bytes[k] = 0;
+            }
+        }
+    }
     return MCF_OK;
 }
 
@@ -623,7 +680,7 @@ static int walks_per_lane() {
     if (!v) {
         const char *e = getenv("MCF_WALKS_PER_LANE");
         v = e ? atoi(e) : 14;
-        if (v != 1 && v != 2 && v != 4) v = 14;  // 14 = one walk, 4 CTAs/SM (no spills): best measured
+        if (v != 1 && v != 2 && v != 4 && v != 16 && v != 24) v = 14;  // 14 = one walk, 4 CTAs/SM (no spills): best measured
     }
     return v;
 }
@@ -728,6 +785,8 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
                     case 2: k_walk_action<false, true, 2><<<walk_grid(k_walk_action<false, true, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 4: k_walk_action<false, true, 4><<<walk_grid(k_walk_action<false, true, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 14: k_walk_action<false, true, 1, 4><<<walk_grid(k_walk_action<false, true, 1, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 16: k_walk_action<false, true, 1, 6><<<walk_grid(k_walk_action<false, true, 1, 6>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 24: k_walk_action<false, true, 2, 4><<<walk_grid(k_walk_action<false, true, 2, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     default: k_walk_action<false, true, 1><<<walk_grid(k_walk_action<false, true, 1>, 256, 0), 256, 0, s>>>(a, xw);
                 }
             }
@@ -739,6 +798,8 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
                     case 2: k_walk_action<false, false, 2><<<walk_grid(k_walk_action<false, false, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 4: k_walk_action<false, false, 4><<<walk_grid(k_walk_action<false, false, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 14: k_walk_action<false, false, 1, 4><<<walk_grid(k_walk_action<false, false, 1, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 16: k_walk_action<false, false, 1, 6><<<walk_grid(k_walk_action<false, false, 1, 6>, 256, 0), 256, 0, s>>>(a, xw); break;
+                    case 24: k_walk_action<false, false, 2, 4><<<walk_grid(k_walk_action<false, false, 2, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     default: k_walk_action<false, false, 1><<<walk_grid(k_walk_action<false, false, 1>, 256, 0), 256, 0, s>>>(a, xw);
                 }
             }
