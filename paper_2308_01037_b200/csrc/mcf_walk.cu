@@ -466,8 +466,6 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
                                               long long row_end, NodeHdr *__restrict__ aux,
                                               const int *__restrict__ long_rows, long long n_long, int long_blocks) {
     __shared__ double prod[SPMV_WARPS][SEG_CAP];
-    __shared__ unsigned char rmap[SPMV_WARPS][SEG_CAP];
-    __shared__ long long delta[SPMV_WARPS][32];
     __shared__ double part[SPMV_WARPS];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if ((int)blockIdx.x < long_blocks) {
@@ -511,6 +509,8 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
         return;
     }
     // ---- short rows: 32 consecutive rows per warp ---------------------------
+    // The warp's short rows form runs of consecutive rows between long rows;
+    // each run's entries are one contiguous CSR range, walked SEG_CAP at a time.
     const long long i0 = row_begin + ((long long)(blockIdx.x - long_blocks) * SPMV_WARPS + w) * 32;
     if (i0 >= row_end) return;
     const long long i = i0 + lane;
@@ -521,40 +521,46 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
         e1 = row_ptr[i + 1];
     }
     const bool mine = in && e1 - e0 <= LONG_ROW;
-    const int len = mine ? (int)(e1 - e0) : 0;
-    int inc = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(MCF_FULL, inc, o);
-        if (lane >= o) inc += t;
-    }
-    const int start = inc - len, total = __shfl_sync(MCF_FULL, inc, 31);
-    delta[w][lane] = e0 - start;
+    const int nl = row_end - i0 < 32 ? (int)(row_end - i0) : 32;  // valid lanes (warp-uniform)
+    unsigned longm = __ballot_sync(MCF_FULL, in && !mine);
     double s = 0.0;
-    for (int P = 0; P < total; P += SEG_CAP) {
-        const int lo = max(start, P), hi = min(start + len, P + SEG_CAP);
-        for (int t = lo; t < hi; ++t) rmap[w][t - P] = (unsigned char)lane;
-        __syncwarp();
-        const int cnt = min(SEG_CAP, total - P);
-        int c[SEG_CAP / 32];
-        double a[SEG_CAP / 32];
+    int first = 0;
+    while (first < nl) {
+        const int stop = longm ? __ffs(longm) - 1 : nl;  // run = lanes [first, stop)
+        if (stop > first) {
+            const long long run_lo = __shfl_sync(MCF_FULL, e0, first);
+            const long long run_hi = __shfl_sync(MCF_FULL, e1, stop - 1);
+            const bool member = lane >= first && lane < stop;
+            const long long rs = e0 - run_lo, re = e1 - run_lo;  // my row inside the run
+            for (long long P = 0; P < run_hi - run_lo; P += SEG_CAP) {
+                const int cnt = (int)(run_hi - run_lo - P < SEG_CAP ? run_hi - run_lo - P : SEG_CAP);
+                int c[SEG_CAP / 32];
+                double av[SEG_CAP / 32];
 #pragma unroll
-        for (int k = 0; k < SEG_CAP / 32; ++k) {
-            const int t = lane + 32 * k;
-            if (t < cnt) {
-                const long long e = P + t + delta[w][rmap[w][t]];
-                c[k] = __ldg(col_ids + e);
-                a[k] = UNI ? uval : __ldg(vals + e);
+                for (int k = 0; k < SEG_CAP / 32; ++k) {
+                    const int t = lane + 32 * k;
+                    if (t < cnt) {
+                        const long long e = run_lo + P + t;
+                        c[k] = __ldg(col_ids + e);
+                        av[k] = UNI ? uval : __ldg(vals + e);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < SEG_CAP / 32; ++k) {
+                    const int t = lane + 32 * k;
+                    if (t < cnt) prod[w][t] = __dmul_rn(av[k], __ldg(x + c[k]));
+                }
+                __syncwarp();
+                if (member) {
+                    const long long lo = rs > P ? rs : P, hi = re < P + cnt ? re : P + cnt;
+                    for (long long t = lo; t < hi; ++t) s = __dadd_rn(s, prod[w][t - P]);
+                }
+                __syncwarp();
             }
         }
-#pragma unroll
-        for (int k = 0; k < SEG_CAP / 32; ++k) {
-            const int t = lane + 32 * k;
-            if (t < cnt) prod[w][t] = __dmul_rn(a[k], __ldg(x + c[k]));
-        }
-        __syncwarp();
-        for (int t = lo; t < hi; ++t) s = __dadd_rn(s, prod[w][t - P]);
-        __syncwarp();
+        if (!longm) break;
+        first = stop + 1;
+        longm &= longm - 1;
     }
     if (mine) {
         const double out = combine_exact(alpha, v, beta, r, i, s);
