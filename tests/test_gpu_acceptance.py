@@ -81,3 +81,32 @@ def test_estrada_and_ranking_api(mc):
     assert list(rep.ranking) in ([0, 1], [1, 0])
     with pytest.raises(mc.ArgumentError):
         mc.estrada_index(mc.total_communicability(a, 0.1, mc.WalkConfig(100)))
+
+
+def test_cutoff_knee(mc):
+    """#3: error vs W_c in {1e-2..1e-10} at fixed N_s = 1e5 falls (non-increasing)
+    down to a knee and is flat within 2x statistical noise beyond it.  The
+    geometric (Katz) series on a 64-node small world with rho = 0.5 makes the
+    truncation error visible at large W_c: the walk weight decays as
+    (row sum)^k, so W_c sets the walk length."""
+    from paper_2308_01037_b200.graphs import small_world
+    a = small_world(64, 4, 0.1, seed=5)
+    dense = a.csr.toarray()
+    lam = float(np.linalg.eigvalsh(dense)[-1])
+    gamma = 0.5 / lam
+    exact = np.linalg.solve(np.eye(64) - gamma * dense, np.ones(64))
+    g = mc.DeviceGraph(a, gamma=gamma)
+    cutoffs = [10.0 ** -k for k in range(2, 11)]
+    errs = []
+    for wc in cutoffs:
+        e = [np.max(np.abs(mc.rand_funm_action(g, mc.RESOLVENT, np.ones(64),
+                                                mc.WalkConfig(10**5, wc, 100_000, s)).values - exact) / exact)
+             for s in range(8)]
+        errs.append(float(np.mean(e)))
+    plateau = float(np.median(errs[-3:]))
+    knee = next(k for k, e in enumerate(errs) if e <= 2 * plateau)
+    assert knee >= 1, errs                      # the largest cutoff truncates visibly
+    for k in range(knee):                       # non-increasing down to the knee
+        assert errs[k + 1] <= errs[k] * 1.1, errs
+    for e in errs[knee:]:                       # flat beyond it
+        assert plateau / 2 <= e <= 2 * plateau, errs
