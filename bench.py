@@ -5,8 +5,8 @@ and nodes/s; achieved HBM GB/s vs peak).
 Default workload = BASELINE configs[1] ("config 2"): total communicability
 exp(beta A) 1 on a Barabasi-Albert graph, n = 1e6, m = 4, beta = 1/lambda_max,
 30 Taylor terms (max_steps = 28), 10,000 batches x 64 = 640,000 walks.
-A "step" is one full estimator pass: walk budgets, r = A v, the walks, the
-per-column reduction and y = z0 v + z1 r + A q.
+A "step" is one full estimator pass: walk budgets, r = A v (v = 1: the row
+sums), the walks, the per-column reduction and y = z0 v + z1 r + A q.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|1] [--impl mcfunm|reference]
 
@@ -298,7 +298,6 @@ def run_device(args, cfg):
     z = coeffs.prefix(cfg["max_steps"] + 2)
     params = WalkParams(wcfg, z)
     g = DeviceGraph(a, gamma=beta)
-    v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=g.device)  # > 126 MB L2
     # The write leaves L2 full of DIRTY lines whose write-back would otherwise
     # land inside the next timed step; reading a second buffer of the same size
@@ -314,7 +313,7 @@ def run_device(args, cfg):
 
     def step():
         if cfg["kind"] == "action":
-            return parallel.sharded_action(g, coeffs, v, wcfg, params=params)
+            return parallel.sharded_action(g, coeffs, None, wcfg, params=params)  # f(A) 1: v = 1
         return parallel.sharded_diag(g, coeffs, wcfg, params=params)
 
     clocks = Clocks(local) if rank == 0 else None
@@ -435,9 +434,8 @@ def run_device(args, cfg):
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             ge = DeviceGraph(a, gamma=beta)
-            ve = torch.ones(ge.n, dtype=torch.float64, device=ge.device)
             if cfg["kind"] == "action":
-                y, _ = parallel.sharded_action(ge, coeffs, ve, wcfg)
+                y, _ = parallel.sharded_action(ge, coeffs, None, wcfg)
             else:
                 y, _ = parallel.sharded_diag(ge, coeffs, wcfg)
             host = to_host(y)

@@ -151,7 +151,9 @@ MCF_API int mcf_walk_action(mcf_graph *g, const mcf_walk_params *p, const int64_
  * SPEC.md:369-377): the budgets for n_walks (-> ni[n], walk_pre[n+1], as
  * mcf_allocate_walks, computed on an internal stream concurrently with
  * r = A v), the walks of every column, q, optional q_var, and
- * y = zeta0 v + zeta1 r + A q ([dev] n each).  Single process (the multi-GPU
+ * y = zeta0 v + zeta1 r + A q ([dev] n each).  v may be NULL for v = 1 (total
+ * communicability): r is then the row sums of A, bit-identical
+ * to the reference's A @ ones.  Single process (the multi-GPU
  * path composes mcf_spmv / mcf_walk_action with an exchange of q).  No host
  * synchronisation: capturable in a CUDA graph (set p->walk_capacity). */
 MCF_API int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, int64_t n_walks, int64_t *ni,

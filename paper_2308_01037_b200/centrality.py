@@ -79,7 +79,7 @@ def total_communicability(a, gamma: float, config, *, device=None, **kw) -> Cent
     """fTC(i) = (exp(gamma A) 1)_i via rand_funm_action with v = 1."""
     n = _check_graph(a)
     g = _scaled(a, gamma, device)
-    res = rand_funm_action(g, EXPONENTIAL, torch.ones(n, dtype=torch.float64, device=g.device), config, **kw)
+    res = rand_funm_action(g, EXPONENTIAL, None, config, **kw)  # v = 1
     return _report("total-communicability", a,
                    np.asarray(res.values if not torch.is_tensor(res.values) else res.values.cpu()), gamma, res)
 
@@ -136,7 +136,7 @@ def katz_centrality(a, fraction: float, config, method: str = "randomized", *, g
         gamma = gershgorin_gamma(a, fraction)
     g = _scaled(a, gamma, device)
     if method == "randomized":
-        res = rand_funm_action(g, RESOLVENT, torch.ones(n, dtype=torch.float64, device=g.device), config, **kw)
+        res = rand_funm_action(g, RESOLVENT, None, config, **kw)  # v = 1
         vals = res.values.cpu().numpy() if torch.is_tensor(res.values) else res.values
         return _report("katz", a, np.asarray(vals), gamma, res)
     if method == "cg":

@@ -448,14 +448,35 @@ constexpr int HUGE_ROW = 1024;
 constexpr int SEG_CAP = 256;
 constexpr int SPMV_WARPS = 8;
 
+// v == V_ONES stands for the all-ones vector (total communicability)
+#define V_ONES (reinterpret_cast<const double *>(1))
+
 __device__ __forceinline__ double combine_exact(double alpha, const double *v, double beta, const double *r,
                                                 long long i, double s) {
     // ((alpha v) + (beta r)) + s, each operation rounded: the numpy expression
     // z0 * v + z1 * r + A @ q evaluated elementwise
     double h = 0.0;
-    if (v) h = __dmul_rn(alpha, v[i]);
+    if (v) h = v == V_ONES ? alpha : __dmul_rn(alpha, v[i]);
     if (r) h = v ? __dadd_rn(h, __dmul_rn(beta, r[i])) : __dmul_rn(beta, r[i]);
     return (v || r) ? __dadd_rn(h, s) : s;
+}
+
+// r = A 1 for v = 1: the sequential CSR row sum of a_ij, which for a row
+// without negative entries is exactly the |a| row sum already in the header
+// (same additions, same order, a * 1.0 == a); rows with a negative entry are
+// summed again with their signs.  r also lands in hdr.aux for the walk.
+__global__ void k_r_ones(NodeHdr *__restrict__ hdr, const double *__restrict__ vals, long long n, double *__restrict__ r) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const NodeHdr h = load_hdr(hdr + i);
+    double s = h.rsum;
+    if (h.flags & HDR_HAS_NEG) {
+        s = 0.0;
+        for (int t = 0; t < h.deg; ++t) s = __dadd_rn(s, vals[h.start + t]);
+    }
+    if (h.deg == 0) s = 0.0;
+    r[i] = s;
+    hdr[i].aux = s;
 }
 
 template <bool UNI>
@@ -840,13 +861,13 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
 
 // The whole RandFunmAction estimate for one process (Alg. 3): the walk
 // budgets (largest remainder) on a side stream concurrently with r = A v (the
-// SpMV writes r into the walk headers directly), then walks, per-column
-// reduction, y = z0 v + z1 r + A q.  No host synchronisation; the fork/join
+// SpMV writes r into the walk headers directly; v = NULL means v = 1, whose
+// r is the row sums), then walks, per-column reduction, y = z0 v + z1 r + A q.  No host synchronisation; the fork/join
 // uses events, so the whole call captures into one CUDA graph.
 static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks, long long *ni, long long *walk_pre,
                        const double *v, double z0, double z1, double *r, double *q, double *qvar, double *y,
                        long long *stats, cudaStream_t s) {
-    MCF_ARG(g && v && r && q && y && ni && walk_pre, "mcf_funm_action: null argument");
+    MCF_ARG(g && r && q && y && ni && walk_pre, "mcf_funm_action: null argument");
     if (!g->side) {
         MCF_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
         MCF_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
@@ -860,8 +881,15 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     int rc = allocate_walks(g, n_walks, ni, walk_pre, blk, g->side);
     if (rc) return rc;
     MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
-    rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
-    if (rc) return rc;
+    if (v) {
+        rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+        if (rc) return rc;
+    } else {  // v = 1
+        k_r_ones<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, g->n, r);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_r_ones");
+        v = V_ONES;
+    }
     MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     mcf_walk_params pp = *p;
     pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks

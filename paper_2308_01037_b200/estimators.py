@@ -97,11 +97,14 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
 
     r = A v; q_c = sum over the N_c walks from column c of
     sum_k zeta_{k+2} W_k r[l_k] with W_0 = 1/N_c; y = zeta_0 v + zeta_1 r + A q.
+    ``v=None`` means v = 1 (total communicability, Katz): r is then the row
+    sums of A, bit-identical to A @ ones, without a SpMV.
     """
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
     n, nnz = _n_nnz(a)
-    v_np = None if isinstance(v, torch.Tensor) else np.asarray(v, dtype=np.float64)
+    ones = v is None
+    v_np = np.ones(n) if ones else (None if isinstance(v, torch.Tensor) else np.asarray(v, dtype=np.float64))
     if (v.shape if isinstance(v, torch.Tensor) else v_np.shape) != (n,):
         raise ArgumentError(f"v must have length {n}")
     z = coeffs.prefix(cfg.max_steps + 2)
@@ -118,7 +121,8 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
     if replay is None and budgets is None:
         # budgets, r = A v, walks, q, y = z0 v + z1 r + A q in one library call
         r = torch.empty_like(q)
-        y, ni, pre = g.funm_action(params, cfg.n_walks, vd, z[0], z[1], r, q, torch.empty_like(q), qvar, st)
+        y, ni, pre = g.funm_action(params, cfg.n_walks, None if ones else vd, z[0], z[1], r, q, torch.empty_like(q),
+                                   qvar, st)
     elif replay is None:
         ni, pre = _budgets(g, cfg, replay, budgets)
         r = g.spmv(vd)

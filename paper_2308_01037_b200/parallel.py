@@ -58,9 +58,9 @@ def assemble(t: torch.Tensor, group=None) -> torch.Tensor:
     return t
 
 
-def sharded_action(g: DeviceGraph, coeffs, v: torch.Tensor, config, *, params=None, budgets=None, group=None):
+def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=None, group=None):
     """One RandFunmAction pass with this rank's share of the start columns.
-    Returns (y, stats) with y assembled on every rank."""
+    ``v=None`` is v = 1.  Returns (y, stats) with y assembled on every rank."""
     rank, size = world()
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
@@ -71,6 +71,8 @@ def sharded_action(g: DeviceGraph, coeffs, v: torch.Tensor, config, *, params=No
         q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
         r, y = torch.empty_like(q), torch.empty_like(q)
         return g.funm_action(params, cfg.n_walks, v, z[0], z[1], r, q, y, stats=st)[0], st
+    if v is None:
+        v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     cols = column_shards(pre, size)[rank]
     rows = row_shards(g.n, size)[rank]

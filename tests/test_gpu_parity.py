@@ -446,3 +446,20 @@ def test_spmv_short_rows_match_sequential_csr_bitwise(mc, uniform):
     assert np.array_equal(y, m @ x)
     y = g.spmv(t(x), alpha=0.75, v=t(v), beta=-1.25, r=t(r)).cpu().numpy()
     assert np.array_equal(y, 0.75 * v + -1.25 * r + m @ x)
+
+
+@pytest.mark.parametrize("name", ["ba400", "signed6"])
+def test_action_v_ones_row_sums(mc, name):
+    """v = None (v = 1): r is the reference's A @ ones bit for bit (row sums,
+    signed rows summed with their signs), and the estimate equals the one with
+    an explicit ones vector (same walks; y to rounding of the hub-row sums)."""
+    import torch
+    c = golden_io.load(name)
+    g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
+    cfg = mc.WalkConfig(20 * c.n, 1e-6, 28, 3)
+    a1 = mc.rand_funm_action(g, mc.EXPONENTIAL, None, cfg)
+    a2 = mc.rand_funm_action(g, mc.EXPONENTIAL, torch.ones(c.n, dtype=torch.float64, device="cuda"), cfg)
+    m = sparse.csr_array((c.sa.vals, c.sa.col_ids, c.sa.row_ptr), shape=(c.n, c.n))
+    assert np.array_equal(a1.aux["r"].cpu().numpy(), m @ np.ones(c.n))
+    np.testing.assert_allclose(a1.values, a2.values, rtol=1e-13, atol=0)
+    assert a1.emissions == a2.emissions
