@@ -5,6 +5,9 @@
 //   -remainder), p_i = 0 never selected ahead of p_i > 0.
 // The R-th largest remainder is found by an 8-pass MSB-first radix select on
 // the remainder's IEEE bits (non-negative doubles order like their bits).
+#include <cstdlib>
+#include <cstring>
+
 #include "mcf_internal.cuh"
 
 namespace mcf {
@@ -460,6 +463,265 @@ __global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const double *__restri
     }
 }
 
+// ---------------------------------------------------------------------------
+// The whole allocation in ONE persistent kernel (n <= sm_count * 1024 * 8):
+// one CTA per SM, every lane keeps its p values in registers (warp-striped,
+// coalesced), and the passes above become phases separated by grid barriers:
+//   phase 1  floor sums + remainder-value histogram (1024 buckets, min/max)
+//   phase 2  refinement levels: every CTA reads the merged histogram, finds
+//            the bin holding the R-th largest key (redundantly, identically),
+//            and, unless that bin holds one distinct key, histograms the bin's
+//            key range 1024-way again (<= 7 levels for 64-bit keys)
+//   phase 3  the (N_i + [key > T], [key == T]) scan: warp and CTA totals,
+//            CTA prefixes after one more barrier, then N_i, walk_pre and the
+//            walk-block map.
+// p is read once; no other kernel runs.  The grid never exceeds one CTA per
+// SM, so every CTA is resident and the spin barriers cannot deadlock.
+// ---------------------------------------------------------------------------
+constexpr int AF_T = 1024, AF_W = AF_T / 32, AF_KMAX = 8, AF_LEVELS = 8, AF_MAXG = 1024;
+
+struct AllocFused {  // zero-initialised per call
+    unsigned bar;
+    unsigned pad_;
+    unsigned long long total_floor, n_pos;
+    unsigned cnt[AF_LEVELS][NBUCKET];
+    unsigned long long nmin[AF_LEVELS][NBUCKET], max[AF_LEVELS][NBUCKET];  // ~min, max key per bin
+    long long blk_a[AF_MAXG], blk_b[AF_MAXG];
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= target) break;
+            __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// 1024 bins, one per thread, searched from the top: the bin with
+// count(above) < R <= count(above) + count(bin).  Every thread gets the answer.
+__device__ __forceinline__ void find_bin_all(const unsigned *cnt, long long R, int &bin, long long &need) {
+    __shared__ long long wt[AF_W];
+    __shared__ int s_bin;
+    __shared__ long long s_need;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int b = NBUCKET - 1 - t;
+    const long long c = (long long)__ldcg(cnt + b);
+    const long long inc = warp_incl_scan(c);
+    if (lane == 31) wt[w] = inc;
+    if (t == 0) s_bin = -1;
+    __syncthreads();
+    long long above = inc - c;
+    for (int j = 0; j < w; ++j) above += wt[j];
+    if (above < R && R <= above + c) {
+        s_bin = b;
+        s_need = R - above;
+    }
+    __syncthreads();
+    bin = s_bin;
+    need = s_need;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restrict__ p, long long n, double total,
+                                                        long long n_walks, int K, AllocFused *F,
+                                                        long long *__restrict__ ni, long long *__restrict__ walk_pre,
+                                                        int *__restrict__ blk_col) {
+    __shared__ unsigned h[NBUCKET];
+    __shared__ unsigned long long smn[NBUCKET], smx[NBUCKET];
+    __shared__ long long s_wa[AF_W], s_wb[AF_W], s_pa, s_pb;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned G = gridDim.x;
+    const long long base = ((long long)blockIdx.x * AF_W + w) * 32 * K + lane;
+    double pv[AF_KMAX];
+#pragma unroll
+    for (int k = 0; k < AF_KMAX; ++k) {
+        const long long j = base + 32ll * k;
+        pv[k] = (k < K && j < n) ? p[j] : -1.0;  // -1: padding
+    }
+    // ---- phase 1: floor sums, remainder buckets ------------------------------
+    for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
+        h[b] = 0;
+        smn[b] = ~0ull;
+        smx[b] = 0;
+    }
+    __syncthreads();
+    long long fsum = 0, pos = 0;
+#pragma unroll
+    for (int k = 0; k < AF_KMAX; ++k) {
+        if (k >= K) break;
+        long long got = 0;
+        unsigned long long key = 0;
+        if (pv[k] >= 0.0) floor_key(pv[k], total, got, key);
+        fsum += got;
+        if (key) {
+            ++pos;
+            const int bk = rem_bucket(key);
+            atomicAdd(&h[bk], 1u);
+            atomicMin(&smn[bk], key);
+            atomicMax(&smx[bk], key);
+        }
+    }
+    fsum = warp_sum_ll(fsum);
+    pos = warp_sum_ll(pos);
+    if (lane == 0) {
+        if (fsum) atomicAdd(&F->total_floor, (unsigned long long)fsum);
+        if (pos) atomicAdd(&F->n_pos, (unsigned long long)pos);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
+        if (h[b]) {
+            atomicAdd(&F->cnt[0][b], h[b]);
+            atomicMax(&F->nmin[0][b], ~smn[b]);
+            atomicMax(&F->max[0][b], smx[b]);
+        }
+    }
+    unsigned phase = 1;
+    grid_barrier(&F->bar, G * phase++);
+    // ---- phase 2: the threshold key T and the ties to take I -----------------
+    const long long R = n_walks - (long long)__ldcg(&F->total_floor);
+    const long long npos = (long long)__ldcg(&F->n_pos);
+    unsigned long long T = ~0ull;  // R == 0: nothing selected
+    long long I = 0;
+    if (R > npos) {  // every positive key, then the lowest-index p == 0 entries
+        T = 0;
+        I = R - npos;
+    } else if (R > 0) {
+        int bin;
+        long long need;
+        find_bin_all(F->cnt[0], R, bin, need);
+        unsigned long long lo = ~__ldcg(&F->nmin[0][bin]), hi = __ldcg(&F->max[0][bin]);
+        for (int lvl = 1; lo != hi && lvl < AF_LEVELS; ++lvl) {
+            const unsigned long long width = (hi - lo) / NBUCKET + 1;
+            for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
+                h[b] = 0;
+                smn[b] = ~0ull;
+                smx[b] = 0;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < AF_KMAX; ++k) {
+                if (k >= K) break;
+                if (pv[k] <= 0.0) continue;
+                long long got;
+                unsigned long long key;
+                floor_key(pv[k], total, got, key);
+                if (key < lo || key > hi) continue;
+                const int bk = (int)((key - lo) / width);
+                atomicAdd(&h[bk], 1u);
+                atomicMin(&smn[bk], key);
+                atomicMax(&smx[bk], key);
+            }
+            __syncthreads();
+            for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
+                if (h[b]) {
+                    atomicAdd(&F->cnt[lvl][b], h[b]);
+                    atomicMax(&F->nmin[lvl][b], ~smn[b]);
+                    atomicMax(&F->max[lvl][b], smx[b]);
+                }
+            }
+            grid_barrier(&F->bar, G * phase++);
+            find_bin_all(F->cnt[lvl], need, bin, need);
+            lo = ~__ldcg(&F->nmin[lvl][bin]);
+            hi = __ldcg(&F->max[lvl][bin]);
+        }
+        T = lo;  // a single distinct key remains (64-bit keys need <= 7 levels)
+        I = need;
+    }
+    // ---- phase 3: N_i and walk_pre -----------------------------------------
+    long long ta = 0, tb = 0;
+#pragma unroll
+    for (int k = 0; k < AF_KMAX; ++k) {
+        if (k >= K) break;
+        if (pv[k] < 0.0) continue;
+        long long got;
+        unsigned long long key;
+        floor_key(pv[k], total, got, key);
+        ta += got + (key > T ? 1 : 0);
+        tb += key == T ? 1 : 0;
+    }
+    ta = warp_sum_ll(ta);
+    tb = warp_sum_ll(tb);
+    if (lane == 0) {
+        s_wa[w] = ta;
+        s_wb[w] = tb;
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive warp offsets inside the CTA, CTA totals to global
+        const long long va = lane < AF_W ? s_wa[lane] : 0, vb = lane < AF_W ? s_wb[lane] : 0;
+        const long long ia = warp_incl_scan(va), ib = warp_incl_scan(vb);
+        if (lane < AF_W) {
+            s_wa[lane] = ia - va;
+            s_wb[lane] = ib - vb;
+        }
+        if (lane == 31) {
+            F->blk_a[blockIdx.x] = ia;
+            F->blk_b[blockIdx.x] = ib;
+        }
+    }
+    grid_barrier(&F->bar, G * phase++);
+    {  // CTA prefix: sum of the totals of the CTAs before this one
+        long long a = 0, b = 0;
+        for (int j = threadIdx.x; j < (int)blockIdx.x; j += AF_T) {
+            a += __ldcg(&F->blk_a[j]);
+            b += __ldcg(&F->blk_b[j]);
+        }
+        a = warp_sum_ll(a);
+        b = warp_sum_ll(b);
+        __shared__ long long s_ra[AF_W], s_rb[AF_W];
+        if (lane == 0) {
+            s_ra[w] = a;
+            s_rb[w] = b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long sa = 0, sb = 0;
+            for (int j = 0; j < AF_W; ++j) {
+                sa += s_ra[j];
+                sb += s_rb[j];
+            }
+            s_pa = sa;
+            s_pb = sb;
+        }
+        __syncthreads();
+    }
+    long long ra = s_pa + s_wa[w], rb = s_pb + s_wb[w];
+    constexpr long long B = 1ll << WALK_BLK_SHIFT;
+#pragma unroll
+    for (int k = 0; k < AF_KMAX; ++k) {
+        if (k >= K) break;
+        const long long j = base + 32ll * k;
+        long long a = 0, t = 0;
+        if (pv[k] >= 0.0) {
+            long long got;
+            unsigned long long key;
+            floor_key(pv[k], total, got, key);
+            a = got + (key > T ? 1 : 0);
+            t = key == T ? 1 : 0;
+        }
+        const long long xa = warp_incl_scan(a), xb = warp_incl_scan(t);
+        const long long ea = ra + xa - a, eb = rb + xb - t;
+        if (j < n) {
+            const long long nj = a + ((t && eb < I) ? 1 : 0);
+            const long long w0 = ea + (eb < I ? eb : I);
+            ni[j] = nj;
+            walk_pre[j] = w0;
+            if (blk_col)
+                for (long long blk = (w0 + B - 1) >> WALK_BLK_SHIFT; blk * B < w0 + nj; ++blk) blk_col[blk] = (int)j;
+            if (j == n - 1) walk_pre[n] = ea + a + (eb + t < I ? eb + t : I);
+        }
+        ra += __shfl_sync(MCF_FULL, xa, 31);
+        rb += __shfl_sync(MCF_FULL, xb, 31);
+    }
+}
+
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
                     cudaStream_t s) {
     MCF_ARG(g && ni && walk_pre, "mcf_allocate_walks: null argument");
@@ -468,6 +730,19 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     const long long n = g->n;
     if (n == 0) {
         MCF_CUDA(cudaMemsetAsync(walk_pre, 0, sizeof(long long), s));
+        return MCF_OK;
+    }
+    const char *path = getenv("MCF_ALLOC_PATH");
+    const int G = sm_count() < AF_MAXG ? sm_count() : AF_MAXG;
+    const long long K = (n + (long long)G * AF_T - 1) / ((long long)G * AF_T);
+    if (K <= AF_KMAX && !(path && !strcmp(path, "passes"))) {  // one persistent kernel
+        AllocFused *F = nullptr;
+        MCF_CUDA(cudaMallocAsync(&F, sizeof(AllocFused), s));
+        MCF_CUDA(cudaMemsetAsync(F, 0, sizeof(AllocFused), s));
+        k_alloc_fused<<<G, AF_T, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, (int)K, F, ni, walk_pre, blk_col);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_alloc_fused");
+        MCF_CUDA(cudaFreeAsync(F, s));
         return MCF_OK;
     }
     // one zero-initialised block: selection state + the budget scan's look-back words

@@ -65,14 +65,42 @@ def test_device_tables_bitwise(mc, name):
     assert g.info["max_row_abs_sum"] ** 2 == float(c["alpha"])
 
 
+@pytest.fixture(params=["fused", "passes"])
+def alloc_path(request):
+    """Both budget implementations: the persistent one-kernel path (n up to
+    sm_count * 8192) and the multi-pass path used beyond that."""
+    import os
+    old = os.environ.get("MCF_ALLOC_PATH")
+    os.environ["MCF_ALLOC_PATH"] = request.param
+    yield request.param
+    if old is None:
+        os.environ.pop("MCF_ALLOC_PATH", None)
+    else:
+        os.environ["MCF_ALLOC_PATH"] = old
+
+
 @pytest.mark.parametrize("name", golden_io.CASES)
-def test_device_allocation_bitwise(mc, name):
+def test_device_allocation_bitwise(mc, alloc_path, name):
     c = golden_io.load(name)
     g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
     for ns in (1, 7, 1000, 12345, 10 * c.n + 3):
         ni, pre = g.allocate(ns)
         assert np.array_equal(ni.cpu().numpy(), c[f"ni_{ns}"]), ns
         assert int(pre[-1]) == ns
+        assert np.array_equal(pre.cpu().numpy(), np.concatenate([[0], np.cumsum(c[f"ni_{ns}"])]))
+
+
+def test_allocation_large_both_paths(mc, alloc_path):
+    """BA n = 1e6 (config 2): budgets equal the reference rule on the device
+    p for tie-heavy and tie-free budgets, and walk_pre is their prefix sum."""
+    from paper_2308_01037_b200 import graphs
+    g = mc.DeviceGraph(graphs.barabasi_albert(1_000_000, 4, seed=0))
+    p = g.tables()["init_prob"].cpu().numpy()
+    for ns in (640_000, 1, 999_999, 1_000_003, 12_345_679, 3 * 10**7 + 11):
+        ni, pre = g.allocate(ns)
+        ref = port.largest_remainder(p, ns)
+        assert np.array_equal(ni.cpu().numpy(), ref), ns
+        assert np.array_equal(pre.cpu().numpy(), np.concatenate([[0], np.cumsum(ref)])), ns
 
 
 @pytest.mark.parametrize("name", golden_io.CASES)
