@@ -5,6 +5,7 @@
 //   -remainder), p_i = 0 never selected ahead of p_i > 0.
 // The R-th largest remainder is found by an 8-pass MSB-first radix select on
 // the remainder's IEEE bits (non-negative doubles order like their bits).
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const double *__restri
 // The whole allocation in ONE persistent kernel (n <= sm_count * 1024 * 8):
 // one CTA per SM, every lane keeps its p values in registers (warp-striped,
 // coalesced), and the passes above become phases separated by grid barriers:
-//   phase 1  floor sums + remainder-value histogram (1024 buckets, min/max)
+//   phase 1  floor sums + remainder-value histogram (1024 buckets)
 //   phase 2  refinement levels: every CTA reads the merged histogram, finds
 //            the bin holding the R-th largest key (redundantly, identically),
 //            and, unless that bin holds one distinct key, histograms the bin's
@@ -479,41 +480,72 @@ __global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const double *__restri
 // SM, so every CTA is resident and the spin barriers cannot deadlock.
 // ---------------------------------------------------------------------------
 constexpr int AF_T = 1024, AF_W = AF_T / 32, AF_KMAX = 8, AF_LEVELS = 8, AF_MAXG = 1024;
+constexpr int AF_REP = 8;  // replicas of the merged histograms: CTA c adds into copy c % 8 (8x less contention)
 
-struct AllocFused {  // zero-initialised per call
+struct AllocFused {
+    // ---- zeroed by the host (cudaMemsetAsync up to `lvl`)
     unsigned bar;
-    unsigned pad_;
-    unsigned long long total_floor, n_pos;
-    unsigned cnt[AF_LEVELS][NBUCKET];
-    unsigned long long nmin[AF_LEVELS][NBUCKET], max[AF_LEVELS][NBUCKET];  // ~min, max key per bin
-    long long blk_a[AF_MAXG], blk_b[AF_MAXG];
+    unsigned pad_[31];
+    unsigned flag;  // own 128-B line
+    unsigned pad2_[31];
+    unsigned cnt0[AF_REP][NBUCKET];  // level 0: remainder-value buckets
+    unsigned long long trace[32];    // MCF_ALLOC_TRACE builds: CTA 0 phase timestamps
+    // ---- refinement levels, zeroed by the CTAs during phase 1 (first used after barrier 1)
+    struct Level {
+        unsigned cnt[AF_REP][NBUCKET];
+        unsigned long long nmin[AF_REP][NBUCKET], max[AF_REP][NBUCKET];  // ~min, max key per bin
+    } lvl[AF_LEVELS];
+    long long blk_a[AF_MAXG], blk_b[AF_MAXG];  // written before they are read
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned target) {
-    __syncthreads();
+#ifdef MCF_ALLOC_TRACE
+#define AF_TRACE(F, i)                                                              \
+    do {                                                                            \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                  \
+            unsigned long long t_;                                                  \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+            (F)->trace[i] = t_;                                                     \
+        }                                                                           \
+    } while (0)
+#else
+#define AF_TRACE(F, i) \
+    do {               \
+    } while (0)
+#endif
+
+// Grid barrier: arrivals count on one word, the last arriver publishes the
+// phase on a flag in another line, and the other CTAs poll only that flag
+// (with back-off) -- polling the counter itself slows the arrivals down.
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned *flag, unsigned phase, unsigned G) {
+    __syncthreads();  // the CTA's writes happen-before thread 0's release below
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
-        while (true) {
-            unsigned v;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-            if (v >= target) break;
-            __nanosleep(20);
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == G * phase - 1) {
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(phase) : "memory");
+        } else {
+            while (true) {
+                unsigned v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                if (v >= phase) break;
+                __nanosleep(64);
+            }
         }
-        __threadfence();
     }
     __syncthreads();
 }
 
 // 1024 bins, one per thread, searched from the top: the bin with
 // count(above) < R <= count(above) + count(bin).  Every thread gets the answer.
-__device__ __forceinline__ void find_bin_all(const unsigned *cnt, long long R, int &bin, long long &need) {
+__device__ __forceinline__ void find_bin_all(const unsigned (*cnt)[NBUCKET], long long R, int &bin, long long &need) {
     __shared__ long long wt[AF_W];
     __shared__ int s_bin;
     __shared__ long long s_need;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int b = NBUCKET - 1 - t;
-    const long long c = (long long)__ldcg(cnt + b);
+    long long c = 0;
+#pragma unroll
+    for (int r = 0; r < AF_REP; ++r) c += (long long)__ldcg(cnt[r] + b);
     const long long inc = warp_incl_scan(c);
     if (lane == 31) wt[w] = inc;
     if (t == 0) s_bin = -1;
@@ -540,6 +572,14 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned G = gridDim.x;
     const long long base = ((long long)blockIdx.x * AF_W + w) * 32 * K + lane;
+    AF_TRACE(F, 0);
+#ifdef MCF_ALLOC_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        atomicMax(&F->trace[28], t_);  // last CTA to start
+    }
+#endif
     double pv[AF_KMAX];
 #pragma unroll
     for (int k = 0; k < AF_KMAX; ++k) {
@@ -547,11 +587,7 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
         pv[k] = (k < K && j < n) ? p[j] : -1.0;  // -1: padding
     }
     // ---- phase 1: floor sums, remainder buckets ------------------------------
-    for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
-        h[b] = 0;
-        smn[b] = ~0ull;
-        smx[b] = 0;
-    }
+    for (int b = threadIdx.x; b < NBUCKET; b += AF_T) h[b] = 0;
     __syncthreads();
     long long fsum = 0, pos = 0;
 #pragma unroll
@@ -563,31 +599,82 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
         fsum += got;
         if (key) {
             ++pos;
-            const int bk = rem_bucket(key);
-            atomicAdd(&h[bk], 1u);
-            atomicMin(&smn[bk], key);
-            atomicMax(&smx[bk], key);
+            atomicAdd(&h[rem_bucket(key)], 1u);
         }
     }
-    fsum = warp_sum_ll(fsum);
+    fsum = warp_sum_ll(fsum);  // CTA totals to per-CTA slots (no same-address atomics)
     pos = warp_sum_ll(pos);
     if (lane == 0) {
-        if (fsum) atomicAdd(&F->total_floor, (unsigned long long)fsum);
-        if (pos) atomicAdd(&F->n_pos, (unsigned long long)pos);
+        s_wa[w] = fsum;
+        s_wb[w] = pos;
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
-        if (h[b]) {
-            atomicAdd(&F->cnt[0][b], h[b]);
-            atomicMax(&F->nmin[0][b], ~smn[b]);
-            atomicMax(&F->max[0][b], smx[b]);
+    if (w == 0) {
+        const long long a = warp_sum_ll(lane < AF_W ? s_wa[lane] : 0), b = warp_sum_ll(lane < AF_W ? s_wb[lane] : 0);
+        if (lane == 0) {
+            F->blk_a[blockIdx.x] = a;
+            F->blk_b[blockIdx.x] = b;
         }
     }
+#ifdef MCF_ALLOC_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        atomicMax(&F->trace[29], t_);  // last CTA done with its shared histogram
+    }
+#endif
+#ifndef MCF_ALLOC_NOFLUSH
+    for (int b = threadIdx.x; b < NBUCKET; b += AF_T)
+        if (h[b]) atomicAdd(&F->cnt0[blockIdx.x % AF_REP][b], h[b]);
+    {  // zero the refinement levels (1.1 MB) while the other CTAs finish phase 1
+        uint4 *z = reinterpret_cast<uint4 *>(&F->lvl[0]);
+        const long long words = (long long)sizeof(F->lvl) / 16;
+        for (long long i = (long long)blockIdx.x * AF_T + threadIdx.x; i < words; i += (long long)G * AF_T)
+            z[i] = make_uint4(0, 0, 0, 0);
+    }
+#endif
+#ifdef MCF_ALLOC_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        atomicMax(&F->trace[30], t_);  // last CTA done flushing
+    }
+#endif
+    AF_TRACE(F, 1);
     unsigned phase = 1;
-    grid_barrier(&F->bar, G * phase++);
+    grid_barrier(&F->bar, &F->flag, phase, G);
+    ++phase;
+    AF_TRACE(F, 2);
     // ---- phase 2: the threshold key T and the ties to take I -----------------
-    const long long R = n_walks - (long long)__ldcg(&F->total_floor);
-    const long long npos = (long long)__ldcg(&F->n_pos);
+    {
+        long long a = 0, b = 0;
+        for (int j = threadIdx.x; j < (int)G; j += AF_T) {
+            a += __ldcg(&F->blk_a[j]);
+            b += __ldcg(&F->blk_b[j]);
+        }
+        a = warp_sum_ll(a);
+        b = warp_sum_ll(b);
+        if (lane == 0) {
+            s_wa[w] = a;
+            s_wb[w] = b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long sa = 0, sb = 0;
+            for (int j = 0; j < AF_W; ++j) {
+                sa += s_wa[j];
+                sb += s_wb[j];
+            }
+            s_pa = sa;
+            s_pb = sb;
+        }
+        __syncthreads();
+    }
+    const long long R = n_walks - s_pa;  // sum of floor(p N)
+    const long long npos = s_pb;        // entries with p > 0
+    __syncthreads();
     unsigned long long T = ~0ull;  // R == 0: nothing selected
     long long I = 0;
     if (R > npos) {  // every positive key, then the lowest-index p == 0 entries
@@ -596,8 +683,11 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
     } else if (R > 0) {
         int bin;
         long long need;
-        find_bin_all(F->cnt[0], R, bin, need);
-        unsigned long long lo = ~__ldcg(&F->nmin[0][bin]), hi = __ldcg(&F->max[0][bin]);
+        find_bin_all(F->cnt0, R, bin, need);
+        // bucket b holds the remainders in [b/1024, (b+1)/1024) (exact: the
+        // scaling by 1024 is a power of two), i.e. these keys:
+        unsigned long long lo = (unsigned long long)__double_as_longlong((double)bin / NBUCKET) + 1ull;
+        unsigned long long hi = (unsigned long long)__double_as_longlong((double)(bin + 1) / NBUCKET);
         for (int lvl = 1; lo != hi && lvl < AF_LEVELS; ++lvl) {
             const unsigned long long width = (hi - lo) / NBUCKET + 1;
             for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
@@ -609,32 +699,56 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
 #pragma unroll
             for (int k = 0; k < AF_KMAX; ++k) {
                 if (k >= K) break;
-                if (pv[k] <= 0.0) continue;
                 long long got;
-                unsigned long long key;
-                floor_key(pv[k], total, got, key);
-                if (key < lo || key > hi) continue;
-                const int bk = (int)((key - lo) / width);
-                atomicAdd(&h[bk], 1u);
-                atomicMin(&smn[bk], key);
-                atomicMax(&smx[bk], key);
+                unsigned long long key = 0;
+                if (pv[k] > 0.0) floor_key(pv[k], total, got, key);
+                const bool in = key && key >= lo && key <= hi;
+                const unsigned m = __ballot_sync(MCF_FULL, in);
+                if (!m) continue;
+                const int src = __ffs(m) - 1;
+                const unsigned long long k0 = __shfl_sync(MCF_FULL, key, src);
+                if (__all_sync(MCF_FULL, !in || key == k0)) {  // one tied key in the warp: one update
+                    if (lane == src) {
+                        const int bk = (int)((k0 - lo) / width);
+                        atomicAdd(&h[bk], (unsigned)__popc(m));
+                        atomicMin(&smn[bk], k0);
+                        atomicMax(&smx[bk], k0);
+                    }
+                } else if (in) {
+                    const int bk = (int)((key - lo) / width);
+                    atomicAdd(&h[bk], 1u);
+                    atomicMin(&smn[bk], key);
+                    atomicMax(&smx[bk], key);
+                }
             }
             __syncthreads();
             for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
                 if (h[b]) {
-                    atomicAdd(&F->cnt[lvl][b], h[b]);
-                    atomicMax(&F->nmin[lvl][b], ~smn[b]);
-                    atomicMax(&F->max[lvl][b], smx[b]);
+                    const int rep = blockIdx.x % AF_REP;
+                    atomicAdd(&F->lvl[lvl].cnt[rep][b], h[b]);
+                    atomicMax(&F->lvl[lvl].nmin[rep][b], ~smn[b]);
+                    atomicMax(&F->lvl[lvl].max[rep][b], smx[b]);
                 }
             }
-            grid_barrier(&F->bar, G * phase++);
-            find_bin_all(F->cnt[lvl], need, bin, need);
-            lo = ~__ldcg(&F->nmin[lvl][bin]);
-            hi = __ldcg(&F->max[lvl][bin]);
+            AF_TRACE(F, 2 + 2 * lvl - 1);
+            grid_barrier(&F->bar, &F->flag, phase, G);
+    ++phase;
+            AF_TRACE(F, 2 + 2 * lvl);
+            find_bin_all(F->lvl[lvl].cnt, need, bin, need);
+            unsigned long long nmn = 0, mx = 0;
+#pragma unroll
+            for (int r = 0; r < AF_REP; ++r) {
+                const unsigned long long a = __ldcg(&F->lvl[lvl].nmin[r][bin]), b = __ldcg(&F->lvl[lvl].max[r][bin]);
+                nmn = a > nmn ? a : nmn;
+                mx = b > mx ? b : mx;
+            }
+            lo = ~nmn;
+            hi = mx;
         }
         T = lo;  // a single distinct key remains (64-bit keys need <= 7 levels)
         I = need;
     }
+    AF_TRACE(F, 20);
     // ---- phase 3: N_i and walk_pre -----------------------------------------
     long long ta = 0, tb = 0;
 #pragma unroll
@@ -666,7 +780,10 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
             F->blk_b[blockIdx.x] = ib;
         }
     }
-    grid_barrier(&F->bar, G * phase++);
+    AF_TRACE(F, 21);
+    grid_barrier(&F->bar, &F->flag, phase, G);
+    ++phase;
+    AF_TRACE(F, 22);
     {  // CTA prefix: sum of the totals of the CTAs before this one
         long long a = 0, b = 0;
         for (int j = threadIdx.x; j < (int)blockIdx.x; j += AF_T) {
@@ -720,6 +837,7 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
         ra += __shfl_sync(MCF_FULL, xa, 31);
         rb += __shfl_sync(MCF_FULL, xb, 31);
     }
+    AF_TRACE(F, 23);
 }
 
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
@@ -738,7 +856,7 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     if (K <= AF_KMAX && !(path && !strcmp(path, "passes"))) {  // one persistent kernel
         AllocFused *F = nullptr;
         MCF_CUDA(cudaMallocAsync(&F, sizeof(AllocFused), s));
-        MCF_CUDA(cudaMemsetAsync(F, 0, sizeof(AllocFused), s));
+        MCF_CUDA(cudaMemsetAsync(F, 0, offsetof(AllocFused, lvl), s));
         k_alloc_fused<<<G, AF_T, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, (int)K, F, ni, walk_pre, blk_col);
         mcf::note_launch();
         MCF_LAUNCHED("k_alloc_fused");
