@@ -140,13 +140,20 @@ __global__ void __launch_bounds__(256, 4) k_alloc_floor(const double *__restrict
             }
         }
     }
-    got_sum = warp_sum_ll(got_sum);
+    got_sum = warp_sum_ll(got_sum);  // one global atomic per CTA, not per warp
     pos = warp_sum_ll(pos);
+    __shared__ unsigned long long cta_sum[2];
+    if (threadIdx.x < 2) cta_sum[threadIdx.x] = 0;
+    __syncthreads();
     if ((threadIdx.x & 31) == 0) {
-        if (got_sum) atomicAdd(&st->total_floor, (unsigned long long)got_sum);
-        if (pos) atomicAdd(&st->n_pos, (unsigned long long)pos);
+        if (got_sum) atomicAdd(&cta_sum[0], (unsigned long long)got_sum);
+        if (pos) atomicAdd(&cta_sum[1], (unsigned long long)pos);
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        if (cta_sum[0]) atomicAdd(&st->total_floor, cta_sum[0]);
+        if (cta_sum[1]) atomicAdd(&st->n_pos, cta_sum[1]);
+    }
     for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x)
         if (h[b]) atomicAdd(&st->hist[b], h[b]);
     __threadfence();

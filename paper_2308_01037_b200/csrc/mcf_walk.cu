@@ -84,19 +84,27 @@ __device__ __forceinline__ int cdf_pick(const double *__restrict__ cdf, int deg,
     return lo;
 }
 
+// Walk statistics: warp sums into shared counters, then one global atomic
+// per CTA and counter (per-warp atomics on the same 4 words contended at the
+// end of the kernel).  Called once by every thread of the CTA.
 __device__ __forceinline__ void flush_stats(long long *stats, unsigned walks_, unsigned em_, unsigned tr_,
                                             unsigned ab_) {
+    __shared__ unsigned long long cta[4];
+    if (threadIdx.x < 4) cta[threadIdx.x] = 0;
+    __syncthreads();
     long long walks = walks_, em = em_, tr = tr_, ab = ab_;
     walks = warp_sum_ll(walks);
     em = warp_sum_ll(em);
     tr = warp_sum_ll(tr);
     ab = warp_sum_ll(ab);
     if ((threadIdx.x & 31) == 0) {
-        if (walks) atomicAdd((unsigned long long *)&stats[0], (unsigned long long)walks);
-        if (em) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)em);
-        if (tr) atomicAdd((unsigned long long *)&stats[2], (unsigned long long)tr);
-        if (ab) atomicAdd((unsigned long long *)&stats[3], (unsigned long long)ab);
+        if (walks) atomicAdd(&cta[0], (unsigned long long)walks);
+        if (em) atomicAdd(&cta[1], (unsigned long long)em);
+        if (tr) atomicAdd(&cta[2], (unsigned long long)tr);
+        if (ab) atomicAdd(&cta[3], (unsigned long long)ab);
     }
+    __syncthreads();
+    if (threadIdx.x < 4 && cta[threadIdx.x]) atomicAdd((unsigned long long *)&stats[threadIdx.x], cta[threadIdx.x]);
 }
 
 // Walk state of one lane (one walk slot).
