@@ -28,24 +28,50 @@ struct BuildCounters {
 constexpr int LONG_COL = 256;   // columns longer than this get a warp in k_colnorm_long
 constexpr int LEAFCAP = 2048;   // leaves of the pairwise tree a warp keeps in smem
 
-__device__ __forceinline__ void add_row_stats(BuildCounters *cnt, unsigned long long uni, unsigned long long emp,
-                                              unsigned long long neg, unsigned long long maxdeg,
-                                              unsigned long long maxr, unsigned mask = MCF_FULL) {
+// Graph statistics: per-thread accumulators, reduced per warp, merged per CTA
+// in shared memory, then one global atomic per CTA and counter (per-warp
+// atomics on the same few words serialised the table build).
+struct RowStats {
+    unsigned long long uni = 0, emp = 0, neg = 0, maxdeg = 0, maxr = 0, minb = ~0ull, maxb = 0;
+};
+
+__device__ __forceinline__ void stats_init(unsigned long long *sh) {
+    if (threadIdx.x < 7) sh[threadIdx.x] = threadIdx.x == 5 ? ~0ull : 0ull;
+}
+
+// every thread of the CTA calls it once, after stats_init + a barrier
+__device__ __forceinline__ void stats_flush(RowStats r, unsigned long long *sh, BuildCounters *cnt) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        uni += __shfl_xor_sync(mask, uni, o);
-        emp += __shfl_xor_sync(mask, emp, o);
-        neg += __shfl_xor_sync(mask, neg, o);
-        unsigned long long a = __shfl_xor_sync(mask, maxdeg, o), b = __shfl_xor_sync(mask, maxr, o);
-        maxdeg = a > maxdeg ? a : maxdeg;
-        maxr = b > maxr ? b : maxr;
+        r.uni += __shfl_xor_sync(MCF_FULL, r.uni, o);
+        r.emp += __shfl_xor_sync(MCF_FULL, r.emp, o);
+        r.neg += __shfl_xor_sync(MCF_FULL, r.neg, o);
+        unsigned long long a = __shfl_xor_sync(MCF_FULL, r.maxdeg, o), b = __shfl_xor_sync(MCF_FULL, r.maxr, o);
+        r.maxdeg = a > r.maxdeg ? a : r.maxdeg;
+        r.maxr = b > r.maxr ? b : r.maxr;
+        a = __shfl_xor_sync(MCF_FULL, r.minb, o);
+        b = __shfl_xor_sync(MCF_FULL, r.maxb, o);
+        r.minb = a < r.minb ? a : r.minb;
+        r.maxb = b > r.maxb ? b : r.maxb;
     }
     if ((threadIdx.x & 31) == 0) {
-        if (uni) atomicAdd(&cnt->n_uniform, uni);
-        if (emp) atomicAdd(&cnt->n_empty, emp);
-        if (neg) atomicAdd(&cnt->n_negative, neg);
-        atomicMax(&cnt->max_degree, maxdeg);
-        atomicMax(&cnt->max_rsum_bits, maxr);
+        if (r.uni) atomicAdd(&sh[0], r.uni);
+        if (r.emp) atomicAdd(&sh[1], r.emp);
+        if (r.neg) atomicAdd(&sh[2], r.neg);
+        atomicMax(&sh[3], r.maxdeg);
+        atomicMax(&sh[4], r.maxr);
+        atomicMin(&sh[5], r.minb);
+        atomicMax(&sh[6], r.maxb);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (sh[0]) atomicAdd(&cnt->n_uniform, sh[0]);
+        if (sh[1]) atomicAdd(&cnt->n_empty, sh[1]);
+        if (sh[2]) atomicAdd(&cnt->n_negative, sh[2]);
+        if (sh[3]) atomicMax(&cnt->max_degree, sh[3]);
+        if (sh[4]) atomicMax(&cnt->max_rsum_bits, sh[4]);
+        if (sh[5] != ~0ull) atomicMin(&cnt->min_abs_bits, sh[5]);
+        if (sh[6]) atomicMax(&cnt->max_abs_bits, sh[6]);
     }
 }
 
@@ -73,52 +99,48 @@ __global__ void k_mark_long(const long long *__restrict__ ptr, long long n, long
 // (walker.py:124-125) match bit for bit.  Loads are batched 8 at a time.
 __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__restrict__ vals, long long n,
                        NodeHdr *__restrict__ hdr, BuildCounters *__restrict__ cnt) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long uni = 0, emp = 0, neg = 0, maxdeg = 0, maxr = 0, minb = ~0ull, maxb = 0;
-    if (i < n) {
+    __shared__ unsigned long long sh[7];
+    stats_init(sh);
+    __syncthreads();
+    RowStats st;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long s = row_ptr[i], e = row_ptr[i + 1];
-        if (e - s <= LONG_ROW) {
-            double acc = 0.0, mn = INFINITY, mx = 0.0;
-            bool uniform = true;
-            const double first = (e > s) ? fabs(vals[s]) : 0.0;
-            for (long long j = s; j < e; j += 8) {
-                double v[8];
+        if (e - s > LONG_ROW) continue;
+        double acc = 0.0, mn = INFINITY, mx = 0.0;
+        bool uniform = true;
+        unsigned long long neg = 0;
+        const double first = (e > s) ? fabs(vals[s]) : 0.0;
+        for (long long j = s; j < e; j += 8) {
+            double v[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) v[t] = (j + t < e) ? vals[j + t] : 0.0;
+            for (int t = 0; t < 8; ++t) v[t] = (j + t < e) ? vals[j + t] : 0.0;
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    if (j + t < e) {
-                        const double a = fabs(v[t]);
-                        acc = __dadd_rn(acc, a);
-                        uniform &= (a == first);
-                        neg += (v[t] < 0.0);
-                        mn = fmin(mn, a);
-                        mx = fmax(mx, a);
-                    }
+            for (int t = 0; t < 8; ++t) {
+                if (j + t < e) {
+                    const double a = fabs(v[t]);
+                    acc = __dadd_rn(acc, a);
+                    uniform &= (a == first);
+                    neg += (v[t] < 0.0);
+                    mn = fmin(mn, a);
+                    mx = fmax(mx, a);
                 }
             }
-            hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
-            if (e > s) {
-                minb = (unsigned long long)__double_as_longlong(mn);
-                maxb = (unsigned long long)__double_as_longlong(mx);
-            }
-            uni = (uniform && e > s);
-            emp = (e == s);
-            maxdeg = (unsigned long long)(e - s);
-            maxr = (unsigned long long)__double_as_longlong(acc);
         }
+        hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+        if (e > s) {
+            const unsigned long long lo = (unsigned long long)__double_as_longlong(mn);
+            const unsigned long long hi = (unsigned long long)__double_as_longlong(mx);
+            st.minb = lo < st.minb ? lo : st.minb;
+            st.maxb = hi > st.maxb ? hi : st.maxb;
+        }
+        st.uni += (uniform && e > s);
+        st.emp += (e == s);
+        st.neg += neg;
+        st.maxdeg = (unsigned long long)(e - s) > st.maxdeg ? (unsigned long long)(e - s) : st.maxdeg;
+        const unsigned long long rb = (unsigned long long)__double_as_longlong(acc);
+        st.maxr = rb > st.maxr ? rb : st.maxr;
     }
-    add_row_stats(cnt, uni, emp, neg, maxdeg, maxr);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long a = __shfl_xor_sync(MCF_FULL, minb, o), b = __shfl_xor_sync(MCF_FULL, maxb, o);
-        minb = a < minb ? a : minb;
-        maxb = b > maxb ? b : maxb;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (minb != ~0ull) atomicMin(&cnt->min_abs_bits, minb);
-        if (maxb) atomicMax(&cnt->max_abs_bits, maxb);
-    }
+    stats_flush(st, sh, cnt);
 }
 
 // One warp per long row: 32 coalesced loads, then the sequential sum in CSR
@@ -126,7 +148,13 @@ __global__ void k_rows(const long long *__restrict__ row_ptr, const double *__re
 __global__ void k_rows_long(const int *__restrict__ rows, const unsigned long long *count,
                             const long long *__restrict__ row_ptr, const double *__restrict__ vals,
                             NodeHdr *__restrict__ hdr, BuildCounters *__restrict__ cnt) {
-    const int lane = threadIdx.x & 31;
+    __shared__ unsigned long long sh[7];
+    __shared__ __align__(16) double stage[8][256];  // per warp: 256 values in CSR order
+    stats_init(sh);
+    __syncthreads();
+    RowStats st;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *buf = stage[w];
     const long long nl = (long long)*count;
     const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long li = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += warps) {
@@ -136,36 +164,54 @@ __global__ void k_rows_long(const int *__restrict__ rows, const unsigned long lo
         double acc = 0.0, mn = INFINITY, mx = 0.0;
         bool uniform = true;
         unsigned long long neg = 0;
-        for (long long j = s; j < e; j += 32) {
-            const long long jj = j + lane;
-            const double v = jj < e ? vals[jj] : 0.0;
-            const double a = fabs(v);
-            uniform &= __all_sync(MCF_FULL, jj >= e || a == first);
-            if (jj < e) {
-                mn = fmin(mn, a);
-                mx = fmax(mx, a);
+        for (long long j = s; j < e; j += 256) {
+            const int m = (int)(e - j < 256 ? e - j : 256);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {  // coalesced: 8 loads in flight per lane
+                const int o = t * 32 + lane;
+                const double v = o < m ? vals[j + o] : 0.0;
+                const double a = fabs(v);
+                uniform &= (o >= m || a == first);
+                if (o < m) {
+                    mn = fmin(mn, a);
+                    mx = fmax(mx, a);
+                    neg += (v < 0.0);
+                }
+                buf[o] = a;
             }
-            neg += __popc(__ballot_sync(MCF_FULL, jj < e && v < 0.0));
-            const int m = (int)(e - j < 32 ? e - j : 32);
-            for (int t = 0; t < m; ++t) acc = __dadd_rn(acc, __shfl_sync(MCF_FULL, a, t));
+            __syncwarp();
+            if (lane == 0) {  // the sequential CSR-order sum, from shared memory
+                const double2 *b2 = reinterpret_cast<const double2 *>(buf);
+                int t = 0;
+                for (; t + 2 <= m; t += 2) {
+                    const double2 x = b2[t >> 1];
+                    acc = __dadd_rn(__dadd_rn(acc, x.x), x.y);
+                }
+                if (t < m) acc = __dadd_rn(acc, buf[t]);
+            }
+            __syncwarp();
         }
-        if (lane == 0) hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+        uniform = __all_sync(MCF_FULL, uniform);
+        neg = warp_sum_ll((long long)neg);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(MCF_FULL, mn, o));
             mx = fmax(mx, __shfl_xor_sync(MCF_FULL, mx, o));
         }
         if (lane == 0) {
-            atomicMin(&cnt->min_abs_bits, (unsigned long long)__double_as_longlong(mn));
-            atomicMax(&cnt->max_abs_bits, (unsigned long long)__double_as_longlong(mx));
-        }
-        if (lane == 0) {
-            if (uniform) atomicAdd(&cnt->n_uniform, 1ull);
-            if (neg) atomicAdd(&cnt->n_negative, neg);
-            atomicMax(&cnt->max_degree, (unsigned long long)(e - s));
-            atomicMax(&cnt->max_rsum_bits, (unsigned long long)__double_as_longlong(acc));
+            hdr[i] = make_hdr(s, e, acc, uniform, neg != 0);
+            const unsigned long long lo = (unsigned long long)__double_as_longlong(mn);
+            const unsigned long long hi = (unsigned long long)__double_as_longlong(mx);
+            st.minb = lo < st.minb ? lo : st.minb;
+            st.maxb = hi > st.maxb ? hi : st.maxb;
+            st.uni += uniform ? 1 : 0;
+            st.neg += neg;
+            st.maxdeg = (unsigned long long)(e - s) > st.maxdeg ? (unsigned long long)(e - s) : st.maxdeg;
+            const unsigned long long rb = (unsigned long long)__double_as_longlong(acc);
+            st.maxr = rb > st.maxr ? rb : st.maxr;
         }
     }
+    stats_flush(st, sh, cnt);
 }
 
 // Fat walk entries: went[e] = hdr[col[e]], pad = col[e], sign of a_e in flags.
@@ -473,7 +519,7 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     mcf::note_launch();
     k_mark_long<<<nb, 256, 0, s>>>(cp, n, LONG_COL, long_cols, &cnt->n_long_cols);
     mcf::note_launch();
-    k_rows<<<nb, 256, 0, s>>>(rp, g->vals, n, g->hdr, cnt);
+    k_rows<<<(unsigned)(nb < (unsigned)wgrid ? nb : (unsigned)wgrid), 256, 0, s>>>(rp, g->vals, n, g->hdr, cnt);
     mcf::note_launch();
     k_rows_long<<<wgrid, 256, 0, s>>>(g->long_rows, lr_count, rp, g->vals, g->hdr, cnt);
     mcf::note_launch();
