@@ -348,36 +348,74 @@ __global__ void k_colnorm(const long long *__restrict__ csc_ptr, const double *_
     double sq = 0.0;
     if (e > s) {
         sq = __dmul_rn(csc_vals[s], csc_vals[s]);
-        if (e - s > 1) sq = __dadd_rn(sq, pw_sum<true>(csc_vals + s + 1, e - s - 1));
+        const long long m = e - s - 1;
+        const double *a = csc_vals + s + 1;
+        if (m > 128) {  // pairwise_sum for m < LONG_COL = 256: left <= 127, right <= 135 (maybe split once more)
+            long long n2 = m / 2;
+            n2 -= n2 % 8;
+            const long long r = m - n2;
+            double right;
+            if (r <= 128) {
+                right = pw_block<true>(a + n2, r);
+            } else {
+                long long n3 = r / 2;
+                n3 -= n3 % 8;
+                right = __dadd_rn(pw_block<true>(a + n2, n3), pw_block<true>(a + n2 + n3, r - n3));
+            }
+            sq = __dadd_rn(sq, __dadd_rn(pw_block<true>(a, n2), right));
+        } else if (m > 0) {
+            sq = __dadd_rn(sq, pw_block<true>(a, m));
+        }
     }
     col_norm[j] = __dsqrt_rn(sq);
 }
 
-// One warp per long column: lanes evaluate the leaves of the pairwise tree
-// (round robin), lane 0 combines them in the recursion order -> same bits.
-__global__ void __launch_bounds__(64) k_colnorm_long(const int *__restrict__ cols, const unsigned long long *count,
-                                                      const long long *__restrict__ csc_ptr,
-                                                      const double *__restrict__ csc_vals, double *__restrict__ col_norm) {
-    __shared__ double leafbuf[2][LEAFCAP];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double *buf = leafbuf[w];
+// One warp (one CTA) per long column.  Lane 0 enumerates the leaves of the
+// pairwise tree once (offsets into shared memory); rounds of 32 consecutive
+// leaves -- one contiguous value range -- are staged into shared memory with
+// coalesced loads and summed one leaf per lane; lane 0 combines the leaf sums
+// in the recursion order -> the same bits as the sequential evaluation.
+constexpr int LEAFCAP_L = 1024;  // leaves held per column (columns up to ~131k entries; beyond: lane 0 alone)
+
+__global__ void __launch_bounds__(32) k_colnorm_long(const int *__restrict__ cols, const unsigned long long *count,
+                                                     const long long *__restrict__ csc_ptr,
+                                                     const double *__restrict__ csc_vals, double *__restrict__ col_norm) {
+    __shared__ __align__(16) double stage[32 * 128];
+    __shared__ double buf[LEAFCAP_L];
+    __shared__ int lofs[LEAFCAP_L + 1];
+    const int lane = threadIdx.x;
     const long long nl = (long long)*count;
-    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long li = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nl; li += warps) {
+    for (long long li = blockIdx.x; li < nl; li += gridDim.x) {
         const int j = cols[li];
         const long long s = csc_ptr[j], e = csc_ptr[j + 1];
         const double *a = csc_vals + s + 1;
         const long long m = e - s - 1;
-        const long long nleaf = pw_leaf_count(m);
-        double tail = 0.0;
-        if (nleaf > LEAFCAP) {
-            if (lane == 0) tail = pw_sum<true>(a, m);
-        } else {
-            pw_eval(m, [&](int k, long long off, long long len) {
-                if ((k & 31) == lane) buf[k] = pw_block<true>(a + off, len);
+        int nleaf = 0;
+        if (lane == 0) {
+            pw_eval(m, [&](int k, long long off, long long) {
+                if (k < LEAFCAP_L) lofs[k] = (int)off;
+                nleaf = k + 1;
                 return 0.0;
             });
-            __syncwarp();
+            if (nleaf <= LEAFCAP_L) lofs[nleaf] = (int)m;
+        }
+        nleaf = __shfl_sync(MCF_FULL, nleaf, 0);
+        __syncwarp();
+        double tail = 0.0;
+        if (nleaf > LEAFCAP_L) {
+            if (lane == 0) tail = pw_sum<true>(a, m);
+        } else {
+            for (int r0 = 0; r0 < nleaf; r0 += 32) {
+                const int r1 = r0 + 32 < nleaf ? r0 + 32 : nleaf;
+                const int lo = lofs[r0], hi = lofs[r1];
+                for (int o = lane; o < hi - lo; o += 32) stage[o] = a[lo + o];
+                __syncwarp();
+                if (r0 + lane < r1) {
+                    const int k = r0 + lane;
+                    buf[k] = pw_block<true>(stage + (lofs[k] - lo), lofs[k + 1] - lofs[k]);
+                }
+                __syncwarp();
+            }
             if (lane == 0) tail = pw_eval(m, [&](int k, long long, long long) { return buf[k]; });
         }
         if (lane == 0) col_norm[j] = __dsqrt_rn(__dadd_rn(__dmul_rn(csc_vals[s], csc_vals[s]), tail));
@@ -525,7 +563,7 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
     mcf::note_launch();
     k_colnorm<<<nb, 256, 0, s>>>(cp, g->csc_vals, n, g->col_norm);
     mcf::note_launch();
-    k_colnorm_long<<<wgrid, 64, 0, s>>>(long_cols, &cnt->n_long_cols, cp, g->csc_vals, g->col_norm);
+    k_colnorm_long<<<wgrid * 2, 32, 0, s>>>(long_cols, &cnt->n_long_cols, cp, g->csc_vals, g->col_norm);
     mcf::note_launch();
     k_leaf_sums<<<(nl + 255) / 256, 256, 0, s>>>(g->col_norm, d_lo, d_ln, nl, d_leaf);
     mcf::note_launch();

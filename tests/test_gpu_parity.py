@@ -316,7 +316,8 @@ def test_device_tables_bitwise_hub_rows(mc, seed):
     rng = np.random.default_rng(seed)
     n = 3001
     rows, cols = [], []
-    for hub, deg in ((0, 3000), (7, 1500), (100, 300), (2999, 70)):
+    for hub, deg in ((0, 3000), (7, 1500), (100, 300), (2999, 70), (50, 129), (60, 140), (70, 200), (80, 250),
+                     (90, 256), (95, 257), (97, 1030)):
         nb = rng.choice(n, deg, replace=False)
         rows += [hub] * deg
         cols += list(nb)
@@ -491,3 +492,22 @@ def test_action_v_ones_row_sums(mc, name):
     assert np.array_equal(a1.aux["r"].cpu().numpy(), m @ np.ones(c.n))
     np.testing.assert_allclose(a1.values, a2.values, rtol=1e-13, atol=0)
     assert a1.emissions == a2.emissions
+
+
+def test_device_col_norm_beyond_leaf_cap(mc):
+    """A column longer than a warp's leaf table (1024 leaves of <= 128 terms):
+    the lane-0 fallback keeps numpy's pairwise bits."""
+    rng = np.random.default_rng(5)
+    n, deg = 150_001, 140_000
+    nb = rng.choice(np.arange(1, n), deg, replace=False)
+    rows = np.r_[np.zeros(deg, dtype=np.int64), nb]
+    cols = np.r_[nb, np.zeros(deg, dtype=np.int64)]
+    m = sparse.coo_array((rng.normal(size=2 * deg), (rows, cols)), shape=(n, n)).tocsr()
+    m.sum_duplicates()
+    m.sort_indices()
+    a = port.Csr.from_any(m)
+    t = port.transition_tables(a)
+    g = mc.DeviceGraph(as_matrix(a))
+    d = {k: v.cpu().numpy() for k, v in g.tables().items()}
+    assert np.array_equal(d["col_norms"], t.col_norms)
+    assert np.array_equal(d["row_abs_sum"], t.rsum)
