@@ -470,7 +470,7 @@ static void release(mcf_graph *g) {
     if (g->hub_of) cudaFreeAsync(g->hub_of, 0);
     if (g->hub_bits) cudaFreeAsync(g->hub_bits, 0);
     if (g->scratch) cudaFreeAsync(g->scratch, 0);
-    if (g->side) cudaStreamDestroy(g->side);
+    // g->side is the per-device stream shared by all graphs: not destroyed here
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);
     if (g->ev_join) cudaEventDestroy(g->ev_join);
     for (auto &p : g->ev_walk) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }

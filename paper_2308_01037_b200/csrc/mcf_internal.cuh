@@ -105,7 +105,7 @@ struct mcf_graph {
     int device = 0;
     // optional per-launch timing of the dominant kernels (MCF_FLAG_TIME_KERNELS)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_walk, ev_q;
-    // side stream + fork/join events (budgets computed concurrently with r = A v)
+    // side stream (per device, shared) + fork/join events (budgets computed concurrently with r = A v)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };

@@ -15,6 +15,9 @@
 // fixed order, so q does not depend on scheduling, on the number of GPUs or on
 // how the column range is split.
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "mcf_internal.cuh"
 
@@ -722,10 +725,22 @@ static int walks_per_lane() {
 
 template <typename K>
 int walk_grid(K kernel, int threads, size_t smem) {
+    // occupancy queries cost a few microseconds each: cache per (kernel, shape)
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, int, size_t>, int> cache;
+    const auto key = std::make_tuple(reinterpret_cast<const void *>(kernel), threads, smem);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (per_sm < 1) per_sm = 1;
-    return per_sm * sm_count();
+    const int grid = per_sm * sm_count();
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = grid;
+    return grid;
 }
 
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
@@ -876,8 +891,17 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
                        const double *v, double z0, double z1, double *r, double *q, double *qvar, double *y,
                        long long *stats, cudaStream_t s) {
     MCF_ARG(g && r && q && y && ni && walk_pre, "mcf_funm_action: null argument");
-    if (!g->side) {
-        MCF_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+    if (!g->side) {  // one side stream per device, shared by every graph (created once)
+        static std::mutex mu;
+        static std::map<int, cudaStream_t> streams;
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = streams.find(g->device);
+        if (it == streams.end()) {
+            cudaStream_t st;
+            MCF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            it = streams.emplace(g->device, st).first;
+        }
+        g->side = it->second;
         MCF_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
         MCF_CUDA(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
     }

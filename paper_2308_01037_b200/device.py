@@ -55,8 +55,24 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+_ZETA_CACHE: dict = {}  # (device, coefficient bytes) -> device table; the tables are constants
+
+
+def _zeta_table(z: np.ndarray, dev: torch.device) -> torch.Tensor:
+    """Device copy of a coefficient prefix, made once per (device, values):
+    a fresh pageable copy per call would synchronise the host with the stream."""
+    key = (str(dev), z.tobytes())
+    t = _ZETA_CACHE.get(key)
+    if t is None:
+        if len(_ZETA_CACHE) > 256:
+            _ZETA_CACHE.clear()
+        t = torch.from_numpy(z.copy()).to(dev)
+        _ZETA_CACHE[key] = t
+    return t
+
+
 class WalkParams:
-    """mcf_walk_params for one configuration; owns the device zeta table.
+    """mcf_walk_params for one configuration; holds the device zeta table.
 
     walk_capacity = N_s bounds the walks of any column range, which lets the
     library size its buffers without reading the budgets back (no host sync:
@@ -67,7 +83,7 @@ class WalkParams:
         if z.size < config.max_steps + 2:
             raise ArgumentError("zeta table shorter than max_steps + 2")
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.zeta = torch.from_numpy(z).to(dev)
+        self.zeta = _zeta_table(z, dev)
         self.c = N.McfWalkParams(int(config.max_steps), float(config.weight_cutoff),
                                  int(config.seed) & 0xFFFFFFFFFFFFFFFF, self.zeta.data_ptr(),
                                  int(config.n_walks), 0)
