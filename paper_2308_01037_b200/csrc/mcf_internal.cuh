@@ -91,6 +91,12 @@ struct mcf_graph {
     // two (entry, then the target's header).  32 B x nnz; used when the
     // compact tables would not stay in L2.
     mcf::NodeHdr *went = nullptr;
+    // "lean" walk entries for v = 1 on uniform-value graphs: lean[e] = {start,
+    // degree} of col[e].  With every |a| equal, a row's |a| sum -- the weight
+    // factor, and for v = 1 also the payload r -- depends only on its degree
+    // (rsum_by_deg), so a step is ONE dependent random 8-B load.  Built lazily.
+    uint2 *lean = nullptr;
+    double *rsum_by_deg = nullptr;   // max_degree + 1
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;
     void *scratch = nullptr;

@@ -15,6 +15,7 @@
 // fixed order, so q does not depend on scheduling, on the number of GPUs or on
 // how the column range is split.
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -45,6 +46,8 @@ struct WalkCommon {
     int return_only;             // MCF_FLAG_RETURN_ONLY
     long long *stats;
     int *err;
+    const uint2 *__restrict__ lean;         // v = 1 on uniform-value graphs (else null)
+    const double *__restrict__ rsum_by_deg;
     // L2 bulk prefetch of the walk tables at kernel start (bytes 0: none)
     const char *pf[3];
     long long pf_bytes[3];
@@ -226,8 +229,19 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned
 // The header of the entry's target, with pad = target id and HDR_NEG_EDGE =
 // sign of a_e.  Fat layout: one 32-B sector; compact: the entry's packed
 // column id, then the target's header (two dependent sectors).
-template <bool FAT>
+template <bool FAT, bool LEAN = false>
 __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) {
+    if (LEAN) {  // {start, degree} of the target; |a| row sum (= r for v = 1) by degree
+        const uint2 t = __ldg(a.lean + e);
+        NodeHdr h;
+        h.start = (int)t.x;
+        h.deg = (int)t.y;
+        h.flags = HDR_UNIFORM;
+        h.pad = 0;
+        h.rsum = __ldg(a.rsum_by_deg + t.y);
+        h.aux = h.rsum;
+        return h;
+    }
     if (FAT) return load_hdr(a.went + e);
     const int pc = __ldg(a.ecol + e);
     const int nxt = pc & 0x7fffffff;
@@ -264,7 +278,7 @@ struct WalkOcc {  // resident CTAs per SM the register budget is tuned for
 // NW walks per lane, stepped together so their dependent loads overlap.
 // OCC: CTAs per SM the one-walk variant is register-tuned for (4: no spills,
 // 5: more warps with a few spilled registers).
-template <bool REPLAY, bool FAT, int NW, int OCC = 5>
+template <bool REPLAY, bool FAT, int NW, int OCC = 5, bool LEAN = false>
 __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(WalkCommon a, double *__restrict__ xw) {
     l2_prefetch_tables(a);
     const long long wb = __ldg(a.walk_pre + a.col_begin);
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
         }
 #pragma unroll
         for (int s = 0; s < NW; ++s)
-            if (L[s].rel >= 0 && e[s] >= 0) nh[s] = fetch_next<FAT>(a, e[s]);
+            if (L[s].rel >= 0 && e[s] >= 0) nh[s] = fetch_next<FAT, LEAN>(a, e[s]);
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
             if (L[s].rel < 0) continue;
@@ -666,6 +680,8 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.walk_off = nullptr;
     a.entries = nullptr;
     a.colmax = nullptr;
+    a.lean = nullptr;
+    a.rsum_by_deg = nullptr;
     a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
     for (int k = 0; k < 3; ++k) {
         a.pf[k] = nullptr;
@@ -787,9 +803,53 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     return MCF_OK;
 }
 
+// lean[e] = {start, degree} of col[e]
+__global__ void k_build_lean(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids, long long nnz,
+                             uint2 *__restrict__ lean) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int c = col_ids[e];
+    const long long s0 = row_ptr[c], s1 = row_ptr[c + 1];
+    lean[e] = make_uint2((unsigned)s0, (unsigned)(s1 - s0));
+}
+
+// rsum_by_deg[deg(i)] = rsum(i): with every |a| equal, rows of equal degree add
+// the same values in the same order, so every writer stores the same bits
+__global__ void k_rsum_by_deg(const NodeHdr *__restrict__ hdr, long long n, double *__restrict__ tab) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const NodeHdr h = load_hdr(hdr + i);
+    tab[h.deg] = h.deg ? h.rsum : 0.0;
+}
+
+static bool lean_eligible(const mcf_graph *g) {
+    const char *env = getenv("MCF_LEAN_WALK");
+    if (env && !strcmp(env, "0")) return false;
+    return g->uniform_value && g->nnz < (1ll << 31) && g->info.max_degree < (1ll << 31);
+}
+
+static int ensure_lean(mcf_graph *g, cudaStream_t s) {
+    if (g->lean) return MCF_OK;
+    uint2 *lean = nullptr;
+    double *tab = nullptr;
+    MCF_CUDA(cudaMallocAsync(&lean, sizeof(uint2) * g->nnz, s));
+    MCF_CUDA(cudaMallocAsync(&tab, sizeof(double) * (g->info.max_degree + 1), s));
+    MCF_CUDA(cudaMemsetAsync(tab, 0, sizeof(double) * (g->info.max_degree + 1), s));
+    k_build_lean<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->nnz,
+                                                                  lean);
+    mcf::note_launch();
+    k_rsum_by_deg<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->n, tab);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_build_lean");
+    g->lean = lean;
+    g->rsum_by_deg = tab;
+    return MCF_OK;
+}
+
 static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                   const long long *walk_off, const int *entries, const double *r, double *q, double *qvar,
-                  long long *stats, cudaStream_t s, bool replay, bool aux_ready = false, int *blk_ready = nullptr) {
+                  long long *stats, cudaStream_t s, bool replay, bool aux_ready = false, int *blk_ready = nullptr,
+                  bool lean = false) {
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(r && q && stats, "action walk: null r/q/stats");
@@ -818,7 +878,13 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
         k_set_aux<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, r, g->n);
         mcf::note_launch();
     }
-    if (g->went) {
+    if (lean) {
+        rc = ensure_lean(g, s);
+        if (rc) return rc;
+        a.lean = g->lean;
+        a.rsum_by_deg = g->rsum_by_deg;
+        for (int k = 0; k < 3; ++k) a.pf_bytes[k] = 0;  // the L2 prefetch covers the compact tables only
+    } else if (g->went) {
         k_set_aux_fat<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>(g->went, r, g->nnz);
         mcf::note_launch();
     }
@@ -827,7 +893,10 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     if (nw > 0) {
         rc = timed_begin(g, timed, g->ev_walk, s);
         if (rc) return rc;
-        if (g->went) {
+        if (lean) {
+            k_walk_action<false, false, 1, 4, true><<<walk_grid(k_walk_action<false, false, 1, 4, true>, 256, 0), 256, 0,
+                                                      s>>>(a, xw);
+        } else if (g->went) {
             if (replay) {
                 k_walk_action<true, true, 1><<<walk_grid(k_walk_action<true, true, 1>, 256, 0), 256, 0, s>>>(a, xw);
             } else {
@@ -925,7 +994,8 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     mcf_walk_params pp = *p;
     pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks
-    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk);
+    const bool lean = v == V_ONES && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
+    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk, lean);
     if (rc) return rc;
     return spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
 }

@@ -511,3 +511,29 @@ def test_device_col_norm_beyond_leaf_cap(mc):
     d = {k: v.cpu().numpy() for k, v in g.tables().items()}
     assert np.array_equal(d["col_norms"], t.col_norms)
     assert np.array_equal(d["row_abs_sum"], t.rsum)
+
+
+@pytest.mark.parametrize("name", ["ba400", "er300", "kron8"])
+def test_lean_walk_bitwise(mc, name):
+    """v = 1 on a uniform-value graph walks {start, degree} entries with the
+    row sums by degree (one dependent load per step): q and y are bitwise the
+    ones of the header walk (MCF_LEAN_WALK=0), fat and compact layouts."""
+    import os
+    import torch
+    c = golden_io.load(name)
+    a = as_matrix(c.sa, c.symmetric)
+    out = {}
+    for lean in ("1", "0"):
+        os.environ["MCF_LEAN_WALK"] = lean
+        try:
+            for layout in ("compact", "fat"):
+                os.environ["MCF_WALK_LAYOUT"] = layout
+                g = mc.DeviceGraph(a, gamma=0.05)
+                res = mc.rand_funm_action(g, mc.EXPONENTIAL, None, mc.WalkConfig(30 * c.n, 1e-6, 28, 7))
+                out[lean, layout] = (np.asarray(res.values), res.aux["q"].cpu().numpy(), res.emissions)
+        finally:
+            os.environ.pop("MCF_LEAN_WALK", None)
+            os.environ.pop("MCF_WALK_LAYOUT", None)
+    ref = out["0", "compact"]
+    for k, v in out.items():
+        assert np.array_equal(v[0], ref[0]) and np.array_equal(v[1], ref[1]) and v[2] == ref[2], k
