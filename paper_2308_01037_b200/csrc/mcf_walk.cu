@@ -192,7 +192,7 @@ constexpr long long PICK_LAST = -2;  // final draw: only |W| matters, and |a/t| 
 // First half of a step (walker.py:274-281): choose the CSR entry to take from
 // the current row.  Philox-4x32-10 yields 128 bits per (step pair, walk,
 // column): even steps use the first 64, odd steps the second.
-template <bool REPLAY>
+template <bool REPLAY, bool LEAN = false>
 __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned &ab) {
     const NodeHdr &h = L.h;
     if (h.deg == 0) {  // absorbing row (walker.py:274-278)
@@ -222,7 +222,7 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned
     } else {
         r = ((uint64_t)L.r0 << 32) | L.r1;
     }
-    if (h.flags & HDR_UNIFORM) return h.start + (long long)__umul64hi(r, (uint64_t)h.deg);
+    if (LEAN || (h.flags & HDR_UNIFORM)) return h.start + (long long)__umul64hi(r, (uint64_t)h.deg);
     return h.start + cdf_pick(a.cdf + h.start, h.deg, (double)(r >> 11) * 0x1.0p-53);
 }
 
@@ -299,10 +299,12 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
         for (int s = 0; s < NW; ++s) {
             if (L[s].rel < 0) continue;
             // q_c += zeta W r[l]; classic MC diagonal: only back at the start (Alg. 1)
-            const double pay = a.return_only ? ((int)L[s].h.pad == L[s].c ? 1.0 : 0.0) : L[s].h.aux;
+            // lean walks (v = 1, uniform values): the payload r = A 1 is the row sum itself
+            const double pay = LEAN ? L[s].h.rsum
+                                    : (a.return_only ? ((int)L[s].h.pad == L[s].c ? 1.0 : 0.0) : L[s].h.aux);
             L[s].x = fma(__ldg(a.zeta + L[s].k + 2) * L[s].w, pay, L[s].x);
             ++em;
-            e[s] = pick<REPLAY>(a, L[s], ab);
+            e[s] = pick<REPLAY, LEAN>(a, L[s], ab);
         }
 #pragma unroll
         for (int s = 0; s < NW; ++s)
@@ -733,8 +735,10 @@ static int walks_per_lane() {
     static int v = 0;
     if (!v) {
         const char *e = getenv("MCF_WALKS_PER_LANE");
-        v = e ? atoi(e) : 14;
-        if (v != 1 && v != 2 && v != 4 && v != 16 && v != 24) v = 14;  // 14 = one walk, 4 CTAs/SM (no spills): best measured
+        v = e ? atoi(e) : 0;  // 0: each kernel's default
+        // 1/2/4 walks per lane; 14/15/16 = one walk at 4/5/6 CTAs per SM;
+        // 24 = two walks at 4.  -1: the kernel's measured default
+        if (v != 1 && v != 2 && v != 4 && v != 14 && v != 15 && v != 16 && v != 24) v = -1;
     }
     return v;
 }
@@ -894,13 +898,19 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
         rc = timed_begin(g, timed, g->ev_walk, s);
         if (rc) return rc;
         if (lean) {
-            k_walk_action<false, false, 1, 4, true><<<walk_grid(k_walk_action<false, false, 1, 4, true>, 256, 0), 256, 0,
-                                                      s>>>(a, xw);
+            // one walk per lane at 5 CTAs/SM (no spills): measured best for the
+            // one-load chain (4: -12%, 6: equal with spills, 2 walks/lane: -45%)
+            switch (walks_per_lane()) {
+                case 14: k_walk_action<false, false, 1, 4, true><<<walk_grid(k_walk_action<false, false, 1, 4, true>, 256, 0), 256, 0, s>>>(a, xw); break;
+                case 16: k_walk_action<false, false, 1, 6, true><<<walk_grid(k_walk_action<false, false, 1, 6, true>, 256, 0), 256, 0, s>>>(a, xw); break;
+                case 24: k_walk_action<false, false, 2, 4, true><<<walk_grid(k_walk_action<false, false, 2, 4, true>, 256, 0), 256, 0, s>>>(a, xw); break;
+                default: k_walk_action<false, false, 1, 5, true><<<walk_grid(k_walk_action<false, false, 1, 5, true>, 256, 0), 256, 0, s>>>(a, xw);
+            }
         } else if (g->went) {
             if (replay) {
                 k_walk_action<true, true, 1><<<walk_grid(k_walk_action<true, true, 1>, 256, 0), 256, 0, s>>>(a, xw);
             } else {
-                switch (walks_per_lane()) {
+                switch (walks_per_lane() < 0 ? 14 : walks_per_lane()) {  // header walk: 4 CTAs/SM
                     case 2: k_walk_action<false, true, 2><<<walk_grid(k_walk_action<false, true, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 4: k_walk_action<false, true, 4><<<walk_grid(k_walk_action<false, true, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 14: k_walk_action<false, true, 1, 4><<<walk_grid(k_walk_action<false, true, 1, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
@@ -913,7 +923,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
             if (replay) {
                 k_walk_action<true, false, 1><<<walk_grid(k_walk_action<true, false, 1>, 256, 0), 256, 0, s>>>(a, xw);
             } else {
-                switch (walks_per_lane()) {
+                switch (walks_per_lane() < 0 ? 14 : walks_per_lane()) {  // header walk: 4 CTAs/SM
                     case 2: k_walk_action<false, false, 2><<<walk_grid(k_walk_action<false, false, 2>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 4: k_walk_action<false, false, 4><<<walk_grid(k_walk_action<false, false, 4>, 256, 0), 256, 0, s>>>(a, xw); break;
                     case 14: k_walk_action<false, false, 1, 4><<<walk_grid(k_walk_action<false, false, 1, 4>, 256, 0), 256, 0, s>>>(a, xw); break;

@@ -26,14 +26,14 @@ def main(sizes):
         p = WalkParams(cfg, z)
         v = torch.ones(g.n, dtype=torch.float64, device=g.device)
         for _ in range(3):
-            y, st = parallel.sharded_action(g, mc.EXPONENTIAL, v, cfg, params=p)
+            y, st = parallel.sharded_action(g, mc.EXPONENTIAL, None, cfg, params=p)
         torch.cuda.synchronize()
         g.kernel_times(reset=True)
         p.c.flags = _native.MCF_FLAG_TIME_KERNELS
         em = 0
         for _ in range(5):
             flush.zero_()
-            y, st = parallel.sharded_action(g, mc.EXPONENTIAL, v, cfg, params=p)
+            y, st = parallel.sharded_action(g, mc.EXPONENTIAL, None, cfg, params=p)
             em += int(st[1])
         torch.cuda.synchronize()
         wms, _, k = g.kernel_times(reset=True)
