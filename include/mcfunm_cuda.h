@@ -153,9 +153,10 @@ MCF_API int mcf_walk_action(mcf_graph *g, const mcf_walk_params *p, const int64_
  * r = A v), the walks of every column, q, optional q_var, and
  * y = zeta0 v + zeta1 r + A q ([dev] n each).  v may be NULL for v = 1 (total
  * communicability): r is then the row sums of A, bit-identical
- * to the reference's A @ ones.  Single process (the multi-GPU
- * path composes mcf_spmv / mcf_walk_action with an exchange of q).  No host
- * synchronisation: capturable in a CUDA graph (set p->walk_capacity). */
+ * to the reference's A @ ones.  q, q_var, y and stats[4] are overwritten
+ * (unlike mcf_walk_action, stats need not be zeroed).  Single process (the
+ * multi-GPU path composes mcf_spmv / mcf_walk_action with an exchange of q).
+ * No host synchronisation: capturable in a CUDA graph. */
 MCF_API int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, int64_t n_walks, int64_t *ni,
                             int64_t *walk_pre, const double *v, double zeta0, double zeta1, double *r, double *q,
                             double *q_var, double *y, int64_t *stats, void *stream);

@@ -847,8 +847,10 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
     AF_TRACE(F, 23);
 }
 
+// fused_scratch: caller-provided AllocFused whose first fused_scratch_zero_bytes()
+// are already zero (one memset for several scratch blocks), or null
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
-                    cudaStream_t s) {
+                    cudaStream_t s, void *fused_scratch = nullptr) {
     MCF_ARG(g && ni && walk_pre, "mcf_allocate_walks: null argument");
     MCF_ARG(n_walks >= 1, "n_walks must be at least 1");  // walker.py:168-169
     MCF_ARG(n_walks < (1ll << 53), "n_walks must be below 2^53");
@@ -861,13 +863,16 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
     const int G = sm_count() < AF_MAXG ? sm_count() : AF_MAXG;
     const long long K = (n + (long long)G * AF_T - 1) / ((long long)G * AF_T);
     if (K <= AF_KMAX && !(path && !strcmp(path, "passes"))) {  // one persistent kernel
-        AllocFused *F = nullptr;
-        MCF_CUDA(cudaMallocAsync(&F, sizeof(AllocFused), s));
-        MCF_CUDA(cudaMemsetAsync(F, 0, offsetof(AllocFused, lvl), s));
+        const bool own = fused_scratch == nullptr;
+        AllocFused *F = reinterpret_cast<AllocFused *>(fused_scratch);
+        if (own) {
+            MCF_CUDA(cudaMallocAsync(&F, sizeof(AllocFused), s));
+            MCF_CUDA(cudaMemsetAsync(F, 0, offsetof(AllocFused, lvl), s));
+        }
         k_alloc_fused<<<G, AF_T, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, (int)K, F, ni, walk_pre, blk_col);
         mcf::note_launch();
         MCF_LAUNCHED("k_alloc_fused");
-        MCF_CUDA(cudaFreeAsync(F, s));
+        if (own) MCF_CUDA(cudaFreeAsync(F, s));
         return MCF_OK;
     }
     // one zero-initialised block: selection state + the budget scan's look-back words
@@ -900,8 +905,17 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
 }
 
 int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
-                   cudaStream_t s) {
-    return allocate(g, n_walks, ni, walk_pre, blk_col, s);
+                   cudaStream_t s, void *fused_scratch) {
+    return allocate(g, n_walks, ni, walk_pre, blk_col, s, fused_scratch);
+}
+
+size_t fused_scratch_bytes() { return sizeof(AllocFused); }
+size_t fused_scratch_zero_bytes() { return offsetof(AllocFused, lvl); }
+bool fused_alloc_applies(const mcf_graph *g) {
+    const char *path = getenv("MCF_ALLOC_PATH");
+    const int G = sm_count() < AF_MAXG ? sm_count() : AF_MAXG;
+    const long long K = (g->n + (long long)G * AF_T - 1) / ((long long)G * AF_T);
+    return g->n > 0 && K <= AF_KMAX && !(path && !strcmp(path, "passes"));
 }
 
 }  // namespace mcf

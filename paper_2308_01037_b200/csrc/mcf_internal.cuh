@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 #include <utility>
 #include <vector>
@@ -354,7 +355,10 @@ int build_blk_col(const long long *walk_pre, long long col_begin, long long col_
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
 int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s);
 int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
-                   cudaStream_t s);
+                   cudaStream_t s, void *fused_scratch = nullptr);
+size_t fused_scratch_bytes();       // scratch of the one-kernel budget path
+size_t fused_scratch_zero_bytes();  // its prefix that must be zero
+bool fused_alloc_applies(const mcf_graph *g);
 int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end,
                     long long *wb, long long *we, cudaStream_t s);
 int sm_count();

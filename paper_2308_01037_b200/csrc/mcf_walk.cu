@@ -492,8 +492,10 @@ __device__ __forceinline__ double combine_exact(double alpha, const double *v, d
 // without negative entries is exactly the |a| row sum already in the header
 // (same additions, same order, a * 1.0 == a); rows with a negative entry are
 // summed again with their signs.  r also lands in hdr.aux for the walk.
-__global__ void k_r_ones(NodeHdr *__restrict__ hdr, const double *__restrict__ vals, long long n, double *__restrict__ r) {
+__global__ void k_r_ones(NodeHdr *__restrict__ hdr, const double *__restrict__ vals, long long n, double *__restrict__ r,
+                         long long *__restrict__ stats) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 4 && stats) stats[i] = 0;
     if (i >= n) return;
     const NodeHdr h = load_hdr(hdr + i);
     double s = h.rsum;
@@ -853,7 +855,7 @@ static int ensure_lean(mcf_graph *g, cudaStream_t s) {
 static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                   const long long *walk_off, const int *entries, const double *r, double *q, double *qvar,
                   long long *stats, cudaStream_t s, bool replay, bool aux_ready = false, int *blk_ready = nullptr,
-                  bool lean = false) {
+                  bool lean = false, double *xw_ready = nullptr, unsigned *counter_ready = nullptr) {
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(r && q && stats, "action walk: null r/q/stats");
@@ -866,13 +868,15 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     rc = setup_common(g, p, walk_pre, cb, ce, nw, a, &blk, s, blk_ready);
     if (rc) return rc;
     MCF_ARG(nw < (1ll << 31) - 4096, "walks per call must be below 2^31 (split the column range)");
-    double *xw = nullptr;
-    unsigned *counter = nullptr;
+    double *xw = xw_ready;
+    unsigned *counter = counter_ready;  // preallocated: already zero (funm_action's one memset)
     int *err = nullptr;
-    MCF_CUDA(cudaMallocAsync(&xw, sizeof(double) * (nw > 0 ? nw : 1), s));
-    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) + sizeof(int) * 2, s));
+    if (!xw) MCF_CUDA(cudaMallocAsync(&xw, sizeof(double) * (nw > 0 ? nw : 1), s));
+    if (!counter) {
+        MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) + sizeof(int) * 2, s));
+        MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
+    }
     err = (int *)(counter + 2);
-    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
     a.counter = counter;
     a.err = err;
     a.stats = stats;
@@ -950,9 +954,9 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
         MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
         MCF_CUDA(cudaStreamSynchronize(s));
     }
-    cudaFreeAsync(xw, s);
-    cudaFreeAsync(counter, s);
-    cudaFreeAsync(blk, s);
+    if (!xw_ready) cudaFreeAsync(xw, s);
+    if (!counter_ready) cudaFreeAsync(counter, s);
+    if (!blk_ready) cudaFreeAsync(blk, s);
     if (herr) {
         set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) +
                   "): entries missing, surplus, or outside the current row");
@@ -985,18 +989,30 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
         MCF_CUDA(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
     }
     MCF_ARG(p && n_walks >= 1 && n_walks < (1ll << 31) - 4096, "mcf_funm_action: n_walks must be in [1, 2^31 - 4096)");
+    // one scratch block, one memset: [walk counter + error flags | budget-kernel state | blk | xw]
+    const bool fused = fused_alloc_applies(g);
+    const size_t ctl = 256, fz = fused ? fused_scratch_zero_bytes() : 0, fb = fused ? fused_scratch_bytes() : 0;
+    const size_t fb_al = (fb + 255) & ~size_t(255);
+    const long long nblk = (n_walks + (1ll << WALK_BLK_SHIFT) - 1) >> WALK_BLK_SHIFT;
+    const size_t blk_bytes = ((size_t)nblk * sizeof(int) + 255) & ~size_t(255);
+    char *scratch = nullptr;
+    MCF_CUDA(cudaMallocAsync(&scratch, ctl + fb_al + blk_bytes + sizeof(double) * (size_t)n_walks, s));
+    unsigned *counter = reinterpret_cast<unsigned *>(scratch);
+    void *F = fused ? scratch + ctl : nullptr;
+    int *blk = reinterpret_cast<int *>(scratch + ctl + fb_al);
+    double *xw = reinterpret_cast<double *>(scratch + ctl + fb_al + blk_bytes);
+    MCF_CUDA(cudaMemsetAsync(scratch, 0, ctl + fz, s));
     MCF_CUDA(cudaEventRecord(g->ev_fork, s));
     MCF_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
-    int *blk = nullptr;
-    MCF_CUDA(cudaMallocAsync(&blk, sizeof(int) * ((n_walks + (1ll << WALK_BLK_SHIFT) - 1) >> WALK_BLK_SHIFT), g->side));
-    int rc = allocate_walks(g, n_walks, ni, walk_pre, blk, g->side);
+    int rc = allocate_walks(g, n_walks, ni, walk_pre, blk, g->side, F);
     if (rc) return rc;
     MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
     if (v) {
+        MCF_CUDA(cudaMemsetAsync(stats, 0, sizeof(long long) * 4, s));
         rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
         if (rc) return rc;
-    } else {  // v = 1
-        k_r_ones<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, g->n, r);
+    } else {  // v = 1 (the same kernel zeroes the statistics)
+        k_r_ones<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, g->n, r, stats);
         mcf::note_launch();
         MCF_LAUNCHED("k_r_ones");
         v = V_ONES;
@@ -1005,10 +1021,15 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     mcf_walk_params pp = *p;
     pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks
     const bool lean = v == V_ONES && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
-    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk, lean);
+    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk, lean, xw, counter);
     if (rc) return rc;
-    return spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
+    rc = spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
+    if (rc) return rc;
+    MCF_CUDA(cudaFreeAsync(scratch, s));
+    return MCF_OK;
 }
+
+
 
 }  // namespace mcf
 

@@ -18,6 +18,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _native as N
 from .device import DeviceGraph, WalkParams
 from .series import as_stream
 from .walker import check_config
@@ -66,14 +67,15 @@ def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=No
     coeffs = as_stream(coeffs)
     z = coeffs.prefix(cfg.max_steps + 2)
     params = params or WalkParams(cfg, z, g.device)
-    st = g.new_stats()
-    if size == 1 and budgets is None:  # the whole pass in one library call
-        q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
+    if size == 1 and budgets is None:  # the whole pass in one library call (q, y, stats overwritten)
+        q = torch.empty(g.n, dtype=torch.float64, device=g.device)
         r, y = torch.empty_like(q), torch.empty_like(q)
+        st = torch.empty(N.MCF_STATS_LEN, dtype=torch.int64, device=g.device)
         return g.funm_action(params, cfg.n_walks, v, z[0], z[1], r, q, y, stats=st)[0], st
     if v is None:
         v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
+    st = g.new_stats()
     cols = column_shards(pre, size)[rank]
     rows = row_shards(g.n, size)[rank]
     r = g.spmv(v)
@@ -94,6 +96,7 @@ def sharded_diag(g: DeviceGraph, coeffs, config, *, params=None, budgets=None, g
     z = coeffs.prefix(cfg.max_steps + 2)
     params = params or WalkParams(cfg, z, g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
+    st = g.new_stats()
     cols = column_shards(pre, size)[rank] if size > 1 else (0, g.n)
     rows = row_shards(g.n, size)[rank] if size > 1 else (0, g.n)
     pcol = torch.zeros(g.nnz, dtype=torch.float64, device=g.device)
