@@ -229,7 +229,7 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned
 // The header of the entry's target, with pad = target id and HDR_NEG_EDGE =
 // sign of a_e.  Fat layout: one 32-B sector; compact: the entry's packed
 // column id, then the target's header (two dependent sectors).
-template <bool FAT, bool LEAN = false>
+template <bool FAT, bool LEAN = false, bool WITH_ID = false>
 __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) {
     if (LEAN) {  // {start, degree} of the target; |a| row sum (= r for v = 1) by degree
         const uint2 t = __ldg(a.lean + e);
@@ -237,7 +237,8 @@ __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) 
         h.start = (int)t.x;
         h.deg = (int)t.y;
         h.flags = HDR_UNIFORM;
-        h.pad = 0;
+        // the target id (diag emissions): same index, loaded alongside, off the chain
+        h.pad = WITH_ID ? (uint32_t)(__ldg(a.ecol + e) & 0x7fffffff) : 0u;
         h.rsum = __ldg(a.rsum_by_deg + t.y);
         h.aux = h.rsum;
         return h;
@@ -334,8 +335,8 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
 // Each emission is (state, zeta_{k+2} W_k); unused slots of a walk hold -1.
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
-template <int MODE, bool FAT>
-__global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_len, long long off_base,
+template <int MODE, bool FAT, int OCC = 4, bool LEAN = false>
+__global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long slot_len, long long off_base,
                                                    long long *__restrict__ eaux, int *__restrict__ est,
                                                    double *__restrict__ ewt) {
     constexpr bool REPLAY = MODE == EMIT_REPLAY;
@@ -374,9 +375,9 @@ __global__ void __launch_bounds__(256) k_walk_emit(WalkCommon a, long long slot_
         }
         ++em;
         const long long emitted = L.k + 1;
-        const long long e = pick<REPLAY>(a, L, ab);
+        const long long e = pick<REPLAY, LEAN>(a, L, ab);
         NodeHdr nh;
-        if (e >= 0) nh = fetch_next<FAT>(a, e);
+        if (e >= 0) nh = fetch_next<FAT, LEAN, true>(a, e);
         if (e == PICK_END || apply(a, L, e, nh, tr)) {
             if (REPLAY && L.epos != L.eend) atomicOr(a.err, 4);
             if (MODE == EMIT_COUNT) {
@@ -765,50 +766,6 @@ int walk_grid(K kernel, int threads, size_t smem) {
     return grid;
 }
 
-int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
-                     long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
-                     long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
-                     long long *stats, int *err, cudaStream_t s) {
-    WalkCommon a;
-    int *blk = nullptr;
-    int rc = setup_common(g, p, walk_pre, cb, ce, nwalks, a, &blk, s);
-    if (rc) return rc;
-    unsigned *counter = nullptr;
-    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
-    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
-    a.counter = counter;
-    a.err = err;
-    a.stats = stats;
-    a.walk_off = walk_off;
-    a.entries = entries;
-    a.colmax = colmax;
-    const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0 && mode != EMIT_COUNT;
-    rc = timed_begin(g, timed, g->ev_walk, s);
-    if (rc) return rc;
-    if (g->went) {
-        switch (mode) {
-            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, true><<<walk_grid(k_walk_emit<EMIT_FIXED, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
-            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, true><<<walk_grid(k_walk_emit<EMIT_REPLAY, true>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
-            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, true><<<walk_grid(k_walk_emit<EMIT_COUNT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
-            default: k_walk_emit<EMIT_EXPLICIT, true><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
-        }
-    } else {
-        switch (mode) {
-            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false><<<walk_grid(k_walk_emit<EMIT_FIXED, false>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
-            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, false><<<walk_grid(k_walk_emit<EMIT_REPLAY, false>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
-            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false><<<walk_grid(k_walk_emit<EMIT_COUNT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
-            default: k_walk_emit<EMIT_EXPLICIT, false><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
-        }
-    }
-    mcf::note_launch();
-    MCF_LAUNCHED("k_walk_emit");
-    rc = timed_end(timed, g->ev_walk, s);
-    if (rc) return rc;
-    cudaFreeAsync(counter, s);
-    cudaFreeAsync(blk, s);
-    return MCF_OK;
-}
-
 // lean[e] = {start, degree} of col[e]
 __global__ void k_build_lean(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids, long long nnz,
                              uint2 *__restrict__ lean) {
@@ -849,6 +806,64 @@ static int ensure_lean(mcf_graph *g, cudaStream_t s) {
     MCF_LAUNCHED("k_build_lean");
     g->lean = lean;
     g->rsum_by_deg = tab;
+    return MCF_OK;
+}
+
+int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
+                     long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
+                     long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
+                     long long *stats, int *err, cudaStream_t s) {
+    WalkCommon a;
+    int *blk = nullptr;
+    int rc = setup_common(g, p, walk_pre, cb, ce, nwalks, a, &blk, s);
+    if (rc) return rc;
+    unsigned *counter = nullptr;
+    MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
+    MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
+    a.counter = counter;
+    a.err = err;
+    a.stats = stats;
+    a.walk_off = walk_off;
+    a.entries = entries;
+    a.colmax = colmax;
+    const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0 && mode != EMIT_COUNT;
+    rc = timed_begin(g, timed, g->ev_walk, s);
+    if (rc) return rc;
+    // uniform-value graphs: {start, degree} entries + row sums by degree (one
+    // dependent load per step; the emitted id comes from ecol alongside)
+    const bool lean = mode != EMIT_REPLAY && lean_eligible(g);
+    if (lean) {
+        rc = ensure_lean(g, s);
+        if (rc) return rc;
+        a.lean = g->lean;
+        a.rsum_by_deg = g->rsum_by_deg;
+        for (int k = 0; k < 3; ++k) a.pf_bytes[k] = 0;
+        switch (mode) {
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false, 4, true><<<walk_grid(k_walk_emit<EMIT_FIXED, false, 4, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false, 4, true><<<walk_grid(k_walk_emit<EMIT_COUNT, false, 4, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, false, 4, true><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, false, 4, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+        }
+    } else if (g->went) {
+        switch (mode) {
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, true><<<walk_grid(k_walk_emit<EMIT_FIXED, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, true><<<walk_grid(k_walk_emit<EMIT_REPLAY, true>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, true><<<walk_grid(k_walk_emit<EMIT_COUNT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, true><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+        }
+    } else {
+        switch (mode) {
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false><<<walk_grid(k_walk_emit<EMIT_FIXED, false>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, false><<<walk_grid(k_walk_emit<EMIT_REPLAY, false>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false><<<walk_grid(k_walk_emit<EMIT_COUNT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, false><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+        }
+    }
+    mcf::note_launch();
+    MCF_LAUNCHED("k_walk_emit");
+    rc = timed_end(timed, g->ev_walk, s);
+    if (rc) return rc;
+    cudaFreeAsync(counter, s);
+    cudaFreeAsync(blk, s);
     return MCF_OK;
 }
 

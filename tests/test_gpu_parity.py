@@ -537,3 +537,27 @@ def test_lean_walk_bitwise(mc, name):
     ref = out["0", "compact"]
     for k, v in out.items():
         assert np.array_equal(v[0], ref[0]) and np.array_equal(v[1], ref[1]) and v[2] == ref[2], k
+
+
+@pytest.mark.parametrize("name", ["ba400", "er300", "kron8"])
+def test_lean_diag_bitwise(mc, name):
+    """Diag walks on a uniform-value graph use the {start, degree} entries
+    with the id read alongside: d is bitwise the header walk's (both layouts)."""
+    import os
+    c = golden_io.load(name)
+    a = as_matrix(c.sa, c.symmetric)
+    out = {}
+    for lean in ("1", "0"):
+        os.environ["MCF_LEAN_WALK"] = lean
+        try:
+            for layout in ("compact", "fat"):
+                os.environ["MCF_WALK_LAYOUT"] = layout
+                g = mc.DeviceGraph(a, gamma=0.05)
+                res = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(30 * c.n, 1e-6, 28, 7))
+                out[lean, layout] = (np.asarray(res.values), res.emissions, res.truncated)
+        finally:
+            os.environ.pop("MCF_LEAN_WALK", None)
+            os.environ.pop("MCF_WALK_LAYOUT", None)
+    ref = out["0", "compact"]
+    for k, v in out.items():
+        assert np.array_equal(v[0], ref[0]) and v[1:] == ref[1:], k
