@@ -569,10 +569,21 @@ __device__ __forceinline__ void find_bin_all(const unsigned (*cnt)[NBUCKET], lon
     __syncthreads();
 }
 
+// OnesR (optional, funm_action with v = 1): the same pass also writes
+// r = A 1 (the row sums; rows holding a negative value summed with signs)
+// into r and the walk headers, and zeroes the walk statistics -- so one
+// kernel prepares everything the walks need.
+struct OnesR {
+    NodeHdr *hdr;
+    const double *vals;
+    double *r;
+    long long *stats;
+};
+
 __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restrict__ p, long long n, double total,
                                                         long long n_walks, int K, AllocFused *F,
                                                         long long *__restrict__ ni, long long *__restrict__ walk_pre,
-                                                        int *__restrict__ blk_col) {
+                                                        int *__restrict__ blk_col, OnesR ones) {
     __shared__ unsigned h[NBUCKET];
     __shared__ unsigned long long smn[NBUCKET], smx[NBUCKET];
     __shared__ long long s_wa[AF_W], s_wb[AF_W], s_pa, s_pb;
@@ -592,6 +603,22 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
     for (int k = 0; k < AF_KMAX; ++k) {
         const long long j = base + 32ll * k;
         pv[k] = (k < K && j < n) ? p[j] : -1.0;  // -1: padding
+    }
+    if (ones.r) {  // r = A 1 for the same rows (warp-striped, coalesced header reads)
+        if (blockIdx.x == 0 && threadIdx.x < 4) ones.stats[threadIdx.x] = 0;
+#pragma unroll
+        for (int k = 0; k < AF_KMAX; ++k) {
+            const long long j = base + 32ll * k;
+            if (k >= K || j >= n) break;
+            const NodeHdr hj = load_hdr(ones.hdr + j);
+            double rs = hj.deg ? hj.rsum : 0.0;
+            if (hj.flags & HDR_HAS_NEG) {
+                rs = 0.0;
+                for (int t = 0; t < hj.deg; ++t) rs = __dadd_rn(rs, ones.vals[hj.start + t]);
+            }
+            ones.r[j] = rs;
+            ones.hdr[j].aux = rs;
+        }
     }
     // ---- phase 1: floor sums, remainder buckets ------------------------------
     for (int b = threadIdx.x; b < NBUCKET; b += AF_T) h[b] = 0;
@@ -710,20 +737,13 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
                 unsigned long long key = 0;
                 if (pv[k] > 0.0) floor_key(pv[k], total, got, key);
                 const bool in = key && key >= lo && key <= hi;
-                const unsigned m = __ballot_sync(MCF_FULL, in);
-                if (!m) continue;
-                const int src = __ffs(m) - 1;
-                const unsigned long long k0 = __shfl_sync(MCF_FULL, key, src);
-                if (__all_sync(MCF_FULL, !in || key == k0)) {  // one tied key in the warp: one update
-                    if (lane == src) {
-                        const int bk = (int)((k0 - lo) / width);
-                        atomicAdd(&h[bk], (unsigned)__popc(m));
-                        atomicMin(&smn[bk], k0);
-                        atomicMax(&smx[bk], k0);
-                    }
-                } else if (in) {
+                if (!__any_sync(MCF_FULL, in)) continue;
+                // tied keys are the common case here: one shared-memory update per
+                // group of equal keys in the warp (no same-address serialisation)
+                const unsigned grp = __match_any_sync(MCF_FULL, in ? key : 0ull);
+                if (in && lane == __ffs(grp) - 1) {
                     const int bk = (int)((key - lo) / width);
-                    atomicAdd(&h[bk], 1u);
+                    atomicAdd(&h[bk], (unsigned)__popc(grp));
                     atomicMin(&smn[bk], key);
                     atomicMax(&smx[bk], key);
                 }
@@ -738,6 +758,14 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
                 }
             }
             AF_TRACE(F, 2 + 2 * lvl - 1);
+#ifdef MCF_ALLOC_TRACE
+            __syncthreads();
+            if (threadIdx.x == 0 && lvl == 1) {
+                unsigned long long t_;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+                atomicMax(&F->trace[27], t_);  // last CTA done with level 1
+            }
+#endif
             grid_barrier(&F->bar, &F->flag, phase, G);
     ++phase;
             AF_TRACE(F, 2 + 2 * lvl);
@@ -850,7 +878,8 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
 // fused_scratch: caller-provided AllocFused whose first fused_scratch_zero_bytes()
 // are already zero (one memset for several scratch blocks), or null
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
-                    cudaStream_t s, void *fused_scratch = nullptr) {
+                    cudaStream_t s, void *fused_scratch = nullptr, double *r_ones = nullptr,
+                    long long *stats_zero = nullptr) {
     MCF_ARG(g && ni && walk_pre, "mcf_allocate_walks: null argument");
     MCF_ARG(n_walks >= 1, "n_walks must be at least 1");  // walker.py:168-169
     MCF_ARG(n_walks < (1ll << 53), "n_walks must be below 2^53");
@@ -869,7 +898,8 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
             MCF_CUDA(cudaMallocAsync(&F, sizeof(AllocFused), s));
             MCF_CUDA(cudaMemsetAsync(F, 0, offsetof(AllocFused, lvl), s));
         }
-        k_alloc_fused<<<G, AF_T, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, (int)K, F, ni, walk_pre, blk_col);
+        k_alloc_fused<<<G, AF_T, 0, s>>>(g->init_prob, n, (double)n_walks, n_walks, (int)K, F, ni, walk_pre, blk_col,
+                                         OnesR{g->hdr, g->vals, r_ones, stats_zero});
         mcf::note_launch();
         MCF_LAUNCHED("k_alloc_fused");
         if (own) MCF_CUDA(cudaFreeAsync(F, s));
@@ -905,8 +935,8 @@ static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *w
 }
 
 int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
-                   cudaStream_t s, void *fused_scratch) {
-    return allocate(g, n_walks, ni, walk_pre, blk_col, s, fused_scratch);
+                   cudaStream_t s, void *fused_scratch, double *r_ones, long long *stats_zero) {
+    return allocate(g, n_walks, ni, walk_pre, blk_col, s, fused_scratch, r_ones, stats_zero);
 }
 
 size_t fused_scratch_bytes() { return sizeof(AllocFused); }

@@ -1017,22 +1017,29 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     int *blk = reinterpret_cast<int *>(scratch + ctl + fb_al);
     double *xw = reinterpret_cast<double *>(scratch + ctl + fb_al + blk_bytes);
     MCF_CUDA(cudaMemsetAsync(scratch, 0, ctl + fz, s));
-    MCF_CUDA(cudaEventRecord(g->ev_fork, s));
-    MCF_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
-    int rc = allocate_walks(g, n_walks, ni, walk_pre, blk, g->side, F);
-    if (rc) return rc;
-    MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
-    if (v) {
-        MCF_CUDA(cudaMemsetAsync(stats, 0, sizeof(long long) * 4, s));
-        rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+    int rc = MCF_OK;
+    if (!v && fused) {  // v = 1: ONE kernel computes the budgets and r = A 1 (and zeroes stats)
+        rc = allocate_walks(g, n_walks, ni, walk_pre, blk, s, F, r, stats);
         if (rc) return rc;
-    } else {  // v = 1 (the same kernel zeroes the statistics)
-        k_r_ones<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, g->n, r, stats);
-        mcf::note_launch();
-        MCF_LAUNCHED("k_r_ones");
         v = V_ONES;
+    } else {  // budgets on the side stream, concurrently with r = A v
+        MCF_CUDA(cudaEventRecord(g->ev_fork, s));
+        MCF_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
+        rc = allocate_walks(g, n_walks, ni, walk_pre, blk, g->side, F);
+        if (rc) return rc;
+        MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
+        if (v) {
+            MCF_CUDA(cudaMemsetAsync(stats, 0, sizeof(long long) * 4, s));
+            rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+            if (rc) return rc;
+        } else {  // v = 1 (the same kernel zeroes the statistics)
+            k_r_ones<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, g->n, r, stats);
+            mcf::note_launch();
+            MCF_LAUNCHED("k_r_ones");
+            v = V_ONES;
+        }
+        MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     }
-    MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     mcf_walk_params pp = *p;
     pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks
     const bool lean = v == V_ONES && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);

@@ -478,7 +478,7 @@ def test_spmv_short_rows_match_sequential_csr_bitwise(mc, uniform):
 
 
 @pytest.mark.parametrize("name", ["ba400", "signed6"])
-def test_action_v_ones_row_sums(mc, name):
+def test_action_v_ones_row_sums(mc, alloc_path, name):
     """v = None (v = 1): r is the reference's A @ ones bit for bit (row sums,
     signed rows summed with their signs), and the estimate equals the one with
     an explicit ones vector (same walks; y to rounding of the hub-row sums)."""

@@ -9,8 +9,9 @@
 #include <vector>
 using namespace mcf;
 
-int main() {
-    const long long n = 1000000, nw = 640000;
+int main(int argc, char **argv) {
+    long long n = 1000000;
+    const long long nw = 640000;
     std::mt19937_64 rng(1);
     std::vector<double> p(n);
     double tot = 0;
@@ -21,6 +22,15 @@ int main() {
         tot += p[i];
     }
     for (auto &x : p) x /= tot;
+    if (argc > 1) {  // p from a file (float64, e.g. a graph's init_prob)
+        FILE *f = fopen(argv[1], "rb");
+        fseek(f, 0, SEEK_END);
+        n = ftell(f) / 8;
+        fseek(f, 0, SEEK_SET);
+        p.resize(n);
+        if (fread(p.data(), 8, n, f) != (size_t)n) return 1;
+        fclose(f);
+    }
     double *dp;
     long long *ni, *wp;
     AllocFused *F;
@@ -38,13 +48,14 @@ int main() {
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a);
-        k_alloc_fused<<<sms, AF_T>>>(dp, n, (double)nw, nw, (int)K, F, ni, wp, nullptr);
+        k_alloc_fused<<<sms, AF_T>>>(dp, n, (double)nw, nw, (int)K, F, ni, wp, nullptr, OnesR{nullptr, nullptr, nullptr, nullptr});
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         unsigned long long tr[32];
         cudaMemcpy(tr, F->trace, sizeof(tr), cudaMemcpyDeviceToHost);
+        printf("last CTA level-1 done +%.1f, ", (tr[27] - tr[0]) / 1e3);
         printf("last CTA start +%.1f, last shared hist done +%.1f, last flush done +%.1f | ", (tr[28] - tr[0]) / 1e3,
                (tr[29] - tr[0]) / 1e3, (tr[30] - tr[0]) / 1e3);
         printf("K=%lld event %.1f us | phase1 %.1f  bar1 %.1f", K, ms * 1e3, (tr[1] - tr[0]) / 1e3, (tr[2] - tr[1]) / 1e3);
