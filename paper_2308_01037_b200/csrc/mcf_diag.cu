@@ -55,6 +55,7 @@ struct QArgs {
     long long col_begin, col_end;
     double *__restrict__ pcol;
     int uniform;   // every stored value equals `value`: the combine skips csc_vals
+    int push_pct;  // push (bitmap tests) when deg(i) > push_pct/100 * |supp Q_c|
     double value;
     const unsigned long long *__restrict__ colmax;  // per-column max |weight| bits (from the walk kernel)
     int *gkeys;
@@ -143,7 +144,7 @@ __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, co
     if (a.uniform) {
         long long acc = 0;
         const int h = a.hub_of ? __ldg(a.hub_of + i) : -1;
-        if (h >= 0 && ihi - ilo > 4ll * nsupp) {  // push: the support list against i's bitmap
+        if (h >= 0 && 100 * (ihi - ilo) > (long long)a.push_pct * nsupp) {  // push: the support list against i's bitmap
             const unsigned *bits = a.hub_bits + (long long)h * a.hub_words;
             for (int t = lane; t < nsupp; t += 32) {
                 const int k = lkeys[t];
@@ -442,6 +443,10 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.hub_bits = g->hub_bits;
     q.hub_words = g->hub_words;
     q.uniform = g->uniform_value ? 1 : 0;
+    {
+        const char *e = getenv("MCF_PUSH_PCT");
+        q.push_pct = e ? atoi(e) : 100;
+    }
     q.value = g->value;
     q.colmax = colmax;
     q.gkeys = nullptr;

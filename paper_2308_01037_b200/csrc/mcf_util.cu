@@ -230,11 +230,13 @@ __global__ void k_hub_bits(const long long *__restrict__ row_ptr, const int *__r
     }
 }
 
-constexpr long long HUB_MIN_DEG = 2048;
-
 int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s) {
     if (g->hubs_ready) return MCF_OK;
     g->hubs_ready = true;
+    static const long long HUB_MIN_DEG = [] {
+        const char *e = getenv("MCF_HUB_MIN_DEG");
+        return e ? atoll(e) : 2048ll;
+    }();
     if (!g->uniform_value || g->info.max_degree < HUB_MIN_DEG) return MCF_OK;
     const char *env = getenv("MCF_HUB_BITMAP_MB");
     const long long budget = (env ? atoll(env) : 4096ll) << 20;
