@@ -414,10 +414,12 @@ def run_device(args, cfg):
                 "peak_source": peak_src, "bytes_per_step": BYTES_PER_STEP,
                 "kernel_ms_avg": walk_avg_ms, "kernel_share_of_step": (walk_ms_tot / ms) if ms else None,
                 "random_sector_ceiling_gsteps": 37.8,
-                "note": "algorithmic bytes = 64 B x emissions (row header + sampled entry, SURVEY 8d); the fat "
-                        "layout serves them with one random 32-B sector per step. Random HBM sectors top out at "
-                        "~37.8 G/s on this B200 (tools/gups, profiles/r01/gups.txt); L2-resident graphs (config 2) "
-                        "exceed it"}
+                "note": "algorithmic bytes = 64 B x emissions (row header + sampled entry, SURVEY 8d), kept for "
+                        "comparability; on uniform-value graphs the lean layout serves a step with ONE random 8-B "
+                        "entry. Random HBM reads top out at ~37.8 G/s on this B200 and each costs a 128-B line "
+                        "fill (tools/gups, profiles/r01/gups.txt): HBM-resident graphs (config 4) are bound by "
+                        "those fills (~88% of the copy peak in DRAM traffic); L2-resident ones (config 2) by the "
+                        "latency of the one dependent load, hence frac > 1 against HBM"}
     if cfg["kind"] == "diag":
         roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
 
