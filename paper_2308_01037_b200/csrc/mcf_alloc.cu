@@ -604,8 +604,8 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
         const long long j = base + 32ll * k;
         pv[k] = (k < K && j < n) ? p[j] : -1.0;  // -1: padding
     }
+    if (ones.stats && blockIdx.x == 0 && threadIdx.x < 4) ones.stats[threadIdx.x] = 0;
     if (ones.r) {  // r = A 1 for the same rows (warp-striped, coalesced header reads)
-        if (blockIdx.x == 0 && threadIdx.x < 4) ones.stats[threadIdx.x] = 0;
 #pragma unroll
         for (int k = 0; k < AF_KMAX; ++k) {
             const long long j = base + 32ll * k;

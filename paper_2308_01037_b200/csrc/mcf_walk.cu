@@ -479,14 +479,31 @@ constexpr int SPMV_WARPS = 8;
 // v == V_ONES stands for the all-ones vector (total communicability)
 #define V_ONES (reinterpret_cast<const double *>(1))
 
-__device__ __forceinline__ double combine_exact(double alpha, const double *v, double beta, const double *r,
+__device__ __forceinline__ double combine_exact(double alpha, const double *v, double beta, bool has_r, double ri,
                                                 long long i, double s) {
     // ((alpha v) + (beta r)) + s, each operation rounded: the numpy expression
     // z0 * v + z1 * r + A @ q evaluated elementwise
     double h = 0.0;
     if (v) h = v == V_ONES ? alpha : __dmul_rn(alpha, v[i]);
-    if (r) h = v ? __dadd_rn(h, __dmul_rn(beta, r[i])) : __dmul_rn(beta, r[i]);
-    return (v || r) ? __dadd_rn(h, s) : s;
+    if (has_r) h = v ? __dadd_rn(h, __dmul_rn(beta, ri)) : __dmul_rn(beta, ri);
+    return (v || has_r) ? __dadd_rn(h, s) : s;
+}
+
+// r for the combine: r[i], or (lean v = 1 path) the row sum by degree, also
+// stored to rt.out -- r = A 1 is then produced here, after the walks, instead
+// of before them.
+struct RowSumR {
+    const double *tab;  // rsum_by_deg, or null
+    double *out;
+};
+
+__device__ __forceinline__ double r_of(const double *r, const RowSumR &rt, long long i, long long deg) {
+    if (rt.tab) {
+        const double ri = __ldg(rt.tab + deg);
+        rt.out[i] = ri;
+        return ri;
+    }
+    return r ? r[i] : 0.0;
 }
 
 // r = A 1 for v = 1: the sequential CSR row sum of a_ij, which for a row
@@ -515,8 +532,10 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
                                               const double *__restrict__ v, double beta, const double *__restrict__ r,
                                               const double *__restrict__ x, double *__restrict__ y, long long row_begin,
                                               long long row_end, NodeHdr *__restrict__ aux,
-                                              const int *__restrict__ long_rows, long long n_long, int long_blocks) {
+                                              const int *__restrict__ long_rows, long long n_long, int long_blocks,
+                                              RowSumR rt) {
     __shared__ double prod[SPMV_WARPS][SEG_CAP];
+    const bool has_r = r || rt.tab;
     __shared__ double part[SPMV_WARPS];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if ((int)blockIdx.x < long_blocks) {
@@ -532,7 +551,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
                 s += __dmul_rn(UNI ? uval : __ldg(vals + e), __ldg(x + __ldg(col_ids + e)));
             s = warp_sum(s);
             if (lane == 0) {
-                const double out = combine_exact(alpha, v, beta, r, i, s);
+                const double out = combine_exact(alpha, v, beta, has_r, r_of(r, rt, i, e1 - e0), i, s);
                 y[i] = out;
                 if (aux) aux[i].aux = out;
             }
@@ -550,7 +569,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
             if (threadIdx.x < 32) {
                 const double t = warp_sum(threadIdx.x < SPMV_WARPS ? part[threadIdx.x] : 0.0);
                 if (threadIdx.x == 0) {
-                    const double out = combine_exact(alpha, v, beta, r, i, t);
+                    const double out = combine_exact(alpha, v, beta, has_r, r_of(r, rt, i, e1 - e0), i, t);
                     y[i] = out;
                     if (aux) aux[i].aux = out;
                 }
@@ -614,14 +633,14 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
         longm &= longm - 1;
     }
     if (mine) {
-        const double out = combine_exact(alpha, v, beta, r, i, s);
+        const double out = combine_exact(alpha, v, beta, has_r, r_of(r, rt, i, e1 - e0), i, s);
         y[i] = out;
         if (aux) aux[i].aux = out;
     }
 }
 
 int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,
-         long long rb, long long re, cudaStream_t s, NodeHdr *aux = nullptr) {
+         long long rb, long long re, cudaStream_t s, NodeHdr *aux = nullptr, RowSumR rt = RowSumR{nullptr, nullptr}) {
     MCF_ARG(g && x && y, "mcf_spmv: null argument");
     MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv: bad row range");
     if (re == rb) return MCF_OK;
@@ -632,10 +651,10 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
     const unsigned grid = (unsigned)(lb + sb);
     if (g->uniform_value)
         k_spmv<true><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r, x, y, rb,
-                                                      re, aux, g->long_rows, g->n_long_rows, (int)lb);
+                                                      re, aux, g->long_rows, g->n_long_rows, (int)lb, rt);
     else
         k_spmv<false><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r, x, y, rb,
-                                                       re, aux, g->long_rows, g->n_long_rows, (int)lb);
+                                                       re, aux, g->long_rows, g->n_long_rows, (int)lb, rt);
     mcf::note_launch();
     MCF_LAUNCHED("k_spmv");
     return MCF_OK;
@@ -1018,8 +1037,11 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     double *xw = reinterpret_cast<double *>(scratch + ctl + fb_al + blk_bytes);
     MCF_CUDA(cudaMemsetAsync(scratch, 0, ctl + fz, s));
     int rc = MCF_OK;
-    if (!v && fused) {  // v = 1: ONE kernel computes the budgets and r = A 1 (and zeroes stats)
-        rc = allocate_walks(g, n_walks, ni, walk_pre, blk, s, F, r, stats);
+    // v = 1 on a uniform-value graph: the lean walk needs neither r nor
+    // hdr.aux, so r = A 1 (row sums by degree) is written by the final SpMV
+    const bool lean_ones = !v && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
+    if (!v && fused) {  // v = 1: ONE kernel computes the budgets (and r = A 1 unless lean), zeroes stats
+        rc = allocate_walks(g, n_walks, ni, walk_pre, blk, s, F, lean_ones ? nullptr : r, stats);
         if (rc) return rc;
         v = V_ONES;
     } else {  // budgets on the side stream, concurrently with r = A v
@@ -1045,7 +1067,10 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     const bool lean = v == V_ONES && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
     rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk, lean, xw, counter);
     if (rc) return rc;
-    rc = spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
+    if (lean_ones && fused)
+        rc = spmv(g, z0, v, z1, nullptr, q, y, 0, g->n, s, nullptr, RowSumR{g->rsum_by_deg, r});
+    else
+        rc = spmv(g, z0, v, z1, r, q, y, 0, g->n, s);
     if (rc) return rc;
     MCF_CUDA(cudaFreeAsync(scratch, s));
     return MCF_OK;
