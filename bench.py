@@ -422,6 +422,8 @@ def run_device(args, cfg):
                         "latency of the one dependent load, hence frac > 1 against HBM"}
     if cfg["kind"] == "diag":
         roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
+    elif q_ms_tot:  # action: the span before the walks (budgets, r) recorded by mcf_funm_action
+        roofline["prewalk_ms_avg"] = q_ms_tot / max(1, args.steps)
 
     # ---- end to end through the public API (host matrix -> host result) --------------
     e2e = None

@@ -148,10 +148,9 @@ MCF_API int mcf_walk_action(mcf_graph *g, const mcf_walk_params *p, const int64_
                     double *q_var, int64_t *stats, void *stream);
 
 /* The whole RandFunmAction estimate in one call (Alg. 3, PAPER.md:337-367,
- * SPEC.md:369-377): the budgets for n_walks (-> ni[n], walk_pre[n+1], as
- * mcf_allocate_walks, computed on an internal stream concurrently with
- * r = A v), the walks of every column, q, optional q_var, and
- * y = zeta0 v + zeta1 r + A q ([dev] n each).  v may be NULL for v = 1 (total
+ * SPEC.md:369-377): the budgets for n_walks (-> walk_pre[n+1] and, unless
+ * ni is NULL, ni[n], as mcf_allocate_walks), the walks of every column, q,
+ * optional q_var, and y = zeta0 v + zeta1 r + A q ([dev] n each).  v may be NULL for v = 1 (total
  * communicability): r is then the row sums of A, bit-identical
  * to the reference's A @ ones.  q, q_var, y and stats[4] are overwritten
  * (unlike mcf_walk_action, stats need not be zeroed).  Single process (the
@@ -200,8 +199,10 @@ MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const dou
                      int64_t row_begin, int64_t row_end, void *stream);
 
 /* Device time of the kernels launched with MCF_FLAG_TIME_KERNELS since the
- * last reset: the walk kernels (action walks or diag emission walks) and the
- * diag Q-build/combine kernel, in ms, plus the number of timed walk launches.
+ * last reset: the walk kernels (action walks or diag emission walks) and, in
+ * q_ms, the diag Q-build/combine kernel -- or, for mcf_funm_action, the span
+ * before the walks (budgets and r) -- in ms, plus the number of timed walk
+ * launches.
  * Synchronises on the recorded events.  reset != 0 destroys them; reset == 0
  * keeps them, so events captured into a CUDA graph can be re-read after every
  * replay. */

@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const double *__restri
         if (j < n) {
             const long long nj = a[k] + ((b[k] && eb[k] < I) ? 1 : 0);
             const long long w0 = ea[k] + (eb[k] < I ? eb[k] : I);
-            ni[j] = nj;
+            if (ni) ni[j] = nj;
             walk_pre[j] = w0;
             if (blk_col)
                 for (long long blk = (w0 + B - 1) >> WALK_BLK_SHIFT; blk * B < w0 + nj; ++blk) blk_col[blk] = (int)j;
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
         if (j < n) {
             const long long nj = a + ((t && eb < I) ? 1 : 0);
             const long long w0 = ea + (eb < I ? eb : I);
-            ni[j] = nj;
+            if (ni) ni[j] = nj;
             walk_pre[j] = w0;
             if (blk_col)
                 for (long long blk = (w0 + B - 1) >> WALK_BLK_SHIFT; blk * B < w0 + nj; ++blk) blk_col[blk] = (int)j;
@@ -880,7 +880,7 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
 static int allocate(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,
                     cudaStream_t s, void *fused_scratch = nullptr, double *r_ones = nullptr,
                     long long *stats_zero = nullptr) {
-    MCF_ARG(g && ni && walk_pre, "mcf_allocate_walks: null argument");
+    MCF_ARG(g && walk_pre, "mcf_allocate_walks: null argument");  // ni may be null internally (not stored)
     MCF_ARG(n_walks >= 1, "n_walks must be at least 1");  // walker.py:168-169
     MCF_ARG(n_walks < (1ll << 53), "n_walks must be below 2^53");
     const long long n = g->n;
@@ -951,5 +951,9 @@ bool fused_alloc_applies(const mcf_graph *g) {
 }  // namespace mcf
 
 extern "C" int mcf_allocate_walks(mcf_graph *g, int64_t n_walks, int64_t *ni, int64_t *walk_pre, void *stream) {
+    if (!ni) {
+        mcf::set_error("mcf_allocate_walks: null argument");
+        return MCF_ERR_ARGUMENT;
+    }
     return mcf::allocate(g, (long long)n_walks, (long long *)ni, (long long *)walk_pre, nullptr, (cudaStream_t)stream);
 }

@@ -1007,7 +1007,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
 static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks, long long *ni, long long *walk_pre,
                        const double *v, double z0, double z1, double *r, double *q, double *qvar, double *y,
                        long long *stats, cudaStream_t s) {
-    MCF_ARG(g && r && q && y && ni && walk_pre, "mcf_funm_action: null argument");
+    MCF_ARG(g && r && q && y && walk_pre, "mcf_funm_action: null argument");  // ni optional
     if (!g->side) {  // one side stream per device, shared by every graph (created once)
         static std::mutex mu;
         static std::map<int, cudaStream_t> streams;
@@ -1035,8 +1035,12 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     void *F = fused ? scratch + ctl : nullptr;
     int *blk = reinterpret_cast<int *>(scratch + ctl + fb_al);
     double *xw = reinterpret_cast<double *>(scratch + ctl + fb_al + blk_bytes);
+    // MCF_FLAG_TIME_KERNELS: the span up to the walks (budgets, r) goes to the
+    // graph's second timer (mcf_graph_kernel_times' q_ms on the action path)
+    const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0;
+    int rc = timed_begin(g, timed, g->ev_q, s);
+    if (rc) return rc;
     MCF_CUDA(cudaMemsetAsync(scratch, 0, ctl + fz, s));
-    int rc = MCF_OK;
     // v = 1 on a uniform-value graph: the lean walk needs neither r nor
     // hdr.aux, so r = A 1 (row sums by degree) is written by the final SpMV
     const bool lean_ones = !v && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
@@ -1062,6 +1066,8 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
         }
         MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     }
+    rc = timed_end(timed, g->ev_q, s);
+    if (rc) return rc;
     mcf_walk_params pp = *p;
     pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks
     const bool lean = v == V_ONES && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);

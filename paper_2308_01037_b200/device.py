@@ -254,11 +254,12 @@ class DeviceGraph:
                                         _ptr(q), _ptr(qvar), _ptr(stats), self.stream), "mcf_walk_action")
 
     def funm_action(self, params: WalkParams, n_walks: int, v, z0, z1, r, q, y, qvar=None, stats=None,
-                    ni=None, walk_pre=None):
+                    ni=None, walk_pre=None, want_ni: bool = True):
         """Whole single-process RandFunmAction pass in one library call: the
-        budgets for n_walks (computed concurrently with r = A v), walks, q and
-        y.  Returns (y, ni, walk_pre)."""
-        ni = torch.empty(self.n, dtype=torch.int64, device=self.device) if ni is None else ni
+        budgets for n_walks, r = A v (v None: v = 1), walks, q and y.  Returns
+        (y, ni, walk_pre); ni is None when want_ni is False (not stored)."""
+        if ni is None and want_ni:
+            ni = torch.empty(self.n, dtype=torch.int64, device=self.device)
         walk_pre = torch.empty(self.n + 1, dtype=torch.int64, device=self.device) if walk_pre is None else walk_pre
         N.check(N.lib().mcf_funm_action(self.handle, C.byref(params.c), int(n_walks), _ptr(ni), _ptr(walk_pre),
                                         _ptr(v), float(z0), float(z1), _ptr(r), _ptr(q), _ptr(qvar), _ptr(y),

@@ -71,7 +71,7 @@ def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=No
         q = torch.empty(g.n, dtype=torch.float64, device=g.device)
         r, y = torch.empty_like(q), torch.empty_like(q)
         st = torch.empty(N.MCF_STATS_LEN, dtype=torch.int64, device=g.device)
-        return g.funm_action(params, cfg.n_walks, v, z[0], z[1], r, q, y, stats=st)[0], st
+        return g.funm_action(params, cfg.n_walks, v, z[0], z[1], r, q, y, stats=st, want_ni=False)[0], st
     if v is None:
         v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
