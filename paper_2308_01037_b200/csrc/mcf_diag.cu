@@ -38,6 +38,7 @@ constexpr int Q_WARPS = Q_THREADS / 32;
 constexpr int SCAP = 16384;  // shared table slots: 16384 * (4 + 8) B = 192 KB
 constexpr int FILTER_WORDS = 8192;  // 32 KB Bloom filter (262144 bits) in front of every combine lookup
 constexpr int EMPTY_KEY = -1;
+constexpr int DENSE_N = SCAP * 12 / 8;  // node ids a dense Q_c covers in the table's shared memory (24576)
 
 struct QArgs {
     const long long *__restrict__ walk_pre;
@@ -117,6 +118,7 @@ __device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key)
 }
 
 __device__ __forceinline__ long long lookup(const int *keys, const long long *vals, uint32_t mask, int key) {
+    if (!keys) return vals[key];  // dense table (small graphs): Q_c indexed by node id
     uint32_t s = hash_slot(key, mask);
     while (true) {
         int k = keys[s];
@@ -212,7 +214,14 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         while ((long long)cap * 3 < need * 4 + 4) cap <<= 1;                 // and <= 3/4 always
         int *keys;
         long long *vals;
-        if (cap <= (uint32_t)SCAP) {
+        // small graphs (n <= DENSE_N): Q_c is a dense shared array indexed by
+        // node id -- no hashing, no probing (keys == nullptr marks it)
+        const bool dense = a.n <= DENSE_N && need * 4 > a.n;
+        if (dense) {
+            cap = (uint32_t)a.n;
+            keys = nullptr;
+            vals = svals;
+        } else if (cap <= (uint32_t)SCAP) {
             keys = skeys;
             vals = svals;
         } else {
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         }
         const uint32_t mask = cap - 1;
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
-            keys[t] = EMPTY_KEY;
+            if (keys) keys[t] = EMPTY_KEY;
             vals[t] = 0;
         }
         __syncthreads();
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             for (int u = 0; u < U; ++u) {
                 if (sv[u] < 0) continue;
                 const long long q = __double2ll_rn(ldexp(wv[u], E));
-                const int slot = find_or_insert(keys, mask, sv[u]);
+                const int slot = keys ? find_or_insert(keys, mask, sv[u]) : sv[u];
                 atomicAdd(reinterpret_cast<unsigned long long *>(&vals[slot]), (unsigned long long)q);
             }
         }
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         int *lkeys = a.lkeys + (long long)blockIdx.x * a.lcap;
         long long *lvals = a.lvals + (long long)blockIdx.x * a.lcap;
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
-            const int key = keys[t];
+            const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
             if (key != EMPTY_KEY) {
                 const uint32_t b = filter_bit(key);
                 atomicOr(&filt[b >> 5], 1u << (b & 31));
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         __syncthreads();
         if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_work), (unsigned long long)work);
         __syncthreads();
-        if (s_work > BIG_WORK && a.big) {
+        if (s_work > BIG_WORK && a.big && keys) {
             // hand Q_c to k_diag_big: all warps of the GPU share the combine
             if (tid == 0) {
                 s_slot = -1;
