@@ -47,6 +47,7 @@ struct WalkCommon {
     long long *stats;
     int *err;
     const uint2 *__restrict__ lean;         // v = 1 on uniform-value graphs (else null)
+    const long long *__restrict__ row_ptr;  // lean walks: start state of a column
     const double *__restrict__ rsum_by_deg;
     // L2 bulk prefetch of the walk tables at kernel start (bytes 0: none)
     const char *pf[3];
@@ -139,7 +140,7 @@ __device__ __forceinline__ WarpPool make_pool(int nw_total) {
     return WarpPool{0, 0, c & ~31};
 }
 
-template <bool REPLAY>
+template <bool REPLAY, bool LEAN = false>
 __device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, int nw, Lane &L, unsigned &n_walks,
                                        WarpPool &P) {
     const unsigned need = __ballot_sync(MCF_FULL, L.rel == -1);
@@ -168,7 +169,16 @@ __device__ __forceinline__ bool refill(const WalkCommon &a, long long wb, int nw
                 L.c = c;
                 L.wl = (unsigned)(g - pre);
                 L.k = 0;
-                L.h = load_hdr(a.hdr + c);
+                if (LEAN) {  // start state from row_ptr (8 B per node, column-contiguous) and the degree table
+                    const long long rs = __ldg(a.row_ptr + c), re = __ldg(a.row_ptr + c + 1);
+                    L.h.start = (int)rs;
+                    L.h.deg = (int)(re - rs);
+                    L.h.flags = HDR_UNIFORM;
+                    L.h.rsum = __ldg(a.rsum_by_deg + (re - rs));
+                    L.h.aux = L.h.rsum;
+                } else {
+                    L.h = load_hdr(a.hdr + c);
+                }
                 L.h.pad = (uint32_t)c;
                 L.w = 1.0 / (double)nc;       // W0 = 1/N_c (walker.py:263)
                 L.thr = a.cutoff * L.w;       // strict cutoff W_c * W0 (walker.py:264)
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
     while (true) {
         bool more = false;
 #pragma unroll
-        for (int s = 0; s < NW; ++s) more |= refill<REPLAY>(a, wb, nw, L[s], n_walks, P);
+        for (int s = 0; s < NW; ++s) more |= refill<REPLAY, LEAN>(a, wb, nw, L[s], n_walks, P);
         if (!more) break;
         long long e[NW];
         NodeHdr nh[NW];
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long 
     unsigned n_walks = 0, em = 0, tr = 0, ab = 0;
     long long sb = 0, scap = 0, stride = 1;
     double wmax = 0.0;  // this walk's largest |emission| -> per-column max (fixed-point scale of k_diag_q)
-    while (refill<REPLAY>(a, wb, nw, L, n_walks, P)) {
+    while (refill<REPLAY, LEAN>(a, wb, nw, L, n_walks, P)) {
         if (L.rel < 0) continue;
         const long long rel = L.rel;
         if (L.k == 0) {
@@ -706,6 +716,7 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.colmax = nullptr;
     a.lean = nullptr;
     a.rsum_by_deg = nullptr;
+    a.row_ptr = (const long long *)g->row_ptr;
     a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
     for (int k = 0; k < 3; ++k) {
         a.pf[k] = nullptr;
