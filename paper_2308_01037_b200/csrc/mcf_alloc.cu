@@ -487,7 +487,8 @@ __global__ void __launch_bounds__(SCAN_T, 2) k_alloc_scan(const double *__restri
 // SM, so every CTA is resident and the spin barriers cannot deadlock.
 // ---------------------------------------------------------------------------
 constexpr int AF_T = 1024, AF_W = AF_T / 32, AF_KMAX = 8, AF_LEVELS = 8, AF_MAXG = 1024;
-constexpr int AF_REP = 8;  // replicas of the merged histograms: CTA c adds into copy c % 8 (8x less contention)
+constexpr int AF_REP = 8;    // replicas of the merged level-0 counts: CTA c adds into copy c % 8
+constexpr int AF_REP_L = 8;  // replicas of the refinement levels
 
 struct AllocFused {
     // ---- zeroed by the host (cudaMemsetAsync up to `lvl`)
@@ -499,8 +500,8 @@ struct AllocFused {
     unsigned long long trace[32];    // MCF_ALLOC_TRACE builds: CTA 0 phase timestamps
     // ---- refinement levels, zeroed by the CTAs during phase 1 (first used after barrier 1)
     struct Level {
-        unsigned cnt[AF_REP][NBUCKET];
-        unsigned long long nmin[AF_REP][NBUCKET], max[AF_REP][NBUCKET];  // ~min, max key per bin
+        unsigned cnt[AF_REP_L][NBUCKET];
+        unsigned long long nmin[AF_REP_L][NBUCKET], max[AF_REP_L][NBUCKET];  // ~min, max key per bin
     } lvl[AF_LEVELS];
     long long blk_a[AF_MAXG], blk_b[AF_MAXG];  // written before they are read
 };
@@ -544,6 +545,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned *flag, unsi
 
 // 1024 bins, one per thread, searched from the top: the bin with
 // count(above) < R <= count(above) + count(bin).  Every thread gets the answer.
+template <int REP>
 __device__ __forceinline__ void find_bin_all(const unsigned (*cnt)[NBUCKET], long long R, int &bin, long long &need) {
     __shared__ long long wt[AF_W];
     __shared__ int s_bin;
@@ -552,7 +554,7 @@ __device__ __forceinline__ void find_bin_all(const unsigned (*cnt)[NBUCKET], lon
     const int b = NBUCKET - 1 - t;
     long long c = 0;
 #pragma unroll
-    for (int r = 0; r < AF_REP; ++r) c += (long long)__ldcg(cnt[r] + b);
+    for (int r = 0; r < REP; ++r) c += (long long)__ldcg(cnt[r] + b);
     const long long inc = warp_incl_scan(c);
     if (lane == 31) wt[w] = inc;
     if (t == 0) s_bin = -1;
@@ -717,7 +719,7 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
     } else if (R > 0) {
         int bin;
         long long need;
-        find_bin_all(F->cnt0, R, bin, need);
+        find_bin_all<AF_REP>(F->cnt0, R, bin, need);
         // bucket b holds the remainders in [b/1024, (b+1)/1024) (exact: the
         // scaling by 1024 is a power of two), i.e. these keys:
         unsigned long long lo = (unsigned long long)__double_as_longlong((double)bin / NBUCKET) + 1ull;
@@ -730,6 +732,11 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
                 smx[b] = 0;
             }
             __syncthreads();
+            // tied keys are the common case here: a warp counts a run of one key
+            // in registers and updates shared memory once per run (every warp
+            // hitting the same three shared words per item serialised the CTA)
+            unsigned long long run_key = 0;
+            unsigned run_cnt = 0;
 #pragma unroll
             for (int k = 0; k < AF_KMAX; ++k) {
                 if (k >= K) break;
@@ -737,21 +744,41 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
                 unsigned long long key = 0;
                 if (pv[k] > 0.0) floor_key(pv[k], total, got, key);
                 const bool in = key && key >= lo && key <= hi;
-                if (!__any_sync(MCF_FULL, in)) continue;
-                // tied keys are the common case here: one shared-memory update per
-                // group of equal keys in the warp (no same-address serialisation)
-                const unsigned grp = __match_any_sync(MCF_FULL, in ? key : 0ull);
-                if (in && lane == __ffs(grp) - 1) {
-                    const int bk = (int)((key - lo) / width);
-                    atomicAdd(&h[bk], (unsigned)__popc(grp));
-                    atomicMin(&smn[bk], key);
-                    atomicMax(&smx[bk], key);
+                const unsigned m = __ballot_sync(MCF_FULL, in);
+                if (!m) continue;
+                const unsigned long long k0 = __shfl_sync(MCF_FULL, key, __ffs(m) - 1);
+                if (__all_sync(MCF_FULL, !in || key == k0)) {
+                    if (k0 != run_key) {
+                        if (run_cnt && lane == 0) {
+                            const int bk = (int)((run_key - lo) / width);
+                            atomicAdd(&h[bk], run_cnt);
+                            atomicMin(&smn[bk], run_key);
+                            atomicMax(&smx[bk], run_key);
+                        }
+                        run_key = k0;
+                        run_cnt = 0;
+                    }
+                    run_cnt += __popc(m);
+                } else {
+                    const unsigned grp = __match_any_sync(MCF_FULL, in ? key : 0ull);
+                    if (in && lane == __ffs(grp) - 1) {
+                        const int bk = (int)((key - lo) / width);
+                        atomicAdd(&h[bk], (unsigned)__popc(grp));
+                        atomicMin(&smn[bk], key);
+                        atomicMax(&smx[bk], key);
+                    }
                 }
+            }
+            if (run_cnt && lane == 0) {
+                const int bk = (int)((run_key - lo) / width);
+                atomicAdd(&h[bk], run_cnt);
+                atomicMin(&smn[bk], run_key);
+                atomicMax(&smx[bk], run_key);
             }
             __syncthreads();
             for (int b = threadIdx.x; b < NBUCKET; b += AF_T) {
                 if (h[b]) {
-                    const int rep = blockIdx.x % AF_REP;
+                    const int rep = blockIdx.x % AF_REP_L;
                     atomicAdd(&F->lvl[lvl].cnt[rep][b], h[b]);
                     atomicMax(&F->lvl[lvl].nmin[rep][b], ~smn[b]);
                     atomicMax(&F->lvl[lvl].max[rep][b], smx[b]);
@@ -769,10 +796,10 @@ __global__ void __launch_bounds__(AF_T, 1) k_alloc_fused(const double *__restric
             grid_barrier(&F->bar, &F->flag, phase, G);
     ++phase;
             AF_TRACE(F, 2 + 2 * lvl);
-            find_bin_all(F->lvl[lvl].cnt, need, bin, need);
+            find_bin_all<AF_REP_L>(F->lvl[lvl].cnt, need, bin, need);
             unsigned long long nmn = 0, mx = 0;
 #pragma unroll
-            for (int r = 0; r < AF_REP; ++r) {
+            for (int r = 0; r < AF_REP_L; ++r) {
                 const unsigned long long a = __ldcg(&F->lvl[lvl].nmin[r][bin]), b = __ldcg(&F->lvl[lvl].max[r][bin]);
                 nmn = a > nmn ? a : nmn;
                 mx = b > mx ? b : mx;
