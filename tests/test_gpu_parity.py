@@ -561,3 +561,34 @@ def test_lean_diag_bitwise(mc, name):
     ref = out["0", "compact"]
     for k, v in out.items():
         assert np.array_equal(v[0], ref[0]) and v[1:] == ref[1:], k
+
+
+def test_lean_walk_absorbing_and_self_loops(mc):
+    """Uniform-value directed graph with sink rows (absorbing) and self loops:
+    the lean walk (action v = 1 and diag) matches the header walk bitwise."""
+    import os
+    rng = np.random.default_rng(3)
+    n = 500
+    rows = rng.integers(0, n, 3000)
+    cols = rng.integers(0, n, 3000)
+    keep = rows % 7 != 0                     # every 7th row is a sink
+    rows, cols = np.r_[rows[keep], np.arange(0, n, 11)], np.r_[cols[keep], np.arange(0, n, 11)]  # + self loops
+    m = sparse.coo_array((np.full(rows.size, 0.3), (rows, cols)), shape=(n, n)).tocsr()
+    m.sum_duplicates()
+    m.data[:] = 0.3
+    m.sort_indices()
+    a = as_matrix(port.Csr.from_any(m))
+    out = {}
+    for lean in ("1", "0"):
+        os.environ["MCF_LEAN_WALK"] = lean
+        try:
+            g = mc.DeviceGraph(a, gamma=0.5)
+            cfg = mc.WalkConfig(20 * n, 1e-6, 40, 9)
+            ya = mc.rand_funm_action(g, mc.EXPONENTIAL, None, cfg)
+            yd = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg)
+            out[lean] = (np.asarray(ya.values), ya.emissions, ya.absorbed, np.asarray(yd.values), yd.emissions)
+        finally:
+            os.environ.pop("MCF_LEAN_WALK", None)
+    assert out["1"][2] > 0  # some walks were absorbed
+    for x, y in zip(out["1"], out["0"]):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
