@@ -97,6 +97,7 @@ struct mcf_graph {
     // factor, and for v = 1 also the payload r -- depends only on its degree
     // (rsum_by_deg), so a step is ONE dependent random 8-B load.  Built lazily.
     uint2 *lean = nullptr;
+    uint32_t *lean4 = nullptr;       // 4-B variant for nnz < 2^25 (used instead of lean when built)
     double *rsum_by_deg = nullptr;   // max_degree + 1
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;

@@ -47,6 +47,7 @@ struct WalkCommon {
     long long *stats;
     int *err;
     const uint2 *__restrict__ lean;         // v = 1 on uniform-value graphs (else null)
+    const uint32_t *__restrict__ lean4;     // compact 4-B variant (nnz < 2^25), preferred when built
     const long long *__restrict__ row_ptr;  // lean walks: start state of a column
     const double *__restrict__ rsum_by_deg;
     // L2 bulk prefetch of the walk tables at kernel start (bytes 0: none)
@@ -242,14 +243,26 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned
 template <bool FAT, bool LEAN = false, bool WITH_ID = false>
 __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) {
     if (LEAN) {  // {start, degree} of the target; |a| row sum (= r for v = 1) by degree
-        const uint2 t = __ldg(a.lean + e);
         NodeHdr h;
-        h.start = (int)t.x;
-        h.deg = (int)t.y;
+        if (a.lean4) {  // 4-B entries: [0 | deg:6 | start:25], or [1 | target id] for degree >= 63
+            const uint32_t t = __ldg(a.lean4 + e);
+            if (t & 0x80000000u) {
+                const long long s0 = __ldg(a.row_ptr + (t & 0x7fffffffu)), s1 = __ldg(a.row_ptr + (t & 0x7fffffffu) + 1);
+                h.start = (int)s0;
+                h.deg = (int)(s1 - s0);
+            } else {
+                h.start = (int)(t & 0x1ffffffu);
+                h.deg = (int)((t >> 25) & 63u);
+            }
+        } else {
+            const uint2 t = __ldg(a.lean + e);
+            h.start = (int)t.x;
+            h.deg = (int)t.y;
+        }
         h.flags = HDR_UNIFORM;
         // the target id (diag emissions): same index, loaded alongside, off the chain
         h.pad = WITH_ID ? (uint32_t)(__ldg(a.ecol + e) & 0x7fffffff) : 0u;
-        h.rsum = __ldg(a.rsum_by_deg + t.y);
+        h.rsum = __ldg(a.rsum_by_deg + h.deg);
         h.aux = h.rsum;
         return h;
     }
@@ -715,6 +728,7 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.entries = nullptr;
     a.colmax = nullptr;
     a.lean = nullptr;
+    a.lean4 = nullptr;
     a.rsum_by_deg = nullptr;
     a.row_ptr = (const long long *)g->row_ptr;
     a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
@@ -806,6 +820,18 @@ __global__ void k_build_lean(const long long *__restrict__ row_ptr, const int *_
     lean[e] = make_uint2((unsigned)s0, (unsigned)(s1 - s0));
 }
 
+// lean4[e]: [0 | degree:6 | start:25] of col[e] when the degree is below 63,
+// else [1 | col[e]] (the walk then reads row_ptr): half the bytes of lean[]
+// for graphs with nnz < 2^25, so the table stays L2-resident far longer
+__global__ void k_build_lean4(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids, long long nnz,
+                              uint32_t *__restrict__ lean4) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int c = col_ids[e];
+    const long long s0 = row_ptr[c], d = row_ptr[c + 1] - s0;
+    lean4[e] = d < 63 ? ((uint32_t)d << 25) | (uint32_t)s0 : 0x80000000u | (uint32_t)c;
+}
+
 // rsum_by_deg[deg(i)] = rsum(i): with every |a| equal, rows of equal degree add
 // the same values in the same order, so every writer stores the same bits
 __global__ void k_rsum_by_deg(const NodeHdr *__restrict__ hdr, long long n, double *__restrict__ tab) {
@@ -822,19 +848,28 @@ static bool lean_eligible(const mcf_graph *g) {
 }
 
 static int ensure_lean(mcf_graph *g, cudaStream_t s) {
-    if (g->lean) return MCF_OK;
-    uint2 *lean = nullptr;
+    if (g->lean || g->lean4) return MCF_OK;
     double *tab = nullptr;
-    MCF_CUDA(cudaMallocAsync(&lean, sizeof(uint2) * g->nnz, s));
     MCF_CUDA(cudaMallocAsync(&tab, sizeof(double) * (g->info.max_degree + 1), s));
     MCF_CUDA(cudaMemsetAsync(tab, 0, sizeof(double) * (g->info.max_degree + 1), s));
-    k_build_lean<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->nnz,
-                                                                  lean);
+    const char *env = getenv("MCF_LEAN4");
+    if (g->nnz < (1ll << 25) && !(env && !strcmp(env, "0"))) {
+        uint32_t *lean4 = nullptr;
+        MCF_CUDA(cudaMallocAsync(&lean4, sizeof(uint32_t) * g->nnz, s));
+        k_build_lean4<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids,
+                                                                        g->nnz, lean4);
+        g->lean4 = lean4;
+    } else {
+        uint2 *lean = nullptr;
+        MCF_CUDA(cudaMallocAsync(&lean, sizeof(uint2) * g->nnz, s));
+        k_build_lean<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids,
+                                                                      g->nnz, lean);
+        g->lean = lean;
+    }
     mcf::note_launch();
     k_rsum_by_deg<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->n, tab);
     mcf::note_launch();
     MCF_LAUNCHED("k_build_lean");
-    g->lean = lean;
     g->rsum_by_deg = tab;
     return MCF_OK;
 }
@@ -866,6 +901,7 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
         rc = ensure_lean(g, s);
         if (rc) return rc;
         a.lean = g->lean;
+        a.lean4 = g->lean4;
         a.rsum_by_deg = g->rsum_by_deg;
         for (int k = 0; k < 3; ++k) a.pf_bytes[k] = 0;
         switch (mode) {
@@ -935,6 +971,7 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
         rc = ensure_lean(g, s);
         if (rc) return rc;
         a.lean = g->lean;
+        a.lean4 = g->lean4;
         a.rsum_by_deg = g->rsum_by_deg;
         for (int k = 0; k < 3; ++k) a.pf_bytes[k] = 0;  // the L2 prefetch covers the compact tables only
     } else if (g->went) {

@@ -513,8 +513,17 @@ def test_device_col_norm_beyond_leaf_cap(mc):
     assert np.array_equal(d["row_abs_sum"], t.rsum)
 
 
+@pytest.fixture(params=["4", "8"])
+def lean_bytes(request):
+    """Both lean entry formats: 4-B packed (nnz < 2^25, degree < 63 inline) and 8-B."""
+    import os
+    os.environ["MCF_LEAN4"] = "1" if request.param == "4" else "0"
+    yield request.param
+    os.environ.pop("MCF_LEAN4", None)
+
+
 @pytest.mark.parametrize("name", ["ba400", "er300", "kron8"])
-def test_lean_walk_bitwise(mc, name):
+def test_lean_walk_bitwise(mc, lean_bytes, name):
     """v = 1 on a uniform-value graph walks {start, degree} entries with the
     row sums by degree (one dependent load per step): q and y are bitwise the
     ones of the header walk (MCF_LEAN_WALK=0), fat and compact layouts."""
@@ -540,7 +549,7 @@ def test_lean_walk_bitwise(mc, name):
 
 
 @pytest.mark.parametrize("name", ["ba400", "er300", "kron8"])
-def test_lean_diag_bitwise(mc, name):
+def test_lean_diag_bitwise(mc, lean_bytes, name):
     """Diag walks on a uniform-value graph use the {start, degree} entries
     with the id read alongside: d is bitwise the header walk's (both layouts)."""
     import os
@@ -563,7 +572,7 @@ def test_lean_diag_bitwise(mc, name):
         assert np.array_equal(v[0], ref[0]) and v[1:] == ref[1:], k
 
 
-def test_lean_walk_absorbing_and_self_loops(mc):
+def test_lean_walk_absorbing_and_self_loops(mc, lean_bytes):
     """Uniform-value directed graph with sink rows (absorbing) and self loops:
     the lean walk (action v = 1 and diag) matches the header walk bitwise."""
     import os
