@@ -135,6 +135,26 @@ MCF_API int mcf_allocate_walks(mcf_graph *g, int64_t n_walks, int64_t *ni, int64
 MCF_API int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
              const double *x, double *y, int64_t row_begin, int64_t row_end, void *stream);
 
+/* Multi-GPU Alg. 3 combine with the exchange folded in (one process per GPU,
+ * one node; replaces all-gather(q) + SpMV + all-gather(y), PAPER.md:362 and
+ * SURVEY.md 8(e)): y = alpha v + beta r + A x over rows [row_begin, row_end),
+ * gathering x[j] from x_parts[k] for part_bounds[k] <= j < part_bounds[k+1]
+ * (each rank's q buffer, mapped with mcf_peer_open) and storing every row to
+ * all n_outs buffers y_outs[k] (every rank's y).  1 <= n_parts, n_outs <= 8;
+ * pointer arrays are host memory, the buffers device (local or peer). */
+MCF_API int mcf_spmv_peer(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
+                          const double *const *x_parts, const int64_t *part_bounds, int n_parts,
+                          double *const *y_outs, int n_outs, int64_t row_begin, int64_t row_end, void *stream);
+
+/* Peer buffers: cudaMalloc'd, zero-filled, exported as a 64-byte CUDA IPC
+ * handle (mcf_peer_alloc); another process on the node maps it with
+ * mcf_peer_open and unmaps with mcf_peer_close; the owner frees it with
+ * mcf_peer_free. */
+MCF_API int mcf_peer_alloc(int64_t bytes, void **ptr, void *ipc_handle);
+MCF_API int mcf_peer_open(const void *ipc_handle, void **ptr);
+MCF_API int mcf_peer_close(void *ptr);
+MCF_API int mcf_peer_free(void *ptr);
+
 /* Action walks (Alg. 3 inner loops): for
  * every column c in [col_begin, col_end) run N_c = walk_pre[c+1]-walk_pre[c]
  * walks with W0 = 1/N_c and write

@@ -50,6 +50,11 @@ SIGNATURES = {
     "mcf_graph_tables": (C.c_int, [P, P, P, P, P]),
     "mcf_allocate_walks": (C.c_int, [P, I64, P, P, P]),
     "mcf_spmv": (C.c_int, [P, C.c_double, P, C.c_double, P, P, P, I64, I64, P]),
+    "mcf_spmv_peer": (C.c_int, [P, C.c_double, P, C.c_double, P, P, P, C.c_int, P, C.c_int, I64, I64, P]),
+    "mcf_peer_alloc": (C.c_int, [I64, C.POINTER(P), P]),
+    "mcf_peer_open": (C.c_int, [P, C.POINTER(P)]),
+    "mcf_peer_close": (C.c_int, [P]),
+    "mcf_peer_free": (C.c_int, [P]),
     "mcf_walk_action": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P, P, P]),
     "mcf_funm_action": (C.c_int, [P, C.POINTER(McfWalkParams), C.c_int64, P, P, P, C.c_double, C.c_double, P, P, P, P, P, P]),
     "mcf_replay_action": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P, P, P, P]),

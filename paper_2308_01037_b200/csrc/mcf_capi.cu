@@ -1,4 +1,6 @@
 // C ABI entry points that are not tied to one kernel family.
+#include <cstring>
+
 #include "mcf_internal.cuh"
 
 namespace mcf {
@@ -46,6 +48,48 @@ int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t 
     if (walk_ms) *walk_ms = w;
     if (q_ms) *q_ms = q;
     return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Peer buffers for the multi-GPU exchange (one process per GPU, one node):
+// plain cudaMalloc allocations whose CUDA IPC handles the ranks swap (through
+// torch.distributed), so mcf_spmv_peer can read q from, and write y into,
+// the other ranks' memory over NVLink.
+// ---------------------------------------------------------------------------
+int mcf_peer_alloc(int64_t bytes, void **ptr, void *ipc_handle) {
+    if (!ptr || !ipc_handle || bytes <= 0) {
+        mcf::set_error("mcf_peer_alloc: bad argument");
+        return MCF_ERR_ARGUMENT;
+    }
+    cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMemset(*ptr, 0, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(ipc_handle), *ptr);
+    if (e != cudaSuccess) return mcf::cuda_status(e, "mcf_peer_alloc");
+    return MCF_OK;
+}
+
+int mcf_peer_open(const void *ipc_handle, void **ptr) {
+    if (!ptr || !ipc_handle) {
+        mcf::set_error("mcf_peer_open: bad argument");
+        return MCF_ERR_ARGUMENT;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return mcf::cuda_status(e, "mcf_peer_open");
+    return MCF_OK;
+}
+
+int mcf_peer_close(void *ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    if (e != cudaSuccess) return mcf::cuda_status(e, "mcf_peer_close");
+    return MCF_OK;
+}
+
+int mcf_peer_free(void *ptr) {
+    cudaError_t e = cudaFree(ptr);
+    if (e != cudaSuccess) return mcf::cuda_status(e, "mcf_peer_free");
+    return MCF_OK;
 }
 
 }  // extern "C"

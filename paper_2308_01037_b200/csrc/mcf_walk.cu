@@ -549,14 +549,45 @@ __global__ void k_r_ones(NodeHdr *__restrict__ hdr, const double *__restrict__ v
     hdr[i].aux = s;
 }
 
-template <bool UNI>
+// Multi-GPU action without a separate collective (mcf_spmv_peer): x (= q) is
+// gathered straight from the rank that owns each column -- its buffer mapped
+// into this process over NVLink (CUDA IPC) -- and every result row is stored
+// to every rank's y buffer, so the SpMV itself is the exchange.
+constexpr int MAX_PEERS = 8;
+struct PeerArgs {
+    const double *x[MAX_PEERS];       // x[k]: valid on [bounds[k], bounds[k+1])
+    long long bounds[MAX_PEERS + 1];
+    int nparts;
+    double *y[MAX_PEERS];             // every output buffer receives every row
+    int nouts;
+};
+
+template <bool PEER>
+__device__ __forceinline__ double xload(const double *__restrict__ x, const PeerArgs &pa, int c) {
+    if (!PEER) return __ldg(x + c);
+    int k = 0;
+#pragma unroll
+    for (int t = 1; t < MAX_PEERS; ++t) k += (t < pa.nparts && c >= pa.bounds[t]) ? 1 : 0;
+    return __ldg(pa.x[k] + c);
+}
+
+template <bool PEER>
+__device__ __forceinline__ void ystore(double *__restrict__ y, const PeerArgs &pa, long long i, double out) {
+    if (!PEER) {
+        y[i] = out;
+        return;
+    }
+    for (int k = 0; k < pa.nouts; ++k) pa.y[k][i] = out;
+}
+
+template <bool UNI, bool PEER = false>
 __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
                                               const double *__restrict__ vals, double uval, double alpha,
                                               const double *__restrict__ v, double beta, const double *__restrict__ r,
                                               const double *__restrict__ x, double *__restrict__ y, long long row_begin,
                                               long long row_end, NodeHdr *__restrict__ aux,
                                               const int *__restrict__ long_rows, long long n_long, int long_blocks,
-                                              RowSumR rt) {
+                                              RowSumR rt, PeerArgs pa) {
     __shared__ double prod[SPMV_WARPS][SEG_CAP];
     const bool has_r = r || rt.tab;
     __shared__ double part[SPMV_WARPS];
@@ -571,11 +602,11 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
             if (i < row_begin || i >= row_end || e1 - e0 > HUGE_ROW) continue;
             double s = 0.0;
             for (long long e = e0 + lane; e < e1; e += 32)
-                s += __dmul_rn(UNI ? uval : __ldg(vals + e), __ldg(x + __ldg(col_ids + e)));
+                s += __dmul_rn(UNI ? uval : __ldg(vals + e), xload<PEER>(x, pa, __ldg(col_ids + e)));
             s = warp_sum(s);
             if (lane == 0) {
                 const double out = combine_exact(alpha, v, beta, has_r, r_of(r, rt, i, e1 - e0), i, s);
-                y[i] = out;
+                ystore<PEER>(y, pa, i, out);
                 if (aux) aux[i].aux = out;
             }
         }
@@ -585,7 +616,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
             if (i < row_begin || i >= row_end || e1 - e0 <= HUGE_ROW) continue;
             double s = 0.0;
             for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-                s += __dmul_rn(UNI ? uval : __ldg(vals + e), __ldg(x + __ldg(col_ids + e)));
+                s += __dmul_rn(UNI ? uval : __ldg(vals + e), xload<PEER>(x, pa, __ldg(col_ids + e)));
             s = warp_sum(s);
             if (lane == 0) part[w] = s;
             __syncthreads();
@@ -593,7 +624,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
                 const double t = warp_sum(threadIdx.x < SPMV_WARPS ? part[threadIdx.x] : 0.0);
                 if (threadIdx.x == 0) {
                     const double out = combine_exact(alpha, v, beta, has_r, r_of(r, rt, i, e1 - e0), i, t);
-                    y[i] = out;
+                    ystore<PEER>(y, pa, i, out);
                     if (aux) aux[i].aux = out;
                 }
             }
@@ -641,7 +672,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
 #pragma unroll
                 for (int k = 0; k < SEG_CAP / 32; ++k) {
                     const int t = lane + 32 * k;
-                    if (t < cnt) prod[w][t] = __dmul_rn(av[k], __ldg(x + c[k]));
+                    if (t < cnt) prod[w][t] = __dmul_rn(av[k], xload<PEER>(x, pa, c[k]));
                 }
                 __syncwarp();
                 if (member) {
@@ -657,7 +688,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
     }
     if (mine) {
         const double out = combine_exact(alpha, v, beta, has_r, r_of(r, rt, i, e1 - e0), i, s);
-        y[i] = out;
+        ystore<PEER>(y, pa, i, out);
         if (aux) aux[i].aux = out;
     }
 }
@@ -674,12 +705,52 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
     const unsigned grid = (unsigned)(lb + sb);
     if (g->uniform_value)
         k_spmv<true><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r, x, y, rb,
-                                                      re, aux, g->long_rows, g->n_long_rows, (int)lb, rt);
+                                                      re, aux, g->long_rows, g->n_long_rows, (int)lb, rt, PeerArgs{});
     else
         k_spmv<false><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r, x, y, rb,
-                                                       re, aux, g->long_rows, g->n_long_rows, (int)lb, rt);
+                                                       re, aux, g->long_rows, g->n_long_rows, (int)lb, rt, PeerArgs{});
     mcf::note_launch();
     MCF_LAUNCHED("k_spmv");
+    return MCF_OK;
+}
+
+int spmv_peer(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
+              const double *const *x_parts, const long long *bounds, int nparts, double *const *y_outs, int nouts,
+              long long rb, long long re, cudaStream_t s) {
+    MCF_ARG(g && x_parts && bounds && y_outs, "mcf_spmv_peer: null argument");
+    MCF_ARG(nparts >= 1 && nparts <= MAX_PEERS && nouts >= 1 && nouts <= MAX_PEERS, "mcf_spmv_peer: 1..8 parts and outputs");
+    MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv_peer: bad row range");
+    MCF_ARG(bounds[0] == 0 && bounds[nparts] == g->n, "mcf_spmv_peer: parts must cover [0, n)");
+    if (re == rb) return MCF_OK;
+    PeerArgs pa{};
+    for (int k = 0; k < nparts; ++k) {
+        MCF_ARG(x_parts[k] && bounds[k] <= bounds[k + 1], "mcf_spmv_peer: bad part");
+        pa.x[k] = x_parts[k];
+        pa.bounds[k] = bounds[k];
+    }
+    pa.bounds[nparts] = bounds[nparts];
+    pa.nparts = nparts;
+    for (int k = 0; k < nouts; ++k) {
+        MCF_ARG(y_outs[k], "mcf_spmv_peer: null output");
+        pa.y[k] = y_outs[k];
+    }
+    pa.nouts = nouts;
+    const long long *rp = (const long long *)g->row_ptr;
+    long long lb = g->n_long_rows > 0 ? (g->n_long_rows + SPMV_WARPS - 1) / SPMV_WARPS : 0;
+    if (lb > 2 * sm_count()) lb = 2 * sm_count();
+    const long long sb = (re - rb + 32 * SPMV_WARPS - 1) / (32 * SPMV_WARPS);
+    const unsigned grid = (unsigned)(lb + sb);
+    const RowSumR rt{nullptr, nullptr};
+    if (g->uniform_value)
+        k_spmv<true, true><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r,
+                                                            nullptr, nullptr, rb, re, nullptr, g->long_rows,
+                                                            g->n_long_rows, (int)lb, rt, pa);
+    else
+        k_spmv<false, true><<<grid, 32 * SPMV_WARPS, 0, s>>>(rp, g->col_ids, g->vals, g->value, alpha, v, beta, r,
+                                                             nullptr, nullptr, rb, re, nullptr, g->long_rows,
+                                                             g->n_long_rows, (int)lb, rt, pa);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_spmv_peer");
     return MCF_OK;
 }
 
@@ -1141,6 +1212,13 @@ int mcf_funm_action(mcf_graph *g, const mcf_walk_params *p, int64_t n_walks, int
                     int64_t *stats, void *stream) {
     return mcf::funm_action(g, p, (long long)n_walks, (long long *)ni, (long long *)walk_pre, v, zeta0, zeta1, r, q,
                             q_var, y, (long long *)stats, (cudaStream_t)stream);
+}
+
+int mcf_spmv_peer(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
+                  const double *const *x_parts, const int64_t *part_bounds, int n_parts, double *const *y_outs,
+                  int n_outs, int64_t row_begin, int64_t row_end, void *stream) {
+    return mcf::spmv_peer(g, alpha, v, beta, r, x_parts, (const long long *)part_bounds, n_parts, y_outs, n_outs,
+                          (long long)row_begin, (long long)row_end, (cudaStream_t)stream);
 }
 
 int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,

@@ -248,6 +248,18 @@ class DeviceGraph:
                                  int(rb), int(re), self.stream), "mcf_spmv")
         return out
 
+    def spmv_peer(self, x_parts, bounds, y_outs, alpha=0.0, v=None, beta=0.0, r=None, rows=None):
+        """y = alpha v + beta r + A x with x gathered from per-part device
+        buffers (x_parts[k] owns indices [bounds[k], bounds[k+1])) and every
+        row stored to every buffer in y_outs (raw device pointers, local or
+        mapped peer memory; mcf_spmv_peer)."""
+        rb, re = (0, self.n) if rows is None else rows
+        xs = (C.c_void_p * len(x_parts))(*[int(p) for p in x_parts])
+        bs = (C.c_int64 * len(bounds))(*[int(b) for b in bounds])
+        ys = (C.c_void_p * len(y_outs))(*[int(p) for p in y_outs])
+        N.check(N.lib().mcf_spmv_peer(self.handle, float(alpha), _ptr(v), float(beta), _ptr(r), xs, bs, len(x_parts),
+                                      ys, len(y_outs), int(rb), int(re), self.stream), "mcf_spmv_peer")
+
     def walk_action(self, params: WalkParams, walk_pre, r, q, qvar=None, cols=None, stats=None):
         cb, ce = (0, self.n) if cols is None else cols
         N.check(N.lib().mcf_walk_action(self.handle, C.byref(params.c), _ptr(walk_pre), int(cb), int(ce), _ptr(r),

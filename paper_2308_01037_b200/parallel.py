@@ -10,9 +10,16 @@ runs.  The only exchange is assembling the per-column results:
   * diag: the per-entry partials pcol (8 nnz bytes), assembled the same way,
     then d over the rank's row range.
 Results are therefore bitwise identical for 1, 2, 4 and 8 GPUs.
+
+sharded_action_peer folds the action exchange into the combine instead: the
+ranks map each other's q and y buffers (CUDA IPC over NVLink) and one SpMV per
+rank gathers q from the owning ranks and writes its y rows into every rank's
+buffer (mcf_spmv_peer) -- two barriers, no NCCL on the data path.
 """
 
 from __future__ import annotations
+
+import ctypes as C
 
 import numpy as np
 import torch
@@ -57,6 +64,104 @@ def assemble(t: torch.Tensor, group=None) -> torch.Tensor:
     if world()[1] > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over a raw device pointer (zero-copy torch view)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (int(ptr), False), "version": 3}
+
+
+def _device_view(ptr: int, n: int, device) -> torch.Tensor:
+    return torch.as_tensor(_CudaArray(ptr, n), device=device)
+
+
+class _Raw:
+    """A raw device pointer where the binding expects a tensor (data_ptr())."""
+
+    def __init__(self, ptr: int):
+        self.ptr = int(ptr)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class PeerBuffers:
+    """Per-rank device buffers every rank of the node can read and write over
+    NVLink: each rank allocates its own (mcf_peer_alloc), the 64-byte CUDA IPC
+    handles are swapped with an all-gather over ``group``, and every rank maps
+    the others' (mcf_peer_open).  ptrs[k][b] is buffer b of rank k as seen by
+    this process (its own are local)."""
+
+    def __init__(self, nbytes: list[int], group=None):
+        rank, size = world()
+        self.rank = rank
+        self.own, handles = [], []
+        for b in nbytes:
+            ptr, h = C.c_void_p(), C.create_string_buffer(64)
+            N.check(N.lib().mcf_peer_alloc(int(b), C.byref(ptr), h), "mcf_peer_alloc")
+            self.own.append(ptr.value)
+            handles.append(h.raw)
+        allh = [None] * size
+        dist.all_gather_object(allh, handles, group=group)
+        self.ptrs, self.opened = [], []
+        for k in range(size):
+            if k == rank:
+                self.ptrs.append(list(self.own))
+                continue
+            row = []
+            for h in allh[k]:
+                ptr = C.c_void_p()
+                N.check(N.lib().mcf_peer_open(C.create_string_buffer(h, 64), C.byref(ptr)), "mcf_peer_open")
+                row.append(ptr.value)
+                self.opened.append(ptr.value)
+            self.ptrs.append(row)
+
+    def close(self, group=None):
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # nobody still reads our buffers
+        for p in self.opened:
+            N.lib().mcf_peer_close(C.c_void_p(p))
+        dist.barrier(group=group)
+        for p in self.own:
+            N.lib().mcf_peer_free(C.c_void_p(p))
+        self.opened, self.own = [], []
+
+
+def sharded_action_peer(g: DeviceGraph, coeffs, v, config, *, params=None, group=None, peers: PeerBuffers = None):
+    """Multi-GPU RandFunmAction with the exchange folded into the combine:
+    each rank walks its column shard into its own q buffer; after a barrier
+    one SpMV per rank gathers q[j] from the rank owning column j (peer memory
+    over NVLink) and writes its row shard of y into every rank's y buffer
+    (mcf_spmv_peer) -- no all-gather of q or y.  ``v=None`` is v = 1.
+    Returns (y, stats); y holds all rows on every rank."""
+    rank, size = world()
+    cfg = check_config(config)
+    coeffs = as_stream(coeffs)
+    z = coeffs.prefix(cfg.max_steps + 2)
+    params = params or WalkParams(cfg, z, g.device)
+    if v is None:
+        v = torch.ones(g.n, dtype=torch.float64, device=g.device)
+    own = peers is None
+    if own:
+        peers = PeerBuffers([8 * g.n, 8 * g.n], group)
+    ni, pre = g.allocate(cfg.n_walks)
+    shards = column_shards(pre, size)
+    bounds = [shards[0][0]] + [b for _, b in shards]
+    st = g.new_stats()
+    r = g.spmv(v)
+    g.walk_action(params, pre, r, _Raw(peers.ptrs[rank][0]), cols=shards[rank], stats=st)
+    torch.cuda.synchronize()
+    dist.barrier(group=group)  # every rank's q shard is complete
+    g.spmv_peer([peers.ptrs[k][0] for k in range(size)], bounds, [peers.ptrs[k][1] for k in range(size)],
+                alpha=z[0], v=v, beta=z[1], r=r, rows=row_shards(g.n, size)[rank])
+    torch.cuda.synchronize()
+    dist.barrier(group=group)  # every rank's y rows have landed everywhere
+    y = _device_view(peers.ptrs[rank][1], g.n, g.device).clone()
+    if own:
+        peers.close(group)
+    return y, st
 
 
 def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=None, group=None):

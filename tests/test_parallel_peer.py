@@ -1,0 +1,79 @@
+"""The peer-memory action exchange (parallel.sharded_action_peer,
+mcf_spmv_peer) with world size 2.  Two processes share ONE GPU here (the
+sandbox has one): CUDA IPC between processes on a device is the same mapping
+path as between GPUs of a node, the kernels never wait on each other (host
+barriers only), and this checks results, not speed.  y must equal the
+single-process estimate bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as tmp
+
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _as_matrix(a, symmetric):
+    from scipy import sparse
+
+    class M:
+        pass
+    m = M()
+    m.csr = sparse.csr_array((a.vals, a.col_ids.astype(np.int32), a.row_ptr), shape=(a.n, a.n))
+    m.csc = sparse.csc_array((a.csc_vals, a.csc_rows.astype(np.int32), a.csc_ptr), shape=(a.n, a.n))
+    m.symmetric_hint = symmetric
+    return m
+
+
+def _worker(rank, world, port_no, name, n_walks, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2308_01037_b200 as mc
+        from paper_2308_01037_b200 import parallel
+        c = golden_io.load(name)
+        g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
+        y, st = parallel.sharded_action_peer(g, mc.EXPONENTIAL, None, mc.WalkConfig(n_walks, 1e-6, 28, 11))
+        emitted = torch.tensor([int(st[1])])
+        dist.all_reduce(emitted)
+        if rank == 0:
+            out.put((y.cpu().numpy(), int(emitted)))
+        g.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["ba400", "kron8"])
+def test_peer_exchange_matches_single_process(name):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2308_01037_b200 as mc
+    c = golden_io.load(name)
+    n_walks = 50 * c.n
+    ctx = tmp.get_context("spawn")
+    out = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, name, n_walks, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    y2, em2 = out.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
+    ones = torch.ones(c.n, dtype=torch.float64, device="cuda")
+    ref = mc.rand_funm_action(g, mc.EXPONENTIAL, ones, mc.WalkConfig(n_walks, 1e-6, 28, 11))
+    assert em2 == ref.emissions
+    assert np.array_equal(y2, np.asarray(ref.values))
