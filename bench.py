@@ -285,9 +285,17 @@ def run_device(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MCF_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo -- a functional
+    # check of the N > 1 code path on a one-GPU machine, never a measurement
+    shared = os.environ.get("MCF_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _native.lib()
 
     t0 = time.perf_counter()
@@ -311,8 +319,15 @@ def run_device(args, cfg):
         if sweep is not None:
             torch.sum(sweep, dim=0, out=sweep_out)
 
+    # N > 1 action: the exchange runs in peer memory (mcf_spmv_peer over CUDA
+    # IPC / NVLink) unless --transport nccl; the buffers are mapped once
+    peers = (parallel.PeerBuffers([8 * g.n, 8 * g.n]) if world > 1 and cfg["kind"] == "action"
+             and args.transport == "peer" else None)
+
     def step():
         if cfg["kind"] == "action":
+            if peers is not None:
+                return parallel.sharded_action_peer(g, coeffs, None, wcfg, params=params, peers=peers)
             return parallel.sharded_action(g, coeffs, None, wcfg, params=params)  # f(A) 1: v = 1
         return parallel.sharded_diag(g, coeffs, wcfg, params=params)
 
@@ -483,12 +498,15 @@ def run_device(args, cfg):
                        "l2": ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read of another "
                               "buffer to evict the dirty lines" if args.flush == "write+read" else
                               "flushed between timed steps (256 MiB write, untimed)"),
-                       "parallelism": f"start-column shards x{world}, graph replicated"},
+                       "parallelism": f"start-column shards x{world}, graph replicated"
+                                      + (f", exchange: {args.transport}" if world > 1 else "")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "timing": "CUDA-graph replay of one full estimator pass" if graph is not None else "eager steps",
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if peers is not None:
+        peers.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -504,6 +522,8 @@ def main():
     ap.add_argument("--impl", default="mcfunm", choices=["mcfunm", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--flush", choices=["write", "write+read"], default="write")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N > 1 action exchange: peer-memory SpMV (default) or NCCL all-reduce")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
