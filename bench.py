@@ -319,16 +319,19 @@ def run_device(args, cfg):
         if sweep is not None:
             torch.sum(sweep, dim=0, out=sweep_out)
 
-    # N > 1 action: the exchange runs in peer memory (mcf_spmv_peer over CUDA
-    # IPC / NVLink) unless --transport nccl; the buffers are mapped once
-    peers = (parallel.PeerBuffers([8 * g.n, 8 * g.n]) if world > 1 and cfg["kind"] == "action"
-             and args.transport == "peer" else None)
+    # N > 1: the exchange runs in peer memory (mcf_spmv_peer / mcf_diag_combine_peer
+    # over CUDA IPC / NVLink) unless --transport nccl; the buffers are mapped once
+    peers = None
+    if world > 1 and args.transport == "peer":
+        peers = parallel.PeerBuffers([8 * g.n if cfg["kind"] == "action" else 8 * g.nnz, 8 * g.n])
 
     def step():
         if cfg["kind"] == "action":
             if peers is not None:
                 return parallel.sharded_action_peer(g, coeffs, None, wcfg, params=params, peers=peers)
             return parallel.sharded_action(g, coeffs, None, wcfg, params=params)  # f(A) 1: v = 1
+        if peers is not None:
+            return parallel.sharded_diag_peer(g, coeffs, wcfg, params=params, peers=peers)
         return parallel.sharded_diag(g, coeffs, wcfg, params=params)
 
     clocks = Clocks(local) if rank == 0 else None
@@ -523,7 +526,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--flush", choices=["write", "write+read"], default="write")
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
-                    help="N > 1 action exchange: peer-memory SpMV (default) or NCCL all-reduce")
+                    help="N > 1 exchange: peer-memory combine kernels (default) or NCCL all-reduce")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

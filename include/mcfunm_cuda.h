@@ -218,6 +218,14 @@ MCF_API int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_
 MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d,
                      int64_t row_begin, int64_t row_end, void *stream);
 
+/* Multi-GPU diag combine with the exchange folded in (as mcf_spmv_peer):
+ * d over rows [row_begin, row_end), reading pcol[(i, c)] from
+ * pcol_parts[k] for the part k whose column range [col_bounds[k],
+ * col_bounds[k+1]) holds c, and storing every d_i to all n_outs buffers. */
+MCF_API int mcf_diag_combine_peer(mcf_graph *g, double zeta0, double zeta1, const double *const *pcol_parts,
+                                  const int64_t *col_bounds, int n_parts, double *const *d_outs, int n_outs,
+                                  int64_t row_begin, int64_t row_end, void *stream);
+
 /* Device time of the kernels launched with MCF_FLAG_TIME_KERNELS since the
  * last reset: the walk kernels (action walks or diag emission walks) and, in
  * q_ms, the diag Q-build/combine kernel -- or, for mcf_funm_action, the span

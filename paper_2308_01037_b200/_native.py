@@ -61,6 +61,7 @@ SIGNATURES = {
     "mcf_walk_diag": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P]),
     "mcf_replay_diag": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, P, P, P, P]),
     "mcf_diag_combine": (C.c_int, [P, C.c_double, C.c_double, P, P, I64, I64, P]),
+    "mcf_diag_combine_peer": (C.c_int, [P, C.c_double, C.c_double, P, P, C.c_int, P, C.c_int, I64, I64, P]),
     "mcf_walk_qdense": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, I64, P, P]),
 }
 

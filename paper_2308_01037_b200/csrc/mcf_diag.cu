@@ -366,19 +366,23 @@ __global__ void k_big_counts(const BigRec *__restrict__ big, unsigned nrec, long
     if (b < nrec) cnt[b] = big[b].cn;
 }
 
-// d_i = zeta_0 + zeta_1 a_ii + sum over row i of pcol[csr2csc[e]] (4 lanes per row)
+// d_i = zeta_0 + zeta_1 a_ii + sum over row i of pcol[csr2csc[e]] (4 lanes per row).
+// PEER: pcol[(i, c)] is read from the part (rank) owning column c -- mapped
+// peer memory -- and d_i is stored to every output buffer (mcf_diag_combine_peer).
+template <bool PEER = false>
 __global__ void k_diag_final(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
                              const double *__restrict__ vals, const long long *__restrict__ csr2csc,
                              const double *__restrict__ pcol, double z0, double z1, double *__restrict__ d,
-                             long long rb, long long re) {
+                             long long rb, long long re, PeerArgs pa) {
     long long i = rb + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 2);
     int sub = threadIdx.x & 3;
     bool in = i < re;
     double s = 0.0, aii = 0.0;
     if (in) {
         for (long long e = row_ptr[i] + sub; e < row_ptr[i + 1]; e += 4) {
-            s += pcol[csr2csc[e]];
-            if (col_ids[e] == i) aii = vals[e];
+            const int c = col_ids[e];
+            s += PEER ? __ldg(pa.x[peer_owner(pa, c)] + csr2csc[e]) : pcol[csr2csc[e]];
+            if (c == i) aii = vals[e];
         }
     }
 #pragma unroll
@@ -386,7 +390,14 @@ __global__ void k_diag_final(const long long *__restrict__ row_ptr, const int *_
         s += __shfl_xor_sync(MCF_FULL, s, o, 4);
         aii += __shfl_xor_sync(MCF_FULL, aii, o, 4);
     }
-    if (in && sub == 0) d[i] = (z0 + z1 * aii) + s;
+    if (in && sub == 0) {
+        const double out = (z0 + z1 * aii) + s;
+        if (PEER) {
+            for (int k = 0; k < pa.nouts; ++k) pa.y[k][i] = out;
+        } else {
+            d[i] = out;
+        }
+    }
 }
 
 __global__ void k_batch_bounds(const long long *__restrict__ walk_pre, long long cb, long long ce, long long wb,
@@ -767,9 +778,30 @@ static int diag_combine(mcf_graph *g, double z0, double z1, const double *pcol, 
     long long rows = re - rb;
     if (rows == 0) return MCF_OK;
     k_diag_final<<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->vals,
-                                                                   (const long long *)g->csr2csc, pcol, z0, z1, d, rb, re);
+                                                                   (const long long *)g->csr2csc, pcol, z0, z1, d, rb, re,
+                                                                   PeerArgs{});
     mcf::note_launch();
     MCF_LAUNCHED("k_diag_final");
+    return MCF_OK;
+}
+
+static int diag_combine_peer(mcf_graph *g, double z0, double z1, const double *const *pcol_parts,
+                             const long long *col_bounds, int nparts, double *const *d_outs, int nouts, long long rb,
+                             long long re, cudaStream_t s) {
+    MCF_ARG(g, "mcf_diag_combine_peer: null graph");
+    MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_diag_combine_peer: bad row range");
+    PeerArgs pa{};
+    int rc = make_peer_args(pcol_parts, col_bounds, nparts, d_outs, nouts, g->n, &pa);
+    if (rc) return rc;
+    rc = ensure_csr2csc(g, s);
+    if (rc) return rc;
+    const long long rows = re - rb;
+    if (rows == 0) return MCF_OK;
+    k_diag_final<true><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>(
+        (const long long *)g->row_ptr, g->col_ids, g->vals, (const long long *)g->csr2csc, nullptr, z0, z1, nullptr, rb,
+        re, pa);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_diag_final_peer");
     return MCF_OK;
 }
 
@@ -799,6 +831,13 @@ int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_
 int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d, int64_t row_begin,
                      int64_t row_end, void *stream) {
     return mcf::diag_combine(g, zeta0, zeta1, pcol, d, row_begin, row_end, (cudaStream_t)stream);
+}
+
+int mcf_diag_combine_peer(mcf_graph *g, double zeta0, double zeta1, const double *const *pcol_parts,
+                          const int64_t *col_bounds, int n_parts, double *const *d_outs, int n_outs,
+                          int64_t row_begin, int64_t row_end, void *stream) {
+    return mcf::diag_combine_peer(g, zeta0, zeta1, pcol_parts, (const long long *)col_bounds, n_parts, d_outs, n_outs,
+                                  (long long)row_begin, (long long)row_end, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -341,6 +341,31 @@ __device__ __forceinline__ void tile_scan(long long tile, const long long (&a)[S
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory exchange (mcf_spmv_peer, mcf_diag_combine_peer): per-rank
+// input buffers (local or mapped peer memory), each valid on the index range
+// of the columns its rank owns, and the output buffers every result goes to.
+// ---------------------------------------------------------------------------
+constexpr int MAX_PEERS = 8;
+struct PeerArgs {
+    const double *x[MAX_PEERS];       // x[k]: valid where the column is in [bounds[k], bounds[k+1])
+    long long bounds[MAX_PEERS + 1];  // column ranges of the parts
+    int nparts;
+    double *y[MAX_PEERS];             // every output buffer receives every row
+    int nouts;
+};
+
+__device__ __forceinline__ int peer_owner(const PeerArgs &pa, long long col) {
+    int k = 0;
+#pragma unroll
+    for (int t = 1; t < MAX_PEERS; ++t) k += (t < pa.nparts && col >= pa.bounds[t]) ? 1 : 0;
+    return k;
+}
+
+// host: validate and pack the pointer lists (rc != 0 on bad arguments)
+int make_peer_args(const double *const *x_parts, const long long *bounds, int nparts, double *const *y_outs,
+                   int nouts, long long ncols, PeerArgs *pa);
+
+// ---------------------------------------------------------------------------
 // host helpers implemented in mcf_util.cu
 // ---------------------------------------------------------------------------
 int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStream_t s);

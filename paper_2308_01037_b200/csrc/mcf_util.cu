@@ -230,6 +230,27 @@ __global__ void k_hub_bits(const long long *__restrict__ row_ptr, const int *__r
     }
 }
 
+int make_peer_args(const double *const *x_parts, const long long *bounds, int nparts, double *const *y_outs,
+                   int nouts, long long ncols, PeerArgs *pa) {
+    MCF_ARG(x_parts && bounds && y_outs && pa, "peer exchange: null argument");
+    MCF_ARG(nparts >= 1 && nparts <= MAX_PEERS && nouts >= 1 && nouts <= MAX_PEERS,
+            "peer exchange: 1..8 parts and outputs");
+    MCF_ARG(bounds[0] == 0 && bounds[nparts] == ncols, "peer exchange: the parts must cover [0, n)");
+    for (int k = 0; k < nparts; ++k) {
+        MCF_ARG(x_parts[k] && bounds[k] <= bounds[k + 1], "peer exchange: bad part");
+        pa->x[k] = x_parts[k];
+        pa->bounds[k] = bounds[k];
+    }
+    pa->bounds[nparts] = bounds[nparts];
+    pa->nparts = nparts;
+    for (int k = 0; k < nouts; ++k) {
+        MCF_ARG(y_outs[k], "peer exchange: null output");
+        pa->y[k] = y_outs[k];
+    }
+    pa->nouts = nouts;
+    return MCF_OK;
+}
+
 int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s) {
     if (g->hubs_ready) return MCF_OK;
     g->hubs_ready = true;

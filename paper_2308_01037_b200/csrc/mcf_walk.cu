@@ -553,22 +553,10 @@ __global__ void k_r_ones(NodeHdr *__restrict__ hdr, const double *__restrict__ v
 // gathered straight from the rank that owns each column -- its buffer mapped
 // into this process over NVLink (CUDA IPC) -- and every result row is stored
 // to every rank's y buffer, so the SpMV itself is the exchange.
-constexpr int MAX_PEERS = 8;
-struct PeerArgs {
-    const double *x[MAX_PEERS];       // x[k]: valid on [bounds[k], bounds[k+1])
-    long long bounds[MAX_PEERS + 1];
-    int nparts;
-    double *y[MAX_PEERS];             // every output buffer receives every row
-    int nouts;
-};
-
 template <bool PEER>
 __device__ __forceinline__ double xload(const double *__restrict__ x, const PeerArgs &pa, int c) {
     if (!PEER) return __ldg(x + c);
-    int k = 0;
-#pragma unroll
-    for (int t = 1; t < MAX_PEERS; ++t) k += (t < pa.nparts && c >= pa.bounds[t]) ? 1 : 0;
-    return __ldg(pa.x[k] + c);
+    return __ldg(pa.x[peer_owner(pa, c)] + c);
 }
 
 template <bool PEER>
@@ -717,24 +705,12 @@ int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double 
 int spmv_peer(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
               const double *const *x_parts, const long long *bounds, int nparts, double *const *y_outs, int nouts,
               long long rb, long long re, cudaStream_t s) {
-    MCF_ARG(g && x_parts && bounds && y_outs, "mcf_spmv_peer: null argument");
-    MCF_ARG(nparts >= 1 && nparts <= MAX_PEERS && nouts >= 1 && nouts <= MAX_PEERS, "mcf_spmv_peer: 1..8 parts and outputs");
+    MCF_ARG(g, "mcf_spmv_peer: null graph");
     MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv_peer: bad row range");
-    MCF_ARG(bounds[0] == 0 && bounds[nparts] == g->n, "mcf_spmv_peer: parts must cover [0, n)");
-    if (re == rb) return MCF_OK;
     PeerArgs pa{};
-    for (int k = 0; k < nparts; ++k) {
-        MCF_ARG(x_parts[k] && bounds[k] <= bounds[k + 1], "mcf_spmv_peer: bad part");
-        pa.x[k] = x_parts[k];
-        pa.bounds[k] = bounds[k];
-    }
-    pa.bounds[nparts] = bounds[nparts];
-    pa.nparts = nparts;
-    for (int k = 0; k < nouts; ++k) {
-        MCF_ARG(y_outs[k], "mcf_spmv_peer: null output");
-        pa.y[k] = y_outs[k];
-    }
-    pa.nouts = nouts;
+    int rc = make_peer_args(x_parts, bounds, nparts, y_outs, nouts, g->n, &pa);
+    if (rc) return rc;
+    if (re == rb) return MCF_OK;
     const long long *rp = (const long long *)g->row_ptr;
     long long lb = g->n_long_rows > 0 ? (g->n_long_rows + SPMV_WARPS - 1) / SPMV_WARPS : 0;
     if (lb > 2 * sm_count()) lb = 2 * sm_count();

@@ -302,6 +302,17 @@ class DeviceGraph:
                                         int(Q.stride(0)), _ptr(stats), self.stream), "mcf_walk_qdense")
         return Q
 
+    def diag_combine_peer(self, z0, z1, pcol_parts, col_bounds, d_outs, rows=None):
+        """d over a row range with pcol[(i, c)] read from the part owning
+        column c and every d_i stored to every buffer in d_outs (raw device
+        pointers, local or mapped peer memory; mcf_diag_combine_peer)."""
+        rb, re = (0, self.n) if rows is None else rows
+        xs = (C.c_void_p * len(pcol_parts))(*[int(p) for p in pcol_parts])
+        bs = (C.c_int64 * len(col_bounds))(*[int(b) for b in col_bounds])
+        ys = (C.c_void_p * len(d_outs))(*[int(p) for p in d_outs])
+        N.check(N.lib().mcf_diag_combine_peer(self.handle, float(z0), float(z1), xs, bs, len(pcol_parts), ys,
+                                              len(d_outs), int(rb), int(re), self.stream), "mcf_diag_combine_peer")
+
     def diag_combine(self, z0, z1, pcol, d=None, rows=None):
         d = self._f64() if d is None else d
         rb, re = (0, self.n) if rows is None else rows

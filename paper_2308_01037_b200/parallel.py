@@ -164,6 +164,38 @@ def sharded_action_peer(g: DeviceGraph, coeffs, v, config, *, params=None, group
     return y, st
 
 
+def sharded_diag_peer(g: DeviceGraph, coeffs, config, *, params=None, group=None, peers: PeerBuffers = None):
+    """Multi-GPU RandFunmDiag with the exchange folded into the combine: each
+    rank writes the Eq. 20 partials of its column shard into its own pcol
+    buffer; after a barrier one kernel per rank reads every pcol[(i, c)] from
+    the rank owning column c (peer memory) and writes its rows of d into every
+    rank's d buffer (mcf_diag_combine_peer).  Returns (d, stats)."""
+    rank, size = world()
+    cfg = check_config(config)
+    coeffs = as_stream(coeffs)
+    z = coeffs.prefix(cfg.max_steps + 2)
+    params = params or WalkParams(cfg, z, g.device)
+    own = peers is None
+    if own:
+        peers = PeerBuffers([8 * g.nnz, 8 * g.n], group)
+    ni, pre = g.allocate(cfg.n_walks)
+    shards = column_shards(pre, size)
+    bounds = [shards[0][0]] + [b for _, b in shards]
+    st = g.new_stats()
+    _device_view(peers.ptrs[rank][0], g.nnz, g.device).zero_()  # columns without walks keep zero partials
+    g.walk_diag(params, pre, _Raw(peers.ptrs[rank][0]), cols=shards[rank], stats=st)
+    torch.cuda.synchronize()
+    dist.barrier(group=group)  # every rank's partials are complete
+    g.diag_combine_peer(z[0], z[1], [peers.ptrs[k][0] for k in range(size)], bounds,
+                        [peers.ptrs[k][1] for k in range(size)], rows=row_shards(g.n, size)[rank])
+    torch.cuda.synchronize()
+    dist.barrier(group=group)  # every rank's d rows have landed everywhere
+    d = _device_view(peers.ptrs[rank][1], g.n, g.device).clone()
+    if own:
+        peers.close(group)
+    return d, st
+
+
 def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=None, group=None):
     """One RandFunmAction pass with this rank's share of the start columns.
     ``v=None`` is v = 1.  Returns (y, stats) with y assembled on every rank."""

@@ -1,9 +1,9 @@
-"""The peer-memory action exchange (parallel.sharded_action_peer,
-mcf_spmv_peer) with world size 2.  Two processes share ONE GPU here (the
+"""The peer-memory exchanges (parallel.sharded_action_peer / mcf_spmv_peer,
+parallel.sharded_diag_peer / mcf_diag_combine_peer) with world size 2.  Two processes share ONE GPU here (the
 sandbox has one): CUDA IPC between processes on a device is the same mapping
 path as between GPUs of a node, the kernels never wait on each other (host
-barriers only), and this checks results, not speed.  y must equal the
-single-process estimate bit for bit."""
+barriers only), and this checks results, not speed.  y and d must equal the
+single-process estimates bit for bit."""
 import os
 import socket
 
@@ -46,10 +46,11 @@ def _worker(rank, world, port_no, name, n_walks, out):
         c = golden_io.load(name)
         g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
         y, st = parallel.sharded_action_peer(g, mc.EXPONENTIAL, None, mc.WalkConfig(n_walks, 1e-6, 28, 11))
-        emitted = torch.tensor([int(st[1])])
+        d, sd = parallel.sharded_diag_peer(g, mc.EXPONENTIAL, mc.WalkConfig(n_walks, 1e-6, 28, 12))
+        emitted = torch.tensor([int(st[1]), int(sd[1])])
         dist.all_reduce(emitted)
         if rank == 0:
-            out.put((y.cpu().numpy(), int(emitted)))
+            out.put((y.cpu().numpy(), d.cpu().numpy(), emitted.tolist()))
         g.close()
     finally:
         dist.destroy_process_group()
@@ -68,12 +69,14 @@ def test_peer_exchange_matches_single_process(name):
     procs = [ctx.Process(target=_worker, args=(r, 2, port_no, name, n_walks, out)) for r in range(2)]
     for p in procs:
         p.start()
-    y2, em2 = out.get(timeout=300)
+    y2, d2, em2 = out.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
     ones = torch.ones(c.n, dtype=torch.float64, device="cuda")
     ref = mc.rand_funm_action(g, mc.EXPONENTIAL, ones, mc.WalkConfig(n_walks, 1e-6, 28, 11))
-    assert em2 == ref.emissions
+    refd = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(n_walks, 1e-6, 28, 12))
+    assert em2 == [ref.emissions, refd.emissions]
     assert np.array_equal(y2, np.asarray(ref.values))
+    assert np.array_equal(d2, np.asarray(refd.values))
