@@ -601,3 +601,20 @@ def test_lean_walk_absorbing_and_self_loops(mc, lean_bytes):
     assert out["1"][2] > 0  # some walks were absorbed
     for x, y in zip(out["1"], out["0"]):
         assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+@pytest.mark.parametrize("n_walks", [1, 7, 333])
+def test_funm_action_sparse_budgets(mc, alloc_path, n_walks):
+    """Budgets far below n (most columns without walks): the one-call action
+    (budgets, walks, y) equals the step-by-step path (mcf_allocate_walks,
+    mcf_walk_action, mcf_spmv) bit for bit, and the walks number n_walks."""
+    import torch
+    c = golden_io.load("ba400")
+    g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric), gamma=0.05)
+    cfg = mc.WalkConfig(n_walks, 1e-6, 28, 5)
+    ones = torch.ones(c.n, dtype=torch.float64, device="cuda")
+    one_call = mc.rand_funm_action(g, mc.EXPONENTIAL, ones, cfg)
+    ni, _ = g.allocate(n_walks)
+    stepwise = mc.rand_funm_action(g, mc.EXPONENTIAL, ones, cfg, budgets=ni.cpu().numpy())
+    assert one_call.walks == n_walks == stepwise.walks
+    assert np.array_equal(np.asarray(one_call.values), np.asarray(stepwise.values))
