@@ -8,6 +8,7 @@ libmcfunm_cuda.so (include/mcfunm_cuda.h) -- sm_100a kernels, no CPU fallback.
 from .errors import (ArgumentError, ConvergenceError, DataError, DegenerateInputError, DeviceError,  # noqa: F401
                      McfunmError, ParseError, ResourceError)
 from .series import EXPONENTIAL, RESOLVENT, CoefficientStream  # noqa: F401
+from .ingest import GraphSource, load_graph, simple_graph_from_edges, symmetrize_digraph  # noqa: F401
 from .sparsemat import SparseMatrix, row_abs_sums, scale  # noqa: F401
 from .walker import WalkConfig, alpha_diagnostic  # noqa: F401
 

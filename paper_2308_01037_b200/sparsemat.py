@@ -4,8 +4,8 @@ Holds the same (row, col, value) triples in CSR and CSC form (scipy arrays),
 plus the provenance fields of the reference type.  Anything exposing
 ``.csr``/``.csc`` scipy arrays -- including the reference's own
 ``SparseMatrix`` -- is accepted by the estimators, so this type only exists so
-the package runs where the reference is not installed.  File parsers and
-digraph symmetrisation are outside the hot path.
+the package runs where the reference is not installed.  File parsers, the
+cleanup filters and digraph symmetrisation are in ingest.py.
 """
 
 from __future__ import annotations
