@@ -123,9 +123,10 @@ class DeviceGraph:
             self.csc_ptr = _upload(csc.indptr, np.int64, dev)
             self.csc_rows = _upload(csc.indices, np.int32, dev)
             self.csc_vals = _upload(csc.data, np.float64, dev)
-        if self.gamma != 1.0:  # scale() on the device: every stored value times gamma
-            self.vals = self.vals * self.gamma
-            self.csc_vals = self.vals if same else self.csc_vals * self.gamma
+        if self.gamma != 1.0:  # scale() on the device, in place (the uploads are our own copies)
+            self.vals.mul_(self.gamma)
+            if not same:
+                self.csc_vals.mul_(self.gamma)
         self.aliased = same
         self._build()
 
