@@ -464,8 +464,13 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.hub_words = g->hub_words;
     q.uniform = g->uniform_value ? 1 : 0;
     {
+        // push while a bitmap test is cheaper than scanning C_i: the bitmaps are
+        // n bits, so the push/pull break-even moves up with n (measured: R-MAT
+        // 2^22 best at 1x |supp Q_c|, Chung-Lu 1.6e7 at ~4x)
         const char *e = getenv("MCF_PUSH_PCT");
-        q.push_pct = e ? atoi(e) : 100;
+        long long pct = (100ll * g->n) / (1ll << 22);
+        pct = pct < 100 ? 100 : (pct > 400 ? 400 : pct);
+        q.push_pct = e ? atoi(e) : (int)pct;
     }
     q.value = g->value;
     q.colmax = colmax;
