@@ -153,17 +153,22 @@ __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, co
                 if ((__ldg(bits + (k >> 5)) >> (k & 31)) & 1u) acc += lvals[t];
             }
         } else {
-            long long e = ilo + lane;
-            for (; e + 32 < ihi; e += 64) {  // two row ids in flight per lane
-                const int j0 = __ldg(a.csc_rows + e), j1 = __ldg(a.csc_rows + e + 32);
-                const uint32_t b0 = filter_bit(j0), b1 = filter_bit(j1);
-                if (filt[b0 >> 5] & (1u << (b0 & 31))) acc += lookup(keys, vals, mask, j0);
-                if (filt[b1 >> 5] & (1u << (b1 & 31))) acc += lookup(keys, vals, mask, j1);
-            }
-            if (e < ihi) {
-                const int j = __ldg(a.csc_rows + e);
-                const uint32_t b = filter_bit(j);
-                if (filt[b >> 5] & (1u << (b & 31))) acc += lookup(keys, vals, mask, j);
+            // PULL_U row ids in flight per lane: long rows are scanned latency-
+            // bound otherwise (one L2 round trip per 64 ids)
+            constexpr int PULL_U = 8;
+            for (long long e0 = ilo; e0 < ihi; e0 += 32 * PULL_U) {
+                int jv[PULL_U];
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    const long long e = e0 + 32 * u + lane;
+                    jv[u] = e < ihi ? __ldg(a.csc_rows + e) : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    if (jv[u] < 0) continue;
+                    const uint32_t b = filter_bit(jv[u]);
+                    if (filt[b >> 5] & (1u << (b & 31))) acc += lookup(keys, vals, mask, jv[u]);
+                }
             }
         }
         acc = warp_sum_ll(acc);
