@@ -14,6 +14,7 @@
 //                    fixed order (mcf_diag_combine).
 // Partials per CSC entry make the result independent of how columns are
 // split across batches, CTAs or GPUs.
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -80,7 +81,12 @@ struct QArgs {
     long long hub_words;
     unsigned long long *pool_used, pool_cap;
     unsigned *pool_filt;        // FILTER_WORDS per record
+    unsigned long long *prof;   // MCF_DIAG_PROF=1: combine counters (profiling only, else null)
 };
+
+// prof slots: 0 pull pairs, 1 pull ids, 2 pull filter passes, 3 push pairs, 4 push tests, 5 push hits,
+// 6 emissions, 7 support, 8 columns, 9 big columns, 10 cycles Q build, 11 cycles combine, 12 pull hits
+constexpr int PROF_SLOTS = 16;
 
 struct BigRec {
     long long c;      // column
@@ -89,7 +95,10 @@ struct BigRec {
     unsigned cn;      // entries of C_c
 };
 
-constexpr long long BIG_WORK = 1ll << 20;  // combine probes above which a column's Q_c is shared GPU-wide
+constexpr long long BIG_WORK = 1ll << 20;
+constexpr int MAX_LONG = 64;            // parked long (i, c) entries per column
+constexpr long long CHUNK = 1024;       // ids / support tests per shared range of a long entry
+constexpr long long LONG_WORK = 2 * CHUNK;  // combine probes above which a column's Q_c is shared GPU-wide
 
 __device__ __forceinline__ long long slot_of(const QArgs &a, long long g) {
     if (a.slot_len > 0) return (g - a.wb) * a.slot_len;
@@ -133,45 +142,103 @@ __device__ __forceinline__ long long lookup(const int *keys, const long long *va
 // shared-memory word instead of a linear-probing chain.
 __device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key * 0x85EBCA6Bu) >> 14; }
 
+// Uniform-value graphs: the fixed-point sum over one range of the (i, c) work,
+// warp-reduced.
+//   pull (push == false): C_i entries [lo, hi) -- coalesced row ids, Bloom
+//         filter, hash lookup;
+//   push (push == true):  support-list positions [lo, hi) tested against hub
+//         row i's bitmap (cost min(deg i, |supp Q_c|) instead of deg i).
+// The ranges of one pair can be split over warps: integer adds commute, so the
+// sum does not depend on the split, the path or any order (deterministic).
+__device__ __forceinline__ long long uniform_partial(const QArgs &a, const int *keys, const long long *vals,
+                                                     uint32_t mask, const int *lkeys, const long long *lvals,
+                                                     const unsigned *filt, int i, bool push, long long lo,
+                                                     long long hi, int lane) {
+    long long acc = 0;
+    if (push) {
+        const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
+        // PUSH_U tests in flight per lane: key load, then the dependent bitmap word
+        constexpr int PUSH_U = 4;
+        int hits = 0;
+        for (long long t0 = lo; t0 < hi; t0 += 32 * PUSH_U) {
+            int kv[PUSH_U];
+            unsigned wv[PUSH_U];
+#pragma unroll
+            for (int u = 0; u < PUSH_U; ++u) {
+                const long long t = t0 + 32 * u + lane;
+                kv[u] = t < hi ? lkeys[t] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PUSH_U; ++u) wv[u] = kv[u] >= 0 ? __ldg(bits + (kv[u] >> 5)) : 0u;
+#pragma unroll
+            for (int u = 0; u < PUSH_U; ++u)
+                if ((wv[u] >> (kv[u] & 31)) & 1u) {
+                    acc += lvals[t0 + 32 * u + lane];
+                    ++hits;
+                }
+        }
+        if (a.prof) {
+            hits = warp_sum_int(hits);
+            if (lane == 0) {
+                atomicAdd(a.prof + 3, 1ull);
+                atomicAdd(a.prof + 4, (unsigned long long)(hi - lo));
+                atomicAdd(a.prof + 5, (unsigned long long)hits);
+            }
+        }
+    } else {
+        // PULL_U row ids in flight per lane: long rows are scanned latency-
+        // bound otherwise (one L2 round trip per 64 ids)
+        constexpr int PULL_U = 8;
+        int fpass = 0, phit = 0;
+        for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
+            int jv[PULL_U];
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u) {
+                const long long e = e0 + 32 * u + lane;
+                jv[u] = e < hi ? __ldg(a.csc_rows + e) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u) {
+                if (jv[u] < 0) continue;
+                const uint32_t b = filter_bit(jv[u]);
+                if (filt[b >> 5] & (1u << (b & 31))) {
+                    const long long q = lookup(keys, vals, mask, jv[u]);
+                    acc += q;
+                    if (a.prof) {
+                        ++fpass;
+                        phit += q != 0;
+                    }
+                }
+            }
+        }
+        if (a.prof) {
+            fpass = warp_sum_int(fpass);
+            phit = warp_sum_int(phit);
+            if (lane == 0) {
+                atomicAdd(a.prof + 0, 1ull);
+                atomicAdd(a.prof + 1, (unsigned long long)(hi - lo));
+                atomicAdd(a.prof + 2, (unsigned long long)fpass);
+                atomicAdd(a.prof + 12, (unsigned long long)phit);
+            }
+        }
+    }
+    return warp_sum_ll(acc);
+}
+
+// push or pull for the stored entry (i, c), and the length of that work
+__device__ __forceinline__ bool use_push(const QArgs &a, int i, long long deg_i, int nsupp) {
+    return a.hub_of && 100 * deg_i > (long long)a.push_pct * nsupp && __ldg(a.hub_of + i) >= 0;
+}
+
 // Contribution of the stored entry (i, c): a_ic <Q_c, C_i>, one warp.
-//   pull: scan C_i (coalesced row ids), Bloom filter, hash lookup;
-//   push: for a hub row i longer than the table, scan the table's slots and
-//         test membership in i's bitmap (cost min(deg i, cap) instead of deg i).
-// On uniform-value graphs both paths add the fixed-point integers exactly, so
-// the value does not depend on the path or on any order (deterministic).
 __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, const long long *vals, uint32_t mask,
                                              const int *lkeys, const long long *lvals, int nsupp,
                                              const unsigned *filt, int E, int i, double aic, int lane) {
     const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
     if (a.uniform) {
-        long long acc = 0;
-        const int h = a.hub_of ? __ldg(a.hub_of + i) : -1;
-        if (h >= 0 && 100 * (ihi - ilo) > (long long)a.push_pct * nsupp) {  // push: the support list against i's bitmap
-            const unsigned *bits = a.hub_bits + (long long)h * a.hub_words;
-            for (int t = lane; t < nsupp; t += 32) {
-                const int k = lkeys[t];
-                if ((__ldg(bits + (k >> 5)) >> (k & 31)) & 1u) acc += lvals[t];
-            }
-        } else {
-            // PULL_U row ids in flight per lane: long rows are scanned latency-
-            // bound otherwise (one L2 round trip per 64 ids)
-            constexpr int PULL_U = 8;
-            for (long long e0 = ilo; e0 < ihi; e0 += 32 * PULL_U) {
-                int jv[PULL_U];
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) {
-                    const long long e = e0 + 32 * u + lane;
-                    jv[u] = e < ihi ? __ldg(a.csc_rows + e) : -1;
-                }
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) {
-                    if (jv[u] < 0) continue;
-                    const uint32_t b = filter_bit(jv[u]);
-                    if (filt[b >> 5] & (1u << (b & 31))) acc += lookup(keys, vals, mask, jv[u]);
-                }
-            }
-        }
-        acc = warp_sum_ll(acc);
+        const bool push = use_push(a, i, ihi - ilo, nsupp);
+        const long long acc = push ? uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, true, 0, nsupp, lane)
+                                   : uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, false, ilo, ihi, lane);
         return aic * (a.value * ldexp((double)acc, -E));
     }
     double acc = 0.0;
@@ -197,7 +264,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
     __shared__ long long s_col, s_work, s_slot, s_off;
-    __shared__ int s_nsupp;
+    __shared__ int s_nsupp, s_next, s_nlong;
+    __shared__ int s_lt[MAX_LONG], s_lpre[MAX_LONG + 1];  // parked long entries (~t: push) and chunk prefix
+    __shared__ long long s_lacc[MAX_LONG];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
     long long *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
@@ -213,6 +282,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
         if (g0 == g1) continue;
         const long long s0 = slot_of(a, g0), m = slot_of(a, g1) - s0;
+        const long long t_start = a.prof ? clock64() : 0;
         long long need = m < a.n ? m : a.n;
         uint32_t cap = 32;
         while ((long long)cap < need * 2 && cap < (uint32_t)SCAP) cap <<= 1;  // load factor <= 1/2 if it fits smem
@@ -285,6 +355,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         }
         __syncthreads();
         const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
+        const long long t_built = a.prof ? clock64() : 0;
+        if (a.prof && tid == 0) {
+            atomicAdd(a.prof + 6, (unsigned long long)m);
+            atomicAdd(a.prof + 7, (unsigned long long)s_nsupp);
+            atomicAdd(a.prof + 8, 1ull);
+            atomicAdd(a.prof + 10, (unsigned long long)(t_built - t_start));
+        }
 
         // combine work of this column: sum of deg(i) over the entries (i, c)
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
@@ -327,15 +404,97 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 if (tid == 0) a.pool_nsupp[s_slot] = nsupp <= (int)cap ? nsupp : 0x3fffffff;
                 for (int t = tid; t < FILTER_WORDS; t += Q_THREADS)
                     a.pool_filt[s_slot * FILTER_WORDS + t] = filt[t];
+                if (a.prof && tid == 0) atomicAdd(a.prof + 9, 1ull);
                 continue;  // the loop-top barrier orders these copies before the table is reused
             }
         }
 
         // Eq. 20: for every stored (i, c): pcol = a_ic <Q_c, C_i>
-        for (long long t = warp; t < cn; t += Q_WARPS) {
-            const double v = pair_value(a, keys, vals, mask, lkeys, lvals, nsupp, filt, E, a.csc_rows[cs + t],
-                                        a.csc_vals[cs + t], lane);
-            if (lane == 0) a.pcol[cs + t] = v;
+        if (!a.uniform) {
+            for (long long t = warp; t < cn; t += Q_WARPS) {
+                const double v = pair_value(a, keys, vals, mask, lkeys, lvals, nsupp, filt, E, a.csc_rows[cs + t],
+                                            a.csc_vals[cs + t], lane);
+                if (lane == 0) a.pcol[cs + t] = v;
+            }
+        } else {
+            // Uniform values: warps take entries dynamically; an entry whose
+            // scan is longer than LONG_WORK is parked and, once every short
+            // entry is done, split into CHUNK-long ranges that all warps share
+            // (one warp per entry left the CTA waiting on its longest scan).
+            // Range sums are int64 and added with shared atomics: the same
+            // exact total as one warp's scan.
+            if (tid == 0) {
+                s_next = 0;
+                s_nlong = 0;
+            }
+            __syncthreads();
+            while (true) {
+                int t = 0;
+                if (lane == 0) t = atomicAdd(&s_next, 1);
+                t = __shfl_sync(MCF_FULL, t, 0);
+                if (t >= cn) break;
+                const int i = a.csc_rows[cs + t];
+                const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+                const bool push = use_push(a, i, ihi - ilo, nsupp);
+                const long long len = push ? nsupp : ihi - ilo;
+                if (len > LONG_WORK) {
+                    int slot = 0;
+                    if (lane == 0) slot = atomicAdd(&s_nlong, 1);
+                    slot = __shfl_sync(MCF_FULL, slot, 0);
+                    if (slot < MAX_LONG) {
+                        if (lane == 0) {
+                            s_lt[slot] = push ? ~t : t;
+                            s_lacc[slot] = 0;
+                        }
+                        continue;
+                    }
+                }
+                const long long acc = uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, push,
+                                                      push ? 0 : ilo, push ? nsupp : ihi, lane);
+                if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
+            }
+            __syncthreads();
+            const int nl = s_nlong < MAX_LONG ? s_nlong : MAX_LONG;
+            if (nl > 0) {
+                if (tid == 0) {
+                    s_next = 0;
+                    s_lpre[0] = 0;
+                    for (int j = 0; j < nl; ++j) {
+                        const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
+                        const int i = a.csc_rows[cs + t];
+                        const long long len = s_lt[j] < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
+                        s_lpre[j + 1] = s_lpre[j] + (int)((len + CHUNK - 1) / CHUNK);
+                    }
+                }
+                __syncthreads();
+                const int K = s_lpre[nl];
+                while (true) {
+                    int k = 0;
+                    if (lane == 0) k = atomicAdd(&s_next, 1);
+                    k = __shfl_sync(MCF_FULL, k, 0);
+                    if (k >= K) break;
+                    int j = 0;
+                    while (s_lpre[j + 1] <= k) ++j;
+                    const bool push = s_lt[j] < 0;
+                    const int t = push ? ~s_lt[j] : s_lt[j];
+                    const int i = a.csc_rows[cs + t];
+                    const long long base = push ? 0 : a.csc_ptr[i];
+                    const long long end = push ? nsupp : a.csc_ptr[i + 1];
+                    const long long lo = base + (long long)(k - s_lpre[j]) * CHUNK;
+                    const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
+                    const long long acc = uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, push, lo, hi, lane);
+                    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_lacc[j]), (unsigned long long)acc);
+                }
+                __syncthreads();
+                for (int j = tid; j < nl; j += Q_THREADS) {
+                    const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
+                    a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)s_lacc[j], -E));
+                }
+            }
+        }
+        if (a.prof) {
+            __syncthreads();
+            if (tid == 0) atomicAdd(a.prof + 11, (unsigned long long)(clock64() - t_built));
         }
     }
 }
@@ -479,6 +638,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     }
     q.value = g->value;
     q.colmax = colmax;
+    q.prof = nullptr;
+    static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
+    if (prof_on) {
+        MCF_CUDA(cudaMallocAsync(&q.prof, sizeof(unsigned long long) * PROF_SLOTS, s));
+        MCF_CUDA(cudaMemsetAsync(q.prof, 0, sizeof(unsigned long long) * PROF_SLOTS, s));
+    }
     q.gkeys = nullptr;
     q.gvals = nullptr;
     q.gcap = 0;
@@ -554,6 +719,16 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     }
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
+    if (q.prof) {
+        unsigned long long h[PROF_SLOTS];
+        MCF_CUDA(cudaMemcpyAsync(h, q.prof, sizeof(h), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        fprintf(stderr,
+                "[diag-prof] cols %llu big %llu emissions %llu support %llu | pull pairs %llu ids %llu filt %llu hits %llu"
+                " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | sum max pair %llu sum ideal %llu sum max warp %llu\n",
+                h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15]);
+        cudaFreeAsync(q.prof, s);
+    }
     cudaFreeAsync(counter, s);
     cudaFreeAsync(lbuf, s);
     if (gbuf) cudaFreeAsync(gbuf, s);

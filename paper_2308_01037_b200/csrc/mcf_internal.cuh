@@ -162,6 +162,8 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
     return v;
 }
 
+__device__ __forceinline__ int warp_sum_int(int v) { return __reduce_add_sync(MCF_FULL, v); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
