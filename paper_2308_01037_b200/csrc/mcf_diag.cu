@@ -18,7 +18,11 @@
 #include <cstdlib>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "mcf_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mcf {
 
@@ -82,11 +86,12 @@ struct QArgs {
     unsigned long long *pool_used, pool_cap;
     unsigned *pool_filt;        // FILTER_WORDS per record
     unsigned long long *prof;   // MCF_DIAG_PROF=1: combine counters (profiling only, else null)
+    int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
 };
 
 // prof slots: 0 pull pairs, 1 pull ids, 2 pull filter passes, 3 push pairs, 4 push tests, 5 push hits,
 // 6 emissions, 7 support, 8 columns, 9 big columns, 10 cycles Q build, 11 cycles combine, 12 pull hits
-constexpr int PROF_SLOTS = 16;
+constexpr int PROF_SLOTS = 20;  // 16..18: cluster-kernel columns, cycles, emissions
 
 struct BigRec {
     long long c;      // column
@@ -98,7 +103,18 @@ struct BigRec {
 constexpr long long BIG_WORK = 1ll << 20;
 constexpr int MAX_LONG = 64;            // parked long (i, c) entries per column
 constexpr long long CHUNK = 1024;       // ids / support tests per shared range of a long entry
-constexpr long long LONG_WORK = 2 * CHUNK;  // combine probes above which a column's Q_c is shared GPU-wide
+constexpr long long LONG_WORK = 2 * CHUNK;
+constexpr long long SMALL_NEED = (3ll * SCAP - 4) / 4;  // largest table need one CTA's shared table holds (load <= 3/4)
+
+// Cluster size whose distributed shared table (K x SCAP slots, load <= 3/4)
+// holds a column of `need` (<= emissions) entries: 0 if one CTA's table does,
+// or none of 2/4/8 (<= maxk) does (then k_diag_q's global table).
+__device__ __forceinline__ int cluster_class(long long need, int maxk) {
+    if (need <= SMALL_NEED) return 0;
+    for (int k = 2; k <= maxk; k <<= 1)
+        if ((long long)k * SCAP * 3 >= need * 4 + 4) return k;
+    return 0;
+}  // combine probes above which a column's Q_c is shared GPU-wide
 
 __device__ __forceinline__ long long slot_of(const QArgs &a, long long g) {
     if (a.slot_len > 0) return (g - a.wb) * a.slot_len;
@@ -150,10 +166,18 @@ __device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key 
 //         row i's bitmap (cost min(deg i, |supp Q_c|) instead of deg i).
 // The ranges of one pair can be split over warps: integer adds commute, so the
 // sum does not depend on the split, the path or any order (deterministic).
-__device__ __forceinline__ long long uniform_partial(const QArgs &a, const int *keys, const long long *vals,
-                                                     uint32_t mask, const int *lkeys, const long long *lvals,
-                                                     const unsigned *filt, int i, bool push, long long lo,
-                                                     long long hi, int lane) {
+// Q_c in this CTA's shared memory (or its global table, or dense by node id)
+struct LocalTable {
+    const int *keys;
+    const long long *vals;
+    uint32_t mask;
+    __device__ __forceinline__ long long get(int key) const { return lookup(keys, vals, mask, key); }
+};
+
+template <class Table>
+__device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table &tab, const int *lkeys,
+                                                     const long long *lvals, const unsigned *filt, int i, bool push,
+                                                     long long lo, long long hi, int lane) {
     long long acc = 0;
     if (push) {
         const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
@@ -202,7 +226,7 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const int *
                 if (jv[u] < 0) continue;
                 const uint32_t b = filter_bit(jv[u]);
                 if (filt[b >> 5] & (1u << (b & 31))) {
-                    const long long q = lookup(keys, vals, mask, jv[u]);
+                    const long long q = tab.get(jv[u]);
                     acc += q;
                     if (a.prof) {
                         ++fpass;
@@ -237,8 +261,9 @@ __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, co
     const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
     if (a.uniform) {
         const bool push = use_push(a, i, ihi - ilo, nsupp);
-        const long long acc = push ? uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, true, 0, nsupp, lane)
-                                   : uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, false, ilo, ihi, lane);
+        const LocalTable tab{keys, vals, mask};
+        const long long acc = push ? uniform_partial(a, tab, lkeys, lvals, filt, i, true, 0, nsupp, lane)
+                                   : uniform_partial(a, tab, lkeys, lvals, filt, i, false, ilo, ihi, lane);
         return aic * (a.value * ldexp((double)acc, -E));
     }
     double acc = 0.0;
@@ -284,6 +309,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         const long long s0 = slot_of(a, g0), m = slot_of(a, g1) - s0;
         const long long t_start = a.prof ? clock64() : 0;
         long long need = m < a.n ? m : a.n;
+        if (a.cl_maxk && cluster_class(need, a.cl_maxk)) continue;  // k_diag_qc builds this Q_c
         uint32_t cap = 32;
         while ((long long)cap < need * 2 && cap < (uint32_t)SCAP) cap <<= 1;  // load factor <= 1/2 if it fits smem
         while ((long long)cap * 3 < need * 4 + 4) cap <<= 1;                 // and <= 3/4 always
@@ -449,7 +475,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                         continue;
                     }
                 }
-                const long long acc = uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, push,
+                const long long acc = uniform_partial(a, LocalTable{keys, vals, mask}, lkeys, lvals, filt, i, push,
                                                       push ? 0 : ilo, push ? nsupp : ihi, lane);
                 if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
             }
@@ -482,7 +508,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     const long long end = push ? nsupp : a.csc_ptr[i + 1];
                     const long long lo = base + (long long)(k - s_lpre[j]) * CHUNK;
                     const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
-                    const long long acc = uniform_partial(a, keys, vals, mask, lkeys, lvals, filt, i, push, lo, hi, lane);
+                    const long long acc =
+                        uniform_partial(a, LocalTable{keys, vals, mask}, lkeys, lvals, filt, i, push, lo, hi, lane);
                     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_lacc[j]), (unsigned long long)acc);
                 }
                 __syncthreads();
@@ -495,7 +522,247 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         if (a.prof) {
             __syncthreads();
             if (tid == 0) atomicAdd(a.prof + 11, (unsigned long long)(clock64() - t_built));
+            if (tid == 0 && keys == gkeys) {
+                atomicAdd(a.prof + 13, 1ull);
+                atomicAdd(a.prof + 14, (unsigned long long)(clock64() - t_start));
+                atomicAdd(a.prof + 15, (unsigned long long)m);
+            }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Q_c wider than one CTA's shared table: a thread-block cluster of K CTAs (K
+// SMs) holds it in distributed shared memory -- slot s lives in CTA s / SCAP
+// -- instead of a global-memory table (whose random probes went to L2/HBM and
+// were ~90% of the combine time on R-MAT 2^22).  Same fixed-point Q_c, same
+// Bloom filter (each CTA ORs in the others' parts) and support list, same
+// Eq. 20 combine with every warp of the cluster sharing the (i, c) entries;
+// the int64 sums are the ones k_diag_q forms, so pcol is bit-identical.
+// Uniform-value graphs only (the combine's exact integer path).
+// ---------------------------------------------------------------------------
+struct ClusterTable {
+    const int *keys;  // this CTA's part (the same offset in every CTA of the cluster)
+    const long long *vals;
+    uint32_t mask;    // K * SCAP - 1
+    __device__ __forceinline__ long long get(int key) const {
+        cg::cluster_group cl = cg::this_cluster();
+        uint32_t s = hash_slot(key, mask);
+        while (true) {
+            const unsigned r = s / SCAP, l = s % SCAP;
+            const int k = cl.map_shared_rank(keys, r)[l];
+            if (k == key) return cl.map_shared_rank(vals, r)[l];
+            if (k == EMPTY_KEY) return 0;
+            s = (s + 1) & mask;
+        }
+    }
+};
+
+__device__ __forceinline__ uint32_t cluster_find_or_insert(int *keys, uint32_t mask, int key) {
+    cg::cluster_group cl = cg::this_cluster();
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        int *kp = cl.map_shared_rank(keys, s / SCAP) + (s % SCAP);
+        const int k = *kp;
+        if (k == key) return s;
+        if (k == EMPTY_KEY) {
+            const int old = atomicCAS(kp, EMPTY_KEY, key);
+            if (old == EMPTY_KEY || old == key) return s;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+template <int K>
+__global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
+    k_diag_qc(QArgs a, const int *__restrict__ cols, unsigned ncols, unsigned *__restrict__ next_col) {
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    long long *svals = reinterpret_cast<long long *>(smem_raw);
+    int *skeys = reinterpret_cast<int *>(svals + SCAP);
+    unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
+    __shared__ long long s_col;
+    __shared__ int s_nsupp, s_next, s_nlong;  // rank 0's are the cluster's
+    __shared__ int s_lt[MAX_LONG], s_lpre[MAX_LONG + 1];
+    __shared__ long long s_lacc[MAX_LONG];
+    int *r0_nsupp = cl.map_shared_rank(&s_nsupp, 0), *r0_next = cl.map_shared_rank(&s_next, 0);
+    int *r0_nlong = cl.map_shared_rank(&s_nlong, 0), *r0_lt = cl.map_shared_rank(s_lt, 0);
+    int *r0_lpre = cl.map_shared_rank(s_lpre, 0);
+    long long *r0_lacc = cl.map_shared_rank(s_lacc, 0);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const long long lcap = (long long)K * a.lcap;  // the cluster's K consecutive per-CTA list regions
+    int *lkeys = a.lkeys + (long long)(blockIdx.x / K) * lcap;
+    long long *lvals = a.lvals + (long long)(blockIdx.x / K) * lcap;
+    const uint32_t mask = (uint32_t)K * SCAP - 1;
+    const long long CT = (long long)K * Q_THREADS, gt = (long long)rank * Q_THREADS + tid;
+    const ClusterTable tab{skeys, svals, mask};
+
+    while (true) {
+        for (int t = tid; t < SCAP; t += Q_THREADS) {
+            skeys[t] = EMPTY_KEY;
+            svals[t] = 0;
+        }
+        for (int t = tid; t < FILTER_WORDS; t += Q_THREADS) filt[t] = 0u;
+        if (rank == 0 && tid == 0) {
+            const unsigned x = atomicAdd(next_col, 1u);
+            const long long c = x < ncols ? (long long)cols[x] : -1;
+            for (int r = 0; r < K; ++r) *cl.map_shared_rank(&s_col, r) = c;  // every CTA reads its own copy
+            s_nsupp = 0;
+            s_next = 0;
+            s_nlong = 0;
+        }
+        cl.sync();
+        const long long c = s_col;
+        if (c < 0) break;
+        const long long t_start = a.prof ? clock64() : 0;
+        const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
+        const long long s0 = slot_of(a, g0), m = slot_of(a, g1) - s0;
+        const double maxw = __longlong_as_double((long long)a.colmax[c]);
+        int lg_m = 0;
+        while ((1ll << lg_m) < m) ++lg_m;
+        const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // as k_diag_q: sum of m terms < 2^62
+        constexpr int U = 4;
+        for (long long base = 0; base < m; base += (long long)U * CT) {
+            int sv[U];
+            double wv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long i = base + (long long)u * CT + gt;
+                sv[u] = i < m ? __ldcs(a.est + s0 + i) : EMPTY_KEY;
+                wv[u] = i < m ? __ldcs(a.ewt + s0 + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (sv[u] < 0) continue;
+                const long long q = __double2ll_rn(ldexp(wv[u], E));
+                const uint32_t slot = cluster_find_or_insert(skeys, mask, sv[u]);
+                atomicAdd(reinterpret_cast<unsigned long long *>(cl.map_shared_rank(svals, slot / SCAP) + slot % SCAP),
+                          (unsigned long long)q);
+            }
+        }
+        cl.sync();
+        // this CTA's part: Bloom bits and its share of the support list
+        for (int t = tid; t < SCAP; t += Q_THREADS) {
+            const int key = skeys[t];
+            if (key != EMPTY_KEY) {
+                const uint32_t b = filter_bit(key);
+                atomicOr(&filt[b >> 5], 1u << (b & 31));
+                const int p = atomicAdd(r0_nsupp, 1);
+                if (p < lcap) {
+                    lkeys[p] = key;
+                    lvals[p] = svals[t];
+                }
+            }
+        }
+        cl.sync();
+        // OR in the other parts' filters.  Only this CTA writes its filter and
+        // OR only adds bits, so a CTA reading it meanwhile still sees a superset
+        // of this part's keys.
+        for (int r = 1; r < K; ++r) {
+            const unsigned *rf = cl.map_shared_rank(filt, (rank + r) % K);
+            for (int t = tid; t < FILTER_WORDS; t += Q_THREADS) filt[t] |= rf[t];
+        }
+        __syncthreads();
+        const int nsupp_all = *r0_nsupp;
+        const int nsupp = nsupp_all <= lcap ? nsupp_all : 0x3fffffff;  // overflow: never push
+        const long long t_built = a.prof ? clock64() : 0;
+        const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        while (true) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(r0_next, 1);
+            t = __shfl_sync(MCF_FULL, t, 0);
+            if (t >= cn) break;
+            const int i = a.csc_rows[cs + t];
+            const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+            const bool push = use_push(a, i, ihi - ilo, nsupp);
+            const long long len = push ? nsupp : ihi - ilo;
+            if (len > LONG_WORK) {
+                int slot = 0;
+                if (lane == 0) slot = atomicAdd(r0_nlong, 1);
+                slot = __shfl_sync(MCF_FULL, slot, 0);
+                if (slot < MAX_LONG) {
+                    if (lane == 0) {
+                        r0_lt[slot] = push ? ~t : t;
+                        r0_lacc[slot] = 0;
+                    }
+                    continue;
+                }
+            }
+            const long long acc =
+                uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo, push ? nsupp : ihi, lane);
+            if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
+        }
+        cl.sync();
+        const int nl_all = *r0_nlong;
+        const int nl = nl_all < MAX_LONG ? nl_all : MAX_LONG;
+        if (nl > 0) {
+            if (rank == 0 && tid == 0) {
+                s_next = 0;
+                s_lpre[0] = 0;
+                for (int j = 0; j < nl; ++j) {
+                    const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
+                    const int i = a.csc_rows[cs + t];
+                    const long long len = s_lt[j] < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
+                    s_lpre[j + 1] = s_lpre[j] + (int)((len + CHUNK - 1) / CHUNK);
+                }
+            }
+            cl.sync();
+            if (rank != 0) {  // local copies of the parked list (read once per chunk below)
+                for (int j = tid; j <= nl; j += Q_THREADS) {
+                    s_lpre[j] = r0_lpre[j];
+                    if (j < nl) s_lt[j] = r0_lt[j];
+                }
+                __syncthreads();
+            }
+            const int KC = s_lpre[nl];
+            while (true) {
+                int k = 0;
+                if (lane == 0) k = atomicAdd(r0_next, 1);
+                k = __shfl_sync(MCF_FULL, k, 0);
+                if (k >= KC) break;
+                int j = 0;
+                while (s_lpre[j + 1] <= k) ++j;
+                const bool push = s_lt[j] < 0;
+                const int t = push ? ~s_lt[j] : s_lt[j];
+                const int i = a.csc_rows[cs + t];
+                const long long base = push ? 0 : a.csc_ptr[i];
+                const long long end = push ? nsupp : a.csc_ptr[i + 1];
+                const long long lo = base + (long long)(k - s_lpre[j]) * CHUNK;
+                const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
+                const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
+                if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(r0_lacc + j), (unsigned long long)acc);
+            }
+            cl.sync();
+            if (rank == 0)
+                for (int j = tid; j < nl; j += Q_THREADS) {
+                    const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
+                    a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)s_lacc[j], -E));
+                }
+        }
+        if (a.prof && rank == 0 && tid == 0) {
+            atomicAdd(a.prof + 16, 1ull);
+            atomicAdd(a.prof + 17, (unsigned long long)(clock64() - t_start));
+            atomicAdd(a.prof + 18, (unsigned long long)m);
+            atomicAdd(a.prof + 19, (unsigned long long)(t_built - t_start));
+        }
+        cl.sync();  // every remote access of this column is done before the tables and counters are reset
+    }
+}
+
+// columns of [col_begin, col_end) by the cluster size their table needs: list k
+// (K = 2 << k) at cols + k * ncol, counts in cnt[k]
+__global__ void k_cluster_classify(QArgs a, int *__restrict__ cols, long long ncol, unsigned *__restrict__ cnt) {
+    for (long long c = a.col_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; c < a.col_end;
+         c += (long long)gridDim.x * blockDim.x) {
+        const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
+        if (g0 == g1) continue;
+        const long long m = slot_of(a, g1) - slot_of(a, g0);
+        const int k = cluster_class(m < a.n ? m : a.n, a.cl_maxk);
+        if (!k) continue;
+        const int li = k == 2 ? 0 : (k == 4 ? 1 : 2);
+        const unsigned p = atomicAdd(cnt + li, 1u);
+        cols[li * ncol + p] = (int)c;
     }
 }
 
@@ -659,7 +926,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.gkeys = reinterpret_cast<int *>(q.gvals + (size_t)grid * cap);
     }
     // per-CTA support lists (push path): up to half the largest table
-    q.lcap = (cap > SCAP ? cap : SCAP) / 2;
+    q.lcap = cap > 2 * SCAP ? cap / 2 : SCAP;  // >= SCAP: a cluster's list spans its CTAs' regions
     unsigned char *lbuf = nullptr;
     MCF_CUDA(cudaMallocAsync(&lbuf, (size_t)grid * q.lcap * (sizeof(int) + sizeof(long long)), s));
     q.lvals = reinterpret_cast<long long *>(lbuf);
@@ -693,6 +960,49 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     }
     size_t smem = (size_t)SCAP * (sizeof(int) + sizeof(long long)) + FILTER_WORDS * sizeof(unsigned);
     MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // clusters of 2/4/8 CTAs for tables wider than one CTA's shared memory
+    // (uniform-value graphs above the dense size; MCF_DIAG_CLUSTER=0 disables)
+    const char *cl_e = getenv("MCF_DIAG_CLUSTER");
+    const int cl_env = cl_e ? atoi(cl_e) : 8;
+    int cl_grid[3] = {0, 0, 0};
+    q.cl_maxk = 0;
+    if (q.uniform && g->n > DENSE_N && cl_env >= 2) {
+        for (int k = 0; k < 3 && (2 << k) <= cl_env; ++k) {
+            int nc = 0;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 << k);
+            cfg.blockDim = dim3(Q_THREADS);
+            cfg.dynamicSmemBytes = smem;
+            cudaError_t e;
+            if (k == 0) {
+                cudaFuncSetAttribute(k_diag_qc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                e = cudaOccupancyMaxActiveClusters(&nc, (void *)k_diag_qc<2>, &cfg);
+            } else if (k == 1) {
+                cudaFuncSetAttribute(k_diag_qc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                e = cudaOccupancyMaxActiveClusters(&nc, (void *)k_diag_qc<4>, &cfg);
+            } else {
+                cudaFuncSetAttribute(k_diag_qc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                e = cudaOccupancyMaxActiveClusters(&nc, (void *)k_diag_qc<8>, &cfg);
+            }
+            if (e != cudaSuccess || nc < 1) {
+                cudaGetLastError();
+                break;
+            }
+            cl_grid[k] = nc * (2 << k);
+            q.cl_maxk = 2 << k;
+        }
+    }
+    int *cl_cols = nullptr;
+    unsigned *cl_cnt = nullptr;
+    const long long ncol = ce - cb;
+    if (q.cl_maxk) {
+        MCF_CUDA(cudaMallocAsync(&cl_cols, sizeof(int) * 3 * (size_t)ncol + 32, s));
+        cl_cnt = reinterpret_cast<unsigned *>(cl_cols + 3 * ncol);
+        MCF_CUDA(cudaMemsetAsync(cl_cnt, 0, 32, s));
+        k_cluster_classify<<<sm_count() * 4, 256, 0, s>>>(q, cl_cols, ncol, cl_cnt);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_cluster_classify");
+    }
     int rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
     k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
@@ -717,6 +1027,22 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         }
         cudaFreeAsync(pool, s);
     }
+    if (q.cl_maxk) {
+        unsigned hc[8];
+        MCF_CUDA(cudaMemcpyAsync(hc, cl_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        for (int k = 0; k < 3; ++k) {
+            if (!hc[k]) continue;
+            const int *lst = cl_cols + k * ncol;
+            unsigned *nxt = cl_cnt + 4 + k;
+            if (k == 0) k_diag_qc<2><<<cl_grid[0], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
+            else if (k == 1) k_diag_qc<4><<<cl_grid[1], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
+            else k_diag_qc<8><<<cl_grid[2], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
+            mcf::note_launch();
+            MCF_LAUNCHED("k_diag_qc");
+        }
+        cudaFreeAsync(cl_cols, s);
+    }
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
     if (q.prof) {
@@ -725,8 +1051,8 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         MCF_CUDA(cudaStreamSynchronize(s));
         fprintf(stderr,
                 "[diag-prof] cols %llu big %llu emissions %llu support %llu | pull pairs %llu ids %llu filt %llu hits %llu"
-                " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | sum max pair %llu sum ideal %llu sum max warp %llu\n",
-                h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15]);
+                " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | gtable cols %llu cycles %llu emissions %llu | cluster cols %llu cycles %llu emissions %llu build %llu\n",
+                h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15], h[16], h[17], h[18], h[19]);
         cudaFreeAsync(q.prof, s);
     }
     cudaFreeAsync(counter, s);

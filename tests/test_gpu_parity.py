@@ -427,6 +427,46 @@ def test_diag_hub_push_path_bitwise_and_replay(mc):
     assert rel_err(out.values, run.payload) < REL
 
 
+def _multi_hub_graph(seed=0, n=40000, hub_degs=(1500, 3000, 6000, 12000, 24000)):
+    """Uniform-value graph above the dense-Q size with hubs of several degrees,
+    so the hub columns' Q_c need clusters of 2, 4 and 8 CTAs (and one a global
+    table)."""
+    rng = np.random.default_rng(seed)
+    us, vs = [rng.integers(0, n, 6 * n)], [rng.integers(0, n, 6 * n)]
+    for h, d in enumerate(hub_degs):
+        us.append(np.full(d, h, dtype=np.int64))
+        vs.append(rng.choice(np.arange(len(hub_degs), n), d, replace=False))
+    u, v = np.concatenate(us), np.concatenate(vs)
+    keep = u != v
+    m = sparse.coo_array((np.ones(2 * keep.sum()), (np.r_[u[keep], v[keep]], np.r_[v[keep], u[keep]])), shape=(n, n))
+    m = sparse.csr_array(m)
+    m.sum_duplicates()
+    m.data[:] = 1.0
+    a = port.Csr.from_any(m)
+    lam = float(__import__("scipy.sparse.linalg", fromlist=["eigsh"]).eigsh(m, k=1, which="LA", v0=np.ones(n))[0][0])
+    return a.scaled(1.0 / lam)
+
+
+def test_diag_cluster_tables_bitwise(mc):
+    """Q_c wider than one CTA's shared table is held by a cluster of 2/4/8 CTAs
+    in distributed shared memory (k_diag_qc): the estimate equals the
+    global-table path (MCF_DIAG_CLUSTER=0) bit for bit, for every cluster cap."""
+    import os
+    a = _multi_hub_graph()
+    g = mc.DeviceGraph(as_matrix(a, True))
+    cfg = mc.WalkConfig(a.n * 120, 1e-300, 20, 5)
+    outs = {}
+    try:
+        for k in ("0", "2", "4", "8"):
+            os.environ["MCF_DIAG_CLUSTER"] = k
+            outs[k] = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+    finally:
+        os.environ.pop("MCF_DIAG_CLUSTER", None)
+    for k in ("2", "4", "8"):
+        assert np.array_equal(outs[k], outs["0"]), k
+    assert np.all(np.isfinite(outs["0"])) and np.all(outs["0"] > 1.0)
+
+
 def test_rand_funm_full_consistency_and_closed_form(mc):
     """SPEC acceptance 4: diag(rand_funm) == rand_funm_diag (shared seed) to
     1e-12 relative on 16-node instances; SPEC.md:352 closed form; A = 0."""
