@@ -86,6 +86,10 @@ struct QArgs {
     unsigned long long *pool_used, pool_cap;
     unsigned *pool_filt;        // FILTER_WORDS per record
     unsigned long long *prof;   // MCF_DIAG_PROF=1: combine counters (profiling only, else null)
+    int *llist;                 // per-CTA lists of long (i, c) entries (~t: push), llcap each
+    long long llcap;
+    long long long_work;        // LONG_WORK (MCF_DIAG_LONG_WORK overrides: tests)
+    long long big_work;         // BIG_WORK (MCF_DIAG_BIG_WORK overrides: tests)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
 };
 
@@ -104,6 +108,11 @@ constexpr long long BIG_WORK = 1ll << 20;
 constexpr int MAX_LONG = 64;            // parked long (i, c) entries per column
 constexpr long long CHUNK = 1024;       // ids / support tests per shared range of a long entry
 constexpr long long LONG_WORK = 2 * CHUNK;
+// cluster tables are sized for load <= CL_LOAD_NUM / CL_LOAD_DEN (by emission count)
+#ifndef CL_LOAD_NUM
+#define CL_LOAD_NUM 1
+#define CL_LOAD_DEN 1
+#endif
 constexpr long long SMALL_NEED = (3ll * SCAP - 4) / 4;  // largest table need one CTA's shared table holds (load <= 3/4)
 
 // Cluster size whose distributed shared table (K x SCAP slots, load <= 3/4)
@@ -112,7 +121,7 @@ constexpr long long SMALL_NEED = (3ll * SCAP - 4) / 4;  // largest table need on
 __device__ __forceinline__ int cluster_class(long long need, int maxk) {
     if (need <= SMALL_NEED) return 0;
     for (int k = 2; k <= maxk; k <<= 1)
-        if ((long long)k * SCAP * 3 >= need * 4 + 4) return k;
+        if ((long long)k * SCAP * CL_LOAD_DEN >= need * CL_LOAD_NUM + 4) return k;
     return 0;
 }  // combine probes above which a column's Q_c is shared GPU-wide
 
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         __syncthreads();
         if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_work), (unsigned long long)work);
         __syncthreads();
-        if (s_work > BIG_WORK && a.big && keys) {
+        if (s_work > a.big_work && a.big && keys) {
             // hand Q_c to k_diag_big: all warps of the GPU share the combine
             if (tid == 0) {
                 s_slot = -1;
@@ -444,16 +453,18 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             }
         } else {
             // Uniform values: warps take entries dynamically; an entry whose
-            // scan is longer than LONG_WORK is parked and, once every short
-            // entry is done, split into CHUNK-long ranges that all warps share
-            // (one warp per entry left the CTA waiting on its longest scan).
-            // Range sums are int64 and added with shared atomics: the same
-            // exact total as one warp's scan.
+            // scan is longer than LONG_WORK is listed and, once every short
+            // entry is done, split into CHUNK-long ranges that all warps share,
+            // MAX_LONG listed entries at a time (one warp per entry left the
+            // CTA waiting on its longest scan).  Range sums are int64 and added
+            // with shared atomics: the same exact total as one warp's scan.
+            int *llist = a.llist + (long long)blockIdx.x * a.llcap;
             if (tid == 0) {
                 s_next = 0;
                 s_nlong = 0;
             }
             __syncthreads();
+            const LocalTable tab{keys, vals, mask};
             while (true) {
                 int t = 0;
                 if (lane == 0) t = atomicAdd(&s_next, 1);
@@ -463,32 +474,33 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
                 const bool push = use_push(a, i, ihi - ilo, nsupp);
                 const long long len = push ? nsupp : ihi - ilo;
-                if (len > LONG_WORK) {
+                if (len > a.long_work) {
                     int slot = 0;
                     if (lane == 0) slot = atomicAdd(&s_nlong, 1);
                     slot = __shfl_sync(MCF_FULL, slot, 0);
-                    if (slot < MAX_LONG) {
-                        if (lane == 0) {
-                            s_lt[slot] = push ? ~t : t;
-                            s_lacc[slot] = 0;
-                        }
+                    if (slot < a.llcap) {  // (a full list: this warp scans the entry itself)
+                        if (lane == 0) llist[slot] = push ? ~t : t;
                         continue;
                     }
                 }
-                const long long acc = uniform_partial(a, LocalTable{keys, vals, mask}, lkeys, lvals, filt, i, push,
-                                                      push ? 0 : ilo, push ? nsupp : ihi, lane);
+                const long long acc =
+                    uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo, push ? nsupp : ihi, lane);
                 if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
             }
             __syncthreads();
-            const int nl = s_nlong < MAX_LONG ? s_nlong : MAX_LONG;
-            if (nl > 0) {
+            const int nlong = s_nlong < a.llcap ? s_nlong : (int)a.llcap;
+            for (int g0 = 0; g0 < nlong; g0 += MAX_LONG) {
+                const int nl = nlong - g0 < MAX_LONG ? nlong - g0 : MAX_LONG;
                 if (tid == 0) {
                     s_next = 0;
                     s_lpre[0] = 0;
                     for (int j = 0; j < nl; ++j) {
-                        const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
+                        const int lt = llist[g0 + j];
+                        const int t = lt < 0 ? ~lt : lt;
                         const int i = a.csc_rows[cs + t];
-                        const long long len = s_lt[j] < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
+                        const long long len = lt < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
+                        s_lt[j] = lt;
+                        s_lacc[j] = 0;
                         s_lpre[j + 1] = s_lpre[j] + (int)((len + CHUNK - 1) / CHUNK);
                     }
                 }
@@ -508,8 +520,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     const long long end = push ? nsupp : a.csc_ptr[i + 1];
                     const long long lo = base + (long long)(k - s_lpre[j]) * CHUNK;
                     const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
-                    const long long acc =
-                        uniform_partial(a, LocalTable{keys, vals, mask}, lkeys, lvals, filt, i, push, lo, hi, lane);
+                    const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
                     if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_lacc[j]), (unsigned long long)acc);
                 }
                 __syncthreads();
@@ -517,6 +528,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
                     a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)s_lacc[j], -E));
                 }
+                __syncthreads();
             }
         }
         if (a.prof) {
@@ -582,13 +594,12 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
     long long *svals = reinterpret_cast<long long *>(smem_raw);
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
-    __shared__ long long s_col;
+    __shared__ long long s_col, s_work, s_slot, s_off;
     __shared__ int s_nsupp, s_next, s_nlong;  // rank 0's are the cluster's
     __shared__ int s_lt[MAX_LONG], s_lpre[MAX_LONG + 1];
     __shared__ long long s_lacc[MAX_LONG];
     int *r0_nsupp = cl.map_shared_rank(&s_nsupp, 0), *r0_next = cl.map_shared_rank(&s_next, 0);
-    int *r0_nlong = cl.map_shared_rank(&s_nlong, 0), *r0_lt = cl.map_shared_rank(s_lt, 0);
-    int *r0_lpre = cl.map_shared_rank(s_lpre, 0);
+    int *r0_nlong = cl.map_shared_rank(&s_nlong, 0);
     long long *r0_lacc = cl.map_shared_rank(s_lacc, 0);
     const int tid = threadIdx.x, lane = tid & 31;
     const long long lcap = (long long)K * a.lcap;  // the cluster's K consecutive per-CTA list regions
@@ -611,6 +622,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             s_nsupp = 0;
             s_next = 0;
             s_nlong = 0;
+            s_work = 0;
         }
         cl.sync();
         const long long c = s_col;
@@ -668,6 +680,60 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         const int nsupp = nsupp_all <= lcap ? nsupp_all : 0x3fffffff;  // overflow: never push
         const long long t_built = a.prof ? clock64() : 0;
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        if (a.big) {
+            // combine work sum_{i in C_c} deg(i): above BIG_WORK the table goes to
+            // the pool and k_diag_big spreads the entries over the whole GPU (as
+            // k_diag_q does) instead of K SMs working through it at the tail
+            long long work = 0;
+            for (long long t = gt; t < cn; t += CT) {
+                const int i = a.csc_rows[cs + t];
+                work += a.csc_ptr[i + 1] - a.csc_ptr[i];
+            }
+            work = warp_sum_ll(work);
+            if (lane == 0 && work)
+                atomicAdd(reinterpret_cast<unsigned long long *>(cl.map_shared_rank(&s_work, 0)),
+                          (unsigned long long)work);
+            cl.sync();
+            if (rank == 0 && tid == 0) {
+                long long slot = -1, off = 0;
+                const unsigned long long cap = (unsigned long long)K * SCAP;
+                if (s_work > a.big_work && nsupp_all <= (int)cap) {
+                    const unsigned long long o = atomicAdd(a.pool_used, 2ull * cap);
+                    if (o + 2ull * cap <= a.pool_cap) {
+                        const unsigned r = atomicAdd(a.n_big, 1u);
+                        if (r < a.max_big) {
+                            a.big[r] = BigRec{c, (long long)o, (unsigned)cap, (unsigned)cn};
+                            a.pool_E[r] = E;
+                            a.pool_nsupp[r] = nsupp_all;
+                            slot = (long long)r;
+                            off = (long long)o;
+                        }
+                    }
+                }
+                for (int r = 0; r < K; ++r) {
+                    *cl.map_shared_rank(&s_slot, r) = slot;
+                    *cl.map_shared_rank(&s_off, r) = off;
+                }
+            }
+            cl.sync();
+            if (s_slot >= 0) {
+                const long long cap = (long long)K * SCAP, base = s_off + (long long)rank * SCAP;
+                for (int t = tid; t < SCAP; t += Q_THREADS) {
+                    a.pool_keys[base + t] = skeys[t];
+                    a.pool_vals[base + t] = svals[t];
+                }
+                for (long long t = gt; t < nsupp_all; t += CT) {  // support list after the table
+                    a.pool_keys[s_off + cap + t] = lkeys[t];
+                    a.pool_vals[s_off + cap + t] = lvals[t];
+                }
+                if (rank == 0)
+                    for (int t = tid; t < FILTER_WORDS; t += Q_THREADS) a.pool_filt[s_slot * FILTER_WORDS + t] = filt[t];
+                if (a.prof && rank == 0 && tid == 0) atomicAdd(a.prof + 9, 1ull);
+                cl.sync();  // copies done before the next column resets the tables and lists
+                continue;
+            }
+        }
+        int *llist = a.llist + (long long)(blockIdx.x - rank) * a.llcap;  // the cluster's (rank 0's) long list
         while (true) {
             int t = 0;
             if (lane == 0) t = atomicAdd(r0_next, 1);
@@ -677,15 +743,12 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
             const bool push = use_push(a, i, ihi - ilo, nsupp);
             const long long len = push ? nsupp : ihi - ilo;
-            if (len > LONG_WORK) {
+            if (len > a.long_work) {
                 int slot = 0;
                 if (lane == 0) slot = atomicAdd(r0_nlong, 1);
                 slot = __shfl_sync(MCF_FULL, slot, 0);
-                if (slot < MAX_LONG) {
-                    if (lane == 0) {
-                        r0_lt[slot] = push ? ~t : t;
-                        r0_lacc[slot] = 0;
-                    }
+                if (slot < a.llcap) {
+                    if (lane == 0) llist[slot] = push ? ~t : t;
                     continue;
                 }
             }
@@ -694,27 +757,24 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
         }
         cl.sync();
-        const int nl_all = *r0_nlong;
-        const int nl = nl_all < MAX_LONG ? nl_all : MAX_LONG;
-        if (nl > 0) {
-            if (rank == 0 && tid == 0) {
-                s_next = 0;
+        const int nlong_all = *r0_nlong;
+        const int nlong = nlong_all < a.llcap ? nlong_all : (int)a.llcap;
+        for (int g0 = 0; g0 < nlong; g0 += MAX_LONG) {
+            const int nl = nlong - g0 < MAX_LONG ? nlong - g0 : MAX_LONG;
+            if (tid == 0) {  // every CTA builds the same local copy of the group's chunk prefix
                 s_lpre[0] = 0;
                 for (int j = 0; j < nl; ++j) {
-                    const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
+                    const int lt = llist[g0 + j];
+                    const int t = lt < 0 ? ~lt : lt;
                     const int i = a.csc_rows[cs + t];
-                    const long long len = s_lt[j] < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
+                    const long long len = lt < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
+                    s_lt[j] = lt;
                     s_lpre[j + 1] = s_lpre[j] + (int)((len + CHUNK - 1) / CHUNK);
+                    if (rank == 0) s_lacc[j] = 0;
                 }
+                if (rank == 0) s_next = 0;
             }
             cl.sync();
-            if (rank != 0) {  // local copies of the parked list (read once per chunk below)
-                for (int j = tid; j <= nl; j += Q_THREADS) {
-                    s_lpre[j] = r0_lpre[j];
-                    if (j < nl) s_lt[j] = r0_lt[j];
-                }
-                __syncthreads();
-            }
             const int KC = s_lpre[nl];
             while (true) {
                 int k = 0;
@@ -739,6 +799,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                     const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
                     a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)s_lacc[j], -E));
                 }
+            __syncthreads();
         }
         if (a.prof && rank == 0 && tid == 0) {
             atomicAdd(a.prof + 16, 1ull);
@@ -906,6 +967,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.value = g->value;
     q.colmax = colmax;
     q.prof = nullptr;
+    {
+        const char *e = getenv("MCF_DIAG_BIG_WORK");
+        q.big_work = e ? atoll(e) : BIG_WORK;
+        e = getenv("MCF_DIAG_LONG_WORK");
+        q.long_work = e ? atoll(e) : LONG_WORK;
+    }
     static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
     if (prof_on) {
         MCF_CUDA(cudaMallocAsync(&q.prof, sizeof(unsigned long long) * PROF_SLOTS, s));
@@ -931,6 +998,11 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     MCF_CUDA(cudaMallocAsync(&lbuf, (size_t)grid * q.lcap * (sizeof(int) + sizeof(long long)), s));
     q.lvals = reinterpret_cast<long long *>(lbuf);
     q.lkeys = reinterpret_cast<int *>(q.lvals + (size_t)grid * q.lcap);
+    // lists of long (i, c) entries: one per CTA, max_degree entries (a column's
+    // length on symmetric graphs; longer columns scan the overflow inline)
+    q.llcap = g->info.max_degree > 64 ? g->info.max_degree : 64;
+    if (q.llcap > (1ll << 24)) q.llcap = 1ll << 24;
+    MCF_CUDA(cudaMallocAsync(&q.llist, sizeof(int) * (size_t)grid * q.llcap, s));
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) * 4, s));
@@ -1008,6 +1080,22 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
     mcf::note_launch();
     MCF_LAUNCHED("k_diag_q");
+    if (q.cl_maxk) {
+        unsigned hc[8];
+        MCF_CUDA(cudaMemcpyAsync(hc, cl_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+        MCF_CUDA(cudaStreamSynchronize(s));
+        for (int k = 0; k < 3; ++k) {
+            if (!hc[k]) continue;
+            const int *lst = cl_cols + k * ncol;
+            unsigned *nxt = cl_cnt + 4 + k;
+            if (k == 0) k_diag_qc<2><<<cl_grid[0], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
+            else if (k == 1) k_diag_qc<4><<<cl_grid[1], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
+            else k_diag_qc<8><<<cl_grid[2], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
+            mcf::note_launch();
+            MCF_LAUNCHED("k_diag_qc");
+        }
+        cudaFreeAsync(cl_cols, s);
+    }
     if (q.big) {
         unsigned nrec = 0;
         MCF_CUDA(cudaMemcpyAsync(&nrec, q.n_big, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
@@ -1027,22 +1115,6 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         }
         cudaFreeAsync(pool, s);
     }
-    if (q.cl_maxk) {
-        unsigned hc[8];
-        MCF_CUDA(cudaMemcpyAsync(hc, cl_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
-        MCF_CUDA(cudaStreamSynchronize(s));
-        for (int k = 0; k < 3; ++k) {
-            if (!hc[k]) continue;
-            const int *lst = cl_cols + k * ncol;
-            unsigned *nxt = cl_cnt + 4 + k;
-            if (k == 0) k_diag_qc<2><<<cl_grid[0], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
-            else if (k == 1) k_diag_qc<4><<<cl_grid[1], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
-            else k_diag_qc<8><<<cl_grid[2], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
-            mcf::note_launch();
-            MCF_LAUNCHED("k_diag_qc");
-        }
-        cudaFreeAsync(cl_cols, s);
-    }
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
     if (q.prof) {
@@ -1056,6 +1128,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         cudaFreeAsync(q.prof, s);
     }
     cudaFreeAsync(counter, s);
+    cudaFreeAsync(q.llist, s);
     cudaFreeAsync(lbuf, s);
     if (gbuf) cudaFreeAsync(gbuf, s);
     return MCF_OK;

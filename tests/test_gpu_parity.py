@@ -450,7 +450,8 @@ def _multi_hub_graph(seed=0, n=40000, hub_degs=(1500, 3000, 6000, 12000, 24000))
 def test_diag_cluster_tables_bitwise(mc):
     """Q_c wider than one CTA's shared table is held by a cluster of 2/4/8 CTAs
     in distributed shared memory (k_diag_qc): the estimate equals the
-    global-table path (MCF_DIAG_CLUSTER=0) bit for bit, for every cluster cap."""
+    global-table path (MCF_DIAG_CLUSTER=0) bit for bit, for every cluster cap,
+    also when the columns' tables are handed to the GPU-wide k_diag_big."""
     import os
     a = _multi_hub_graph()
     g = mc.DeviceGraph(as_matrix(a, True))
@@ -458,13 +459,24 @@ def test_diag_cluster_tables_bitwise(mc):
     outs = {}
     try:
         for k in ("0", "2", "4", "8"):
-            os.environ["MCF_DIAG_CLUSTER"] = k
-            outs[k] = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+            # BIG_WORK 4096: most hub columns handed to k_diag_big; LONG_WORK 16:
+            # hundreds of (i, c) entries split into shared ranges, in groups
+            for big, long_ in ((None, None), ("4096", None), (None, "16")):
+                os.environ["MCF_DIAG_CLUSTER"] = k
+                for var, val in (("MCF_DIAG_BIG_WORK", big), ("MCF_DIAG_LONG_WORK", long_)):
+                    if val:
+                        os.environ[var] = val
+                    else:
+                        os.environ.pop(var, None)
+                outs[k, big, long_] = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
     finally:
         os.environ.pop("MCF_DIAG_CLUSTER", None)
-    for k in ("2", "4", "8"):
-        assert np.array_equal(outs[k], outs["0"]), k
-    assert np.all(np.isfinite(outs["0"])) and np.all(outs["0"] > 1.0)
+        os.environ.pop("MCF_DIAG_BIG_WORK", None)
+        os.environ.pop("MCF_DIAG_LONG_WORK", None)
+    ref = outs["0", None, None]
+    for key, v in outs.items():
+        assert np.array_equal(v, ref), key
+    assert np.all(np.isfinite(ref)) and np.all(ref > 1.0)
 
 
 def test_rand_funm_full_consistency_and_closed_form(mc):
