@@ -177,10 +177,15 @@ __device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key 
 // sum does not depend on the split, the path or any order (deterministic).
 // Q_c in this CTA's shared memory (or its global table, or dense by node id)
 struct LocalTable {
-    const int *keys;
+    const int *keys;  // null: dense Q_c indexed by node id
     const long long *vals;
     uint32_t mask;
+    bool global;      // table in global memory: probes batched (see uniform_partial)
+    static constexpr bool can_batch = true;
+    __device__ __forceinline__ bool batched() const { return global; }
     __device__ __forceinline__ long long get(int key) const { return lookup(keys, vals, mask, key); }
+    __device__ __forceinline__ int key_at(uint32_t s) const { return keys[s]; }
+    __device__ __forceinline__ long long val_at(uint32_t s) const { return vals[s]; }
 };
 
 template <class Table>
@@ -230,18 +235,66 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
                 const long long e = e0 + 32 * u + lane;
                 jv[u] = e < hi ? __ldg(a.csc_rows + e) : -1;
             }
+            if (!Table::can_batch || !tab.batched()) {
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    if (jv[u] < 0) continue;
+                    const uint32_t b = filter_bit(jv[u]);
+                    if (filt[b >> 5] & (1u << (b & 31))) {
+                        const long long q = tab.get(jv[u]);
+                        acc += q;
+                        if (a.prof) {
+                            ++fpass;
+                            phit += q != 0;
+                        }
+                    }
+                }
+                continue;
+            }
+            // global-memory tables: the Bloom-passing ids are probed together,
+            // every step of the PULL_U linear-probing chains one batch of
+            // independent loads (probing one id after another serialised L2
+            // round trips; in shared / distributed shared memory the scalar
+            // probe above is faster -- measured)
+            if constexpr (Table::can_batch) {
+            unsigned pend = 0u, hit = 0u;
+            uint32_t sl[PULL_U];
 #pragma unroll
             for (int u = 0; u < PULL_U; ++u) {
+                sl[u] = 0;
                 if (jv[u] < 0) continue;
                 const uint32_t b = filter_bit(jv[u]);
                 if (filt[b >> 5] & (1u << (b & 31))) {
-                    const long long q = tab.get(jv[u]);
-                    acc += q;
-                    if (a.prof) {
-                        ++fpass;
-                        phit += q != 0;
+                    pend |= 1u << u;
+                    sl[u] = hash_slot(jv[u], tab.mask);
+                }
+            }
+            if (a.prof) fpass += __popc(pend);
+            while (pend) {
+                int kv[PULL_U];
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) kv[u] = (pend >> u) & 1u ? tab.key_at(sl[u]) : EMPTY_KEY;
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    if (!((pend >> u) & 1u)) continue;
+                    if (kv[u] == jv[u]) {
+                        hit |= 1u << u;
+                        pend &= ~(1u << u);
+                    } else if (kv[u] == EMPTY_KEY) {
+                        pend &= ~(1u << u);
+                    } else {
+                        sl[u] = (sl[u] + 1) & tab.mask;
                     }
                 }
+            }
+            long long qv[PULL_U];
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u) qv[u] = (hit >> u) & 1u ? tab.val_at(sl[u]) : 0;
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u) {
+                acc += qv[u];
+                if (a.prof) phit += qv[u] != 0;
+            }
             }
         }
         if (a.prof) {
@@ -270,7 +323,7 @@ __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, co
     const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
     if (a.uniform) {
         const bool push = use_push(a, i, ihi - ilo, nsupp);
-        const LocalTable tab{keys, vals, mask};
+        const LocalTable tab{keys, vals, mask, true};  // k_diag_big: pool tables in global memory
         const long long acc = push ? uniform_partial(a, tab, lkeys, lvals, filt, i, true, 0, nsupp, lane)
                                    : uniform_partial(a, tab, lkeys, lvals, filt, i, false, ilo, ihi, lane);
         return aic * (a.value * ldexp((double)acc, -E));
@@ -464,7 +517,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 s_nlong = 0;
             }
             __syncthreads();
-            const LocalTable tab{keys, vals, mask};
+            const LocalTable tab{keys, vals, mask, keys != nullptr && keys == gkeys};
             while (true) {
                 int t = 0;
                 if (lane == 0) t = atomicAdd(&s_next, 1);
@@ -557,6 +610,8 @@ struct ClusterTable {
     const int *keys;  // this CTA's part (the same offset in every CTA of the cluster)
     const long long *vals;
     uint32_t mask;    // K * SCAP - 1
+    static constexpr bool can_batch = false;
+    __device__ __forceinline__ bool batched() const { return false; }
     __device__ __forceinline__ long long get(int key) const {
         cg::cluster_group cl = cg::this_cluster();
         uint32_t s = hash_slot(key, mask);
@@ -1034,8 +1089,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     MCF_CUDA(cudaFuncSetAttribute(k_diag_q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // clusters of 2/4/8 CTAs for tables wider than one CTA's shared memory
     // (uniform-value graphs above the dense size; MCF_DIAG_CLUSTER=0 disables)
+    // Measured: R-MAT 2^22 diag 10.1 -> 7.7 s with clusters up to 8; Chung-Lu
+    // 1.6e7 10.7 -> 11.5 s (its wide columns are hub columns of 10^4-10^5
+    // short entries, each probing remote shared memory).  Default: clusters
+    // below n = 2^23, global tables above; MCF_DIAG_CLUSTER=K overrides.
     const char *cl_e = getenv("MCF_DIAG_CLUSTER");
-    const int cl_env = cl_e ? atoi(cl_e) : 8;
+    const int cl_env = cl_e ? atoi(cl_e) : (g->n < (1ll << 23) ? 8 : 0);
     int cl_grid[3] = {0, 0, 0};
     q.cl_maxk = 0;
     if (q.uniform && g->n > DENSE_N && cl_env >= 2) {
