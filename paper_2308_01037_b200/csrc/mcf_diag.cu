@@ -14,6 +14,7 @@
 //                    fixed order (mcf_diag_combine).
 // Partials per CSC entry make the result independent of how columns are
 // split across batches, CTAs or GPUs.
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -88,6 +89,10 @@ struct QArgs {
     unsigned long long *prof;   // MCF_DIAG_PROF=1: combine counters (profiling only, else null)
     int *llist;                 // per-CTA lists of long (i, c) entries (~t: push), llcap each
     long long llcap;
+    int *lbase;                 // k_diag_q: first piece of each listed entry, its piece sum,
+    unsigned long long *lacc;   // and the piece -> entry map (ocap per CTA)
+    int *lown;
+    long long ocap;
     long long long_work;        // LONG_WORK (MCF_DIAG_LONG_WORK overrides: tests)
     long long big_work;         // BIG_WORK (MCF_DIAG_BIG_WORK overrides: tests)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
@@ -351,9 +356,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
     int *skeys = reinterpret_cast<int *>(svals + SCAP);
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
     __shared__ long long s_col, s_work, s_slot, s_off;
-    __shared__ int s_nsupp, s_next, s_nlong;
-    __shared__ int s_lt[MAX_LONG], s_lpre[MAX_LONG + 1];  // parked long entries (~t: push) and chunk prefix
-    __shared__ long long s_lacc[MAX_LONG];
+    __shared__ int s_nsupp, s_next, s_nlong, s_nchunk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int *gkeys = a.gkeys ? a.gkeys + (long long)blockIdx.x * a.gcap : nullptr;
     long long *gvals = a.gvals ? a.gvals + (long long)blockIdx.x * a.gcap : nullptr;
@@ -506,18 +509,25 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             }
         } else {
             // Uniform values: warps take entries dynamically; an entry whose
-            // scan is longer than LONG_WORK is listed and, once every short
-            // entry is done, split into CHUNK-long ranges that all warps share,
-            // MAX_LONG listed entries at a time (one warp per entry left the
-            // CTA waiting on its longest scan).  Range sums are int64 and added
-            // with shared atomics: the same exact total as one warp's scan.
-            int *llist = a.llist + (long long)blockIdx.x * a.llcap;
+            // scan is longer than LONG_WORK is listed with a range of CHUNK-long
+            // pieces (a chunk -> entry map), and once every short entry is done
+            // all warps share the pieces of every listed entry (one warp per
+            // entry left the CTA waiting on its longest scan).  Piece sums are
+            // int64 and added atomically: the same exact total as one warp's
+            // scan.  A list or map that is full: the warp scans the entry itself.
+            const long long rb = (long long)blockIdx.x;
+            int *llist = a.llist + rb * a.llcap;
+            int *lbase = a.lbase + rb * a.llcap;
+            unsigned long long *lacc = a.lacc + rb * a.llcap;
+            int *lown = a.lown + rb * a.ocap;
             if (tid == 0) {
                 s_next = 0;
                 s_nlong = 0;
+                s_nchunk = 0;
             }
             __syncthreads();
-            const LocalTable tab{keys, vals, mask, keys != nullptr && keys == gkeys};
+            // (global tables here: scalar probes measured faster than batched, k_diag_big the reverse)
+            const LocalTable tab{keys, vals, mask, false};
             while (true) {
                 int t = 0;
                 if (lane == 0) t = atomicAdd(&s_next, 1);
@@ -528,12 +538,23 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 const bool push = use_push(a, i, ihi - ilo, nsupp);
                 const long long len = push ? nsupp : ihi - ilo;
                 if (len > a.long_work) {
-                    int slot = 0;
-                    if (lane == 0) slot = atomicAdd(&s_nlong, 1);
+                    const int nch = (int)((len + CHUNK - 1) / CHUNK);
+                    int slot = 0, base = 0;
+                    if (lane == 0) {
+                        slot = atomicAdd(&s_nlong, 1);
+                        base = slot < a.llcap ? atomicAdd(&s_nchunk, nch) : 0;
+                    }
                     slot = __shfl_sync(MCF_FULL, slot, 0);
-                    if (slot < a.llcap) {  // (a full list: this warp scans the entry itself)
-                        if (lane == 0) llist[slot] = push ? ~t : t;
-                        continue;
+                    base = __shfl_sync(MCF_FULL, base, 0);
+                    if (slot < a.llcap) {
+                        const bool fits = (long long)base + nch <= a.ocap;
+                        for (long long k = base + lane; k < base + nch && k < a.ocap; k += 32) lown[k] = fits ? slot : -1;
+                        if (lane == 0) {
+                            llist[slot] = fits ? (push ? ~t : t) : INT_MAX;  // INT_MAX: scanned here
+                            lbase[slot] = base;
+                            lacc[slot] = 0ull;
+                        }
+                        if (fits) continue;
                     }
                 }
                 const long long acc =
@@ -542,46 +563,35 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             }
             __syncthreads();
             const int nlong = s_nlong < a.llcap ? s_nlong : (int)a.llcap;
-            for (int g0 = 0; g0 < nlong; g0 += MAX_LONG) {
-                const int nl = nlong - g0 < MAX_LONG ? nlong - g0 : MAX_LONG;
-                if (tid == 0) {
-                    s_next = 0;
-                    s_lpre[0] = 0;
-                    for (int j = 0; j < nl; ++j) {
-                        const int lt = llist[g0 + j];
-                        const int t = lt < 0 ? ~lt : lt;
-                        const int i = a.csc_rows[cs + t];
-                        const long long len = lt < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
-                        s_lt[j] = lt;
-                        s_lacc[j] = 0;
-                        s_lpre[j + 1] = s_lpre[j] + (int)((len + CHUNK - 1) / CHUNK);
-                    }
-                }
+            if (nlong > 0) {
+                const long long K = s_nchunk < a.ocap ? s_nchunk : a.ocap;
+                if (tid == 0) s_next = 0;
                 __syncthreads();
-                const int K = s_lpre[nl];
                 while (true) {
                     int k = 0;
                     if (lane == 0) k = atomicAdd(&s_next, 1);
                     k = __shfl_sync(MCF_FULL, k, 0);
                     if (k >= K) break;
-                    int j = 0;
-                    while (s_lpre[j + 1] <= k) ++j;
-                    const bool push = s_lt[j] < 0;
-                    const int t = push ? ~s_lt[j] : s_lt[j];
+                    const int j = lown[k];
+                    if (j < 0) continue;
+                    const int lt = llist[j];
+                    const bool push = lt < 0;
+                    const int t = push ? ~lt : lt;
                     const int i = a.csc_rows[cs + t];
                     const long long base = push ? 0 : a.csc_ptr[i];
                     const long long end = push ? nsupp : a.csc_ptr[i + 1];
-                    const long long lo = base + (long long)(k - s_lpre[j]) * CHUNK;
+                    const long long lo = base + (long long)(k - lbase[j]) * CHUNK;
                     const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
                     const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
-                    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&s_lacc[j]), (unsigned long long)acc);
+                    if (lane == 0) atomicAdd(lacc + j, (unsigned long long)acc);
                 }
                 __syncthreads();
-                for (int j = tid; j < nl; j += Q_THREADS) {
-                    const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
-                    a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)s_lacc[j], -E));
+                for (int j = tid; j < nlong; j += Q_THREADS) {
+                    const int lt = llist[j];
+                    if (lt == INT_MAX) continue;
+                    const int t = lt < 0 ? ~lt : lt;
+                    a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)(long long)__ldcg(lacc + j), -E));
                 }
-                __syncthreads();
             }
         }
         if (a.prof) {
@@ -1057,7 +1067,15 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     // length on symmetric graphs; longer columns scan the overflow inline)
     q.llcap = g->info.max_degree > 64 ? g->info.max_degree : 64;
     if (q.llcap > (1ll << 24)) q.llcap = 1ll << 24;
-    MCF_CUDA(cudaMallocAsync(&q.llist, sizeof(int) * (size_t)grid * q.llcap, s));
+    q.ocap = 2 * q.llcap + 2 * (q.big_work / CHUNK) + 1024;
+    {
+        unsigned char *lb = nullptr;
+        MCF_CUDA(cudaMallocAsync(&lb, (size_t)grid * (q.llcap * (8 + 4 + 4) + q.ocap * 4), s));
+        q.lacc = reinterpret_cast<unsigned long long *>(lb);
+        q.llist = reinterpret_cast<int *>(q.lacc + (size_t)grid * q.llcap);
+        q.lbase = q.llist + (size_t)grid * q.llcap;
+        q.lown = q.lbase + (size_t)grid * q.llcap;
+    }
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) * 4, s));
@@ -1187,7 +1205,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         cudaFreeAsync(q.prof, s);
     }
     cudaFreeAsync(counter, s);
-    cudaFreeAsync(q.llist, s);
+    cudaFreeAsync(q.lacc, s);
     cudaFreeAsync(lbuf, s);
     if (gbuf) cudaFreeAsync(gbuf, s);
     return MCF_OK;
