@@ -171,6 +171,20 @@ __device__ __forceinline__ long long lookup(const int *keys, const long long *va
 // miss (C_i entries no walk from c visited): the filter answers them with one
 // shared-memory word instead of a linear-probing chain.
 __device__ __forceinline__ uint32_t filter_bit(int key) { return ((uint32_t)key * 0x85EBCA6Bu) >> 14; }
+__device__ __forceinline__ uint32_t filter_bit2(int key) { return ((uint32_t)key * 0xC2B2AE35u) >> 14; }
+
+// Two bits per key (k = 2): at the ~10^4 keys of a shared-memory Q_c the false
+// positive rate drops from ~4% to ~0.2%, at 6.5e4 from 22% to 15%.
+__device__ __forceinline__ bool filter_test(const unsigned *filt, int key) {
+    const uint32_t b = filter_bit(key), b2 = filter_bit2(key);
+    return ((filt[b >> 5] >> (b & 31)) & (filt[b2 >> 5] >> (b2 & 31)) & 1u) != 0;
+}
+
+__device__ __forceinline__ void filter_add(unsigned *filt, int key) {
+    const uint32_t b = filter_bit(key), b2 = filter_bit2(key);
+    atomicOr(&filt[b >> 5], 1u << (b & 31));
+    atomicOr(&filt[b2 >> 5], 1u << (b2 & 31));
+}
 
 // Uniform-value graphs: the fixed-point sum over one range of the (i, c) work,
 // warp-reduced.
@@ -244,8 +258,7 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
 #pragma unroll
                 for (int u = 0; u < PULL_U; ++u) {
                     if (jv[u] < 0) continue;
-                    const uint32_t b = filter_bit(jv[u]);
-                    if (filt[b >> 5] & (1u << (b & 31))) {
+                    if (filter_test(filt, jv[u])) {
                         const long long q = tab.get(jv[u]);
                         acc += q;
                         if (a.prof) {
@@ -268,8 +281,7 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
             for (int u = 0; u < PULL_U; ++u) {
                 sl[u] = 0;
                 if (jv[u] < 0) continue;
-                const uint32_t b = filter_bit(jv[u]);
-                if (filt[b >> 5] & (1u << (b & 31))) {
+                if (filter_test(filt, jv[u])) {
                     pend |= 1u << u;
                     sl[u] = hash_slot(jv[u], tab.mask);
                 }
@@ -336,8 +348,7 @@ __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, co
     double acc = 0.0;
     for (long long e = ilo + lane; e < ihi; e += 32) {
         const int j = __ldg(a.csc_rows + e);
-        const uint32_t b = filter_bit(j);
-        if (filt[b >> 5] & (1u << (b & 31)))
+        if (filter_test(filt, j))
             acc = fma(__ldg(a.csc_vals + e), ldexp((double)lookup(keys, vals, mask, j), -E), acc);
     }
     return aic * warp_sum(acc);
@@ -433,8 +444,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
             const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
             if (key != EMPTY_KEY) {
-                const uint32_t b = filter_bit(key);
-                atomicOr(&filt[b >> 5], 1u << (b & 31));
+                filter_add(filt, key);
                 if (a.uniform) {
                     const int p = atomicAdd(&s_nsupp, 1);
                     if (p < a.lcap) {
@@ -723,8 +733,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         for (int t = tid; t < SCAP; t += Q_THREADS) {
             const int key = skeys[t];
             if (key != EMPTY_KEY) {
-                const uint32_t b = filter_bit(key);
-                atomicOr(&filt[b >> 5], 1u << (b & 31));
+                filter_add(filt, key);
                 const int p = atomicAdd(r0_nsupp, 1);
                 if (p < lcap) {
                     lkeys[p] = key;
