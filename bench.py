@@ -419,7 +419,10 @@ def run_device(args, cfg):
     # ---- dominant kernel roofline -------------------------------------------------------
     peak, peak_src = measured_peak()
     walk_avg_ms = walk_ms_tot / max(1, walk_launches)
-    em_per_walk_launch = em_per_step / world  # this rank's launches process its share
+    # this rank's launches process its share of a step; diag runs batch a step
+    # into several walk launches (emission-buffer budget), each one a slice
+    walk_launches_per_step = max(1.0, walk_launches / max(1, args.steps))
+    em_per_walk_launch = em_per_step / world / walk_launches_per_step
     achieved = BYTES_PER_STEP * em_per_walk_launch / (walk_avg_ms / 1e3) / 1e9 if walk_avg_ms > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
@@ -438,8 +441,14 @@ def run_device(args, cfg):
                         "fill (tools/gups, profiles/r01/gups.txt): HBM-resident graphs (config 4) are bound by "
                         "those fills (~88% of the copy peak in DRAM traffic); L2-resident ones (config 2) by the "
                         "latency of the one dependent load, hence frac > 1 against HBM"}
+    roofline["walk_launches_per_step"] = walk_launches_per_step
     if cfg["kind"] == "diag":
         roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
+        roofline["combine"] = {
+            "kernels": "k_diag_q, k_diag_qc<K>, k_diag_big (Q_c build + Eq. 20 combine)",
+            "ms_per_step": q_ms_tot / max(1, args.steps),
+            "share_of_step": (q_ms_tot / ms) if ms else None,
+            "bound": "probe round trips to shared / distributed shared / L2 tables (DESIGN 6), not DRAM bandwidth"}
     elif q_ms_tot:  # action: the span before the walks (budgets, r) recorded by mcf_funm_action
         roofline["prewalk_ms_avg"] = q_ms_tot / max(1, args.steps)
 

@@ -95,6 +95,7 @@ struct QArgs {
     long long ocap;
     long long long_work;        // LONG_WORK (MCF_DIAG_LONG_WORK overrides: tests)
     long long big_work;         // BIG_WORK (MCF_DIAG_BIG_WORK overrides: tests)
+    long long cl_base;          // first scratch region of the cluster kernels' CTAs (= k_diag_q's grid)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
 };
 
@@ -678,8 +679,10 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
     long long *r0_lacc = cl.map_shared_rank(s_lacc, 0);
     const int tid = threadIdx.x, lane = tid & 31;
     const long long lcap = (long long)K * a.lcap;  // the cluster's K consecutive per-CTA list regions
-    int *lkeys = a.lkeys + (long long)(blockIdx.x / K) * lcap;
-    long long *lvals = a.lvals + (long long)(blockIdx.x / K) * lcap;
+    // per-CTA scratch regions after k_diag_q's (the two kernels run concurrently)
+    const long long cta = a.cl_base + blockIdx.x;
+    int *lkeys = a.lkeys + (long long)((cta - rank) / K) * lcap;
+    long long *lvals = a.lvals + (long long)((cta - rank) / K) * lcap;
     const uint32_t mask = (uint32_t)K * SCAP - 1;
     const long long CT = (long long)K * Q_THREADS, gt = (long long)rank * Q_THREADS + tid;
     const ClusterTable tab{skeys, svals, mask};
@@ -807,7 +810,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                 continue;
             }
         }
-        int *llist = a.llist + (long long)(blockIdx.x - rank) * a.llcap;  // the cluster's (rank 0's) long list
+        int *llist = a.llist + (long long)(cta - rank) * a.llcap;  // the cluster's (rank 0's) long list
         while (true) {
             int t = 0;
             if (lane == 0) t = atomicAdd(r0_next, 1);
@@ -1069,9 +1072,13 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     // per-CTA support lists (push path): up to half the largest table
     q.lcap = cap > 2 * SCAP ? cap / 2 : SCAP;  // >= SCAP: a cluster's list spans its CTAs' regions
     unsigned char *lbuf = nullptr;
-    MCF_CUDA(cudaMallocAsync(&lbuf, (size_t)grid * q.lcap * (sizeof(int) + sizeof(long long)), s));
+    // scratch regions: k_diag_q's grid, then as many for the cluster kernels
+    // running beside it (uniform-value graphs above the dense size)
+    q.cl_base = grid;
+    const long long nreg = (q.uniform && g->n > DENSE_N) ? 2ll * grid : grid;
+    MCF_CUDA(cudaMallocAsync(&lbuf, (size_t)nreg * q.lcap * (sizeof(int) + sizeof(long long)), s));
     q.lvals = reinterpret_cast<long long *>(lbuf);
-    q.lkeys = reinterpret_cast<int *>(q.lvals + (size_t)grid * q.lcap);
+    q.lkeys = reinterpret_cast<int *>(q.lvals + (size_t)nreg * q.lcap);
     // lists of long (i, c) entries: one per CTA, max_degree entries (a column's
     // length on symmetric graphs; longer columns scan the overflow inline)
     q.llcap = g->info.max_degree > 64 ? g->info.max_degree : 64;
@@ -1079,11 +1086,11 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.ocap = 2 * q.llcap + 2 * (q.big_work / CHUNK) + 1024;
     {
         unsigned char *lb = nullptr;
-        MCF_CUDA(cudaMallocAsync(&lb, (size_t)grid * (q.llcap * (8 + 4 + 4) + q.ocap * 4), s));
+        MCF_CUDA(cudaMallocAsync(&lb, (size_t)nreg * (q.llcap * (8 + 4 + 4) + q.ocap * 4), s));
         q.lacc = reinterpret_cast<unsigned long long *>(lb);
-        q.llist = reinterpret_cast<int *>(q.lacc + (size_t)grid * q.llcap);
-        q.lbase = q.llist + (size_t)grid * q.llcap;
-        q.lown = q.lbase + (size_t)grid * q.llcap;
+        q.llist = reinterpret_cast<int *>(q.lacc + (size_t)nreg * q.llcap);
+        q.lbase = q.llist + (size_t)nreg * q.llcap;
+        q.lown = q.lbase + (size_t)nreg * q.llcap;
     }
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));
@@ -1163,13 +1170,18 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     }
     int rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
-    k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
-    mcf::note_launch();
-    MCF_LAUNCHED("k_diag_q");
     if (q.cl_maxk) {
+        // The cluster kernels go first and k_diag_q runs beside them on the side
+        // stream: clusters of 4/8 CTAs only fit 128-132 of the 148 SMs, and
+        // k_diag_q's persistent CTAs take the rest (and every SM a finished
+        // cluster kernel frees).  Integer partials: the split does not matter.
         unsigned hc[8];
         MCF_CUDA(cudaMemcpyAsync(hc, cl_cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
         MCF_CUDA(cudaStreamSynchronize(s));
+        rc = ensure_side_stream(g);
+        if (rc) return rc;
+        MCF_CUDA(cudaEventRecord(g->ev_fork, s));  // before the cluster kernels: k_diag_q does not wait for them
+        MCF_CUDA(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
         for (int k = 0; k < 3; ++k) {
             if (!hc[k]) continue;
             const int *lst = cl_cols + k * ncol;
@@ -1180,7 +1192,16 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
             mcf::note_launch();
             MCF_LAUNCHED("k_diag_qc");
         }
+        k_diag_q<<<grid, Q_THREADS, smem, g->side>>>(q);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_diag_q");
+        MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
+        MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
         cudaFreeAsync(cl_cols, s);
+    } else {
+        k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_diag_q");
     }
     if (q.big) {
         unsigned nrec = 0;

@@ -382,6 +382,7 @@ int build_blk_col(const long long *walk_pre, long long col_begin, long long col_
                   int **blk_col, cudaStream_t s);
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
 int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s);
+int ensure_side_stream(mcf_graph *g);
 // r_ones/stats_zero (fused path only, see fused_alloc_applies): also write
 // r = A 1 into r_ones and the headers, and zero stats_zero[4]
 int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *walk_pre, int *blk_col,

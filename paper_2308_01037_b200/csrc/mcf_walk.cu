@@ -1094,6 +1094,26 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     return MCF_OK;
 }
 
+// One side stream per device, shared by every graph (created once), and the
+// graph's fork/join events: budgets beside r = A v in the action path, the
+// global-table combine beside the cluster kernels in the diag path.
+int ensure_side_stream(mcf_graph *g) {
+    if (g->side) return MCF_OK;
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = streams.find(g->device);
+    if (it == streams.end()) {
+        cudaStream_t st;
+        MCF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        it = streams.emplace(g->device, st).first;
+    }
+    MCF_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+    MCF_CUDA(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+    g->side = it->second;
+    return MCF_OK;
+}
+
 // The whole RandFunmAction estimate for one process (Alg. 3): the walk
 // budgets (largest remainder) on a side stream concurrently with r = A v (the
 // SpMV writes r into the walk headers directly; v = NULL means v = 1, whose
@@ -1103,20 +1123,8 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
                        const double *v, double z0, double z1, double *r, double *q, double *qvar, double *y,
                        long long *stats, cudaStream_t s) {
     MCF_ARG(g && r && q && y && walk_pre, "mcf_funm_action: null argument");  // ni optional
-    if (!g->side) {  // one side stream per device, shared by every graph (created once)
-        static std::mutex mu;
-        static std::map<int, cudaStream_t> streams;
-        std::lock_guard<std::mutex> lock(mu);
-        auto it = streams.find(g->device);
-        if (it == streams.end()) {
-            cudaStream_t st;
-            MCF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-            it = streams.emplace(g->device, st).first;
-        }
-        g->side = it->second;
-        MCF_CUDA(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
-        MCF_CUDA(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
-    }
+    int rc0 = ensure_side_stream(g);
+    if (rc0) return rc0;
     MCF_ARG(p && n_walks >= 1 && n_walks < (1ll << 31) - 4096, "mcf_funm_action: n_walks must be in [1, 2^31 - 4096)");
     // one scratch block, one memset: [walk counter + error flags | budget-kernel state | blk | xw]
     const bool fused = fused_alloc_applies(g);
