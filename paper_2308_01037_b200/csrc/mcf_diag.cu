@@ -93,7 +93,8 @@ struct QArgs {
     unsigned long long *lacc;   // and the piece -> entry map (ocap per CTA)
     int *lown;
     long long ocap;
-    long long long_work;        // LONG_WORK (MCF_DIAG_LONG_WORK overrides: tests)
+    long long long_work;        // LONG_WORK: split threshold of the cluster kernels (MCF_DIAG_LONG_WORK)
+    long long long_work_q;      // k_diag_q's (MCF_DIAG_LONG_WORK_Q; measured best lower: one CTA per column)
     long long big_work;         // BIG_WORK (MCF_DIAG_BIG_WORK overrides: tests)
     long long cl_base;          // first scratch region of the cluster kernels' CTAs (= k_diag_q's grid)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
@@ -114,6 +115,7 @@ constexpr long long BIG_WORK = 1ll << 20;
 constexpr int MAX_LONG = 64;            // parked long (i, c) entries per column
 constexpr long long CHUNK = 1024;       // ids / support tests per shared range of a long entry
 constexpr long long LONG_WORK = 2 * CHUNK;
+constexpr long long LONG_WORK_Q = CHUNK / 2;  // Chung-Lu 1.6e7: 9.6 -> 9.3 s (R-MAT 2^22 prefers 2048 in the clusters)
 // cluster tables are sized for load <= CL_LOAD_NUM / CL_LOAD_DEN (by emission count)
 #ifndef CL_LOAD_NUM
 #define CL_LOAD_NUM 1
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
                 const bool push = use_push(a, i, ihi - ilo, nsupp);
                 const long long len = push ? nsupp : ihi - ilo;
-                if (len > a.long_work) {
+                if (len > a.long_work_q) {
                     const int nch = (int)((len + CHUNK - 1) / CHUNK);
                     int slot = 0, base = 0;
                     if (lane == 0) {
@@ -1049,6 +1051,8 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.big_work = e ? atoll(e) : BIG_WORK;
         e = getenv("MCF_DIAG_LONG_WORK");
         q.long_work = e ? atoll(e) : LONG_WORK;
+        e = getenv("MCF_DIAG_LONG_WORK_Q");
+        q.long_work_q = e ? atoll(e) : LONG_WORK_Q;
     }
     static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
     if (prof_on) {

@@ -463,7 +463,8 @@ def test_diag_cluster_tables_bitwise(mc):
             # hundreds of (i, c) entries split into shared ranges, in groups
             for big, long_ in ((None, None), ("4096", None), (None, "16")):
                 os.environ["MCF_DIAG_CLUSTER"] = k
-                for var, val in (("MCF_DIAG_BIG_WORK", big), ("MCF_DIAG_LONG_WORK", long_)):
+                for var, val in (("MCF_DIAG_BIG_WORK", big), ("MCF_DIAG_LONG_WORK", long_),
+                                 ("MCF_DIAG_LONG_WORK_Q", long_)):
                     if val:
                         os.environ[var] = val
                     else:
@@ -473,6 +474,7 @@ def test_diag_cluster_tables_bitwise(mc):
         os.environ.pop("MCF_DIAG_CLUSTER", None)
         os.environ.pop("MCF_DIAG_BIG_WORK", None)
         os.environ.pop("MCF_DIAG_LONG_WORK", None)
+        os.environ.pop("MCF_DIAG_LONG_WORK_Q", None)
     ref = outs["0", None, None]
     for key, v in outs.items():
         assert np.array_equal(v, ref), key
