@@ -1036,11 +1036,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.uniform = g->uniform_value ? 1 : 0;
     {
         // push while a bitmap test is cheaper than scanning C_i: the bitmaps are
-        // n bits, so the push/pull break-even moves up with n (measured: R-MAT
-        // 2^22 best at 1x |supp Q_c|, Chung-Lu 1.6e7 at ~4x)
+        // n bits, so the push/pull break-even moves up with n (measured with the
+        // two-bit filter and shared long scans: R-MAT 2^22 best at 2x |supp Q_c|,
+        // Chung-Lu 1.6e7 at 8-16x)
         const char *e = getenv("MCF_PUSH_PCT");
-        long long pct = (100ll * g->n) / (1ll << 22);
-        pct = pct < 100 ? 100 : (pct > 400 ? 400 : pct);
+        long long pct = (200ll * g->n) / (1ll << 22);
+        pct = pct < 200 ? 200 : (pct > 1600 ? 1600 : pct);
         q.push_pct = e ? atoi(e) : (int)pct;
     }
     q.value = g->value;
