@@ -300,6 +300,12 @@ def run_device(args, cfg):
 
     t0 = time.perf_counter()
     a, beta, n_walks = make_graph(cfg, pinned=True, scale=args.scale)
+    per_gpu_walks = n_walks
+    if world > 1 and args.scaling == "weak":
+        # weak scaling (the path partitions by start column, run instructions 5):
+        # every GPU keeps the config's walk budget, the N-GPU job walks N times
+        # as many over the same graph (its estimate has N times the samples)
+        n_walks = per_gpu_walks * world
     coeffs = coeff_stream(cfg)
     log(f"[bench] graph n={a.n} nnz={a.nnz} beta={beta:.6e} walks={n_walks} ({time.perf_counter() - t0:.1f}s)")
     wcfg = mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"], cfg["seed"])
@@ -501,10 +507,11 @@ def run_device(args, cfg):
         line = {
             "metric": "walk-steps/s", "baseline_metric": BASELINE_METRIC, "value": value, "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "nodes_per_s": nodes_per_s,
             "config": {"workload": cfg["workload"], "n": g.n, "nnz": g.nnz, "n_walks": int(n_walks),
+                       "walks_per_gpu": int(n_walks // world),
                        "emissions_per_step": em_per_step, "beta": beta, "max_steps": cfg["max_steps"],
                        "weight_cutoff": cfg["cutoff"], "seed": cfg["seed"], "sampling": "philox (device RNG)",
                        "l2": ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read of another "
@@ -540,6 +547,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale (config 4)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = every GPU keeps the config's walk budget (default); strong = the config's "
+                         "budget split over the GPUs")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.scale and cfg["graph"] == "rmat":
