@@ -448,6 +448,13 @@ def run_device(args, cfg):
                         "those fills (~88% of the copy peak in DRAM traffic); L2-resident ones (config 2) by the "
                         "latency of the one dependent load, hence frac > 1 against HBM"}
     roofline["walk_launches_per_step"] = walk_launches_per_step
+    # the walk's own ceilings (tools/gups.cu, profiles/r01/gups.txt): one dependent
+    # random load per step, 279 G/s when the table is L2-resident, 37.8 G/s from HBM
+    if walk_avg_ms > 0:
+        ksteps = em_per_walk_launch / (walk_avg_ms / 1e3)
+        roofline["kernel_steps_per_s"] = ksteps
+        roofline["l2_random_load_ceiling_gsteps"] = 279.2
+        roofline["frac_of_l2_random_load_ceiling"] = ksteps / 279.2e9
     if cfg["kind"] == "diag":
         roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
         roofline["combine"] = {
