@@ -54,6 +54,16 @@ def column_shards(walk_pre, parts: int):
     return [(int(cuts[i]), int(cuts[i + 1])) for i in range(parts)]
 
 
+def _shards(peers, g, pre, n_walks: int, parts: int):
+    """column_shards, remembered per (graph, N_s, parts) on the peer buffers."""
+    key = (id(g), int(n_walks), int(parts))
+    hit = peers.shard_cache.get(key)
+    if hit is None or hit[0] is not g:
+        hit = (g, column_shards(pre, parts))
+        peers.shard_cache[key] = hit
+    return hit[1]
+
+
 def row_shards(n: int, parts: int):
     b = [n * k // parts for k in range(parts + 1)]
     return [(b[i], b[i + 1]) for i in range(parts)]
@@ -97,6 +107,9 @@ class PeerBuffers:
     def __init__(self, nbytes: list[int], group=None):
         rank, size = world()
         self.rank = rank
+        # column shards by (graph, N_s, ranks): a function of the budgets only,
+        # so repeated passes skip the device-to-host read that finds them
+        self.shard_cache = {}
         self.own, handles = [], []
         for b in nbytes:
             ptr, h = C.c_void_p(), C.create_string_buffer(64)
@@ -147,7 +160,7 @@ def sharded_action_peer(g: DeviceGraph, coeffs, v, config, *, params=None, group
     if own:
         peers = PeerBuffers([8 * g.n, 8 * g.n], group)
     ni, pre = g.allocate(cfg.n_walks)
-    shards = column_shards(pre, size)
+    shards = _shards(peers, g, pre, cfg.n_walks, size)
     bounds = [shards[0][0]] + [b for _, b in shards]
     st = g.new_stats()
     r = g.spmv(v)
@@ -179,7 +192,7 @@ def sharded_diag_peer(g: DeviceGraph, coeffs, config, *, params=None, group=None
     if own:
         peers = PeerBuffers([8 * g.nnz, 8 * g.n], group)
     ni, pre = g.allocate(cfg.n_walks)
-    shards = column_shards(pre, size)
+    shards = _shards(peers, g, pre, cfg.n_walks, size)
     bounds = [shards[0][0]] + [b for _, b in shards]
     st = g.new_stats()
     _device_view(peers.ptrs[rank][0], g.nnz, g.device).zero_()  # columns without walks keep zero partials
