@@ -244,6 +244,10 @@ template <bool FAT, bool LEAN = false, bool WITH_ID = false>
 __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) {
     if (LEAN) {  // {start, degree} of the target; |a| row sum (= r for v = 1) by degree
         NodeHdr h;
+        // the target id (diag emissions): issued together with the entry load,
+        // consumed only at the end, so the two round trips overlap (measured:
+        // reading it after decoding the entry stalled the diag walk a second time)
+        const int idv = WITH_ID ? __ldg(a.ecol + e) : 0;
         if (a.lean4) {  // 4-B entries: [0 | deg:6 | start:25], or [1 | target id] for degree >= 63
             const uint32_t t = __ldg(a.lean4 + e);
             if (t & 0x80000000u) {
@@ -260,8 +264,7 @@ __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) 
             h.deg = (int)t.y;
         }
         h.flags = HDR_UNIFORM;
-        // the target id (diag emissions): same index, loaded alongside, off the chain
-        h.pad = WITH_ID ? (uint32_t)(__ldg(a.ecol + e) & 0x7fffffff) : 0u;
+        h.pad = WITH_ID ? (uint32_t)(idv & 0x7fffffff) : 0u;
         h.rsum = __ldg(a.rsum_by_deg + h.deg);
         h.aux = h.rsum;
         return h;
@@ -392,8 +395,9 @@ __global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long 
         }
         if (MODE != EMIT_COUNT) {
             const double om = __ldg(a.zeta + L.k + 2) * L.w;
-            est[sb + L.k * stride] = (int)L.h.pad;
-            ewt[sb + L.k * stride] = om;
+            // streaming stores: the emission buffer (GBs) must not evict the walk tables from L2
+            __stcs(est + sb + L.k * stride, (int)L.h.pad);
+            __stcs(ewt + sb + L.k * stride, om);
             wmax = fmax(wmax, fabs(om));
         }
         ++em;
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long 
             if (MODE == EMIT_COUNT) {
                 eaux[rel] = emitted;
             } else {
-                for (long long t = emitted; t < scap; ++t) est[sb + t * stride] = -1;
+                for (long long t = emitted; t < scap; ++t) __stcs(est + sb + t * stride, -1);
                 if (wmax > 0.0) atomicMax(a.colmax + L.c, (unsigned long long)__double_as_longlong(wmax));
             }
             L.rel = -1;
