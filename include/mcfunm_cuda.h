@@ -52,6 +52,15 @@ extern "C" {
 #define MCF_FLAG_RETURN_ONLY 2  /* action walks accumulate zeta W only at emissions where the walk is
                                    back at its start node (classic MC diagonal, Alg. 1) */
 
+/* Run only the walks w (index inside their column) with w = g mod G, every
+ * other walk contributing nothing (W0 stays 1/N_c): the G group estimates of
+ * a diag or action pass sum to the full estimate, and their spread gives the
+ * standard error (batch means; SPEC.md:410 asks for a per-walk SE).  G in
+ * [1, 256] and g < G are packed with MCF_GROUP_FLAGS.  Device-RNG walks only. */
+#define MCF_FLAG_WALK_GROUP 4
+#define MCF_GROUP_FLAGS(G, g) (MCF_FLAG_WALK_GROUP | ((((G) - 1) & 0xff) << 8) | (((g) & 0xff) << 16))
+#define MCF_GROUP_COUNT(flags) ((((flags) >> 8) & 0xff) + 1)
+#define MCF_GROUP_INDEX(flags) (((flags) >> 16) & 0xff)
 typedef struct mcf_graph mcf_graph;
 
 /* Square sparse matrix in both CSR and CSC form, already scaled by gamma
@@ -218,6 +227,16 @@ MCF_API int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_
 MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d,
                      int64_t row_begin, int64_t row_end, void *stream);
 
+/* Estimated variance of d_i for rows [row_begin, row_end) from G >= 2 walk-
+ * group passes of mcf_walk_diag (MCF_GROUP_FLAGS(G, g), g = 0..G-1):
+ * pcol_groups holds the G partial vectors back to back (G x nnz, CSC order).
+ * Per entry (i, c) the between-group spread of the per-walk mean estimates
+ * Var(pcol[(i, c)]) (batch means, G' = min(G, N_c) - 1 degrees of freedom);
+ * columns are independent, so var_i = sum_c Var(pcol[(i, c)]).  The standard
+ * error SPEC.md:410 attaches to every result (there from a 1% walk subsample). */
+MCF_API int mcf_diag_variance(mcf_graph *g, const double *pcol_groups, int groups, const int64_t *walk_pre,
+                              double *var, int64_t row_begin, int64_t row_end, void *stream);
+
 /* Multi-GPU diag combine with the exchange folded in (as mcf_spmv_peer):
  * d over rows [row_begin, row_end), reading pcol[(i, c)] from
  * pcol_parts[k] for the part k whose column range [col_bounds[k],
@@ -225,6 +244,15 @@ MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const dou
 MCF_API int mcf_diag_combine_peer(mcf_graph *g, double zeta0, double zeta1, const double *const *pcol_parts,
                                   const int64_t *col_bounds, int n_parts, double *const *d_outs, int n_outs,
                                   int64_t row_begin, int64_t row_end, void *stream);
+
+/* Work estimate per column for cost-balanced column shards (multi-GPU,
+ * SURVEY 8(e)): cost[c] (int64, [dev] n) = N_c for mode 0 (action walks);
+ * for mode 1 (diag) the emissions 3 N_c (max_steps + 1) plus the Eq. 20
+ * combine's probes sum_{i in C_c} min(deg i, N_c (max_steps + 1))
+ * (PAPER.md:303).  No counterpart in the reference (single process); the
+ * paper balances by OpenMP dynamic scheduling. */
+MCF_API int mcf_column_costs(mcf_graph *g, const int64_t *walk_pre, int64_t max_steps, int mode, int64_t *cost,
+                             void *stream);
 
 /* Device time of the kernels launched with MCF_FLAG_TIME_KERNELS since the
  * last reset: the walk kernels (action walks or diag emission walks) and, in

@@ -17,6 +17,12 @@ LIB_PATH = os.environ.get("MCFUNM_CUDA_LIB", os.path.join(_HERE, "lib", "libmcfu
 MCF_STATS_LEN = 4
 MCF_FLAG_TIME_KERNELS = 1
 MCF_FLAG_RETURN_ONLY = 2
+MCF_FLAG_WALK_GROUP = 4
+
+
+def group_flags(groups: int, index: int) -> int:
+    """MCF_GROUP_FLAGS(G, g) of include/mcfunm_cuda.h: only walks w = g mod G."""
+    return MCF_FLAG_WALK_GROUP | (((groups - 1) & 0xFF) << 8) | ((index & 0xFF) << 16)
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -63,6 +69,8 @@ SIGNATURES = {
     "mcf_diag_combine": (C.c_int, [P, C.c_double, C.c_double, P, P, I64, I64, P]),
     "mcf_diag_combine_peer": (C.c_int, [P, C.c_double, C.c_double, P, P, C.c_int, P, C.c_int, I64, I64, P]),
     "mcf_walk_qdense": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, I64, P, P]),
+    "mcf_column_costs": (C.c_int, [P, P, I64, C.c_int, P, P]),
+    "mcf_diag_variance": (C.c_int, [P, P, C.c_int, P, P, I64, I64, P]),
 }
 
 _lib = None

@@ -18,6 +18,7 @@ from .device import DeviceGraph
 from .errors import ArgumentError, ConvergenceError
 from .estimators import FunmResult, rand_funm_action, rand_funm_diag
 from .series import EXPONENTIAL, RESOLVENT
+from .walker import alpha_diagnostic
 
 
 @dataclass
@@ -126,14 +127,23 @@ def cg_katz(g: DeviceGraph, b: torch.Tensor, tol: float = 1e-10, max_iter: int =
 
 
 def katz_centrality(a, fraction: float, config, method: str = "randomized", *, gamma: float | None = None,
-                    device=None, **kw) -> CentralityReport:
+                    allow_alpha_ge_1: bool = False, device=None, **kw) -> CentralityReport:
     """KC = (I - gamma A)^-1 1 with gamma = fraction / max row sum (Gershgorin,
-    SPEC.md:525-533).  ``gamma`` may be given explicitly (BASELINE config 4 uses
-    0.85 / lambda_max, where alpha >= 1: the walks still terminate by the
-    weight cutoff)."""
+    SPEC.md:525-533).  ``gamma`` may be given explicitly.  The randomized
+    method rejects alpha = (gamma max_i sum_j |a_ij|)^2 >= 1 (SPEC.md:529,
+    Theorem 1: the walk series is not guaranteed to converge) unless
+    ``allow_alpha_ge_1`` is set -- BASELINE config 4 (gamma = 0.85/lambda_max,
+    alpha >> 1) runs that way: its walks still end at the weight cutoff
+    (SURVEY.md §3.2), and the estimate is checked against CG."""
     n = _check_graph(a)
     if gamma is None:
         gamma = gershgorin_gamma(a, fraction)
+    elif method == "randomized" and not allow_alpha_ge_1:
+        m2 = (float(a.info["max_row_abs_sum"]) ** 2 if isinstance(a, DeviceGraph) else alpha_diagnostic(a))
+        alpha = float(gamma) ** 2 * m2
+        if alpha >= 1.0:
+            raise ArgumentError(f"resolvent with alpha = {alpha:.4g} >= 1 after scaling is rejected "
+                                "(Theorem 1, SPEC.md:529); pass allow_alpha_ge_1=True to run it anyway")
     g = _scaled(a, gamma, device)
     if method == "randomized":
         res = rand_funm_action(g, RESOLVENT, None, config, **kw)  # v = 1

@@ -971,34 +971,6 @@ __global__ void k_diag_final(const long long *__restrict__ row_ptr, const int *_
     }
 }
 
-__global__ void k_batch_bounds(const long long *__restrict__ walk_pre, long long cb, long long ce, long long wb,
-                               long long cap_walks, long long nb, long long *__restrict__ bounds) {
-    long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b > nb) return;
-    if (b == 0) { bounds[0] = cb; return; }
-    if (b == nb) { bounds[nb] = ce; return; }
-    long long target = wb + b * cap_walks;  // largest c in [cb, ce] with walk_pre[c] <= target
-    long long lo = cb, hi = ce;
-    while (lo < hi) {
-        long long mid = (lo + hi + 1) >> 1;
-        if (walk_pre[mid] <= target) lo = mid;
-        else hi = mid - 1;
-    }
-    bounds[b] = lo;
-}
-
-__global__ void k_max_walks(const long long *__restrict__ walk_pre, long long cb, long long ce,
-                            unsigned long long *out) {
-    long long c = cb + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long v = (c < ce) ? (unsigned long long)(walk_pre[c + 1] - walk_pre[c]) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long x = __shfl_xor_sync(MCF_FULL, v, o);
-        v = x > v ? x : v;
-    }
-    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
-}
-
 // default emission-buffer budget (slots of 12 B): 2^30 -> 12 GiB of the 180 GB
 static long long emission_budget() {
     static long long v = 0;
@@ -1055,9 +1027,11 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         e = getenv("MCF_DIAG_LONG_WORK_Q");
         q.long_work_q = e ? atoll(e) : LONG_WORK_Q;
     }
+    AsyncFrees frees(s);  // every stream-ordered allocation below, on every return path
     static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
     if (prof_on) {
         MCF_CUDA(cudaMallocAsync(&q.prof, sizeof(unsigned long long) * PROF_SLOTS, s));
+        frees.keep(q.prof);
         MCF_CUDA(cudaMemsetAsync(q.prof, 0, sizeof(unsigned long long) * PROF_SLOTS, s));
     }
     q.gkeys = nullptr;
@@ -1071,6 +1045,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     if (cap > SCAP) {
         q.gcap = cap;
         MCF_CUDA(cudaMallocAsync(&gbuf, (size_t)grid * cap * (sizeof(int) + sizeof(double)), s));
+        frees.keep(gbuf);
         q.gvals = reinterpret_cast<long long *>(gbuf);
         q.gkeys = reinterpret_cast<int *>(q.gvals + (size_t)grid * cap);
     }
@@ -1082,6 +1057,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     q.cl_base = grid;
     const long long nreg = (q.uniform && g->n > DENSE_N) ? 2ll * grid : grid;
     MCF_CUDA(cudaMallocAsync(&lbuf, (size_t)nreg * q.lcap * (sizeof(int) + sizeof(long long)), s));
+    frees.keep(lbuf);
     q.lvals = reinterpret_cast<long long *>(lbuf);
     q.lkeys = reinterpret_cast<int *>(q.lvals + (size_t)nreg * q.lcap);
     // lists of long (i, c) entries: one per CTA, max_degree entries (a column's
@@ -1092,6 +1068,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     {
         unsigned char *lb = nullptr;
         MCF_CUDA(cudaMallocAsync(&lb, (size_t)nreg * (q.llcap * (8 + 4 + 4) + q.ocap * 4), s));
+        frees.keep(lb);
         q.lacc = reinterpret_cast<unsigned long long *>(lb);
         q.llist = reinterpret_cast<int *>(q.lacc + (size_t)nreg * q.llcap);
         q.lbase = q.llist + (size_t)nreg * q.llcap;
@@ -1099,6 +1076,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     }
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));
+    frees.keep(counter);
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) * 4, s));
     q.counter = counter;
     q.n_big = reinterpret_cast<unsigned *>(counter + 1);
@@ -1110,6 +1088,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     if (cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(long long)) + (size_t)max_big * FILTER_WORDS * 4 +
                                        sizeof(BigRec) * max_big + 2 * sizeof(int) * max_big,
                         s) == cudaSuccess) {
+        frees.keep(pool);
         q.pool_vals = reinterpret_cast<long long *>(pool);
         q.pool_keys = reinterpret_cast<int *>(q.pool_vals + pool_cap);
         q.pool_filt = reinterpret_cast<unsigned *>(q.pool_keys + pool_cap);
@@ -1167,6 +1146,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     const long long ncol = ce - cb;
     if (q.cl_maxk) {
         MCF_CUDA(cudaMallocAsync(&cl_cols, sizeof(int) * 3 * (size_t)ncol + 32, s));
+        frees.keep(cl_cols);
         cl_cnt = reinterpret_cast<unsigned *>(cl_cols + 3 * ncol);
         MCF_CUDA(cudaMemsetAsync(cl_cnt, 0, 32, s));
         k_cluster_classify<<<sm_count() * 4, 256, 0, s>>>(q, cl_cols, ncol, cl_cnt);
@@ -1202,7 +1182,6 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         MCF_LAUNCHED("k_diag_q");
         MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
         MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
-        cudaFreeAsync(cl_cols, s);
     } else {
         k_diag_q<<<grid, Q_THREADS, smem, s>>>(q);
         mcf::note_launch();
@@ -1216,6 +1195,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         if (nrec > 0) {
             long long *cnt = nullptr;
             MCF_CUDA(cudaMallocAsync(&cnt, sizeof(long long) * (2 * (size_t)nrec + 1), s));
+            frees.keep(cnt);
             k_big_counts<<<(nrec + 255) / 256, 256, 0, s>>>(q.big, nrec, cnt);
             mcf::note_launch();
             rc = exclusive_scan_i64(cnt, cnt + nrec, nrec, s);
@@ -1223,9 +1203,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
             k_diag_big<<<sm_count() * 8, 256, 0, s>>>(q, cnt + nrec, nrec);
             mcf::note_launch();
             MCF_LAUNCHED("k_diag_big");
-            cudaFreeAsync(cnt, s);
         }
-        cudaFreeAsync(pool, s);
     }
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
@@ -1237,12 +1215,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
                 "[diag-prof] cols %llu big %llu emissions %llu support %llu | pull pairs %llu ids %llu filt %llu hits %llu"
                 " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | gtable cols %llu cycles %llu emissions %llu | cluster cols %llu cycles %llu emissions %llu build %llu\n",
                 h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15], h[16], h[17], h[18], h[19]);
-        cudaFreeAsync(q.prof, s);
     }
-    cudaFreeAsync(counter, s);
-    cudaFreeAsync(q.lacc, s);
-    cudaFreeAsync(lbuf, s);
-    if (gbuf) cudaFreeAsync(gbuf, s);
     return MCF_OK;
 }
 
@@ -1252,52 +1225,59 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(pcol && stats, "diag walk: null pcol/stats");
+    if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
+    MCF_ARG(!(replay && (p->flags & MCF_FLAG_WALK_GROUP)), "walk groups apply to device-RNG walks, not replay");
     rc = ensure_hub_bitmaps(g, s);
     if (rc) return rc;
-    if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
+    // walks of at most 64 steps get fixed slots; longer caps (cutoff-
+    // terminated walks, e.g. max_steps = 10^4) use a count pass instead
+    const bool fixed = p->max_steps <= 64;
+    const long long L = fixed ? p->max_steps : 64;
+    // column batches of at most cap_walks walks (+ one column): the emission
+    // buffer budget (MCF_EMISSION_SLOTS); replay takes the range in one batch
+    std::vector<long long> hb;
+    unsigned long long hmax = 0;
+    long long cap_walks = replay ? (1ll << 62) : emission_budget() / L;
+    rc = column_batches(walk_pre, cb, ce, cap_walks, hb, &hmax, s);
+    if (rc) return rc;
     long long wb = 0, we = 0;
     rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
     if (rc) return rc;
     if (we == wb) return MCF_OK;
+    MCF_ARG(hmax < (1ull << 31), "a column's walk budget must be below 2^31");
+    AsyncFrees frees(s);
     int *err = nullptr;
-    unsigned long long *maxw = nullptr;
-    MCF_CUDA(cudaMallocAsync(&err, sizeof(int) + sizeof(unsigned long long) + 4, s));
-    maxw = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(err) + 8);
+    MCF_CUDA(cudaMallocAsync(&err, 16, s));
+    frees.keep(err);
     MCF_CUDA(cudaMemsetAsync(err, 0, 16, s));
-    long long ncol = ce - cb;
-    k_max_walks<<<(unsigned)((ncol + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, maxw);
-    mcf::note_launch();
-    MCF_LAUNCHED("k_max_walks");
-    unsigned long long hmax = 0;
-    MCF_CUDA(cudaMemcpyAsync(&hmax, maxw, sizeof(hmax), cudaMemcpyDeviceToHost, s));
-    MCF_CUDA(cudaStreamSynchronize(s));
     unsigned long long *colmax = nullptr;  // per-column max |emission| for the fixed-point scale
     MCF_CUDA(cudaMallocAsync(&colmax, sizeof(unsigned long long) * g->n, s));
+    frees.keep(colmax);
     MCF_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * g->n, s));
+    const bool timed = (p->flags & MCF_FLAG_TIME_KERNELS) != 0;
 
     if (replay) {
+        MCF_ARG(we - wb < WALKS_PER_LAUNCH, "replay: walks per call must be below 2^31 (split the column range)");
         long long hoff[2];
         MCF_CUDA(cudaMemcpyAsync(&hoff[0], walk_off + wb, 8, cudaMemcpyDeviceToHost, s));
         MCF_CUDA(cudaMemcpyAsync(&hoff[1], walk_off + we, 8, cudaMemcpyDeviceToHost, s));
         MCF_CUDA(cudaStreamSynchronize(s));
-        long long slots = hoff[1] - hoff[0] + (we - wb);
+        const long long slots = hoff[1] - hoff[0] + (we - wb);
         int *est = nullptr;
         double *ewt = nullptr;
         MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * slots, s));
+        frees.keep(est);
         MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * slots, s));
-        rc = launch_walk_emit(g, p, walk_pre, cb, ce, we - wb, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est, ewt,
-                              colmax, stats, err, s);
+        frees.keep(ewt);
+        rc = launch_walk_emit(g, p, walk_pre, cb, ce, we - wb, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est,
+                              ewt, colmax, stats, err, s);
         if (rc) return rc;
         // table size is bounded by min(slots, n) per column
-        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, colmax, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
+        rc = run_q(timed, g, colmax, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
         if (rc) return rc;
         int herr = 0;
         MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
         MCF_CUDA(cudaStreamSynchronize(s));
-        cudaFreeAsync(est, s);
-        cudaFreeAsync(ewt, s);
-        cudaFreeAsync(err, s);
-        cudaFreeAsync(colmax, s);
         if (herr) {
             set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) + ")");
             return MCF_ERR_ARGUMENT;
@@ -1305,74 +1285,77 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         return MCF_OK;
     }
 
-    // walks of at most FIXED_MAX steps get fixed slots; longer caps (cutoff-
-    // terminated walks, e.g. max_steps = 10^4) use a count pass instead
-    const bool fixed = p->max_steps <= 64;
-    const long long L = fixed ? p->max_steps : 64;
-    long long cap_walks = emission_budget() / L;
-    if (cap_walks < (long long)hmax) cap_walks = (long long)hmax;
-    long long nb = (we - wb + cap_walks - 1) / cap_walks;
-    long long *dbounds = nullptr;
-    MCF_CUDA(cudaMallocAsync(&dbounds, sizeof(long long) * (nb + 1), s));
-    k_batch_bounds<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, wb, cap_walks, nb, dbounds);
-    mcf::note_launch();
-    MCF_LAUNCHED("k_batch_bounds");
-    long long *hb = new long long[nb + 1];
-    MCF_CUDA(cudaMemcpyAsync(hb, dbounds, sizeof(long long) * (nb + 1), cudaMemcpyDeviceToHost, s));
-    MCF_CUDA(cudaStreamSynchronize(s));
     long long buf_slots = (cap_walks + (long long)hmax) * L;
+    if (buf_slots > (we - wb) * L) buf_slots = (we - wb) * L;
     int *est = nullptr;
     double *ewt = nullptr;
     MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * buf_slots, s));
-    MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s));
-    for (long long b = 0; b < nb; ++b) {
-        long long c0 = hb[b], c1 = hb[b + 1];
-        if (c1 <= c0) continue;
+    {
+        const cudaError_t e_ = cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s);
+        if (e_ != cudaSuccess) {
+            cudaFreeAsync(est, s);
+            return cuda_status(e_, "cudaMallocAsync(ewt)");
+        }
+    }
+    for (size_t b = 0; b + 1 < hb.size(); ++b) {
+        const long long c0 = hb[b], c1 = hb[b + 1];
         long long bw0 = 0, bw1 = 0;
         rc = read_walk_range(walk_pre, c0, c1, &bw0, &bw1, s);
         if (rc) break;
         if (bw1 == bw0) continue;
         if (fixed) {
-            rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est, ewt, colmax,
-                                  stats, err, s);
+            rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_FIXED, nullptr, nullptr, L, 0, nullptr, est,
+                                  ewt, colmax, stats, err, s);
             if (rc) break;
-            rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, colmax, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol, (long long)hmax * L, s);
+            rc = run_q(timed, g, colmax, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol,
+                       (long long)hmax * L, s);
             if (rc) break;
             continue;
         }
         // variable-length walks: count pass, scan, emit at exact offsets
-        long long nwb = bw1 - bw0;
+        const long long nwb = bw1 - bw0;
         long long *elen = nullptr;
-        MCF_CUDA(cudaMallocAsync(&elen, sizeof(long long) * (2 * nwb + 1), s));
+        cudaError_t ce_ = cudaMallocAsync(&elen, sizeof(long long) * (2 * nwb + 1), s);
+        if (ce_ != cudaSuccess) {
+            rc = cuda_status(ce_, "cudaMallocAsync(elen)");
+            break;
+        }
+        AsyncFrees batch_frees(s);
+        batch_frees.keep(elen);
         long long *eoff = elen + nwb;
-        rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, nwb, EMIT_COUNT, nullptr, nullptr, 0, 0, elen, nullptr, nullptr,
                               nullptr, stats, err, s);
         if (rc) break;
         rc = exclusive_scan_i64(elen, eoff, nwb, s);
         if (rc) break;
         long long total = 0;
-        MCF_CUDA(cudaMemcpyAsync(&total, eoff + nwb, sizeof(long long), cudaMemcpyDeviceToHost, s));
-        MCF_CUDA(cudaStreamSynchronize(s));
+        ce_ = cudaMemcpyAsync(&total, eoff + nwb, sizeof(long long), cudaMemcpyDeviceToHost, s);
+        if (ce_ == cudaSuccess) ce_ = cudaStreamSynchronize(s);
+        if (ce_ != cudaSuccess) {
+            rc = cuda_status(ce_, "emission count");
+            break;
+        }
         if (total > buf_slots) {
             cudaFreeAsync(est, s);
             cudaFreeAsync(ewt, s);
+            est = nullptr;
+            ewt = nullptr;
             buf_slots = total;
-            MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * buf_slots, s));
-            MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s));
+            ce_ = cudaMallocAsync(&est, sizeof(int) * buf_slots, s);
+            if (ce_ == cudaSuccess) ce_ = cudaMallocAsync(&ewt, sizeof(double) * buf_slots, s);
+            if (ce_ != cudaSuccess) {
+                rc = cuda_status(ce_, "cudaMallocAsync(emissions)");
+                break;
+            }
         }
-        rc = launch_walk_emit(g, p, walk_pre, c0, c1, bw1 - bw0, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, colmax,
-                              stats, err, s);
+        rc = launch_walk_emit(g, p, walk_pre, c0, c1, nwb, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt,
+                              colmax, stats, err, s);
         if (rc) break;
-        rc = run_q((p->flags & MCF_FLAG_TIME_KERNELS) != 0, g, colmax, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
-        cudaFreeAsync(elen, s);
+        rc = run_q(timed, g, colmax, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
         if (rc) break;
     }
-    delete[] hb;
-    cudaFreeAsync(colmax, s);
-    cudaFreeAsync(est, s);
-    cudaFreeAsync(ewt, s);
-    cudaFreeAsync(dbounds, s);
-    cudaFreeAsync(err, s);
+    if (est) cudaFreeAsync(est, s);
+    if (ewt) cudaFreeAsync(ewt, s);
     return rc;
 }
 
@@ -1426,12 +1409,16 @@ static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     MCF_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * ldq * (ce - cb), s));
     if (we == wb) return MCF_OK;
     const long long nw = we - wb;
+    MCF_ARG(nw < WALKS_PER_LAUNCH, "mcf_walk_qdense: walks per call must be below 2^31 (split the column range)");
+    AsyncFrees frees(s);
     unsigned long long *colmax = nullptr;
     long long *elen = nullptr;
     int *err = nullptr;
     MCF_CUDA(cudaMallocAsync(&colmax, sizeof(unsigned long long) * g->n, s));
+    frees.keep(colmax);
     MCF_CUDA(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * g->n, s));
     MCF_CUDA(cudaMallocAsync(&elen, sizeof(long long) * (2 * nw + 1) + 16, s));
+    frees.keep(elen);
     long long *eoff = elen + nw;
     err = reinterpret_cast<int *>(eoff + nw + 1);
     MCF_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
@@ -1447,7 +1434,9 @@ static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     int *est = nullptr;
     double *ewt = nullptr;
     MCF_CUDA(cudaMallocAsync(&est, sizeof(int) * (total > 0 ? total : 1), s));
+    frees.keep(est);
     MCF_CUDA(cudaMallocAsync(&ewt, sizeof(double) * (total > 0 ? total : 1), s));
+    frees.keep(ewt);
     rc = launch_walk_emit(g, p, walk_pre, cb, ce, nw, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt, colmax,
                           stats, err, s);
     if (rc) return rc;
@@ -1458,10 +1447,62 @@ static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     k_qdense<<<grid, 512, smem, s>>>(walk_pre, cb, ce, wb, eoff, est, ewt, colmax, g->n, Q, ldq);
     mcf::note_launch();
     MCF_LAUNCHED("k_qdense");
-    cudaFreeAsync(est, s);
-    cudaFreeAsync(ewt, s);
-    cudaFreeAsync(elen, s);
-    cudaFreeAsync(colmax, s);
+    return MCF_OK;
+}
+
+// Variance of d_i from G walk-group passes (MCF_FLAG_WALK_GROUP): for every
+// entry (i, c), the group partials P_g = pcol_g[(i, c)] (walks w = g mod G of
+// column c, W0 = 1/N_c) give group means Y_g = N_c P_g / n_g of the per-walk
+// contribution, n_g = |{w < N_c : w = g mod G}|; the between-group sum of
+// squares SSB = sum_g n_g (Y_g - Y)^2, Y = sum_g P_g, has expectation
+// (G' - 1) sigma_c^2 (G' = min(G, N_c) non-empty groups), so
+// Var(pcol) ~ SSB / ((G' - 1) N_c), and Var(d_i) = sum_c Var(pcol[(i, c)])
+// (columns are independent).  4 lanes per row, as k_diag_final.
+__global__ void k_diag_variance(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                                const long long *__restrict__ csr2csc, const double *__restrict__ pg, long long nnz,
+                                int G, const long long *__restrict__ walk_pre, double *__restrict__ var, long long rb,
+                                long long re) {
+    const long long i = rb + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 2);
+    const int sub = threadIdx.x & 3;
+    double s = 0.0;
+    if (i < re) {
+        for (long long e = row_ptr[i] + sub; e < row_ptr[i + 1]; e += 4) {
+            const int c = col_ids[e];
+            const long long nc = walk_pre[c + 1] - walk_pre[c];
+            const long long gn = nc < G ? nc : G;
+            if (gn < 2) continue;
+            const long long p = csr2csc[e];
+            double tot = 0.0;
+            for (int g = 0; g < G; ++g) tot += pg[(long long)g * nnz + p];
+            const double ybar = tot;  // mean per-walk contribution: N_c * pcol / N_c
+            double ssb = 0.0;
+            for (int g = 0; g < gn; ++g) {
+                const double ng = (double)(nc / G + (g < nc % G ? 1 : 0));
+                const double yg = (double)nc * pg[(long long)g * nnz + p] / ng;
+                ssb += ng * (yg - ybar) * (yg - ybar);
+            }
+            s += ssb / ((double)(gn - 1) * (double)nc);
+        }
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, 4);
+    if (i < re && sub == 0) var[i] = s;
+}
+
+static int diag_variance(mcf_graph *g, const double *pcol_groups, int groups, const long long *walk_pre, double *var,
+                         long long rb, long long re, cudaStream_t s) {
+    MCF_ARG(g && pcol_groups && walk_pre && var, "mcf_diag_variance: null argument");
+    MCF_ARG(groups >= 2 && groups <= 256, "mcf_diag_variance: groups must be in [2, 256]");
+    MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_diag_variance: bad row range");
+    int rc = ensure_csr2csc(g, s);
+    if (rc) return rc;
+    const long long rows = re - rb;
+    if (rows == 0) return MCF_OK;
+    k_diag_variance<<<(unsigned)((rows * 4 + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids,
+                                                                       (const long long *)g->csr2csc, pcol_groups,
+                                                                       g->nnz, groups, walk_pre, var, rb, re);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_diag_variance");
     return MCF_OK;
 }
 
@@ -1522,6 +1563,12 @@ int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_
                     int64_t col_end, double *Q, int64_t ldq, int64_t *stats, void *stream) {
     return mcf::qdense(g, p, (const long long *)walk_pre, col_begin, col_end, Q, ldq, (long long *)stats,
                        (cudaStream_t)stream);
+}
+
+int mcf_diag_variance(mcf_graph *g, const double *pcol_groups, int groups, const int64_t *walk_pre, double *var,
+                      int64_t row_begin, int64_t row_end, void *stream) {
+    return mcf::diag_variance(g, pcol_groups, groups, (const long long *)walk_pre, var, row_begin, row_end,
+                              (cudaStream_t)stream);
 }
 
 int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d, int64_t row_begin,

@@ -22,6 +22,23 @@ void set_error(const std::string &msg);
 int cuda_status(cudaError_t e, const char *what);
 void note_launch();  // counts kernel launches (mcf_kernel_launches)
 
+// Stream-ordered allocations released on every return path of a host driver
+// (error returns included): frees run in reverse order on the stream.
+struct AsyncFrees {
+    cudaStream_t s;
+    std::vector<void *> p;
+    explicit AsyncFrees(cudaStream_t st) : s(st) {}
+    template <class T>
+    T *keep(T *x) {
+        p.push_back((void *)x);
+        return x;
+    }
+    ~AsyncFrees() {
+        for (auto it = p.rbegin(); it != p.rend(); ++it)
+            if (*it) cudaFreeAsync(*it, s);
+    }
+};
+
 }  // namespace mcf
 
 #define MCF_CUDA(call)                                                  \
@@ -391,6 +408,10 @@ int allocate_walks(mcf_graph *g, long long n_walks, long long *ni, long long *wa
 size_t fused_scratch_bytes();       // scratch of the one-kernel budget path
 size_t fused_scratch_zero_bytes();  // its prefix that must be zero
 bool fused_alloc_applies(const mcf_graph *g);
+int column_batches(const long long *walk_pre, long long cb, long long ce, long long cap_walks,
+                   std::vector<long long> &bounds, unsigned long long *max_walks, cudaStream_t s);
+// largest walk count one walk launch takes (lane walk indices are int)
+constexpr long long WALKS_PER_LAUNCH = (1ll << 31) - 4096;
 int read_walk_range(const long long *walk_pre, long long col_begin, long long col_end,
                     long long *wb, long long *we, cudaStream_t s);
 int sm_count();

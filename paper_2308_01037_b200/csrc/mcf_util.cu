@@ -123,11 +123,12 @@ int exclusive_scan_i64(const long long *in, long long *out, long long n, cudaStr
 // walk-block -> column index for a column range
 // ---------------------------------------------------------------------------
 __global__ void k_blk_col(const long long *__restrict__ walk_pre, long long col_begin, long long col_end,
-                          int *__restrict__ blk_col) {
+                          long long capacity, int *__restrict__ blk_col) {
     long long c = col_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= col_end) return;
     const long long walk_begin = __ldg(walk_pre + col_begin);
     long long a = walk_pre[c] - walk_begin, b = walk_pre[c + 1] - walk_begin;
+    if (b > capacity) b = capacity;  // walks past the capacity are never run (the walk kernels clamp)
     if (b <= a) return;
     const long long B = 1ll << WALK_BLK_SHIFT;
     for (long long blk = (a + B - 1) >> WALK_BLK_SHIFT; blk * B < b; ++blk) blk_col[blk] = (int)c;
@@ -140,9 +141,76 @@ int build_blk_col(const long long *walk_pre, long long col_begin, long long col_
     MCF_CUDA(cudaMallocAsync(blk_col, sizeof(int) * nb, s));
     long long nc = col_end - col_begin;
     if (nc > 0 && capacity > 0) {
-        k_blk_col<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(walk_pre, col_begin, col_end, *blk_col);
+        k_blk_col<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(walk_pre, col_begin, col_end, capacity, *blk_col);
         mcf::note_launch();
         MCF_LAUNCHED("k_blk_col");
+    }
+    return MCF_OK;
+}
+
+__global__ void k_batch_bounds(const long long *__restrict__ walk_pre, long long cb, long long ce, long long wb,
+                               long long cap_walks, long long nb, long long *__restrict__ bounds) {
+    long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    if (b == 0) { bounds[0] = cb; return; }
+    if (b == nb) { bounds[nb] = ce; return; }
+    long long target = wb + b * cap_walks;  // largest c in [cb, ce] with walk_pre[c] <= target
+    long long lo = cb, hi = ce;
+    while (lo < hi) {
+        long long mid = (lo + hi + 1) >> 1;
+        if (walk_pre[mid] <= target) lo = mid;
+        else hi = mid - 1;
+    }
+    bounds[b] = lo;
+}
+
+__global__ void k_max_walks(const long long *__restrict__ walk_pre, long long cb, long long ce,
+                            unsigned long long *out) {
+    long long c = cb + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = (c < ce) ? (unsigned long long)(walk_pre[c + 1] - walk_pre[c]) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_xor_sync(MCF_FULL, v, o);
+        v = x > v ? x : v;
+    }
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(out, v);
+}
+
+// Column batches of [cb, ce) with at most cap_walks + max N_c walks each
+// (bounds[b] .. bounds[b+1]); *max_walks = the largest N_c of the range.
+// Synchronises the stream.
+int column_batches(const long long *walk_pre, long long cb, long long ce, long long cap_walks,
+                   std::vector<long long> &bounds, unsigned long long *max_walks, cudaStream_t s) {
+    bounds.assign(1, cb);
+    if (ce <= cb) {
+        bounds.push_back(ce);
+        if (max_walks) *max_walks = 0;
+        return MCF_OK;
+    }
+    long long wb = 0, we = 0;
+    int rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
+    if (rc) return rc;
+    if (cap_walks < 1) cap_walks = 1;
+    const long long nb = (we - wb + cap_walks - 1) / cap_walks > 0 ? (we - wb + cap_walks - 1) / cap_walks : 1;
+    unsigned long long *d = nullptr;
+    MCF_CUDA(cudaMallocAsync(&d, sizeof(long long) * (nb + 2), s));
+    MCF_CUDA(cudaMemsetAsync(d, 0, sizeof(long long), s));
+    const long long ncol = ce - cb;
+    k_max_walks<<<(unsigned)((ncol + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, d);
+    mcf::note_launch();
+    long long *db = reinterpret_cast<long long *>(d + 1);
+    k_batch_bounds<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, s>>>(walk_pre, cb, ce, wb, cap_walks, nb, db);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_batch_bounds");
+    std::vector<unsigned long long> h((size_t)nb + 2);
+    MCF_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(long long) * (nb + 2), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    MCF_CUDA(cudaFreeAsync(d, s));
+    if (max_walks) *max_walks = h[0];
+    bounds.clear();
+    for (long long b = 0; b <= nb; ++b) {
+        const long long v = (long long)h[1 + b];
+        if (bounds.empty() || v != bounds.back()) bounds.push_back(v);
     }
     return MCF_OK;
 }
@@ -302,3 +370,53 @@ int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s) {
 }
 
 }  // namespace mcf
+
+// ---------------------------------------------------------------------------
+// Per-column work estimates for cost-balanced column shards (SURVEY 8(e):
+// "contiguous column ranges balanced by the prefix sum of N_i x expected
+// length").  Action: N_c walks.  Diag: the walk emissions N_c (L + 1)
+// weighted by DIAG_WALK_WEIGHT plus the Eq. 20 combine's probes
+// sum_{i in C_c} min(deg i, N_c (L + 1)) (one warp per column, CSC order).
+// ---------------------------------------------------------------------------
+namespace mcf {
+
+constexpr long long DIAG_WALK_WEIGHT = 3;  // measured: a walk emission costs ~2.5 combine probes (R-MAT 2^22)
+
+__global__ void k_column_costs(const long long *__restrict__ walk_pre, const long long *__restrict__ csc_ptr,
+                               const int *__restrict__ csc_rows, const long long *__restrict__ row_ptr, long long n,
+                               long long steps, int mode, long long *__restrict__ cost) {
+    const long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= n) return;
+    const long long nc = walk_pre[c + 1] - walk_pre[c];
+    if (mode == 0 || nc == 0) {
+        if (lane == 0) cost[c] = nc;
+        return;
+    }
+    const long long m = nc * steps;
+    long long acc = 0;
+    for (long long e = csc_ptr[c] + lane; e < csc_ptr[c + 1]; e += 32) {
+        const int i = __ldg(csc_rows + e);
+        const long long d = __ldg(row_ptr + i + 1) - __ldg(row_ptr + i);
+        acc += d < m ? d : m;
+    }
+    acc = warp_sum_ll(acc);
+    if (lane == 0) cost[c] = DIAG_WALK_WEIGHT * m + acc;
+}
+
+}  // namespace mcf
+
+extern "C" int mcf_column_costs(mcf_graph *g, const int64_t *walk_pre, int64_t max_steps, int mode, int64_t *cost,
+                                void *stream) {
+    MCF_ARG(g && walk_pre && cost, "mcf_column_costs: null argument");
+    MCF_ARG(mode == 0 || mode == 1, "mcf_column_costs: mode must be 0 (action) or 1 (diag)");
+    MCF_ARG(max_steps >= 1, "mcf_column_costs: max_steps must be at least 1");
+    if (g->n == 0) return MCF_OK;
+    const long long steps = max_steps + 1;
+    mcf::k_column_costs<<<(unsigned)((g->n * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        (const long long *)walk_pre, (const long long *)g->csc_ptr, g->csc_rows, (const long long *)g->row_ptr, g->n,
+        steps, mode, (long long *)cost);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_column_costs");
+    return MCF_OK;
+}

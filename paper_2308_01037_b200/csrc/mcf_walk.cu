@@ -35,6 +35,7 @@ struct WalkCommon {
     const long long *__restrict__ walk_pre;
     const int *__restrict__ blk_col;
     long long col_begin, col_end;  // walk range = [walk_pre[col_begin], walk_pre[col_end]), read on the device
+    long long capacity;            // walks the per-walk buffers hold (a larger range is clamped and flagged)
     int col_last;
     long long max_steps;
     double cutoff;
@@ -44,6 +45,7 @@ struct WalkCommon {
     unsigned *counter;  // walks handed out (chunked, relative to the range start)
     unsigned long long *colmax;  // diag: per-column max |emission| (IEEE bits), or null
     int return_only;             // MCF_FLAG_RETURN_ONLY
+    unsigned grp_n, grp_i;       // MCF_FLAG_WALK_GROUP: run only walks w = grp_i mod grp_n (0: all)
     long long *stats;
     int *err;
     const uint2 *__restrict__ lean;         // v = 1 on uniform-value graphs (else null)
@@ -139,6 +141,17 @@ __device__ __forceinline__ WarpPool make_pool(int nw_total) {
     int c = nw_total / (warps * 8);
     c = c < 32 ? 32 : (c > 256 ? 256 : c);
     return WarpPool{0, 0, c & ~31};
+}
+
+// Walks of the launch: the range read from walk_pre, clamped to the buffers'
+// capacity (budgets summing past the caller's walk_capacity would otherwise
+// write past them); a clamp sets error bit 8, which the host reports.
+__device__ __forceinline__ int clamp_walks(const WalkCommon &a, long long nw) {
+    if (nw > a.capacity) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && a.err) atomicOr(a.err, 8);
+        nw = a.capacity;
+    }
+    return (int)nw;
 }
 
 template <bool REPLAY, bool LEAN = false>
@@ -309,7 +322,7 @@ template <bool REPLAY, bool FAT, int NW, int OCC = 5, bool LEAN = false>
 __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(WalkCommon a, double *__restrict__ xw) {
     l2_prefetch_tables(a);
     const long long wb = __ldg(a.walk_pre + a.col_begin);
-    const int nw = (int)(__ldg(a.walk_pre + a.col_end) - wb);
+    const int nw = clamp_walks(a, __ldg(a.walk_pre + a.col_end) - wb);
     Lane L[NW];
 #pragma unroll
     for (int s = 0; s < NW; ++s) L[s].rel = -1;
@@ -325,6 +338,12 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
 #pragma unroll
         for (int s = 0; s < NW; ++s) {
             if (L[s].rel < 0) continue;
+            if (a.grp_n && L[s].k == 0 && L[s].wl % a.grp_n != a.grp_i) {  // walk outside the group
+                xw[L[s].rel] = 0.0;
+                L[s].rel = -1;
+                --n_walks;
+                continue;
+            }
             // q_c += zeta W r[l]; classic MC diagonal: only back at the start (Alg. 1)
             // lean walks (v = 1, uniform values): the payload r = A 1 is the row sum itself
             const double pay = LEAN ? L[s].h.rsum
@@ -368,7 +387,7 @@ __global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long 
     constexpr bool REPLAY = MODE == EMIT_REPLAY;
     if (MODE != EMIT_COUNT) l2_prefetch_tables(a);
     const long long wb = __ldg(a.walk_pre + a.col_begin);
-    const int nw = (int)(__ldg(a.walk_pre + a.col_end) - wb);
+    const int nw = clamp_walks(a, __ldg(a.walk_pre + a.col_end) - wb);
     Lane L;
     L.rel = -1;
     WarpPool P = make_pool(nw);
@@ -391,6 +410,14 @@ __global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long 
             } else if (MODE == EMIT_EXPLICIT) {
                 sb = eaux[rel];
                 scap = eaux[rel + 1] - sb;
+            }
+            if (!REPLAY && a.grp_n && L.wl % a.grp_n != a.grp_i) {  // walk outside the group: no emission
+                if (MODE == EMIT_COUNT) eaux[rel] = 0;
+                else
+                    for (long long t = 0; t < scap; ++t) __stcs(est + sb + t * stride, -1);
+                --n_walks;
+                L.rel = -1;
+                continue;
             }
         }
         if (MODE != EMIT_COUNT) {
@@ -745,6 +772,8 @@ int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *
             "weight_cutoff must lie strictly between 0 and 1");                         // walker.py:64-65
     MCF_ARG(p->max_steps < (1ll << 31), "max_steps must be below 2^31");
     MCF_ARG(p->zeta, "zeta coefficients missing");
+    MCF_ARG(!(p->flags & MCF_FLAG_WALK_GROUP) || MCF_GROUP_INDEX(p->flags) < MCF_GROUP_COUNT(p->flags),
+            "walk group index must be below the group count");
     MCF_ARG(0 <= cb && cb <= ce && ce <= g->n, "bad column range");
     return MCF_OK;
 }
@@ -770,6 +799,8 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.blk_col = *blk;
     a.col_begin = cb;
     a.col_end = ce;
+    a.capacity = capacity;
+    a.err = nullptr;
     a.col_last = (int)(ce > cb ? ce - 1 : cb);
     a.max_steps = p->max_steps;
     a.cutoff = p->weight_cutoff;
@@ -783,6 +814,8 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.rsum_by_deg = nullptr;
     a.row_ptr = (const long long *)g->row_ptr;
     a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
+    a.grp_n = (p->flags & MCF_FLAG_WALK_GROUP) ? (unsigned)MCF_GROUP_COUNT(p->flags) : 0u;
+    a.grp_i = (p->flags & MCF_FLAG_WALK_GROUP) ? (unsigned)MCF_GROUP_INDEX(p->flags) : 0u;
     for (int k = 0; k < 3; ++k) {
         a.pf[k] = nullptr;
         a.pf_bytes[k] = 0;
@@ -929,12 +962,16 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
                      long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
                      long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
                      long long *stats, int *err, cudaStream_t s) {
+    MCF_ARG(nwalks < WALKS_PER_LAUNCH, "walks per launch must be below 2^31 - 4096");
+    AsyncFrees frees(s);
     WalkCommon a;
     int *blk = nullptr;
     int rc = setup_common(g, p, walk_pre, cb, ce, nwalks, a, &blk, s);
     if (rc) return rc;
+    frees.keep(blk);
     unsigned *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long), s));
+    frees.keep(counter);
     MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     a.counter = counter;
     a.err = err;
@@ -977,35 +1014,63 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     }
     mcf::note_launch();
     MCF_LAUNCHED("k_walk_emit");
-    rc = timed_end(timed, g->ev_walk, s);
-    if (rc) return rc;
-    cudaFreeAsync(counter, s);
-    cudaFreeAsync(blk, s);
-    return MCF_OK;
+    return timed_end(timed, g->ev_walk, s);
 }
 
 static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                   const long long *walk_off, const int *entries, const double *r, double *q, double *qvar,
                   long long *stats, cudaStream_t s, bool replay, bool aux_ready = false, int *blk_ready = nullptr,
-                  bool lean = false, double *xw_ready = nullptr, unsigned *counter_ready = nullptr) {
+                  bool lean = false, double *xw_ready = nullptr, unsigned *counter_ready = nullptr,
+                  bool capacity_exact = false) {
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
     MCF_ARG(r && q && stats, "action walk: null r/q/stats");
+    MCF_ARG(!(replay && (p->flags & MCF_FLAG_WALK_GROUP)), "walk groups apply to device-RNG walks, not replay");
     if (replay) MCF_ARG(walk_off && entries, "replay: null stream");
-    WalkCommon a;
-    int *blk = nullptr;
     long long nw = 0;
     rc = walk_capacity(p, walk_pre, cb, ce, &nw, s);
     if (rc) return rc;
+    if (nw >= WALKS_PER_LAUNCH && !blk_ready) {
+        // more walks than one launch indexes (int lanes): read the exact count
+        // and, if it is still too large, run the range in column batches of at
+        // most 2^30 walks (+ one column) -- q per column is the same either way
+        long long wb = 0, we = 0;
+        rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
+        if (rc) return rc;
+        nw = we - wb;
+        if (nw >= WALKS_PER_LAUNCH) {
+            std::vector<long long> hb;
+            unsigned long long hmax = 0;
+            rc = column_batches(walk_pre, cb, ce, 1ll << 30, hb, &hmax, s);
+            if (rc) return rc;
+            MCF_ARG(hmax < (1ull << 30), "a column's walk budget must be below 2^30");
+            mcf_walk_params pb = *p;
+            pb.walk_capacity = 0;  // each batch reads its exact range
+            for (size_t b = 0; b + 1 < hb.size(); ++b) {
+                rc = action(g, &pb, walk_pre, hb[b], hb[b + 1], walk_off, entries, r, q, qvar, stats, s, replay,
+                            b > 0 || aux_ready, nullptr, lean);
+                if (rc) return rc;
+            }
+            return MCF_OK;
+        }
+    }
+    MCF_ARG(nw < WALKS_PER_LAUNCH, "walks per call must be below 2^31 - 4096 (split the column range)");
+    AsyncFrees frees(s);
+    WalkCommon a;
+    int *blk = nullptr;
     rc = setup_common(g, p, walk_pre, cb, ce, nw, a, &blk, s, blk_ready);
     if (rc) return rc;
-    MCF_ARG(nw < (1ll << 31) - 4096, "walks per call must be below 2^31 (split the column range)");
+    if (!blk_ready) frees.keep(blk);
     double *xw = xw_ready;
     unsigned *counter = counter_ready;  // preallocated: already zero (funm_action's one memset)
     int *err = nullptr;
-    if (!xw) MCF_CUDA(cudaMallocAsync(&xw, sizeof(double) * (nw > 0 ? nw : 1), s));
+    if (!xw) {
+        MCF_CUDA(cudaMallocAsync(&xw, sizeof(double) * (nw > 0 ? nw : 1), s));
+        frees.keep(xw);
+    }
     if (!counter) {
         MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) + sizeof(int) * 2, s));
+        frees.keep(counter);
         MCF_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
     }
     err = (int *)(counter + 2);
@@ -1083,13 +1148,20 @@ static int action(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
         MCF_LAUNCHED("k_col_reduce");
     }
     int herr = 0;
-    if (replay) {
+    // replay streams are always checked; a caller-supplied walk_capacity (an
+    // upper bound the device cannot verify without a sync) is checked whenever
+    // the stream is not being captured into a CUDA graph
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    MCF_CUDA(cudaStreamIsCapturing(s, &cap_st));
+    if (replay || (p->walk_capacity > 0 && !capacity_exact && cap_st == cudaStreamCaptureStatusNone)) {
         MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
         MCF_CUDA(cudaStreamSynchronize(s));
     }
-    if (!xw_ready) cudaFreeAsync(xw, s);
-    if (!counter_ready) cudaFreeAsync(counter, s);
-    if (!blk_ready) cudaFreeAsync(blk, s);
+    if (herr & 8) {
+        set_error("walk budgets of the column range exceed walk_capacity (" + std::to_string(p->walk_capacity) +
+                  "): pass the exact walk count or 0");
+        return MCF_ERR_ARGUMENT;
+    }
     if (herr) {
         set_error("replay stream inconsistent with the walk (code " + std::to_string(herr) +
                   "): entries missing, surplus, or outside the current row");
@@ -1129,7 +1201,34 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     MCF_ARG(g && r && q && y && walk_pre, "mcf_funm_action: null argument");  // ni optional
     int rc0 = ensure_side_stream(g);
     if (rc0) return rc0;
-    MCF_ARG(p && n_walks >= 1 && n_walks < (1ll << 31) - 4096, "mcf_funm_action: n_walks must be in [1, 2^31 - 4096)");
+    MCF_ARG(p && n_walks >= 1, "mcf_funm_action: n_walks must be at least 1");
+    if (n_walks >= WALKS_PER_LAUNCH) {
+        // more walks than one launch indexes: budgets, r = A v, then the walks
+        // in column batches (mcf_walk_action's path), then y -- not capturable
+        AsyncFrees frees(s);
+        long long *ni_ = ni;
+        if (!ni_) {
+            MCF_CUDA(cudaMallocAsync(&ni_, sizeof(long long) * g->n, s));
+            frees.keep(ni_);
+        }
+        int rc = allocate_walks(g, n_walks, ni_, walk_pre, nullptr, s);
+        if (rc) return rc;
+        MCF_CUDA(cudaMemsetAsync(stats, 0, sizeof(long long) * 4, s));
+        if (v) {
+            rc = spmv(g, 0.0, nullptr, 0.0, nullptr, v, r, 0, g->n, s, g->hdr);
+            if (rc) return rc;
+        } else {
+            k_r_ones<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, g->n, r, stats);
+            mcf::note_launch();
+            MCF_LAUNCHED("k_r_ones");
+        }
+        mcf_walk_params pp = *p;
+        pp.walk_capacity = 0;
+        const bool lean = !v && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
+        rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, nullptr, lean);
+        if (rc) return rc;
+        return spmv(g, z0, v ? v : V_ONES, z1, r, q, y, 0, g->n, s);
+    }
     // one scratch block, one memset: [walk counter + error flags | budget-kernel state | blk | xw]
     const bool fused = fused_alloc_applies(g);
     const size_t ctl = 256, fz = fused ? fused_scratch_zero_bytes() : 0, fb = fused ? fused_scratch_bytes() : 0;
@@ -1178,7 +1277,8 @@ static int funm_action(mcf_graph *g, const mcf_walk_params *p, long long n_walks
     mcf_walk_params pp = *p;
     pp.walk_capacity = n_walks;  // exact: the budgets sum to n_walks
     const bool lean = v == V_ONES && !(p->flags & MCF_FLAG_RETURN_ONLY) && lean_eligible(g);
-    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk, lean, xw, counter);
+    rc = action(g, &pp, walk_pre, 0, g->n, nullptr, nullptr, r, q, qvar, stats, s, false, true, blk, lean, xw, counter,
+                true);
     if (rc) return rc;
     if (lean_ones && fused)
         rc = spmv(g, z0, v, z1, nullptr, q, y, 0, g->n, s, nullptr, RowSumR{g->rsum_by_deg, r});

@@ -88,6 +88,18 @@ class WalkParams:
                                  int(config.seed) & 0xFFFFFFFFFFFFFFFF, self.zeta.data_ptr(),
                                  int(config.n_walks), 0)
 
+    def derive(self, capacity: int | None = None, flags: int | None = None) -> "WalkParams":
+        """A copy with another walk_capacity (the exact walk count of a call:
+        a shard's walks, or the sum of explicit budgets; 0 = read it on the
+        device) and/or flags; shares the device zeta table."""
+        out = WalkParams.__new__(WalkParams)
+        out.zeta = self.zeta
+        c = self.c
+        out.c = N.McfWalkParams(c.max_steps, c.weight_cutoff, c.seed, c.zeta,
+                                c.walk_capacity if capacity is None else int(capacity),
+                                c.flags if flags is None else int(flags))
+        return out
+
 
 class DeviceGraph:
     """Square sparse matrix on one GPU, scaled by ``gamma`` on the device.
@@ -313,6 +325,22 @@ class DeviceGraph:
         ys = (C.c_void_p * len(d_outs))(*[int(p) for p in d_outs])
         N.check(N.lib().mcf_diag_combine_peer(self.handle, float(z0), float(z1), xs, bs, len(pcol_parts), ys,
                                               len(d_outs), int(rb), int(re), self.stream), "mcf_diag_combine_peer")
+
+    def column_costs(self, walk_pre, max_steps: int, mode: str = "diag") -> torch.Tensor:
+        """Per-column work estimate (int64, device) for cost-balanced shards:
+        N_c for action; emissions plus Eq. 20 combine probes for diag."""
+        cost = torch.empty(self.n, dtype=torch.int64, device=self.device)
+        N.check(N.lib().mcf_column_costs(self.handle, _ptr(walk_pre), int(max_steps), 1 if mode == "diag" else 0,
+                                         _ptr(cost), self.stream), "mcf_column_costs")
+        return cost
+
+    def diag_variance(self, pcol_groups: torch.Tensor, walk_pre, var=None, rows=None):
+        """Var(d_i) from G walk-group partial vectors (pcol_groups: G x nnz)."""
+        var = self._f64() if var is None else var
+        rb, re = (0, self.n) if rows is None else rows
+        N.check(N.lib().mcf_diag_variance(self.handle, _ptr(pcol_groups), int(pcol_groups.shape[0]), _ptr(walk_pre),
+                                          _ptr(var), int(rb), int(re), self.stream), "mcf_diag_variance")
+        return var
 
     def diag_combine(self, z0, z1, pcol, d=None, rows=None):
         d = self._f64() if d is None else d

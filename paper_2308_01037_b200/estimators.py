@@ -67,14 +67,19 @@ def _cfg_echo(cfg, coeffs, mode):
 
 
 def _budgets(g: DeviceGraph, cfg, replay, budgets):
+    """(ni, walk_pre, total walks).  Explicit budgets and replay streams carry
+    their own walk count, which becomes the calls' exact walk_capacity (the
+    device buffers are sized by it; a mismatch with config.n_walks is fine)."""
     if replay is not None:
         pre = np.asarray(replay.walk_pre, dtype=np.int64)
         if pre.size != g.n + 1:
             raise ArgumentError("replay stream has the wrong number of columns")
-        return g.budgets(np.diff(pre))
+        ni = np.diff(pre)
+        return (*g.budgets(ni), int(ni.sum()))
     if budgets is not None:
-        return g.budgets(budgets)
-    return g.allocate(cfg.n_walks)
+        b = np.asarray(budgets, dtype=np.int64)
+        return (*g.budgets(b), int(b.sum()))
+    return (*g.allocate(cfg.n_walks), int(cfg.n_walks))
 
 
 def _replay_tensors(g: DeviceGraph, replay):
@@ -124,15 +129,15 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
         y, ni, pre = g.funm_action(params, cfg.n_walks, None if ones else vd, z[0], z[1], r, q, torch.empty_like(q),
                                    qvar, st)
     elif replay is None:
-        ni, pre = _budgets(g, cfg, replay, budgets)
+        ni, pre, total = _budgets(g, cfg, replay, budgets)
         r = g.spmv(vd)
-        g.walk_action(params, pre, r, q, qvar, stats=st)
+        g.walk_action(params.derive(capacity=total), pre, r, q, qvar, stats=st)
         y = g.spmv(q, alpha=z[0], v=vd, beta=z[1], r=r)
     else:
-        ni, pre = _budgets(g, cfg, replay, budgets)
+        ni, pre, total = _budgets(g, cfg, replay, budgets)
         r = g.spmv(vd)                       # r = A v
         off, ent = _replay_tensors(g, replay)
-        g.replay_action(params, pre, off, ent, r, q, stats=st)
+        g.replay_action(params.derive(capacity=total), pre, off, ent, r, q, stats=st)
         y = g.spmv(q, alpha=z[0], v=vd, beta=z[1], r=r)   # y = z0 v + z1 r + A q
     res = FunmResult(y if as_tensor else to_host(y), "action", config=_cfg_echo(cfg, coeffs, mode))
     _stats(res, st)
@@ -149,10 +154,17 @@ def rand_funm_action(a, coeffs, v, config, *, replay=None, budgets=None, stderr:
 
 
 def rand_funm_diag(a, coeffs, config, *, replay=None, budgets=None, device=None,
-                   as_tensor: bool = False) -> FunmResult:
+                   as_tensor: bool = False, stderr: bool = False, groups: int = 16) -> FunmResult:
     """d ~ diag f(A) by Eq. 20:
     d_i = zeta_0 + zeta_1 a_ii + sum_c a_ic <Q_c, C_i>,
-    Q_c[j] = sum over visits of j by walks from c of zeta_{k+2} W_k (W_0 = 1/N_c)."""
+    Q_c[j] = sum over visits of j by walks from c of zeta_{k+2} W_k (W_0 = 1/N_c).
+
+    ``stderr=True`` attaches the Monte Carlo standard error of every d_i
+    (SPEC.md:410): ``groups`` more passes, each walking only the walks
+    w = g mod groups of every column (same Philox streams), give per-entry
+    batch means whose spread estimates Var(pcol[(i, c)]); the columns are
+    independent, so Var(d_i) is their sum (mcf_diag_variance).  Device RNG
+    only; costs ``groups`` extra estimator passes."""
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
     n, nnz = _n_nnz(a)
@@ -160,9 +172,13 @@ def rand_funm_diag(a, coeffs, config, *, replay=None, budgets=None, device=None,
     mode = "replay" if replay is not None else "philox"
     if nnz == 0:  # A = 0 -> d = zeta_0 exactly
         return FunmResult(np.full(n, z[0]), "diag", config=_cfg_echo(cfg, coeffs, mode))
+    if stderr and replay is not None:
+        raise ArgumentError("stderr needs device-RNG walks (not replay)")
+    if stderr and not 2 <= int(groups) <= 256:
+        raise ArgumentError("groups must be in [2, 256]")
     g = _graph(a, device)
-    params = WalkParams(cfg, z, g.device)
-    ni, pre = _budgets(g, cfg, replay, budgets)
+    ni, pre, total = _budgets(g, cfg, replay, budgets)
+    params = WalkParams(cfg, z, g.device).derive(capacity=total)
     pcol = torch.zeros(g.nnz, dtype=torch.float64, device=g.device)
     st = g.new_stats()
     if replay is None:
@@ -174,6 +190,16 @@ def rand_funm_diag(a, coeffs, config, *, replay=None, budgets=None, device=None,
     res = FunmResult(d if as_tensor else to_host(d), "diag", config=_cfg_echo(cfg, coeffs, mode))
     _stats(res, st)
     res.aux = {"pcol": pcol, "ni": ni, "walk_pre": pre}
+    if stderr:
+        from . import _native as N
+        G = int(groups)
+        pg = torch.zeros((G, g.nnz), dtype=torch.float64, device=g.device)
+        gst = g.new_stats()
+        for k in range(G):
+            g.walk_diag(params.derive(flags=N.group_flags(G, k)), pre, pg[k], stats=gst)
+        var = g.diag_variance(pg, pre)
+        res.stderr = torch.sqrt(var).cpu().numpy()
+        res.aux["groups"] = G
     return res
 
 
@@ -206,15 +232,16 @@ def rand_funm_entry(a, coeffs, v, i: int, config, *, replay=None, device=None) -
     if hi == lo:  # empty row: y_i = zeta_0 v_i exactly, no walk
         return empty
     if replay is not None:
-        ni, pre = _budgets(g, cfg, replay, None)
+        ni, pre, total = _budgets(g, cfg, replay, None)
     else:
         p = g.tables()["init_prob"][cols].cpu().numpy()
         nib = np.zeros(n, dtype=np.int64)
         if p.sum() > 0:
             nib[cols.cpu().numpy()] = largest_remainder(p / p.sum(), cfg.n_walks)
         ni, pre = g.budgets(nib)
+        total = int(nib.sum())
     vd = torch.from_numpy(np.ascontiguousarray(v_np)).to(g.device)
-    params = WalkParams(cfg, z, g.device)
+    params = WalkParams(cfg, z, g.device).derive(capacity=total)
     r = g.spmv(vd)
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
     st = g.new_stats()
@@ -260,8 +287,9 @@ def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None 
                           config=_cfg_echo(cfg, coeffs, smode))
     g = _graph(a, device)
     rows = [int(i)] if mode == "entry" else None
+    rtotal = None
     if replay is not None:
-        ni, pre = _budgets(g, cfg, replay, None)
+        ni, pre, rtotal = _budgets(g, cfg, replay, None)
     else:
         nib = np.zeros(n, dtype=np.int64)
         nib[rows if rows is not None else slice(None)] = cfg.n_walks
@@ -285,7 +313,7 @@ def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None 
             g.walk_action(params, pre, payload, q, cols=(lo, hi), stats=st)
     else:
         off, ent = _replay_tensors(g, replay)
-        g.replay_action(params, pre, off, ent, payload, q, stats=st)
+        g.replay_action(params.derive(capacity=rtotal), pre, off, ent, payload, q, stats=st)
     out = to_host(q)
     res = FunmResult(out if mode != "entry" else np.array([out[int(i)]]), "mc-" + mode,
                      config=_cfg_echo(cfg, coeffs, smode))

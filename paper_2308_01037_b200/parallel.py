@@ -3,23 +3,29 @@ sharded.
 
 Every column's walks run on exactly one rank; the Philox stream is keyed by
 (seed, column, walk, step), so a column produces the same bits wherever it
-runs.  The only exchange is assembling the per-column results:
-  * action: q (8 n bytes) -- each rank contributes its own column range, the
-    rest of its vector is zero, so a SUM all-reduce is an exact concatenation;
-    then y over the rank's row range, assembled the same way;
-  * diag: the per-entry partials pcol (8 nnz bytes), assembled the same way,
-    then d over the rank's row range.
-Results are therefore bitwise identical for 1, 2, 4 and 8 GPUs.
+runs.  Shards are contiguous column ranges balanced by a per-column cost
+(``mcf_column_costs``: walks for action; emissions plus Eq. 20 combine probes
+for diag -- the hub columns of R-MAT / Chung-Lu graphs hold most of the
+combine work), and every call gets its shard's exact walk count as
+walk_capacity (per-rank buffers are sized by the shard, not by N_s).  The
+only exchange is assembling the per-column results:
+  * action: q by column shard (all_gather_into_tensor of each rank's own
+    range), then y by row shard;
+  * diag: the per-entry partials of a column shard (a contiguous CSC range),
+    then d by row shard.
+Results are bitwise identical for 1, 2, 4 and 8 GPUs.
 
-sharded_action_peer folds the action exchange into the combine instead: the
-ranks map each other's q and y buffers (CUDA IPC over NVLink) and one SpMV per
-rank gathers q from the owning ranks and writes its y rows into every rank's
-buffer (mcf_spmv_peer) -- two barriers, no NCCL on the data path.
+sharded_action_peer / sharded_diag_peer fold the exchange into the combine
+instead: the ranks map each other's buffers (CUDA IPC over NVLink) and one
+kernel per rank gathers q (or the partials) from the owning ranks and writes
+its rows of y (or d) into every rank's buffer -- two barriers, no NCCL on the
+data path.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 import torch
@@ -37,43 +43,67 @@ def world():
     return 0, 1
 
 
-def column_shards(walk_pre, parts: int):
-    """Contiguous column ranges with ~equal walk counts (walk_pre: n+1 prefix)."""
-    if torch.is_tensor(walk_pre):  # search on the device, copy back parts+1 ints
-        n = walk_pre.numel() - 1
-        k = torch.arange(1, parts, device=walk_pre.device, dtype=torch.int64)
-        tgt = (walk_pre[-1] * k + parts - 1) // parts
-        inner = torch.searchsorted(walk_pre, tgt, side="left").cpu().numpy()
+def _cuts(prefix, parts: int):
+    """Indices k_1..k_{parts-1} splitting a non-decreasing prefix (length n+1)
+    into parts of ~equal total: k_j = first index with prefix >= j/parts of
+    the total."""
+    if torch.is_tensor(prefix):  # search on the device, copy back parts-1 ints
+        k = torch.arange(1, parts, device=prefix.device, dtype=torch.int64)
+        tgt = (prefix[-1] * k + parts - 1) // parts
+        return torch.searchsorted(prefix, tgt, side="left").cpu().numpy()
+    pre = np.asarray(prefix, dtype=np.int64)
+    tgt = (int(pre[-1]) * np.arange(1, parts) + parts - 1) // parts
+    return np.searchsorted(pre, tgt, side="left")
+
+
+def column_shards(walk_pre, parts: int, cost=None):
+    """Contiguous start-column ranges, one per rank.  Balanced by walk count
+    (walk_pre: n+1 prefix), or -- with ``cost`` (per-column work, e.g.
+    DeviceGraph.column_costs) -- by the prefix sum of the cost (SURVEY 8(e):
+    "balanced by the prefix sum of N_i x expected length"; the paper fixes the
+    same imbalance with dynamic scheduling)."""
+    n = (walk_pre.numel() if torch.is_tensor(walk_pre) else len(walk_pre)) - 1
+    if cost is None:
+        inner = _cuts(walk_pre, parts)
     else:
-        pre = np.asarray(walk_pre, dtype=np.int64)
-        n = pre.size - 1
-        tgt = (int(pre[-1]) * np.arange(1, parts) + parts - 1) // parts
-        inner = np.searchsorted(pre, tgt, side="left")
+        cp = torch.zeros(n + 1, dtype=torch.int64, device=cost.device) if torch.is_tensor(cost) else np.zeros(n + 1, np.int64)
+        if torch.is_tensor(cost):
+            torch.cumsum(cost, 0, out=cp[1:])
+        else:
+            cp[1:] = np.cumsum(np.asarray(cost, dtype=np.int64))
+        inner = _cuts(cp, parts)
     cuts = np.concatenate([[0], inner, [n]])
     cuts = np.maximum.accumulate(np.minimum(cuts, n))
     return [(int(cuts[i]), int(cuts[i + 1])) for i in range(parts)]
 
 
-def _shards(peers, g, pre, n_walks: int, parts: int):
-    """column_shards, remembered per (graph, N_s, parts) on the peer buffers."""
-    key = (id(g), int(n_walks), int(parts))
+def shard_walks(walk_pre, shards):
+    """Walk count of every shard (the exact walk_capacity of its calls)."""
+    idx = [shards[0][0]] + [b for _, b in shards]
+    if torch.is_tensor(walk_pre):
+        v = walk_pre[torch.tensor(idx, device=walk_pre.device)].cpu().numpy()
+    else:
+        v = np.asarray(walk_pre, dtype=np.int64)[idx]
+    return [int(v[i + 1] - v[i]) for i in range(len(shards))]
+
+
+def _shards(peers, g, pre, n_walks: int, parts: int, mode: str, max_steps: int):
+    """Cost-balanced column shards and their walk counts, remembered per
+    (graph, N_s, ranks, mode) on the peer buffers (a function of the budgets
+    only, so repeated passes skip the device reads that find them)."""
+    key = (id(g), int(n_walks), int(parts), mode, int(max_steps))
     hit = peers.shard_cache.get(key)
-    if hit is None or hit[0] is not g:
-        hit = (g, column_shards(pre, parts))
+    if hit is None or hit[0]() is not g:
+        cost = g.column_costs(pre, max_steps, mode) if parts > 1 else None
+        sh = column_shards(pre, parts, cost)
+        hit = (weakref.ref(g), sh, shard_walks(pre, sh))
         peers.shard_cache[key] = hit
-    return hit[1]
+    return hit[1], hit[2]
 
 
 def row_shards(n: int, parts: int):
     b = [n * k // parts for k in range(parts + 1)]
     return [(b[i], b[i + 1]) for i in range(parts)]
-
-
-def assemble(t: torch.Tensor, group=None) -> torch.Tensor:
-    """Disjoint per-rank pieces (zeros elsewhere) -> full vector on every rank."""
-    if world()[1] > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t
 
 
 class _CudaArray:
@@ -160,11 +190,12 @@ def sharded_action_peer(g: DeviceGraph, coeffs, v, config, *, params=None, group
     if own:
         peers = PeerBuffers([8 * g.n, 8 * g.n], group)
     ni, pre = g.allocate(cfg.n_walks)
-    shards = _shards(peers, g, pre, cfg.n_walks, size)
+    shards, walks = _shards(peers, g, pre, cfg.n_walks, size, "action", cfg.max_steps)
     bounds = [shards[0][0]] + [b for _, b in shards]
     st = g.new_stats()
     r = g.spmv(v)
-    g.walk_action(params, pre, r, _Raw(peers.ptrs[rank][0]), cols=shards[rank], stats=st)
+    g.walk_action(params.derive(capacity=walks[rank]), pre, r, _Raw(peers.ptrs[rank][0]), cols=shards[rank],
+                  stats=st)
     torch.cuda.synchronize()
     dist.barrier(group=group)  # every rank's q shard is complete
     g.spmv_peer([peers.ptrs[k][0] for k in range(size)], bounds, [peers.ptrs[k][1] for k in range(size)],
@@ -192,11 +223,11 @@ def sharded_diag_peer(g: DeviceGraph, coeffs, config, *, params=None, group=None
     if own:
         peers = PeerBuffers([8 * g.nnz, 8 * g.n], group)
     ni, pre = g.allocate(cfg.n_walks)
-    shards = _shards(peers, g, pre, cfg.n_walks, size)
+    shards, walks = _shards(peers, g, pre, cfg.n_walks, size, "diag", cfg.max_steps)
     bounds = [shards[0][0]] + [b for _, b in shards]
     st = g.new_stats()
     _device_view(peers.ptrs[rank][0], g.nnz, g.device).zero_()  # columns without walks keep zero partials
-    g.walk_diag(params, pre, _Raw(peers.ptrs[rank][0]), cols=shards[rank], stats=st)
+    g.walk_diag(params.derive(capacity=walks[rank]), pre, _Raw(peers.ptrs[rank][0]), cols=shards[rank], stats=st)
     torch.cuda.synchronize()
     dist.barrier(group=group)  # every rank's partials are complete
     g.diag_combine_peer(z[0], z[1], [peers.ptrs[k][0] for k in range(size)], bounds,
@@ -209,9 +240,34 @@ def sharded_diag_peer(g: DeviceGraph, coeffs, config, *, params=None, group=None
     return d, st
 
 
+def gather_ranges(t: torch.Tensor, bounds, group=None) -> torch.Tensor:
+    """Every rank holds its own slice t[bounds[r]:bounds[r+1]] (contiguous,
+    disjoint, covering [bounds[0], bounds[-1])); after the call every rank
+    holds all of them.  One NCCL all_gather_into_tensor of equal-length
+    (padded) pieces: each rank sends only its own bytes, not a zero-padded
+    full vector (an all-reduce moves twice as much)."""
+    rank, size = world()
+    if size == 1:
+        return t
+    lens = [int(bounds[k + 1] - bounds[k]) for k in range(size)]
+    L = max(1, max(lens))
+    # gloo (CPU tests, the shared-GPU functional mode) gathers host tensors
+    dev = t.device if dist.get_backend(group) != "gloo" else torch.device("cpu")
+    send = torch.zeros(L, dtype=t.dtype, device=dev)
+    send[:lens[rank]] = t[bounds[rank]:bounds[rank + 1]].to(dev)
+    recv = torch.empty(size * L, dtype=t.dtype, device=dev)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    recv = recv.to(t.device)
+    for k in range(size):
+        if k != rank and lens[k]:
+            t[bounds[k]:bounds[k + 1]] = recv[k * L:k * L + lens[k]]
+    return t
+
+
 def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=None, group=None):
     """One RandFunmAction pass with this rank's share of the start columns.
-    ``v=None`` is v = 1.  Returns (y, stats) with y assembled on every rank."""
+    ``v=None`` is v = 1.  Returns (y, stats) with y assembled on every rank:
+    q is all-gathered by column shard, y by row shard."""
     rank, size = world()
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
@@ -226,34 +282,46 @@ def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=No
         v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     st = g.new_stats()
-    cols = column_shards(pre, size)[rank]
-    rows = row_shards(g.n, size)[rank]
+    shards = column_shards(pre, size)
+    walks = shard_walks(pre, shards)
+    rows = row_shards(g.n, size)
     r = g.spmv(v)
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
-    g.walk_action(params, pre, r, q, cols=cols, stats=st)
-    assemble(q, group)
+    g.walk_action(params.derive(capacity=walks[rank]), pre, r, q, cols=shards[rank], stats=st)
+    gather_ranges(q, [shards[0][0]] + [b for _, b in shards], group)
     y = torch.zeros(g.n, dtype=torch.float64, device=g.device) if size > 1 else None
-    y = g.spmv(q, alpha=z[0], v=v, beta=z[1], r=r, out=y, rows=rows)
-    assemble(y, group)
+    y = g.spmv(q, alpha=z[0], v=v, beta=z[1], r=r, out=y, rows=rows[rank])
+    gather_ranges(y, [rows[0][0]] + [b for _, b in rows], group)
     return y, st
 
 
 def sharded_diag(g: DeviceGraph, coeffs, config, *, params=None, budgets=None, group=None):
-    """One RandFunmDiag pass with this rank's share of the start columns."""
+    """One RandFunmDiag pass with this rank's share of the start columns
+    (cost-balanced shards).  The per-entry partials of a column shard are a
+    contiguous CSC range, all-gathered; then d by row shard, all-gathered.
+    Bitwise identical to one GPU."""
     rank, size = world()
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
     z = coeffs.prefix(cfg.max_steps + 2)
     params = params or WalkParams(cfg, z, g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
-    st = g.new_stats()
-    cols = column_shards(pre, size)[rank] if size > 1 else (0, g.n)
-    rows = row_shards(g.n, size)[rank] if size > 1 else (0, g.n)
+    if size > 1:
+        shards = column_shards(pre, size, g.column_costs(pre, cfg.max_steps, "diag"))
+        walks = shard_walks(pre, shards)
+        cols = shards[rank]
+        cap = walks[rank]
+    else:
+        cols = (0, g.n)
+        cap = int(pre[-1]) if budgets is not None else cfg.n_walks
+    rows = row_shards(g.n, size)
     pcol = torch.zeros(g.nnz, dtype=torch.float64, device=g.device)
     st = g.new_stats()
-    g.walk_diag(params, pre, pcol, cols=cols, stats=st)
-    assemble(pcol, group)
+    g.walk_diag(params.derive(capacity=cap), pre, pcol, cols=cols, stats=st)
+    if size > 1:
+        cb = g.csc_ptr[torch.tensor([shards[0][0]] + [b for _, b in shards], device=g.device)].cpu().numpy()
+        gather_ranges(pcol, cb, group)
     d = torch.zeros(g.n, dtype=torch.float64, device=g.device)
-    g.diag_combine(z[0], z[1], pcol, d, rows=rows)
-    assemble(d, group)
+    g.diag_combine(z[0], z[1], pcol, d, rows=rows[rank])
+    gather_ranges(d, [rows[0][0]] + [b for _, b in rows], group)
     return d, st
