@@ -2,17 +2,26 @@
 """Benchmark of the walk-sampling estimator (BASELINE.json metric: walk-steps/s
 and nodes/s; achieved HBM GB/s vs peak).
 
-Default workload = BASELINE configs[1] ("config 2"): total communicability
-exp(beta A) 1 on a Barabasi-Albert graph, n = 1e6, m = 4, beta = 1/lambda_max,
-30 Taylor terms (max_steps = 28), 10,000 batches x 64 = 640,000 walks.
-A "step" is one full estimator pass: walk budgets, r = A v (v = 1: the row
-sums), the walks, the per-column reduction and y = z0 v + z1 r + A q.
+Default workload (N = 1) = BASELINE configs[2] ("config 3"), the largest
+configuration that fits one GPU and the one the metric is quoted on for a
+single B200: subgraph centrality diag(exp(beta A)) on a symmetrised R-MAT
+graph, scale 22, edge factor 16, beta = 1/lambda_max, 25 Taylor terms
+(max_steps = 23), 200 walks per node.  A "step" is one full estimator pass:
+walk budgets, the walks, the Q_c rows and the Eq. 20 combine, d.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|1] [--impl mcfunm|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3|1|2|4|5] [--impl mcfunm|reference]
 
-Under torchrun (N > 1) the start columns are sharded over the ranks and the
-per-column results assembled with NCCL (paper_2308_01037_b200/parallel.py).
-Prints one JSON line on rank 0.
+Inputs come from tools/bench_graphs.py: a fixed recipe (numpy / scipy / torch
+only), cached so both arms read the same CSR and beta bits.
+
+--impl reference times the reference's own CPU algorithm -- the oracle port
+of walker.run_walks_batch (same PCG64DXSM streams, global searchsorted) plus
+the restated Eq. 20 / Alg. 3 accumulation -- on all host cores, over a
+stratified sample of the walked columns, extrapolated to the full estimate
+(BASELINE.md §3).  Under torchrun (N > 1) the device arm shards the start
+columns over the ranks (cost-balanced, paper_2308_01037_b200/parallel.py) and
+assembles the result in peer memory or over NCCL.  Prints one JSON line on
+rank 0.
 """
 
 from __future__ import annotations
@@ -20,6 +29,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -31,66 +41,63 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BASELINE_METRIC = "walk-steps/s and nodes/s at 1/2/4/8 B200; achieved HBM GB/s vs peak"
-BYTES_PER_STEP = 64  # two dependent random 32-B sectors per emitted step (DESIGN.md §4)
+BYTES_PER_STEP = 64  # two dependent random 32-B sectors per emitted step (SURVEY 8d)
 
 CONFIGS = {
-    2: dict(workload="config2: total communicability exp(beta A) 1, Barabasi-Albert n=1e6 m=4, "
-                     "beta=1/lambda_max, 30 Taylor terms, 10,000 batches x 64 walks",
-            kind="action", graph="ba", n=1_000_000, m=4, n_walks=640_000, max_steps=28, cutoff=1e-300, seed=0),
     1: dict(workload="config1: subgraph centrality diag(exp(beta A)), Erdos-Renyi n=1e4 mean degree 8 (LCC), "
                      "beta=1/lambda_max, 30 Taylor terms, 1000 walks per node",
             kind="diag", graph="er", n=10_000, deg=8, walks_per_node=1000, max_steps=28, cutoff=1e-300, seed=0),
+    2: dict(workload="config2: total communicability exp(beta A) 1, Barabasi-Albert n=1e6 m=4, "
+                     "beta=1/lambda_max, 30 Taylor terms, 10,000 batches x 64 walks",
+            kind="action", graph="ba", n=1_000_000, m=4, n_walks=640_000, max_steps=28, cutoff=1e-300, seed=0),
     3: dict(workload="config3: subgraph centrality diag(exp(beta A)), symmetrised R-MAT scale 22 edge factor 16 "
                      "(.57,.19,.19,.05), no loops/duplicates, beta=1/lambda_max, 25 Taylor terms, 200 walks per node",
             kind="diag", graph="rmat", scale=22, ef=16, walks_per_node=200, max_steps=23, cutoff=1e-300, seed=0),
-    5: dict(workload="config5: subgraph centrality diag(exp(beta A)), Chung-Lu n=1.6e7 exponent 2.1 mean degree 20 "
-                     "max degree 1e5, beta=1/lambda_max, 25 Taylor terms, 100 walks per node",
-            kind="diag", graph="chunglu", n=16_000_000, walks_per_node=100, max_steps=23, cutoff=1e-300, seed=0),
     4: dict(workload="config4: Katz resolvent (I - gamma A)^-1 1, symmetrised R-MAT scale 24 edge factor 16 "
                      "(.57,.19,.19,.05), no loops/duplicates, gamma=0.85/lambda_max, W_c=1e-8, 100 walks per node",
             kind="action", graph="rmat", scale=24, ef=16, walks_per_node=100, max_steps=10_000, cutoff=1e-8, seed=0,
             func="resolvent", gamma_frac=0.85),
+    5: dict(workload="config5: subgraph centrality diag(exp(beta A)), Chung-Lu n=1.6e7 exponent 2.1 mean degree 20 "
+                     "max degree 1e5, beta=1/lambda_max, 25 Taylor terms, 100 walks per node",
+            kind="diag", graph="chunglu", n=16_000_000, walks_per_node=100, max_steps=23, cutoff=1e-300, seed=0),
 }
+DEFAULT_CONFIG = 3
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def make_graph(cfg, pinned=False, scale=None):
-    """Host SparseMatrix (for the e2e leg), the scale factor (beta, or the Katz
-    gamma) and N_s.  R-MAT configs are generated on the GPU and copied to
-    pinned host memory once (setup, untimed)."""
-    from paper_2308_01037_b200 import graphs
-    if cfg["graph"] in ("rmat", "chunglu"):
+def graph_spec(cfg):
+    keys = ("graph", "n", "m", "deg", "scale", "ef", "seed")
+    return {k: cfg[k] for k in keys if k in cfg}
+
+
+def make_graph(cfg, pinned=False):
+    """Host SparseMatrix of the config's graph (values 1), the scale factor
+    (beta = 1/lambda_max, or the Katz gamma) and N_s, from the cached recipe."""
+    from paper_2308_01037_b200.sparsemat import SparseMatrix
+    from tools import bench_graphs
+    t0 = time.perf_counter()
+    gd = bench_graphs.load(graph_spec(cfg), log=log)
+    n, rp, ci = gd["n"], gd["row_ptr"], gd["col_ids"]
+    vals = np.ones(ci.size)
+    if pinned:
         import torch
-        from paper_2308_01037_b200.device import DeviceGraph
-        from paper_2308_01037_b200.sparsemat import SparseMatrix
-        sc = scale or cfg.get("scale")
-        if cfg["graph"] == "rmat":
-            n, rp, ci = graphs.rmat_device(sc, cfg["ef"], seed=cfg["seed"])
-        else:
-            n, rp, ci = graphs.chung_lu_device(cfg["n"], seed=cfg["seed"])
-        g1 = DeviceGraph.from_device_arrays(n, rp, ci, torch.ones(ci.numel(), dtype=torch.float64, device=rp.device))
-        lam = graphs.lambda_max_device(g1)
-        g1.close()
-        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (rp, ci)]
-        host[0].copy_(rp)
-        host[1].copy_(ci)
-        vals = torch.ones(ci.numel(), dtype=torch.float64, pin_memory=True)
-        a = SparseMatrix.from_csr_arrays(n, host[0].numpy(), host[1].numpy(), vals.numpy(), symmetric_hint=True,
-                                         meta={"generator": cfg["graph"], "scale": sc, "lambda_max": lam})
-        a._pinned = (host, vals)
-        del rp, ci
-        torch.cuda.empty_cache()
-        scale_factor = cfg.get("gamma_frac", 1.0) / lam
-    elif cfg["graph"] == "ba":
-        a = graphs.barabasi_albert(cfg["n"], cfg["m"], seed=cfg["seed"], pinned=pinned)
-        scale_factor = 1.0 / graphs.lambda_max(a)
-    else:
-        a = graphs.erdos_renyi_lcc(cfg["n"], cfg["deg"], seed=cfg["seed"])
-        scale_factor = 1.0 / graphs.lambda_max(a)
-    n_walks = cfg.get("n_walks") or cfg["walks_per_node"] * a.n
+        bufs = [torch.empty(x.shape, dtype={np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,
+                                             np.dtype(np.float64): torch.float64}[x.dtype], pin_memory=True)
+                for x in (rp, ci, vals)]
+        for bt, x in zip(bufs, (rp, ci, vals)):
+            bt.numpy()[:] = x
+        rp, ci, vals = (bt.numpy() for bt in bufs)
+    a = SparseMatrix.from_csr_arrays(n, rp, ci, vals, symmetric_hint=True,
+                                     meta={"generator": cfg["graph"], "lambda_max": gd["lambda_max"]})
+    if pinned:
+        a._pinned = bufs
+    scale_factor = cfg.get("gamma_frac", 1.0) / gd["lambda_max"]
+    n_walks = cfg.get("n_walks") or cfg["walks_per_node"] * n
+    log(f"[bench] graph {cfg['graph']} n={n} nnz={ci.size} lambda_max={gd['lambda_max']:.12g} "
+        f"({'cached' if gd.get('cached') else 'generated'}, {time.perf_counter() - t0:.1f}s)")
     return a, scale_factor, n_walks
 
 
@@ -106,6 +113,18 @@ def measured_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_cpu():
+    model = platform.processor() or ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "os_cpu_count": os.cpu_count()}
 
 
 # --------------------------------------------------------------------------
@@ -174,104 +193,201 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------
-# CPU legs (oracle port of the reference, sampled)
+# CPU legs: the reference algorithm (oracle/port.py), stratified column sample
 # --------------------------------------------------------------------------
 _CPU = {}
 
 
-def _cpu_worker(cols):
+def _cpu_worker(task):
+    """One chunk of sampled start columns of one stratum: (stratum, columns,
+    emissions, CPU seconds).  Runs in a forked worker that shares the tables."""
     from oracle import port
+    stratum, cols = task
     g = _CPU
-    t0 = time.perf_counter()
+    t0 = time.process_time()
     if g["kind"] == "action":
         _, em = port.action_columns(g["t"], g["r"], g["z"], g["ni"], cols, g["max_steps"], g["cutoff"], g["seed"])
     else:
-        _, em = port.diag_columns(g["A"], g["t"], g["z"], g["ni"], cols, g["max_steps"], g["cutoff"], g["seed"])
-    return em, time.perf_counter() - t0
+        out = np.zeros(g["A"].n)
+        _, em = port.diag_columns(g["A"], g["t"], g["z"], g["ni"], cols, g["max_steps"], g["cutoff"], g["seed"],
+                                  out=out)
+    return stratum, len(cols), em, time.process_time() - t0
 
 
 class CpuBaseline:
-    """The reference's CPU algorithm (oracle/port.py restatement, same
-    PCG64DXSM streams and searchsorted walker) over a bounded, evenly spaced
-    sample of the walked columns, on all host cores (fork pool)."""
+    """The reference's CPU algorithm on the host cores: the oracle port of
+    walker.py (per-column PCG64DXSM streams, global searchsorted walker,
+    walker.py:173-290) plus the restated accumulation and combine (Eq. 20 /
+    Alg. 3), one forked worker per core over start-column chunks (the result
+    does not depend on the split: every column has its own stream).
+
+    Full estimates take minutes to hours on a CPU, so every run times a
+    seeded, cost-stratified sample of the walked columns: the walked columns
+    are sorted by their work estimate (walk emissions and, for diag, the Eq.
+    20 probes -- the combine dominates on hub columns) and cut into STRATA
+    groups of equal total work; each run draws columns from every group.  The
+    full single-core time is the size-weighted sum of the per-group CPU time
+    per column; the all-core time divides it by the cores times the measured
+    parallel efficiency of the run."""
+
+    STRATA = 8
 
     def __init__(self, a, beta, n_walks, cfg, cores=None):
         import multiprocessing as mp
         from oracle import port
         t0 = time.perf_counter()
-        A = port.Csr.from_any(a).scaled(beta)
+        n = int(a.n)
+        rp = np.asarray(a.csr.indptr, dtype=np.int64)
+        ci = np.asarray(a.csr.indices, dtype=np.int64)
+        vals = np.asarray(a.csr.data, dtype=np.float64) * beta
+        # symmetric 0/1 graphs: the CSC arrays are the CSR arrays
+        A = port.Csr(n, rp, ci, vals, rp, ci, vals)
         t = port.transition_tables(A)
         ni = port.allocate(t, n_walks)
         z = port.zeta_prefix(cfg.get("func", "exponential"), cfg["max_steps"] + 2)
-        _CPU.update(kind=cfg["kind"], t=t, A=A, ni=ni, z=z, r=A.scipy_csr() @ np.ones(A.n),
-                    max_steps=cfg["max_steps"], cutoff=cfg["cutoff"], seed=cfg["seed"])
-        self.setup_s = time.perf_counter() - t0
+        r = A.scipy_csr() @ np.ones(n) if cfg["kind"] == "action" else None
+        _CPU.update(kind=cfg["kind"], t=t, A=A, ni=ni, z=z, r=r, max_steps=cfg["max_steps"], cutoff=cfg["cutoff"],
+                    seed=cfg["seed"])
+        self.n = n
+        self.kind = cfg["kind"]
         self.walked = np.flatnonzero(ni)
-        self.ni = ni
-        self.n = A.n
-        self.total_emissions_est = None
+        deg = np.diff(rp)
+        steps = min(cfg["max_steps"], 64) + 1
+        m = ni[self.walked] * steps
+        if cfg["kind"] == "diag":  # sum_{i in C_c} min(deg i, m_c) (CSC = CSR: symmetric)
+            col_of = np.repeat(np.arange(n), deg)
+            probes = np.bincount(col_of, weights=np.minimum(deg[ci], (ni * steps)[col_of]), minlength=n)
+            del col_of
+            cost = 3 * m + probes[self.walked]
+        else:
+            cost = m
+        order = np.argsort(cost, kind="stable")
+        cum = np.cumsum(cost[order].astype(np.float64))
+        cuts = np.searchsorted(cum, cum[-1] * np.arange(1, self.STRATA) / self.STRATA)
+        self.strata = [g for g in np.split(self.walked[order], cuts) if g.size]
+        self.stratum_cost = [float(np.sum(c)) for c in np.split(cost[order], cuts) if c.size]
         self.cores = cores or os.cpu_count() or 1
+        self.setup_s = time.perf_counter() - t0
         self.pool = mp.get_context("fork").Pool(self.cores)
-        # calibrate: per-column cost on a small evenly spaced probe
-        probe = self.walked[:: max(1, self.walked.size // 256)][:256]
-        em, dt = _cpu_worker(probe)
-        self.sec_per_col = dt / max(1, probe.size)
-        self.em_per_col = em / max(1, probe.size)
+        # calibration: CPU seconds per work unit on a small sample of every stratum
+        rng = np.random.default_rng(12345)
+        probe = [(k, rng.choice(s, size=min(s.size, 4), replace=False)) for k, s in enumerate(self.strata)]
+        res = self.pool.map(_cpu_worker, probe)
+        work = sum(self.stratum_cost[k] / self.strata[k].size * len(c) for k, c in probe)
+        self.sec_per_work = max(1e-12, sum(x[3] for x in res) / max(1.0, work))
+        self.runs = []
+        self.run_index = 0
+        log(f"[cpu] tables {self.setup_s:.1f}s, {self.walked.size} walked columns in {len(self.strata)} strata, "
+            f"{self.cores} workers")
 
     def run(self, budget_s):
-        k = int(min(self.walked.size, max(self.cores, self.cores * budget_s / max(self.sec_per_col, 1e-9))))
-        cols = self.walked[np.linspace(0, self.walked.size - 1, k).astype(np.int64)]
-        chunks = np.array_split(cols, self.cores * 4)
+        """One timed sample of about ``budget_s`` wall seconds on all cores."""
+        rng = np.random.default_rng(1000 + self.run_index)
+        self.run_index += 1
+        per = budget_s * self.cores / len(self.strata)  # CPU seconds per stratum
+        tasks = []
+        for k, s in enumerate(self.strata):
+            mean_work = self.stratum_cost[k] / s.size
+            want = int(min(s.size, max(1, round(per / (self.sec_per_work * mean_work)))))
+            cols = np.sort(rng.choice(s, size=want, replace=False))
+            pieces = max(1, min(want, self.cores))
+            tasks += [(k, c) for c in np.array_split(cols, pieces) if c.size]
         t0 = time.perf_counter()
-        res = self.pool.map(_cpu_worker, chunks)
+        res = self.pool.map(_cpu_worker, tasks, chunksize=1)
         wall = time.perf_counter() - t0
-        em = sum(r[0] for r in res)
-        return em, wall, k
+        self.runs.append((res, wall))
+        return res, wall
 
-    def describe(self, k):
-        return (f"{k} of {self.walked.size} walked start columns (evenly spaced by index), full walks of each "
-                f"column, reference PCG64DXSM streams; {self.cores} processes")
+    def estimate(self, runs=None):
+        """Extrapolated full estimate from the recorded sample runs."""
+        runs = self.runs if runs is None else runs
+        S = len(self.strata)
+        cols, em, cpu = np.zeros(S), np.zeros(S), np.zeros(S)
+        wall = cpu_all = 0.0
+        for res, w in runs:
+            wall += w
+            for k, nc, e, c in res:
+                cols[k] += nc
+                em[k] += e
+                cpu[k] += c
+                cpu_all += c
+        size = np.array([s.size for s in self.strata], dtype=np.float64)
+        have = cols > 0
+        t1 = float(np.sum(size[have] * cpu[have] / cols[have]))
+        e_full = float(np.sum(size[have] * em[have] / cols[have]))
+        eff = min(1.0, cpu_all / max(1e-9, wall * self.cores))
+        t_all = t1 / (self.cores * eff)
+        return {"emissions_full": e_full, "t1_full_s": t1, "t_all_full_s": t_all, "parallel_efficiency": eff,
+                "steps_per_s": e_full / t_all, "steps_per_s_1core": e_full / t1, "nodes_per_s": self.n / t_all,
+                "sample_columns": int(cols.sum()), "sample_emissions": int(em.sum()), "sample_wall_s": wall,
+                "sample_steps_per_s": float(em.sum()) / max(1e-9, wall)}
+
+    def describe(self, est):
+        return (f"{est['sample_columns']} sampled start columns (with repetition across runs; {self.walked.size} walked in all) ({est['sample_emissions']:.3g} "
+                f"emissions, {est['sample_wall_s']:.1f} s wall on {self.cores} processes), seeded and stratified "
+                f"into {len(self.strata)} groups of equal estimated work (walk emissions"
+                f"{' + Eq. 20 probes' if self.kind == 'diag' else ''}); full estimate extrapolated by group size "
+                f"(parallel efficiency {est['parallel_efficiency']:.2f}); reference algorithm = oracle port "
+                f"(PCG64DXSM streams, global searchsorted walker)")
 
     def close(self):
         self.pool.terminate()
 
 
-# --------------------------------------------------------------------------
+def cpu_line(cb, est):
+    return {"value": est["steps_per_s"], "unit": "steps/s", "cores": cb.cores, "kind": "port",
+            "sample": cb.describe(est), "value_1core": est["steps_per_s_1core"],
+            "nodes_per_s": est["nodes_per_s"], "full_estimate_s_all_cores": est["t_all_full_s"],
+            "full_estimate_s_1core": est["t1_full_s"], "sample_steps_per_s": est["sample_steps_per_s"],
+            "host": host_cpu(), "tables_s": cb.setup_s}
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     a, beta, n_walks = make_graph(cfg)
-    if cfg["graph"] in ("rmat", "chunglu"):
-        print(json.dumps({"impl": "reference", "unavailable": "the reference CPU algorithm needs ~80 GB of host RAM "
-                                                              "for this R-MAT graph's numpy tables"}), flush=True)
-        return 0
     cpu = CpuBaseline(a, beta, n_walks, cfg)
-    per_step = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = max(4.0, 75.0 / max(1, args.steps))
     for _ in range(args.warmup):
-        cpu.run(per_step / 4)
-    em_tot, wall_tot, k = 0, 0.0, 0
+        cpu.run(max(1.0, per_step / 4))
+    cpu.runs = []
     for _ in range(args.steps):
-        em, wall, k = cpu.run(per_step)
-        em_tot += em
-        wall_tot += wall
+        cpu.run(per_step)
+    est = cpu.estimate()
     cpu.close()
-    value = em_tot / wall_tot
-    total_em = cpu.em_per_col * cpu.walked.size
+    value = est["steps_per_s"]
     line = {
         "impl": "reference", "metric": "walk-steps/s", "baseline_metric": BASELINE_METRIC, "value": value,
         "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall_tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * est["t_all_full_s"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "nodes_per_s": cpu.n / (total_em / value),
+        "nodes_per_s": est["nodes_per_s"],
         "config": {"workload": cfg["workload"], "n": int(a.n), "nnz": int(a.nnz), "n_walks": int(n_walks),
                    "beta": beta, "max_steps": cfg["max_steps"], "weight_cutoff": cfg["cutoff"]},
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cpu.cores, "kind": "port",
-                         "sample": cpu.describe(k)},
+        "cpu_baseline": cpu_line(cpu, est),
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "timing": "each step = one stratified sample of the estimate on all host cores; value and ms_per_step are "
+                  "the full estimate extrapolated from the K timed samples",
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------------------
+# device arm
+# --------------------------------------------------------------------------
+def combine_bytes(g, pre):
+    """Algorithmic bytes of the Eq. 20 combine per estimate:
+    sum over walked columns c of sum_{a in C_c} (32 + 4 deg a) -- the (i, c)
+    entry's CSC offsets and the ids of C_a.  Device reduction (setup only)."""
+    import torch
+    deg = (g.csc_ptr[1:] - g.csc_ptr[:-1])
+    per_col = torch.zeros(g.n, dtype=torch.float64, device=g.device)
+    col_of = torch.repeat_interleave(torch.arange(g.n, device=g.device), deg)
+    per_col.index_add_(0, col_of, (32 + 4 * deg[g.csc_rows.to(torch.int64)]).to(torch.float64))
+    walked = (pre[1:] - pre[:-1]) > 0
+    return float(per_col[walked].sum())
 
 
 def run_device(args, cfg):
@@ -298,35 +414,22 @@ def run_device(args, cfg):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _native.lib()
 
-    t0 = time.perf_counter()
-    a, beta, n_walks = make_graph(cfg, pinned=True, scale=args.scale)
+    a, beta, n_walks = make_graph(cfg, pinned=True)
     per_gpu_walks = n_walks
     if world > 1 and args.scaling == "weak":
-        # weak scaling (the path partitions by start column, run instructions 5):
-        # every GPU keeps the config's walk budget, the N-GPU job walks N times
-        # as many over the same graph (its estimate has N times the samples)
+        # weak scaling: every GPU keeps the config's walk budget, the N-GPU job
+        # walks N times as many over the same graph
         n_walks = per_gpu_walks * world
     coeffs = coeff_stream(cfg)
-    log(f"[bench] graph n={a.n} nnz={a.nnz} beta={beta:.6e} walks={n_walks} ({time.perf_counter() - t0:.1f}s)")
     wcfg = mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"], cfg["seed"])
     z = coeffs.prefix(cfg["max_steps"] + 2)
     params = WalkParams(wcfg, z)
     g = DeviceGraph(a, gamma=beta)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=g.device)  # > 126 MB L2
-    # The write leaves L2 full of DIRTY lines whose write-back would otherwise
-    # land inside the next timed step; reading a second buffer of the same size
-    # (untimed) evicts them, so each step starts with no input cached and a
-    # clean L2 ("write": the write alone).
-    sweep = torch.zeros(32 << 20, dtype=torch.int64, device=g.device) if args.flush == "write+read" else None
-    sweep_out = torch.empty((), dtype=torch.int64, device=g.device)
 
     def flush_l2():
         flush.zero_()
-        if sweep is not None:
-            torch.sum(sweep, dim=0, out=sweep_out)
 
-    # N > 1: the exchange runs in peer memory (mcf_spmv_peer / mcf_diag_combine_peer
-    # over CUDA IPC / NVLink) unless --transport nccl; the buffers are mapped once
     peers = None
     if world > 1 and args.transport == "peer":
         peers = parallel.PeerBuffers([8 * g.n if cfg["kind"] == "action" else 8 * g.nnz, 8 * g.n])
@@ -346,8 +449,8 @@ def run_device(args, cfg):
     torch.cuda.synchronize()
     g.kernel_times(reset=True)
 
-    # One estimator pass has no host synchronisation on the action path, so on
-    # one GPU it is captured once as a CUDA graph and replayed per step.
+    # One action pass has no host synchronisation, so on one GPU it is captured
+    # once as a CUDA graph and replayed per step.
     params.c.flags = _native.MCF_FLAG_TIME_KERNELS
     graph = None
     launches_per_step = None
@@ -411,7 +514,6 @@ def run_device(args, cfg):
     if graph is None:
         walk_ms_tot, q_ms_tot, walk_launches = w_, q_, n_
     params.c.flags = 0
-    # emissions of the whole job (all ranks) over the timed steps
     em_t = torch.stack([s_[1] for s_ in stats]).sum().to(torch.float64).reshape(1)
     if world > 1:
         dist.all_reduce(em_t)
@@ -422,46 +524,51 @@ def run_device(args, cfg):
     value = em_per_step * args.steps / (ms / 1e3)
     nodes_per_s = g.n * args.steps / (ms / 1e3)
 
-    # ---- dominant kernel roofline -------------------------------------------------------
+    # ---- rooflines: the walk kernel and (diag) the Eq. 20 combine ------------------------
     peak, peak_src = measured_peak()
     walk_avg_ms = walk_ms_tot / max(1, walk_launches)
-    # this rank's launches process its share of a step; diag runs batch a step
-    # into several walk launches (emission-buffer budget), each one a slice
     walk_launches_per_step = max(1.0, walk_launches / max(1, args.steps))
     em_per_walk_launch = em_per_step / world / walk_launches_per_step
-    achieved = BYTES_PER_STEP * em_per_walk_launch / (walk_avg_ms / 1e3) / 1e9 if walk_avg_ms > 0 else None
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
-    if os.path.exists(tp):
-        with open(tp) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "kernel": "k_walk_action" if cfg["kind"] == "action" else "k_walk_emit",
-                "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "peak_source": peak_src, "bytes_per_step": BYTES_PER_STEP,
-                "kernel_ms_avg": walk_avg_ms, "kernel_share_of_step": (walk_ms_tot / ms) if ms else None,
-                "random_sector_ceiling_gsteps": 37.8,
-                "note": "algorithmic bytes = 64 B x emissions (row header + sampled entry, SURVEY 8d), kept for "
-                        "comparability; on uniform-value graphs the lean layout serves a step with ONE random 8-B "
-                        "entry. Random HBM reads top out at ~37.8 G/s on this B200 and each costs a 128-B line "
-                        "fill (tools/gups, profiles/r01/gups.txt): HBM-resident graphs (config 4) are bound by "
-                        "those fills (~88% of the copy peak in DRAM traffic); L2-resident ones (config 2) by the "
-                        "latency of the one dependent load, hence frac > 1 against HBM"}
-    roofline["walk_launches_per_step"] = walk_launches_per_step
-    # the walk's own ceilings (tools/gups.cu, profiles/r01/gups.txt): one dependent
-    # random load per step, 279 G/s when the table is L2-resident, 37.8 G/s from HBM
-    if walk_avg_ms > 0:
-        ksteps = em_per_walk_launch / (walk_avg_ms / 1e3)
-        roofline["kernel_steps_per_s"] = ksteps
-        roofline["l2_random_load_ceiling_gsteps"] = 279.2
-        roofline["frac_of_l2_random_load_ceiling"] = ksteps / 279.2e9
+    w_ach = BYTES_PER_STEP * em_per_walk_launch / (walk_avg_ms / 1e3) / 1e9 if walk_avg_ms > 0 else None
+
+    def traffic_of(kernel):
+        tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as fh:
+                t = json.load(fh)
+            return t.get(kernel, {}).get("dram_bytes_per_launch") if kernel in t else (
+                t.get("dram_bytes_per_launch") if kernel.startswith("k_walk") else None)
+        return None
+
+    walk_kernel = "k_walk_action" if cfg["kind"] == "action" else "k_walk_emit"
+    walk = {"bound": "hbm", "kernel": walk_kernel, "achieved": w_ach, "peak": peak, "unit": "GB/s",
+            "frac": (w_ach / peak) if w_ach else None, "traffic": traffic_of(walk_kernel), "peak_source": peak_src,
+            "bytes_per_step": BYTES_PER_STEP, "kernel_ms_avg": walk_avg_ms,
+            "launches_per_step": walk_launches_per_step,
+            "kernel_share_of_step": (walk_ms_tot / ms) if ms else None,
+            "kernel_steps_per_s": em_per_walk_launch / (walk_avg_ms / 1e3) if walk_avg_ms > 0 else None,
+            "l2_random_load_ceiling_gsteps": 279.2, "hbm_random_sector_ceiling_gsteps": 37.8,
+            "note": "algorithmic bytes = 64 B x emissions (row header + sampled entry, SURVEY 8d); the lean layout "
+                    "serves a step with ONE random 4/8-B entry, so L2-resident graphs run above 'HBM' speed and "
+                    "HBM-resident ones are bound by 128-B line fills (profiles/r01/gups.txt)"}
+    roofline = walk
     if cfg["kind"] == "diag":
-        roofline["q_kernel_ms"] = q_ms_tot / max(1, args.steps)
-        roofline["combine"] = {
-            "kernels": "k_diag_q, k_diag_qc<K>, k_diag_big (Q_c build + Eq. 20 combine)",
-            "ms_per_step": q_ms_tot / max(1, args.steps),
-            "share_of_step": (q_ms_tot / ms) if ms else None,
-            "bound": "probe round trips to shared / distributed shared / L2 tables (DESIGN 6), not DRAM bandwidth"}
+        _, pre_ = g.allocate(wcfg.n_walks)
+        cbytes = combine_bytes(g, pre_)
+        c_ms = q_ms_tot / max(1, args.steps)
+        c_ach = cbytes / (c_ms / 1e3) / 1e9 if c_ms > 0 else None
+        combine = {"bound": "hbm", "kernel": "k_diag_q + k_diag_qc<2/4/8> + k_diag_big (Eq. 20 combine)",
+                   "achieved": c_ach, "peak": peak, "unit": "GB/s", "frac": (c_ach / peak) if c_ach else None,
+                   "traffic": traffic_of("combine"), "peak_source": peak_src,
+                   "algorithmic_bytes_per_step": cbytes,
+                   "bytes_rule": "sum over walked c of sum_{a in C_c} (32 + 4 deg a) (SURVEY 8d)",
+                   "kernel_ms_avg": c_ms, "kernel_share_of_step": (q_ms_tot / ms) if ms else None}
+        if c_ms > walk_avg_ms * walk_launches_per_step:  # the dominant phase leads
+            roofline = dict(combine)
+            roofline["walk"] = walk
+        else:
+            roofline = dict(walk)
+            roofline["combine"] = combine
     elif q_ms_tot:  # action: the span before the walks (budgets, r) recorded by mcf_funm_action
         roofline["prewalk_ms_avg"] = q_ms_tot / max(1, args.steps)
 
@@ -470,9 +577,11 @@ def run_device(args, cfg):
     if not args.no_e2e:
         h2d = int(a.csr.indptr.nbytes + a.csr.indices.nbytes + a.csr.data.nbytes)
         d2h = 8 * a.n
+        step_s = ms / args.steps / 1e3
+        reps = max(1, args.steps if step_s < 1.0 else min(args.steps, 3))
+        e2e_warm = 1 if step_s >= 1.0 else max(1, args.warmup)
         e2e_ms = []
-        e2e_warm = max(1, args.warmup)  # first calls warm the pinned/device allocators
-        for i in range(max(1, args.steps) + e2e_warm):
+        for i in range(reps + e2e_warm):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -495,36 +604,38 @@ def run_device(args, cfg):
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
             e_ms = float(t_ms.item())
         e2e = {"value": em_per_step * len(e2e_ms) / (e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / len(e2e_ms),
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / len(e2e_ms), "reps": len(e2e_ms),
                "nodes_per_s": g.n * len(e2e_ms) / (e_ms / 1e3),
-               "path": "DeviceGraph(host SparseMatrix, gamma) + estimator + y to host: pinned H2D of CSR, pinned D2H of y"}
+               "path": "DeviceGraph(host SparseMatrix, gamma) + estimator + result to host: pinned H2D of the CSR, "
+                       "table build, the estimate, pinned D2H"}
 
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------
     cpu = None
-    if cfg["graph"] in ("rmat", "chunglu"):
-        cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": "not run: the oracle's numpy tables for this graph need tens of GB of host RAM (SURVEY §8c)"}
-    elif rank == 0 and world == 1 and not args.no_cpu:
-        cb = CpuBaseline(a, beta, n_walks, cfg)
-        em, wall, k = cb.run(args.cpu_seconds)
-        cpu = {"value": em / wall, "unit": "steps/s", "cores": cb.cores, "kind": "port", "sample": cb.describe(k)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        del g  # the device graph is no longer needed; free host staging before the CPU tables
+        torch.cuda.empty_cache()
+        cb = CpuBaseline(a, beta, wcfg.n_walks, cfg)
+        cb.run(args.cpu_seconds)
+        cpu = cpu_line(cb, cb.estimate())
         cb.close()
+        n_rows, nnz = a.n, a.nnz
+    else:
+        n_rows, nnz = g.n, g.nnz
 
     if rank == 0:
         line = {
             "metric": "walk-steps/s", "baseline_metric": BASELINE_METRIC, "value": value, "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "dtype": "f64", "data": "synthetic (tools/bench_graphs.py recipe)",
             "nodes_per_s": nodes_per_s,
-            "config": {"workload": cfg["workload"], "n": g.n, "nnz": g.nnz, "n_walks": int(n_walks),
+            "config": {"workload": cfg["workload"], "n": int(n_rows), "nnz": int(nnz), "n_walks": int(n_walks),
                        "walks_per_gpu": int(n_walks // world),
                        "emissions_per_step": em_per_step, "beta": beta, "max_steps": cfg["max_steps"],
                        "weight_cutoff": cfg["cutoff"], "seed": cfg["seed"], "sampling": "philox (device RNG)",
-                       "l2": ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read of another "
-                              "buffer to evict the dirty lines" if args.flush == "write+read" else
-                              "flushed between timed steps (256 MiB write, untimed)"),
-                       "parallelism": f"start-column shards x{world}, graph replicated"
+                       "l2": "flushed between timed steps (256 MiB write, untimed); the config-3 graph (0.5 GB of "
+                             "CSR ids) exceeds L2 anyway",
+                       "parallelism": f"start-column shards x{world} (cost-balanced), graph replicated"
                                       + (f", exchange: {args.transport}" if world > 1 else "")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "timing": "CUDA-graph replay of one full estimator pass" if graph is not None else "eager steps",
@@ -542,26 +653,25 @@ def run_device(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="mcfunm", choices=["mcfunm", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--flush", choices=["write", "write+read"], default="write")
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
-                    help="N > 1 exchange: peer-memory combine kernels (default) or NCCL all-reduce")
+                    help="N > 1 exchange: peer-memory combine kernels (default) or NCCL all-gather")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps instead of a captured CUDA graph")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale (config 4)")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N > 1: weak = every GPU keeps the config's walk budget (default); strong = the config's "
-                         "budget split over the GPUs")
+    ap.add_argument("--cpu-seconds", type=float, default=60.0, help="wall seconds of the CPU baseline's sample")
+    ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale (configs 3, 4)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N > 1: strong = the config's walk budget split over the GPUs (default: configs 3-5 fix "
+                         "walks per node); weak = every GPU keeps the config's budget")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.scale and cfg["graph"] == "rmat":
+        cfg["workload"] = cfg["workload"].replace(f"scale {cfg['scale']}", f"scale {args.scale}")
         cfg["scale"] = args.scale
-        cfg["workload"] = cfg["workload"].replace("scale 24", f"scale {args.scale}")
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_device(args, cfg)

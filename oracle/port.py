@@ -553,22 +553,56 @@ def action_columns(t: Tables, r: np.ndarray, z: np.ndarray, ni: np.ndarray, cols
     return out, em
 
 
+def _ranges(starts: np.ndarray, lens: np.ndarray) -> np.ndarray:
+    """Concatenation of the index ranges [starts[k], starts[k] + lens[k])."""
+    tot = int(lens.sum())
+    if tot == 0:
+        return np.zeros(0, dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    return np.repeat(starts - off, lens) + np.arange(tot, dtype=np.int64)
+
+
 def diag_columns(a: Csr, t: Tables, z: np.ndarray, ni: np.ndarray, cols, max_steps: int, cutoff: float,
-                 seed: int):
-    """Eq. 20 contributions {i: sum} of the given columns and their emissions."""
-    contrib, em = {}, 0
+                 seed: int, out: np.ndarray | None = None, chunk_ids: int = 1 << 22):
+    """Eq. 20 contributions of the given columns and their emissions: the
+    reference walker (batch_walks = walker.py:245-290) builds Q_c as in
+    funm_diag, then d_i += a_ic <Q_c, C_i> for i in C_c, the inner products
+    vectorised over all of C_c (gather of the C_i row ids, products, segment
+    sums; at most ``chunk_ids`` ids at a time).  Q_c is reset only where the
+    walks touched it.  Returns ({i: sum}, emissions), or (out, emissions) when
+    a dense accumulator ``out`` is given."""
+    contrib, em = ({} if out is None else out), 0
     qrow = np.zeros(a.n)
     for c in cols:
-        qrow[:] = 0.0
+        touched = []
 
         def on_step(k, s, w, ids):
             np.add.at(qrow, s, z[k + 2] * w)
+            touched.append(s)
         e, _ = batch_walks(t, int(c), int(ni[c]), max_steps, cutoff, column_stream(seed, int(c)), on_step)
         em += e
         lo, hi = a.csc_ptr[c], a.csc_ptr[c + 1]
-        for i, aic in zip(a.csc_rows[lo:hi], a.csc_vals[lo:hi]):
-            ilo, ihi = a.csc_ptr[i], a.csc_ptr[i + 1]
-            contrib[int(i)] = contrib.get(int(i), 0.0) + aic * (qrow[a.csc_rows[ilo:ihi]] @ a.csc_vals[ilo:ihi])
+        rows, aic = a.csc_rows[lo:hi], a.csc_vals[lo:hi]
+        starts, lens = a.csc_ptr[rows], a.csc_ptr[rows + 1] - a.csc_ptr[rows]
+        p = 0
+        while p < rows.size:  # groups of C_c entries with at most chunk_ids ids in total
+            q = p + max(1, int(np.searchsorted(np.cumsum(lens[p:]), chunk_ids, side="right")))
+            idx = _ranges(starts[p:q], lens[p:q])
+            prod = qrow[a.csc_rows[idx]] * a.csc_vals[idx]
+            seg = np.zeros(q - p)
+            nz = lens[p:q] > 0
+            if idx.size:
+                bounds = np.concatenate([[0], np.cumsum(lens[p:q])[:-1]])[nz]
+                seg[nz] = np.add.reduceat(prod, bounds)
+            vals = aic[p:q] * seg
+            if out is None:
+                for i, v in zip(rows[p:q], vals):
+                    contrib[int(i)] = contrib.get(int(i), 0.0) + v
+            else:
+                np.add.at(out, rows[p:q], vals)
+            p = q
+        if touched:
+            qrow[np.concatenate(touched)] = 0.0
     return contrib, em
 
 

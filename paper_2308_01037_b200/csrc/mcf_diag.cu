@@ -96,6 +96,8 @@ struct QArgs {
     long long long_work;        // LONG_WORK: split threshold of the cluster kernels (MCF_DIAG_LONG_WORK)
     long long long_work_q;      // k_diag_q's (MCF_DIAG_LONG_WORK_Q; measured best lower: one CTA per column)
     long long big_work;         // BIG_WORK (MCF_DIAG_BIG_WORK overrides: tests)
+    long long chunk_q;          // ids / support tests per shared piece of a long entry: k_diag_q (MCF_DIAG_CHUNK_Q)
+    long long chunk_c;          // ... and the cluster kernels (MCF_DIAG_CHUNK)
     long long cl_base;          // first scratch region of the cluster kernels' CTAs (= k_diag_q's grid)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
 };
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 const bool push = use_push(a, i, ihi - ilo, nsupp);
                 const long long len = push ? nsupp : ihi - ilo;
                 if (len > a.long_work_q) {
-                    const int nch = (int)((len + CHUNK - 1) / CHUNK);
+                    const int nch = (int)((len + a.chunk_q - 1) / a.chunk_q);
                     int slot = 0, base = 0;
                     if (lane == 0) {
                         slot = atomicAdd(&s_nlong, 1);
@@ -593,8 +595,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     const int i = a.csc_rows[cs + t];
                     const long long base = push ? 0 : a.csc_ptr[i];
                     const long long end = push ? nsupp : a.csc_ptr[i + 1];
-                    const long long lo = base + (long long)(k - lbase[j]) * CHUNK;
-                    const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
+                    const long long lo = base + (long long)(k - lbase[j]) * a.chunk_q;
+                    const long long hi = lo + a.chunk_q < end ? lo + a.chunk_q : end;
                     const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
                     if (lane == 0) atomicAdd(lacc + j, (unsigned long long)acc);
                 }
@@ -848,7 +850,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                     const int i = a.csc_rows[cs + t];
                     const long long len = lt < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
                     s_lt[j] = lt;
-                    s_lpre[j + 1] = s_lpre[j] + (int)((len + CHUNK - 1) / CHUNK);
+                    s_lpre[j + 1] = s_lpre[j] + (int)((len + a.chunk_c - 1) / a.chunk_c);
                     if (rank == 0) s_lacc[j] = 0;
                 }
                 if (rank == 0) s_next = 0;
@@ -867,8 +869,8 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                 const int i = a.csc_rows[cs + t];
                 const long long base = push ? 0 : a.csc_ptr[i];
                 const long long end = push ? nsupp : a.csc_ptr[i + 1];
-                const long long lo = base + (long long)(k - s_lpre[j]) * CHUNK;
-                const long long hi = lo + CHUNK < end ? lo + CHUNK : end;
+                const long long lo = base + (long long)(k - s_lpre[j]) * a.chunk_c;
+                const long long hi = lo + a.chunk_c < end ? lo + a.chunk_c : end;
                 const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
                 if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(r0_lacc + j), (unsigned long long)acc);
             }
@@ -1026,6 +1028,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.long_work = e ? atoll(e) : LONG_WORK;
         e = getenv("MCF_DIAG_LONG_WORK_Q");
         q.long_work_q = e ? atoll(e) : LONG_WORK_Q;
+        e = getenv("MCF_DIAG_CHUNK_Q");
+        q.chunk_q = e ? atoll(e) : CHUNK;
+        e = getenv("MCF_DIAG_CHUNK");
+        q.chunk_c = e ? atoll(e) : CHUNK;
+        if (q.chunk_q < 32) q.chunk_q = 32;
+        if (q.chunk_c < 32) q.chunk_c = 32;
     }
     AsyncFrees frees(s);  // every stream-ordered allocation below, on every return path
     static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
@@ -1064,7 +1072,7 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     // length on symmetric graphs; longer columns scan the overflow inline)
     q.llcap = g->info.max_degree > 64 ? g->info.max_degree : 64;
     if (q.llcap > (1ll << 24)) q.llcap = 1ll << 24;
-    q.ocap = 2 * q.llcap + 2 * (q.big_work / CHUNK) + 1024;
+    q.ocap = 2 * q.llcap + 2 * (q.big_work / q.chunk_q) + 1024;
     {
         unsigned char *lb = nullptr;
         MCF_CUDA(cudaMallocAsync(&lb, (size_t)nreg * (q.llcap * (8 + 4 + 4) + q.ocap * 4), s));
