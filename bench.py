@@ -269,16 +269,19 @@ class CpuBaseline:
         self.cores = cores or os.cpu_count() or 1
         self.setup_s = time.perf_counter() - t0
         self.pool = mp.get_context("fork").Pool(self.cores)
-        # calibration: CPU seconds per work unit on a small sample of every stratum
+        # calibration: CPU seconds per column of every stratum, from one or two
+        # columns each (one task per column); refined after every run
         rng = np.random.default_rng(12345)
-        probe = [(k, rng.choice(s, size=min(s.size, 4), replace=False)) for k, s in enumerate(self.strata)]
-        res = self.pool.map(_cpu_worker, probe)
-        work = sum(self.stratum_cost[k] / self.strata[k].size * len(c) for k, c in probe)
-        self.sec_per_work = max(1e-12, sum(x[3] for x in res) / max(1.0, work))
+        probe = [(k, np.array([c])) for k, s in enumerate(self.strata)
+                 for c in rng.choice(s, size=min(s.size, 2), replace=False)]
+        res = self.pool.map(_cpu_worker, probe, chunksize=1)
+        self.obs = np.zeros((len(self.strata), 2))  # per stratum: columns, CPU seconds
+        for k, nc, _, c in res:
+            self.obs[k] += (nc, c)
         self.runs = []
         self.run_index = 0
         log(f"[cpu] tables {self.setup_s:.1f}s, {self.walked.size} walked columns in {len(self.strata)} strata, "
-            f"{self.cores} workers")
+            f"{self.cores} workers, calibration {self.obs[:, 1].sum():.1f} CPU-s")
 
     def run(self, budget_s):
         """One timed sample of about ``budget_s`` wall seconds on all cores."""
@@ -287,14 +290,16 @@ class CpuBaseline:
         per = budget_s * self.cores / len(self.strata)  # CPU seconds per stratum
         tasks = []
         for k, s in enumerate(self.strata):
-            mean_work = self.stratum_cost[k] / s.size
-            want = int(min(s.size, max(1, round(per / (self.sec_per_work * mean_work)))))
+            sec_per_col = self.obs[k, 1] / max(1.0, self.obs[k, 0])
+            want = int(min(s.size, max(1, round(per / max(sec_per_col, 1e-6)))))
             cols = np.sort(rng.choice(s, size=want, replace=False))
             pieces = max(1, min(want, self.cores))
             tasks += [(k, c) for c in np.array_split(cols, pieces) if c.size]
         t0 = time.perf_counter()
         res = self.pool.map(_cpu_worker, tasks, chunksize=1)
         wall = time.perf_counter() - t0
+        for k, nc, _, c in res:
+            self.obs[k] += (nc, c)
         self.runs.append((res, wall))
         return res, wall
 

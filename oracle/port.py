@@ -690,3 +690,51 @@ def mc_baseline(a: Csr, tag: str, walks_per_row: int, cutoff: float = 1e-6, max_
     if rec:
         res.record = rec.finish()
     return res
+
+
+# --------------------------------------------------------------------------
+# node-subset replay at full size ("for large configs, replay a
+# node subset S using columns U_{a in S} N(a)")
+# --------------------------------------------------------------------------
+def record_subset(a: Csr, t: Tables, z: np.ndarray, ni: np.ndarray, cols, subset, max_steps: int,
+                  cutoff: float, seed: int):
+    """Walk the given columns with the reference walker (batch_walks,
+    per-column PCG64DXSM streams) over the FULL model, recording every walk's
+    entry stream, and accumulate the Eq. 20 terms of the nodes in ``subset``
+    only: d_a += a_ac <Q_c, C_a> for a in subset and C_c.  Returns
+    ([(c, walk_off_local int64[N_c + 1], entries int32)], {a: sum}, emissions)."""
+    sub = set(int(x) for x in subset)
+    recs, contrib, em = [], {}, 0
+    qrow = np.zeros(a.n)
+    for c in cols:
+        c = int(c)
+        nc = int(ni[c])
+        steps = []
+        touched = []
+
+        def on_step(k, s, w, ids):
+            np.add.at(qrow, s, z[k + 2] * w)
+            touched.append(s)
+
+        def on_draw(k, ids, e):
+            steps.append((ids.copy(), e.astype(np.int32)))
+        e_, _ = batch_walks(t, c, nc, max_steps, cutoff, column_stream(seed, c), on_step, on_draw)
+        em += e_
+        cnt = np.zeros(nc, dtype=np.int64)
+        for ids, _ in steps:
+            cnt[ids] += 1
+        off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        ent = np.empty(int(off[-1]), dtype=np.int32)
+        fill = off[:-1].copy()
+        for ids, e in steps:  # steps arrive in k order: per-walk streams stay in step order
+            ent[fill[ids]] = e
+            fill[ids] += 1
+        recs.append((c, off, ent))
+        lo, hi = a.csc_ptr[c], a.csc_ptr[c + 1]
+        for i, aic in zip(a.csc_rows[lo:hi], a.csc_vals[lo:hi]):
+            if int(i) in sub:
+                ilo, ihi = a.csc_ptr[i], a.csc_ptr[i + 1]
+                contrib[int(i)] = contrib.get(int(i), 0.0) + aic * (qrow[a.csc_rows[ilo:ihi]] @ a.csc_vals[ilo:ihi])
+        if touched:
+            qrow[np.concatenate(touched)] = 0.0
+    return recs, contrib, em

@@ -17,6 +17,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include <cooperative_groups.h>
@@ -100,11 +101,16 @@ struct QArgs {
     long long chunk_c;          // ... and the cluster kernels (MCF_DIAG_CHUNK)
     long long cl_base;          // first scratch region of the cluster kernels' CTAs (= k_diag_q's grid)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
+    int opt;                    // MCF_DIAG_OPT: OPT_PIPE | OPT_SPEC | OPT_BLOCKED
 };
 
 // prof slots: 0 pull pairs, 1 pull ids, 2 pull filter passes, 3 push pairs, 4 push tests, 5 push hits,
 // 6 emissions, 7 support, 8 columns, 9 big columns, 10 cycles Q build, 11 cycles combine, 12 pull hits
-constexpr int PROF_SLOTS = 20;  // 16..18: cluster-kernel columns, cycles, emissions
+// per table class (0 k_diag_q shared table, 1 k_diag_q global table, 2 dense,
+// 3 clusters, 4 k_diag_big): pull pairs, ids, filter passes, hits, push pairs,
+// tests, push hits, spare
+constexpr int PROF_BASE = 20, PROF_CLS = 8, PROF_NCLS = 5;
+constexpr int PROF_SLOTS = PROF_BASE + PROF_CLS * PROF_NCLS;  // 16..18: cluster-kernel columns, cycles, emissions
 
 struct BigRec {
     long long c;      // column
@@ -161,9 +167,17 @@ __device__ __forceinline__ int find_or_insert(int *keys, uint32_t mask, int key)
     }
 }
 
-__device__ __forceinline__ long long lookup(const int *keys, const long long *vals, uint32_t mask, int key) {
+__device__ __forceinline__ long long lookup(const int *keys, const long long *vals, uint32_t mask, int key,
+                                            bool spec = false) {
     if (!keys) return vals[key];  // dense table (small graphs): Q_c indexed by node id
     uint32_t s = hash_slot(key, mask);
+    if (spec) {  // the home slot's value loaded with its key: one round trip for a hit at home
+        const int k = keys[s];
+        const long long v = vals[s];
+        if (k == key) return v;
+        if (k == EMPTY_KEY) return 0;
+        s = (s + 1) & mask;
+    }
     while (true) {
         int k = keys[s];
         if (k == key) return vals[s];
@@ -180,16 +194,35 @@ __device__ __forceinline__ uint32_t filter_bit2(int key) { return ((uint32_t)key
 
 // Two bits per key (k = 2): at the ~10^4 keys of a shared-memory Q_c the false
 // positive rate drops from ~4% to ~0.2%, at 6.5e4 from 22% to 15%.
-__device__ __forceinline__ bool filter_test(const unsigned *filt, int key) {
+// Blocked variant (MCF_DIAG_OPT bit 4): three bits of ONE 32-bit word, so a
+// test is a single shared-memory load instead of two.
+__device__ __forceinline__ uint32_t filter_block_mask(int key) {
+    const uint32_t h = (uint32_t)key * 0xC2B2AE35u;
+    return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u)) | (1u << ((h >> 17) & 31u));
+}
+__device__ __forceinline__ uint32_t filter_block_word(int key) { return ((uint32_t)key * 0x85EBCA6Bu) >> 19; }
+
+__device__ __forceinline__ bool filter_test(const unsigned *filt, int key, bool blocked = false) {
+    if (blocked) {
+        const uint32_t m = filter_block_mask(key);
+        return (filt[filter_block_word(key)] & m) == m;
+    }
     const uint32_t b = filter_bit(key), b2 = filter_bit2(key);
     return ((filt[b >> 5] >> (b & 31)) & (filt[b2 >> 5] >> (b2 & 31)) & 1u) != 0;
 }
 
-__device__ __forceinline__ void filter_add(unsigned *filt, int key) {
+__device__ __forceinline__ void filter_add(unsigned *filt, int key, bool blocked = false) {
+    if (blocked) {
+        atomicOr(&filt[filter_block_word(key)], filter_block_mask(key));
+        return;
+    }
     const uint32_t b = filter_bit(key), b2 = filter_bit2(key);
     atomicOr(&filt[b >> 5], 1u << (b & 31));
     atomicOr(&filt[b2 >> 5], 1u << (b2 & 31));
 }
+
+enum { OPT_PIPE = 1, OPT_SPEC = 2, OPT_BLOCKED = 4 };
+constexpr int DIAG_OPT_DEFAULT = 0;
 
 // Uniform-value graphs: the fixed-point sum over one range of the (i, c) work,
 // warp-reduced.
@@ -207,7 +240,9 @@ struct LocalTable {
     bool global;      // table in global memory: probes batched (see uniform_partial)
     static constexpr bool can_batch = true;
     __device__ __forceinline__ bool batched() const { return global; }
-    __device__ __forceinline__ long long get(int key) const { return lookup(keys, vals, mask, key); }
+    __device__ __forceinline__ long long get(int key, bool spec = false) const {
+        return lookup(keys, vals, mask, key, spec);
+    }
     __device__ __forceinline__ int key_at(uint32_t s) const { return keys[s]; }
     __device__ __forceinline__ long long val_at(uint32_t s) const { return vals[s]; }
 };
@@ -215,7 +250,7 @@ struct LocalTable {
 template <class Table>
 __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table &tab, const int *lkeys,
                                                      const long long *lvals, const unsigned *filt, int i, bool push,
-                                                     long long lo, long long hi, int lane) {
+                                                     long long lo, long long hi, int lane, int pcls = 0) {
     long long acc = 0;
     if (push) {
         const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
@@ -245,6 +280,10 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
                 atomicAdd(a.prof + 3, 1ull);
                 atomicAdd(a.prof + 4, (unsigned long long)(hi - lo));
                 atomicAdd(a.prof + 5, (unsigned long long)hits);
+                unsigned long long *pc = a.prof + PROF_BASE + PROF_CLS * pcls;
+                atomicAdd(pc + 4, 1ull);
+                atomicAdd(pc + 5, (unsigned long long)(hi - lo));
+                atomicAdd(pc + 6, (unsigned long long)hits);
             }
         }
     } else {
@@ -252,6 +291,42 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
         // bound otherwise (one L2 round trip per 64 ids)
         constexpr int PULL_U = 8;
         int fpass = 0, phit = 0;
+        const bool blocked = (a.opt & OPT_BLOCKED) != 0, spec = (a.opt & OPT_SPEC) != 0;
+        if ((a.opt & OPT_PIPE) && (!Table::can_batch || !tab.batched())) {
+            // software-pipelined scan: block b+1's ids are loaded before block
+            // b is filtered and probed, so the L2/HBM round trip of the id
+            // stream overlaps the shared-memory work
+            int jv[PULL_U], jn[PULL_U];
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u) {
+                const long long e = lo + 32 * u + lane;
+                jv[u] = e < hi ? __ldg(a.csc_rows + e) : -1;
+            }
+            for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
+                const long long e1 = e0 + 32 * PULL_U;
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    const long long e = e1 + 32 * u + lane;
+                    jn[u] = e < hi ? __ldg(a.csc_rows + e) : -1;
+                }
+                bool pass[PULL_U];
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) pass[u] = jv[u] >= 0 && filter_test(filt, jv[u], blocked);
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    if (pass[u]) {
+                        const long long q = tab.get(jv[u], spec);
+                        acc += q;
+                        if (a.prof) {
+                            ++fpass;
+                            phit += q != 0;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) jv[u] = jn[u];
+            }
+        } else
         for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
             int jv[PULL_U];
 #pragma unroll
@@ -263,8 +338,8 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
 #pragma unroll
                 for (int u = 0; u < PULL_U; ++u) {
                     if (jv[u] < 0) continue;
-                    if (filter_test(filt, jv[u])) {
-                        const long long q = tab.get(jv[u]);
+                    if (filter_test(filt, jv[u], blocked)) {
+                        const long long q = tab.get(jv[u], spec);
                         acc += q;
                         if (a.prof) {
                             ++fpass;
@@ -286,7 +361,7 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
             for (int u = 0; u < PULL_U; ++u) {
                 sl[u] = 0;
                 if (jv[u] < 0) continue;
-                if (filter_test(filt, jv[u])) {
+                if (filter_test(filt, jv[u], blocked)) {
                     pend |= 1u << u;
                     sl[u] = hash_slot(jv[u], tab.mask);
                 }
@@ -327,6 +402,11 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
                 atomicAdd(a.prof + 1, (unsigned long long)(hi - lo));
                 atomicAdd(a.prof + 2, (unsigned long long)fpass);
                 atomicAdd(a.prof + 12, (unsigned long long)phit);
+                unsigned long long *pc = a.prof + PROF_BASE + PROF_CLS * pcls;
+                atomicAdd(pc + 0, 1ull);
+                atomicAdd(pc + 1, (unsigned long long)(hi - lo));
+                atomicAdd(pc + 2, (unsigned long long)fpass);
+                atomicAdd(pc + 3, (unsigned long long)phit);
             }
         }
     }
@@ -346,14 +426,14 @@ __device__ __forceinline__ double pair_value(const QArgs &a, const int *keys, co
     if (a.uniform) {
         const bool push = use_push(a, i, ihi - ilo, nsupp);
         const LocalTable tab{keys, vals, mask, true};  // k_diag_big: pool tables in global memory
-        const long long acc = push ? uniform_partial(a, tab, lkeys, lvals, filt, i, true, 0, nsupp, lane)
-                                   : uniform_partial(a, tab, lkeys, lvals, filt, i, false, ilo, ihi, lane);
+        const long long acc = push ? uniform_partial(a, tab, lkeys, lvals, filt, i, true, 0, nsupp, lane, 4)
+                                   : uniform_partial(a, tab, lkeys, lvals, filt, i, false, ilo, ihi, lane, 4);
         return aic * (a.value * ldexp((double)acc, -E));
     }
     double acc = 0.0;
     for (long long e = ilo + lane; e < ihi; e += 32) {
         const int j = __ldg(a.csc_rows + e);
-        if (filter_test(filt, j))
+        if (filter_test(filt, j, (a.opt & OPT_BLOCKED) != 0))
             acc = fma(__ldg(a.csc_vals + e), ldexp((double)lookup(keys, vals, mask, j), -E), acc);
     }
     return aic * warp_sum(acc);
@@ -449,7 +529,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
         for (uint32_t t = tid; t < cap; t += Q_THREADS) {
             const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
             if (key != EMPTY_KEY) {
-                filter_add(filt, key);
+                filter_add(filt, key, (a.opt & OPT_BLOCKED) != 0);
                 if (a.uniform) {
                     const int p = atomicAdd(&s_nsupp, 1);
                     if (p < a.lcap) {
@@ -543,6 +623,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
             __syncthreads();
             // (global tables here: scalar probes measured faster than batched, k_diag_big the reverse)
             const LocalTable tab{keys, vals, mask, false};
+            const int pcls = keys == nullptr ? 2 : (keys == gkeys ? 1 : 0);
             while (true) {
                 int t = 0;
                 if (lane == 0) t = atomicAdd(&s_next, 1);
@@ -572,8 +653,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                         if (fits) continue;
                     }
                 }
-                const long long acc =
-                    uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo, push ? nsupp : ihi, lane);
+                const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo,
+                                                      push ? nsupp : ihi, lane, pcls);
                 if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
             }
             __syncthreads();
@@ -597,7 +678,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                     const long long end = push ? nsupp : a.csc_ptr[i + 1];
                     const long long lo = base + (long long)(k - lbase[j]) * a.chunk_q;
                     const long long hi = lo + a.chunk_q < end ? lo + a.chunk_q : end;
-                    const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
+                    const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane, pcls);
                     if (lane == 0) atomicAdd(lacc + j, (unsigned long long)acc);
                 }
                 __syncthreads();
@@ -637,9 +718,17 @@ struct ClusterTable {
     uint32_t mask;    // K * SCAP - 1
     static constexpr bool can_batch = false;
     __device__ __forceinline__ bool batched() const { return false; }
-    __device__ __forceinline__ long long get(int key) const {
+    __device__ __forceinline__ long long get(int key, bool spec = false) const {
         cg::cluster_group cl = cg::this_cluster();
         uint32_t s = hash_slot(key, mask);
+        if (spec) {  // home slot key and value in one round trip
+            const unsigned r = s / SCAP, l = s % SCAP;
+            const int k = cl.map_shared_rank(keys, r)[l];
+            const long long v = cl.map_shared_rank(vals, r)[l];
+            if (k == key) return v;
+            if (k == EMPTY_KEY) return 0;
+            s = (s + 1) & mask;
+        }
         while (true) {
             const unsigned r = s / SCAP, l = s % SCAP;
             const int k = cl.map_shared_rank(keys, r)[l];
@@ -740,7 +829,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         for (int t = tid; t < SCAP; t += Q_THREADS) {
             const int key = skeys[t];
             if (key != EMPTY_KEY) {
-                filter_add(filt, key);
+                filter_add(filt, key, (a.opt & OPT_BLOCKED) != 0);
                 const int p = atomicAdd(r0_nsupp, 1);
                 if (p < lcap) {
                     lkeys[p] = key;
@@ -834,7 +923,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                 }
             }
             const long long acc =
-                uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo, push ? nsupp : ihi, lane);
+                uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo, push ? nsupp : ihi, lane, 3);
             if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
         }
         cl.sync();
@@ -871,7 +960,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                 const long long end = push ? nsupp : a.csc_ptr[i + 1];
                 const long long lo = base + (long long)(k - s_lpre[j]) * a.chunk_c;
                 const long long hi = lo + a.chunk_c < end ? lo + a.chunk_c : end;
-                const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane);
+                const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane, 3);
                 if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(r0_lacc + j), (unsigned long long)acc);
             }
             cl.sync();
@@ -974,14 +1063,10 @@ __global__ void k_diag_final(const long long *__restrict__ row_ptr, const int *_
 }
 
 // default emission-buffer budget (slots of 12 B): 2^30 -> 12 GiB of the 180 GB
-static long long emission_budget() {
-    static long long v = 0;
-    if (!v) {
-        const char *e = getenv("MCF_EMISSION_SLOTS");
-        v = e ? atoll(e) : (1ll << 30);
-        if (v < (1ll << 16)) v = 1ll << 16;
-    }
-    return v;
+static long long emission_budget() {  // read per call: tests switch it at run time
+    const char *e = getenv("MCF_EMISSION_SLOTS");
+    long long v = e ? atoll(e) : (1ll << 30);
+    return v < (1ll << 16) ? (1ll << 16) : v;
 }
 
 static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre, long long cb,
@@ -1028,6 +1113,8 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.long_work = e ? atoll(e) : LONG_WORK;
         e = getenv("MCF_DIAG_LONG_WORK_Q");
         q.long_work_q = e ? atoll(e) : LONG_WORK_Q;
+        e = getenv("MCF_DIAG_OPT");
+        q.opt = e ? atoi(e) : DIAG_OPT_DEFAULT;
         e = getenv("MCF_DIAG_CHUNK_Q");
         q.chunk_q = e ? atoll(e) : CHUNK;
         e = getenv("MCF_DIAG_CHUNK");
@@ -1093,7 +1180,8 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     const unsigned max_big = 32768;
     const unsigned long long pool_cap = 1ull << 27;  // 1.5 GiB of (key, value) slots
     unsigned char *pool = nullptr;
-    if (cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(long long)) + (size_t)max_big * FILTER_WORDS * 4 +
+    const char *pool_env = getenv("MCF_DIAG_POOL");  // "0": no pool (the allocation-failure path; tests)
+    if (!(pool_env && !strcmp(pool_env, "0")) && cudaMallocAsync(&pool, pool_cap * (sizeof(int) + sizeof(long long)) + (size_t)max_big * FILTER_WORDS * 4 +
                                        sizeof(BigRec) * max_big + 2 * sizeof(int) * max_big,
                         s) == cudaSuccess) {
         frees.keep(pool);
@@ -1223,6 +1311,11 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
                 "[diag-prof] cols %llu big %llu emissions %llu support %llu | pull pairs %llu ids %llu filt %llu hits %llu"
                 " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | gtable cols %llu cycles %llu emissions %llu | cluster cols %llu cycles %llu emissions %llu build %llu\n",
                 h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15], h[16], h[17], h[18], h[19]);
+        for (int k = 0; k < PROF_NCLS; ++k) {
+            const unsigned long long *c = h + PROF_BASE + PROF_CLS * k;
+            fprintf(stderr, "[diag-prof-cls] %d pull pairs %llu ids %llu filt %llu hits %llu | push pairs %llu tests %llu hits %llu\n",
+                    k, c[0], c[1], c[2], c[3], c[4], c[5], c[6]);
+        }
     }
     return MCF_OK;
 }

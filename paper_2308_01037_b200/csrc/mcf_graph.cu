@@ -469,6 +469,7 @@ static void release(mcf_graph *g) {
     if (g->went) cudaFreeAsync(g->went, 0);
     if (g->lean) cudaFreeAsync(g->lean, 0);
     if (g->lean4) cudaFreeAsync(g->lean4, 0);
+    if (g->lean_id) cudaFreeAsync(g->lean_id, 0);
     if (g->rsum_by_deg) cudaFreeAsync(g->rsum_by_deg, 0);
     if (g->hub_of) cudaFreeAsync(g->hub_of, 0);
     if (g->hub_bits) cudaFreeAsync(g->hub_bits, 0);

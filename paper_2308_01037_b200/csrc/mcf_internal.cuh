@@ -115,6 +115,12 @@ struct mcf_graph {
     // (rsum_by_deg), so a step is ONE dependent random 8-B load.  Built lazily.
     uint2 *lean = nullptr;
     uint32_t *lean4 = nullptr;       // 4-B variant for nnz < 2^25 (used instead of lean when built)
+    // diag walks (the emitted state id is needed too): lean_id[e] packs
+    // [deg : li_dbits | col[e] : li_ibits | start : li_sbits] of col[e] in 8 B,
+    // so a step is one random load instead of the lean entry plus ecol[e];
+    // deg = 2^li_dbits - 1 escapes to row_ptr (hub targets).  Built lazily.
+    unsigned long long *lean_id = nullptr;
+    int li_sbits = 0, li_ibits = 0, li_dbits = 0;
     double *rsum_by_deg = nullptr;   // max_degree + 1
     int *long_rows = nullptr;        // rows with degree > LONG_ROW (SpMV / table build bins)
     long long n_long_rows = 0;

@@ -50,6 +50,8 @@ struct WalkCommon {
     int *err;
     const uint2 *__restrict__ lean;         // v = 1 on uniform-value graphs (else null)
     const uint32_t *__restrict__ lean4;     // compact 4-B variant (nnz < 2^25), preferred when built
+    const unsigned long long *__restrict__ lean_id;  // diag: {start, id, degree} of col[e] in 8 B (or null)
+    int li_sbits, li_ibits, li_dbits;
     const long long *__restrict__ row_ptr;  // lean walks: start state of a column
     const double *__restrict__ rsum_by_deg;
     // L2 bulk prefetch of the walk tables at kernel start (bytes 0: none)
@@ -257,6 +259,19 @@ template <bool FAT, bool LEAN = false, bool WITH_ID = false>
 __device__ __forceinline__ NodeHdr fetch_next(const WalkCommon &a, long long e) {
     if (LEAN) {  // {start, degree} of the target; |a| row sum (= r for v = 1) by degree
         NodeHdr h;
+        if (WITH_ID && a.lean_id) {  // one 8-B entry: start, target id and degree together
+            const unsigned long long t = __ldg(a.lean_id + e);
+            const unsigned long long smask = (1ull << a.li_sbits) - 1, imask = (1ull << a.li_ibits) - 1;
+            const unsigned long long dmax = (1ull << a.li_dbits) - 1;
+            h.start = (int)(t & smask);
+            h.pad = (uint32_t)((t >> a.li_sbits) & imask);
+            const unsigned long long d = t >> (a.li_sbits + a.li_ibits);
+            h.deg = d < dmax ? (int)d : (int)(__ldg(a.row_ptr + h.pad + 1) - h.start);  // hub target: row_ptr
+            h.flags = HDR_UNIFORM;
+            h.rsum = __ldg(a.rsum_by_deg + h.deg);
+            h.aux = h.rsum;
+            return h;
+        }
         // the target id (diag emissions): issued together with the entry load,
         // consumed only at the end, so the two round trips overlap (measured:
         // reading it after decoding the entry stalled the diag walk a second time)
@@ -811,6 +826,8 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.colmax = nullptr;
     a.lean = nullptr;
     a.lean4 = nullptr;
+    a.lean_id = nullptr;
+    a.li_sbits = a.li_ibits = a.li_dbits = 0;
     a.rsum_by_deg = nullptr;
     a.row_ptr = (const long long *)g->row_ptr;
     a.return_only = (p->flags & MCF_FLAG_RETURN_ONLY) ? 1 : 0;
@@ -925,10 +942,48 @@ __global__ void k_rsum_by_deg(const NodeHdr *__restrict__ hdr, long long n, doub
     tab[h.deg] = h.deg ? h.rsum : 0.0;
 }
 
+// lean_id[e] = [deg : dbits | col[e] : ibits | row start : sbits] of col[e]
+__global__ void k_build_lean_id(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids, long long nnz,
+                                int sbits, int ibits, int dbits, unsigned long long *__restrict__ out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    const int c = col_ids[e];
+    const long long s0 = row_ptr[c], d = row_ptr[c + 1] - s0;
+    const unsigned long long dmax = (1ull << dbits) - 1;
+    const unsigned long long dd = (unsigned long long)d < dmax ? (unsigned long long)d : dmax;
+    out[e] = (dd << (sbits + ibits)) | ((unsigned long long)c << sbits) | (unsigned long long)s0;
+}
+
+static int bits_for(long long v) {  // bits to hold values 0..v
+    int b = 1;
+    while (b < 63 && (1ll << b) <= v) ++b;
+    return b;
+}
+
 static bool lean_eligible(const mcf_graph *g) {
     const char *env = getenv("MCF_LEAN_WALK");
     if (env && !strcmp(env, "0")) return false;
     return g->uniform_value && g->nnz < (1ll << 31) && g->info.max_degree < (1ll << 31);
+}
+
+// The diag walk's one-load table (MCF_LEAN_ID=0 disables: ecol[e] beside the lean entry)
+static int ensure_lean_id(mcf_graph *g, cudaStream_t s) {
+    if (g->lean_id) return MCF_OK;
+    const char *env = getenv("MCF_LEAN_ID");
+    if (env && !strcmp(env, "0")) return MCF_OK;
+    const int sb = bits_for(g->nnz), ib = bits_for(g->n - 1), db = 64 - sb - ib;
+    if (db < 6) return MCF_OK;  // too few degree bits: keep the two-array walk
+    unsigned long long *t = nullptr;
+    MCF_CUDA(cudaMallocAsync(&t, sizeof(unsigned long long) * g->nnz, s));
+    k_build_lean_id<<<(unsigned)((g->nnz + 255) / 256), 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids,
+                                                                       g->nnz, sb, ib, db, t);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_build_lean_id");
+    g->lean_id = t;
+    g->li_sbits = sb;
+    g->li_ibits = ib;
+    g->li_dbits = db;
+    return MCF_OK;
 }
 
 static int ensure_lean(mcf_graph *g, cudaStream_t s) {
@@ -988,8 +1043,14 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
     if (lean) {
         rc = ensure_lean(g, s);
         if (rc) return rc;
+        rc = ensure_lean_id(g, s);
+        if (rc) return rc;
         a.lean = g->lean;
         a.lean4 = g->lean4;
+        a.lean_id = g->lean_id;
+        a.li_sbits = g->li_sbits;
+        a.li_ibits = g->li_ibits;
+        a.li_dbits = g->li_dbits;
         a.rsum_by_deg = g->rsum_by_deg;
         for (int k = 0; k < 3; ++k) a.pf_bytes[k] = 0;
         switch (mode) {

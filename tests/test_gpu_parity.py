@@ -615,13 +615,18 @@ def test_lean_diag_bitwise(mc, lean_bytes, name):
         try:
             for layout in ("compact", "fat"):
                 os.environ["MCF_WALK_LAYOUT"] = layout
-                g = mc.DeviceGraph(a, gamma=0.05)
-                res = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(30 * c.n, 1e-6, 28, 7))
-                out[lean, layout] = (np.asarray(res.values), res.emissions, res.truncated)
+                # lean walks: the one-load {start, id, degree} entries (default)
+                # and the lean entry with ecol[e] alongside (MCF_LEAN_ID=0)
+                for lid in (("1", "0") if lean == "1" else ("1",)):
+                    os.environ["MCF_LEAN_ID"] = lid
+                    g = mc.DeviceGraph(a, gamma=0.05)
+                    res = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(30 * c.n, 1e-6, 28, 7))
+                    out[lean, layout, lid] = (np.asarray(res.values), res.emissions, res.truncated)
         finally:
             os.environ.pop("MCF_LEAN_WALK", None)
             os.environ.pop("MCF_WALK_LAYOUT", None)
-    ref = out["0", "compact"]
+            os.environ.pop("MCF_LEAN_ID", None)
+    ref = out["0", "compact", "1"]
     for k, v in out.items():
         assert np.array_equal(v[0], ref[0]) and v[1:] == ref[1:], k
 
