@@ -101,7 +101,9 @@ struct QArgs {
     long long chunk_c;          // ... and the cluster kernels (MCF_DIAG_CHUNK)
     long long cl_base;          // first scratch region of the cluster kernels' CTAs (= k_diag_q's grid)
     int cl_maxk;                // > 0: columns whose table needs a cluster of <= cl_maxk CTAs go to k_diag_qc
-    int opt;                    // MCF_DIAG_OPT: OPT_PIPE | OPT_SPEC | OPT_BLOCKED
+    int opt;                    // MCF_DIAG_OPT: OPT_PIPE | OPT_SPEC | OPT_BLOCKED | OPT_EXACT
+    unsigned *cbits;            // OPT_EXACT: per-cluster exact membership bitmap of Q_c's keys (n bits each)
+    long long cwords;
 };
 
 // prof slots: 0 pull pairs, 1 pull ids, 2 pull filter passes, 3 push pairs, 4 push tests, 5 push hits,
@@ -221,7 +223,7 @@ __device__ __forceinline__ void filter_add(unsigned *filt, int key, bool blocked
     atomicOr(&filt[b2 >> 5], 1u << (b2 & 31));
 }
 
-enum { OPT_PIPE = 1, OPT_SPEC = 2, OPT_BLOCKED = 4 };
+enum { OPT_SPEC = 2, OPT_BLOCKED = 4, OPT_EXACT = 8 };  // (bit 1: a pipelined scan, measured no gain, removed)
 constexpr int DIAG_OPT_DEFAULT = 0;
 
 // Uniform-value graphs: the fixed-point sum over one range of the (i, c) work,
@@ -245,6 +247,7 @@ struct LocalTable {
     }
     __device__ __forceinline__ int key_at(uint32_t s) const { return keys[s]; }
     __device__ __forceinline__ long long val_at(uint32_t s) const { return vals[s]; }
+    __device__ __forceinline__ bool maybe(int) const { return true; }
 };
 
 template <class Table>
@@ -292,41 +295,6 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
         constexpr int PULL_U = 8;
         int fpass = 0, phit = 0;
         const bool blocked = (a.opt & OPT_BLOCKED) != 0, spec = (a.opt & OPT_SPEC) != 0;
-        if ((a.opt & OPT_PIPE) && (!Table::can_batch || !tab.batched())) {
-            // software-pipelined scan: block b+1's ids are loaded before block
-            // b is filtered and probed, so the L2/HBM round trip of the id
-            // stream overlaps the shared-memory work
-            int jv[PULL_U], jn[PULL_U];
-#pragma unroll
-            for (int u = 0; u < PULL_U; ++u) {
-                const long long e = lo + 32 * u + lane;
-                jv[u] = e < hi ? __ldg(a.csc_rows + e) : -1;
-            }
-            for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
-                const long long e1 = e0 + 32 * PULL_U;
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) {
-                    const long long e = e1 + 32 * u + lane;
-                    jn[u] = e < hi ? __ldg(a.csc_rows + e) : -1;
-                }
-                bool pass[PULL_U];
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) pass[u] = jv[u] >= 0 && filter_test(filt, jv[u], blocked);
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) {
-                    if (pass[u]) {
-                        const long long q = tab.get(jv[u], spec);
-                        acc += q;
-                        if (a.prof) {
-                            ++fpass;
-                            phit += q != 0;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) jv[u] = jn[u];
-            }
-        } else
         for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
             int jv[PULL_U];
 #pragma unroll
@@ -338,7 +306,7 @@ __device__ __forceinline__ long long uniform_partial(const QArgs &a, const Table
 #pragma unroll
                 for (int u = 0; u < PULL_U; ++u) {
                     if (jv[u] < 0) continue;
-                    if (filter_test(filt, jv[u], blocked)) {
+                    if (filter_test(filt, jv[u], blocked) && tab.maybe(jv[u])) {
                         const long long q = tab.get(jv[u], spec);
                         acc += q;
                         if (a.prof) {
@@ -716,23 +684,31 @@ struct ClusterTable {
     const int *keys;  // this CTA's part (the same offset in every CTA of the cluster)
     const long long *vals;
     uint32_t mask;    // K * SCAP - 1
+    const unsigned *exact;  // OPT_EXACT: the cluster's membership bitmap (L2), or null
+    // a key the Bloom filter passed is probed remotely only if it is really in
+    // Q_c: the filter's false positives (~half the passes on wide columns)
+    // would walk the longest linear-probing chains in distributed shared memory
+    __device__ __forceinline__ bool maybe(int key) const {
+        return !exact || ((__ldcg(exact + (key >> 5)) >> (key & 31)) & 1u);
+    }
     static constexpr bool can_batch = false;
     __device__ __forceinline__ bool batched() const { return false; }
+    int *const *kb;               // kb[r] / vb[r]: CTA r's key / value array (mapped once per kernel)
+    long long *const *vb;
     __device__ __forceinline__ long long get(int key, bool spec = false) const {
-        cg::cluster_group cl = cg::this_cluster();
         uint32_t s = hash_slot(key, mask);
         if (spec) {  // home slot key and value in one round trip
             const unsigned r = s / SCAP, l = s % SCAP;
-            const int k = cl.map_shared_rank(keys, r)[l];
-            const long long v = cl.map_shared_rank(vals, r)[l];
+            const int k = kb[r][l];
+            const long long v = vb[r][l];
             if (k == key) return v;
             if (k == EMPTY_KEY) return 0;
             s = (s + 1) & mask;
         }
         while (true) {
             const unsigned r = s / SCAP, l = s % SCAP;
-            const int k = cl.map_shared_rank(keys, r)[l];
-            if (k == key) return cl.map_shared_rank(vals, r)[l];
+            const int k = kb[r][l];
+            if (k == key) return vb[r][l];
             if (k == EMPTY_KEY) return 0;
             s = (s + 1) & mask;
         }
@@ -765,11 +741,8 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + SCAP);
     __shared__ long long s_col, s_work, s_slot, s_off;
     __shared__ int s_nsupp, s_next, s_nlong;  // rank 0's are the cluster's
-    __shared__ int s_lt[MAX_LONG], s_lpre[MAX_LONG + 1];
-    __shared__ long long s_lacc[MAX_LONG];
     int *r0_nsupp = cl.map_shared_rank(&s_nsupp, 0), *r0_next = cl.map_shared_rank(&s_next, 0);
     int *r0_nlong = cl.map_shared_rank(&s_nlong, 0);
-    long long *r0_lacc = cl.map_shared_rank(s_lacc, 0);
     const int tid = threadIdx.x, lane = tid & 31;
     const long long lcap = (long long)K * a.lcap;  // the cluster's K consecutive per-CTA list regions
     // per-CTA scratch regions after k_diag_q's (the two kernels run concurrently)
@@ -778,7 +751,17 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
     long long *lvals = a.lvals + (long long)((cta - rank) / K) * lcap;
     const uint32_t mask = (uint32_t)K * SCAP - 1;
     const long long CT = (long long)K * Q_THREADS, gt = (long long)rank * Q_THREADS + tid;
-    const ClusterTable tab{skeys, svals, mask};
+    unsigned *cbits = (a.opt & OPT_EXACT) && a.cbits ? a.cbits + (long long)(blockIdx.x / K) * a.cwords : nullptr;
+    __shared__ int *s_kb[K];
+    __shared__ long long *s_vb[K];
+    if (tid < K) {
+        s_kb[tid] = cl.map_shared_rank(skeys, tid);
+        s_vb[tid] = cl.map_shared_rank(svals, tid);
+    }
+    __syncthreads();
+    const ClusterTable tab{skeys, svals, mask, cbits, s_kb, s_vb};
+    __shared__ int s_nchunk, s_next2;  // rank 0's: pieces of the column's long entries, piece counter
+    int *r0_nchunk = cl.map_shared_rank(&s_nchunk, 0), *r0_next2 = cl.map_shared_rank(&s_next2, 0);
 
     while (true) {
         for (int t = tid; t < SCAP; t += Q_THREADS) {
@@ -794,6 +777,8 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             s_next = 0;
             s_nlong = 0;
             s_work = 0;
+            s_nchunk = 0;
+            s_next2 = 0;
         }
         cl.sync();
         const long long c = s_col;
@@ -903,7 +888,21 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
                 continue;
             }
         }
-        int *llist = a.llist + (long long)(cta - rank) * a.llcap;  // the cluster's (rank 0's) long list
+        if (cbits) {  // exact membership bits of this CTA's keys (cleared after the column)
+            for (int t = tid; t < SCAP; t += Q_THREADS) {
+                const int key = skeys[t];
+                if (key != EMPTY_KEY) atomicOr(cbits + (key >> 5), 1u << (key & 31));
+            }
+            __threadfence();
+            cl.sync();
+        }
+        // the cluster's (rank 0's) lists: long entries, their first piece and
+        // piece sum, and the piece -> entry map (global scratch, read with .cg)
+        const long long reg = cta - rank;
+        int *llist = a.llist + reg * a.llcap;
+        int *lbase = a.lbase + reg * a.llcap;
+        unsigned long long *lacc = a.lacc + reg * a.llcap;
+        int *lown = a.lown + reg * a.ocap;
         while (true) {
             int t = 0;
             if (lane == 0) t = atomicAdd(r0_next, 1);
@@ -914,12 +913,26 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             const bool push = use_push(a, i, ihi - ilo, nsupp);
             const long long len = push ? nsupp : ihi - ilo;
             if (len > a.long_work) {
-                int slot = 0;
-                if (lane == 0) slot = atomicAdd(r0_nlong, 1);
+                // listed with a range of pieces; after the short entries every
+                // warp of the cluster shares all pieces of all listed entries
+                // in ONE phase (int64 piece sums: the same total as one warp)
+                const int nch = (int)((len + a.chunk_c - 1) / a.chunk_c);
+                int slot = 0, base = 0;
+                if (lane == 0) {
+                    slot = atomicAdd(r0_nlong, 1);
+                    base = slot < a.llcap ? atomicAdd(r0_nchunk, nch) : 0;
+                }
                 slot = __shfl_sync(MCF_FULL, slot, 0);
+                base = __shfl_sync(MCF_FULL, base, 0);
                 if (slot < a.llcap) {
-                    if (lane == 0) llist[slot] = push ? ~t : t;
-                    continue;
+                    const bool fits = (long long)base + nch <= a.ocap;
+                    for (long long k = base + lane; k < base + nch && k < a.ocap; k += 32) lown[k] = fits ? slot : -1;
+                    if (lane == 0) {
+                        llist[slot] = fits ? (push ? ~t : t) : INT_MAX;  // INT_MAX: scanned here
+                        lbase[slot] = base;
+                        lacc[slot] = 0ull;
+                    }
+                    if (fits) continue;
                 }
             }
             const long long acc =
@@ -929,47 +942,33 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         cl.sync();
         const int nlong_all = *r0_nlong;
         const int nlong = nlong_all < a.llcap ? nlong_all : (int)a.llcap;
-        for (int g0 = 0; g0 < nlong; g0 += MAX_LONG) {
-            const int nl = nlong - g0 < MAX_LONG ? nlong - g0 : MAX_LONG;
-            if (tid == 0) {  // every CTA builds the same local copy of the group's chunk prefix
-                s_lpre[0] = 0;
-                for (int j = 0; j < nl; ++j) {
-                    const int lt = llist[g0 + j];
-                    const int t = lt < 0 ? ~lt : lt;
-                    const int i = a.csc_rows[cs + t];
-                    const long long len = lt < 0 ? nsupp : a.csc_ptr[i + 1] - a.csc_ptr[i];
-                    s_lt[j] = lt;
-                    s_lpre[j + 1] = s_lpre[j] + (int)((len + a.chunk_c - 1) / a.chunk_c);
-                    if (rank == 0) s_lacc[j] = 0;
-                }
-                if (rank == 0) s_next = 0;
-            }
-            cl.sync();
-            const int KC = s_lpre[nl];
+        if (nlong > 0) {
+            const long long KC = *r0_nchunk < a.ocap ? *r0_nchunk : a.ocap;
             while (true) {
                 int k = 0;
-                if (lane == 0) k = atomicAdd(r0_next, 1);
+                if (lane == 0) k = atomicAdd(r0_next2, 1);
                 k = __shfl_sync(MCF_FULL, k, 0);
                 if (k >= KC) break;
-                int j = 0;
-                while (s_lpre[j + 1] <= k) ++j;
-                const bool push = s_lt[j] < 0;
-                const int t = push ? ~s_lt[j] : s_lt[j];
+                const int j = __ldcg(lown + k);
+                if (j < 0) continue;
+                const int lt = __ldcg(llist + j);
+                const bool push = lt < 0;
+                const int t = push ? ~lt : lt;
                 const int i = a.csc_rows[cs + t];
                 const long long base = push ? 0 : a.csc_ptr[i];
                 const long long end = push ? nsupp : a.csc_ptr[i + 1];
-                const long long lo = base + (long long)(k - s_lpre[j]) * a.chunk_c;
+                const long long lo = base + (long long)(k - __ldcg(lbase + j)) * a.chunk_c;
                 const long long hi = lo + a.chunk_c < end ? lo + a.chunk_c : end;
                 const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane, 3);
-                if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(r0_lacc + j), (unsigned long long)acc);
+                if (lane == 0 && acc) atomicAdd(lacc + j, (unsigned long long)acc);
             }
             cl.sync();
-            if (rank == 0)
-                for (int j = tid; j < nl; j += Q_THREADS) {
-                    const int t = s_lt[j] < 0 ? ~s_lt[j] : s_lt[j];
-                    a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)s_lacc[j], -E));
-                }
-            __syncthreads();
+            for (long long j = gt; j < nlong; j += CT) {
+                const int lt = __ldcg(llist + j);
+                if (lt == INT_MAX) continue;
+                const int t = lt < 0 ? ~lt : lt;
+                a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)(long long)__ldcg(lacc + j), -E));
+            }
         }
         if (a.prof && rank == 0 && tid == 0) {
             atomicAdd(a.prof + 16, 1ull);
@@ -978,6 +977,13 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             atomicAdd(a.prof + 19, (unsigned long long)(t_built - t_start));
         }
         cl.sync();  // every remote access of this column is done before the tables and counters are reset
+        if (cbits) {  // clear the bitmap words of this CTA's keys before the next column sets its own
+            for (int t = tid; t < SCAP; t += Q_THREADS) {
+                const int key = skeys[t];
+                if (key != EMPTY_KEY) __stcg(cbits + (key >> 5), 0u);
+            }
+            __threadfence();
+        }
     }
 }
 
@@ -1237,6 +1243,17 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
             q.cl_maxk = 2 << k;
         }
     }
+    q.cbits = nullptr;
+    q.cwords = (g->n + 31) / 32;
+    if (q.cl_maxk && (q.opt & OPT_EXACT)) {  // one n-bit bitmap per concurrently resident cluster
+        long long ncl = 0;
+        for (int k = 0; k < 3; ++k) ncl = ncl > cl_grid[k] / (2 << k) ? ncl : cl_grid[k] / (2 << k);
+        if (ncl > 0) {
+            MCF_CUDA(cudaMallocAsync(&q.cbits, sizeof(unsigned) * q.cwords * ncl, s));
+            frees.keep(q.cbits);
+            MCF_CUDA(cudaMemsetAsync(q.cbits, 0, sizeof(unsigned) * q.cwords * ncl, s));
+        }
+    }
     int *cl_cols = nullptr;
     unsigned *cl_cnt = nullptr;
     const long long ncol = ce - cb;
@@ -1251,6 +1268,16 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     }
     int rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
+    // MCF_DIAG_PROF: a timeline of the combine's kernels (ms from the start)
+    std::vector<std::pair<const char *, cudaEvent_t>> tl;
+    auto mark = [&](const char *what, cudaStream_t st) {
+        if (!q.prof) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tl.emplace_back(what, e);
+    };
+    mark("start", s);
     if (q.cl_maxk) {
         // The cluster kernels go first and k_diag_q runs beside them on the side
         // stream: clusters of 4/8 CTAs only fit 128-132 of the 148 SMs, and
@@ -1272,10 +1299,12 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
             else k_diag_qc<8><<<cl_grid[2], Q_THREADS, smem, s>>>(q, lst, hc[k], nxt);
             mcf::note_launch();
             MCF_LAUNCHED("k_diag_qc");
+            mark(k == 0 ? "qc2 end" : (k == 1 ? "qc4 end" : "qc8 end"), s);
         }
         k_diag_q<<<grid, Q_THREADS, smem, g->side>>>(q);
         mcf::note_launch();
         MCF_LAUNCHED("k_diag_q");
+        mark("k_diag_q end (side)", g->side);
         MCF_CUDA(cudaEventRecord(g->ev_join, g->side));
         MCF_CUDA(cudaStreamWaitEvent(s, g->ev_join, 0));
     } else {
@@ -1296,9 +1325,11 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
             mcf::note_launch();
             rc = exclusive_scan_i64(cnt, cnt + nrec, nrec, s);
             if (rc) return rc;
+            mark("big start", s);
             k_diag_big<<<sm_count() * 8, 256, 0, s>>>(q, cnt + nrec, nrec);
             mcf::note_launch();
             MCF_LAUNCHED("k_diag_big");
+            mark("big end", s);
         }
     }
     rc = timed_end(timed, g->ev_q, s);
@@ -1311,6 +1342,14 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
                 "[diag-prof] cols %llu big %llu emissions %llu support %llu | pull pairs %llu ids %llu filt %llu hits %llu"
                 " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | gtable cols %llu cycles %llu emissions %llu | cluster cols %llu cycles %llu emissions %llu build %llu\n",
                 h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15], h[16], h[17], h[18], h[19]);
+        std::string line = "[diag-timeline]";
+        for (auto &x : tl) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl[0].second, x.second);
+            line += std::string(" ") + x.first + "=" + std::to_string(ms);
+        }
+        for (auto &x : tl) cudaEventDestroy(x.second);
+        fprintf(stderr, "%s\n", line.c_str());
         for (int k = 0; k < PROF_NCLS; ++k) {
             const unsigned long long *c = h + PROF_BASE + PROF_CLS * k;
             fprintf(stderr, "[diag-prof-cls] %d pull pairs %llu ids %llu filt %llu hits %llu | push pairs %llu tests %llu hits %llu\n",

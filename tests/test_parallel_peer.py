@@ -80,3 +80,71 @@ def test_peer_exchange_matches_single_process(name):
     assert em2 == [ref.emissions, refd.emissions]
     assert np.array_equal(y2, np.asarray(ref.values))
     assert np.array_equal(d2, np.asarray(refd.values))
+
+
+def _worker_big(rank, world, port_no, name, n_walks, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2308_01037_b200 as mc
+        from paper_2308_01037_b200 import parallel
+        c = golden_io.load(name)
+        g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
+        cfg = mc.WalkConfig(n_walks, 1e-6, 28, 21)
+        y, st = parallel.sharded_action(g, mc.EXPONENTIAL, None, cfg)        # NCCL-style all-gather path (gloo here)
+        d, sd = parallel.sharded_diag(g, mc.EXPONENTIAL, mc.WalkConfig(50 * c.n, 1e-6, 28, 22))
+        emitted = torch.tensor([int(st[1]), int(sd[1])])
+        dist.all_reduce(emitted)
+        if rank == 0:
+            out.put((y.cpu().numpy(), d.cpu().numpy(), emitted.tolist()))
+        g.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_action_beyond_2_31_walks_single_and_two_ranks():
+    """N_s > 2^31 walks (the reference has no cap, walker.py:55, :263): one
+    process runs them in column batches inside mcf_funm_action; two ranks
+    each get a cost-balanced shard with its own walk capacity.  q / y equal
+    the explicit per-half launches, and 1 vs 2 ranks, bit for bit; the diag
+    all-gather path (per-entry partials of each rank's CSC range) as well."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2308_01037_b200 as mc
+    from paper_2308_01037_b200.device import WalkParams
+    name = "ba400"
+    c = golden_io.load(name)
+    n_walks = (1 << 31) + 12_345_678
+    g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
+    cfg = mc.WalkConfig(n_walks, 1e-6, 28, 21)
+    ref = mc.rand_funm_action(g, mc.EXPONENTIAL, None, cfg)   # one call: batched inside the library
+    assert ref.walks == n_walks
+    # the same walks as two explicit column halves (each < 2^31 walks)
+    z = mc.EXPONENTIAL.prefix(30)
+    ni, pre = g.allocate(n_walks)
+    half = int(torch.searchsorted(pre, pre[-1] // 2).item())
+    q = torch.zeros(g.n, dtype=torch.float64, device="cuda")
+    r = g.spmv(torch.ones(g.n, dtype=torch.float64, device="cuda"))
+    st = g.new_stats()
+    params = WalkParams(cfg, z)
+    for cols in ((0, half), (half, g.n)):
+        cap = int(pre[cols[1]] - pre[cols[0]])
+        assert cap < (1 << 31)
+        g.walk_action(params.derive(capacity=cap), pre, r, q, cols=cols, stats=st)
+    assert np.array_equal(q.cpu().numpy(), ref.aux["q"].cpu().numpy())
+    refd = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(50 * c.n, 1e-6, 28, 22))
+    ctx = tmp.get_context("spawn")
+    out = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_worker_big, args=(k, 2, port_no, name, n_walks, out)) for k in range(2)]
+    for p in procs:
+        p.start()
+    y2, d2, em2 = out.get(timeout=900)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert em2 == [ref.emissions, refd.emissions]
+    assert np.array_equal(y2, np.asarray(ref.values))
+    assert np.array_equal(d2, np.asarray(refd.values))

@@ -62,7 +62,7 @@ def main():
             ref = d.clone()
         else:
             same = bool(torch.equal(ref, d))
-        best = min(times)
+        best = min(times) if times else (0.0, 0.0, 0.0)
         print(json.dumps({"setting": s or "default", "ms": best[0], "walk_ms": best[1], "combine_ms": best[2],
                           "bitwise_same": same}), flush=True)
 
