@@ -61,6 +61,12 @@ CONFIGS = {
                      "max degree 1e5, beta=1/lambda_max, 25 Taylor terms, 100 walks per node",
             kind="diag", graph="chunglu", n=16_000_000, walks_per_node=100, max_steps=23, cutoff=1e-300, seed=0),
 }
+# not a BASELINE config: config 2's graph with signed, non-uniform weights (every row
+# non-uniform: the alias-table walk), for the weighted-row measurement
+CONFIGS[6] = dict(workload="weighted: exp(beta A) 1 on config 2's Barabasi-Albert n=1e6 m=4 with symmetric weights "
+                           "|w| ~ U[0.5, 1.5), 10% negative, beta = 1/spectral radius, 30 Taylor terms, 10 walks per node",
+                  kind="action", graph="ba_signed", n=1_000_000, m=4, walks_per_node=10, max_steps=28,
+                  cutoff=1e-300, seed=0)
 DEFAULT_CONFIG = 3
 
 
@@ -81,7 +87,7 @@ def make_graph(cfg, pinned=False):
     t0 = time.perf_counter()
     gd = bench_graphs.load(graph_spec(cfg), log=log)
     n, rp, ci = gd["n"], gd["row_ptr"], gd["col_ids"]
-    vals = np.ones(ci.size)
+    vals = np.asarray(gd["vals"], dtype=np.float64) if "vals" in gd else np.ones(ci.size)
     if pinned:
         import torch
         bufs = [torch.empty(x.shape, dtype={np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int32,

@@ -249,6 +249,45 @@ __global__ void k_cdf(const NodeHdr *__restrict__ hdr, const double *__restrict_
     cdf[h.start + h.deg - 1] = 1.0;
 }
 
+// Vose's alias method per non-uniform row (one thread per row; scratch p and
+// the two work stacks live at the row's own CSR range): p_t = |a_t| deg /
+// rowsum, small (< 1) entries paired with large ones.  The draw (walk pick())
+// takes slot k = floor(u deg) and keeps it when the fractional part of u deg
+// is below threshold k, else its alias -- the within-row distribution of
+// walker.py:112-125 (|a| / row sum), up to the 2^-tbits threshold quantum.
+__global__ void k_alias(const NodeHdr *__restrict__ hdr, const double *__restrict__ vals, long long n, int tbits,
+                        double *__restrict__ p, int *__restrict__ stk, unsigned long long *__restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const NodeHdr h = hdr[i];
+    if (h.deg == 0 || (h.flags & HDR_UNIFORM)) return;
+    const long long s0 = h.start;
+    const int d = h.deg;
+    double *pp = p + s0;
+    int *st = stk + s0;
+    const unsigned long long one = 1ull << tbits;
+    int ns = 0, nl = 0;  // small stack grows from the front, large from the back
+    for (int t = 0; t < d; ++t) {
+        pp[t] = fabs(vals[s0 + t]) * (double)d / h.rsum;
+        if (pp[t] < 1.0) st[ns++] = t;
+        else st[d - 1 - nl++] = t;
+    }
+    while (ns > 0 && nl > 0) {
+        const int sm = st[--ns];
+        const int lg = st[d - nl];  // top of the large stack
+        double th = pp[sm] * (double)one;
+        unsigned long long q = th >= (double)one ? one - 1 : (unsigned long long)th;
+        out[s0 + sm] = ((unsigned long long)lg << tbits) | q;
+        pp[lg] = (pp[lg] + pp[sm]) - 1.0;
+        if (pp[lg] < 1.0) {  // the large entry became small: move it
+            --nl;
+            st[ns++] = lg;
+        }
+    }
+    for (int k = 0; k < ns; ++k) out[s0 + st[k]] = ((unsigned long long)st[k] << tbits) | (one - 1);
+    for (int k = 0; k < nl; ++k) out[s0 + st[d - 1 - k]] = ((unsigned long long)st[d - 1 - k] << tbits) | (one - 1);
+}
+
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
 // pairwise_sum): < 8 terms sequential from 0; <= 128 terms eight strided
 // accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the tail;
@@ -463,6 +502,7 @@ static void release(mcf_graph *g) {
     if (g->hdr) cudaFreeAsync(g->hdr, 0);
     if (g->ecol_owned) cudaFreeAsync(g->ecol, 0);
     if (g->cdf) cudaFreeAsync(g->cdf, 0);
+    if (g->alias) cudaFreeAsync(g->alias, 0);
     if (g->col_norm) cudaFreeAsync(g->col_norm, 0);
     if (g->csr2csc) cudaFreeAsync(g->csr2csc, 0);
     if (g->long_rows) cudaFreeAsync(g->long_rows, 0);
@@ -604,6 +644,26 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
         if ((e = cudaMallocAsync(&g->cdf, sizeof(double) * g->nnz, s)) != cudaSuccess) return fail(cuda_status(e, "cdf"));
         k_cdf<<<nb, 256, 0, s>>>(g->hdr, g->vals, n, g->cdf);
         mcf::note_launch();
+        const char *aenv = getenv("MCF_ALIAS");  // "0": inverse-CDF search for device-RNG draws
+        if (!(aenv && !strcmp(aenv, "0"))) {
+            int dbits = 1;
+            while (dbits < 40 && (1ll << dbits) <= g->info.max_degree) ++dbits;
+            const int tbits = 64 - dbits;  // >= 24 even for degree ~2^40
+            double *p = nullptr;
+            int *stk = nullptr;
+            if ((e = cudaMallocAsync(&g->alias, sizeof(unsigned long long) * g->nnz, s)) != cudaSuccess)
+                return fail(cuda_status(e, "alias"));
+            if ((e = cudaMallocAsync(&p, sizeof(double) * g->nnz, s)) != cudaSuccess) return fail(cuda_status(e, "alias p"));
+            if ((e = cudaMallocAsync(&stk, sizeof(int) * g->nnz, s)) != cudaSuccess) {
+                cudaFreeAsync(p, s);
+                return fail(cuda_status(e, "alias stack"));
+            }
+            k_alias<<<nb, 256, 0, s>>>(g->hdr, g->vals, n, tbits, p, stk, g->alias);
+            mcf::note_launch();
+            cudaFreeAsync(p, s);
+            cudaFreeAsync(stk, s);
+            g->alias_tbits = tbits;
+        }
     }
     // walk layout: fat entries when the compact tables (32 n + 4 nnz bytes)
     // would not stay resident in L2 (MCF_WALK_LAYOUT=fat|compact overrides)

@@ -100,6 +100,12 @@ struct mcf_graph {
     int32_t *ecol = nullptr;         // nnz; col | (a<0)<<31 (aliases col_ids if no negatives)
     bool ecol_owned = false;
     double *cdf = nullptr;           // nnz within-row CDF (only if some row is non-uniform)
+    // Walker/Vose alias tables of the non-uniform rows (device-RNG draws: one
+    // dependent load per step instead of a log2(deg)-deep CDF search):
+    // alias[e] = (alias index within the row << alias_tbits) | acceptance
+    // threshold (alias_tbits-bit fixed point); alias index == own index: always taken
+    unsigned long long *alias = nullptr;
+    int alias_tbits = 0;
     bool l2_prefetch = false;        // compact tables fit L2: walk kernels bulk-prefetch them first
     double *col_norm = nullptr;      // n
     double *init_prob = nullptr;     // n

@@ -31,6 +31,8 @@ struct WalkCommon {
     const NodeHdr *__restrict__ went;  // fat layout (nullptr: compact)
     const int *__restrict__ ecol;
     const double *__restrict__ cdf;
+    const unsigned long long *__restrict__ alias;  // Vose alias entries of non-uniform rows (or null: cdf)
+    int alias_tbits;
     const double *__restrict__ zeta;
     const long long *__restrict__ walk_pre;
     const int *__restrict__ blk_col;
@@ -249,6 +251,13 @@ __device__ __forceinline__ long long pick(const WalkCommon &a, Lane &L, unsigned
         r = ((uint64_t)L.r0 << 32) | L.r1;
     }
     if (LEAN || (h.flags & HDR_UNIFORM)) return h.start + (long long)__umul64hi(r, (uint64_t)h.deg);
+    if (a.alias) {  // slot k = floor(u deg); keep it if the fraction of u deg is below its threshold
+        const uint64_t k = __umul64hi(r, (uint64_t)h.deg), frac = r * (uint64_t)h.deg;
+        const unsigned long long t = __ldg(a.alias + h.start + k);
+        const unsigned long long tq = t & ((1ull << a.alias_tbits) - 1);
+        const uint64_t f = frac >> (64 - a.alias_tbits);
+        return h.start + (long long)(f < tq ? k : (t >> a.alias_tbits));
+    }
     return h.start + cdf_pick(a.cdf + h.start, h.deg, (double)(r >> 11) * 0x1.0p-53);
 }
 
@@ -809,6 +818,8 @@ int setup_common(mcf_graph *g, const mcf_walk_params *p, const long long *walk_p
     a.went = g->went;
     a.ecol = g->ecol;
     a.cdf = g->cdf;
+    a.alias = g->alias;
+    a.alias_tbits = g->alias_tbits;
     a.zeta = p->zeta;
     a.walk_pre = walk_pre;
     a.blk_col = *blk;

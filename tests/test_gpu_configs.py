@@ -3,10 +3,8 @@
 * config 1 (ER n=1e4 LCC, diag): every node's estimate against the exact
   diagonal of exp(beta A) (fp64 eigh on the GPU), with the per-node standard
   error of rand_funm_diag(stderr=True);
-* config 2 (BA n=1e6, action): 64 replicate estimates against the exact
-  MASKED target y* = v + r + A (mask . q_exact) (with N_s = 640,000
-  most columns get 0 or 1 walk, so the estimator is unbiased for y*, not for
-  exp(beta A) 1), replicate standard errors;
+* config 2 (BA n=1e6, action): the reference's entry streams for every
+  walked column replayed at full size (1e-10);
 * config 3 (R-MAT 2^22, diag): the multi-batch emission path and the
   big-column fallback give the same d bit for bit as the default batching.
 
@@ -74,45 +72,89 @@ def test_config1_diag_vs_exact_eigh():
     assert np.max(rel) < 1e-3  # ~1e-4 single run
 
 
-def _masked_target(g, z, max_steps, ni):
-    """y* = z0 v + z1 r + A (mask . q_exact), q_exact = sum_{k<max_steps}
-    zeta_{k+2} A^k r, r = A 1; mask = columns with N_c > 0."""
-    ones = torch.ones(g.n, dtype=torch.float64, device=g.device)
-    r = g.spmv(ones)
-    q = torch.zeros_like(r)
-    x = r.clone()
-    for k in range(max_steps):
-        q += z[k + 2] * x
-        x = g.spmv(x)
-    q = torch.where(ni > 0, q, torch.zeros_like(q))
-    return g.spmv(q, alpha=z[0], v=ones, beta=z[1], r=r)
+_WREC = {}
 
 
-def test_config2_action_vs_masked_exact():
-    """Config 2: total communicability on BA(1e6, 4), 640,000 walks; 64
-    replicate seeds; z from the replicate spread (t with 63 dof)."""
+def _weighted_worker(cols):
+    from oracle import port
+    s = _WREC
+    recs, _, em = port.record_subset(s["A"], s["t"], s["z"], s["ni"], cols, [], s["max_steps"], s["cutoff"],
+                                     s["seed"])
+    q, _ = port.action_columns(s["t"], s["r"], s["z"], s["ni"], cols, s["max_steps"], s["cutoff"], s["seed"])
+    return recs, q, em
+
+
+def _record_action(A, t, ni, z, r, max_steps, cutoff, seed):
+    """Entry streams of every walked column by the reference walker (oracle
+    port, forked pool over column chunks) and the reference's q; returns the
+    replay Record, y = z0 + z1 r + A q (v = 1) and the emission count."""
+    import multiprocessing as mp
+
+    from oracle import port
+    _WREC.update(A=A, t=t, z=z, ni=ni, r=r, max_steps=max_steps, cutoff=cutoff, seed=seed)
+    cols = np.flatnonzero(ni)
+    procs = os.cpu_count() or 1
+    with mp.get_context("fork").Pool(procs) as pool:
+        parts = pool.map(_weighted_worker, [c for c in np.array_split(cols, procs * 8) if c.size])
+    n = A.n
+    q = np.zeros(n)
+    recs = []
+    em = 0
+    for rr, qq, e in parts:
+        recs += rr
+        em += e
+        for c, v in qq.items():
+            q[c] = v
+    y_ref = z[0] + z[1] * r + A.scipy_csr() @ q
+    walk_pre = np.concatenate([[0], np.cumsum(ni)])
+    walk_off = np.zeros(int(walk_pre[-1]) + 1, dtype=np.int64)
+    ents, base = [], 0
+    for c, off, ent in sorted(recs, key=lambda x: x[0]):
+        g0 = walk_pre[c]
+        walk_off[g0 + 1:g0 + off.size] = base + off[1:]
+        ents.append(ent)
+        base += ent.size
+    walk_off = np.maximum.accumulate(walk_off)
+    return port.Record(walk_pre, walk_off, np.concatenate(ents)), y_ref, em
+
+
+def test_config2_full_replay():
+    """Config 2 at FULL size (BA n = 1e6, m = 4, 640,000 walks, 30 Taylor
+    terms): the reference walker's entry streams for every walked column
+    (PCG64DXSM per column, global searchsorted) replayed on the device give the
+    reference's exp(beta A) 1 to 1e-10 (north-star replay mode), with the same
+    emission count; the device budgets equal the reference allocation.
+
+    (The device-RNG z-test of SURVEY 4 is not applied here: with N_i in
+    {0, 1, 2} the per-node estimate at beta lambda_max = 1 is heavy-tailed --
+    walks through hubs multiply their weight by beta deg per step -- so the
+    replicate mean sits below the masked target with an underestimated spread.
+    The reference algorithm itself shows it: 64 replicates of the oracle port
+    on BA(2e4) give z mean -0.26, max |z| 14.9 (DESIGN 5).  Config 1 carries
+    the statistical check.)"""
     _need_gpu()
     import paper_2308_01037_b200 as mc
+    from oracle import port
     cfg = bench.CONFIGS[2]
-    g, beta, n_walks = _device_graph(cfg)
-    zeta = mc.EXPONENTIAL.prefix(cfg["max_steps"] + 2)
-    R = 64
-    ys = torch.empty((R, g.n), dtype=torch.float64, device="cuda")
-    for s in range(R):
-        res = mc.rand_funm_action(g, mc.EXPONENTIAL, None, mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"],
-                                                                         100 + s), as_tensor=True)
-        ys[s] = res.values
-    ni = res.aux["ni"]
-    target = _masked_target(g, zeta, cfg["max_steps"], ni)
-    mean = ys.mean(0)
-    se = ys.std(0) / math.sqrt(R)
-    target, mean, se = target.cpu().numpy(), mean.cpu().numpy(), se.cpu().numpy()
-    det = se == 0  # nodes whose estimate does not depend on the walks
-    assert np.allclose(mean[det], target[det], rtol=1e-12, atol=0)
-    z = (mean[~det] - target[~det]) / se[~det]
-    _z_acceptance(z, dof=R - 1, what="config2 action")
-    # the unmasked bias of the design (reported, not asserted): exact f(A) 1
-    print("config2: columns with walks", int((ni > 0).sum()), "of", g.n)
+    a, beta, n_walks = bench.make_graph(cfg)
+    n = a.n
+    rp = np.asarray(a.csr.indptr, dtype=np.int64)
+    ci = np.asarray(a.csr.indices, dtype=np.int64)
+    A = port.Csr(n, rp, ci, np.full(ci.size, beta), rp, ci, np.full(ci.size, beta))
+    t = port.transition_tables(A)
+    ni = port.allocate(t, n_walks)
+    z = port.zeta_prefix("exponential", cfg["max_steps"] + 2)
+    r = A.scipy_csr() @ np.ones(n)
+    rec, y_ref, em = _record_action(A, t, ni, z, r, cfg["max_steps"], cfg["cutoff"], cfg["seed"])
+    g = mc.DeviceGraph(a, gamma=beta)
+    dni, _ = g.allocate(n_walks)
+    assert np.array_equal(dni.cpu().numpy(), ni)
+    res = mc.rand_funm_action(g, mc.EXPONENTIAL, np.ones(n), mc.WalkConfig(n_walks, cfg["cutoff"],
+                                                                           cfg["max_steps"], cfg["seed"]), replay=rec)
+    rel = np.max(np.abs(res.values - y_ref) / np.abs(y_ref))
+    print(f"config2 full replay: walks {n_walks} emissions {em} max rel err {rel:.3e}")
+    assert res.emissions == em
+    assert rel < 1e-10
 
 
 def test_config3_multibatch_and_pool_fallback_bitwise(monkeypatch):
@@ -234,3 +276,43 @@ def test_config3_node_subset_replay():
     print(f"config3 subset replay: |S|={S.size} columns={cols.size} walks={walk_pre[-1]} emissions={em} "
           f"max rel err {rel.max():.3e}")
     assert rel.max() < 1e-10
+
+
+def test_weighted_signed_replay_1e5():
+    """Weighted, signed rows at 1e5 nodes (the inverse-CDF
+    draw and the copysign(row sum, a) weight update, walker.py:112-125):
+    the reference walker's entry streams on the weighted Barabasi-Albert graph
+    (n = 1e5, |w| ~ U[0.5, 1.5), 10% negative) replayed on the device give
+    the reference's f(A) 1 to 1e-10; the device-RNG estimate (alias-table
+    draws) agrees with the exact series by the SURVEY 4 rule (per-walk SEs)."""
+    _need_gpu()
+    import paper_2308_01037_b200 as mc
+    from oracle import port
+    from paper_2308_01037_b200.sparsemat import SparseMatrix
+    from tools import bench_graphs
+    gd = bench_graphs.load({"graph": "ba_signed", "n": 100_000, "m": 4, "seed": 3})
+    n, rp, ci, w = gd["n"], gd["row_ptr"], gd["col_ids"], gd["vals"]
+    gamma = 1.0 / gd["lambda_max"]
+    a = SparseMatrix.from_csr_arrays(n, rp, ci, w, symmetric_hint=True)
+    A = port.Csr(n, rp, ci.astype(np.int64), w * gamma, rp, ci.astype(np.int64), w * gamma)
+    t = port.transition_tables(A)
+    max_steps, cutoff, seed, n_walks = 28, 1e-300, 5, 4 * n
+    ni = port.allocate(t, n_walks)
+    z = port.zeta_prefix("exponential", max_steps + 2)
+    r = A.scipy_csr() @ np.ones(n)
+    rec, y_ref, em = _record_action(A, t, ni, z, r, max_steps, cutoff, seed)
+    g = mc.DeviceGraph(a, gamma=gamma)
+    assert g.info["n_uniform_rows"] < n // 2  # weighted: the non-uniform (alias / CDF) paths
+    cfg = mc.WalkConfig(n_walks, cutoff, max_steps, seed)
+    res = mc.rand_funm_action(g, mc.EXPONENTIAL, np.ones(n), cfg, replay=rec)
+    rel = np.max(np.abs(res.values - y_ref) / np.maximum(np.abs(y_ref), 1e-300))
+    print(f"weighted replay n={n}: emissions {em} max rel err {rel:.3e}")
+    assert res.emissions == em
+    assert rel < 1e-10
+    # device RNG (alias draws) against the exact 30-term series, per-walk SE
+    est = mc.rand_funm_action(g, mc.EXPONENTIAL, np.ones(n), mc.WalkConfig(400 * n, cutoff, max_steps, 9),
+                              stderr=True)
+    exact = port.taylor_action(A, "exponential", np.ones(n), max_steps + 1)
+    ok = est.stderr > 0
+    zsc = (est.values[ok] - exact[ok]) / est.stderr[ok]
+    _z_acceptance(zsc, what="weighted device RNG")
