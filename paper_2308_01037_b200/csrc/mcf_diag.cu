@@ -114,6 +114,16 @@ struct QArgs {
 constexpr int PROF_BASE = 20, PROF_CLS = 8, PROF_NCLS = 5;
 constexpr int PROF_SLOTS = PROF_BASE + PROF_CLS * PROF_NCLS;  // 16..18: cluster-kernel columns, cycles, emissions
 
+__device__ __forceinline__ int ld_relaxed_i32(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_i32(int *p, int v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_volatile_i32(const int *p) { return *(const volatile int *)p; }
+
 struct BigRec {
     long long c;      // column
     long long off;    // table offset in the pool
@@ -763,8 +773,9 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
     }
     __syncthreads();
     const ClusterTable tab{skeys, svals, mask, cbits, (a.opt & OPT_CBATCH) != 0, s_kb, s_vb};
-    __shared__ int s_nchunk, s_next2;  // rank 0's: pieces of the column's long entries, piece counter
+    __shared__ int s_nchunk, s_next2, s_done;  // rank 0's: pieces reserved, piece counter, entries done
     int *r0_nchunk = cl.map_shared_rank(&s_nchunk, 0), *r0_next2 = cl.map_shared_rank(&s_next2, 0);
+    int *r0_done = cl.map_shared_rank(&s_done, 0);
 
     while (true) {
         for (int t = tid; t < SCAP; t += Q_THREADS) {
@@ -782,6 +793,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             s_work = 0;
             s_nchunk = 0;
             s_next2 = 0;
+            s_done = 0;
         }
         cl.sync();
         const long long c = s_col;
@@ -906,72 +918,105 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         int *lbase = a.lbase + reg * a.llcap;
         unsigned long long *lacc = a.lacc + reg * a.llcap;
         int *lown = a.lown + reg * a.ocap;
+        // One phase for the whole (i, c) work: warps take entries; a long entry
+        // is listed with a range of pieces (piece -> entry map lown, written
+        // before the piece becomes visible); a warp with no entry left takes
+        // pieces, waiting for a piece it drew to be published, and leaves once
+        // every entry is done and its piece index is past the final count.
+        // No barrier between the short entries and the pieces, so warps never
+        // idle while one finishes a long entry.  (int64 piece sums: the same
+        // total as one warp's scan.)  lown is -1 until written (reset by its
+        // consumer), -3 for a piece whose entry did not fit the map.
+        bool entries_left = true;
         while (true) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(r0_next, 1);
-            t = __shfl_sync(MCF_FULL, t, 0);
-            if (t >= cn) break;
-            const int i = a.csc_rows[cs + t];
-            const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
-            const bool push = use_push(a, i, ihi - ilo, nsupp);
-            const long long len = push ? nsupp : ihi - ilo;
-            if (len > a.long_work) {
-                // listed with a range of pieces; after the short entries every
-                // warp of the cluster shares all pieces of all listed entries
-                // in ONE phase (int64 piece sums: the same total as one warp)
-                const int nch = (int)((len + a.chunk_c - 1) / a.chunk_c);
-                int slot = 0, base = 0;
-                if (lane == 0) {
-                    slot = atomicAdd(r0_nlong, 1);
-                    base = slot < a.llcap ? atomicAdd(r0_nchunk, nch) : 0;
-                }
-                slot = __shfl_sync(MCF_FULL, slot, 0);
-                base = __shfl_sync(MCF_FULL, base, 0);
-                if (slot < a.llcap) {
-                    const bool fits = (long long)base + nch <= a.ocap;
-                    for (long long k = base + lane; k < base + nch && k < a.ocap; k += 32) lown[k] = fits ? slot : -1;
-                    if (lane == 0) {
-                        llist[slot] = fits ? (push ? ~t : t) : INT_MAX;  // INT_MAX: scanned here
-                        lbase[slot] = base;
-                        lacc[slot] = 0ull;
+            if (entries_left) {
+                int t = 0;
+                if (lane == 0) t = atomicAdd(r0_next, 1);
+                t = __shfl_sync(MCF_FULL, t, 0);
+                if (t < cn) {
+                    const int i = a.csc_rows[cs + t];
+                    const long long ilo = a.csc_ptr[i], ihi = a.csc_ptr[i + 1];
+                    const bool push = use_push(a, i, ihi - ilo, nsupp);
+                    const long long len = push ? nsupp : ihi - ilo;
+                    bool listed = false;
+                    if (len > a.long_work) {
+                        const int nch = (int)((len + a.chunk_c - 1) / a.chunk_c);
+                        int slot = 0, base = 0;
+                        if (lane == 0) {
+                            slot = atomicAdd(r0_nlong, 1);
+                            base = slot < a.llcap ? atomicAdd(r0_nchunk, nch) : 0;
+                        }
+                        slot = __shfl_sync(MCF_FULL, slot, 0);
+                        base = __shfl_sync(MCF_FULL, base, 0);
+                        if (slot < a.llcap) {
+                            const bool fits = (long long)base + nch <= a.ocap;
+                            if (lane == 0) {
+                                llist[slot] = fits ? (push ? ~t : t) : INT_MAX;  // INT_MAX: scanned here
+                                lbase[slot] = base;
+                                lacc[slot] = 0ull;
+                            }
+                            __syncwarp();
+                            __threadfence();  // the entry's record before its pieces are published
+                            for (long long k = base + lane; k < base + nch && k < a.ocap; k += 32)
+                                st_relaxed_i32(lown + k, fits ? slot : -3);
+                            listed = fits;
+                        }
                     }
-                    if (fits) continue;
+                    if (!listed) {
+                        const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo,
+                                                              push ? nsupp : ihi, lane, 3);
+                        if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
+                    }
+                    __syncwarp();
+                    if (lane == 0) atomicAdd(r0_done, 1);
+                    continue;
                 }
+                entries_left = false;
             }
-            const long long acc =
-                uniform_partial(a, tab, lkeys, lvals, filt, i, push, push ? 0 : ilo, push ? nsupp : ihi, lane, 3);
-            if (lane == 0) a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)acc, -E));
+            int k = 0;
+            if (lane == 0) k = atomicAdd(r0_next2, 1);
+            k = __shfl_sync(MCF_FULL, k, 0);
+            if (k >= a.ocap) break;
+            int j = -1;
+            bool stop = false;
+            if (lane == 0) {
+                unsigned ns = 32;
+                while (true) {
+                    j = ld_relaxed_i32(lown + k);
+                    if (j != -1) break;
+                    if (ld_volatile_i32(r0_done) == cn && k >= ld_volatile_i32(r0_nchunk)) {
+                        stop = true;
+                        break;
+                    }
+                    __nanosleep(ns);
+                    if (ns < 256) ns <<= 1;
+                }
+                if (!stop) st_relaxed_i32(lown + k, -1);  // consumed: the map is clean for the next column
+            }
+            stop = __shfl_sync(MCF_FULL, stop, 0);
+            j = __shfl_sync(MCF_FULL, j, 0);
+            if (stop) break;
+            if (j < 0) continue;
+            __threadfence();  // acquire side of the publication: the entry record is visible
+            const int lt = __ldcg(llist + j);
+            const bool push = lt < 0;
+            const int t = push ? ~lt : lt;
+            const int i = a.csc_rows[cs + t];
+            const long long base = push ? 0 : a.csc_ptr[i];
+            const long long end = push ? nsupp : a.csc_ptr[i + 1];
+            const long long lo = base + (long long)(k - __ldcg(lbase + j)) * a.chunk_c;
+            const long long hi = lo + a.chunk_c < end ? lo + a.chunk_c : end;
+            const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane, 3);
+            if (lane == 0 && acc) atomicAdd(lacc + j, (unsigned long long)acc);
         }
         cl.sync();
         const int nlong_all = *r0_nlong;
         const int nlong = nlong_all < a.llcap ? nlong_all : (int)a.llcap;
-        if (nlong > 0) {
-            const long long KC = *r0_nchunk < a.ocap ? *r0_nchunk : a.ocap;
-            while (true) {
-                int k = 0;
-                if (lane == 0) k = atomicAdd(r0_next2, 1);
-                k = __shfl_sync(MCF_FULL, k, 0);
-                if (k >= KC) break;
-                const int j = __ldcg(lown + k);
-                if (j < 0) continue;
-                const int lt = __ldcg(llist + j);
-                const bool push = lt < 0;
-                const int t = push ? ~lt : lt;
-                const int i = a.csc_rows[cs + t];
-                const long long base = push ? 0 : a.csc_ptr[i];
-                const long long end = push ? nsupp : a.csc_ptr[i + 1];
-                const long long lo = base + (long long)(k - __ldcg(lbase + j)) * a.chunk_c;
-                const long long hi = lo + a.chunk_c < end ? lo + a.chunk_c : end;
-                const long long acc = uniform_partial(a, tab, lkeys, lvals, filt, i, push, lo, hi, lane, 3);
-                if (lane == 0 && acc) atomicAdd(lacc + j, (unsigned long long)acc);
-            }
-            cl.sync();
-            for (long long j = gt; j < nlong; j += CT) {
-                const int lt = __ldcg(llist + j);
-                if (lt == INT_MAX) continue;
-                const int t = lt < 0 ? ~lt : lt;
-                a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)(long long)__ldcg(lacc + j), -E));
-            }
+        for (long long j = gt; j < nlong; j += CT) {
+            const int lt = __ldcg(llist + j);
+            if (lt == INT_MAX) continue;
+            const int t = lt < 0 ? ~lt : lt;
+            a.pcol[cs + t] = a.csc_vals[cs + t] * (a.value * ldexp((double)(long long)__ldcg(lacc + j), -E));
         }
         if (a.prof && rank == 0 && tid == 0) {
             atomicAdd(a.prof + 16, 1ull);
@@ -1177,6 +1222,9 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
         q.llist = reinterpret_cast<int *>(q.lacc + (size_t)nreg * q.llcap);
         q.lbase = q.llist + (size_t)nreg * q.llcap;
         q.lown = q.lbase + (size_t)nreg * q.llcap;
+        // the cluster kernels' piece maps (regions after k_diag_q's) start unwritten (-1)
+        if (nreg > grid)
+            MCF_CUDA(cudaMemsetAsync(q.lown + (size_t)grid * q.ocap, 0xff, sizeof(int) * (size_t)(nreg - grid) * q.ocap, s));
     }
     unsigned long long *counter = nullptr;
     MCF_CUDA(cudaMallocAsync(&counter, sizeof(unsigned long long) * 4, s));

