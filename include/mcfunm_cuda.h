@@ -140,7 +140,10 @@ MCF_API int mcf_allocate_walks(mcf_graph *g, int64_t n_walks, int64_t *ni, int64
 /* y = alpha * v + beta * r + A x over rows [row_begin, row_end) ([dev] n; v, r
  * may be NULL).  With alpha = beta = 0 this is r = A v; with
  * (zeta_0, zeta_1, q) it is the Alg. 3 combine y = z0 v + z1 r + A q
- * (PAPER.md:362). */
+ * (PAPER.md:362).  x = NULL means x = 1 with alpha = beta = 0: y = A 1 as
+ * row sums in CSR order, bit-identical to the reference's A @ ones (what
+ * mcf_funm_action uses for v = 1; the general x path sums long rows
+ * warp-parallel). */
 MCF_API int mcf_spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r,
              const double *x, double *y, int64_t row_begin, int64_t row_end, void *stream);
 

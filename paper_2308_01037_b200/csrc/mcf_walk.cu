@@ -736,11 +736,34 @@ __global__ void __launch_bounds__(256, 4) k_spmv(const long long *__restrict__ r
     }
 }
 
+// y_i = (A 1)_i for rows [rb, re): the row sums in CSR order, bit-identical
+// to the reference's A @ ones (scipy's sequential CSR matvec, walker.py /
+// PAPER.md:345 with v = 1): |a| sums from the headers, signed rows re-summed
+__global__ void k_row_sums(const NodeHdr *__restrict__ hdr, const double *__restrict__ vals, long long rb,
+                           long long re, double *__restrict__ y) {
+    const long long i = rb + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= re) return;
+    const NodeHdr h = load_hdr(hdr + i);
+    double s = h.rsum;
+    if (h.flags & HDR_HAS_NEG) {
+        s = 0.0;
+        for (int t = 0; t < h.deg; ++t) s = __dadd_rn(s, vals[h.start + t]);
+    }
+    y[i] = h.deg ? s : 0.0;
+}
+
 int spmv(mcf_graph *g, double alpha, const double *v, double beta, const double *r, const double *x, double *y,
          long long rb, long long re, cudaStream_t s, NodeHdr *aux = nullptr, RowSumR rt = RowSumR{nullptr, nullptr}) {
-    MCF_ARG(g && x && y, "mcf_spmv: null argument");
+    MCF_ARG(g && y, "mcf_spmv: null argument");
     MCF_ARG(0 <= rb && rb <= re && re <= g->n, "mcf_spmv: bad row range");
     if (re == rb) return MCF_OK;
+    if (!x) {  // x = 1: the row sums (alpha = beta = 0 only)
+        MCF_ARG(alpha == 0.0 && beta == 0.0 && !aux, "mcf_spmv: x = NULL (row sums) takes alpha = beta = 0");
+        k_row_sums<<<(unsigned)((re - rb + 255) / 256), 256, 0, s>>>(g->hdr, g->vals, rb, re, y);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_row_sums");
+        return MCF_OK;
+    }
     const long long *rp = (const long long *)g->row_ptr;
     long long lb = g->n_long_rows > 0 ? (g->n_long_rows + SPMV_WARPS - 1) / SPMV_WARPS : 0;
     if (lb > 2 * sm_count()) lb = 2 * sm_count();

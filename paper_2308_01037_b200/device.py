@@ -255,6 +255,8 @@ class DeviceGraph:
 
     # ------------------------------------------------------------------ kernels
     def spmv(self, x, alpha=0.0, v=None, beta=0.0, r=None, out=None, rows=None):
+        """y = alpha v + beta r + A x; x None: y = A 1 as CSR-order row sums
+        (bit-identical to the reference's A @ ones)."""
         out = self._f64() if out is None else out
         rb, re = (0, self.n) if rows is None else rows
         N.check(N.lib().mcf_spmv(self.handle, float(alpha), _ptr(v), float(beta), _ptr(r), _ptr(x), _ptr(out),

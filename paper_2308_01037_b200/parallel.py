@@ -184,7 +184,8 @@ def sharded_action_peer(g: DeviceGraph, coeffs, v, config, *, params=None, group
     coeffs = as_stream(coeffs)
     z = coeffs.prefix(cfg.max_steps + 2)
     params = params or WalkParams(cfg, z, g.device)
-    if v is None:
+    ones = v is None
+    if ones:
         v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     own = peers is None
     if own:
@@ -193,7 +194,7 @@ def sharded_action_peer(g: DeviceGraph, coeffs, v, config, *, params=None, group
     shards, walks = _shards(peers, g, pre, cfg.n_walks, size, "action", cfg.max_steps)
     bounds = [shards[0][0]] + [b for _, b in shards]
     st = g.new_stats()
-    r = g.spmv(v)
+    r = g.spmv(None if ones else v)  # v = 1: CSR-order row sums, as the one-GPU mcf_funm_action
     g.walk_action(params.derive(capacity=walks[rank]), pre, r, _Raw(peers.ptrs[rank][0]), cols=shards[rank],
                   stats=st)
     torch.cuda.synchronize()
@@ -278,14 +279,15 @@ def sharded_action(g: DeviceGraph, coeffs, v, config, *, params=None, budgets=No
         r, y = torch.empty_like(q), torch.empty_like(q)
         st = torch.empty(N.MCF_STATS_LEN, dtype=torch.int64, device=g.device)
         return g.funm_action(params, cfg.n_walks, v, z[0], z[1], r, q, y, stats=st, want_ni=False)[0], st
-    if v is None:
+    ones = v is None
+    if ones:
         v = torch.ones(g.n, dtype=torch.float64, device=g.device)
     ni, pre = budgets if budgets is not None else g.allocate(cfg.n_walks)
     st = g.new_stats()
     shards = column_shards(pre, size)
     walks = shard_walks(pre, shards)
     rows = row_shards(g.n, size)
-    r = g.spmv(v)
+    r = g.spmv(None if ones else v)  # v = 1: CSR-order row sums, as the one-GPU mcf_funm_action
     q = torch.zeros(g.n, dtype=torch.float64, device=g.device)
     g.walk_action(params.derive(capacity=walks[rank]), pre, r, q, cols=shards[rank], stats=st)
     gather_ranges(q, [shards[0][0]] + [b for _, b in shards], group)

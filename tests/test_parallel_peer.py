@@ -74,8 +74,7 @@ def test_peer_exchange_matches_single_process(name):
         p.join(timeout=60)
         assert p.exitcode == 0
     g = mc.DeviceGraph(_as_matrix(c.sa, c.symmetric), gamma=0.05)
-    ones = torch.ones(c.n, dtype=torch.float64, device="cuda")
-    ref = mc.rand_funm_action(g, mc.EXPONENTIAL, ones, mc.WalkConfig(n_walks, 1e-6, 28, 11))
+    ref = mc.rand_funm_action(g, mc.EXPONENTIAL, None, mc.WalkConfig(n_walks, 1e-6, 28, 11))  # v = 1 as the shards
     refd = mc.rand_funm_diag(g, mc.EXPONENTIAL, mc.WalkConfig(n_walks, 1e-6, 28, 12))
     assert em2 == [ref.emissions, refd.emissions]
     assert np.array_equal(y2, np.asarray(ref.values))
