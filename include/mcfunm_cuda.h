@@ -225,6 +225,16 @@ MCF_API int mcf_replay_diag(mcf_graph *g, const mcf_walk_params *p, const int64_
 MCF_API int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, int64_t col_begin,
                             int64_t col_end, double *Q, int64_t ldq, int64_t *stats, void *stream);
 
+/* The full estimate F = zeta_0 I + zeta_1 A + A Q A (Alg. 2 / Eq. 19,
+ * SPEC.md:347-356) into the dense row-major F ([dev] n x ldf), Q in blocks of
+ * `block` walked columns ("row blocks", default 1024): per block
+ * the dense Q rows (as mcf_walk_qdense, transposed), R^T = A^T Q_b^T and
+ * F += A[:, block] R, both products over the sparse A (CSC / CSR), fixed
+ * summation orders.  walk_pre from mcf_allocate_walks.  n <= 16384 (dense
+ * output), else MCF_ERR_RESOURCE; synchronises `stream`. */
+MCF_API int mcf_funm_full(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, double zeta0,
+                          double zeta1, double *F, int64_t ldf, int64_t block, int64_t *stats, void *stream);
+
 /* d_i = zeta_0 + zeta_1 a_ii + sum_{c} pcol[(i,c)] for rows [row_begin, row_end)
  * (Eq. 20 final sum), fixed summation order. */
 MCF_API int mcf_diag_combine(mcf_graph *g, double zeta0, double zeta1, const double *pcol, double *d,

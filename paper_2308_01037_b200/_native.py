@@ -70,6 +70,7 @@ SIGNATURES = {
     "mcf_diag_combine_peer": (C.c_int, [P, C.c_double, C.c_double, P, P, C.c_int, P, C.c_int, I64, I64, P]),
     "mcf_walk_qdense": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, I64, P, P]),
     "mcf_column_costs": (C.c_int, [P, P, I64, C.c_int, P, P]),
+    "mcf_funm_full": (C.c_int, [P, C.POINTER(McfWalkParams), P, C.c_double, C.c_double, P, I64, I64, P, P]),
     "mcf_diag_variance": (C.c_int, [P, P, C.c_int, P, P, I64, I64, P]),
 }
 

@@ -1560,7 +1560,7 @@ __global__ void __launch_bounds__(512) k_qdense(const long long *__restrict__ wa
                                                 long long wb, const long long *__restrict__ eoff,
                                                 const int *__restrict__ est, const double *__restrict__ ewt,
                                                 const unsigned long long *__restrict__ colmax, long long n,
-                                                double *__restrict__ Q, long long ldq) {
+                                                double *__restrict__ Q, long long ldq, int trans) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     long long *row = reinterpret_cast<long long *>(smem_raw);
     for (long long c = cb + blockIdx.x; c < ce; c += gridDim.x) {
@@ -1579,17 +1579,21 @@ __global__ void __launch_bounds__(512) k_qdense(const long long *__restrict__ wa
                           (unsigned long long)__double2ll_rn(ldexp(ewt[s0 + i], E)));
         }
         __syncthreads();
-        double *out = Q + (c - cb) * ldq;
-        for (long long j = threadIdx.x; j < n; j += blockDim.x) out[j] = ldexp((double)row[j], -E);
+        if (trans) {  // Q^T: column (c - cb) of an n x (ce - cb) row-major block
+            for (long long j = threadIdx.x; j < n; j += blockDim.x) Q[j * ldq + (c - cb)] = ldexp((double)row[j], -E);
+        } else {
+            double *out = Q + (c - cb) * ldq;
+            for (long long j = threadIdx.x; j < n; j += blockDim.x) out[j] = ldexp((double)row[j], -E);
+        }
         __syncthreads();
     }
 }
 
 static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
-                  double *Q, long long ldq, long long *stats, cudaStream_t s) {
+                  double *Q, long long ldq, long long *stats, cudaStream_t s, bool trans = false) {
     int rc = check_params(g, p, walk_pre, cb, ce);
     if (rc) return rc;
-    MCF_ARG(Q && stats && ldq >= g->n, "mcf_walk_qdense: null Q/stats or ldq < n");
+    MCF_ARG(Q && stats && ldq >= (trans ? ce - cb : g->n), "mcf_walk_qdense: null Q/stats or ldq too small");
     if (g->n > QDENSE_MAX_N) {
         set_error("dense Q rows need n <= 16384 (use rand_funm_diag / rand_funm_action for larger graphs)");
         return MCF_ERR_RESOURCE;
@@ -1597,7 +1601,7 @@ static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     long long wb = 0, we = 0;
     rc = read_walk_range(walk_pre, cb, ce, &wb, &we, s);
     if (rc) return rc;
-    MCF_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * ldq * (ce - cb), s));
+    MCF_CUDA(cudaMemsetAsync(Q, 0, sizeof(double) * ldq * (trans ? g->n : ce - cb), s));
     if (we == wb) return MCF_OK;
     const long long nw = we - wb;
     MCF_ARG(nw < WALKS_PER_LAUNCH, "mcf_walk_qdense: walks per call must be below 2^31 (split the column range)");
@@ -1635,7 +1639,7 @@ static int qdense(mcf_graph *g, const mcf_walk_params *p, const long long *walk_
     MCF_CUDA(cudaFuncSetAttribute(k_qdense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     long long nc = ce - cb;
     int grid = (int)(nc < 4 * sm_count() ? nc : 4 * sm_count());
-    k_qdense<<<grid, 512, smem, s>>>(walk_pre, cb, ce, wb, eoff, est, ewt, colmax, g->n, Q, ldq);
+    k_qdense<<<grid, 512, smem, s>>>(walk_pre, cb, ce, wb, eoff, est, ewt, colmax, g->n, Q, ldq, trans ? 1 : 0);
     mcf::note_launch();
     MCF_LAUNCHED("k_qdense");
     return MCF_OK;
@@ -1678,6 +1682,148 @@ __global__ void k_diag_variance(const long long *__restrict__ row_ptr, const int
 #pragma unroll
     for (int o = 2; o > 0; o >>= 1) s += __shfl_xor_sync(MCF_FULL, s, o, 4);
     if (i < re && sub == 0) var[i] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Full estimate F = zeta_0 I + zeta_1 A + A Q A (Alg. 2 / Eq. 19,
+// SPEC.md:347-356) with the sparse A: per block of b walked columns,
+//   Q_b^T (n x b)      dense Q rows of the block, written transposed (k_qdense)
+//   R^T = A^T Q_b^T     SpMM over the CSC of A: a warp per output row, lanes
+//                       over the block's columns, entries in CSC order
+//   R   = (R^T)^T       tiled shared-memory transpose
+//   F  += A[:, block] R SpMM: a warp per row i of F, the row's entries in
+//                       [cb, ce) in CSR order, lanes over F's columns
+// Every sum has a fixed order: deterministic.  Dense output, n <= 16384.
+// ---------------------------------------------------------------------------
+__global__ void k_dense_init(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                             const double *__restrict__ vals, long long n, double z0, double z1,
+                             double *__restrict__ F, long long ldf) {
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double *row = F + i * ldf;
+    for (long long j = lane; j < n; j += 32) row[j] = j == i ? z0 : 0.0;
+    __syncwarp();
+    for (long long e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) {
+        const int c = col_ids[e];
+        row[c] = (c == i ? z0 : 0.0) + z1 * vals[e];
+    }
+}
+
+// Y[k, r] = sum over CSC column k of a_jk X[j, r]  (Y = A^T X, X: n x b, Y: n x b)
+__global__ void k_spmm_at(const long long *__restrict__ csc_ptr, const int *__restrict__ csc_rows,
+                          const double *__restrict__ csc_vals, long long n, const double *__restrict__ X, long long b,
+                          double *__restrict__ Y) {
+    const long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (k >= n) return;
+    for (long long r0 = 0; r0 < b; r0 += 32 * 4) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (long long e = csc_ptr[k]; e < csc_ptr[k + 1]; ++e) {
+            const long long j = csc_rows[e];
+            const double a = csc_vals[e];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long r = r0 + u * 32 + lane;
+                if (r < b) acc[u] = fma(a, X[j * b + r], acc[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long r = r0 + u * 32 + lane;
+            if (r < b) Y[k * b + r] = acc[u];
+        }
+    }
+}
+
+// out (cols x rows) = in (rows x cols)^T, 32 x 32 shared-memory tiles
+__global__ void k_transpose(const double *__restrict__ in, long long rows, long long cols, double *__restrict__ out) {
+    __shared__ double tile[32][33];
+    const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const long long r = r0 + dy, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[dy][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const long long c = c0 + dy, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) out[c * rows + r] = tile[threadIdx.x][dy];
+    }
+}
+
+// F[i, :] += sum over the entries (i, c) of row i with c in [cb, ce) of a_ic R[c - cb, :]
+__global__ void k_spmm_rows_blk(const long long *__restrict__ row_ptr, const int *__restrict__ col_ids,
+                                const double *__restrict__ vals, long long n, long long cb, long long ce,
+                                const double *__restrict__ R, double *__restrict__ F, long long ldf) {
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    long long lo = row_ptr[i], hi = row_ptr[i + 1];
+    {  // first entry with column >= cb (columns sorted within the row)
+        long long a = lo, z = hi;
+        while (a < z) {
+            const long long m = (a + z) >> 1;
+            if (col_ids[m] < cb) a = m + 1;
+            else z = m;
+        }
+        lo = a;
+    }
+    if (lo >= hi || col_ids[lo] >= ce) return;
+    double *row = F + i * ldf;
+    for (long long k0 = 0; k0 < n; k0 += 32 * 4) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (long long e = lo; e < hi && col_ids[e] < ce; ++e) {
+            const double a = vals[e];
+            const double *rr = R + (long long)(col_ids[e] - cb) * n;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long k = k0 + u * 32 + lane;
+                if (k < n) acc[u] = fma(a, rr[k], acc[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long k = k0 + u * 32 + lane;
+            if (k < n) row[k] += acc[u];
+        }
+    }
+}
+
+static int funm_full(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, double z0, double z1,
+                     double *F, long long ldf, long long block, long long *stats, cudaStream_t s) {
+    MCF_ARG(g && p && walk_pre && F && stats, "mcf_funm_full: null argument");
+    MCF_ARG(ldf >= g->n, "mcf_funm_full: ldf < n");
+    if (g->n > QDENSE_MAX_N) {
+        set_error("the dense estimate needs n <= 16384 (use rand_funm_diag / rand_funm_action for larger graphs)");
+        return MCF_ERR_RESOURCE;
+    }
+    const long long n = g->n;
+    if (block < 1 || block > n) block = n < 1024 ? n : 1024;
+    AsyncFrees frees(s);
+    double *qt = nullptr, *rt = nullptr, *r = nullptr;
+    MCF_CUDA(cudaMallocAsync(&qt, sizeof(double) * n * block, s));
+    frees.keep(qt);
+    MCF_CUDA(cudaMallocAsync(&rt, sizeof(double) * n * block, s));
+    frees.keep(rt);
+    MCF_CUDA(cudaMallocAsync(&r, sizeof(double) * n * block, s));
+    frees.keep(r);
+    const unsigned wgrid = (unsigned)((n * 32 + 255) / 256);
+    k_dense_init<<<wgrid, 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->vals, n, z0, z1, F, ldf);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_dense_init");
+    for (long long cb = 0; cb < n; cb += block) {
+        const long long ce = cb + block < n ? cb + block : n, b = ce - cb;
+        int rc = qdense(g, p, walk_pre, cb, ce, qt, b, stats, s, true);  // Q_b^T, n x b
+        if (rc) return rc;
+        k_spmm_at<<<wgrid, 256, 0, s>>>((const long long *)g->csc_ptr, g->csc_rows, g->csc_vals, n, qt, b, rt);
+        mcf::note_launch();
+        k_transpose<<<dim3((unsigned)((b + 31) / 32), (unsigned)((n + 31) / 32)), dim3(32, 8), 0, s>>>(rt, n, b, r);
+        mcf::note_launch();
+        k_spmm_rows_blk<<<wgrid, 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->vals, n, cb, ce, r, F, ldf);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_spmm_rows_blk");
+    }
+    return MCF_OK;
 }
 
 static int diag_variance(mcf_graph *g, const double *pcol_groups, int groups, const long long *walk_pre, double *var,
@@ -1754,6 +1900,12 @@ int mcf_walk_qdense(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_
                     int64_t col_end, double *Q, int64_t ldq, int64_t *stats, void *stream) {
     return mcf::qdense(g, p, (const long long *)walk_pre, col_begin, col_end, Q, ldq, (long long *)stats,
                        (cudaStream_t)stream);
+}
+
+int mcf_funm_full(mcf_graph *g, const mcf_walk_params *p, const int64_t *walk_pre, double zeta0, double zeta1,
+                  double *F, int64_t ldf, int64_t block, int64_t *stats, void *stream) {
+    return mcf::funm_full(g, p, (const long long *)walk_pre, zeta0, zeta1, F, ldf, block, (long long *)stats,
+                          (cudaStream_t)stream);
 }
 
 int mcf_diag_variance(mcf_graph *g, const double *pcol_groups, int groups, const int64_t *walk_pre, double *var,

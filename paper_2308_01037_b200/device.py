@@ -317,6 +317,13 @@ class DeviceGraph:
                                         int(Q.stride(0)), _ptr(stats), self.stream), "mcf_walk_qdense")
         return Q
 
+    def funm_full(self, params: WalkParams, walk_pre, z0, z1, F, block: int = 1024, stats=None):
+        """F = z0 I + z1 A + A Q A (dense row-major F, n x n) with the sparse A
+        products in the library (mcf_funm_full)."""
+        N.check(N.lib().mcf_funm_full(self.handle, C.byref(params.c), _ptr(walk_pre), float(z0), float(z1), _ptr(F),
+                                      int(F.stride(0)), int(block), _ptr(stats), self.stream), "mcf_funm_full")
+        return F
+
     def diag_combine_peer(self, z0, z1, pcol_parts, col_bounds, d_outs, rows=None):
         """d over a row range with pcol[(i, c)] read from the part owning
         column c and every d_i stored to every buffer in d_outs (raw device

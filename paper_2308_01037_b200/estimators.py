@@ -263,15 +263,18 @@ def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None 
     device walk engine: ``config.n_walks`` walks from EVERY row (Alg. 1's per-row
     N_s; total n N_s), W0 = 1/N_s, each step adds zeta_k W_k (from k = 0).
     mode "diag": f_ii (only emissions back at i); "action": y_i = sum zeta_k
-    W_k v[l_k]; "entry": the action of row i only.  ("full" f(A) is not
-    supported: n^2 output.)"""
+    W_k v[l_k]; "entry": the action of row i only; "full": the whole n x n
+    estimate F[i, j] = sum over the walks from i of zeta_k W_k [l_k = j]
+    (dense rows from the walk emissions, mcf_walk_qdense; n <= 16384)."""
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
-    if mode not in ("diag", "action", "entry"):
-        raise ArgumentError(f"mc_baseline mode must be diag, action or entry (got '{mode}')")
+    if mode not in ("diag", "action", "entry", "full"):
+        raise ArgumentError(f"mc_baseline mode must be diag, action, entry or full (got '{mode}')")
     n, nnz = _n_nnz(a)
     z = coeffs.prefix(cfg.max_steps + 1)
     zs = np.concatenate([[0.0, 0.0], z])  # the kernel reads zeta[k + 2]: shift Alg. 1's zeta_k by two
+    if mode == "full":
+        return _mc_full(a, coeffs, cfg, z, zs, n, nnz, device)
     if mode in ("action", "entry"):
         if v is None:
             raise ArgumentError("action/entry mode needs v")
@@ -321,13 +324,38 @@ def mc_baseline(a, coeffs, config, mode: str = "diag", *, v=None, i: int | None 
     return res
 
 
+def _mc_full(a, coeffs, cfg, z, zs, n, nnz, device, block: int = 1024) -> FunmResult:
+    """Alg. 1 full matrix (SPEC.md:389-397 mode "full"): N_s walks from every
+    row, W0 = 1/N_s, F[i, l_k] += zeta_k W_k -- the dense Q rows of the walk
+    emissions with the coefficient table shifted by two (k_qdense, fixed-point
+    accumulation: deterministic)."""
+    from .errors import ResourceError
+    from .walker import WalkConfig
+    if n > 16384:
+        raise ResourceError(f"the dense MC estimate needs n <= 16384 (got n={n})")
+    if nnz == 0:
+        return FunmResult(z[0] * np.eye(n), "mc-full", config=_cfg_echo(cfg, coeffs, "philox"))
+    g = _graph(a, device)
+    ni, pre = g.budgets(np.full(n, cfg.n_walks, dtype=np.int64))
+    params = WalkParams(WalkConfig(max(1, cfg.n_walks * n), cfg.weight_cutoff, cfg.max_steps, cfg.seed), zs, g.device)
+    F = torch.empty((n, n), dtype=torch.float64, device=g.device)
+    st = g.new_stats()
+    per = max(1, min(block, (1 << 30) // max(1, cfg.n_walks)))  # < 2^31 walks per call
+    for cb in range(0, n, per):
+        ce = min(n, cb + per)
+        g.walk_qdense(params.derive(capacity=cfg.n_walks * (ce - cb)), pre, F[cb:ce], (cb, ce), stats=st)
+    res = FunmResult(to_host(F), "mc-full", config=_cfg_echo(cfg, coeffs, "philox"))
+    _stats(res, st)
+    return res
+
+
 def rand_funm(a, coeffs, config, *, block: int = 1024, device=None, as_tensor: bool = False) -> FunmResult:
     """Full matrix estimate F ~ f(A) = zeta_0 I + zeta_1 A + A Q A (PAPER.md
     Alg. 2 / Eq. 19), Q assembled in row blocks of ``block``
-    columns so one block of Q is live at a time.  The walks and Q rows run in
-    libmcfunm_cuda; the two products per block are dense fp64 GEMMs (cuBLAS).
-    Dense output: n <= 16384 (ResourceError otherwise, advising the diag or
-    action estimators)."""
+    columns so one block of Q is live at a time.  The walks, the Q rows and the
+    two products per block (Q_b A and A[:, block] R, over the SPARSE A) run in
+    libmcfunm_cuda (mcf_funm_full).  Dense output: n <= 16384 (ResourceError
+    otherwise, advising the diag or action estimators)."""
     from .errors import ResourceError
     cfg = check_config(config)
     coeffs = as_stream(coeffs)
@@ -340,17 +368,10 @@ def rand_funm(a, coeffs, config, *, block: int = 1024, device=None, as_tensor: b
     g = _graph(a, device)
     params = WalkParams(cfg, z, g.device)
     ni, pre = g.allocate(cfg.n_walks)
-    A = torch.zeros((n, n), dtype=torch.float64, device=g.device)
-    rows = torch.repeat_interleave(torch.arange(n, device=g.device), g.row_ptr.diff())
-    A[rows, g.col_ids.to(torch.int64)] = g.vals
-    F = z[0] * torch.eye(n, dtype=torch.float64, device=g.device) + z[1] * A
+    F = torch.empty((n, n), dtype=torch.float64, device=g.device)
     st = g.new_stats()
-    Qb = torch.empty((min(block, n), n), dtype=torch.float64, device=g.device)
-    for cb in range(0, n, block):
-        ce = min(n, cb + block)
-        q = Qb[: ce - cb]
-        g.walk_qdense(params, pre, q, (cb, ce), stats=st)
-        F += A[:, cb:ce] @ (q @ A)  # C_c Q_c A summed over the block's columns (Eq. 19)
+    # blocks of walked columns: Q_b A and A[:, block] (Q_b A) over the sparse A (Eq. 19)
+    g.funm_full(params.derive(capacity=0), pre, z[0], z[1], F, block=block, stats=st)
     res = FunmResult(F if as_tensor else to_host(F), "full", config=_cfg_echo(cfg, coeffs, "philox"))
     _stats(res, st)
     res.aux = {"ni": ni, "walk_pre": pre}

@@ -504,6 +504,51 @@ def test_rand_funm_full_consistency_and_closed_form(mc):
     assert np.array_equal(z, np.eye(3))
 
 
+def test_rand_funm_sparse_products_match_dense(mc):
+    """rand_funm's sparse-A block products (mcf_funm_full) equal the dense
+    formula z0 I + z1 A + A (Q A) built from the same Q rows (mcf_walk_qdense)
+    to rounding, on a weighted non-symmetric 300-node matrix."""
+    import torch
+    from paper_2308_01037_b200.device import WalkParams
+    rng = np.random.default_rng(5)
+    n = 300
+    m = sparse.random(n, n, density=0.03, random_state=7, format="csr") * 0.3
+    m.setdiag(0)
+    m.eliminate_zeros()
+    m.sort_indices()
+    a = mc.SparseMatrix(sparse.csr_array(m), sparse.csc_array(m.tocsc()))
+    cfg = mc.WalkConfig(60 * n, 1e-8, 60, 3)
+    full = mc.rand_funm(a, mc.EXPONENTIAL, cfg, block=64, as_tensor=True).values
+    g = mc.DeviceGraph(a)
+    z = mc.EXPONENTIAL.prefix(62)
+    ni, pre = g.allocate(cfg.n_walks)
+    Q = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    g.walk_qdense(WalkParams(cfg, z), pre, Q, (0, n), stats=g.new_stats())
+    A = torch.from_numpy(m.toarray()).cuda()
+    ref = z[0] * torch.eye(n, dtype=torch.float64, device="cuda") + z[1] * A + A @ (Q @ A)
+    assert torch.allclose(full, ref, rtol=1e-12, atol=1e-15)
+
+
+def test_mc_baseline_full(mc):
+    """mc_baseline mode "full": the 2-node path closed form
+    (SPEC example: N_s = 1e6 per row within 1e-2 of cosh / sinh 0.1), A = 0 ->
+    zeta_0 I, and diag(full) = the MC diagonal of the same walks to 1e-12."""
+    a2 = mc.SparseMatrix.from_dense([[0, 0.1], [0.1, 0]], True)
+    f2 = mc.mc_baseline(a2, mc.EXPONENTIAL, mc.WalkConfig(10**6, 1e-10, 200, 0), mode="full").values
+    np.testing.assert_allclose(f2, [[np.cosh(0.1), np.sinh(0.1)], [np.sinh(0.1), np.cosh(0.1)]], atol=1e-2)
+    z = mc.mc_baseline(mc.SparseMatrix(sparse.csr_array((3, 3)), sparse.csc_array((3, 3))), mc.EXPONENTIAL,
+                       mc.WalkConfig(10), mode="full").values
+    assert np.array_equal(z, np.eye(3))
+    c = golden_io.load("er300")
+    a = as_matrix(c.sa, True)
+    cfg = mc.WalkConfig(200, 1e-8, 40, 4)
+    full = mc.mc_baseline(a, mc.EXPONENTIAL, cfg, mode="full").values
+    diag = mc.mc_baseline(a, mc.EXPONENTIAL, cfg, mode="diag").values
+    np.testing.assert_allclose(np.diag(full), diag, rtol=1e-12, atol=1e-300)
+    exact = port.dense_funm(c.sa, "exponential", 40)
+    assert np.max(np.abs(full - exact)) < 0.1 * np.max(np.abs(exact))
+
+
 @pytest.mark.parametrize("uniform", [False, True])
 def test_spmv_short_rows_match_sequential_csr_bitwise(mc, uniform):
     """Rows of <= 64 entries: y = z0 v + z1 r + A x equals numpy/scipy's
