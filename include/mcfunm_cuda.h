@@ -278,6 +278,39 @@ MCF_API int mcf_column_costs(mcf_graph *g, const int64_t *walk_pre, int64_t max_
 MCF_API int mcf_graph_kernel_times(mcf_graph *g, double *walk_ms, double *q_ms, int64_t *walk_launches,
                                    int reset);
 
+/* ---- graph generation and ingest on the device ----------
+ * Edges are 64-bit keys (u << 32) | v. */
+
+/* R-MAT: `draws` edges, each `scale` levels of the reference's quadrant rule
+ * (graphgen.py:138-143: row bit r >= a + b; column bit a <= r < a + b or
+ * r >= a + b + c), Philox-4x32-10 uniforms keyed by seed. */
+MCF_API int mcf_gen_rmat_keys(int scale, int64_t draws, double a, double b, double c, uint64_t seed, uint64_t *keys,
+                              void *stream);
+
+/* Chung-Lu: m edges, both endpoints drawn from the cumulative expected-degree
+ * distribution cdf[n] (normalised, increasing). */
+MCF_API int mcf_gen_chung_lu_keys(const double *cdf, int64_t n, int64_t m, uint64_t seed, uint64_t *keys,
+                                  void *stream);
+
+#define MCF_EDGES_DROP_LOOPS 1          /* remove (u, u) (sparsemat.py:258-260) */
+#define MCF_EDGES_ADD_REVERSE 2         /* undirected: add (v, u) for every (u, v) (sparsemat.py:262-264) */
+#define MCF_EDGES_FAIL_ON_DUPLICATES 4  /* duplicates -> MCF_ERR_ARGUMENT instead of being merged */
+
+/* Edge keys -> CSR with n rows (the cleanup filters of simple_graph_from_edges,
+ * sparsemat.py:243-290, in the reference's order: loops, undirected
+ * expansion, duplicates): row_ptr[n+1] and col_ids (capacity col_cap >= the
+ * resulting nnz, e.g. 2 m), columns sorted within every row.  *nnz receives
+ * the edge count.  Synchronises `stream`. */
+MCF_API int mcf_edges_to_csr(const uint64_t *keys, int64_t m, int64_t n, int flags, int64_t *row_ptr,
+                             int32_t *col_ids, int64_t col_cap, int64_t *nnz, void *stream);
+
+/* Isolated-node compaction (sparsemat.py:271-278): the nodes with an incident
+ * edge are renumbered in order; new_row_ptr[n_out+1] (caller capacity n+1),
+ * old_ids[n_out] (their original ids), col_ids remapped in place.
+ * Synchronises `stream`. */
+MCF_API int mcf_csr_compact(int64_t n, const int64_t *row_ptr, int32_t *col_ids, int64_t nnz, int64_t *new_row_ptr,
+                            int64_t *old_ids, int64_t *n_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,9 @@ MCF_STATS_LEN = 4
 MCF_FLAG_TIME_KERNELS = 1
 MCF_FLAG_RETURN_ONLY = 2
 MCF_FLAG_WALK_GROUP = 4
+MCF_EDGES_DROP_LOOPS = 1
+MCF_EDGES_ADD_REVERSE = 2
+MCF_EDGES_FAIL_ON_DUPLICATES = 4
 
 
 def group_flags(groups: int, index: int) -> int:
@@ -70,6 +73,10 @@ SIGNATURES = {
     "mcf_diag_combine_peer": (C.c_int, [P, C.c_double, C.c_double, P, P, C.c_int, P, C.c_int, I64, I64, P]),
     "mcf_walk_qdense": (C.c_int, [P, C.POINTER(McfWalkParams), P, I64, I64, P, I64, P, P]),
     "mcf_column_costs": (C.c_int, [P, P, I64, C.c_int, P, P]),
+    "mcf_gen_rmat_keys": (C.c_int, [C.c_int, I64, C.c_double, C.c_double, C.c_double, C.c_uint64, P, P]),
+    "mcf_gen_chung_lu_keys": (C.c_int, [P, I64, I64, C.c_uint64, P, P]),
+    "mcf_edges_to_csr": (C.c_int, [P, I64, I64, C.c_int, P, P, I64, C.POINTER(I64), P]),
+    "mcf_csr_compact": (C.c_int, [I64, P, P, I64, P, P, C.POINTER(I64), P]),
     "mcf_funm_full": (C.c_int, [P, C.POINTER(McfWalkParams), P, C.c_double, C.c_double, P, I64, I64, P, P]),
     "mcf_diag_variance": (C.c_int, [P, P, C.c_int, P, P, I64, I64, P]),
 }

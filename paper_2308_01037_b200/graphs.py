@@ -97,9 +97,10 @@ def _csr_from_sorted_keys(keys, scale: int, n: int):
     return row_ptr, cols
 
 
-def rmat_device(scale: int, edge_factor: int = 16, pa: float = 0.57, pb: float = 0.19, pc: float = 0.19,
+def rmat_torch(scale: int, edge_factor: int = 16, pa: float = 0.57, pb: float = 0.19, pc: float = 0.19,
                 seed: int = 0, device="cuda", chunk: int = 1 << 26):
-    """Symmetrised R-MAT on the GPU (BASELINE configs 3-4): edge_factor * 2^scale
+    """Symmetrised R-MAT with torch ops (the bench recipe, tools/bench_graphs.py,
+    which must load no repository library): edge_factor * 2^scale
     draws, one uniform per level with the reference's quadrant rule
     (graphgen.py:138-143: row bit r >= pa+pb, column bit r in [pa, pa+pb) or
     r >= pa+pb+pc), then both directions, loops and duplicates removed.  No
@@ -133,6 +134,99 @@ def rmat_device(scale: int, edge_factor: int = 16, pa: float = 0.57, pb: float =
     return n, row_ptr, cols
 
 
+def edges_to_csr_device(keys, n: int, flags: int):
+    """Edge keys (u << 32) | v (int64 tensor on the GPU) -> CSR (row_ptr int64,
+    col_ids int32) with the library's cleanup kernels (mcf_edges_to_csr)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+    dev = keys.device
+    cap = keys.numel() * (2 if flags & N.MCF_EDGES_ADD_REVERSE else 1)
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col_ids = torch.empty(max(1, cap), dtype=torch.int32, device=dev)
+    nnz = C.c_int64()
+    s = torch.cuda.current_stream(dev).cuda_stream
+    N.check(N.lib().mcf_edges_to_csr(keys.data_ptr(), keys.numel(), int(n), int(flags), row_ptr.data_ptr(),
+                                     col_ids.data_ptr(), int(cap), C.byref(nnz), s), "mcf_edges_to_csr")
+    return row_ptr, col_ids[:nnz.value]
+
+
+def compact_isolated_device(n: int, row_ptr, col_ids):
+    """Drop the nodes with no incident edge, renumbering the rest in order
+    (mcf_csr_compact).  Returns (n_out, row_ptr, col_ids, original_ids)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+    dev = row_ptr.device
+    new_rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    old = torch.empty(n, dtype=torch.int64, device=dev)
+    n_out = C.c_int64()
+    s = torch.cuda.current_stream(dev).cuda_stream
+    N.check(N.lib().mcf_csr_compact(int(n), row_ptr.data_ptr(), col_ids.data_ptr(), col_ids.numel(),
+                                    new_rp.data_ptr(), old.data_ptr(), C.byref(n_out), s), "mcf_csr_compact")
+    k = n_out.value
+    return k, new_rp[:k + 1].clone(), col_ids, old[:k].clone()
+
+
+def rmat_device(scale: int, edge_factor: int = 16, pa: float = 0.57, pb: float = 0.19, pc: float = 0.19,
+                seed: int = 0, device="cuda"):
+    """Symmetrised R-MAT generated by the library kernels (mcf_gen_rmat_keys:
+    edge_factor * 2^scale draws of the reference's quadrant rule,
+    graphgen.py:138-143; mcf_edges_to_csr: loops dropped, both directions,
+    duplicates merged, rows sorted).  No isolated-node compaction: n = 2^scale
+    rows.  Returns (n, row_ptr int64, col_ids int32) on the device."""
+    import torch
+
+    from . import _native as N
+    n = 1 << scale
+    draws = edge_factor << scale
+    keys = torch.empty(draws, dtype=torch.int64, device=device)
+    s = torch.cuda.current_stream(keys.device).cuda_stream
+    N.check(N.lib().mcf_gen_rmat_keys(int(scale), int(draws), float(pa), float(pb), float(pc),
+                                      int(seed) & 0xFFFFFFFFFFFFFFFF, keys.data_ptr(), s), "mcf_gen_rmat_keys")
+    row_ptr, col_ids = edges_to_csr_device(keys, n, N.MCF_EDGES_DROP_LOOPS | N.MCF_EDGES_ADD_REVERSE)
+    return n, row_ptr, col_ids
+
+
+def chung_lu_device(n: int, exponent: float = 2.1, mean_degree: float = 20.0, max_degree: float = 1e5,
+                    seed: int = 0, device="cuda"):
+    """Chung-Lu power-law graph by the library kernels: the truncated-Pareto
+    expected degrees of chung_lu_torch, n mean / 2 edges whose endpoints are
+    drawn from their cumulative distribution (mcf_gen_chung_lu_keys), then
+    mcf_edges_to_csr.  Returns (n, row_ptr, col_ids) on the device."""
+    import torch
+
+    from . import _native as N
+    a = exponent - 1.0
+
+    def weights(wmin):
+        u = (torch.arange(n, dtype=torch.float64, device=device) + 0.5) / n
+        r = (wmin / max_degree) ** a
+        return wmin * (1.0 - u * (1.0 - r)) ** (-1.0 / a)
+
+    lo, hi = 1e-3, mean_degree
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if float(weights(mid).mean()) < mean_degree:
+            lo = mid
+        else:
+            hi = mid
+    w = torch.flip(weights(0.5 * (lo + hi)), [0])
+    cdf = torch.cumsum(w, 0)
+    cdf /= cdf[-1].clone()
+    m = int(round(n * mean_degree / 2))
+    keys = torch.empty(m, dtype=torch.int64, device=device)
+    s = torch.cuda.current_stream(keys.device).cuda_stream
+    N.check(N.lib().mcf_gen_chung_lu_keys(cdf.data_ptr(), int(n), int(m), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                          keys.data_ptr(), s), "mcf_gen_chung_lu_keys")
+    row_ptr, col_ids = edges_to_csr_device(keys, n, N.MCF_EDGES_DROP_LOOPS | N.MCF_EDGES_ADD_REVERSE)
+    return n, row_ptr, col_ids
+
+
 def lambda_max_device(g, iters: int = 300) -> float:
     """Largest eigenvalue of a symmetric nonnegative matrix on the device:
     power iteration on A + I (the +1 shift keeps -lambda_max away) with the
@@ -148,9 +242,9 @@ def lambda_max_device(g, iters: int = 300) -> float:
     return float((x @ y) / (x @ x))
 
 
-def chung_lu_device(n: int, exponent: float = 2.1, mean_degree: float = 20.0, max_degree: float = 1e5,
+def chung_lu_torch(n: int, exponent: float = 2.1, mean_degree: float = 20.0, max_degree: float = 1e5,
                     seed: int = 0, device="cuda", chunk: int = 1 << 26):
-    """Chung-Lu power-law graph on the GPU (BASELINE config 5): expected
+    """Chung-Lu power-law graph with torch ops (the bench recipe): expected
     degrees w_i from a truncated Pareto(exponent) on [w_min, max_degree] with
     w_min solved for the requested mean (deterministic quantiles, hubs first),
     n*mean/2 edges with both endpoints drawn proportionally to w, then both

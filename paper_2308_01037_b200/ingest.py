@@ -113,6 +113,8 @@ def simple_graph_from_edges(u, v, directed: bool = False, drop_loops: bool = Tru
     dev = _device(device)
     u = torch.as_tensor(np.asarray(u, dtype=np.int64)).to(dev)
     v = torch.as_tensor(np.asarray(v, dtype=np.int64)).to(dev)
+    if dev.type == "cuda":
+        return _simple_graph_kernels(u, v, directed, drop_loops, drop_duplicates, drop_isolated, meta)
     if drop_loops and u.numel():
         keep = u != v
         u, v = u[keep], v[keep]
@@ -153,6 +155,36 @@ def simple_graph_from_edges(u, v, directed: bool = False, drop_loops: bool = Tru
     return SparseMatrix(csr, csc, not directed, original_ids, dict(meta or {}))
 
 
+def _simple_graph_kernels(u, v, directed, drop_loops, drop_duplicates, drop_isolated, meta) -> SparseMatrix:
+    """The same filters as library kernels (mcf_edges_to_csr: loops, undirected
+    expansion, duplicates, sorted rows; mcf_csr_compact: isolated nodes)."""
+    import torch
+
+    from . import _native as N
+    from .graphs import compact_isolated_device, edges_to_csr_device
+    if u.numel() == 0:
+        raise DegenerateInputError("graph is empty after filtering")
+    top = int(torch.maximum(u.max(), v.max()).item()) + 1
+    if top >= (1 << 31) or int(torch.minimum(u.min(), v.min()).item()) < 0:
+        raise ArgumentError("node ids must lie in [0, 2^31)")
+    keys = (u << 32) | v
+    flags = ((N.MCF_EDGES_DROP_LOOPS if drop_loops else 0) | (0 if directed else N.MCF_EDGES_ADD_REVERSE)
+             | (0 if drop_duplicates else N.MCF_EDGES_FAIL_ON_DUPLICATES))
+    row_ptr, col_ids = edges_to_csr_device(keys, top, flags)
+    if col_ids.numel() == 0:
+        raise DegenerateInputError("graph is empty after filtering")
+    n, original_ids = top, None
+    if drop_isolated:
+        k, row_ptr, col_ids, old = compact_isolated_device(top, row_ptr, col_ids)
+        if k != top:
+            n, original_ids = k, old.cpu().numpy()
+    csr = sparse.csr_array((np.ones(int(col_ids.numel())), col_ids.cpu().numpy(), row_ptr.cpu().numpy()), shape=(n, n))
+    csr.has_sorted_indices = True
+    csc = sparse.csc_array(csr.tocsc())
+    csc.sort_indices()
+    return SparseMatrix(csr, csc, not directed, original_ids, dict(meta or {}))
+
+
 def load_graph(source: GraphSource, device=None) -> SparseMatrix:
     """Read a graph file; return its binary adjacency matrix with the
     requested filters applied (sparsemat.py:301-317)."""
@@ -176,8 +208,23 @@ def symmetrize_digraph(a) -> SparseMatrix:
     block matrix [[0, A], [A^T, 0]] -- out-copies are rows 0..n-1, in-copies
     n..2n-1."""
     csr = sparse.csr_array(a.csr)
-    block = sparse.csr_array(sparse.bmat([[None, csr], [csr.T, None]], format="csr"))
-    block.sort_indices()
+    n = int(csr.shape[0])
+    block = None
+    if csr.nnz and np.all(csr.data == 1.0):
+        import torch
+        if torch.cuda.is_available():  # binary adjacency: the block structure built by the library kernels
+            from .graphs import edges_to_csr_device
+            coo = csr.tocoo()
+            i = torch.from_numpy(coo.row.astype(np.int64)).cuda()
+            j = torch.from_numpy(coo.col.astype(np.int64)).cuda() + n
+            keys = torch.cat([(i << 32) | j, (j << 32) | i])  # (i, n + j) and its transpose (n + j, i)
+            rp, ci = edges_to_csr_device(keys, 2 * n, 0)
+            block = sparse.csr_array((np.ones(int(ci.numel())), ci.cpu().numpy(), rp.cpu().numpy()),
+                                     shape=(2 * n, 2 * n))
+            block.has_sorted_indices = True
+    if block is None:
+        block = sparse.csr_array(sparse.bmat([[None, csr], [csr.T, None]], format="csr"))
+        block.sort_indices()
     meta = dict(getattr(a, "meta", None) or {})
     meta["symmetrized_blocks"] = int(csr.shape[0])
     if getattr(a, "original_ids", None) is not None:

@@ -76,3 +76,62 @@ def test_filter_edge_cases():
         load_graph(GraphSource(os.path.join(HERE, "bad_cols.txt")), device="cpu")
     with pytest.raises(McfunmError, match="not found"):
         load_graph(GraphSource(os.path.join(HERE, "missing.txt")), device="cpu")
+
+
+@pytest.mark.gpu
+def test_filter_kernels_match_torch_path():
+    """mcf_edges_to_csr / mcf_csr_compact (GPU) against the torch path (CPU) on
+    random edge lists with loops, duplicates, both directions and isolated
+    ids: identical CSR, ids and errors."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2308_01037_b200.errors import ArgumentError
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        n = int(rng.integers(50, 5000))
+        m = int(rng.integers(10, 20 * n))
+        u = rng.integers(0, n, m)
+        v = np.where(rng.random(m) < 0.05, u, rng.integers(0, n, m))  # some loops
+        u[: m // 10] = (u[: m // 10] % 7) * 3  # a few hubs
+        for directed in (False, True):
+            for iso in (True, False):
+                a = simple_graph_from_edges(u, v, directed=directed, drop_isolated=iso, device="cpu")
+                b = simple_graph_from_edges(u, v, directed=directed, drop_isolated=iso, device="cuda")
+                assert a.n == b.n
+                assert np.array_equal(a.csr.indptr, b.csr.indptr) and np.array_equal(a.csr.indices, b.csr.indices)
+                assert (a.original_ids is None) == (b.original_ids is None)
+                if a.original_ids is not None:
+                    assert np.array_equal(a.original_ids, b.original_ids)
+        with pytest.raises(ArgumentError):
+            simple_graph_from_edges(np.r_[u, u[:1]], np.r_[v, v[:1]], drop_duplicates=False, device="cuda")
+
+
+@pytest.mark.gpu
+def test_generator_kernels():
+    """R-MAT and Chung-Lu by the library kernels: symmetric, sorted rows, no
+    loops or duplicates, and the same degree statistics as the torch recipes
+    (same rule, different random streams)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from scipy import sparse
+    from paper_2308_01037_b200 import graphs
+    for kind in ("rmat", "chunglu"):
+        if kind == "rmat":
+            n, rp, ci = graphs.rmat_device(16, 16, seed=2)
+            n2, rp2, ci2 = graphs.rmat_torch(16, 16, seed=2)
+        else:
+            n, rp, ci = graphs.chung_lu_device(200_000, seed=2)
+            n2, rp2, ci2 = graphs.chung_lu_torch(200_000, seed=2)
+        rp, ci = rp.cpu().numpy(), ci.cpu().numpy()
+        a = sparse.csr_array((np.ones(ci.size), ci, rp), shape=(n, n))
+        assert abs(a - a.T).nnz == 0
+        rows = np.repeat(np.arange(n), np.diff(rp))
+        assert not np.any(rows == ci)
+        same_row = rows[1:] == rows[:-1]
+        assert np.all(ci[1:][same_row] > ci[:-1][same_row])  # sorted, no duplicates
+        nnz2 = int(ci2.numel())
+        assert abs(ci.size - nnz2) < 0.01 * nnz2, (kind, ci.size, nnz2)
+        d1, d2 = np.diff(rp).max(), int((rp2[1:] - rp2[:-1]).max())
+        assert abs(d1 - d2) < 0.15 * d2, (kind, d1, d2)
