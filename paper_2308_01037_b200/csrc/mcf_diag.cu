@@ -112,7 +112,8 @@ struct QArgs {
 // 3 clusters, 4 k_diag_big): pull pairs, ids, filter passes, hits, push pairs,
 // tests, push hits, spare
 constexpr int PROF_BASE = 20, PROF_CLS = 8, PROF_NCLS = 5;
-constexpr int PROF_SLOTS = PROF_BASE + PROF_CLS * PROF_NCLS;  // 16..18: cluster-kernel columns, cycles, emissions
+constexpr int PROF_PH = PROF_BASE + PROF_CLS * PROF_NCLS;  // cluster phase cycles (rank 0): 6 slots
+constexpr int PROF_SLOTS = PROF_PH + 8;  // 16..18: cluster-kernel columns, cycles, emissions
 
 __device__ __forceinline__ int ld_relaxed_i32(const int *p) {
     int v;
@@ -777,6 +778,14 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
     int *r0_nchunk = cl.map_shared_rank(&s_nchunk, 0), *r0_next2 = cl.map_shared_rank(&s_next2, 0);
     int *r0_done = cl.map_shared_rank(&s_done, 0);
 
+    long long ph_prev = a.prof ? clock64() : 0;  // phase timestamps (rank 0, thread 0; MCF_DIAG_PROF)
+    auto phase = [&](int k) {
+        if (a.prof && rank == 0 && tid == 0) {
+            const long long t = clock64();
+            atomicAdd(a.prof + PROF_PH + k, (unsigned long long)(t - ph_prev));
+            ph_prev = t;
+        }
+    };
     while (true) {
         for (int t = tid; t < SCAP; t += Q_THREADS) {
             skeys[t] = EMPTY_KEY;
@@ -798,6 +807,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         cl.sync();
         const long long c = s_col;
         if (c < 0) break;
+        phase(0);  // zeroing + column fetch
         const long long t_start = a.prof ? clock64() : 0;
         const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
         const long long s0 = slot_of(a, g0), m = slot_of(a, g1) - s0;
@@ -825,6 +835,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             }
         }
         cl.sync();
+        phase(1);  // Q_c build
         // this CTA's part: Bloom bits and its share of the support list
         for (int t = tid; t < SCAP; t += Q_THREADS) {
             const int key = skeys[t];
@@ -849,6 +860,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
         const int nsupp_all = *r0_nsupp;
         const int nsupp = nsupp_all <= lcap ? nsupp_all : 0x3fffffff;  // overflow: never push
         const long long t_built = a.prof ? clock64() : 0;
+        phase(2);  // filter + support list + filter merge
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
         if (a.big) {
             // combine work sum_{i in C_c} deg(i): above BIG_WORK the table goes to
@@ -911,6 +923,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             __threadfence();
             cl.sync();
         }
+        phase(3);  // big check + exact bits
         // the cluster's (rank 0's) lists: long entries, their first piece and
         // piece sum, and the piece -> entry map (global scratch, read with .cg)
         const long long reg = cta - rank;
@@ -1010,6 +1023,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             if (lane == 0 && acc) atomicAdd(lacc + j, (unsigned long long)acc);
         }
         cl.sync();
+        phase(4);  // entries and pieces
         const int nlong_all = *r0_nlong;
         const int nlong = nlong_all < a.llcap ? nlong_all : (int)a.llcap;
         for (long long j = gt; j < nlong; j += CT) {
@@ -1025,6 +1039,7 @@ __global__ void __cluster_dims__(K, 1, 1) __launch_bounds__(Q_THREADS, 1)
             atomicAdd(a.prof + 19, (unsigned long long)(t_built - t_start));
         }
         cl.sync();  // every remote access of this column is done before the tables and counters are reset
+        phase(5);  // finalize + end barrier
         if (cbits) {  // clear the bitmap words of this CTA's keys before the next column sets its own
             for (int t = tid; t < SCAP; t += Q_THREADS) {
                 const int key = skeys[t];
@@ -1393,6 +1408,9 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
                 "[diag-prof] cols %llu big %llu emissions %llu support %llu | pull pairs %llu ids %llu filt %llu hits %llu"
                 " | push pairs %llu tests %llu hits %llu | cyc build %.3e combine %.3e | gtable cols %llu cycles %llu emissions %llu | cluster cols %llu cycles %llu emissions %llu build %llu\n",
                 h[8], h[9], h[6], h[7], h[0], h[1], h[2], h[12], h[3], h[4], h[5], (double)h[10], (double)h[11], h[13], h[14], h[15], h[16], h[17], h[18], h[19]);
+        fprintf(stderr, "[diag-phases] zero+fetch %.3e build %.3e filter %.3e big+exact %.3e pairs %.3e final %.3e\n",
+                (double)h[PROF_PH + 0], (double)h[PROF_PH + 1], (double)h[PROF_PH + 2], (double)h[PROF_PH + 3],
+                (double)h[PROF_PH + 4], (double)h[PROF_PH + 5]);
         std::string line = "[diag-timeline]";
         for (auto &x : tl) {
             float ms = 0.f;
