@@ -199,6 +199,29 @@ __device__ __forceinline__ long long lookup(const int *keys, const long long *va
     }
 }
 
+// int64 add into shared memory as two native 32-bit atomics (the 64-bit
+// shared atomicAdd is a CAS loop, which hot keys turn into long spins): the
+// low word's returned old value tells the one adder that wrapped it to carry.
+// The slot holds the exact sum mod 2^64 (two's complement) once all adds land.
+__device__ __forceinline__ void smem_add_i64(long long *p, long long v) {
+    unsigned *w = reinterpret_cast<unsigned *>(p);
+    const unsigned long long u = (unsigned long long)v;
+    const unsigned lo = (unsigned)u, hi = (unsigned)(u >> 32);
+    const unsigned old = atomicAdd(w, lo);
+    const unsigned up = hi + (old + lo < old ? 1u : 0u);
+    if (up) atomicAdd(w + 1, up);
+}
+
+// sum of v over the lanes of `mask` (the caller's match group), exact mod
+// 2^64: three digit sums of <= 22 bits each never overflow 32 bits
+__device__ __forceinline__ long long group_sum_i64(unsigned mask, long long v) {
+    const unsigned long long u = (unsigned long long)v;
+    const unsigned long long s0 = __reduce_add_sync(mask, (unsigned)(u & 0x3FFFFFull));
+    const unsigned long long s1 = __reduce_add_sync(mask, (unsigned)((u >> 22) & 0x1FFFFFull));
+    const unsigned long long s2 = __reduce_add_sync(mask, (unsigned)(u >> 43));
+    return (long long)(s0 + (s1 << 22) + (s2 << 43));
+}
+
 // Bloom bit of a key (independent of the table hash).  Most combine lookups
 // miss (C_i entries no walk from c visited): the filter answers them with one
 // shared-memory word instead of a linear-probing chain.
@@ -495,7 +518,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) k_diag_q(QArgs a) {
                 if (sv[u] < 0) continue;
                 const long long q = __double2ll_rn(ldexp(wv[u], E));
                 const int slot = keys ? find_or_insert(keys, mask, sv[u]) : sv[u];
-                atomicAdd(reinterpret_cast<unsigned long long *>(&vals[slot]), (unsigned long long)q);
+                smem_add_i64(&vals[slot], q);
             }
         }
         __syncthreads();
@@ -1097,6 +1120,515 @@ __global__ void k_big_counts(const BigRec *__restrict__ big, unsigned nrec, long
     if (b < nrec) cnt[b] = big[b].cn;
 }
 
+// ---------------------------------------------------------------------------
+// Combine units (uniform-value graphs; the default).  A walked column c whose
+// Q_c is too wide for one CTA's shared table is split into K = 2^k units by
+// KEY GROUP (key_group, NGROUPS): unit u builds, in its own shared memory,
+// the part of Q_c whose keys fall in its group range, and adds
+// sum_{j in C_i, group(j) in range} Q_c[j] for every entry (i, c) -- a
+// contiguous slice of the group-ordered column C_i (g->ckeys, g->gofs).  The
+// K int64 partials of an entry sum to the int64 <Q_c, C_i> the single-table
+// kernels form, so pcol is bit-identical to theirs, with every probe in local
+// shared memory: no distributed shared memory, no cluster barriers, no global
+// tables, no GPU-wide hand-off of big columns.  One persistent kernel takes the
+// units of all columns, widest first (K = NGROUPS ... 1).
+// Inside a unit: 32 entries per warp-step have their slices located together
+// (coalesced metadata loads); slices of <= UNIT_SERIAL ids are scanned by one
+// lane each, longer ones (and push entries) are queued and cut into pieces of
+// `chunk` ids that all warps share.  Partials of split entries are int64
+// atomics into the entry's pcol slot (zeroed by k_unit_classify), converted to
+// fp64 when the column's last unit finishes (deterministic: integer sums).
+// ---------------------------------------------------------------------------
+constexpr int UNIT_SERIAL = 24;  // slice length scanned by one lane
+constexpr int UNIT_BUCKETS = GROUP_BITS + 1;  // K = 1, 2, ..., NGROUPS
+constexpr int UPROF_SLOTS = 16;
+
+struct UArgs {
+    const long long *__restrict__ walk_pre;
+    long long wb, slot_len;
+    const long long *__restrict__ eoff;
+    const long long *__restrict__ walk_off;
+    long long off_base;
+    const int *__restrict__ est;
+    const double *__restrict__ ewt;
+    const long long *__restrict__ csc_ptr;
+    const int *__restrict__ csc_rows;
+    const double *__restrict__ csc_vals;
+    const int *__restrict__ ckeys;
+    const int *__restrict__ gidx;
+    const int *__restrict__ gofs;
+    long long n;
+    long long c0, ncol;  // the batch's column range [c0, c0 + ncol)
+    double *__restrict__ pcol;
+    double value;
+    const unsigned long long *__restrict__ colmax;
+    int push_pct;
+    int opt;
+    const int *hub_of;
+    const unsigned *hub_bits;
+    long long hub_words;
+    const int *__restrict__ lists;  // bucket k's columns at lists + k * ncol
+    const unsigned *__restrict__ bcnt;  // columns per bucket
+    unsigned long long *counter;
+    int *done;           // per column of the batch: finished units
+    int *lkeys;          // per-CTA support list (lcap each)
+    long long *lvals;
+    long long lcap;
+    int *qt;             // per-CTA queue of long entries: entry (~t: push), slice start, length, piece prefix
+    long long *qlo;
+    int *qlen;
+    long long *qpre;
+    long long qcap;
+    int *pmap;           // per-CTA piece -> queue entry map (pcap each; wider units binary-search qpre)
+    long long pcap;
+    long long chunk;
+    long long small_need;  // widest table need of a one-unit column
+    long long ucap;        // table need per unit of a split column
+    int dense_n;           // n at or below which a one-unit column may use a dense Q_c
+    int *err;              // bit 8: a unit table overflowed
+    unsigned long long *prof;
+};
+
+__device__ __forceinline__ long long uslot(const UArgs &a, long long g) {
+    if (a.slot_len > 0) return (g - a.wb) * a.slot_len;
+    if (a.eoff) return a.eoff[g - a.wb];
+    return a.walk_off[g] - a.off_base + (g - a.wb);
+}
+
+// units a column's table need takes (power of two; 0: too wide for NGROUPS units)
+__device__ __forceinline__ int unit_count(long long need, long long small_need, long long ucap, bool dense_ok) {
+    if (dense_ok || need <= small_need) return 1;
+    const long long k = (need + ucap - 1) / ucap;
+    int K = 2;
+    while (K < k) K <<= 1;
+    return K <= NGROUPS ? K : 0;
+}
+
+// One warp per 32 columns of the batch: unit count, bucket lists (warp-
+// aggregated appends), pcol slots of walked columns zeroed, done counters.
+// need_max[0] = widest need that did not fit NGROUPS units (host falls back).
+__global__ void k_unit_classify(UArgs a, int *__restrict__ lists, unsigned *__restrict__ bcnt,
+                                unsigned long long *__restrict__ too_wide) {
+    const int lane = threadIdx.x & 31;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long base = w0 * 32; base < a.ncol; base += nw * 32) {
+        const long long c = a.c0 + base + lane;
+        int b = -1;
+        if (base + lane < a.ncol) {
+            const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
+            if (g0 != g1) {
+                const long long m = uslot(a, g1) - uslot(a, g0);
+                const long long need = m < a.n ? m : a.n;
+                const bool dense_ok = a.n <= a.dense_n;
+                const int K = unit_count(need, a.small_need, a.ucap, dense_ok);
+                if (K == 0) {
+                    atomicMax(too_wide, (unsigned long long)need);
+                } else {
+                    b = 31 - __clz(K);
+                }
+                a.done[base + lane] = 0;
+            }
+        }
+        for (int k = 0; k < UNIT_BUCKETS; ++k) {
+            const unsigned msk = __ballot_sync(MCF_FULL, b == k);
+            if (!msk) continue;
+            unsigned p0 = 0;
+            if (lane == __ffs(msk) - 1) p0 = atomicAdd(bcnt + k, (unsigned)__popc(msk));
+            p0 = __shfl_sync(MCF_FULL, p0, __ffs(msk) - 1);
+            if (b == k) lists[k * a.ncol + p0 + __popc(msk & lanemask_lt())] = (int)c;
+        }
+        // zero the pcol slots of the walked columns (atomics land there)
+        unsigned walked = __ballot_sync(MCF_FULL, b >= 0);
+        while (walked) {
+            const int l = __ffs(walked) - 1;
+            walked &= walked - 1;
+            const long long cc = a.c0 + base + l;
+            const long long lo = a.csc_ptr[cc], hi = a.csc_ptr[cc + 1];
+            for (long long e = lo + lane; e < hi; e += 32) a.pcol[e] = 0.0;
+        }
+    }
+}
+
+// insert with an occupancy guard: a table past its limit drops the key and
+// flags the overflow (never expected: need per unit has a ~12 sigma margin)
+__device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, int *nkeys, int limit, int *err) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        const int k = keys[s];
+        if (k == key) return (int)s;
+        if (k == EMPTY_KEY) {
+            if (*(volatile int *)nkeys >= limit) {
+                atomicOr(err, 256);
+                return -1;
+            }
+            const int old = atomicCAS(&keys[s], EMPTY_KEY, key);
+            if (old == EMPTY_KEY) {
+                atomicAdd(nkeys, 1);
+                return (int)s;
+            }
+            if (old == key) return (int)s;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+// sum of Q_c over the ids ckeys[lo, hi) (warp-cooperative, PULL_U ids per
+// lane in flight) or over the unit's support positions [lo, hi) tested
+// against hub row i's bitmap (push)
+__device__ __forceinline__ long long unit_scan(const UArgs &a, const int *keys, const long long *vals, uint32_t mask,
+                                               const unsigned *filt, const int *lkeys, const long long *lvals,
+                                               int i, bool push, long long lo, long long hi, int lane) {
+    long long acc = 0;
+    if (push) {
+        const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
+        constexpr int PUSH_U = 4;
+        for (long long t0 = lo; t0 < hi; t0 += 32 * PUSH_U) {
+            int kv[PUSH_U];
+            unsigned wv[PUSH_U];
+#pragma unroll
+            for (int u = 0; u < PUSH_U; ++u) {
+                const long long t = t0 + 32 * u + lane;
+                kv[u] = t < hi ? lkeys[t] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PUSH_U; ++u) wv[u] = kv[u] >= 0 ? __ldg(bits + (kv[u] >> 5)) : 0u;
+#pragma unroll
+            for (int u = 0; u < PUSH_U; ++u)
+                if ((wv[u] >> (kv[u] & 31)) & 1u) acc += lvals[t0 + 32 * u + lane];
+        }
+    } else {
+        constexpr int PULL_U = 8;
+        for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
+            int jv[PULL_U];
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u) {
+                const long long e = e0 + 32 * u + lane;
+                jv[u] = e < hi ? __ldg(a.ckeys + e) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PULL_U; ++u)
+                if (jv[u] >= 0 && filter_test(filt, jv[u])) acc += lookup(keys, vals, mask, jv[u]);
+        }
+    }
+    return warp_sum_ll(acc);
+}
+
+template <int TH, int CAP, int FW>
+__global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    long long *svals = reinterpret_cast<long long *>(smem_raw);
+    int *skeys = reinterpret_cast<int *>(svals + CAP);
+    unsigned *filt = reinterpret_cast<unsigned *>(skeys + CAP);
+    constexpr int NWARP = TH / 32;
+    __shared__ long long s_c, s_np, s_wsum[NWARP];
+    __shared__ int s_u, s_lg, s_next, s_nq, s_nsupp, s_nkeys, s_last, s_sidx;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int *lkeys = a.lkeys + (long long)blockIdx.x * a.lcap;
+    long long *lvals = a.lvals + (long long)blockIdx.x * a.lcap;
+    int *qt = a.qt + (long long)blockIdx.x * a.qcap;
+    long long *qlo = a.qlo + (long long)blockIdx.x * a.qcap;
+    int *qlen = a.qlen + (long long)blockIdx.x * a.qcap;
+    long long *qpre = a.qpre + (long long)blockIdx.x * (a.qcap + 1);
+    int *pmap = a.pmap + (long long)blockIdx.x * a.pcap;
+    unsigned long long pr[5] = {0, 0, 0, 0, 0};  // MCF_DIAG_PROF: serial entries, serial ids, pieces, pull ids, push tests
+
+    while (true) {
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long x = atomicAdd(a.counter, 1ull);
+            long long c = -1;
+            int u = 0, lg = 0, sidx = 0;
+            for (int k = UNIT_BUCKETS - 1; k >= 0; --k) {  // widest columns first
+                const unsigned long long nu = (unsigned long long)__ldcg(a.bcnt + k) << k;
+                if (x < nu) {
+                    sidx = (int)(x >> k);
+                    c = a.lists[k * a.ncol + sidx];
+                    u = (int)(x & ((1ull << k) - 1));
+                    lg = k;
+                    break;
+                }
+                x -= nu;
+            }
+            s_c = c;
+            s_u = u;
+            s_lg = lg;
+            s_next = 0;
+            s_nq = 0;
+            s_nsupp = 0;
+            s_nkeys = 0;
+            s_np = 0;
+        }
+        __syncthreads();
+        const long long c = s_c;
+        if (c < 0) break;
+        const int u = s_u, lg = s_lg, K = 1 << lg, shift = GROUP_BITS - lg;
+        const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
+        const long long s0 = uslot(a, g0), m = uslot(a, g1) - s0;
+        const long long need = m < a.n ? m : a.n;
+        const long long t_start = a.prof ? clock64() : 0;
+        // table: one unit -> sized by need (k_diag_q's rule); K units -> need / K
+        // plus a 1/8 + 64 margin for the group's share of the support
+        const bool dense = K == 1 && a.n <= a.dense_n && need * 4 > a.n;
+        long long need_u = K == 1 ? need : need / K + need / (8 * K) + 64;
+        if (need_u > need) need_u = need;
+        uint32_t cap = 32;
+        while ((long long)cap < need_u * 2 && cap < (uint32_t)CAP) cap <<= 1;
+        while ((long long)cap * 3 < need_u * 4 + 4 && cap < (uint32_t)CAP) cap <<= 1;
+        int *keys = dense ? nullptr : skeys;
+        long long *vals = svals;
+        if (dense) cap = (uint32_t)a.n;
+        const uint32_t mask = cap - 1;
+        const int limit = (int)(cap - cap / 8);
+        for (uint32_t t = tid; t < cap; t += TH) {
+            if (keys) keys[t] = EMPTY_KEY;
+            vals[t] = 0;
+        }
+        for (int t = tid; t < FW; t += TH) filt[t] = 0u;
+        __syncthreads();
+        const double maxw = __longlong_as_double((long long)a.colmax[c]);
+        int lg_m = 0;
+        while ((1ll << lg_m) < m) ++lg_m;
+        const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // as k_diag_q: sum of m terms < 2^62
+        // Q_c over this unit's key groups
+        constexpr int U = 4;
+        for (long long base = 0; base < m; base += (long long)U * TH) {
+            int sv[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const long long i = base + (long long)q * TH + tid;
+                sv[q] = i < m ? __ldcs(a.est + s0 + i) : EMPTY_KEY;
+                if (K > 1 && sv[q] >= 0 && (int)(key_group(sv[q]) >> shift) != u) sv[q] = EMPTY_KEY;
+            }
+            double wv[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) wv[q] = sv[q] >= 0 ? __ldcs(a.ewt + s0 + base + (long long)q * TH + tid) : 0.0;
+            // lanes holding the same key add once (step-major slots: a warp's
+            // 32 walks share the start state at step 0 and hubs later on)
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                long long qv = sv[q] >= 0 ? __double2ll_rn(ldexp(wv[q], E)) : 0;
+                const unsigned same = __match_any_sync(MCF_FULL, sv[q]);
+                if (sv[q] < 0) continue;
+                if (__popc(same) > 1) {
+                    qv = group_sum_i64(same, qv);
+                    if (lane != __ffs(same) - 1) continue;
+                }
+                const int slot = keys ? unit_insert(keys, mask, sv[q], &s_nkeys, limit, a.err) : sv[q];
+                if (slot >= 0) smem_add_i64(&vals[slot], qv);
+            }
+        }
+        __syncthreads();
+        // Bloom filter and support list of this unit's part
+        for (uint32_t t = tid; t < cap; t += TH) {
+            const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
+            if (key != EMPTY_KEY) {
+                filter_add(filt, key);
+                const int p = atomicAdd(&s_nsupp, 1);
+                if (p < a.lcap) {
+                    lkeys[p] = key;
+                    lvals[p] = vals[t];
+                }
+            }
+        }
+        __syncthreads();
+        const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
+        const long long t_built = a.prof ? clock64() : 0;
+        const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        const double scale = a.value;
+        // phase A: 32 entries per warp-step
+        while (true) {
+            int t0 = 0;
+            if (lane == 0) t0 = atomicAdd(&s_next, 32);
+            t0 = __shfl_sync(MCF_FULL, t0, 0);
+            if (t0 >= cn) break;
+            const int t = t0 + lane;
+            const bool valid = t < cn;
+            int i = 0;
+            long long lo = 0, hi = 0;
+            bool grp_filter = false, push = false;
+            if (valid) {
+                i = __ldg(a.csc_rows + cs + t);
+                lo = __ldg(a.csc_ptr + i);
+                hi = __ldg(a.csc_ptr + i + 1);
+                if (K > 1) {
+                    if (hi - lo > GROUP_OFS_MIN) {
+                        const int *of = a.gofs + (long long)__ldg(a.gidx + i) * (NGROUPS + 1);
+                        const int gl = u << shift;
+                        const long long b0 = __ldg(of + gl), b1 = __ldg(of + gl + (1 << shift));
+                        hi = lo + b1;
+                        lo = lo + b0;
+                    } else {
+                        grp_filter = true;
+                    }
+                }
+                push = !grp_filter && a.hub_of && 100 * (hi - lo) > (long long)a.push_pct * nsupp &&
+                       __ldg(a.hub_of + i) >= 0;
+            }
+            const bool serial = valid && !push && (grp_filter || hi - lo <= UNIT_SERIAL);
+            long long acc = 0;
+            if (serial) {
+                for (long long e = lo; e < hi; e += 4) {
+                    int jv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) jv[q] = e + q < hi ? __ldg(a.ckeys + e + q) : -1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (jv[q] < 0) continue;
+                        if (grp_filter && (int)(key_group(jv[q]) >> shift) != u) continue;
+                        if (filter_test(filt, jv[q])) acc += lookup(keys, vals, mask, jv[q]);
+                    }
+                }
+                if (a.prof) {
+                    pr[0] += 1;
+                    pr[1] += (unsigned long long)(hi - lo);
+                }
+                if (K == 1) {
+                    a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp((double)acc, -E));
+                } else if (acc) {
+                    atomicAdd(reinterpret_cast<unsigned long long *>(a.pcol + cs + t), (unsigned long long)acc);
+                }
+            }
+            const bool queued = valid && !serial && nsupp > 0 && (push || hi > lo);
+            const unsigned qm = __ballot_sync(MCF_FULL, queued);
+            if (qm) {
+                int qb = 0;
+                if (lane == 0) qb = atomicAdd(&s_nq, __popc(qm));
+                qb = __shfl_sync(MCF_FULL, qb, 0);
+                if (queued) {
+                    const int k = qb + __popc(qm & lanemask_lt());
+                    if (k < a.qcap) {
+                        qt[k] = push ? ~t : t;
+                        qlo[k] = push ? 0 : lo;
+                        qlen[k] = (int)(push ? nsupp : hi - lo);
+                    } else {
+                        atomicOr(a.err, 512);  // queue overflow (qcap >= max degree: not expected)
+                    }
+                }
+            }
+            if (!queued && valid && !serial && K == 1)  // nothing to scan: the zero partial
+                a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp(0.0, -E));
+        }
+        __syncthreads();
+        const int nq = s_nq < a.qcap ? s_nq : (int)a.qcap;
+        // piece prefix over the queue (block-wide scan, chunks of TH)
+        for (int b0 = 0; b0 < nq; b0 += TH) {
+            const int k = b0 + tid;
+            long long v = k < nq ? (qlen[k] + a.chunk - 1) / a.chunk : 0;
+            long long inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long x = __shfl_up_sync(MCF_FULL, inc, o);
+                if (lane >= o) inc += x;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            __syncthreads();
+            if (warp == 0) {
+                long long ws = lane < NWARP ? s_wsum[lane] : 0, wi = ws;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long x = __shfl_up_sync(MCF_FULL, wi, o);
+                    if (lane >= o) wi += x;
+                }
+                if (lane < NWARP) s_wsum[lane] = wi - ws;
+            }
+            __syncthreads();
+            const long long carry = s_np;
+            if (k < nq) {
+                const long long p0 = carry + s_wsum[warp] + inc - v;
+                qpre[k] = p0;
+                for (long long p = p0; p < p0 + v && p < a.pcap; ++p) pmap[p] = k;
+            }
+            __syncthreads();
+            if (tid == TH - 1) s_np = carry + s_wsum[warp] + inc;
+            __syncthreads();
+        }
+        const long long npieces = s_np;
+        if (tid == 0) {
+            qpre[nq] = npieces;
+            s_next = 0;
+        }
+        __syncthreads();
+        // phase B: pieces of the queued entries, all warps
+        while (true) {
+            int x = 0;
+            if (lane == 0) x = atomicAdd(&s_next, 1);
+            x = __shfl_sync(MCF_FULL, x, 0);
+            if (x >= npieces) break;
+            int lo_j = 0, hi_j = nq - 1;  // last entry j with qpre[j] <= x
+            if (npieces <= a.pcap) lo_j = hi_j = pmap[x];
+            while (lo_j < hi_j) {
+                const int mid = (lo_j + hi_j + 1) >> 1;
+                if (qpre[mid] <= x) lo_j = mid;
+                else hi_j = mid - 1;
+            }
+            const int j = lo_j;
+            const int qtj = qt[j];
+            const bool push = qtj < 0;
+            const int t = push ? ~qtj : qtj;
+            const long long p = x - qpre[j], len = qlen[j];
+            const long long b = qlo[j] + p * a.chunk;
+            const long long e = qlo[j] + (len < (p + 1) * a.chunk ? len : (p + 1) * a.chunk);
+            const int i = push ? __ldg(a.csc_rows + cs + t) : 0;
+            const long long acc = unit_scan(a, keys, vals, mask, filt, lkeys, lvals, i, push, b, e, lane);
+            if (a.prof && lane == 0) {
+                pr[2] += 1;
+                pr[push ? 4 : 3] += (unsigned long long)(e - b);
+            }
+            if (lane == 0) {
+                const bool whole = len <= a.chunk;
+                if (K == 1 && whole) a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp((double)acc, -E));
+                else if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(a.pcol + cs + t), (unsigned long long)acc);
+            }
+        }
+        __syncthreads();
+        // int64 sums -> fp64: one-unit columns convert their split entries,
+        // a split column's last unit converts all of its entries
+        if (K == 1) {
+            for (int k = tid; k < nq; k += TH) {
+                if (qlen[k] <= a.chunk) continue;
+                const int qtj = qt[k], t = qtj < 0 ? ~qtj : qtj;
+                const long long v = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(a.pcol + cs + t));
+                a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp((double)v, -E));
+            }
+        } else {
+            if (tid == 0) {
+                __threadfence();
+                const int old = atomicAdd(a.done + (c - a.c0), 1);
+                s_last = old == K - 1;
+            }
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                for (long long t = tid; t < cn; t += TH) {
+                    const long long v =
+                        (long long)__ldcg(reinterpret_cast<const unsigned long long *>(a.pcol + cs + t));
+                    a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp((double)v, -E));
+                }
+            }
+        }
+        if (a.prof && tid == 0) {
+            const long long t_end = clock64();
+            atomicAdd(a.prof + 0, 1ull);
+            atomicAdd(a.prof + 1, (unsigned long long)cn);
+            atomicAdd(a.prof + 2, (unsigned long long)nq);
+            atomicAdd(a.prof + 3, (unsigned long long)m);
+            atomicAdd(a.prof + 4, (unsigned long long)nsupp);
+            atomicAdd(a.prof + 5, (unsigned long long)(t_built - t_start));
+            atomicAdd(a.prof + 6, (unsigned long long)(t_end - t_built));
+            atomicAdd(a.prof + 7 + (lg < 8 ? lg : 7), 1ull);
+        }
+    }
+    if (a.prof) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            unsigned long long v = pr[k];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MCF_FULL, v, o);
+            if (lane == 0 && v) atomicAdd(a.prof + UPROF_SLOTS + k, v);
+        }
+    }
+}
+
 // d_i = zeta_0 + zeta_1 a_ii + sum over row i of pcol[csr2csc[e]] (4 lanes per row).
 // PEER: pcol[(i, c)] is read from the part (rank) owning column c -- mapped
 // peer memory -- and d_i is stored to every output buffer (mcf_diag_combine_peer).
@@ -1138,10 +1670,187 @@ static long long emission_budget() {  // read per call: tests switch it at run t
     return v < (1ll << 16) ? (1ll << 16) : v;
 }
 
+// the push/pull break-even of the combine (see run_q)
+static int push_pct_for(const mcf_graph *g) {
+    const char *e = getenv("MCF_PUSH_PCT");
+    long long pct = (200ll * g->n) / (1ll << 22);
+    pct = pct < 200 ? 200 : (pct > 1600 ? 1600 : pct);
+    return e ? atoi(e) : (int)pct;
+}
+
+template <int TH, int CAP, int FW>
+static int launch_units(UArgs &a, int grid, cudaStream_t s) {
+    const size_t smem = (size_t)CAP * (sizeof(int) + sizeof(long long)) + FW * sizeof(unsigned);
+    MCF_CUDA(cudaFuncSetAttribute(k_diag_unit<TH, CAP, FW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_diag_unit<TH, CAP, FW><<<grid, TH, smem, s>>>(a);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_diag_unit");
+    return MCF_OK;
+}
+
+// The combine by units (uniform-value graphs).  *fallback = true (nothing run)
+// when a column's table would need more than NGROUPS units.
+static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre,
+                     long long cb, long long ce, long long wb, long long slot_len, const long long *eoff,
+                     const long long *walk_off, long long off_base, const int *est, const double *ewt, double *pcol,
+                     cudaStream_t s, bool *fallback) {
+    *fallback = false;
+    const long long ncol = ce - cb;
+    if (ncol <= 0) return MCF_OK;
+    int rc = ensure_group_keys(g, s);
+    if (rc) return rc;
+    static const int th = [] {
+        const char *e = getenv("MCF_UNIT_THREADS");  // 1024 (one CTA per SM, 16384-slot tables) or 512 (two)
+        return e && atoi(e) == 512 ? 512 : 1024;
+    }();
+    const int cap = th == 1024 ? 16384 : 8192;
+    UArgs a{};
+    a.walk_pre = walk_pre;
+    a.wb = wb;
+    a.slot_len = slot_len;
+    a.eoff = eoff;
+    a.walk_off = walk_off;
+    a.off_base = off_base;
+    a.est = est;
+    a.ewt = ewt;
+    a.csc_ptr = (const long long *)g->csc_ptr;
+    a.csc_rows = g->csc_rows;
+    a.csc_vals = g->csc_vals;
+    a.ckeys = g->ckeys;
+    a.gidx = g->gidx;
+    a.gofs = g->gofs;
+    a.n = g->n;
+    a.c0 = cb;
+    a.ncol = ncol;
+    a.pcol = pcol;
+    a.value = g->value;
+    a.colmax = colmax;
+    a.push_pct = push_pct_for(g);
+    a.hub_of = g->hub_of;
+    a.hub_bits = g->hub_bits;
+    a.hub_words = g->hub_words;
+    {
+        const char *e = getenv("MCF_UNIT_CHUNK");
+        a.chunk = e ? atoll(e) : 1024;
+        if (a.chunk < 32) a.chunk = 32;
+    }
+    a.small_need = (3ll * cap - 4) / 4;
+    a.ucap = (long long)cap * 5 / 8;
+    a.dense_n = cap * 12 / 8;
+    if (const char *e = getenv("MCF_UNIT_SMALL_NEED")) {  // tests: split narrow columns too (no dense tables)
+        const long long v = atoll(e);
+        if (v >= 1 && v < a.small_need) {
+            a.small_need = v;
+            a.ucap = v * 5 / 6 > 0 ? v * 5 / 6 : 1;
+            a.dense_n = 0;
+        }
+    }
+    AsyncFrees frees(s);
+    static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
+    const int grid = sm_count() * (th == 1024 ? 1 : 2);
+    // small device block: bucket counts, work counter, too-wide need, error bits, profile
+    unsigned char *blk = nullptr;
+    const size_t blk_bytes = 256 + sizeof(unsigned long long) * 2 * UPROF_SLOTS;
+    MCF_CUDA(cudaMallocAsync(&blk, blk_bytes, s));
+    frees.keep(blk);
+    MCF_CUDA(cudaMemsetAsync(blk, 0, blk_bytes, s));
+    unsigned *bcnt = reinterpret_cast<unsigned *>(blk);                              // 16 x u32
+    unsigned long long *counter = reinterpret_cast<unsigned long long *>(blk + 64);  // work counter
+    unsigned long long *too_wide = counter + 1;
+    int *err = reinterpret_cast<int *>(blk + 96);
+    a.bcnt = bcnt;
+    a.counter = counter;
+    a.err = err;
+    a.prof = prof_on ? reinterpret_cast<unsigned long long *>(blk + 256) : nullptr;
+    int *lists = nullptr;
+    MCF_CUDA(cudaMallocAsync(&lists, sizeof(int) * ((size_t)UNIT_BUCKETS * ncol + (size_t)ncol), s));
+    frees.keep(lists);
+    a.lists = lists;
+    a.done = lists + (size_t)UNIT_BUCKETS * ncol;
+    // per-CTA scratch: support list (a table's keys) and the entry queue
+    // (one slot per entry of the widest column)
+    a.lcap = cap;
+    a.qcap = g->info.max_degree > 64 ? g->info.max_degree : 64;
+    unsigned char *scr = nullptr;
+    a.pcap = 1ll << 18;
+    const size_t per_cta = (size_t)a.lcap * (sizeof(int) + sizeof(long long)) +
+                           (size_t)a.qcap * (sizeof(int) + sizeof(long long) + sizeof(int) + sizeof(long long)) + 8 +
+                           (size_t)a.pcap * sizeof(int);
+    MCF_CUDA(cudaMallocAsync(&scr, per_cta * grid + 64, s));
+    frees.keep(scr);
+    {
+        unsigned char *p = scr;
+        a.lvals = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * a.lcap * grid;
+        a.qlo = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * a.qcap * grid;
+        a.qpre = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * (a.qcap + 1) * grid;
+        a.lkeys = reinterpret_cast<int *>(p);
+        p += sizeof(int) * a.lcap * grid;
+        a.qt = reinterpret_cast<int *>(p);
+        p += sizeof(int) * a.qcap * grid;
+        a.qlen = reinterpret_cast<int *>(p);
+        p += sizeof(int) * a.qcap * grid;
+        a.pmap = reinterpret_cast<int *>(p);
+    }
+    {
+        const long long warps = (ncol + 31) / 32;
+        const long long blocks = (warps * 32 + 255) / 256;
+        k_unit_classify<<<(unsigned)(blocks < 65536 ? blocks : 65536), 256, 0, s>>>(a, lists, bcnt, too_wide);
+        mcf::note_launch();
+        MCF_LAUNCHED("k_unit_classify");
+    }
+    unsigned long long hw = 0;
+    MCF_CUDA(cudaMemcpyAsync(&hw, too_wide, sizeof(hw), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    if (hw) {
+        *fallback = true;
+        return MCF_OK;
+    }
+    rc = timed_begin(g, timed, g->ev_q, s);
+    if (rc) return rc;
+    rc = th == 1024 ? launch_units<1024, 16384, 8192>(a, grid, s) : launch_units<512, 8192, 4096>(a, grid, s);
+    if (rc) return rc;
+    rc = timed_end(timed, g->ev_q, s);
+    if (rc) return rc;
+    int herr = 0;
+    MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    unsigned long long hp[2 * UPROF_SLOTS];
+    if (a.prof) MCF_CUDA(cudaMemcpyAsync(hp, a.prof, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    unsigned hb[UNIT_BUCKETS];
+    if (a.prof) MCF_CUDA(cudaMemcpyAsync(hb, bcnt, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    if (a.prof) {
+        fprintf(stderr,
+                "[unit-prof] units %llu visits %llu queued %llu emissions %llu support %llu | cyc build %.3e pairs %.3e |"
+                " serial %llu ids %llu | pieces %llu pull ids %llu push tests %llu | cols by K:",
+                hp[0], hp[1], hp[2], hp[3], hp[4], (double)hp[5], (double)hp[6], hp[UPROF_SLOTS], hp[UPROF_SLOTS + 1],
+                hp[UPROF_SLOTS + 2], hp[UPROF_SLOTS + 3], hp[UPROF_SLOTS + 4]);
+        for (int k = 0; k < UNIT_BUCKETS; ++k) fprintf(stderr, " %u", hb[k]);
+        fprintf(stderr, "\n");
+    }
+    if (herr) {
+        set_error("diag combine: unit table or queue overflow (code " + std::to_string(herr) + ")");
+        return MCF_ERR_CUDA;
+    }
+    return MCF_OK;
+}
+
 static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre, long long cb,
                  long long ce, long long wb, long long slot_len, const long long *eoff, const long long *walk_off,
                  long long off_base, const int *est, const double *ewt, double *pcol,
                  long long max_slots_per_col, cudaStream_t s) {
+    {
+        // uniform-value graphs: the unit combine unless MCF_DIAG_UNITS=0
+        const char *e = getenv("MCF_DIAG_UNITS");
+        if (g->uniform_value && !(e && !strcmp(e, "0"))) {
+            bool fallback = false;
+            const int rc = run_units(timed, g, colmax, walk_pre, cb, ce, wb, slot_len, eoff, walk_off, off_base, est,
+                                     ewt, pcol, s, &fallback);
+            if (rc || !fallback) return rc;
+        }
+    }
     QArgs q;
     q.walk_pre = walk_pre;
     q.wb = wb;
@@ -1593,8 +2302,7 @@ __global__ void __launch_bounds__(512) k_qdense(const long long *__restrict__ wa
         for (long long i = threadIdx.x; i < m; i += blockDim.x) {
             const int s = est[s0 + i];
             if (s >= 0)
-                atomicAdd(reinterpret_cast<unsigned long long *>(&row[s]),
-                          (unsigned long long)__double2ll_rn(ldexp(ewt[s0 + i], E)));
+                smem_add_i64(&row[s], __double2ll_rn(ldexp(ewt[s0 + i], E)));
         }
         __syncthreads();
         if (trans) {  // Q^T: column (c - cb) of an n x (ce - cb) row-major block

@@ -513,6 +513,9 @@ static void release(mcf_graph *g) {
     if (g->rsum_by_deg) cudaFreeAsync(g->rsum_by_deg, 0);
     if (g->hub_of) cudaFreeAsync(g->hub_of, 0);
     if (g->hub_bits) cudaFreeAsync(g->hub_bits, 0);
+    if (g->ckeys) cudaFreeAsync(g->ckeys, 0);
+    if (g->gidx) cudaFreeAsync(g->gidx, 0);
+    if (g->gofs) cudaFreeAsync(g->gofs, 0);
     if (g->scratch) cudaFreeAsync(g->scratch, 0);
     // g->side is the per-device stream shared by all graphs: not destroyed here
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);

@@ -136,6 +136,14 @@ struct mcf_graph {
     unsigned *hub_bits = nullptr;    // n_hubs x hub_words
     long long hub_words = 0;
     bool hubs_ready = false;
+    // diag combine units (uniform-value graphs, built lazily): every CSC
+    // column's row ids reordered by (key_group(id), id), so the unit that owns
+    // a range of key groups finds its ids as one contiguous slice; columns
+    // longer than GROUP_OFS_MIN keep their NGROUPS + 1 slice offsets
+    int32_t *ckeys = nullptr;        // nnz
+    int32_t *gidx = nullptr;         // n: offset-table row of a long column, or -1
+    int32_t *gofs = nullptr;         // n_long x (NGROUPS + 1), relative to csc_ptr[c]
+    long long n_gofs = 0;
     bool uniform_value = false;      // all stored values equal `value` (0/1 graphs scaled by gamma)
     double value = 0.0;
     mcf_graph_info info{};
@@ -215,6 +223,24 @@ __device__ __forceinline__ NodeHdr load_hdr(const NodeHdr *h) {
     r.rsum = __hiloint2double(b.y, b.x);
     r.aux = __hiloint2double(b.w, b.z);
     return r;
+}
+
+// Key groups of the diag combine units: a node id's group is the top GROUP_BITS
+// bits of a full-avalanche hash (independent of the table slot and Bloom
+// hashes, which are multiplicative), so every group holds ~1/NGROUPS of any
+// support set.  A column split into K units gives unit u the groups
+// [u NGROUPS / K, (u + 1) NGROUPS / K).
+constexpr int GROUP_BITS = 7;
+constexpr int NGROUPS = 1 << GROUP_BITS;
+constexpr int GROUP_OFS_MIN = 32;  // columns longer than this keep their group slice offsets
+__device__ __forceinline__ uint32_t key_group(int key) {
+    uint32_t h = (uint32_t)key;  // lowbias32
+    h ^= h >> 16;
+    h *= 0x7feb352du;
+    h ^= h >> 15;
+    h *= 0x846ca68bu;
+    h ^= h >> 16;
+    return h >> (32 - GROUP_BITS);
 }
 
 // rows longer than this get a CTA each in SpMV (load balance on hub rows)
@@ -411,6 +437,7 @@ int build_blk_col(const long long *walk_pre, long long col_begin, long long col_
                   int **blk_col, cudaStream_t s);
 int ensure_csr2csc(mcf_graph *g, cudaStream_t s);
 int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s);
+int ensure_group_keys(mcf_graph *g, cudaStream_t s);
 int ensure_side_stream(mcf_graph *g);
 // r_ones/stats_zero (fused path only, see fused_alloc_applies): also write
 // r = A 1 into r_ones and the headers, and zero stats_zero[4]

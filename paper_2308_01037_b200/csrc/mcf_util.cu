@@ -336,7 +336,9 @@ int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s) {
     MCF_CUDA(cudaMallocAsync(&hist, sizeof(unsigned long long) * 64 + 16, s));
     MCF_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 64 + 16, s));
     const unsigned nb = (unsigned)((g->n + 255) / 256);
-    k_deg_hist<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->n, hist);
+    // C_i is column i of A: the bitmaps (and the hub degree) come from the CSC
+    // (== the CSR on symmetric graphs)
+    k_deg_hist<<<nb, 256, 0, s>>>((const long long *)g->csc_ptr, g->n, hist);
     mcf::note_launch();
     unsigned long long h[64];
     MCF_CUDA(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -358,14 +360,125 @@ int ensure_hub_bitmaps(mcf_graph *g, cudaStream_t s) {
     MCF_CUDA(cudaMallocAsync(&g->hub_bits, sizeof(unsigned) * words * above, s));
     MCF_CUDA(cudaMemsetAsync(g->hub_bits, 0, sizeof(unsigned) * words * above, s));
     unsigned *cnt = reinterpret_cast<unsigned *>(hist + 64);
-    k_mark_hubs<<<nb, 256, 0, s>>>((const long long *)g->row_ptr, g->n, 1ll << bsel, (int)above, g->hub_of, cnt);
+    k_mark_hubs<<<nb, 256, 0, s>>>((const long long *)g->csc_ptr, g->n, 1ll << bsel, (int)above, g->hub_of, cnt);
     mcf::note_launch();
-    k_hub_bits<<<sm_count() * 4, 256, 0, s>>>((const long long *)g->row_ptr, g->col_ids, g->hub_of, g->n, words,
+    k_hub_bits<<<sm_count() * 4, 256, 0, s>>>((const long long *)g->csc_ptr, g->csc_rows, g->hub_of, g->n, words,
                                             g->hub_bits);
     mcf::note_launch();
     MCF_LAUNCHED("hub bitmaps");
     g->hub_words = words;
     cudaFreeAsync(hist, s);
+    return MCF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Group-ordered CSC row ids for the diag combine units (mcf_diag.cu): column
+// c's ids reordered by (key_group(id), CSC position), a stable counting sort
+// by one warp per column; columns longer than GROUP_OFS_MIN also keep the
+// NGROUPS + 1 group slice offsets, so a unit owning a group range reads one
+// contiguous slice of every C_i it scans.
+// ---------------------------------------------------------------------------
+__global__ void k_mark_long_cols(const long long *__restrict__ csc_ptr, long long n, int *__restrict__ gidx,
+                                 unsigned *count) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    int o = -1;
+    if (csc_ptr[c + 1] - csc_ptr[c] > GROUP_OFS_MIN) o = (int)atomicAdd(count, 1u);
+    gidx[c] = o;
+}
+
+constexpr int GK_WARPS = 8;
+
+__global__ void __launch_bounds__(GK_WARPS * 32) k_group_keys(const long long *__restrict__ csc_ptr,
+                                                              const int *__restrict__ csc_rows, long long n,
+                                                              const int *__restrict__ gidx, int *__restrict__ gofs,
+                                                              int *__restrict__ ckeys) {
+    __shared__ int cnt[GK_WARPS][NGROUPS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int *wc = cnt[w];
+    for (long long c = (long long)blockIdx.x * GK_WARPS + w; c < n; c += (long long)gridDim.x * GK_WARPS) {
+        const long long lo = csc_ptr[c], hi = csc_ptr[c + 1], deg = hi - lo;
+        if (deg == 0) continue;
+        if (deg <= 32) {  // one chunk: rank = ids of smaller group + same group at lower lanes
+            const bool v = lane < deg;
+            const int j = v ? csc_rows[lo + lane] : 0;
+            const int gj = v ? (int)key_group(j) : NGROUPS;
+            int pos = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int gl = __shfl_sync(MCF_FULL, gj, l);
+                pos += (gl < gj) || (gl == gj && l < lane);
+            }
+            if (v) ckeys[lo + pos] = j;
+            continue;  // deg <= GROUP_OFS_MIN: no offsets
+        }
+        for (int k = lane; k < NGROUPS; k += 32) wc[k] = 0;
+        __syncwarp();
+        for (long long e = lo + lane; e < hi; e += 32) atomicAdd(&wc[key_group(csc_rows[e])], 1);
+        __syncwarp();
+        // exclusive scan of the NGROUPS counts (NGROUPS / 32 per lane)
+        constexpr int PER = NGROUPS / 32;
+        int v[PER], s = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            v[k] = wc[lane * PER + k];
+            s += v[k];
+        }
+        int inc = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(MCF_FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        int run = inc - s;
+        const int o = gidx[c];
+        int *of = o >= 0 ? gofs + (long long)o * (NGROUPS + 1) : nullptr;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            wc[lane * PER + k] = run;
+            if (of) of[lane * PER + k] = run;
+            run += v[k];
+        }
+        if (of && lane == 31) of[NGROUPS] = run;
+        __syncwarp();
+        // stable scatter, chunk by chunk in CSC order
+        for (long long e0 = lo; e0 < hi; e0 += 32) {
+            const long long e = e0 + lane;
+            const bool ok = e < hi;
+            const int j = ok ? csc_rows[e] : 0;
+            const int gj = ok ? (int)key_group(j) : NGROUPS + lane;  // invalid lanes: unique dummy groups
+            const unsigned same = __match_any_sync(MCF_FULL, gj);
+            const int rank = __popc(same & lanemask_lt());
+            const int base = ok ? wc[gj] : 0;
+            __syncwarp();
+            if (ok && rank == 0) wc[gj] += __popc(same);
+            __syncwarp();
+            if (ok) ckeys[lo + base + rank] = j;
+        }
+        __syncwarp();
+    }
+}
+
+int ensure_group_keys(mcf_graph *g, cudaStream_t s) {
+    if (g->ckeys) return MCF_OK;
+    MCF_CUDA(cudaMallocAsync(&g->gidx, sizeof(int) * (g->n > 0 ? g->n : 1), s));
+    unsigned *cnt = nullptr;
+    MCF_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned), s));
+    MCF_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s));
+    k_mark_long_cols<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>((const long long *)g->csc_ptr, g->n, g->gidx, cnt);
+    mcf::note_launch();
+    unsigned nl = 0;
+    MCF_CUDA(cudaMemcpyAsync(&nl, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaStreamSynchronize(s));
+    cudaFreeAsync(cnt, s);
+    g->n_gofs = nl;
+    MCF_CUDA(cudaMallocAsync(&g->gofs, sizeof(int) * (size_t)(nl > 0 ? nl : 1) * (NGROUPS + 1), s));
+    MCF_CUDA(cudaMallocAsync(&g->ckeys, sizeof(int) * (size_t)(g->nnz > 0 ? g->nnz : 1), s));
+    const long long blocks = (g->n + GK_WARPS - 1) / GK_WARPS;
+    k_group_keys<<<(unsigned)(blocks < 65536 ? blocks : 65536), GK_WARPS * 32, 0, s>>>(
+        (const long long *)g->csc_ptr, g->csc_rows, g->n, g->gidx, g->gofs, g->ckeys);
+    mcf::note_launch();
+    MCF_LAUNCHED("k_group_keys");
     return MCF_OK;
 }
 

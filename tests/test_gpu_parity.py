@@ -457,6 +457,7 @@ def test_diag_cluster_tables_bitwise(mc):
     g = mc.DeviceGraph(as_matrix(a, True))
     cfg = mc.WalkConfig(a.n * 120, 1e-300, 20, 5)
     outs = {}
+    os.environ["MCF_DIAG_UNITS"] = "0"
     try:
         for k in ("0", "2", "4", "8"):
             # BIG_WORK 4096: most hub columns handed to k_diag_big; LONG_WORK 16:
@@ -475,6 +476,21 @@ def test_diag_cluster_tables_bitwise(mc):
         os.environ.pop("MCF_DIAG_BIG_WORK", None)
         os.environ.pop("MCF_DIAG_LONG_WORK", None)
         os.environ.pop("MCF_DIAG_LONG_WORK_Q", None)
+        os.environ.pop("MCF_DIAG_UNITS", None)
+    # the default combine (units: tables split by key group, every probe local)
+    # with its natural splits, with every column split into up to 128 units,
+    # and with tiny pieces of the queued entries
+    try:
+        for need, chunk in ((None, None), ("64", None), ("700", "32")):
+            for var, val in (("MCF_UNIT_SMALL_NEED", need), ("MCF_UNIT_CHUNK", chunk)):
+                if val:
+                    os.environ[var] = val
+                else:
+                    os.environ.pop(var, None)
+            outs["units", need, chunk] = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+    finally:
+        os.environ.pop("MCF_UNIT_SMALL_NEED", None)
+        os.environ.pop("MCF_UNIT_CHUNK", None)
     ref = outs["0", None, None]
     for key, v in outs.items():
         assert np.array_equal(v, ref), key
