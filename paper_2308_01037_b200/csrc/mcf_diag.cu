@@ -1273,12 +1273,53 @@ __device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, in
     }
 }
 
+// The unit kernel's table in shared memory, addressed by 32-bit shared
+// addresses (no generic-pointer conversions in the probe loops): keys (int),
+// values (int64) and a one-word-per-key Bloom filter (three bits of one
+// 32-bit word: one shared load answers most misses).
+struct UTab {
+    unsigned keys, vals, filt;  // shared-window byte addresses
+    uint32_t mask;              // hash table: slots - 1
+    bool dense;                 // values indexed by node id (small graphs), no keys
+};
+__device__ __forceinline__ unsigned lds32(unsigned addr) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ long long lds64(unsigned addr) {
+    long long v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ bool utab_maybe(const UTab &t, int key) {
+    const uint32_t m = filter_block_mask(key);
+    return (lds32(t.filt + 4 * filter_block_word(key)) & m) == m;
+}
+__device__ __forceinline__ long long utab_get(const UTab &t, int key) {
+    if (t.dense) return lds64(t.vals + 8u * (unsigned)key);
+    uint32_t s = hash_slot(key, t.mask);
+    while (true) {
+        const int k = (int)lds32(t.keys + 4 * s);
+        if (k == key) return lds64(t.vals + 8 * s);
+        if (k == EMPTY_KEY) return 0;
+        s = (s + 1) & t.mask;
+    }
+}
+// jv[u] for a lane-varying u < 8 without local memory (a select tree)
+__device__ __forceinline__ int sel8(const int (&v)[8], int u) {
+    const int a0 = (u & 1) ? v[1] : v[0], a1 = (u & 1) ? v[3] : v[2];
+    const int a2 = (u & 1) ? v[5] : v[4], a3 = (u & 1) ? v[7] : v[6];
+    const int b0 = (u & 2) ? a1 : a0, b1 = (u & 2) ? a3 : a2;
+    return (u & 4) ? b1 : b0;
+}
+
 // sum of Q_c over the ids ckeys[lo, hi) (warp-cooperative, PULL_U ids per
 // lane in flight) or over the unit's support positions [lo, hi) tested
 // against hub row i's bitmap (push)
-__device__ __forceinline__ long long unit_scan(const UArgs &a, const int *keys, const long long *vals, uint32_t mask,
-                                               const unsigned *filt, const int *lkeys, const long long *lvals,
-                                               int i, bool push, long long lo, long long hi, int lane) {
+__device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, const int *lkeys,
+                                               const long long *lvals, int i, bool push, long long lo, long long hi,
+                                               int lane) {
     long long acc = 0;
     if (push) {
         const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
@@ -1298,17 +1339,28 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const int *keys, 
                 if ((wv[u] >> (kv[u] & 31)) & 1u) acc += lvals[t0 + 32 * u + lane];
         }
     } else {
+        // 8 ids per lane in flight; the Bloom-passing ones (bit mask) are then
+        // probed one after another, so a warp runs the probe code max-over-
+        // lanes-of-passes times instead of once per id slot
         constexpr int PULL_U = 8;
-        for (long long e0 = lo; e0 < hi; e0 += 32 * PULL_U) {
+        const int *ids = a.ckeys + lo;
+        const int len = (int)(hi - lo);
+        for (int e0 = 0; e0 < len; e0 += 32 * PULL_U) {
             int jv[PULL_U];
 #pragma unroll
             for (int u = 0; u < PULL_U; ++u) {
-                const long long e = e0 + 32 * u + lane;
-                jv[u] = e < hi ? __ldg(a.ckeys + e) : -1;
+                const int e = e0 + 32 * u + lane;
+                jv[u] = e < len ? __ldg(ids + e) : -1;
             }
+            unsigned pm = 0;
 #pragma unroll
             for (int u = 0; u < PULL_U; ++u)
-                if (jv[u] >= 0 && filter_test(filt, jv[u])) acc += lookup(keys, vals, mask, jv[u]);
+                if (jv[u] >= 0 && utab_maybe(tab, jv[u])) pm |= 1u << u;
+            while (pm) {
+                const int u = __ffs(pm) - 1;
+                pm &= pm - 1;
+                acc += utab_get(tab, sel8(jv, u));
+            }
         }
     }
     return warp_sum_ll(acc);
@@ -1407,6 +1459,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
             // 32 walks share the start state at step 0 and hubs later on)
 #pragma unroll
             for (int q = 0; q < U; ++q) {
+                if (!__any_sync(MCF_FULL, sv[q] >= 0)) continue;  // no key of this unit in the warp's slot
                 long long qv = sv[q] >= 0 ? __double2ll_rn(ldexp(wv[q], E)) : 0;
                 const unsigned same = __match_any_sync(MCF_FULL, sv[q]);
                 if (sv[q] < 0) continue;
@@ -1423,7 +1476,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         for (uint32_t t = tid; t < cap; t += TH) {
             const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
             if (key != EMPTY_KEY) {
-                filter_add(filt, key);
+                filter_add(filt, key, true);
                 const int p = atomicAdd(&s_nsupp, 1);
                 if (p < a.lcap) {
                     lkeys[p] = key;
@@ -1435,6 +1488,8 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
         const long long t_built = a.prof ? clock64() : 0;
         const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
+                       (unsigned)__cvta_generic_to_shared(filt), mask, dense};
         const double scale = a.value;
         // phase A: 32 entries per warp-step
         while (true) {
@@ -1476,7 +1531,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
                     for (int q = 0; q < 4; ++q) {
                         if (jv[q] < 0) continue;
                         if (grp_filter && (int)(key_group(jv[q]) >> shift) != u) continue;
-                        if (filter_test(filt, jv[q])) acc += lookup(keys, vals, mask, jv[q]);
+                        if (utab_maybe(tab, jv[q])) acc += utab_get(tab, jv[q]);
                     }
                 }
                 if (a.prof) {
@@ -1570,7 +1625,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
             const long long b = qlo[j] + p * a.chunk;
             const long long e = qlo[j] + (len < (p + 1) * a.chunk ? len : (p + 1) * a.chunk);
             const int i = push ? __ldg(a.csc_rows + cs + t) : 0;
-            const long long acc = unit_scan(a, keys, vals, mask, filt, lkeys, lvals, i, push, b, e, lane);
+            const long long acc = unit_scan(a, tab, lkeys, lvals, i, push, b, e, lane);
             if (a.prof && lane == 0) {
                 pr[2] += 1;
                 pr[push ? 4 : 3] += (unsigned long long)(e - b);
