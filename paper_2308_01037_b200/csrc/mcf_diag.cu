@@ -1187,6 +1187,12 @@ struct UArgs {
     int dense_n;           // n at or below which a one-unit column may use a dense Q_c
     int *err;              // bit 8: a unit table overflowed
     unsigned long long *prof;
+    // emissions of the split columns regrouped by unit (k_unit_partition), or
+    // null: then every unit scans the whole column and keeps its groups
+    int *pest;
+    double *pewt;
+    int *pofs;                          // per split column: K + 1 unit offsets (relative to its first slot)
+    long long pbase[UNIT_BUCKETS];      // bucket k's first offset row in pofs
 };
 
 __device__ __forceinline__ long long uslot(const UArgs &a, long long g) {
@@ -1246,6 +1252,93 @@ __global__ void k_unit_classify(UArgs a, int *__restrict__ lists, unsigned *__re
             const long long cc = a.c0 + base + l;
             const long long lo = a.csc_ptr[cc], hi = a.csc_ptr[cc + 1];
             for (long long e = lo + lane; e < hi; e += 32) a.pcol[e] = 0.0;
+        }
+    }
+}
+
+// Emissions of every split column (K >= 2) regrouped by unit: unit u's
+// emissions land in [s0 + pofs[u], s0 + pofs[u + 1]) of pest/pewt (order
+// inside a unit is arbitrary: Q_c sums are integers).  One CTA per column,
+// widest first; a counting pass, a scan, a scatter pass.
+constexpr int PART_TH = 512;
+__global__ void __launch_bounds__(PART_TH) k_unit_partition(UArgs a, unsigned *__restrict__ next) {
+    __shared__ int cnt[NGROUPS];
+    __shared__ long long s_c;
+    __shared__ int s_k, s_sidx;
+    const int tid = threadIdx.x, lane = tid & 31;
+    while (true) {
+        __syncthreads();
+        if (tid == 0) {
+            unsigned x = atomicAdd(next, 1u);
+            int k = UNIT_BUCKETS - 1;
+            for (; k >= 1; --k) {
+                const unsigned nb = __ldcg(a.bcnt + k);
+                if (x < nb) break;
+                x -= nb;
+            }
+            s_k = k;
+            s_sidx = (int)x;
+            s_c = k >= 1 ? (long long)a.lists[k * a.ncol + x] : -1;
+        }
+        __syncthreads();
+        const long long c = s_c;
+        if (c < 0) break;
+        const int k = s_k, K = 1 << k, shift = GROUP_BITS - k;
+        const long long s0 = uslot(a, a.walk_pre[c]), m = uslot(a, a.walk_pre[c + 1]) - s0;
+        for (int t = tid; t < K; t += PART_TH) cnt[t] = 0;
+        __syncthreads();
+        // warp-aggregated per-unit counts (hot keys share a unit)
+        for (long long b = 0; b < m; b += 4 * PART_TH) {
+            int st[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long i = b + q * PART_TH + tid;
+                st[q] = i < m ? __ldcs(a.est + s0 + i) : -1;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int uq = st[q] >= 0 ? (int)(key_group(st[q]) >> shift) : -1;
+                const unsigned same = __match_any_sync(MCF_FULL, uq);
+                if (uq >= 0 && lane == __ffs(same) - 1) atomicAdd(&cnt[uq], __popc(same));
+            }
+        }
+        __syncthreads();
+        int *of = a.pofs + a.pbase[k] + (long long)s_sidx * (K + 1);
+        if (tid == 0) {
+            int run = 0;
+            for (int t = 0; t < K; ++t) {
+                const int v = cnt[t];
+                of[t] = run;
+                cnt[t] = run;
+                run += v;
+            }
+            of[K] = run;
+        }
+        __syncthreads();
+        for (long long b = 0; b < m; b += 4 * PART_TH) {
+            int st[4];
+            double wt[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long i = b + q * PART_TH + tid;
+                st[q] = i < m ? __ldcs(a.est + s0 + i) : -1;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) wt[q] = st[q] >= 0 ? __ldcs(a.ewt + s0 + b + q * PART_TH + tid) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int uq = st[q] >= 0 ? (int)(key_group(st[q]) >> shift) : -1;
+                const unsigned same = __match_any_sync(MCF_FULL, uq);
+                const int leader = __ffs(same) - 1;
+                int p0 = 0;
+                if (uq >= 0 && lane == leader) p0 = atomicAdd(&cnt[uq], __popc(same));
+                p0 = __shfl_sync(MCF_FULL, p0, leader);
+                if (uq >= 0) {
+                    const long long p = s0 + p0 + __popc(same & lanemask_lt());
+                    a.pest[p] = st[q];
+                    a.pewt[p] = wt[q];
+                }
+            }
         }
     }
 }
@@ -1405,6 +1498,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
             s_c = c;
             s_u = u;
             s_lg = lg;
+            s_sidx = sidx;
             s_next = 0;
             s_nq = 0;
             s_nsupp = 0;
@@ -1419,11 +1513,24 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         const long long s0 = uslot(a, g0), m = uslot(a, g1) - s0;
         const long long need = m < a.n ? m : a.n;
         const long long t_start = a.prof ? clock64() : 0;
+        // this unit's emissions: the whole column (filtered by group below), or
+        // its regrouped slice [s0 + e0, s0 + e1) of pest / pewt
+        const bool parted = K > 1 && a.pest;
+        long long e0 = 0, e1 = m;
+        if (parted) {
+            const int *of = a.pofs + a.pbase[lg] + (long long)s_sidx * (K + 1) + u;
+            e0 = of[0];
+            e1 = of[1];
+        }
+        const int *__restrict__ est = parted ? a.pest : a.est;
+        const double *__restrict__ ewt = parted ? a.pewt : a.ewt;
         // table: one unit -> sized by need (k_diag_q's rule); K units -> need / K
-        // plus a 1/8 + 64 margin for the group's share of the support
+        // plus a 1/8 + 64 margin for the group's share of the support (and at
+        // most the unit's emission count when known)
         const bool dense = K == 1 && a.n <= a.dense_n && need * 4 > a.n;
         long long need_u = K == 1 ? need : need / K + need / (8 * K) + 64;
         if (need_u > need) need_u = need;
+        if (parted && need_u > e1 - e0) need_u = e1 - e0;
         uint32_t cap = 32;
         while ((long long)cap < need_u * 2 && cap < (uint32_t)CAP) cap <<= 1;
         while ((long long)cap * 3 < need_u * 4 + 4 && cap < (uint32_t)CAP) cap <<= 1;
@@ -1444,17 +1551,21 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // as k_diag_q: sum of m terms < 2^62
         // Q_c over this unit's key groups
         constexpr int U = 4;
-        for (long long base = 0; base < m; base += (long long)U * TH) {
+        for (long long base = e0; base < e1; base += (long long)U * TH) {
             int sv[U];
 #pragma unroll
-            for (int q = 0; q < U; ++q) {
+            for (int q = 0; q < U; ++q) {  // all U loads issued before any is used
                 const long long i = base + (long long)q * TH + tid;
-                sv[q] = i < m ? __ldcs(a.est + s0 + i) : EMPTY_KEY;
-                if (K > 1 && sv[q] >= 0 && (int)(key_group(sv[q]) >> shift) != u) sv[q] = EMPTY_KEY;
+                sv[q] = i < e1 ? __ldcs(est + s0 + i) : EMPTY_KEY;
+            }
+            if (K > 1 && !parted) {
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (sv[q] >= 0 && (int)(key_group(sv[q]) >> shift) != u) sv[q] = EMPTY_KEY;
             }
             double wv[U];
 #pragma unroll
-            for (int q = 0; q < U; ++q) wv[q] = sv[q] >= 0 ? __ldcs(a.ewt + s0 + base + (long long)q * TH + tid) : 0.0;
+            for (int q = 0; q < U; ++q) wv[q] = sv[q] >= 0 ? __ldcs(ewt + s0 + base + (long long)q * TH + tid) : 0.0;
             // lanes holding the same key add once (step-major slots: a warp's
             // 32 walks share the start state at step 0 and hubs later on)
 #pragma unroll
@@ -1672,6 +1783,8 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
             atomicAdd(a.prof + 5, (unsigned long long)(t_built - t_start));
             atomicAdd(a.prof + 6, (unsigned long long)(t_end - t_built));
             atomicAdd(a.prof + 7 + (lg < 8 ? lg : 7), 1ull);
+            atomicAdd(a.prof + 2 * UPROF_SLOTS + (lg < 8 ? lg : 7), (unsigned long long)(t_end - t_start));
+            atomicAdd(a.prof + 2 * UPROF_SLOTS + 8 + (lg < 8 ? lg : 7), (unsigned long long)(t_built - t_start));
         }
     }
     if (a.prof) {
@@ -1748,7 +1861,7 @@ static int launch_units(UArgs &a, int grid, cudaStream_t s) {
 static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre,
                      long long cb, long long ce, long long wb, long long slot_len, const long long *eoff,
                      const long long *walk_off, long long off_base, const int *est, const double *ewt, double *pcol,
-                     cudaStream_t s, bool *fallback) {
+                     int *pest, double *pewt, cudaStream_t s, bool *fallback) {
     *fallback = false;
     const long long ncol = ce - cb;
     if (ncol <= 0) return MCF_OK;
@@ -1805,7 +1918,7 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     const int grid = sm_count() * (th == 1024 ? 1 : 2);
     // small device block: bucket counts, work counter, too-wide need, error bits, profile
     unsigned char *blk = nullptr;
-    const size_t blk_bytes = 256 + sizeof(unsigned long long) * 2 * UPROF_SLOTS;
+    const size_t blk_bytes = 256 + sizeof(unsigned long long) * 3 * UPROF_SLOTS;
     MCF_CUDA(cudaMallocAsync(&blk, blk_bytes, s));
     frees.keep(blk);
     MCF_CUDA(cudaMemsetAsync(blk, 0, blk_bytes, s));
@@ -1857,11 +1970,34 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
         MCF_LAUNCHED("k_unit_classify");
     }
     unsigned long long hw = 0;
+    unsigned hbc[UNIT_BUCKETS];
     MCF_CUDA(cudaMemcpyAsync(&hw, too_wide, sizeof(hw), cudaMemcpyDeviceToHost, s));
+    MCF_CUDA(cudaMemcpyAsync(hbc, bcnt, sizeof(hbc), cudaMemcpyDeviceToHost, s));
     MCF_CUDA(cudaStreamSynchronize(s));
     if (hw) {
         *fallback = true;
         return MCF_OK;
+    }
+    // regroup the split columns' emissions by unit (when the second buffer exists)
+    long long npofs = 0, nsplit = 0;
+    for (int k = 0; k < UNIT_BUCKETS; ++k) {
+        a.pbase[k] = npofs;
+        if (k >= 1) {
+            npofs += (long long)hbc[k] * ((1ll << k) + 1);
+            nsplit += hbc[k];
+        }
+    }
+    a.pest = nullptr;
+    a.pewt = nullptr;
+    a.pofs = nullptr;
+    if (pest && pewt && nsplit > 0) {
+        MCF_CUDA(cudaMallocAsync(&a.pofs, sizeof(int) * (size_t)npofs, s));
+        frees.keep(a.pofs);
+        a.pest = pest;
+        a.pewt = pewt;
+        k_unit_partition<<<sm_count() * 4, PART_TH, 0, s>>>(a, reinterpret_cast<unsigned *>(blk + 128));
+        mcf::note_launch();
+        MCF_LAUNCHED("k_unit_partition");
     }
     rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
@@ -1871,7 +2007,7 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     if (rc) return rc;
     int herr = 0;
     MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    unsigned long long hp[2 * UPROF_SLOTS];
+    unsigned long long hp[3 * UPROF_SLOTS];
     if (a.prof) MCF_CUDA(cudaMemcpyAsync(hp, a.prof, sizeof(hp), cudaMemcpyDeviceToHost, s));
     unsigned hb[UNIT_BUCKETS];
     if (a.prof) MCF_CUDA(cudaMemcpyAsync(hb, bcnt, sizeof(hb), cudaMemcpyDeviceToHost, s));
@@ -1883,6 +2019,10 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
                 hp[0], hp[1], hp[2], hp[3], hp[4], (double)hp[5], (double)hp[6], hp[UPROF_SLOTS], hp[UPROF_SLOTS + 1],
                 hp[UPROF_SLOTS + 2], hp[UPROF_SLOTS + 3], hp[UPROF_SLOTS + 4]);
         for (int k = 0; k < UNIT_BUCKETS; ++k) fprintf(stderr, " %u", hb[k]);
+        fprintf(stderr, " | cycles by K:");
+        for (int k = 0; k < UNIT_BUCKETS; ++k) fprintf(stderr, " %.3e", (double)hp[2 * UPROF_SLOTS + k]);
+        fprintf(stderr, " | build cycles by K:");
+        for (int k = 0; k < UNIT_BUCKETS; ++k) fprintf(stderr, " %.3e", (double)hp[2 * UPROF_SLOTS + 8 + k]);
         fprintf(stderr, "\n");
     }
     if (herr) {
@@ -1895,14 +2035,14 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
 static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre, long long cb,
                  long long ce, long long wb, long long slot_len, const long long *eoff, const long long *walk_off,
                  long long off_base, const int *est, const double *ewt, double *pcol,
-                 long long max_slots_per_col, cudaStream_t s) {
+                 long long max_slots_per_col, cudaStream_t s, int *pest = nullptr, double *pewt = nullptr) {
     {
         // uniform-value graphs: the unit combine unless MCF_DIAG_UNITS=0
         const char *e = getenv("MCF_DIAG_UNITS");
         if (g->uniform_value && !(e && !strcmp(e, "0"))) {
             bool fallback = false;
             const int rc = run_units(timed, g, colmax, walk_pre, cb, ce, wb, slot_len, eoff, walk_off, off_base, est,
-                                     ewt, pcol, s, &fallback);
+                                     ewt, pcol, pest, pewt, s, &fallback);
             if (rc || !fallback) return rc;
         }
     }
@@ -2192,6 +2332,27 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
     return MCF_OK;
 }
 
+// second emission buffer for the unit combine's regrouped split columns
+// (uniform-value graphs, MCF_DIAG_UNITS / MCF_UNIT_PARTITION not "0");
+// an allocation failure leaves both null (units then filter by group)
+static void alloc_regroup(const mcf_graph *g, long long slots, int **pest, double **pewt, cudaStream_t s) {
+    *pest = nullptr;
+    *pewt = nullptr;
+    const char *e = getenv("MCF_DIAG_UNITS"), *e2 = getenv("MCF_UNIT_PARTITION");
+    if (!g->uniform_value || (e && !strcmp(e, "0")) || (e2 && !strcmp(e2, "0")) || slots <= 0) return;
+    if (cudaMallocAsync(pest, sizeof(int) * slots, s) != cudaSuccess) {
+        cudaGetLastError();
+        *pest = nullptr;
+        return;
+    }
+    if (cudaMallocAsync(pewt, sizeof(double) * slots, s) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeAsync(*pest, s);
+        *pest = nullptr;
+        *pewt = nullptr;
+    }
+}
+
 static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                 const long long *walk_off, const int *entries, double *pcol, long long *stats, cudaStream_t s,
                 bool replay) {
@@ -2245,8 +2406,14 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         rc = launch_walk_emit(g, p, walk_pre, cb, ce, we - wb, EMIT_REPLAY, walk_off, entries, 0, hoff[0], nullptr, est,
                               ewt, colmax, stats, err, s);
         if (rc) return rc;
+        int *pest = nullptr;
+        double *pewt = nullptr;
+        alloc_regroup(g, slots, &pest, &pewt, s);
+        frees.keep(pest);
+        frees.keep(pewt);
         // table size is bounded by min(slots, n) per column
-        rc = run_q(timed, g, colmax, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s);
+        rc = run_q(timed, g, colmax, walk_pre, cb, ce, wb, 0, nullptr, walk_off, hoff[0], est, ewt, pcol, slots, s, pest,
+                   pewt);
         if (rc) return rc;
         int herr = 0;
         MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2270,6 +2437,10 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
             return cuda_status(e_, "cudaMallocAsync(ewt)");
         }
     }
+    int *pest = nullptr;
+    double *pewt = nullptr;
+    alloc_regroup(g, buf_slots, &pest, &pewt, s);
+    long long pslots = pest ? buf_slots : 0;
     for (size_t b = 0; b + 1 < hb.size(); ++b) {
         const long long c0 = hb[b], c1 = hb[b + 1];
         long long bw0 = 0, bw1 = 0;
@@ -2281,7 +2452,7 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
                                   ewt, colmax, stats, err, s);
             if (rc) break;
             rc = run_q(timed, g, colmax, walk_pre, c0, c1, bw0, L, nullptr, nullptr, 0, est, ewt, pcol,
-                       (long long)hmax * L, s);
+                       (long long)hmax * L, s, pest, pewt);
             if (rc) break;
             continue;
         }
@@ -2324,11 +2495,20 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
         rc = launch_walk_emit(g, p, walk_pre, c0, c1, nwb, EMIT_EXPLICIT, nullptr, nullptr, 0, 0, eoff, est, ewt,
                               colmax, stats, err, s);
         if (rc) break;
-        rc = run_q(timed, g, colmax, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s);
+        if (pest && total > pslots) {  // the regroup buffer follows the emission buffer's size
+            cudaFreeAsync(pest, s);
+            cudaFreeAsync(pewt, s);
+            alloc_regroup(g, total, &pest, &pewt, s);
+            pslots = pest ? total : 0;
+        }
+        rc = run_q(timed, g, colmax, walk_pre, c0, c1, bw0, 0, eoff, nullptr, 0, est, ewt, pcol, total, s,
+                   pest && total <= pslots ? pest : nullptr, pest && total <= pslots ? pewt : nullptr);
         if (rc) break;
     }
     if (est) cudaFreeAsync(est, s);
     if (ewt) cudaFreeAsync(ewt, s);
+    if (pest) cudaFreeAsync(pest, s);
+    if (pewt) cudaFreeAsync(pewt, s);
     return rc;
 }
 

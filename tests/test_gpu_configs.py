@@ -170,7 +170,7 @@ def test_config3_multibatch_and_pool_fallback_bitwise(monkeypatch):
     wc = mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"], 0)
     ref = mc.rand_funm_diag(g, mc.EXPONENTIAL, wc, as_tensor=True)
     assert ref.emissions > 1.8e10
-    for env in ({"MCF_EMISSION_SLOTS": str(1 << 28)}, {"MCF_DIAG_UNITS": "0"},
+    for env in ({"MCF_EMISSION_SLOTS": str(1 << 28)}, {"MCF_UNIT_PARTITION": "0"}, {"MCF_DIAG_UNITS": "0"},
                 {"MCF_DIAG_UNITS": "0", "MCF_DIAG_POOL": "0"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)

@@ -481,16 +481,17 @@ def test_diag_cluster_tables_bitwise(mc):
     # with its natural splits, with every column split into up to 128 units,
     # and with tiny pieces of the queued entries
     try:
-        for need, chunk in ((None, None), ("64", None), ("700", "32")):
-            for var, val in (("MCF_UNIT_SMALL_NEED", need), ("MCF_UNIT_CHUNK", chunk)):
+        for need, chunk, part in ((None, None, None), ("64", None, None), ("700", "32", None), ("64", None, "0")):
+            for var, val in (("MCF_UNIT_SMALL_NEED", need), ("MCF_UNIT_CHUNK", chunk), ("MCF_UNIT_PARTITION", part)):
                 if val:
                     os.environ[var] = val
                 else:
                     os.environ.pop(var, None)
-            outs["units", need, chunk] = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+            outs["units", need, chunk, part] = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
     finally:
         os.environ.pop("MCF_UNIT_SMALL_NEED", None)
         os.environ.pop("MCF_UNIT_CHUNK", None)
+        os.environ.pop("MCF_UNIT_PARTITION", None)
     ref = outs["0", None, None]
     for key, v in outs.items():
         assert np.array_equal(v, ref), key
