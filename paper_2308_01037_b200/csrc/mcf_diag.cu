@@ -1445,10 +1445,14 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
                 const int e = e0 + 32 * u + lane;
                 jv[u] = e < len ? __ldg(ids + e) : -1;
             }
+            // branch-free Bloom stage: the PULL_U filter words load together
             unsigned pm = 0;
 #pragma unroll
-            for (int u = 0; u < PULL_U; ++u)
-                if (jv[u] >= 0 && utab_maybe(tab, jv[u])) pm |= 1u << u;
+            for (int u = 0; u < PULL_U; ++u) {
+                const uint32_t fm = filter_block_mask(jv[u]);
+                const unsigned w = lds32(tab.filt + 4 * filter_block_word(jv[u]));
+                pm |= (unsigned)(((w & fm) == fm) & (jv[u] >= 0)) << u;
+            }
             while (pm) {
                 const int u = __ffs(pm) - 1;
                 pm &= pm - 1;
@@ -1457,6 +1461,62 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
         }
     }
     return warp_sum_ll(acc);
+}
+
+// A unit and what its CTA needs to start it.  Thread 0 fetches the NEXT unit
+// (work counter, bucket lists, walk prefix, slice offsets, column pointers)
+// while the current one is combined, and asks the copy engine to pull its
+// emission slice into L2.
+struct UnitRec {
+    long long c, s0, m, e0, e1, cs, cn;
+    unsigned long long maxw;
+    int u, lg, sidx;
+};
+
+__device__ __forceinline__ void l2_prefetch_range(const void *p, long long bytes) {
+    const char *b = reinterpret_cast<const char *>((reinterpret_cast<uintptr_t>(p)) & ~(uintptr_t)15);
+    long long len = bytes + (reinterpret_cast<const char *>(p) - b);
+    if (len > (1ll << 20)) len = 1ll << 20;  // the first MiB: the rest streams in behind the reads
+    for (long long o = 0; o < len; o += 32768) {
+        const unsigned n = (unsigned)(((len - o < 32768 ? len - o : 32768) + 15) & ~15ll);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b + o), "r"(n) : "memory");
+    }
+}
+
+__device__ __forceinline__ void unit_fetch(const UArgs &a, const unsigned *sbc, UnitRec &r) {
+    unsigned long long x = atomicAdd(a.counter, 1ull);
+    r.c = -1;
+    for (int k = UNIT_BUCKETS - 1; k >= 0; --k) {  // widest columns first
+        const unsigned long long nu = (unsigned long long)sbc[k] << k;
+        if (x < nu) {
+            r.sidx = (int)(x >> k);
+            r.c = a.lists[k * a.ncol + r.sidx];
+            r.u = (int)(x & ((1ull << k) - 1));
+            r.lg = k;
+            break;
+        }
+        x -= nu;
+    }
+    if (r.c < 0) return;
+    const long long c = r.c;
+    const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
+    r.s0 = uslot(a, g0);
+    r.m = uslot(a, g1) - r.s0;
+    r.cs = a.csc_ptr[c];
+    r.cn = a.csc_ptr[c + 1] - r.cs;
+    r.maxw = a.colmax[c];
+    r.e0 = 0;
+    r.e1 = r.m;
+    const bool parted = r.lg > 0 && a.pest;
+    if (parted) {
+        const int *of = a.pofs + a.pbase[r.lg] + (long long)r.sidx * ((1 << r.lg) + 1) + r.u;
+        r.e0 = of[0];
+        r.e1 = of[1];
+    }
+    if (r.e1 > r.e0) {
+        l2_prefetch_range((parted ? a.pest : a.est) + r.s0 + r.e0, (r.e1 - r.e0) * 4);
+        l2_prefetch_range((parted ? a.pewt : a.ewt) + r.s0 + r.e0, (r.e1 - r.e0) * 8);
+    }
 }
 
 template <int TH, int CAP, int FW>
@@ -1477,28 +1537,20 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
     long long *qpre = a.qpre + (long long)blockIdx.x * (a.qcap + 1);
     int *pmap = a.pmap + (long long)blockIdx.x * a.pcap;
     unsigned long long pr[5] = {0, 0, 0, 0, 0};  // MCF_DIAG_PROF: serial entries, serial ids, pieces, pull ids, push tests
+    __shared__ unsigned s_bc[UNIT_BUCKETS];
+    __shared__ UnitRec s_cur, s_nxt;
+    if (tid < UNIT_BUCKETS) s_bc[tid] = __ldcg(a.bcnt + tid);
+    __syncthreads();
+    if (tid == 0) unit_fetch(a, s_bc, s_nxt);
 
     while (true) {
         __syncthreads();
         if (tid == 0) {
-            unsigned long long x = atomicAdd(a.counter, 1ull);
-            long long c = -1;
-            int u = 0, lg = 0, sidx = 0;
-            for (int k = UNIT_BUCKETS - 1; k >= 0; --k) {  // widest columns first
-                const unsigned long long nu = (unsigned long long)__ldcg(a.bcnt + k) << k;
-                if (x < nu) {
-                    sidx = (int)(x >> k);
-                    c = a.lists[k * a.ncol + sidx];
-                    u = (int)(x & ((1ull << k) - 1));
-                    lg = k;
-                    break;
-                }
-                x -= nu;
-            }
-            s_c = c;
-            s_u = u;
-            s_lg = lg;
-            s_sidx = sidx;
+            s_cur = s_nxt;
+            s_c = s_cur.c;
+            s_u = s_cur.u;
+            s_lg = s_cur.lg;
+            s_sidx = s_cur.sidx;
             s_next = 0;
             s_nq = 0;
             s_nsupp = 0;
@@ -1509,19 +1561,13 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         const long long c = s_c;
         if (c < 0) break;
         const int u = s_u, lg = s_lg, K = 1 << lg, shift = GROUP_BITS - lg;
-        const long long g0 = a.walk_pre[c], g1 = a.walk_pre[c + 1];
-        const long long s0 = uslot(a, g0), m = uslot(a, g1) - s0;
+        const long long s0 = s_cur.s0, m = s_cur.m;
         const long long need = m < a.n ? m : a.n;
         const long long t_start = a.prof ? clock64() : 0;
         // this unit's emissions: the whole column (filtered by group below), or
         // its regrouped slice [s0 + e0, s0 + e1) of pest / pewt
         const bool parted = K > 1 && a.pest;
-        long long e0 = 0, e1 = m;
-        if (parted) {
-            const int *of = a.pofs + a.pbase[lg] + (long long)s_sidx * (K + 1) + u;
-            e0 = of[0];
-            e1 = of[1];
-        }
+        const long long e0 = s_cur.e0, e1 = s_cur.e1;
         const int *__restrict__ est = parted ? a.pest : a.est;
         const double *__restrict__ ewt = parted ? a.pewt : a.ewt;
         // table: one unit -> sized by need (k_diag_q's rule); K units -> need / K
@@ -1545,7 +1591,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         }
         for (int t = tid; t < FW; t += TH) filt[t] = 0u;
         __syncthreads();
-        const double maxw = __longlong_as_double((long long)a.colmax[c]);
+        const double maxw = __longlong_as_double((long long)s_cur.maxw);
         int lg_m = 0;
         while ((1ll << lg_m) < m) ++lg_m;
         const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // as k_diag_q: sum of m terms < 2^62
@@ -1565,7 +1611,10 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
             }
             double wv[U];
 #pragma unroll
-            for (int q = 0; q < U; ++q) wv[q] = sv[q] >= 0 ? __ldcs(ewt + s0 + base + (long long)q * TH + tid) : 0.0;
+            for (int q = 0; q < U; ++q) {  // (unfiltered ranges: issued with the key loads, not after them)
+                const long long i = base + (long long)q * TH + tid;
+                wv[q] = (K == 1 || parted ? i < e1 : sv[q] >= 0) ? __ldcs(ewt + s0 + i) : 0.0;
+            }
             // lanes holding the same key add once (step-major slots: a warp's
             // 32 walks share the start state at step 0 and hubs later on)
 #pragma unroll
@@ -1598,7 +1647,8 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         __syncthreads();
         const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
         const long long t_built = a.prof ? clock64() : 0;
-        const long long cs = a.csc_ptr[c], cn = a.csc_ptr[c + 1] - cs;
+        const long long cs = s_cur.cs, cn = s_cur.cn;
+        if (tid == 0) unit_fetch(a, s_bc, s_nxt);  // the next unit, behind this one's entries
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
                        (unsigned)__cvta_generic_to_shared(filt), mask, dense};
         const double scale = a.value;
