@@ -124,6 +124,33 @@ def test_replay_matches_reference(mc, layout, name):
         assert out.walks == r["n_walks"]
 
 
+@pytest.mark.parametrize("name", golden_io.CASES)
+def test_unit_combine_replay_golden(mc, name, monkeypatch):
+    """The unit combine (the default above the dense-Q size) forced onto the
+    golden graphs: dense one-unit tables, hashed one-unit tables and columns
+    split into up to 128 key-group units all replay the reference's streams to
+    1e-10, bit-identical to the single-table combine."""
+    c = golden_io.load(name)
+    g = mc.DeviceGraph(as_matrix(c.sa, c.symmetric))
+    for j, r in enumerate(c.runs):
+        if r["mode"] != "diag":
+            continue
+        p = f"r{j}_"
+        cfg = mc.WalkConfig(r["n_walks"], r["cutoff"], r["max_steps"], r["seed"])
+        monkeypatch.setenv("MCF_DIAG_UNITS", "0")
+        ref = mc.rand_funm_diag(g, r["tag"], cfg, replay=c.record(j)).values
+        for env in ({"MCF_DIAG_UNITS": "1"}, {"MCF_DIAG_UNITS": "1", "MCF_UNIT_SMALL_NEED": "64"},
+                    {"MCF_DIAG_UNITS": "1", "MCF_UNIT_SMALL_NEED": "8", "MCF_UNIT_CHUNK": "32"},
+                    {"MCF_DIAG_UNITS": "1", "MCF_UNIT_SMALL_NEED": "64", "MCF_UNIT_PARTITION": "0"}):
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            out = mc.rand_funm_diag(g, r["tag"], cfg, replay=c.record(j))
+            for k in env:
+                monkeypatch.delenv(k)
+            assert rel_err(out.values, c[p + "d"]) < REL, env
+            assert np.array_equal(out.values, ref), env  # (weighted graphs: the single-table path both times)
+
+
 def test_replay_rejects_corrupt_stream(mc):
     c = golden_io.load("signed6")
     g = mc.DeviceGraph(as_matrix(c.sa))
