@@ -1183,6 +1183,8 @@ struct UArgs {
     long long pcap;
     long long chunk;
     long long small_need;  // widest table need of a one-unit column
+    long long small_cut;   // one-unit columns up to this need go to the small-table kernel (list UNIT_BUCKETS)
+    long long mid_cut;     // ... up to this one to the mid-size kernel (list UNIT_BUCKETS + 1)
     long long ucap;        // table need per unit of a split column
     int dense_n;           // n at or below which a one-unit column may use a dense Q_c
     int *err;              // bit 8: a unit table overflowed
@@ -1232,15 +1234,19 @@ __global__ void k_unit_classify(UArgs a, int *__restrict__ lists, unsigned *__re
                     atomicMax(too_wide, (unsigned long long)need);
                 } else {
                     b = 31 - __clz(K);
+                    if (K == 1 && !dense_ok && need <= a.small_cut) b = UNIT_BUCKETS;           // 4 tables per SM
+                    else if (K == 1 && !dense_ok && need <= a.mid_cut) b = UNIT_BUCKETS + 1;  // 2 tables per SM
                 }
                 a.done[base + lane] = 0;
             }
         }
-        for (int k = 0; k < UNIT_BUCKETS; ++k) {
+        for (int k = 0; k <= UNIT_BUCKETS + 1; ++k) {
             const unsigned msk = __ballot_sync(MCF_FULL, b == k);
             if (!msk) continue;
             unsigned p0 = 0;
-            if (lane == __ffs(msk) - 1) p0 = atomicAdd(bcnt + k, (unsigned)__popc(msk));
+            // counts: buckets 0..7 at [k]; the small / mid tiers at [16] / [24] (zeros after each)
+            const int ci = k < UNIT_BUCKETS ? k : 16 + 8 * (k - UNIT_BUCKETS);
+            if (lane == __ffs(msk) - 1) p0 = atomicAdd(bcnt + ci, (unsigned)__popc(msk));
             p0 = __shfl_sync(MCF_FULL, p0, __ffs(msk) - 1);
             if (b == k) lists[k * a.ncol + p0 + __popc(msk & lanemask_lt())] = (int)c;
         }
@@ -1374,7 +1380,9 @@ struct UTab {
     unsigned keys, vals, filt;  // shared-window byte addresses
     uint32_t mask;              // hash table: slots - 1
     bool dense;                 // values indexed by node id (small graphs), no keys
+    int fshift;                 // Bloom word of a key: (key * C) >> fshift (the kernel's 2^(32 - fshift) words)
 };
+__device__ __forceinline__ uint32_t ufilt_word(int key, int fshift) { return ((uint32_t)key * 0x85EBCA6Bu) >> fshift; }
 __device__ __forceinline__ unsigned lds32(unsigned addr) {
     unsigned v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -1387,7 +1395,7 @@ __device__ __forceinline__ long long lds64(unsigned addr) {
 }
 __device__ __forceinline__ bool utab_maybe(const UTab &t, int key) {
     const uint32_t m = filter_block_mask(key);
-    return (lds32(t.filt + 4 * filter_block_word(key)) & m) == m;
+    return (lds32(t.filt + 4 * ufilt_word(key, t.fshift)) & m) == m;
 }
 __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
     if (t.dense) return lds64(t.vals + 8u * (unsigned)key);
@@ -1450,7 +1458,7 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
 #pragma unroll
             for (int u = 0; u < PULL_U; ++u) {
                 const uint32_t fm = filter_block_mask(jv[u]);
-                const unsigned w = lds32(tab.filt + 4 * filter_block_word(jv[u]));
+                const unsigned w = lds32(tab.filt + 4 * ufilt_word(jv[u], tab.fshift));
                 pm |= (unsigned)(((w & fm) == fm) & (jv[u] >= 0)) << u;
             }
             while (pm) {
@@ -1520,12 +1528,14 @@ __device__ __forceinline__ void unit_fetch(const UArgs &a, const unsigned *sbc, 
 }
 
 template <int TH, int CAP, int FW>
-__global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
+__global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     long long *svals = reinterpret_cast<long long *>(smem_raw);
     int *skeys = reinterpret_cast<int *>(svals + CAP);
     unsigned *filt = reinterpret_cast<unsigned *>(skeys + CAP);
     constexpr int NWARP = TH / 32;
+    static_assert((FW & (FW - 1)) == 0 && FW >= 32, "Bloom filter words: a power of two");
+    constexpr int FSHIFT = 32 - __builtin_ctz(FW);
     __shared__ long long s_c, s_np, s_wsum[NWARP];
     __shared__ int s_u, s_lg, s_next, s_nq, s_nsupp, s_nkeys, s_last, s_sidx;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1636,7 +1646,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         for (uint32_t t = tid; t < cap; t += TH) {
             const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
             if (key != EMPTY_KEY) {
-                filter_add(filt, key, true);
+                atomicOr(&filt[ufilt_word(key, FSHIFT)], filter_block_mask(key));
                 const int p = atomicAdd(&s_nsupp, 1);
                 if (p < a.lcap) {
                     lkeys[p] = key;
@@ -1650,7 +1660,7 @@ __global__ void __launch_bounds__(TH, TH >= 1024 ? 1 : 2) k_diag_unit(UArgs a) {
         const long long cs = s_cur.cs, cn = s_cur.cn;
         if (tid == 0) unit_fetch(a, s_bc, s_nxt);  // the next unit, behind this one's entries
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
-                       (unsigned)__cvta_generic_to_shared(filt), mask, dense};
+                       (unsigned)__cvta_generic_to_shared(filt), mask, dense, FSHIFT};
         const double scale = a.value;
         // phase A: 32 entries per warp-step
         while (true) {
@@ -1972,19 +1982,28 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     MCF_CUDA(cudaMallocAsync(&blk, blk_bytes, s));
     frees.keep(blk);
     MCF_CUDA(cudaMemsetAsync(blk, 0, blk_bytes, s));
-    unsigned *bcnt = reinterpret_cast<unsigned *>(blk);                              // 16 x u32
-    unsigned long long *counter = reinterpret_cast<unsigned long long *>(blk + 64);  // work counter
-    unsigned long long *too_wide = counter + 1;
-    int *err = reinterpret_cast<int *>(blk + 96);
+    unsigned *bcnt = reinterpret_cast<unsigned *>(blk);                               // 32 x u32 (see classify)
+    unsigned long long *counter = reinterpret_cast<unsigned long long *>(blk + 128);  // work counter
+    unsigned long long *too_wide = counter + 1;                                       // (+ tier counters at 144, 152)
+    int *err = reinterpret_cast<int *>(blk + 160);
     a.bcnt = bcnt;
     a.counter = counter;
     a.err = err;
     a.prof = prof_on ? reinterpret_cast<unsigned long long *>(blk + 256) : nullptr;
     int *lists = nullptr;
-    MCF_CUDA(cudaMallocAsync(&lists, sizeof(int) * ((size_t)UNIT_BUCKETS * ncol + (size_t)ncol), s));
+    MCF_CUDA(cudaMallocAsync(&lists, sizeof(int) * ((size_t)(UNIT_BUCKETS + 2) * ncol + (size_t)ncol), s));
     frees.keep(lists);
     a.lists = lists;
-    a.done = lists + (size_t)UNIT_BUCKETS * ncol;
+    a.done = lists + (size_t)(UNIT_BUCKETS + 2) * ncol;
+    {
+        // narrow one-unit columns (Chung-Lu 1.6e7: 15.7M of 15.8M walked columns,
+        // 1-3K emissions each) run 4 CTAs per SM with 4096-slot tables (or 2
+        // with 8192), so several columns' latency chains overlap per SM
+        const char *e = getenv("MCF_UNIT_SMALL_CUT");
+        a.small_cut = e ? atoll(e) : 4096 * 2 / 3;
+        e = getenv("MCF_UNIT_MID_CUT");
+        a.mid_cut = e ? atoll(e) : 8192 * 2 / 3;
+    }
     // per-CTA scratch: support list (a table's keys) and the entry queue
     // (one slot per entry of the widest column)
     a.lcap = cap;
@@ -2020,10 +2039,11 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
         MCF_LAUNCHED("k_unit_classify");
     }
     unsigned long long hw = 0;
-    unsigned hbc[UNIT_BUCKETS];
+    unsigned hbc[32];
     MCF_CUDA(cudaMemcpyAsync(&hw, too_wide, sizeof(hw), cudaMemcpyDeviceToHost, s));
     MCF_CUDA(cudaMemcpyAsync(hbc, bcnt, sizeof(hbc), cudaMemcpyDeviceToHost, s));
     MCF_CUDA(cudaStreamSynchronize(s));
+    const unsigned hbc_small = hbc[16], hbc_mid = hbc[24];
     if (hw) {
         *fallback = true;
         return MCF_OK;
@@ -2045,14 +2065,50 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
         frees.keep(a.pofs);
         a.pest = pest;
         a.pewt = pewt;
-        k_unit_partition<<<sm_count() * 4, PART_TH, 0, s>>>(a, reinterpret_cast<unsigned *>(blk + 128));
+        k_unit_partition<<<sm_count() * 4, PART_TH, 0, s>>>(a, reinterpret_cast<unsigned *>(blk + 168));
         mcf::note_launch();
         MCF_LAUNCHED("k_unit_partition");
     }
+    // the small- and mid-table kernels' arguments: their list as bucket 0,
+    // their own counter and per-CTA scratch
+    auto tier_args = [&](int tier, int per_sm, long long lcap, UArgs &t) -> int {
+        t = a;
+        const int gs = sm_count() * per_sm;
+        t.lists = lists + (size_t)(UNIT_BUCKETS + tier) * ncol;
+        t.bcnt = bcnt + 16 + 8 * tier;  // bucket 0 = this tier's count, 1..7 = 0
+        t.counter = reinterpret_cast<unsigned long long *>(blk + 144 + 8 * tier);
+        t.lcap = lcap;
+        t.pcap = 1ll << 16;
+        const size_t per_cta = (size_t)t.lcap * (sizeof(int) + sizeof(long long)) +
+                               (size_t)t.qcap * (sizeof(int) + sizeof(long long) + sizeof(int) + sizeof(long long)) + 8 +
+                               (size_t)t.pcap * sizeof(int);
+        unsigned char *p = nullptr;
+        MCF_CUDA(cudaMallocAsync(&p, per_cta * gs + 64, s));
+        frees.keep(p);
+        t.lvals = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * t.lcap * gs;
+        t.qlo = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * t.qcap * gs;
+        t.qpre = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * (t.qcap + 1) * gs;
+        t.lkeys = reinterpret_cast<int *>(p);
+        p += sizeof(int) * t.lcap * gs;
+        t.qt = reinterpret_cast<int *>(p);
+        p += sizeof(int) * t.qcap * gs;
+        t.qlen = reinterpret_cast<int *>(p);
+        p += sizeof(int) * t.qcap * gs;
+        t.pmap = reinterpret_cast<int *>(p);
+        return MCF_OK;
+    };
+    UArgs as{}, am{};
+    if (hbc_small > 0 && (rc = tier_args(0, 4, 4096, as))) return rc;
+    if (hbc_mid > 0 && (rc = tier_args(1, 2, 8192, am))) return rc;
     rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
     rc = th == 1024 ? launch_units<1024, 16384, 8192>(a, grid, s) : launch_units<512, 8192, 4096>(a, grid, s);
     if (rc) return rc;
+    if (hbc_mid > 0 && (rc = launch_units<512, 8192, 4096>(am, sm_count() * 2, s))) return rc;
+    if (hbc_small > 0 && (rc = launch_units<256, 4096, 2048>(as, sm_count() * 4, s))) return rc;
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
     int herr = 0;
