@@ -1407,12 +1407,27 @@ __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
         s = (s + 1) & t.mask;
     }
 }
+#ifndef UNIT_PULL_U
+#define UNIT_PULL_U 8
+#endif
 // jv[u] for a lane-varying u < 8 without local memory (a select tree)
 __device__ __forceinline__ int sel8(const int (&v)[8], int u) {
     const int a0 = (u & 1) ? v[1] : v[0], a1 = (u & 1) ? v[3] : v[2];
     const int a2 = (u & 1) ? v[5] : v[4], a3 = (u & 1) ? v[7] : v[6];
     const int b0 = (u & 2) ? a1 : a0, b1 = (u & 2) ? a3 : a2;
     return (u & 4) ? b1 : b0;
+}
+template <int N>
+__device__ __forceinline__ int selu(const int (&v)[N], int u) {
+    if constexpr (N == 8) {
+        return sel8(v, u);
+    } else {
+        static_assert(N == 16, "8 or 16 ids per lane");
+        const int lo8[8] = {v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]};
+        const int hi8[8] = {v[8], v[9], v[10], v[11], v[12], v[13], v[14], v[15]};
+        const int a = sel8(lo8, u & 7), b = sel8(hi8, u & 7);
+        return (u & 8) ? b : a;
+    }
 }
 
 // sum of Q_c over the ids ckeys[lo, hi) (warp-cooperative, PULL_U ids per
@@ -1443,7 +1458,7 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
         // 8 ids per lane in flight; the Bloom-passing ones (bit mask) are then
         // probed one after another, so a warp runs the probe code max-over-
         // lanes-of-passes times instead of once per id slot
-        constexpr int PULL_U = 8;
+        constexpr int PULL_U = UNIT_PULL_U;
         const int *ids = a.ckeys + lo;
         const int len = (int)(hi - lo);
         for (int e0 = 0; e0 < len; e0 += 32 * PULL_U) {
@@ -1464,7 +1479,7 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
             while (pm) {
                 const int u = __ffs(pm) - 1;
                 pm &= pm - 1;
-                acc += utab_get(tab, sel8(jv, u));
+                acc += utab_get(tab, selu<PULL_U>(jv, u));
             }
         }
     }
