@@ -542,12 +542,14 @@ def run_device(args, cfg):
     em_per_walk_launch = em_per_step / world / walk_launches_per_step
     w_ach = BYTES_PER_STEP * em_per_walk_launch / (walk_avg_ms / 1e3) / 1e9 if walk_avg_ms > 0 else None
 
-    def traffic_of(kernel):
+    def traffic_of(kernel, per="dram_bytes_per_launch"):
+        # ncu dram__bytes_read.sum + dram__bytes_write.sum of the same command
+        # (tools/gpu_traffic.sh -> profiles/traffic_configN.json)
         tp = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
         if os.path.exists(tp):
             with open(tp) as fh:
                 t = json.load(fh)
-            return t.get(kernel, {}).get("dram_bytes_per_launch") if kernel in t else (
+            return t.get(kernel, {}).get(per) if kernel in t else (
                 t.get("dram_bytes_per_launch") if kernel.startswith("k_walk") else None)
         return None
 
@@ -568,9 +570,12 @@ def run_device(args, cfg):
         cbytes = combine_bytes(g, pre_)
         c_ms = q_ms_tot / max(1, args.steps)
         c_ach = cbytes / (c_ms / 1e3) / 1e9 if c_ms > 0 else None
-        combine = {"bound": "hbm", "kernel": "k_diag_q + k_diag_qc<2/4/8> + k_diag_big (Eq. 20 combine)",
+        combine = {"bound": "hbm",
+                   "kernel": ("k_diag_unit<1024/512/256> (Eq. 20 combine by key-group units)" if g.n > 24576
+                              else "k_diag_q (Eq. 20 combine, dense Q_c)"),
                    "achieved": c_ach, "peak": peak, "unit": "GB/s", "frac": (c_ach / peak) if c_ach else None,
-                   "traffic": traffic_of("combine"), "peak_source": peak_src,
+                   "traffic": traffic_of("combine", "dram_bytes_per_step"), "traffic_unit": "bytes per step",
+                   "peak_source": peak_src,
                    "algorithmic_bytes_per_step": cbytes,
                    "bytes_rule": "sum over walked c of sum_{a in C_c} (32 + 4 deg a) (SURVEY 8d)",
                    "kernel_ms_avg": c_ms, "kernel_share_of_step": (q_ms_tot / ms) if ms else None}

@@ -707,6 +707,11 @@ static int create(const mcf_csr *c, cudaStream_t s, mcf_graph **out) {
 extern "C" {
 
 int mcf_graph_create(const mcf_csr *csr, void *stream, mcf_graph **out) {
+    // MCF_L2_FETCH=<bytes>: the L2 fetch-granularity hint (cudaLimitMaxL2FetchGranularity)
+    // for this process's device -- the walks' random 8-B entry loads want 32-B fills
+    if (const char *e = getenv("MCF_L2_FETCH")) {
+        if (cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoll(e)) != cudaSuccess) cudaGetLastError();
+    }
     return mcf::create(csr, (cudaStream_t)stream, out);
 }
 
