@@ -1383,6 +1383,11 @@ struct UTab {
     int fshift;                 // Bloom word of a key: (key * C) >> fshift (the kernel's 2^(32 - fshift) words)
 };
 __device__ __forceinline__ uint32_t ufilt_word(int key, int fshift) { return ((uint32_t)key * 0x85EBCA6Bu) >> fshift; }
+// one bit per key: the 5 hash bits just below the word index (a miss costs a
+// multiply, two shifts and one shared load; measured cheaper than three bits)
+__device__ __forceinline__ uint32_t ufilt_bit(int key, int fshift) {
+    return 1u << ((((uint32_t)key * 0x85EBCA6Bu) >> (fshift - 5)) & 31u);
+}
 __device__ __forceinline__ unsigned lds32(unsigned addr) {
     unsigned v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -1394,7 +1399,7 @@ __device__ __forceinline__ long long lds64(unsigned addr) {
     return v;
 }
 __device__ __forceinline__ bool utab_maybe(const UTab &t, int key) {
-    const uint32_t m = filter_block_mask(key);
+    const uint32_t m = ufilt_bit(key, t.fshift);
     return (lds32(t.filt + 4 * ufilt_word(key, t.fshift)) & m) == m;
 }
 __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
@@ -1459,22 +1464,20 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
         // probed one after another, so a warp runs the probe code max-over-
         // lanes-of-passes times instead of once per id slot
         constexpr int PULL_U = UNIT_PULL_U;
-        const int *ids = a.ckeys + lo;
-        const int len = (int)(hi - lo);
-        for (int e0 = 0; e0 < len; e0 += 32 * PULL_U) {
+        // a lane's ids at p[0], p[32], ... (immediate offsets), `rem` of them left
+        const int *p = a.ckeys + lo + lane;
+        int rem = (int)(hi - lo) - lane;
+        for (; rem > 0; rem -= 32 * PULL_U, p += 32 * PULL_U) {
             int jv[PULL_U];
 #pragma unroll
-            for (int u = 0; u < PULL_U; ++u) {
-                const int e = e0 + 32 * u + lane;
-                jv[u] = e < len ? __ldg(ids + e) : -1;
-            }
+            for (int u = 0; u < PULL_U; ++u) jv[u] = 32 * u < rem ? __ldg(p + 32 * u) : -1;
             // branch-free Bloom stage: the PULL_U filter words load together
             unsigned pm = 0;
 #pragma unroll
             for (int u = 0; u < PULL_U; ++u) {
-                const uint32_t fm = filter_block_mask(jv[u]);
-                const unsigned w = lds32(tab.filt + 4 * ufilt_word(jv[u], tab.fshift));
-                pm |= (unsigned)(((w & fm) == fm) & (jv[u] >= 0)) << u;
+                const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
+                const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
+                pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & (unsigned)(jv[u] >= 0)) << u;
             }
             while (pm) {
                 const int u = __ffs(pm) - 1;
@@ -1661,7 +1664,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         for (uint32_t t = tid; t < cap; t += TH) {
             const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
             if (key != EMPTY_KEY) {
-                atomicOr(&filt[ufilt_word(key, FSHIFT)], filter_block_mask(key));
+                atomicOr(&filt[ufilt_word(key, FSHIFT)], ufilt_bit(key, FSHIFT));
                 const int p = atomicAdd(&s_nsupp, 1);
                 if (p < a.lcap) {
                     lkeys[p] = key;
