@@ -1381,6 +1381,7 @@ struct UTab {
     uint32_t mask;              // hash table: slots - 1
     bool dense;                 // values indexed by node id (small graphs), no keys
     int fshift;                 // Bloom word of a key: (key * C) >> fshift (the kernel's 2^(32 - fshift) words)
+    int tshift;                 // home slot: (key * phi) >> tshift == hash_slot(key, mask) (slots a power of two)
 };
 __device__ __forceinline__ uint32_t ufilt_word(int key, int fshift) { return ((uint32_t)key * 0x85EBCA6Bu) >> fshift; }
 // one bit per key: the 5 hash bits just below the word index (a miss costs a
@@ -1404,7 +1405,7 @@ __device__ __forceinline__ bool utab_maybe(const UTab &t, int key) {
 }
 __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
     if (t.dense) return lds64(t.vals + 8u * (unsigned)key);
-    uint32_t s = hash_slot(key, t.mask);
+    uint32_t s = ((uint32_t)key * 0x9E3779B1u) >> t.tshift;
     while (true) {
         const int k = (int)lds32(t.keys + 4 * s);
         if (k == key) return lds64(t.vals + 8 * s);
@@ -1413,7 +1414,7 @@ __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
     }
 }
 #ifndef UNIT_PULL_U
-#define UNIT_PULL_U 8
+#define UNIT_PULL_U 16
 #endif
 // jv[u] for a lane-varying u < 8 without local memory (a select tree)
 __device__ __forceinline__ int sel8(const int (&v)[8], int u) {
@@ -1678,7 +1679,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         const long long cs = s_cur.cs, cn = s_cur.cn;
         if (tid == 0) unit_fetch(a, s_bc, s_nxt);  // the next unit, behind this one's entries
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
-                       (unsigned)__cvta_generic_to_shared(filt), mask, dense, FSHIFT};
+                       (unsigned)__cvta_generic_to_shared(filt), mask, dense, FSHIFT, 32 - (31 - __clz((int)cap))};
         const double scale = a.value;
         // phase A: 32 entries per warp-step
         while (true) {
