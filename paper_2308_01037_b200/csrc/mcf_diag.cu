@@ -1403,13 +1403,20 @@ __device__ __forceinline__ bool utab_maybe(const UTab &t, int key) {
     const uint32_t m = ufilt_bit(key, t.fshift);
     return (lds32(t.filt + 4 * ufilt_word(key, t.fshift)) & m) == m;
 }
+// The unit kernel's dynamic shared memory by name (values at 0, keys at
+// 8 CAP): array accesses with constant offsets compile to LDS [reg + imm],
+// with no shared-window base to rematerialise per probe.
+extern __shared__ __align__(16) unsigned char mcf_usmem[];
+template <int CAP>
 __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
-    if (t.dense) return lds64(t.vals + 8u * (unsigned)key);
+    const long long *v = reinterpret_cast<const long long *>(mcf_usmem);
+    if (t.dense) return v[key];
+    const int *k = reinterpret_cast<const int *>(mcf_usmem + 8 * CAP);
     uint32_t s = ((uint32_t)key * 0x9E3779B1u) >> t.tshift;
     while (true) {
-        const int k = (int)lds32(t.keys + 4 * s);
-        if (k == key) return lds64(t.vals + 8 * s);
-        if (k == EMPTY_KEY) return 0;
+        const int ks = k[s];
+        if (ks == key) return v[s];
+        if (ks == EMPTY_KEY) return 0;
         s = (s + 1) & t.mask;
     }
 }
@@ -1439,6 +1446,7 @@ __device__ __forceinline__ int selu(const int (&v)[N], int u) {
 // sum of Q_c over the ids ckeys[lo, hi) (warp-cooperative, PULL_U ids per
 // lane in flight) or over the unit's support positions [lo, hi) tested
 // against hub row i's bitmap (push)
+template <int CAP>
 __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, const int *lkeys,
                                                const long long *lvals, int i, bool push, long long lo, long long hi,
                                                int lane) {
@@ -1483,7 +1491,7 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
             while (pm) {
                 const int u = __ffs(pm) - 1;
                 pm &= pm - 1;
-                acc += utab_get(tab, selu<PULL_U>(jv, u));
+                acc += utab_get<CAP>(tab, selu<PULL_U>(jv, u));
             }
         }
     }
@@ -1721,7 +1729,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                     for (int q = 0; q < 4; ++q) {
                         if (jv[q] < 0) continue;
                         if (grp_filter && (int)(key_group(jv[q]) >> shift) != u) continue;
-                        if (utab_maybe(tab, jv[q])) acc += utab_get(tab, jv[q]);
+                        if (utab_maybe(tab, jv[q])) acc += utab_get<CAP>(tab, jv[q]);
                     }
                 }
                 if (a.prof) {
@@ -1815,7 +1823,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
             const long long b = qlo[j] + p * a.chunk;
             const long long e = qlo[j] + (len < (p + 1) * a.chunk ? len : (p + 1) * a.chunk);
             const int i = push ? __ldg(a.csc_rows + cs + t) : 0;
-            const long long acc = unit_scan(a, tab, lkeys, lvals, i, push, b, e, lane);
+            const long long acc = unit_scan<CAP>(a, tab, lkeys, lvals, i, push, b, e, lane);
             if (a.prof && lane == 0) {
                 pr[2] += 1;
                 pr[push ? 4 : 3] += (unsigned long long)(e - b);
