@@ -56,10 +56,18 @@ def _worker(rank, world, port_no, name, n_walks, out):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("units", [None, "split"])
 @pytest.mark.parametrize("name", ["ba400", "kron8"])
-def test_peer_exchange_matches_single_process(name):
+def test_peer_exchange_matches_single_process(name, units, monkeypatch):
+    """units="split": the diag combine by key-group units (forced on these
+    small graphs, every column split, narrow-column tiers) on each rank's
+    column shard; the spawned ranks inherit the environment."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
+    if units:
+        monkeypatch.setenv("MCF_DIAG_UNITS", "1")
+        monkeypatch.setenv("MCF_UNIT_SMALL_NEED", "64")
+        monkeypatch.setenv("MCF_UNIT_SMALL_CUT", "32")
     import paper_2308_01037_b200 as mc
     c = golden_io.load(name)
     n_walks = 50 * c.n
