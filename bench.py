@@ -554,7 +554,14 @@ def run_device(args, cfg):
         return None
 
     walk_kernel = "k_walk_action" if cfg["kind"] == "action" else "k_walk_emit"
+    # L2-resident walk tables (configs 1, 2: < ~100 MB of CSR ids): the walk runs
+    # above "HBM speed" and is bound by dependent L2 loads -- report it against
+    # the measured L2 random-load ceiling too (profiles/r01/gups.txt)
+    l2_resident = 4 * g.nnz + 16 * g.n < 100 * 2 ** 20
+    w_steps = em_per_walk_launch / (walk_avg_ms / 1e3) if walk_avg_ms > 0 else None
     walk = {"bound": "hbm", "kernel": walk_kernel, "achieved": w_ach, "peak": peak, "unit": "GB/s",
+            "l2_resident": l2_resident,
+            "l2_frac": (w_steps / 279.2e9) if (w_steps and l2_resident) else None,
             "frac": (w_ach / peak) if w_ach else None, "traffic": traffic_of(walk_kernel), "peak_source": peak_src,
             "bytes_per_step": BYTES_PER_STEP, "kernel_ms_avg": walk_avg_ms,
             "launches_per_step": walk_launches_per_step,
