@@ -562,6 +562,8 @@ def run_device(args, cfg):
     walk = {"bound": "hbm", "kernel": walk_kernel, "achieved": w_ach, "peak": peak, "unit": "GB/s",
             "l2_resident": l2_resident,
             "l2_frac": (w_steps / 279.2e9) if (w_steps and l2_resident) else None,
+            # measured DRAM traffic per launch (ncu) over the launch time: what the
+            # HBM actually moved -- each random 8-B entry costs a line fill
             "frac": (w_ach / peak) if w_ach else None, "traffic": traffic_of(walk_kernel), "peak_source": peak_src,
             "bytes_per_step": BYTES_PER_STEP, "kernel_ms_avg": walk_avg_ms,
             "launches_per_step": walk_launches_per_step,
@@ -571,6 +573,11 @@ def run_device(args, cfg):
             "note": "algorithmic bytes = 64 B x emissions (row header + sampled entry, SURVEY 8d); the lean layout "
                     "serves a step with ONE random 4/8-B entry, so L2-resident graphs run above 'HBM' speed and "
                     "HBM-resident ones are bound by 128-B line fills (profiles/r01/gups.txt)"}
+    wt = walk.get("traffic")
+    if wt and walk_avg_ms > 0:
+        walk["traffic_gbs"] = wt / (walk_avg_ms / 1e3) / 1e9
+        walk["traffic_frac"] = walk["traffic_gbs"] / peak
+        walk["traffic_bytes_per_step"] = wt / em_per_walk_launch if em_per_walk_launch else None
     roofline = walk
     if cfg["kind"] == "diag":
         _, pre_ = g.allocate(wcfg.n_walks)
