@@ -2042,7 +2042,7 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     // per-CTA scratch: support list (a table's keys) and the entry queue
     // (one slot per entry of the widest column)
     a.lcap = cap;
-    a.qcap = g->info.max_degree > 64 ? g->info.max_degree : 64;
+    a.qcap = g->max_col_degree > 64 ? g->max_col_degree : 64;  // one queue slot per entry of the longest column
     unsigned char *scr = nullptr;
     a.pcap = 1ll << 18;
     const size_t per_cta = (size_t)a.lcap * (sizeof(int) + sizeof(long long)) +

@@ -144,6 +144,7 @@ struct mcf_graph {
     int32_t *gidx = nullptr;         // n: offset-table row of a long column, or -1
     int32_t *gofs = nullptr;         // n_long x (NGROUPS + 1), relative to csc_ptr[c]
     long long n_gofs = 0;
+    long long max_col_degree = 0;    // longest CSC column (set with ckeys): a unit's entry queue capacity
     bool uniform_value = false;      // all stored values equal `value` (0/1 graphs scaled by gamma)
     double value = 0.0;
     mcf_graph_info info{};

@@ -383,8 +383,10 @@ __global__ void k_mark_long_cols(const long long *__restrict__ csc_ptr, long lon
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n) return;
     int o = -1;
-    if (csc_ptr[c + 1] - csc_ptr[c] > GROUP_OFS_MIN) o = (int)atomicAdd(count, 1u);
+    const long long d = csc_ptr[c + 1] - csc_ptr[c];
+    if (d > GROUP_OFS_MIN) o = (int)atomicAdd(count, 1u);
     gidx[c] = o;
+    if (d > 0) atomicMax(reinterpret_cast<unsigned long long *>(count + 2), (unsigned long long)d);  // longest column
 }
 
 constexpr int GK_WARPS = 8;
@@ -462,15 +464,17 @@ __global__ void __launch_bounds__(GK_WARPS * 32) k_group_keys(const long long *_
 int ensure_group_keys(mcf_graph *g, cudaStream_t s) {
     if (g->ckeys) return MCF_OK;
     MCF_CUDA(cudaMallocAsync(&g->gidx, sizeof(int) * (g->n > 0 ? g->n : 1), s));
-    unsigned *cnt = nullptr;
-    MCF_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned), s));
-    MCF_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s));
+    unsigned *cnt = nullptr;  // [0]: long columns, [2..3]: the longest column (u64)
+    MCF_CUDA(cudaMallocAsync(&cnt, 16, s));
+    MCF_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
     k_mark_long_cols<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>((const long long *)g->csc_ptr, g->n, g->gidx, cnt);
     mcf::note_launch();
-    unsigned nl = 0;
-    MCF_CUDA(cudaMemcpyAsync(&nl, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    unsigned hc[4] = {0, 0, 0, 0};
+    MCF_CUDA(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s));
     MCF_CUDA(cudaStreamSynchronize(s));
     cudaFreeAsync(cnt, s);
+    const unsigned nl = hc[0];
+    g->max_col_degree = (long long)(((unsigned long long)hc[3] << 32) | hc[2]);
     g->n_gofs = nl;
     MCF_CUDA(cudaMallocAsync(&g->gofs, sizeof(int) * (size_t)(nl > 0 ? nl : 1) * (NGROUPS + 1), s));
     MCF_CUDA(cudaMallocAsync(&g->ckeys, sizeof(int) * (size_t)(g->nnz > 0 ? g->nnz : 1), s));

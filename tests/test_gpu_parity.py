@@ -525,6 +525,37 @@ def test_diag_cluster_tables_bitwise(mc):
     assert np.all(np.isfinite(ref)) and np.all(ref > 1.0)
 
 
+def test_unit_combine_directed_long_column(mc, monkeypatch):
+    """An unsymmetric uniform-value graph above the dense-Q size whose column
+    0 (20,000 entries) is far longer than any row: the unit combine (default,
+    and with every column split) equals the single-table combine bit for bit
+    -- CSC-side slices, hub bitmaps from the CSC, an entry queue sized by the
+    longest column."""
+    rng = np.random.default_rng(7)
+    n = 30000
+    u, v = rng.integers(0, n, 8 * n), rng.integers(0, n, 8 * n)
+    u = np.concatenate([u, rng.choice(np.arange(1, n), 20000, replace=False)])
+    v = np.concatenate([v, np.zeros(20000, dtype=np.int64)])
+    keep = u != v
+    m = sparse.csr_array((np.ones(keep.sum()), (u[keep], v[keep])), shape=(n, n))
+    m.sum_duplicates()
+    m.data[:] = 1.0
+    a = port.Csr.from_any(m)
+    assert np.diff(a.csc_ptr).max() > 10 * np.diff(a.row_ptr).max()
+    a = a.scaled(1.0 / float(np.diff(a.row_ptr).max()))
+    g = mc.DeviceGraph(as_matrix(a, False))
+    cfg = mc.WalkConfig(n * 40, 1e-300, 12, 3)
+    monkeypatch.setenv("MCF_DIAG_UNITS", "0")
+    ref = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+    monkeypatch.delenv("MCF_DIAG_UNITS")
+    out = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+    assert np.array_equal(out, ref)
+    monkeypatch.setenv("MCF_UNIT_SMALL_NEED", "64")
+    out = mc.rand_funm_diag(g, mc.EXPONENTIAL, cfg).values
+    assert np.array_equal(out, ref)
+    assert np.all(np.isfinite(ref)) and np.all(ref >= 1.0)
+
+
 def test_rand_funm_full_consistency_and_closed_form(mc):
     """SPEC acceptance 4: diag(rand_funm) == rand_funm_diag (shared seed) to
     1e-12 relative on 16-node instances; SPEC.md:352 closed form; A = 0."""
