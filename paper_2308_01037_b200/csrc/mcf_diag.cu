@@ -1423,6 +1423,9 @@ __device__ __forceinline__ long long utab_get(const UTab &t, int key) {
 #ifndef UNIT_PULL_U
 #define UNIT_PULL_U 16
 #endif
+#ifndef UNIT_PUSH_U
+#define UNIT_PUSH_U 4
+#endif
 // jv[u] for a lane-varying u < 8 without local memory (a select tree)
 __device__ __forceinline__ int sel8(const int (&v)[8], int u) {
     const int a0 = (u & 1) ? v[1] : v[0], a1 = (u & 1) ? v[3] : v[2];
@@ -1453,7 +1456,7 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
     long long acc = 0;
     if (push) {
         const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
-        constexpr int PUSH_U = 4;
+        constexpr int PUSH_U = UNIT_PUSH_U;
         for (long long t0 = lo; t0 < hi; t0 += 32 * PUSH_U) {
             int kv[PUSH_U];
             unsigned wv[PUSH_U];
