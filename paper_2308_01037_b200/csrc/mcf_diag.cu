@@ -1182,6 +1182,7 @@ struct UArgs {
     int *pmap;           // per-CTA piece -> queue entry map (pcap each; wider units binary-search qpre)
     long long pcap;
     long long chunk;
+    int serial_small;      // slices scanned by one lane in phase A when the column has < 32 entries per warp
     long long small_need;  // widest table need of a one-unit column
     long long small_cut;   // one-unit columns up to this need go to the small-table kernel (list UNIT_BUCKETS)
     long long mid_cut;     // ... up to this one to the mid-size kernel (list UNIT_BUCKETS + 1)
@@ -1692,7 +1693,10 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
                        (unsigned)__cvta_generic_to_shared(filt), mask, dense, FSHIFT, 32 - (31 - __clz((int)cap))};
         const double scale = a.value;
-        // phase A: 32 entries per warp-step
+        // phase A: 32 entries per warp-step.  A column with fewer entries than
+        // the CTA has lanes leaves most warps idle here, so it queues its
+        // slices longer than a few ids for phase B, where all warps share them
+        const int serial_max = cn >= 32 * NWARP ? UNIT_SERIAL : a.serial_small;
         while (true) {
             int t0 = 0;
             if (lane == 0) t0 = atomicAdd(&s_next, 32);
@@ -1721,7 +1725,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                 push = !grp_filter && a.hub_of && 100 * (hi - lo) > (long long)a.push_pct * nsupp &&
                        __ldg(a.hub_of + i) >= 0;
             }
-            const bool serial = valid && !push && (grp_filter || hi - lo <= UNIT_SERIAL);
+            const bool serial = valid && !push && (grp_filter || hi - lo <= serial_max);
             long long acc = 0;
             if (serial) {
                 for (long long e = lo; e < hi; e += 4) {
@@ -1995,6 +1999,10 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     a.hub_of = g->hub_of;
     a.hub_bits = g->hub_bits;
     a.hub_words = g->hub_words;
+    {
+        const char *e = getenv("MCF_UNIT_SERIAL_SMALL");
+        a.serial_small = e ? atoi(e) : 2;  // measured: config 5 4.27 -> 4.17 s, config 3 unchanged
+    }
     {
         const char *e = getenv("MCF_UNIT_CHUNK");
         a.chunk = e ? atoll(e) : 1024;
