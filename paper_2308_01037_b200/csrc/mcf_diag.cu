@@ -1689,7 +1689,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
         const long long t_built = a.prof ? clock64() : 0;
         const long long cs = s_cur.cs, cn = s_cur.cn;
-        if (tid == 0) unit_fetch(a, s_bc, s_nxt);  // the next unit, behind this one's entries
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
                        (unsigned)__cvta_generic_to_shared(filt), mask, dense, FSHIFT, 32 - (31 - __clz((int)cap))};
         const double scale = a.value;
@@ -1809,6 +1808,9 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
             s_next = 0;
         }
         __syncthreads();
+        // the next unit, fetched by thread 0 while the other warps take this
+        // unit's pieces (phase B has no barrier until all pieces are done)
+        if (tid == 0) unit_fetch(a, s_bc, s_nxt);
         // phase B: pieces of the queued entries, all warps
         while (true) {
             int x = 0;
