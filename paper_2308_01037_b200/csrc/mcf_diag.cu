@@ -1636,6 +1636,10 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         int lg_m = 0;
         while ((1ll << lg_m) < m) ++lg_m;
         const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // as k_diag_q: sum of m terms < 2^62
+        // w 2^E as one multiply when 2^E is a normal double (exact: a power-of-two
+        // scaling rounds like ldexp, subnormal results included)
+        const bool escale_ok = E >= -1022 && E <= 1023;
+        const double escale = escale_ok ? __longlong_as_double((long long)(E + 1023) << 52) : 0.0;
         // Q_c over this unit's key groups
         constexpr int U = 4;
         for (long long base = e0; base < e1; base += (long long)U * TH) {
@@ -1661,7 +1665,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
 #pragma unroll
             for (int q = 0; q < U; ++q) {
                 if (!__any_sync(MCF_FULL, sv[q] >= 0)) continue;  // no key of this unit in the warp's slot
-                long long qv = sv[q] >= 0 ? __double2ll_rn(ldexp(wv[q], E)) : 0;
+                long long qv = sv[q] >= 0 ? __double2ll_rn(escale_ok ? wv[q] * escale : ldexp(wv[q], E)) : 0;
                 const unsigned same = __match_any_sync(MCF_FULL, sv[q]);
                 if (sv[q] < 0) continue;
                 if (__popc(same) > 1) {
