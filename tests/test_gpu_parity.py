@@ -556,6 +556,27 @@ def test_unit_combine_directed_long_column(mc, monkeypatch):
     assert np.all(np.isfinite(ref)) and np.all(ref >= 1.0)
 
 
+def test_unit_combine_variable_length_walks(mc, monkeypatch):
+    """Cutoff-terminated walks (resolvent, max_steps 10^3 > 64: count pass,
+    scan, emissions at explicit offsets) through the unit combine, natural
+    and forced splits, equal the single-table combine bit for bit."""
+    a = _multi_hub_graph(seed=3)
+    g = mc.DeviceGraph(as_matrix(a, True))
+    cfg = mc.WalkConfig(a.n * 30, 1e-6, 1000, 9)
+    monkeypatch.setenv("MCF_DIAG_UNITS", "0")
+    ref = mc.rand_funm_diag(g, mc.RESOLVENT, cfg)
+    monkeypatch.delenv("MCF_DIAG_UNITS")
+    assert ref.emissions > a.n * 30 * 3
+    for env in ({}, {"MCF_UNIT_SMALL_NEED": "256"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        out = mc.rand_funm_diag(g, mc.RESOLVENT, cfg)
+        for k in env:
+            monkeypatch.delenv(k)
+        assert out.emissions == ref.emissions
+        assert np.array_equal(out.values, ref.values), env
+
+
 def test_rand_funm_full_consistency_and_closed_form(mc):
     """SPEC acceptance 4: diag(rand_funm) == rand_funm_diag (shared seed) to
     1e-12 relative on 16-node instances; SPEC.md:352 closed form; A = 0."""
