@@ -1171,9 +1171,6 @@ struct UArgs {
     const unsigned *__restrict__ bcnt;  // columns per bucket
     unsigned long long *counter;
     int *done;           // per column of the batch: finished units
-    int *lkeys;          // per-CTA support list (lcap each)
-    long long *lvals;
-    long long lcap;
     int *qt;             // per-CTA queue of long entries: entry (~t: push), slice start, length, piece prefix
     long long *qlo;
     int *qlen;
@@ -1451,9 +1448,8 @@ __device__ __forceinline__ int selu(const int (&v)[N], int u) {
 // lane in flight) or over the unit's support positions [lo, hi) tested
 // against hub row i's bitmap (push)
 template <int CAP>
-__device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, const int *lkeys,
-                                               const long long *lvals, int i, bool push, long long lo, long long hi,
-                                               int lane) {
+__device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, int i, bool push, long long lo,
+                                               long long hi, int lane) {
     long long acc = 0;
     if (push) {
         const unsigned *bits = a.hub_bits + (long long)__ldg(a.hub_of + i) * a.hub_words;
@@ -1464,13 +1460,13 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
 #pragma unroll
             for (int u = 0; u < PUSH_U; ++u) {
                 const long long t = t0 + 32 * u + lane;
-                kv[u] = t < hi ? lkeys[t] : -1;
+                kv[u] = t < hi ? reinterpret_cast<const int *>(mcf_usmem + 8 * CAP)[t] : -1;  // table slot (or empty)
             }
 #pragma unroll
             for (int u = 0; u < PUSH_U; ++u) wv[u] = kv[u] >= 0 ? __ldg(bits + (kv[u] >> 5)) : 0u;
 #pragma unroll
             for (int u = 0; u < PUSH_U; ++u)
-                if ((wv[u] >> (kv[u] & 31)) & 1u) acc += lvals[t0 + 32 * u + lane];
+                if ((wv[u] >> (kv[u] & 31)) & 1u) acc += reinterpret_cast<const long long *>(mcf_usmem)[t0 + 32 * u + lane];
         }
     } else {
         // 8 ids per lane in flight; the Bloom-passing ones (bit mask) are then
@@ -1570,8 +1566,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
     __shared__ long long s_c, s_np, s_wsum[NWARP];
     __shared__ int s_u, s_lg, s_next, s_nq, s_nsupp, s_nkeys, s_last, s_sidx;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int *lkeys = a.lkeys + (long long)blockIdx.x * a.lcap;
-    long long *lvals = a.lvals + (long long)blockIdx.x * a.lcap;
     int *qt = a.qt + (long long)blockIdx.x * a.qcap;
     long long *qlo = a.qlo + (long long)blockIdx.x * a.qcap;
     int *qlen = a.qlen + (long long)blockIdx.x * a.qcap;
@@ -1677,20 +1671,22 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
             }
         }
         __syncthreads();
-        // Bloom filter and support list of this unit's part
-        for (uint32_t t = tid; t < cap; t += TH) {
-            const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
-            if (key != EMPTY_KEY) {
-                atomicOr(&filt[ufilt_word(key, FSHIFT)], ufilt_bit(key, FSHIFT));
-                const int p = atomicAdd(&s_nsupp, 1);
-                if (p < a.lcap) {
-                    lkeys[p] = key;
-                    lvals[p] = vals[t];
+        // Bloom filter and key count of this unit's part (push entries scan
+        // the table's slots themselves: no support list to write)
+        {
+            int cnt = 0;
+            for (uint32_t t = tid; t < cap; t += TH) {
+                const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
+                if (key != EMPTY_KEY) {
+                    atomicOr(&filt[ufilt_word(key, FSHIFT)], ufilt_bit(key, FSHIFT));
+                    ++cnt;
                 }
             }
+            cnt = warp_sum_int(cnt);
+            if (lane == 0 && cnt) atomicAdd(&s_nsupp, cnt);
         }
         __syncthreads();
-        const int nsupp = s_nsupp <= a.lcap ? s_nsupp : 0x3fffffff;  // overflow: never push
+        const int nsupp = keys ? s_nsupp : 0x3fffffff;  // dense tables: never push
         const long long t_built = a.prof ? clock64() : 0;
         const long long cs = s_cur.cs, cn = s_cur.cn;
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
@@ -1763,7 +1759,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                     if (k < a.qcap) {
                         qt[k] = push ? ~t : t;
                         qlo[k] = push ? 0 : lo;
-                        qlen[k] = (int)(push ? nsupp : hi - lo);
+                        qlen[k] = (int)(push ? cap : hi - lo);  // push: the table's slots
                     } else {
                         atomicOr(a.err, 512);  // queue overflow (qcap >= max degree: not expected)
                     }
@@ -1836,7 +1832,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
             const long long b = qlo[j] + p * a.chunk;
             const long long e = qlo[j] + (len < (p + 1) * a.chunk ? len : (p + 1) * a.chunk);
             const int i = push ? __ldg(a.csc_rows + cs + t) : 0;
-            const long long acc = unit_scan<CAP>(a, tab, lkeys, lvals, i, push, b, e, lane);
+            const long long acc = unit_scan<CAP>(a, tab, i, push, b, e, lane);
             if (a.prof && lane == 0) {
                 pr[2] += 1;
                 pr[push ? 4 : 3] += (unsigned long long)(e - b);
@@ -2056,33 +2052,30 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
         e = getenv("MCF_UNIT_MID_CUT");
         a.mid_cut = e ? atoll(e) : 8192 * 2 / 3;
     }
-    // per-CTA scratch: support list (a table's keys) and the entry queue
-    // (one slot per entry of the widest column)
-    a.lcap = cap;
-    a.qcap = g->max_col_degree > 64 ? g->max_col_degree : 64;  // one queue slot per entry of the longest column
-    unsigned char *scr = nullptr;
+    // per-CTA scratch: the entry queue (one slot per entry of the longest
+    // column) and the piece map
+    a.qcap = g->max_col_degree > 64 ? g->max_col_degree : 64;
+    // carve one per-CTA scratch block for a kernel of `gs` CTAs
+    auto carve_scratch = [&](UArgs &t, int gs) -> int {
+        const size_t per_cta = (size_t)t.qcap * (sizeof(int) + sizeof(long long) + sizeof(int) + sizeof(long long)) + 8 +
+                               (size_t)t.pcap * sizeof(int);
+        unsigned char *p = nullptr;
+        MCF_CUDA(cudaMallocAsync(&p, per_cta * gs + 64, s));
+        frees.keep(p);
+        t.qlo = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * t.qcap * gs;
+        t.qpre = reinterpret_cast<long long *>(p);
+        p += sizeof(long long) * (t.qcap + 1) * gs;
+        t.qt = reinterpret_cast<int *>(p);
+        p += sizeof(int) * t.qcap * gs;
+        t.qlen = reinterpret_cast<int *>(p);
+        p += sizeof(int) * t.qcap * gs;
+        t.pmap = reinterpret_cast<int *>(p);
+        return MCF_OK;
+    };
     a.pcap = 1ll << 18;
-    const size_t per_cta = (size_t)a.lcap * (sizeof(int) + sizeof(long long)) +
-                           (size_t)a.qcap * (sizeof(int) + sizeof(long long) + sizeof(int) + sizeof(long long)) + 8 +
-                           (size_t)a.pcap * sizeof(int);
-    MCF_CUDA(cudaMallocAsync(&scr, per_cta * grid + 64, s));
-    frees.keep(scr);
-    {
-        unsigned char *p = scr;
-        a.lvals = reinterpret_cast<long long *>(p);
-        p += sizeof(long long) * a.lcap * grid;
-        a.qlo = reinterpret_cast<long long *>(p);
-        p += sizeof(long long) * a.qcap * grid;
-        a.qpre = reinterpret_cast<long long *>(p);
-        p += sizeof(long long) * (a.qcap + 1) * grid;
-        a.lkeys = reinterpret_cast<int *>(p);
-        p += sizeof(int) * a.lcap * grid;
-        a.qt = reinterpret_cast<int *>(p);
-        p += sizeof(int) * a.qcap * grid;
-        a.qlen = reinterpret_cast<int *>(p);
-        p += sizeof(int) * a.qcap * grid;
-        a.pmap = reinterpret_cast<int *>(p);
-    }
+    rc = carve_scratch(a, grid);
+    if (rc) return rc;
     {
         const long long warps = (ncol + 31) / 32;
         const long long blocks = (warps * 32 + 255) / 256;
@@ -2123,38 +2116,17 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     }
     // the small- and mid-table kernels' arguments: their list as bucket 0,
     // their own counter and per-CTA scratch
-    auto tier_args = [&](int tier, int per_sm, long long lcap, UArgs &t) -> int {
+    auto tier_args = [&](int tier, int per_sm, UArgs &t) -> int {
         t = a;
-        const int gs = sm_count() * per_sm;
         t.lists = lists + (size_t)(UNIT_BUCKETS + tier) * ncol;
         t.bcnt = bcnt + 16 + 8 * tier;  // bucket 0 = this tier's count, 1..7 = 0
         t.counter = reinterpret_cast<unsigned long long *>(blk + 144 + 8 * tier);
-        t.lcap = lcap;
         t.pcap = 1ll << 16;
-        const size_t per_cta = (size_t)t.lcap * (sizeof(int) + sizeof(long long)) +
-                               (size_t)t.qcap * (sizeof(int) + sizeof(long long) + sizeof(int) + sizeof(long long)) + 8 +
-                               (size_t)t.pcap * sizeof(int);
-        unsigned char *p = nullptr;
-        MCF_CUDA(cudaMallocAsync(&p, per_cta * gs + 64, s));
-        frees.keep(p);
-        t.lvals = reinterpret_cast<long long *>(p);
-        p += sizeof(long long) * t.lcap * gs;
-        t.qlo = reinterpret_cast<long long *>(p);
-        p += sizeof(long long) * t.qcap * gs;
-        t.qpre = reinterpret_cast<long long *>(p);
-        p += sizeof(long long) * (t.qcap + 1) * gs;
-        t.lkeys = reinterpret_cast<int *>(p);
-        p += sizeof(int) * t.lcap * gs;
-        t.qt = reinterpret_cast<int *>(p);
-        p += sizeof(int) * t.qcap * gs;
-        t.qlen = reinterpret_cast<int *>(p);
-        p += sizeof(int) * t.qcap * gs;
-        t.pmap = reinterpret_cast<int *>(p);
-        return MCF_OK;
+        return carve_scratch(t, sm_count() * per_sm);
     };
     UArgs as{}, am{};
-    if (hbc_small > 0 && (rc = tier_args(0, 4, 4096, as))) return rc;
-    if (hbc_mid > 0 && (rc = tier_args(1, 2, 8192, am))) return rc;
+    if (hbc_small > 0 && (rc = tier_args(0, 4, as))) return rc;
+    if (hbc_mid > 0 && (rc = tier_args(1, 2, am))) return rc;
     rc = timed_begin(g, timed, g->ev_q, s);
     if (rc) return rc;
     rc = th == 1024 ? launch_units<1024, 16384, 8192>(a, grid, s) : launch_units<512, 8192, 4096>(a, grid, s);
