@@ -1990,12 +1990,13 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     a.value = g->value;
     a.colmax = colmax;
     {
-        // push (hub-bitmap tests) when the slice is longer than push_pct/100 x
-        // the unit's keys: measured best 800 at n = 2^22 (R-MAT) and 1600 at
-        // 1.6e7 (Chung-Lu) -- a test is a random load into an n-bit bitmap
+        // push (hub-bitmap tests of the table's slots) when the slice is longer
+        // than push_pct/100 x the unit's keys: measured best ~600 at n = 2^22
+        // (R-MAT) and ~1200 at 1.6e7 (Chung-Lu) -- a test is a random load into
+        // an n-bit bitmap
         const char *e = getenv("MCF_UNIT_PUSH_PCT");
-        double pct = 800.0 * sqrt((double)g->n / (double)(1ll << 22));
-        pct = pct < 800.0 ? 800.0 : (pct > 6400.0 ? 6400.0 : pct);
+        double pct = 600.0 * sqrt((double)g->n / (double)(1ll << 22));
+        pct = pct < 600.0 ? 600.0 : (pct > 4800.0 ? 4800.0 : pct);
         a.push_pct = e ? atoi(e) : (int)pct;
     }
     a.hub_of = g->hub_of;
