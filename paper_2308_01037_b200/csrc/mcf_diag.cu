@@ -1349,7 +1349,9 @@ __global__ void __launch_bounds__(PART_TH) k_unit_partition(UArgs a, unsigned *_
 
 // insert with an occupancy guard: a table past its limit drops the key and
 // flags the overflow (never expected: need per unit has a ~12 sigma margin)
-__device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, int *nkeys, int limit, int *err) {
+// The lane that inserts a new key also sets its Bloom bit and counts it.
+__device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, int *nkeys, int limit, int *err,
+                                           unsigned *filt, int fshift) {
     uint32_t s = hash_slot(key, mask);
     while (true) {
         const int k = keys[s];
@@ -1362,6 +1364,8 @@ __device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, in
             const int old = atomicCAS(&keys[s], EMPTY_KEY, key);
             if (old == EMPTY_KEY) {
                 atomicAdd(nkeys, 1);
+                const uint32_t h = (uint32_t)key * 0x85EBCA6Bu;
+                atomicOr(filt + (h >> fshift), 1u << ((h >> (fshift - 5)) & 31u));
                 return (int)s;
             }
             if (old == key) return (int)s;
@@ -1626,6 +1630,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         }
         for (int t = tid; t < FW; t += TH) filt[t] = 0u;
         __syncthreads();
+        const long long t_zeroed = a.prof ? clock64() : 0;
         const double maxw = __longlong_as_double((long long)s_cur.maxw);
         int lg_m = 0;
         while ((1ll << lg_m) < m) ++lg_m;
@@ -1666,27 +1671,21 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                     qv = group_sum_i64(same, qv);
                     if (lane != __ffs(same) - 1) continue;
                 }
-                const int slot = keys ? unit_insert(keys, mask, sv[q], &s_nkeys, limit, a.err) : sv[q];
+                const int slot = keys ? unit_insert(keys, mask, sv[q], &s_nkeys, limit, a.err, filt, FSHIFT) : sv[q];
                 if (slot >= 0) smem_add_i64(&vals[slot], qv);
             }
         }
         __syncthreads();
-        // Bloom filter and key count of this unit's part (push entries scan
-        // the table's slots themselves: no support list to write)
-        {
-            int cnt = 0;
-            for (uint32_t t = tid; t < cap; t += TH) {
-                const int key = keys ? keys[t] : (vals[t] != 0 ? (int)t : EMPTY_KEY);
-                if (key != EMPTY_KEY) {
-                    atomicOr(&filt[ufilt_word(key, FSHIFT)], ufilt_bit(key, FSHIFT));
-                    ++cnt;
-                }
-            }
-            cnt = warp_sum_int(cnt);
-            if (lane == 0 && cnt) atomicAdd(&s_nsupp, cnt);
+        const long long t_inserted = a.prof ? clock64() : 0;
+        // Bloom filter and key count: set by the inserting lanes; a dense Q_c
+        // (small graphs) gets its filter from a pass over the node ids (push
+        // entries scan the table's slots themselves: no support list)
+        if (!keys) {
+            for (uint32_t t = tid; t < cap; t += TH)
+                if (vals[t] != 0) atomicOr(&filt[ufilt_word((int)t, FSHIFT)], ufilt_bit((int)t, FSHIFT));
+            __syncthreads();
         }
-        __syncthreads();
-        const int nsupp = keys ? s_nsupp : 0x3fffffff;  // dense tables: never push
+        const int nsupp = keys ? s_nkeys : 0x3fffffff;  // dense tables: never push
         const long long t_built = a.prof ? clock64() : 0;
         const long long cs = s_cur.cs, cn = s_cur.cn;
         const UTab tab{(unsigned)__cvta_generic_to_shared(skeys), (unsigned)__cvta_generic_to_shared(svals),
@@ -1881,6 +1880,11 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
             atomicAdd(a.prof + 7 + (lg < 8 ? lg : 7), 1ull);
             atomicAdd(a.prof + 2 * UPROF_SLOTS + (lg < 8 ? lg : 7), (unsigned long long)(t_end - t_start));
             atomicAdd(a.prof + 2 * UPROF_SLOTS + 8 + (lg < 8 ? lg : 7), (unsigned long long)(t_built - t_start));
+            const int ph = lg == 0 ? 0 : 4;  // build sub-phases: one-unit columns, split columns
+            atomicAdd(a.prof + 3 * UPROF_SLOTS + ph + 0, (unsigned long long)(t_zeroed - t_start));
+            atomicAdd(a.prof + 3 * UPROF_SLOTS + ph + 1, (unsigned long long)(t_inserted - t_zeroed));
+            atomicAdd(a.prof + 3 * UPROF_SLOTS + ph + 2, (unsigned long long)(t_built - t_inserted));
+            atomicAdd(a.prof + 3 * UPROF_SLOTS + ph + 3, (unsigned long long)(e1 - e0));
         }
     }
     if (a.prof) {
@@ -2027,7 +2031,7 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     const int grid = sm_count() * (th == 1024 ? 1 : 2);
     // small device block: bucket counts, work counter, too-wide need, error bits, profile
     unsigned char *blk = nullptr;
-    const size_t blk_bytes = 256 + sizeof(unsigned long long) * 3 * UPROF_SLOTS;
+    const size_t blk_bytes = 256 + sizeof(unsigned long long) * 4 * UPROF_SLOTS;
     MCF_CUDA(cudaMallocAsync(&blk, blk_bytes, s));
     frees.keep(blk);
     MCF_CUDA(cudaMemsetAsync(blk, 0, blk_bytes, s));
@@ -2138,7 +2142,7 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     if (rc) return rc;
     int herr = 0;
     MCF_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    unsigned long long hp[3 * UPROF_SLOTS];
+    unsigned long long hp[4 * UPROF_SLOTS];
     if (a.prof) MCF_CUDA(cudaMemcpyAsync(hp, a.prof, sizeof(hp), cudaMemcpyDeviceToHost, s));
     unsigned hb[UNIT_BUCKETS];
     if (a.prof) MCF_CUDA(cudaMemcpyAsync(hb, bcnt, sizeof(hb), cudaMemcpyDeviceToHost, s));
@@ -2154,7 +2158,11 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
         for (int k = 0; k < UNIT_BUCKETS; ++k) fprintf(stderr, " %.3e", (double)hp[2 * UPROF_SLOTS + k]);
         fprintf(stderr, " | build cycles by K:");
         for (int k = 0; k < UNIT_BUCKETS; ++k) fprintf(stderr, " %.3e", (double)hp[2 * UPROF_SLOTS + 8 + k]);
-        fprintf(stderr, "\n");
+        fprintf(stderr, " | build phases K=1 zero %.3e insert %.3e filter %.3e emissions %.3e"
+                        " K>1 zero %.3e insert %.3e filter %.3e emissions %.3e\n",
+                (double)hp[3 * UPROF_SLOTS + 0], (double)hp[3 * UPROF_SLOTS + 1], (double)hp[3 * UPROF_SLOTS + 2],
+                (double)hp[3 * UPROF_SLOTS + 3], (double)hp[3 * UPROF_SLOTS + 4], (double)hp[3 * UPROF_SLOTS + 5],
+                (double)hp[3 * UPROF_SLOTS + 6], (double)hp[3 * UPROF_SLOTS + 7]);
     }
     if (herr) {
         set_error("diag combine: unit table or queue overflow (code " + std::to_string(herr) + ")");
