@@ -1352,7 +1352,7 @@ __global__ void __launch_bounds__(PART_TH) k_unit_partition(UArgs a, unsigned *_
 // The lane that inserts a new key also sets its Bloom bit and counts it.
 __device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, int *nkeys, int limit, int *err,
                                            unsigned *filt, int fshift) {
-    uint32_t s = hash_slot(key, mask);
+    uint32_t s = hash_slot(key, mask) & ~3u;  // home: the key's aligned quad (utab_get reads it with one load)
     while (true) {
         const int k = keys[s];
         if (k == key) return (int)s;
@@ -1409,18 +1409,42 @@ __device__ __forceinline__ bool utab_maybe(const UTab &t, int key) {
 // 8 CAP): array accesses with constant offsets compile to LDS [reg + imm],
 // with no shared-window base to rematerialise per probe.
 extern __shared__ __align__(16) unsigned char mcf_usmem[];
+// Linear probing from the key's aligned quad of slots: one 16-B shared load
+// answers a lookup unless all four slots hold other keys (the table is at
+// most half full, so that is rare); the hit's value is read once, after the
+// loop, so lanes that needed another quad do not split the value load.
+// sb: the dynamic shared window's address (held in a register by the caller).
+__device__ __forceinline__ int4 lds128(unsigned addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 template <int CAP>
-__device__ __forceinline__ long long utab_get(const UTab &t, int key) {
-    const long long *v = reinterpret_cast<const long long *>(mcf_usmem);
-    if (t.dense) return v[key];
-    const int *k = reinterpret_cast<const int *>(mcf_usmem + 8 * CAP);
-    uint32_t s = ((uint32_t)key * 0x9E3779B1u) >> t.tshift;
+__device__ __forceinline__ long long utab_get(const UTab &t, unsigned sb, int key) {
+    if (t.dense) return lds64(sb + 8u * (unsigned)key);
+    uint32_t s = (((uint32_t)key * 0x9E3779B1u) >> t.tshift) & ~3u;
+    int slot;
     while (true) {
-        const int ks = k[s];
-        if (ks == key) return v[s];
-        if (ks == EMPTY_KEY) return 0;
-        s = (s + 1) & t.mask;
+        const int4 k = lds128(sb + 8u * CAP + 4u * s);
+        const bool e0 = k.x == key, e1 = k.y == key, e2 = k.z == key, e3 = k.w == key;
+        if (e0 | e1 | e2 | e3) {
+            slot = (int)s + (e0 ? 0 : (e1 ? 1 : (e2 ? 2 : 3)));
+            break;
+        }
+        if ((k.x | k.y | k.z | k.w) < 0) {  // an empty slot in the quad: the key is absent
+            slot = -1;
+            break;
+        }
+        s = (s + 4) & t.mask;
     }
+    return slot >= 0 ? lds64(sb + 8u * (unsigned)slot) : 0ll;
+}
+// the dynamic shared window's address, in a register the compiler cannot
+// rematerialise (recomputing it from the CTA's cluster rank costs 5-6
+// instructions per probe at this kernel's 64-register budget)
+__device__ __forceinline__ unsigned usmem_base() {
+    unsigned b = (unsigned)__cvta_generic_to_shared(mcf_usmem);
+    return __shfl_sync(MCF_FULL, b, 0);
 }
 #ifndef UNIT_PULL_U
 #define UNIT_PULL_U 16
@@ -1478,24 +1502,45 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
         // lanes-of-passes times instead of once per id slot
         constexpr int PULL_U = UNIT_PULL_U;
         // a lane's ids at p[0], p[32], ... (immediate offsets), `rem` of them left
+        const unsigned sb = usmem_base();
         const int *p = a.ckeys + lo + lane;
-        int rem = (int)(hi - lo) - lane;
-        for (; rem > 0; rem -= 32 * PULL_U, p += 32 * PULL_U) {
+        // ids left for the warp (uniform); a lane's are `remw - lane`
+        for (int remw = (int)(hi - lo); remw > 0; remw -= 32 * PULL_U, p += 32 * PULL_U) {
             int jv[PULL_U];
-#pragma unroll
-            for (int u = 0; u < PULL_U; ++u) jv[u] = 32 * u < rem ? __ldg(p + 32 * u) : -1;
-            // branch-free Bloom stage: the PULL_U filter words load together
             unsigned pm = 0;
+            if (remw >= 32 * PULL_U) {  // full block: no bounds predicates, every id valid
 #pragma unroll
-            for (int u = 0; u < PULL_U; ++u) {
-                const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
-                const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
-                pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & (unsigned)(jv[u] >= 0)) << u;
+                for (int u = 0; u < PULL_U; ++u) jv[u] = __ldg(p + 32 * u);
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
+                    const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
+                    pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & 1u) << u;
+                }
+            } else {
+                const int rem = remw - lane;
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) jv[u] = 32 * u < rem ? __ldg(p + 32 * u) : -1;
+                // branch-free Bloom stage: the PULL_U filter words load together
+#pragma unroll
+                for (int u = 0; u < PULL_U; ++u) {
+                    const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
+                    const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
+                    pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & (unsigned)(jv[u] >= 0)) << u;
+                }
             }
-            while (pm) {
-                const int u = __ffs(pm) - 1;
-                pm &= pm - 1;
-                acc += utab_get<CAP>(tab, selu<PULL_U>(jv, u));
+            if (tab.dense) {  // (small graphs) Q_c indexed by node id
+                while (pm) {
+                    const int u = __ffs(pm) - 1;
+                    pm &= pm - 1;
+                    acc += lds64(sb + 8u * (unsigned)selu<PULL_U>(jv, u));
+                }
+            } else {
+                while (pm) {
+                    const int u = __ffs(pm) - 1;
+                    pm &= pm - 1;
+                    acc += utab_get<CAP>(tab, sb, selu<PULL_U>(jv, u));
+                }
             }
         }
     }
@@ -1734,7 +1779,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                     for (int q = 0; q < 4; ++q) {
                         if (jv[q] < 0) continue;
                         if (grp_filter && (int)(key_group(jv[q]) >> shift) != u) continue;
-                        if (utab_maybe(tab, jv[q])) acc += utab_get<CAP>(tab, jv[q]);
+                        if (utab_maybe(tab, jv[q])) acc += utab_get<CAP>(tab, (unsigned)__cvta_generic_to_shared(mcf_usmem), jv[q]);
                     }
                 }
                 if (a.prof) {
