@@ -353,6 +353,18 @@ def cpu_line(cb, est):
             "host": host_cpu(), "tables_s": cb.setup_s}
 
 
+def config_dict(cfg, n, nnz, n_walks, beta, world, transport):
+    """The workload definition, identical in both arms' lines (the driver compares them key by key);
+    arm-specific facts (RNG, emission count) sit beside it, not inside."""
+    return {"workload": cfg["workload"], "n": int(n), "nnz": int(nnz), "n_walks": int(n_walks),
+            "walks_per_gpu": int(n_walks // world), "beta": beta, "max_steps": cfg["max_steps"],
+            "weight_cutoff": cfg["cutoff"], "seed": cfg["seed"],
+            "l2": "device arm: L2 flushed between timed steps (256 MiB write, untimed), and the graphs of configs "
+                  "3-5 exceed L2 anyway; CPU arm: a fresh column sample every step",
+            "parallelism": f"start-column shards x{world} (cost-balanced), graph replicated"
+                           + (f", exchange: {transport}" if world > 1 else "")}
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -374,8 +386,8 @@ def run_reference(args, cfg):
         "ms_per_step": 1e3 * est["t_all_full_s"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "nodes_per_s": est["nodes_per_s"],
-        "config": {"workload": cfg["workload"], "n": int(a.n), "nnz": int(a.nnz), "n_walks": int(n_walks),
-                   "beta": beta, "max_steps": cfg["max_steps"], "weight_cutoff": cfg["cutoff"]},
+        "config": config_dict(cfg, a.n, a.nnz, n_walks, beta, args.gpus, args.transport),
+        "sampling": "PCG64DXSM per-column substreams (the reference's RNG)",
         "cpu_baseline": cpu_line(cpu, est),
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "timing": "each step = one stratified sample of the estimate on all host cores; value and ms_per_step are "
@@ -659,14 +671,8 @@ def run_device(args, cfg):
             "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (tools/bench_graphs.py recipe)",
             "nodes_per_s": nodes_per_s,
-            "config": {"workload": cfg["workload"], "n": int(n_rows), "nnz": int(nnz), "n_walks": int(n_walks),
-                       "walks_per_gpu": int(n_walks // world),
-                       "emissions_per_step": em_per_step, "beta": beta, "max_steps": cfg["max_steps"],
-                       "weight_cutoff": cfg["cutoff"], "seed": cfg["seed"], "sampling": "philox (device RNG)",
-                       "l2": "flushed between timed steps (256 MiB write, untimed); the config-3 graph (0.5 GB of "
-                             "CSR ids) exceeds L2 anyway",
-                       "parallelism": f"start-column shards x{world} (cost-balanced), graph replicated"
-                                      + (f", exchange: {args.transport}" if world > 1 else "")},
+            "config": config_dict(cfg, n_rows, nnz, n_walks, beta, world, args.transport),
+            "emissions_per_step": em_per_step, "sampling": "philox (device RNG)",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "timing": "CUDA-graph replay of one full estimator pass" if graph is not None else "eager steps",
             "clocks": clk,
