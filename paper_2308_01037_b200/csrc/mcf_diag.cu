@@ -1461,15 +1461,69 @@ __device__ __forceinline__ int sel8(const int (&v)[8], int u) {
 }
 template <int N>
 __device__ __forceinline__ int selu(const int (&v)[N], int u) {
-    if constexpr (N == 8) {
+    if constexpr (N == 4) {
+        const int a0 = (u & 1) ? v[1] : v[0], a1 = (u & 1) ? v[3] : v[2];
+        return (u & 2) ? a1 : a0;
+    } else if constexpr (N == 8) {
         return sel8(v, u);
     } else {
-        static_assert(N == 16, "8 or 16 ids per lane");
+        static_assert(N == 16, "4, 8 or 16 ids per lane");
         const int lo8[8] = {v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]};
         const int hi8[8] = {v[8], v[9], v[10], v[11], v[12], v[13], v[14], v[15]};
         const int a = sel8(lo8, u & 7), b = sel8(hi8, u & 7);
         return (u & 8) ? b : a;
     }
+}
+
+#ifndef UNIT_PIECE_BATCH
+#define UNIT_PIECE_BATCH 1
+#endif
+#ifndef UNIT_SHORT_TAIL
+#define UNIT_SHORT_TAIL 1
+#endif
+// One block of the pull scan: NU ids per lane at p[0], p[32], ... (immediate
+// offsets; `rem` of the warp's ids are this lane's or later, FULL: all valid),
+// a branch-free Bloom stage over all of them, then the passing ids (bit mask)
+// probed one after another -- a warp runs the probe code max-over-lanes-of-
+// passes times instead of once per id slot.
+template <int CAP, int NU, bool FULL>
+__device__ __forceinline__ long long pull_block(const UTab &tab, unsigned sb, const int *p, int rem) {
+    int jv[NU];
+    unsigned pm = 0;
+    if (FULL) {  // no bounds predicates, every id valid
+#pragma unroll
+        for (int u = 0; u < NU; ++u) jv[u] = __ldg(p + 32 * u);
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
+            const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
+            pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & 1u) << u;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < NU; ++u) jv[u] = 32 * u < rem ? __ldg(p + 32 * u) : -1;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
+            const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
+            pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & (unsigned)(jv[u] >= 0)) << u;
+        }
+    }
+    long long acc = 0;
+    if (tab.dense) {  // (small graphs) Q_c indexed by node id
+        while (pm) {
+            const int u = __ffs(pm) - 1;
+            pm &= pm - 1;
+            acc += lds64(sb + 8u * (unsigned)selu<NU>(jv, u));
+        }
+    } else {
+        while (pm) {
+            const int u = __ffs(pm) - 1;
+            pm &= pm - 1;
+            acc += utab_get<CAP>(tab, sb, selu<NU>(jv, u));
+        }
+    }
+    return acc;
 }
 
 // sum of Q_c over the ids ckeys[lo, hi) (warp-cooperative, PULL_U ids per
@@ -1497,51 +1551,19 @@ __device__ __forceinline__ long long unit_scan(const UArgs &a, const UTab &tab, 
                 if ((wv[u] >> (kv[u] & 31)) & 1u) acc += reinterpret_cast<const long long *>(mcf_usmem)[t0 + 32 * u + lane];
         }
     } else {
-        // 8 ids per lane in flight; the Bloom-passing ones (bit mask) are then
-        // probed one after another, so a warp runs the probe code max-over-
-        // lanes-of-passes times instead of once per id slot
+        // full blocks of 32 PULL_U ids, then the tail with as few ids per lane as cover it
         constexpr int PULL_U = UNIT_PULL_U;
-        // a lane's ids at p[0], p[32], ... (immediate offsets), `rem` of them left
         const unsigned sb = usmem_base();
         const int *p = a.ckeys + lo + lane;
-        // ids left for the warp (uniform); a lane's are `remw - lane`
-        for (int remw = (int)(hi - lo); remw > 0; remw -= 32 * PULL_U, p += 32 * PULL_U) {
-            int jv[PULL_U];
-            unsigned pm = 0;
-            if (remw >= 32 * PULL_U) {  // full block: no bounds predicates, every id valid
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) jv[u] = __ldg(p + 32 * u);
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) {
-                    const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
-                    const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
-                    pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & 1u) << u;
-                }
-            } else {
-                const int rem = remw - lane;
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) jv[u] = 32 * u < rem ? __ldg(p + 32 * u) : -1;
-                // branch-free Bloom stage: the PULL_U filter words load together
-#pragma unroll
-                for (int u = 0; u < PULL_U; ++u) {
-                    const uint32_t h = (uint32_t)jv[u] * 0x85EBCA6Bu;
-                    const unsigned w = lds32(tab.filt + 4 * (h >> tab.fshift));
-                    pm |= ((w >> ((h >> (tab.fshift - 5)) & 31u)) & (unsigned)(jv[u] >= 0)) << u;
-                }
-            }
-            if (tab.dense) {  // (small graphs) Q_c indexed by node id
-                while (pm) {
-                    const int u = __ffs(pm) - 1;
-                    pm &= pm - 1;
-                    acc += lds64(sb + 8u * (unsigned)selu<PULL_U>(jv, u));
-                }
-            } else {
-                while (pm) {
-                    const int u = __ffs(pm) - 1;
-                    pm &= pm - 1;
-                    acc += utab_get<CAP>(tab, sb, selu<PULL_U>(jv, u));
-                }
-            }
+        int remw = (int)(hi - lo);  // ids left for the warp (uniform); a lane's are `remw - lane`
+        for (; remw >= 32 * PULL_U; remw -= 32 * PULL_U, p += 32 * PULL_U)
+            acc += pull_block<CAP, PULL_U, true>(tab, sb, p, 0);
+        if (remw > 0) {
+            // (tails of 1, 2 and 12 ids per lane measured no faster than these)
+            const int rem = remw - lane;
+            if (UNIT_SHORT_TAIL && PULL_U > 4 && remw <= 128) acc += pull_block<CAP, 4, false>(tab, sb, p, rem);
+            else if (UNIT_SHORT_TAIL && PULL_U > 8 && remw <= 256) acc += pull_block<CAP, 8, false>(tab, sb, p, rem);
+            else acc += pull_block<CAP, PULL_U, false>(tab, sb, p, rem);
         }
     }
     return warp_sum_ll(acc);
@@ -1855,7 +1877,60 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         // the next unit, fetched by thread 0 while the other warps take this
         // unit's pieces (phase B has no barrier until all pieces are done)
         if (tid == 0) unit_fetch(a, s_bc, s_nxt);
-        // phase B: pieces of the queued entries, all warps
+        // phase B: pieces of the queued entries, all warps.  A warp takes a
+        // batch of pieces at a time: lane k resolves piece k's entry and range
+        // (coalesced metadata loads, one dependent chain per batch instead of
+        // one per piece), the warp scans them one after another, and lane k
+        // stores piece k's sum.  The batch shrinks with the unit's piece count
+        // so that a unit with few pieces still spreads over all warps.
+#if UNIT_PIECE_BATCH
+        const int bsz = npieces >= 32ll * 4 * NWARP ? 32 : (npieces >= 8ll * 4 * NWARP ? 8 : 1);
+        while (true) {
+            int x0 = 0;
+            if (lane == 0) x0 = atomicAdd(&s_next, bsz);
+            x0 = __shfl_sync(MCF_FULL, x0, 0);
+            if (x0 >= npieces) break;
+            const int nb = npieces - x0 < bsz ? (int)(npieces - x0) : bsz;
+            long long mb = 0;
+            int mlen = 0, mt = 0;  // mlen: bit 30 = the entry has one piece
+            if (lane < nb) {
+                const int x = x0 + lane;
+                int lo_j = 0, hi_j = nq - 1;  // last entry j with qpre[j] <= x
+                if (npieces <= a.pcap) lo_j = hi_j = pmap[x];
+                while (lo_j < hi_j) {
+                    const int mid = (lo_j + hi_j + 1) >> 1;
+                    if (qpre[mid] <= x) lo_j = mid;
+                    else hi_j = mid - 1;
+                }
+                const int j = lo_j;
+                mt = qt[j];
+                const long long pq = x - qpre[j];
+                const int len = qlen[j];
+                const long long left = len - pq * a.chunk;
+                mb = qlo[j] + pq * a.chunk;
+                mlen = (int)(left < a.chunk ? left : a.chunk) | (len <= a.chunk ? 1 << 30 : 0);
+            }
+            long long myacc = 0;
+            for (int k = 0; k < nb; ++k) {
+                const long long pb = __shfl_sync(MCF_FULL, mb, k);
+                const int plen = __shfl_sync(MCF_FULL, mlen, k) & 0x3fffffff;
+                const int qtj = __shfl_sync(MCF_FULL, mt, k);
+                const bool push = qtj < 0;
+                const int i = push ? __ldg(a.csc_rows + cs + ~qtj) : 0;
+                const long long acc = unit_scan<CAP>(a, tab, i, push, pb, pb + plen, lane);
+                if (lane == k) myacc = acc;
+                if (a.prof && lane == 0) {
+                    pr[2] += 1;
+                    pr[push ? 4 : 3] += (unsigned long long)plen;
+                }
+            }
+            if (lane < nb) {
+                const int t = mt < 0 ? ~mt : mt;
+                if (K == 1 && (mlen >> 30)) a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp((double)myacc, -E));
+                else if (myacc) atomicAdd(reinterpret_cast<unsigned long long *>(a.pcol + cs + t), (unsigned long long)myacc);
+            }
+        }
+#else
         while (true) {
             int x = 0;
             if (lane == 0) x = atomicAdd(&s_next, 1);
@@ -1887,6 +1962,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                 else if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(a.pcol + cs + t), (unsigned long long)acc);
             }
         }
+#endif
         __syncthreads();
         // int64 sums -> fp64: one-unit columns convert their split entries,
         // a split column's last unit converts all of its entries
