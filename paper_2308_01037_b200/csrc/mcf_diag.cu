@@ -1179,6 +1179,7 @@ struct UArgs {
     int *pmap;           // per-CTA piece -> queue entry map (pcap each; wider units binary-search qpre)
     long long pcap;
     long long chunk;
+    int dbg_skip;          // MCF_UNIT_DEBUG_SKIP (timing experiments only): 1 = no scans, 2 = no build either
     int serial_small;      // slices scanned by one lane in phase A when the column has < 32 entries per warp
     long long small_need;  // widest table need of a one-unit column
     long long small_cut;   // one-unit columns up to this need go to the small-table kernel (list UNIT_BUCKETS)
@@ -1419,6 +1420,58 @@ __device__ __forceinline__ int4 lds128(unsigned addr) {
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
+// shared-space atomics by 32-bit shared address (the build loop below: no
+// generic-pointer address-space checks, reductions where no value returns)
+__device__ __forceinline__ int atoms_cas32(unsigned addr, int cmp, int val) {
+    int old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(addr), "r"(cmp), "r"(val) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned atoms_add32(unsigned addr, unsigned v) {
+    unsigned old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void reds_add32(unsigned addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void reds_or32(unsigned addr, unsigned v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Find or claim `key` in the unit table (keys at shared address kb, cap =
+// mask + 1 slots): scan the quads from the key's home quad, one 16-B load
+// each; the key goes to the first slot in probe order that holds it or is
+// empty, so utab_get's "an empty slot ends the search" stays true.  A lost
+// claim re-reads the same quad.  Returns the slot (fresh: this lane claimed
+// it) or -1 when the table is over its limit (error bit 256 set).
+__device__ __forceinline__ int unit_claim(unsigned kb, uint32_t mask, int tshift, int key, unsigned nk_addr, int limit,
+                                          int *err, bool &fresh) {
+    uint32_t s = (((uint32_t)key * 0x9E3779B1u) >> tshift) & ~3u;
+    for (uint32_t quads = 0; quads <= (mask >> 2) + 1; ++quads) {
+        while (true) {
+            const int4 k = lds128(kb + 4u * s);
+            const bool h0 = k.x == key || k.x == EMPTY_KEY, h1 = k.y == key || k.y == EMPTY_KEY;
+            const bool h2 = k.z == key || k.z == EMPTY_KEY, h3 = k.w == key || k.w == EMPTY_KEY;
+            if (!(h0 | h1 | h2 | h3)) break;  // four other keys: next quad
+            const int j = h0 ? 0 : (h1 ? 1 : (h2 ? 2 : 3));
+            const int kv = h0 ? k.x : (h1 ? k.y : (h2 ? k.z : k.w));
+            if (kv == key) return (int)s + j;
+            if ((int)lds32(nk_addr) >= limit) {
+                atomicOr(err, 256);
+                return -1;
+            }
+            const int old = atoms_cas32(kb + 4u * (s + j), EMPTY_KEY, key);
+            if (old == EMPTY_KEY) {
+                fresh = true;
+                return (int)s + j;
+            }
+            if (old == key) return (int)s + j;
+        }
+        s = (s + 4) & mask;
+    }
+    atomicOr(err, 256);  // every quad full (the key count lags the claims by at most one warp step)
+    return -1;
+}
 template <int CAP>
 __device__ __forceinline__ long long utab_get(const UTab &t, unsigned sb, int key) {
     if (t.dense) return lds64(sb + 8u * (unsigned)key);
@@ -1475,6 +1528,9 @@ __device__ __forceinline__ int selu(const int (&v)[N], int u) {
     }
 }
 
+#ifndef UNIT_BUILD2
+#define UNIT_BUILD2 1
+#endif
 #ifndef UNIT_PIECE_BATCH
 #define UNIT_PIECE_BATCH 1
 #endif
@@ -1708,7 +1764,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         const double escale = escale_ok ? __longlong_as_double((long long)(E + 1023) << 52) : 0.0;
         // Q_c over this unit's key groups
         constexpr int U = 4;
-        for (long long base = e0; base < e1; base += (long long)U * TH) {
+        for (long long base = e0; base < (a.dbg_skip >= 2 ? e0 : e1); base += (long long)U * TH) {
             int sv[U];
 #pragma unroll
             for (int q = 0; q < U; ++q) {  // all U loads issued before any is used
@@ -1727,7 +1783,46 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                 wv[q] = (K == 1 || parted ? i < e1 : sv[q] >= 0) ? __ldcs(ewt + s0 + i) : 0.0;
             }
             // lanes holding the same key add once (step-major slots: a warp's
-            // 32 walks share the start state at step 0 and hubs later on)
+            // 32 walks share the start state at step 0 and hubs later on); the
+            // group's first lane finds or claims the slot, then all such lanes
+            // together set the new keys' Bloom bits, count them (one add per
+            // warp) and add their sums (two 32-bit atomics with carry)
+#if UNIT_BUILD2
+            const unsigned sbb = (unsigned)__cvta_generic_to_shared(smem_raw);
+            const unsigned nk_addr = (unsigned)__cvta_generic_to_shared(&s_nkeys);
+            const int tshift_b = 32 - (31 - __clz((int)cap));
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int key = sv[q];
+                if (!__any_sync(MCF_FULL, key >= 0)) continue;  // no key of this unit in the warp's slot (uniform)
+                long long qv = key >= 0 ? __double2ll_rn(escale_ok ? wv[q] * escale : ldexp(wv[q], E)) : 0;
+                const unsigned same = __match_any_sync(MCF_FULL, key);
+                bool lead = key >= 0;
+                if (lead && __popc(same) > 1) {
+                    qv = group_sum_i64(same, qv);
+                    lead = lane == __ffs(same) - 1;
+                }
+                int slot = -1;
+                bool fresh = false;
+                if (lead) slot = keys ? unit_claim(sbb + 8u * CAP, mask, tshift_b, key, nk_addr, limit, a.err, fresh) : key;
+                const unsigned fm = __ballot_sync(MCF_FULL, fresh);
+                if (fm) {
+                    if (fresh) {
+                        const uint32_t h = (uint32_t)key * 0x85EBCA6Bu;
+                        reds_or32(sbb + 12u * CAP + 4u * (h >> FSHIFT), 1u << ((h >> (FSHIFT - 5)) & 31u));
+                    }
+                    if (lane == 0) reds_add32(nk_addr, (unsigned)__popc(fm));
+                }
+                if (slot >= 0) {
+                    const unsigned long long uq = (unsigned long long)qv;
+                    const unsigned lo = (unsigned)uq, hi = (unsigned)(uq >> 32);
+                    const unsigned addr = sbb + 8u * (unsigned)slot;
+                    const unsigned oldw = atoms_add32(addr, lo);
+                    const unsigned up = hi + (oldw + lo < oldw ? 1u : 0u);
+                    if (up) reds_add32(addr + 4u, up);
+                }
+            }
+#else
 #pragma unroll
             for (int q = 0; q < U; ++q) {
                 if (!__any_sync(MCF_FULL, sv[q] >= 0)) continue;  // no key of this unit in the warp's slot
@@ -1741,6 +1836,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                 const int slot = keys ? unit_insert(keys, mask, sv[q], &s_nkeys, limit, a.err, filt, FSHIFT) : sv[q];
                 if (slot >= 0) smem_add_i64(&vals[slot], qv);
             }
+#endif
         }
         __syncthreads();
         const long long t_inserted = a.prof ? clock64() : 0;
@@ -1762,7 +1858,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         // the CTA has lanes leaves most warps idle here, so it queues its
         // slices longer than a few ids for phase B, where all warps share them
         const int serial_max = cn >= 32 * NWARP ? UNIT_SERIAL : a.serial_small;
-        while (true) {
+        while (!a.dbg_skip) {
             int t0 = 0;
             if (lane == 0) t0 = atomicAdd(&s_next, 32);
             t0 = __shfl_sync(MCF_FULL, t0, 0);
@@ -2129,7 +2225,9 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     a.hub_words = g->hub_words;
     {
         const char *e = getenv("MCF_UNIT_SERIAL_SMALL");
-        a.serial_small = e ? atoi(e) : 2;  // measured: config 5 4.27 -> 4.17 s, config 3 unchanged
+        a.serial_small = e ? atoi(e) : 2;
+        e = getenv("MCF_UNIT_DEBUG_SKIP");
+        a.dbg_skip = e ? atoi(e) : 0;  // measured: config 5 4.27 -> 4.17 s, config 3 unchanged
     }
     {
         const char *e = getenv("MCF_UNIT_CHUNK");
