@@ -1755,8 +1755,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         __syncthreads();
         const long long t_zeroed = a.prof ? clock64() : 0;
         const double maxw = __longlong_as_double((long long)s_cur.maxw);
-        int lg_m = 0;
-        while ((1ll << lg_m) < m) ++lg_m;
+        const int lg_m = m <= 1 ? 0 : 64 - __clzll(m - 1);  // smallest lg with 2^lg >= m
         const int E = maxw > 0.0 ? 61 - ilogb(maxw) - lg_m : 0;  // as k_diag_q: sum of m terms < 2^62
         // w 2^E as one multiply when 2^E is a normal double (exact: a power-of-two
         // scaling rounds like ldexp, subnormal results included)
