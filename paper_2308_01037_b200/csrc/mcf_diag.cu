@@ -1348,33 +1348,6 @@ __global__ void __launch_bounds__(PART_TH) k_unit_partition(UArgs a, unsigned *_
     }
 }
 
-// insert with an occupancy guard: a table past its limit drops the key and
-// flags the overflow (never expected: need per unit has a ~12 sigma margin)
-// The lane that inserts a new key also sets its Bloom bit and counts it.
-__device__ __forceinline__ int unit_insert(int *keys, uint32_t mask, int key, int *nkeys, int limit, int *err,
-                                           unsigned *filt, int fshift) {
-    uint32_t s = hash_slot(key, mask) & ~3u;  // home: the key's aligned quad (utab_get reads it with one load)
-    while (true) {
-        const int k = keys[s];
-        if (k == key) return (int)s;
-        if (k == EMPTY_KEY) {
-            if (*(volatile int *)nkeys >= limit) {
-                atomicOr(err, 256);
-                return -1;
-            }
-            const int old = atomicCAS(&keys[s], EMPTY_KEY, key);
-            if (old == EMPTY_KEY) {
-                atomicAdd(nkeys, 1);
-                const uint32_t h = (uint32_t)key * 0x85EBCA6Bu;
-                atomicOr(filt + (h >> fshift), 1u << ((h >> (fshift - 5)) & 31u));
-                return (int)s;
-            }
-            if (old == key) return (int)s;
-        }
-        s = (s + 1) & mask;
-    }
-}
-
 // The unit kernel's table in shared memory, addressed by 32-bit shared
 // addresses (no generic-pointer conversions in the probe loops): keys (int),
 // values (int64) and a one-word-per-key Bloom filter (three bits of one
@@ -1438,8 +1411,10 @@ __device__ __forceinline__ void reds_add32(unsigned addr, unsigned v) {
 __device__ __forceinline__ void reds_or32(unsigned addr, unsigned v) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-// Find or claim `key` in the unit table (keys at shared address kb, cap =
-// mask + 1 slots): scan the quads from the key's home quad, one 16-B load
+// Find or claim `key` in the unit table, with an occupancy guard: a table
+// past its limit drops the key and flags the overflow (never expected: need
+// per unit has a ~12 sigma margin).  Keys at shared address kb, cap =
+// mask + 1 slots.  Scan the quads from the key's home quad, one 16-B load
 // each; the key goes to the first slot in probe order that holds it or is
 // empty, so utab_get's "an empty slot ends the search" stays true.  A lost
 // claim re-reads the same quad.  Returns the slot (fresh: this lane claimed
@@ -1528,12 +1503,6 @@ __device__ __forceinline__ int selu(const int (&v)[N], int u) {
     }
 }
 
-#ifndef UNIT_BUILD2
-#define UNIT_BUILD2 1
-#endif
-#ifndef UNIT_PIECE_BATCH
-#define UNIT_PIECE_BATCH 1
-#endif
 #ifndef UNIT_SHORT_TAIL
 #define UNIT_SHORT_TAIL 1
 #endif
@@ -1786,7 +1755,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
             // group's first lane finds or claims the slot, then all such lanes
             // together set the new keys' Bloom bits, count them (one add per
             // warp) and add their sums (two 32-bit atomics with carry)
-#if UNIT_BUILD2
             const unsigned sbb = (unsigned)__cvta_generic_to_shared(smem_raw);
             const unsigned nk_addr = (unsigned)__cvta_generic_to_shared(&s_nkeys);
             const int tshift_b = 32 - (31 - __clz((int)cap));
@@ -1821,21 +1789,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                     if (up) reds_add32(addr + 4u, up);
                 }
             }
-#else
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                if (!__any_sync(MCF_FULL, sv[q] >= 0)) continue;  // no key of this unit in the warp's slot
-                long long qv = sv[q] >= 0 ? __double2ll_rn(escale_ok ? wv[q] * escale : ldexp(wv[q], E)) : 0;
-                const unsigned same = __match_any_sync(MCF_FULL, sv[q]);
-                if (sv[q] < 0) continue;
-                if (__popc(same) > 1) {
-                    qv = group_sum_i64(same, qv);
-                    if (lane != __ffs(same) - 1) continue;
-                }
-                const int slot = keys ? unit_insert(keys, mask, sv[q], &s_nkeys, limit, a.err, filt, FSHIFT) : sv[q];
-                if (slot >= 0) smem_add_i64(&vals[slot], qv);
-            }
-#endif
         }
         __syncthreads();
         const long long t_inserted = a.prof ? clock64() : 0;
@@ -1978,7 +1931,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
         // one per piece), the warp scans them one after another, and lane k
         // stores piece k's sum.  The batch shrinks with the unit's piece count
         // so that a unit with few pieces still spreads over all warps.
-#if UNIT_PIECE_BATCH
         const int bsz = npieces >= 32ll * 4 * NWARP ? 32 : (npieces >= 8ll * 4 * NWARP ? 8 : 1);
         while (true) {
             int x0 = 0;
@@ -2025,39 +1977,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) k_diag_unit(UArgs a) {
                 else if (myacc) atomicAdd(reinterpret_cast<unsigned long long *>(a.pcol + cs + t), (unsigned long long)myacc);
             }
         }
-#else
-        while (true) {
-            int x = 0;
-            if (lane == 0) x = atomicAdd(&s_next, 1);
-            x = __shfl_sync(MCF_FULL, x, 0);
-            if (x >= npieces) break;
-            int lo_j = 0, hi_j = nq - 1;  // last entry j with qpre[j] <= x
-            if (npieces <= a.pcap) lo_j = hi_j = pmap[x];
-            while (lo_j < hi_j) {
-                const int mid = (lo_j + hi_j + 1) >> 1;
-                if (qpre[mid] <= x) lo_j = mid;
-                else hi_j = mid - 1;
-            }
-            const int j = lo_j;
-            const int qtj = qt[j];
-            const bool push = qtj < 0;
-            const int t = push ? ~qtj : qtj;
-            const long long p = x - qpre[j], len = qlen[j];
-            const long long b = qlo[j] + p * a.chunk;
-            const long long e = qlo[j] + (len < (p + 1) * a.chunk ? len : (p + 1) * a.chunk);
-            const int i = push ? __ldg(a.csc_rows + cs + t) : 0;
-            const long long acc = unit_scan<CAP>(a, tab, i, push, b, e, lane);
-            if (a.prof && lane == 0) {
-                pr[2] += 1;
-                pr[push ? 4 : 3] += (unsigned long long)(e - b);
-            }
-            if (lane == 0) {
-                const bool whole = len <= a.chunk;
-                if (K == 1 && whole) a.pcol[cs + t] = a.csc_vals[cs + t] * (scale * ldexp((double)acc, -E));
-                else if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(a.pcol + cs + t), (unsigned long long)acc);
-            }
-        }
-#endif
         __syncthreads();
         // int64 sums -> fp64: one-unit columns convert their split entries,
         // a split column's last unit converts all of its entries
