@@ -605,6 +605,21 @@ def run_device(args, cfg):
                    "algorithmic_bytes_per_step": cbytes,
                    "bytes_rule": "sum over walked c of sum_{a in C_c} (32 + 4 deg a) (SURVEY 8d)",
                    "kernel_ms_avg": c_ms, "kernel_share_of_step": (q_ms_tot / ms) if ms else None}
+        # what actually limits it: the committed ncu capture's pipe utilisation (not measured in this run)
+        pp = os.path.join(ROOT, "profiles", "r02", f"ncu_unit_config{args.config}.json")
+        if g.n > 24576 and os.path.exists(pp):
+            try:
+                with open(pp) as f:
+                    k = json.load(f)[0]
+                pct = lambda key: float(k[key].split()[0])
+                combine["limiter"] = {
+                    "alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                    "lsu_data_pipe_pct": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                    "issue_active_pct": pct("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+                    "note": "co-limited by instruction issue and shared-memory wavefronts, not by HBM",
+                    "source": "profiles/r02/" + os.path.basename(pp) + " (ncu --set full of one launch)"}
+            except (KeyError, ValueError, IndexError, OSError):
+                pass
         if c_ms > walk_avg_ms * walk_launches_per_step:  # the dominant phase leads
             roofline = dict(combine)
             roofline["walk"] = walk
