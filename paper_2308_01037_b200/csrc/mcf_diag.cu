@@ -33,7 +33,7 @@ int check_params(const mcf_graph *g, const mcf_walk_params *p, const long long *
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                      long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
                      long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
-                     long long *stats, int *err, cudaStream_t s);
+                     long long *stats, int *err, cudaStream_t s, int max_sms = 0);
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
 }  // namespace mcf
@@ -2093,6 +2093,9 @@ static int launch_units(UArgs &a, int grid, cudaStream_t s) {
 
 // The combine by units (uniform-value graphs).  *fallback = true (nothing run)
 // when a column's table would need more than NGROUPS units.
+// SMs the unit kernels leave free (set by diag() around run_q while the next batch's walk runs beside them)
+static thread_local int t_reserve_sms = 0;
+
 static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax, const long long *walk_pre,
                      long long cb, long long ce, long long wb, long long slot_len, const long long *eoff,
                      const long long *walk_off, long long off_base, const int *est, const double *ewt, double *pcol,
@@ -2165,7 +2168,9 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     }
     AsyncFrees frees(s);
     static const bool prof_on = getenv("MCF_DIAG_PROF") != nullptr;
-    const int grid = sm_count() * (th == 1024 ? 1 : 2);
+    // SMs left to the next batch's walk (diag(): walk / combine overlap)
+    const int sms = sm_count() - t_reserve_sms > 8 ? sm_count() - t_reserve_sms : sm_count();
+    const int grid = sms * (th == 1024 ? 1 : 2);
     // small device block: bucket counts, work counter, too-wide need, error bits, profile
     unsigned char *blk = nullptr;
     const size_t blk_bytes = 256 + sizeof(unsigned long long) * 4 * UPROF_SLOTS;
@@ -2273,8 +2278,8 @@ static int run_units(bool timed, mcf_graph *g, const unsigned long long *colmax,
     if (rc) return rc;
     rc = th == 1024 ? launch_units<1024, 16384, 8192>(a, grid, s) : launch_units<512, 8192, 4096>(a, grid, s);
     if (rc) return rc;
-    if (hbc_mid > 0 && (rc = launch_units<512, 8192, 4096>(am, sm_count() * 2, s))) return rc;
-    if (hbc_small > 0 && (rc = launch_units<256, 4096, 2048>(as, sm_count() * 4, s))) return rc;
+    if (hbc_mid > 0 && (rc = launch_units<512, 8192, 4096>(am, sms * 2, s))) return rc;
+    if (hbc_small > 0 && (rc = launch_units<256, 4096, 2048>(as, sms * 4, s))) return rc;
     rc = timed_end(timed, g->ev_q, s);
     if (rc) return rc;
     int herr = 0;
@@ -2326,6 +2331,9 @@ static int run_q(bool timed, mcf_graph *g, const unsigned long long *colmax, con
             if (rc || !fallback) return rc;
         }
     }
+    // (the single-table / cluster path below uses the side stream itself: inside an overlapped batch loop,
+    // diag(), it first lets the walk running there finish)
+    if (t_reserve_sms > 0 && g->side) MCF_CUDA(cudaStreamSynchronize(g->side));
     QArgs q;
     q.walk_pre = walk_pre;
     q.wb = wb;
@@ -2634,6 +2642,19 @@ static void alloc_regroup(const mcf_graph *g, long long slots, int **pest, doubl
     }
 }
 
+// SMs reserved for the next batch's walk while a batch is combined.  MCF_DIAG_OVERLAP: 0 = serial batches,
+// N > 0 = N SMs; unset = start at 20 and adapt (*adaptive) from the measured durations of each walk / combine
+// pair (diag()).  Only where the unit combine runs (uniform-value graphs above the dense-Q size).  Timing
+// only: results do not depend on it.
+static int overlap_sms(const mcf_graph *g, bool *adaptive) {
+    const char *e = getenv("MCF_DIAG_OVERLAP");
+    const int v = e ? atoi(e) : 20;
+    *adaptive = e == nullptr;
+    const char *u = getenv("MCF_DIAG_UNITS");
+    if (!g->uniform_value || g->n <= DENSE_N || v <= 0 || (u && !strcmp(u, "0"))) return 0;
+    return v < sm_count() - 8 ? v : sm_count() - 8;
+}
+
 static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                 const long long *walk_off, const int *entries, double *pcol, long long *stats, cudaStream_t s,
                 bool replay) {
@@ -2722,6 +2743,109 @@ static int diag(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pr
     double *pewt = nullptr;
     alloc_regroup(g, buf_slots, &pest, &pewt, s);
     long long pslots = pest ? buf_slots : 0;
+    // Walk / combine overlap (fixed-slot walks, two or more batches): the walk is bound by DRAM random-access
+    // latency and the unit combine by instruction issue, so batch b + 1's walk runs on a few reserved SMs (side
+    // stream, second emission buffer) while batch b is combined on the others.  Same kernels, same data:
+    // results are bitwise those of the serial loop below.
+    bool ov_adapt = false;
+    int ov = overlap_sms(g, &ov_adapt);
+    if (fixed && ov > 0 && hb.size() > 2 && ensure_side_stream(g) == MCF_OK) {
+        int *est2 = nullptr;
+        double *ewt2 = nullptr;
+        if (cudaMallocAsync(&est2, sizeof(int) * buf_slots, s) == cudaSuccess &&
+            cudaMallocAsync(&ewt2, sizeof(double) * buf_slots, s) == cudaSuccess) {
+            const size_t nb = hb.size() - 1;
+            std::vector<long long> r0(nb), r1(nb);
+            for (size_t b = 0; b < nb && !rc; ++b) rc = read_walk_range(walk_pre, hb[b], hb[b + 1], &r0[b], &r1[b], s);
+            int *ebuf[2] = {est, est2};
+            double *wbuf[2] = {ewt, ewt2};
+            // (timing events: the adaptive SM split below reads the walk's and the combine's durations)
+            cudaEvent_t ev_w[2] = {nullptr, nullptr}, ev_q[2] = {nullptr, nullptr}, ev_init = nullptr;
+            cudaEvent_t ev_ws = nullptr, ev_cs = nullptr;  // start of the side walk / of the combine beside it
+            for (int k = 0; k < 2 && !rc; ++k) {
+                if (cudaEventCreate(&ev_w[k]) != cudaSuccess || cudaEventCreate(&ev_q[k]) != cudaSuccess)
+                    rc = cuda_status(cudaGetLastError(), "cudaEventCreate");
+            }
+            if (!rc && (cudaEventCreateWithFlags(&ev_init, cudaEventDisableTiming) != cudaSuccess ||
+                        cudaEventCreate(&ev_ws) != cudaSuccess || cudaEventCreate(&ev_cs) != cudaSuccess))
+                rc = cuda_status(cudaGetLastError(), "cudaEventCreate");
+            cudaStream_t side = g->side;
+            if (!rc) {  // the side stream starts after this call's setup (err, colmax, buffers) on s
+                cudaEventRecord(ev_init, s);
+                cudaStreamWaitEvent(side, ev_init, 0);
+            }
+            // first non-empty batch: its walk has the GPU to itself
+            size_t b = 0;
+            while (b < nb && r1[b] == r0[b]) ++b;
+            if (!rc && b < nb)
+                rc = launch_walk_emit(g, p, walk_pre, hb[b], hb[b + 1], r1[b] - r0[b], EMIT_FIXED, nullptr, nullptr, L, 0,
+                                      nullptr, ebuf[0], wbuf[0], colmax, stats, err, s);
+            int cur = 0;
+            while (!rc && b < nb) {
+                size_t nx = b + 1;
+                while (nx < nb && r1[nx] == r0[nx]) ++nx;
+                if (nx < nb) {  // next batch's walk into the other buffer, once its previous combine is done
+                    if (ev_q[cur ^ 1]) cudaStreamWaitEvent(side, ev_q[cur ^ 1], 0);
+                    cudaEventRecord(ev_ws, side);
+                    rc = launch_walk_emit(g, p, walk_pre, hb[nx], hb[nx + 1], r1[nx] - r0[nx], EMIT_FIXED, nullptr,
+                                          nullptr, L, 0, nullptr, ebuf[cur ^ 1], wbuf[cur ^ 1], colmax, stats, err, side,
+                                          ov);
+                    if (rc) break;
+                    cudaEventRecord(ev_w[cur ^ 1], side);
+                }
+                t_reserve_sms = nx < nb ? ov : 0;
+                cudaEventRecord(ev_cs, s);
+                rc = run_q(timed, g, colmax, walk_pre, hb[b], hb[b + 1], r0[b], L, nullptr, nullptr, 0, ebuf[cur],
+                           wbuf[cur], pcol, (long long)hmax * L, s, pest, pewt);
+                t_reserve_sms = 0;
+                if (rc) break;
+                cudaEventRecord(ev_q[cur], s);
+                if (nx < nb) {
+                    if (ov_adapt) {
+                        // Balance the two sides for the next pair from this pair's durations: the walk's time
+                        // scales with 1 / W, the combine's with 1 / (SMs - W), so they would have ended together at
+                        // W* = SMs tw W / (tw W + tc (SMs - W)); move halfway there.  (Waiting for the walk here
+                        // costs nothing: the next walk and the next combine both wait for it anyway.)
+                        static const double bias = [] { const char *e = getenv("MCF_OVERLAP_BIAS"); return e ? atof(e) : 1.3; }();
+                        float tw = 0.f, tc = 0.f;
+                        if (cudaEventSynchronize(ev_q[cur]) == cudaSuccess && cudaEventSynchronize(ev_w[cur ^ 1]) == cudaSuccess &&
+                            cudaEventElapsedTime(&tw, ev_ws, ev_w[cur ^ 1]) == cudaSuccess &&
+                            cudaEventElapsedTime(&tc, ev_cs, ev_q[cur]) == cudaSuccess && tw > 0.f && tc > 0.f) {
+                            const double S = sm_count(), W = ov, twb = bias * tw;  // (bias: a late walk stalls every SM)
+                            const double wstar = S * twb * W / (twb * W + tc * (S - W));
+                            int nv = (int)(0.5 * (W + wstar) + 0.5);
+                            nv = nv < 4 ? 4 : (nv > sm_count() / 2 ? sm_count() / 2 : nv);
+                            if (getenv("MCF_DIAG_PROF"))
+                                fprintf(stderr, "[overlap] batch %zu: walk %.1f ms on %d SMs, combine %.1f ms -> %d SMs\n", b,
+                                        tw, ov, tc, nv);
+                            ov = nv;
+                        }
+                        cudaGetLastError();
+                    }
+                    cudaStreamWaitEvent(s, ev_w[cur ^ 1], 0);
+                }
+                b = nx;
+                cur ^= 1;
+            }
+            cudaStreamSynchronize(side);  // (error paths: nothing of this call is left running on the side stream)
+            for (int k = 0; k < 2; ++k) {
+                if (ev_w[k]) cudaEventDestroy(ev_w[k]);
+                if (ev_q[k]) cudaEventDestroy(ev_q[k]);
+            }
+            if (ev_init) cudaEventDestroy(ev_init);
+            if (ev_ws) cudaEventDestroy(ev_ws);
+            if (ev_cs) cudaEventDestroy(ev_cs);
+            cudaFreeAsync(est2, s);
+            cudaFreeAsync(ewt2, s);
+            if (est) cudaFreeAsync(est, s);
+            if (ewt) cudaFreeAsync(ewt, s);
+            if (pest) cudaFreeAsync(pest, s);
+            if (pewt) cudaFreeAsync(pewt, s);
+            return rc;
+        }
+        cudaGetLastError();  // no room for a second emission buffer: the serial loop
+        if (est2) cudaFreeAsync(est2, s);
+    }
     for (size_t b = 0; b + 1 < hb.size(); ++b) {
         const long long c0 = hb[b], c1 = hb[b + 1];
         long long bw0 = 0, bw1 = 0;

@@ -404,8 +404,9 @@ __global__ void __launch_bounds__(256, (WalkOcc<NW, OCC>::v)) k_walk_action(Walk
 // Each emission is (state, zeta_{k+2} W_k); unused slots of a walk hold -1.
 enum { EMIT_FIXED = 0, EMIT_REPLAY = 1, EMIT_COUNT = 2, EMIT_EXPLICIT = 3 };
 
-template <int MODE, bool FAT, int OCC = 4, bool LEAN = false>
-__global__ void __launch_bounds__(256, OCC) k_walk_emit(WalkCommon a, long long slot_len, long long off_base,
+// TH: threads per CTA (1024 with OCC 1: one CTA owns an SM -- the walks that run beside a combine, diag())
+template <int MODE, bool FAT, int OCC = 4, bool LEAN = false, int TH = 256>
+__global__ void __launch_bounds__(TH, OCC) k_walk_emit(WalkCommon a, long long slot_len, long long off_base,
                                                    long long *__restrict__ eaux, int *__restrict__ est,
                                                    double *__restrict__ ewt) {
     constexpr bool REPLAY = MODE == EMIT_REPLAY;
@@ -1050,8 +1051,11 @@ static int ensure_lean(mcf_graph *g, cudaStream_t s) {
 int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *walk_pre, long long cb, long long ce,
                      long long nwalks, int mode, const long long *walk_off, const int *entries, long long slot_len,
                      long long off_base, long long *eaux, int *est, double *ewt, unsigned long long *colmax,
-                     long long *stats, int *err, cudaStream_t s) {
+                     long long *stats, int *err, cudaStream_t s, int max_sms) {
     MCF_ARG(nwalks < WALKS_PER_LAUNCH, "walks per launch must be below 2^31 - 4096");
+    // max_sms > 0: a grid sized for that many SMs (the walk pools take any grid), for walks that run beside
+    // the previous batch's combine
+    auto grid_for = [&](int full) { return max_sms > 0 && max_sms < sm_count() ? full / sm_count() * max_sms : full; };
     AsyncFrees frees(s);
     WalkCommon a;
     int *blk = nullptr;
@@ -1088,23 +1092,32 @@ int launch_walk_emit(mcf_graph *g, const mcf_walk_params *p, const long long *wa
         a.rsum_by_deg = g->rsum_by_deg;
         for (int k = 0; k < 3; ++k) a.pf_bytes[k] = 0;
         switch (mode) {
-            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false, 4, true><<<walk_grid(k_walk_emit<EMIT_FIXED, false, 4, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
-            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false, 4, true><<<walk_grid(k_walk_emit<EMIT_COUNT, false, 4, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
-            default: k_walk_emit<EMIT_EXPLICIT, false, 4, true><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, false, 4, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+            case EMIT_FIXED:
+                if (max_sms > 0 && max_sms < sm_count()) {
+                    // one 1024-thread CTA per reserved SM: no other CTA fits beside it, so the walk and the
+                    // combine split the SMs cleanly.  (More walks per lane on fewer threads -- 2 x 1024, 4 x 512,
+                    // 8 x 256 -- measured 1.2-3x slower: on a few SMs the walk is bound by issue, the Philox
+                    // rounds, not by load latency.)
+                    k_walk_emit<EMIT_FIXED, false, 1, true, 1024><<<max_sms, 1024, 0, s>>>(a, slot_len, 0, eaux, est, ewt);
+                } else
+                    k_walk_emit<EMIT_FIXED, false, 4, true><<<walk_grid(k_walk_emit<EMIT_FIXED, false, 4, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt);
+                break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false, 4, true><<<grid_for(walk_grid(k_walk_emit<EMIT_COUNT, false, 4, true>, 256, 0)), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, false, 4, true><<<grid_for(walk_grid(k_walk_emit<EMIT_EXPLICIT, false, 4, true>, 256, 0)), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
         }
     } else if (g->went) {
         switch (mode) {
-            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, true><<<walk_grid(k_walk_emit<EMIT_FIXED, true>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
-            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, true><<<walk_grid(k_walk_emit<EMIT_REPLAY, true>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
-            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, true><<<walk_grid(k_walk_emit<EMIT_COUNT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
-            default: k_walk_emit<EMIT_EXPLICIT, true><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, true>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, true><<<grid_for(walk_grid(k_walk_emit<EMIT_FIXED, true>, 256, 0)), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, true><<<grid_for(walk_grid(k_walk_emit<EMIT_REPLAY, true>, 256, 0)), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, true><<<grid_for(walk_grid(k_walk_emit<EMIT_COUNT, true>, 256, 0)), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, true><<<grid_for(walk_grid(k_walk_emit<EMIT_EXPLICIT, true>, 256, 0)), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
         }
     } else {
         switch (mode) {
-            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false><<<walk_grid(k_walk_emit<EMIT_FIXED, false>, 256, 0), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
-            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, false><<<walk_grid(k_walk_emit<EMIT_REPLAY, false>, 256, 0), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
-            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false><<<walk_grid(k_walk_emit<EMIT_COUNT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
-            default: k_walk_emit<EMIT_EXPLICIT, false><<<walk_grid(k_walk_emit<EMIT_EXPLICIT, false>, 256, 0), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
+            case EMIT_FIXED: k_walk_emit<EMIT_FIXED, false><<<grid_for(walk_grid(k_walk_emit<EMIT_FIXED, false>, 256, 0)), 256, 0, s>>>(a, slot_len, 0, eaux, est, ewt); break;
+            case EMIT_REPLAY: k_walk_emit<EMIT_REPLAY, false><<<grid_for(walk_grid(k_walk_emit<EMIT_REPLAY, false>, 256, 0)), 256, 0, s>>>(a, 0, off_base, eaux, est, ewt); break;
+            case EMIT_COUNT: k_walk_emit<EMIT_COUNT, false><<<grid_for(walk_grid(k_walk_emit<EMIT_COUNT, false>, 256, 0)), 256, 0, s>>>(a, 0, 0, eaux, est, ewt); break;
+            default: k_walk_emit<EMIT_EXPLICIT, false><<<grid_for(walk_grid(k_walk_emit<EMIT_EXPLICIT, false>, 256, 0)), 256, 0, s>>>(a, 0, 0, eaux, est, ewt);
         }
     }
     mcf::note_launch();

@@ -160,9 +160,9 @@ def test_config2_full_replay():
 def test_config3_multibatch_and_pool_fallback_bitwise(monkeypatch):
     """Config 3 at full size: the default combine (units), the single-table /
     cluster / GPU-wide combine it replaced (MCF_DIAG_UNITS=0), 4x more emission
-    batches (MCF_EMISSION_SLOTS = 2^28) and, on the old combine, no big-column
-    pool (MCF_DIAG_POOL=0: the allocation-failure path) give the same d bit
-    for bit."""
+    batches (MCF_EMISSION_SLOTS = 2^28), serial and overlapped batches
+    (MCF_DIAG_OVERLAP) and, on the old combine, no big-column pool
+    (MCF_DIAG_POOL=0: the allocation-failure path) give the same d bit for bit."""
     _need_gpu()
     import paper_2308_01037_b200 as mc
     cfg = bench.CONFIGS[3]
@@ -170,8 +170,10 @@ def test_config3_multibatch_and_pool_fallback_bitwise(monkeypatch):
     wc = mc.WalkConfig(n_walks, cfg["cutoff"], cfg["max_steps"], 0)
     ref = mc.rand_funm_diag(g, mc.EXPONENTIAL, wc, as_tensor=True)
     assert ref.emissions > 1.8e10
-    for env in ({"MCF_EMISSION_SLOTS": str(1 << 28)}, {"MCF_UNIT_PARTITION": "0"}, {"MCF_DIAG_UNITS": "0"},
-                {"MCF_DIAG_UNITS": "0", "MCF_DIAG_POOL": "0"}):
+    # (MCF_DIAG_OVERLAP: serial batches / the next batch's walk beside the combine on 8 or 24 reserved SMs)
+    for env in ({"MCF_EMISSION_SLOTS": str(1 << 28)}, {"MCF_UNIT_PARTITION": "0"}, {"MCF_DIAG_OVERLAP": "0"},
+                {"MCF_DIAG_OVERLAP": "8"}, {"MCF_DIAG_OVERLAP": "24", "MCF_EMISSION_SLOTS": str(1 << 28)},
+                {"MCF_DIAG_UNITS": "0"}, {"MCF_DIAG_UNITS": "0", "MCF_DIAG_POOL": "0"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         out = mc.rand_funm_diag(g, mc.EXPONENTIAL, wc, as_tensor=True)

@@ -1,0 +1,15 @@
+# walk/combine overlap sweep: reserved SMs x walks per lane (configs 3 and 5)
+D=gpurun_out/${1:-ov}; mkdir -p $D
+timeout 1500 python -m pytest tests/test_gpu_configs.py -q -x -k "multibatch" > $D/pytest.log 2>&1; echo "pytest exit $?" >> $D/pytest.log
+tail -3 $D/pytest.log
+for nw in 4 2 8; do for ov in ${2:-6 10 16}; do
+  MCF_WALK_NW=$nw MCF_DIAG_OVERLAP=$ov timeout 600 python bench.py --config 3 --steps 2 --warmup 1 --no-cpu --no-e2e > $D/c3_nw${nw}_ov$ov.json 2> $D/c3_nw${nw}_ov$ov.err
+  MCF_WALK_NW=$nw MCF_DIAG_OVERLAP=$ov timeout 600 python bench.py --config 5 --steps 1 --warmup 1 --no-cpu --no-e2e > $D/c5_nw${nw}_ov$ov.json 2> $D/c5_nw${nw}_ov$ov.err
+done; done
+python - "$D" <<'P'
+import json,glob,sys
+for f in sorted(glob.glob(sys.argv[1]+'/c*_*.json')):
+    try:
+        d=json.loads(open(f).read().strip().splitlines()[-1]); print(f.split('/')[-1], round(d['ms_per_step'],1), round(d['roofline']['kernel_ms_avg'],1))
+    except Exception as e: print(f,'ERR',e)
+P
