@@ -552,6 +552,11 @@ def run_device(args, cfg):
     # kernel intervals overlap and neither kernel has the GPU.  The per-kernel durations the rooflines use come
     # from ONE extra estimate with serial batches (MCF_DIAG_OVERLAP=0), outside the timed region.
     k_steps, k_ms, kernel_timing = args.steps, ms, "the timed steps"
+    timed_region_kernels = {"combine_ms_per_step": q_ms_tot / max(1, args.steps),
+                            "walk_ms_per_launch": walk_ms_tot / max(1, walk_launches),
+                            "walk_launches_per_step": walk_launches / max(1, args.steps),
+                            "note": "event-timed inside the timed steps; with the walk / combine overlap the two "
+                                    "intervals run side by side on disjoint SMs"}
     if (cfg["kind"] == "diag" and world == 1 and g.n > 24576 and os.environ.get("MCF_DIAG_OVERLAP") is None
             and os.environ.get("MCF_DIAG_UNITS") != "0"):
         os.environ["MCF_DIAG_OVERLAP"] = "0"
@@ -628,7 +633,7 @@ def run_device(args, cfg):
                    "algorithmic_bytes_per_step": cbytes,
                    "bytes_rule": "sum over walked c of sum_{a in C_c} (32 + 4 deg a) (SURVEY 8d)",
                    "kernel_ms_avg": c_ms, "kernel_share_of_step": (q_ms_tot / k_ms) if k_ms else None,
-                   "kernel_timing": kernel_timing}
+                   "kernel_timing": kernel_timing, "timed_region_kernels": timed_region_kernels}
         # what actually limits it: the committed ncu capture's pipe utilisation (not measured in this run)
         pp = os.path.join(ROOT, "profiles", "r02", f"ncu_unit_config{args.config}.json")
         if g.n > 24576 and os.path.exists(pp):
